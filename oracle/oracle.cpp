@@ -1,0 +1,1172 @@
+// oracle.cpp -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+//
+// Plain single-threaded fp64 CPU oracle of the solve phase of the paper's
+// AMG-preconditioned Krylov solver for Stokes systems (arXiv 2006.06052).
+// Every function cites the PAPER.md passage it follows, or the SURVEY.md §8(c)
+// reading (C0..C12) taken where the paper is silent.  No blocking, fusion or
+// reordering beyond what the cited definition states.  Built with
+// -O2 -ffp-contract=off: every product and sum is rounded separately, in the
+// order written.  Shares no code with the CUDA library.
+//
+// Parity-unpinned pieces (pinned only by invariants / small dense solves, see
+// DESIGN.md): absolute iteration counts, level sizes of the large configs.
+
+#include "oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+using std::vector;
+
+struct orc_mat {
+  int32_t n = 0, m = 0, b = 1;   // block rows, block cols, block size
+  vector<int32_t> ptr, col;      // C0: CSR over blocks, sorted unique columns
+  vector<double> val;            // nnz * b * b, row-major blocks
+  int64_t nnz() const { return (int64_t)col.size(); }
+  const double* blk(int64_t k) const { return val.data() + k * b * b; }
+  double* blk(int64_t k) { return val.data() + k * b * b; }
+};
+
+static inline double f32r(double v) { return (double)(float)v; }  // RNE narrowing (C9)
+
+extern "C" void orc_params_default(orc_params* p) {
+  p->solver = ORC_GMRES;
+  p->gmres_m = 30;
+  p->precond = ORC_PC_AMG;
+  p->maxiter = 1000;
+  p->hier_f32 = 1;
+  p->vec_f32 = 1;
+  p->smoother = ORC_SPAI0;
+  p->jacobi_omega = 2.0 / 3.0;
+  p->sa_omega = 2.0 / 3.0;
+  p->eps_strong = 1e-3;
+  p->coarse_enough = 3000;
+  p->max_levels = 20;
+  p->npre = 1;
+  p->npost = 1;
+  p->schur_p_component = 3;
+  p->nparts = 1;
+}
+
+// ---------------------------------------------------------------- C0 containers
+extern "C" orc_mat* orc_mat_new(int32_t n_rows, int32_t n_cols, int32_t b, const int32_t* ptr,
+                                const int32_t* col, const double* val) {
+  if (n_rows < 0 || n_cols < 0 || b < 1 || b > 8) return nullptr;
+  orc_mat* A = new orc_mat;
+  A->n = n_rows;
+  A->m = n_cols;
+  A->b = b;
+  A->ptr.assign(ptr, ptr + n_rows + 1);
+  int64_t nnz = A->ptr[n_rows];
+  A->col.assign(col, col + nnz);
+  A->val.assign(val, val + nnz * b * b);
+  return A;
+}
+
+extern "C" void orc_mat_free(orc_mat* A) { delete A; }
+
+extern "C" void orc_mat_info(const orc_mat* A, int64_t* out) {
+  out[0] = A->n;
+  out[1] = A->m;
+  out[2] = A->b;
+  out[3] = A->nnz();
+}
+
+extern "C" void orc_mat_export(const orc_mat* A, int32_t* ptr, int32_t* col, double* val) {
+  std::copy(A->ptr.begin(), A->ptr.end(), ptr);
+  std::copy(A->col.begin(), A->col.end(), col);
+  std::copy(A->val.begin(), A->val.end(), val);
+}
+
+// S1, PAPER.md:658-672 (§4 worked example): one block per non-empty b x b tile,
+// absent scalars inside a stored tile are explicit zeros.
+extern "C" orc_mat* orc_csr_to_bsr(int32_t n, int32_t m, int32_t b, const int32_t* ptr,
+                                   const int32_t* col, const double* val) {
+  if (b < 1 || n % b != 0 || m % b != 0) return nullptr;
+  orc_mat* A = new orc_mat;
+  A->n = n / b;
+  A->m = m / b;
+  A->b = b;
+  A->ptr.assign(A->n + 1, 0);
+  for (int32_t I = 0; I < A->n; ++I) {
+    vector<int32_t> cols;
+    for (int r = 0; r < b; ++r)
+      for (int32_t k = ptr[I * b + r]; k < ptr[I * b + r + 1]; ++k) cols.push_back(col[k] / b);
+    std::sort(cols.begin(), cols.end());
+    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+    size_t base = A->col.size();
+    for (int32_t J : cols) A->col.push_back(J);
+    A->val.resize(A->col.size() * b * b, 0.0);
+    for (int r = 0; r < b; ++r)
+      for (int32_t k = ptr[I * b + r]; k < ptr[I * b + r + 1]; ++k) {
+        int32_t J = col[k] / b, c = col[k] % b;
+        size_t pos = base + (std::lower_bound(cols.begin(), cols.end(), J) - cols.begin());
+        A->val[pos * b * b + r * b + c] += val[k];
+      }
+    A->ptr[I + 1] = (int32_t)A->col.size();
+  }
+  return A;
+}
+
+// ---------------------------------------------------------------- C1 SpMV
+// y_I = alpha * sum_{k in row I} A_k x_{col k} + beta * y_I ; beta == 0 overwrites.
+// PAPER.md:284-312 (§2.3 backend spmv primitive); SURVEY.md §8(c) C1.
+static void spmv(const orc_mat& A, double alpha, const double* x, double beta, double* y,
+                 bool round_f32) {
+  const int b = A.b;
+  vector<double> acc(b);
+  for (int32_t I = 0; I < A.n; ++I) {
+    std::fill(acc.begin(), acc.end(), 0.0);
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) {
+      const double* a = A.blk(k);
+      const double* xj = x + (int64_t)A.col[k] * b;
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) acc[r] = acc[r] + a[r * b + c] * xj[c];
+    }
+    for (int r = 0; r < b; ++r) {
+      double v = alpha * acc[r];
+      if (beta != 0.0) v = v + beta * y[(int64_t)I * b + r];
+      y[(int64_t)I * b + r] = round_f32 ? f32r(v) : v;
+    }
+  }
+}
+
+extern "C" int orc_spmv(const orc_mat* A, double alpha, const double* x, double beta, double* y) {
+  spmv(*A, alpha, x, beta, y, false);
+  return ORC_OK;
+}
+
+// r = f - A x (backend::residual)
+static void residual(const orc_mat& A, const double* f, const double* x, double* out, bool rf) {
+  const int b = A.b;
+  vector<double> acc(b);
+  for (int32_t I = 0; I < A.n; ++I) {
+    std::fill(acc.begin(), acc.end(), 0.0);
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) {
+      const double* a = A.blk(k);
+      const double* xj = x + (int64_t)A.col[k] * b;
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) acc[r] = acc[r] + a[r * b + c] * xj[c];
+    }
+    for (int r = 0; r < b; ++r) {
+      double v = f[(int64_t)I * b + r] - acc[r];
+      out[(int64_t)I * b + r] = rf ? f32r(v) : v;
+    }
+  }
+}
+
+static double dot(const vector<double>& a, const vector<double>& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s = s + a[i] * b[i];
+  return s;
+}
+static double nrm2(const vector<double>& a) { return std::sqrt(dot(a, a)); }
+
+// ---------------------------------------------------------------- block helpers
+// Frobenius norm squared, row-major order (C2 reading: Frobenius).
+static double fro2(const double* a, int b) {
+  double s = 0.0;
+  for (int i = 0; i < b * b; ++i) s = s + a[i] * a[i];
+  return s;
+}
+
+// b x b inverse by Gauss-Jordan with partial pivoting (first maximal |pivot|).
+// A pivot below 1e-14 * ||X||_F is singular.
+static int block_inverse(int b, const double* x, double* inv) {
+  double M[64], R[64];
+  for (int i = 0; i < b * b; ++i) M[i] = x[i];
+  for (int i = 0; i < b; ++i)
+    for (int j = 0; j < b; ++j) R[i * b + j] = (i == j) ? 1.0 : 0.0;
+  const double fn = std::sqrt(fro2(x, b));
+  for (int c = 0; c < b; ++c) {
+    int p = c;
+    for (int r = c + 1; r < b; ++r)
+      if (std::fabs(M[r * b + c]) > std::fabs(M[p * b + c])) p = r;
+    if (!(std::fabs(M[p * b + c]) > 1e-14 * fn)) return ORC_ESINGULAR_BLOCK;
+    if (p != c)
+      for (int j = 0; j < b; ++j) {
+        std::swap(M[p * b + j], M[c * b + j]);
+        std::swap(R[p * b + j], R[c * b + j]);
+      }
+    const double d = M[c * b + c];
+    for (int j = 0; j < b; ++j) {
+      M[c * b + j] = M[c * b + j] / d;
+      R[c * b + j] = R[c * b + j] / d;
+    }
+    for (int r = 0; r < b; ++r) {
+      if (r == c) continue;
+      const double f = M[r * b + c];
+      for (int j = 0; j < b; ++j) {
+        M[r * b + j] = M[r * b + j] - f * M[c * b + j];
+        R[r * b + j] = R[r * b + j] - f * R[c * b + j];
+      }
+    }
+  }
+  for (int i = 0; i < b * b; ++i) inv[i] = R[i];
+  return ORC_OK;
+}
+
+extern "C" int orc_block_inverse(int32_t b, const double* blk, double* inv) {
+  return block_inverse(b, blk, inv);
+}
+
+// c = a * b for b x b blocks; each entry summed over m ascending from the first product.
+static void blk_mul(int b, const double* a, const double* bb, double* c) {
+  for (int r = 0; r < b; ++r)
+    for (int cc = 0; cc < b; ++cc) {
+      double t = a[r * b] * bb[cc];
+      for (int m = 1; m < b; ++m) t = t + a[r * b + m] * bb[m * b + cc];
+      c[r * b + cc] = t;
+    }
+}
+
+static int64_t find_block(const orc_mat& A, int32_t I, int32_t J) {
+  auto b0 = A.col.begin() + A.ptr[I], e0 = A.col.begin() + A.ptr[I + 1];
+  auto it = std::lower_bound(b0, e0, J);
+  if (it == e0 || *it != J) return -1;
+  return it - A.col.begin();
+}
+
+// ---------------------------------------------------------------- C2 strength
+// strong(I,J), I != J, block (I,J) present: ||A_IJ||_F^2 > eps^2 ||A_II||_F ||A_JJ||_F
+// (PAPER.md:247-248, 257 eps_strong), dropped across slabs (C12),
+// then symmetric closure S <- S u S^T.  Returns adjacency lists (sorted, unique).
+static vector<int32_t> slab_bounds(int32_t n, int32_t nparts) {
+  vector<int32_t> bd(nparts + 1);
+  for (int32_t r = 0; r <= nparts; ++r) bd[r] = (int32_t)((int64_t)r * n / nparts);
+  return bd;
+}
+
+static int strength(const orc_mat& A, double eps, const vector<int32_t>& part_of,
+                    vector<vector<int32_t>>& adj) {
+  const int b = A.b;
+  vector<double> dn(A.n);
+  for (int32_t I = 0; I < A.n; ++I) {
+    int64_t k = find_block(A, I, I);
+    if (k < 0) return ORC_EZERODIAG;
+    dn[I] = std::sqrt(fro2(A.blk(k), b));
+  }
+  adj.assign(A.n, {});
+  const double eps2 = eps * eps;
+  for (int32_t I = 0; I < A.n; ++I)
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) {
+      int32_t J = A.col[k];
+      if (J == I || J >= A.n) continue;
+      if (part_of[I] != part_of[J]) continue;
+      if (fro2(A.blk(k), b) > eps2 * dn[I] * dn[J]) {
+        adj[I].push_back(J);
+        adj[J].push_back(I);  // symmetric closure
+      }
+    }
+  for (auto& a : adj) {
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+  }
+  return ORC_OK;
+}
+
+static vector<int32_t> part_of_rows(int32_t n, const vector<int32_t>& bd) {
+  vector<int32_t> p(n);
+  for (size_t r = 0; r + 1 < bd.size(); ++r)
+    for (int32_t i = bd[r]; i < bd[r + 1]; ++i) p[i] = (int32_t)r;
+  return p;
+}
+
+extern "C" int64_t orc_strength(const orc_mat* A, double eps, int32_t nparts, int32_t* ptr,
+                                int32_t* col) {
+  vector<vector<int32_t>> adj;
+  auto bd = slab_bounds(A->n, nparts < 1 ? 1 : nparts);
+  int rc = strength(*A, eps, part_of_rows(A->n, bd), adj);
+  if (rc != ORC_OK) return rc;
+  int64_t e = 0;
+  for (int32_t I = 0; I < A->n; ++I) {
+    if (ptr) ptr[I] = (int32_t)e;
+    for (int32_t J : adj[I]) {
+      if (col) col[e] = J;
+      ++e;
+    }
+  }
+  if (ptr) ptr[A->n] = (int32_t)e;
+  return e;
+}
+
+// ---------------------------------------------------------------- C3 aggregation
+// Pass 1 (SPEC.md:488 rule): for I ascending, if I is unassigned,
+// not isolated and none of its strong neighbours is assigned, open a new
+// aggregate with I and all its strong neighbours.  Pass 2: every still
+// unassigned non-isolated node joins the pass-1 aggregate of its lowest-index
+// strong neighbour assigned in pass 1.  Isolated nodes stay -1.
+static int32_t aggregate(const vector<vector<int32_t>>& adj, vector<int32_t>& agg,
+                         vector<int32_t>* roots) {
+  const int32_t n = (int32_t)adj.size();
+  agg.assign(n, -1);
+  if (roots) roots->assign(n, 0);
+  int32_t count = 0;
+  for (int32_t I = 0; I < n; ++I) {
+    if (agg[I] >= 0 || adj[I].empty()) continue;
+    bool free_nb = true;
+    for (int32_t J : adj[I])
+      if (agg[J] >= 0) {
+        free_nb = false;
+        break;
+      }
+    if (!free_nb) continue;
+    int32_t id = count++;
+    agg[I] = id;
+    if (roots) (*roots)[I] = 1;
+    for (int32_t J : adj[I]) agg[J] = id;
+  }
+  vector<int32_t> pass1 = agg;
+  for (int32_t I = 0; I < n; ++I) {
+    if (pass1[I] >= 0 || adj[I].empty()) continue;
+    for (int32_t J : adj[I])  // ascending: the first assigned one is the lowest index
+      if (pass1[J] >= 0) {
+        agg[I] = pass1[J];
+        break;
+      }
+  }
+  return count;
+}
+
+extern "C" int32_t orc_aggregate(const orc_mat* A, double eps, int32_t nparts, int32_t* agg) {
+  vector<vector<int32_t>> adj;
+  auto bd = slab_bounds(A->n, nparts < 1 ? 1 : nparts);
+  int rc = strength(*A, eps, part_of_rows(A->n, bd), adj);
+  if (rc != ORC_OK) return rc;
+  vector<int32_t> a;
+  int32_t nc = aggregate(adj, a, nullptr);
+  std::copy(a.begin(), a.end(), agg);
+  return nc;
+}
+
+extern "C" int32_t orc_roots(const orc_mat* A, double eps, int32_t nparts, int32_t* is_root) {
+  vector<vector<int32_t>> adj;
+  auto bd = slab_bounds(A->n, nparts < 1 ? 1 : nparts);
+  int rc = strength(*A, eps, part_of_rows(A->n, bd), adj);
+  if (rc != ORC_OK) return rc;
+  vector<int32_t> a, r;
+  int32_t nc = aggregate(adj, a, &r);
+  std::copy(r.begin(), r.end(), is_root);
+  return nc;
+}
+
+// ---------------------------------------------------------------- sparse products
+// C = A * B (Gustavson), structural pattern sorted ascending, nothing dropped;
+// every C_ij accumulated over k ascending from 0: C_ij = C_ij + (A_ik B_kj)
+// (SURVEY.md C6 fixed-order reading).
+static orc_mat spgemm(const orc_mat& A, const orc_mat& B) {
+  const int b = A.b;
+  orc_mat C;
+  C.n = A.n;
+  C.m = B.m;
+  C.b = b;
+  C.ptr.assign(A.n + 1, 0);
+  vector<int64_t> pos(B.m, -1);
+  vector<int32_t> cols;
+  vector<double> tmp(b * b);
+  for (int32_t i = 0; i < A.n; ++i) {
+    cols.clear();
+    for (int32_t ka = A.ptr[i]; ka < A.ptr[i + 1]; ++ka) {
+      int32_t k = A.col[ka];
+      for (int32_t kb = B.ptr[k]; kb < B.ptr[k + 1]; ++kb) {
+        int32_t j = B.col[kb];
+        if (pos[j] == -2) continue;
+        pos[j] = -2;
+        cols.push_back(j);
+      }
+    }
+    std::sort(cols.begin(), cols.end());
+    int64_t base = (int64_t)C.col.size();
+    for (size_t t = 0; t < cols.size(); ++t) {
+      pos[cols[t]] = base + (int64_t)t;
+      C.col.push_back(cols[t]);
+    }
+    C.val.resize(C.col.size() * b * b, 0.0);
+    for (int32_t ka = A.ptr[i]; ka < A.ptr[i + 1]; ++ka) {
+      int32_t k = A.col[ka];
+      for (int32_t kb = B.ptr[k]; kb < B.ptr[k + 1]; ++kb) {
+        blk_mul(b, A.blk(ka), B.blk(kb), tmp.data());
+        double* c = C.blk(pos[B.col[kb]]);
+        for (int e = 0; e < b * b; ++e) c[e] = c[e] + tmp[e];
+      }
+    }
+    for (int32_t j : cols) pos[j] = -1;
+    C.ptr[i + 1] = (int32_t)C.col.size();
+  }
+  return C;
+}
+
+// R = P^T, each block transposed ("R = P^T")
+static orc_mat transpose(const orc_mat& P) {
+  const int b = P.b;
+  orc_mat R;
+  R.n = P.m;
+  R.m = P.n;
+  R.b = b;
+  R.ptr.assign(P.m + 1, 0);
+  for (int32_t c : P.col) R.ptr[c + 1]++;
+  for (int32_t i = 0; i < P.m; ++i) R.ptr[i + 1] += R.ptr[i];
+  R.col.resize(P.col.size());
+  R.val.resize(P.val.size());
+  vector<int32_t> fill(R.ptr.begin(), R.ptr.end() - 1);
+  for (int32_t I = 0; I < P.n; ++I)  // ascending I: rows of R come out sorted
+    for (int32_t k = P.ptr[I]; k < P.ptr[I + 1]; ++k) {
+      int32_t c = P.col[k];
+      int32_t d = fill[c]++;
+      R.col[d] = I;
+      const double* s = P.blk(k);
+      double* t = R.blk(d);
+      for (int r = 0; r < b; ++r)
+        for (int cc = 0; cc < b; ++cc) t[cc * b + r] = s[r * b + cc];
+    }
+  return R;
+}
+
+// ---------------------------------------------------------------- C4/C5 prolongator
+// P_tent(I, agg(I)) = I_b (C4).  A_F keeps the diagonal and strong blocks; every
+// weak off-diagonal block is added (ascending column) into its row's diagonal
+// (C5 lumping).  P = P_tent - omega * (D^-1 (A_F P_tent)), D_I = A_F,II,
+// omega = sa_omega (C5 reading: 2/3).  PAPER.md:195, 209 (smoothed_aggregation).
+static int smoothed_prolongator(const orc_mat& A, const vector<vector<int32_t>>& adj,
+                                const vector<int32_t>& agg, int32_t nc, double omega,
+                                orc_mat& P) {
+  const int b = A.b, bb = b * b;
+  // A_F
+  orc_mat AF;
+  AF.n = A.n;
+  AF.m = A.m;
+  AF.b = b;
+  AF.ptr.assign(A.n + 1, 0);
+  vector<double> Dinv((size_t)A.n * bb);
+  for (int32_t I = 0; I < A.n; ++I) {
+    int64_t kd = find_block(A, I, I);
+    if (kd < 0) return ORC_EZERODIAG;
+    vector<double> D(A.blk(kd), A.blk(kd) + bb);
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) {
+      int32_t J = A.col[k];
+      if (J == I) continue;
+      bool strong = std::binary_search(adj[I].begin(), adj[I].end(), J);
+      if (!strong)
+        for (int e = 0; e < bb; ++e) D[e] = D[e] + A.blk(k)[e];
+    }
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) {
+      int32_t J = A.col[k];
+      bool keep = (J == I) || std::binary_search(adj[I].begin(), adj[I].end(), J);
+      if (!keep) continue;
+      AF.col.push_back(J);
+      const double* src = (J == I) ? D.data() : A.blk(k);
+      AF.val.insert(AF.val.end(), src, src + bb);
+    }
+    AF.ptr[I + 1] = (int32_t)AF.col.size();
+    int rc = block_inverse(b, D.data(), &Dinv[(size_t)I * bb]);
+    if (rc != ORC_OK) return rc;
+  }
+  // P_tent
+  orc_mat Pt;
+  Pt.n = A.n;
+  Pt.m = nc;
+  Pt.b = b;
+  Pt.ptr.assign(A.n + 1, 0);
+  for (int32_t I = 0; I < A.n; ++I) {
+    if (agg[I] >= 0) {
+      Pt.col.push_back(agg[I]);
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) Pt.val.push_back(r == c ? 1.0 : 0.0);
+    }
+    Pt.ptr[I + 1] = (int32_t)Pt.col.size();
+  }
+  orc_mat T = spgemm(AF, Pt);  // pattern(A_F P_tent), contains pattern(P_tent)
+  P = T;
+  vector<double> dt(bb);
+  for (int32_t I = 0; I < A.n; ++I)
+    for (int32_t k = T.ptr[I]; k < T.ptr[I + 1]; ++k) {
+      blk_mul(b, &Dinv[(size_t)I * bb], T.blk(k), dt.data());
+      double* p = P.blk(k);
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) {
+          double pt = (T.col[k] == agg[I] && r == c) ? 1.0 : 0.0;
+          p[r * b + c] = pt - omega * dt[r * b + c];
+        }
+    }
+  return ORC_OK;
+}
+
+// ---------------------------------------------------------------- C8 smoother
+// SPAI0: M_I = theta_I A_II^-1, theta_I = ||A_II||_F^2 / sum_J ||A_IJ||_F^2
+// (block generalisation of Broker-Grote SPAI(0)).
+// Damped Jacobi: M_I = omega_J A_II^-1.
+static int smoother_blocks(const orc_mat& A, int kind, double omega_j, vector<double>& M) {
+  const int b = A.b, bb = b * b;
+  M.assign((size_t)A.n * bb, 0.0);
+  vector<double> inv(bb);
+  for (int32_t I = 0; I < A.n; ++I) {
+    int64_t kd = find_block(A, I, I);
+    if (kd < 0) return ORC_EZERODIAG;
+    int rc = block_inverse(b, A.blk(kd), inv.data());
+    if (rc != ORC_OK) return rc;
+    double theta = omega_j;
+    if (kind == ORC_SPAI0) {
+      double den = 0.0;
+      for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k) den = den + fro2(A.blk(k), b);
+      theta = fro2(A.blk(kd), b) / den;
+    }
+    for (int e = 0; e < bb; ++e) M[(size_t)I * bb + e] = theta * inv[e];
+  }
+  return ORC_OK;
+}
+
+// ---------------------------------------------------------------- hierarchy
+struct Level {
+  orc_mat A, P, R;          // fp64 setup values
+  vector<int32_t> agg;
+  int32_t nc = 0;
+  vector<double> M;         // fp64 setup values
+  orc_mat As, Ps, Rs;       // solve copies (narrowed when hier_f32)
+  vector<double> Ms;
+};
+
+struct Coarse {
+  int32_t N = 0;
+  vector<double> LU;        // dense N x N, row-major, partial pivoting
+  vector<int32_t> piv;
+};
+
+struct orc_solver {
+  orc_params p;
+  orc_mat A;                // outer operator, fp64
+  bool schur = false;
+  int32_t bh = 0;           // block size of the AMG hierarchy
+  vector<Level> lv;
+  orc_mat Acoarse;          // coarsest matrix (fp64)
+  Coarse coarse;
+  // Schur split (C10) on A's block pattern
+  orc_mat Au;
+  vector<double> Bv, BTv;   // nnz * 3 (row pc, cols vel) and (rows vel, col pc)
+  vector<double> Shat_diag, mS;
+  vector<double> Bs, BTs, mSs;
+  vector<int32_t> vel;      // velocity component indices
+};
+
+static orc_mat narrowed(const orc_mat& A) {
+  orc_mat B = A;
+  for (double& v : B.val) v = f32r(v);
+  return B;
+}
+
+// Dense LU with partial pivoting of the scalar expansion (C7).
+static int coarse_factor(const orc_mat& A, Coarse& C) {
+  const int b = A.b;
+  const int32_t N = A.n * b;
+  C.N = N;
+  C.LU.assign((size_t)N * N, 0.0);
+  C.piv.assign(N, 0);
+  for (int32_t I = 0; I < A.n; ++I)
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k)
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c)
+          C.LU[(size_t)(I * b + r) * N + (size_t)A.col[k] * b + c] = A.blk(k)[r * b + c];
+  double* a = C.LU.data();
+  for (int32_t c = 0; c < N; ++c) {
+    int32_t p = c;
+    for (int32_t r = c + 1; r < N; ++r)
+      if (std::fabs(a[(size_t)r * N + c]) > std::fabs(a[(size_t)p * N + c])) p = r;
+    if (a[(size_t)p * N + c] == 0.0) return ORC_ESINGULAR_BLOCK;
+    C.piv[c] = p;
+    if (p != c)
+      for (int32_t j = 0; j < N; ++j) std::swap(a[(size_t)p * N + j], a[(size_t)c * N + j]);
+    for (int32_t r = c + 1; r < N; ++r) {
+      double l = a[(size_t)r * N + c] / a[(size_t)c * N + c];
+      a[(size_t)r * N + c] = l;
+      for (int32_t j = c + 1; j < N; ++j) a[(size_t)r * N + j] = a[(size_t)r * N + j] - l * a[(size_t)c * N + j];
+    }
+  }
+  return ORC_OK;
+}
+
+static void coarse_solve(const Coarse& C, const double* f, double* x, bool rf) {
+  const int32_t N = C.N;
+  vector<double> y(f, f + N);
+  for (int32_t c = 0; c < N; ++c) std::swap(y[c], y[C.piv[c]]);
+  for (int32_t r = 0; r < N; ++r)
+    for (int32_t j = 0; j < r; ++j) y[r] = y[r] - C.LU[(size_t)r * N + j] * y[j];
+  for (int32_t r = N - 1; r >= 0; --r) {
+    for (int32_t j = r + 1; j < N; ++j) y[r] = y[r] - C.LU[(size_t)r * N + j] * y[j];
+    y[r] = y[r] / C.LU[(size_t)r * N + r];
+  }
+  for (int32_t i = 0; i < N; ++i) x[i] = rf ? f32r(y[i]) : y[i];
+}
+
+// C7: repeat C2-C6 while n_l * b > coarse_enough and l < max_levels - 1;
+// stop if n_c == 0 or n_c >= n_l.  Coarsest: dense LU.
+static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
+  const orc_params& p = s.p;
+  orc_mat A = A0;
+  vector<int32_t> bd = slab_bounds(A.n, p.nparts < 1 ? 1 : p.nparts);
+  s.lv.clear();
+  while ((int64_t)A.n * A.b > p.coarse_enough && (int32_t)s.lv.size() < p.max_levels - 1) {
+    vector<vector<int32_t>> adj;
+    int rc = strength(A, p.eps_strong, part_of_rows(A.n, bd), adj);
+    if (rc != ORC_OK) return rc;
+    Level L;
+    vector<int32_t> roots;
+    L.nc = aggregate(adj, L.agg, &roots);
+    if (L.nc == 0 || L.nc >= A.n) break;
+    rc = smoothed_prolongator(A, adj, L.agg, L.nc, p.sa_omega, L.P);
+    if (rc != ORC_OK) return rc;
+    L.R = transpose(L.P);
+    rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
+    if (rc != ORC_OK) return rc;
+    orc_mat AP = spgemm(A, L.P);
+    orc_mat Ac = spgemm(L.R, AP);
+    // coarse slab bounds: aggregates are numbered in ascending root order (C3, C12)
+    vector<int32_t> nb(bd.size(), 0);
+    for (size_t r = 1; r < bd.size(); ++r) {
+      int32_t cnt = 0;
+      for (int32_t i = 0; i < bd[r]; ++i) cnt += roots[i];
+      nb[r] = cnt;
+    }
+    bd = nb;
+    L.A = std::move(A);
+    A = std::move(Ac);
+    s.lv.push_back(std::move(L));
+  }
+  if ((int64_t)A.n * A.b > 16384) return ORC_EINVAL;  // coarsening stalled: dense solve too large
+  s.Acoarse = A;
+  int rc = coarse_factor(A, s.coarse);
+  if (rc != ORC_OK) return rc;
+  for (Level& L : s.lv) {
+    L.As = p.hier_f32 ? narrowed(L.A) : L.A;
+    L.Ps = p.hier_f32 ? narrowed(L.P) : L.P;
+    L.Rs = p.hier_f32 ? narrowed(L.R) : L.R;
+    L.Ms = L.M;
+    if (p.hier_f32)
+      for (double& v : L.Ms) v = f32r(v);
+  }
+  return ORC_OK;
+}
+
+// ---------------------------------------------------------------- C9 V-cycle
+// V(l, f): if l == L: return A_L^-1 f
+//          x = M f;  r = f - A x;  xc = V(l+1, R r);  x = x + P xc;  x = x + M (f - A x)
+// (npre = npost = 1 reading).  Every line computes in fp64 and
+// rounds once when its vector is stored (vec_f32).
+static void apply_M(const vector<double>& M, int b, int32_t n, const double* f, double* x, bool rf) {
+  for (int32_t I = 0; I < n; ++I)
+    for (int r = 0; r < b; ++r) {
+      double t = 0.0;
+      for (int c = 0; c < b; ++c) t = t + M[(size_t)I * b * b + r * b + c] * f[(int64_t)I * b + c];
+      x[(int64_t)I * b + r] = rf ? f32r(t) : t;
+    }
+}
+
+// x' = x + M (f - A x), every row from the old x (Jacobi-type)
+static void smooth_step(const orc_mat& A, const vector<double>& M, const double* f,
+                        vector<double>& x, bool rf) {
+  const int b = A.b;
+  vector<double> res((size_t)A.n * b), xn((size_t)A.n * b);
+  residual(A, f, x.data(), res.data(), false);
+  for (int32_t I = 0; I < A.n; ++I)
+    for (int r = 0; r < b; ++r) {
+      double t = 0.0;
+      for (int c = 0; c < b; ++c) t = t + M[(size_t)I * b * b + r * b + c] * res[(int64_t)I * b + c];
+      double v = x[(int64_t)I * b + r] + t;
+      xn[(int64_t)I * b + r] = rf ? f32r(v) : v;
+    }
+  x.swap(xn);
+}
+
+static void vcycle(const orc_solver& s, size_t l, const vector<double>& f, vector<double>& x) {
+  const bool rf = s.p.vec_f32 != 0;
+  if (l == s.lv.size()) {
+    x.assign(f.size(), 0.0);
+    coarse_solve(s.coarse, f.data(), x.data(), rf);
+    return;
+  }
+  const Level& L = s.lv[l];
+  const int b = L.As.b;
+  const int32_t n = L.As.n;
+  x.assign((size_t)n * b, 0.0);
+  apply_M(L.Ms, b, n, f.data(), x.data(), rf);
+  for (int k = 1; k < s.p.npre; ++k) smooth_step(L.As, L.Ms, f.data(), x, rf);
+  vector<double> r((size_t)n * b);
+  residual(L.As, f.data(), x.data(), r.data(), rf);
+  vector<double> fc((size_t)L.nc * b), xc;
+  spmv(L.Rs, 1.0, r.data(), 0.0, fc.data(), rf);
+  vcycle(s, l + 1, fc, xc);
+  spmv(L.Ps, 1.0, xc.data(), 1.0, x.data(), rf);
+  for (int k = 0; k < s.p.npost; ++k) smooth_step(L.As, L.Ms, f.data(), x, rf);
+}
+
+// ---------------------------------------------------------------- C10 Schur
+// Split by block component on A's block pattern: velocity = all components but
+// pc, pressure = pc.  A_u (3x3), B (row pc x vel cols), B^T-part (vel rows x col
+// pc), C (pc,pc).  Shat = C - diag(B diag(A_u)^-1 B^T) (Eq. 10, PAPER.md:541-543,
+// adjust_p = 1 PAPER.md:622; diag(A_u) the scalar diagonal).  m_S = SPAI0(Shat):
+// m_i = Shat_ii / sum_j Shat_ij^2.
+static int schur_setup(orc_solver& s) {
+  const orc_mat& A = s.A;
+  const int b = A.b, pc = s.p.schur_p_component;
+  if (pc < 0 || pc >= b || b < 2) return ORC_EINVAL;
+  s.vel.clear();
+  for (int c = 0; c < b; ++c)
+    if (c != pc) s.vel.push_back(c);
+  const int bu = b - 1;
+  orc_mat& Au = s.Au;
+  Au.n = A.n;
+  Au.m = A.m;
+  Au.b = bu;
+  Au.ptr = A.ptr;
+  Au.col = A.col;
+  Au.val.assign((size_t)A.nnz() * bu * bu, 0.0);
+  s.Bv.assign((size_t)A.nnz() * bu, 0.0);
+  s.BTv.assign((size_t)A.nnz() * bu, 0.0);
+  vector<double> Cv(A.nnz());
+  for (int64_t k = 0; k < A.nnz(); ++k) {
+    const double* a = A.blk(k);
+    for (int r = 0; r < bu; ++r)
+      for (int c = 0; c < bu; ++c) Au.val[k * bu * bu + r * bu + c] = a[s.vel[r] * b + s.vel[c]];
+    for (int d = 0; d < bu; ++d) {
+      s.Bv[k * bu + d] = a[pc * b + s.vel[d]];
+      s.BTv[k * bu + d] = a[s.vel[d] * b + pc];
+    }
+    Cv[k] = a[pc * b + pc];
+  }
+  s.Shat_diag.assign(A.n, 0.0);
+  s.mS.assign(A.n, 0.0);
+  for (int32_t i = 0; i < A.n; ++i) {
+    int64_t kd = find_block(A, i, i);
+    if (kd < 0) return ORC_EZERODIAG;
+    double sum = 0.0;
+    for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      int32_t J = A.col[k];
+      int64_t kJJ = find_block(A, J, J), kJi = find_block(A, J, i);
+      if (kJJ < 0) return ORC_EZERODIAG;
+      if (kJi < 0) continue;  // structurally absent transpose entry contributes nothing
+      for (int d = 0; d < bu; ++d) {
+        double diag = Au.val[kJJ * bu * bu + d * bu + d];
+        if (diag == 0.0) return ORC_EZERODIAG;
+        double t = s.Bv[k * bu + d] * (1.0 / diag);
+        sum = sum + t * s.BTv[kJi * bu + d];
+      }
+    }
+    s.Shat_diag[i] = Cv[kd] - sum;
+    double den = 0.0;
+    for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      double v = (k == kd) ? s.Shat_diag[i] : Cv[k];
+      den = den + v * v;
+    }
+    if (den == 0.0) return ORC_EZERODIAG;
+    s.mS[i] = s.Shat_diag[i] / den;
+  }
+  s.Bs = s.Bv;
+  s.BTs = s.BTv;
+  s.mSs = s.mS;
+  if (s.p.hier_f32) {
+    for (double& v : s.Bs) v = f32r(v);
+    for (double& v : s.BTs) v = f32r(v);
+    for (double& v : s.mSs) v = f32r(v);
+  }
+  return ORC_OK;
+}
+
+// Eq. 9a then 9b with one application each:
+//   u* = V_u(r_u);  p = m_S o (r_p - B u*);  u = V_u(r_u - B^T p);  z = (u, p)
+static void schur_apply(const orc_solver& s, const double* r, double* z) {
+  const orc_mat& A = s.A;
+  const int b = A.b, pc = s.p.schur_p_component, bu = b - 1;
+  const bool rf = s.p.vec_f32 != 0;
+  const int32_t n = A.n;
+  vector<double> ru((size_t)n * bu), rp(n);
+  for (int32_t I = 0; I < n; ++I) {
+    for (int d = 0; d < bu; ++d) {
+      double v = r[(int64_t)I * b + s.vel[d]];
+      ru[(int64_t)I * bu + d] = rf ? f32r(v) : v;
+    }
+    double v = r[(int64_t)I * b + pc];
+    rp[I] = rf ? f32r(v) : v;
+  }
+  vector<double> us, u;
+  vcycle(s, 0, ru, us);
+  vector<double> p(n);
+  for (int32_t I = 0; I < n; ++I) {  // p = m_S o (r_p - B u*)
+    double acc = 0.0;
+    for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k)
+      for (int d = 0; d < bu; ++d) acc = acc + s.Bs[(size_t)k * bu + d] * us[(int64_t)A.col[k] * bu + d];
+    double v = s.mSs[I] * (rp[I] - acc);
+    p[I] = rf ? f32r(v) : v;
+  }
+  vector<double> ru2((size_t)n * bu);
+  for (int32_t I = 0; I < n; ++I) {  // r_u' = r_u - B^T p
+    for (int d = 0; d < bu; ++d) {
+      double acc = 0.0;
+      for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k)
+        acc = acc + s.BTs[(size_t)k * bu + d] * p[A.col[k]];
+      double v = ru[(int64_t)I * bu + d] - acc;
+      ru2[(int64_t)I * bu + d] = rf ? f32r(v) : v;
+    }
+  }
+  vcycle(s, 0, ru2, u);
+  for (int32_t I = 0; I < n; ++I) {
+    for (int d = 0; d < bu; ++d) z[(int64_t)I * b + s.vel[d]] = u[(int64_t)I * bu + d];
+    z[(int64_t)I * b + pc] = p[I];
+  }
+}
+
+static void precond(const orc_solver& s, const double* r, double* z) {
+  const int64_t N = (int64_t)s.A.n * s.A.b;
+  if (s.p.precond == ORC_PC_NONE) {
+    std::copy(r, r + N, z);
+    return;
+  }
+  if (s.schur) {
+    schur_apply(s, r, z);
+    return;
+  }
+  // monolithic AMG: narrow once, V-cycle, widen exactly (C9 precision paragraph)
+  vector<double> f(r, r + N), x;
+  if (s.p.vec_f32)
+    for (double& v : f) v = f32r(v);
+  vcycle(s, 0, f, x);
+  std::copy(x.begin(), x.end(), z);
+}
+
+extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out) {
+  if (!A || !p || !out || A->n != A->m) return ORC_EINVAL;
+  orc_solver* s = new orc_solver;
+  s->p = *p;
+  s->A = *A;
+  int rc = ORC_OK;
+  if (p->precond == ORC_PC_SCHUR) {
+    s->schur = true;
+    rc = schur_setup(*s);
+    if (rc == ORC_OK) rc = build_hierarchy(*s, s->Au);
+  } else if (p->precond == ORC_PC_AMG) {
+    rc = build_hierarchy(*s, s->A);
+  }
+  if (rc != ORC_OK) {
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return ORC_OK;
+}
+
+extern "C" void orc_free(orc_solver* s) { delete s; }
+extern "C" int32_t orc_levels(const orc_solver* s) {
+  return s->p.precond == ORC_PC_NONE ? 0 : (int32_t)s->lv.size() + 1;
+}
+
+extern "C" const orc_mat* orc_level_mat(const orc_solver* s, int32_t level, int32_t which) {
+  if (level < 0) return nullptr;
+  if ((size_t)level == s->lv.size()) return which == 0 ? &s->Acoarse : nullptr;
+  if ((size_t)level > s->lv.size()) return nullptr;
+  const Level& L = s->lv[level];
+  return which == 0 ? &L.A : which == 1 ? &L.P : which == 2 ? &L.R : nullptr;
+}
+extern "C" const int32_t* orc_level_agg(const orc_solver* s, int32_t level) {
+  if (level < 0 || (size_t)level >= s->lv.size()) return nullptr;
+  return s->lv[level].agg.data();
+}
+extern "C" const double* orc_level_M(const orc_solver* s, int32_t level) {
+  if (level < 0 || (size_t)level >= s->lv.size()) return nullptr;
+  return s->lv[level].M.data();
+}
+extern "C" const orc_mat* orc_schur_Au(const orc_solver* s) { return s->schur ? &s->Au : nullptr; }
+extern "C" const double* orc_schur_Shat_diag(const orc_solver* s) {
+  return s->schur ? s->Shat_diag.data() : nullptr;
+}
+extern "C" const double* orc_schur_mS(const orc_solver* s) { return s->schur ? s->mS.data() : nullptr; }
+
+extern "C" int orc_vcycle(const orc_solver* s, const double* f, double* x) {
+  if (s->p.precond == ORC_PC_NONE) return ORC_EINVAL;
+  const orc_mat& A0 = s->lv.empty() ? s->Acoarse : s->lv[0].A;
+  vector<double> fv(f, f + (int64_t)A0.n * A0.b), xv;
+  vcycle(*s, 0, fv, xv);
+  std::copy(xv.begin(), xv.end(), x);
+  return ORC_OK;
+}
+
+extern "C" int orc_precond(const orc_solver* s, const double* r, double* z) {
+  precond(*s, r, z);
+  return ORC_OK;
+}
+
+// ---------------------------------------------------------------- C11 Krylov
+static bool is_fin(double v) { return std::isfinite(v); }
+
+// PCG (cfg 1).  Stop on the recurrence ||r|| <= rtol ||b||, then verify the true
+// residual; if it fails, continue from r = b - A x.
+static int solve_cg(const orc_solver& s, const double* bp, double* xp, double rtol,
+                    orc_report* rep, double* hist) {
+  const int64_t N = (int64_t)s.A.n * s.A.b;
+  vector<double> b(bp, bp + N), x(xp, xp + N), r(N), z(N), p(N), q(N);
+  const double nb = nrm2(b);
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  double nr = nrm2(r);
+  if (hist) hist[0] = nr / nb;
+  int it = 0;
+  int status = ORC_NOT_CONVERGED;
+  if (nr <= rtol * nb) status = ORC_OK;
+  bool restart = true;
+  double rho = 0.0;
+  while (status != ORC_OK && it < s.p.maxiter) {
+    if (restart) {
+      precond(s, r.data(), z.data());
+      p = z;
+      rho = dot(r, z);
+      restart = false;
+    }
+    spmv(s.A, 1.0, p.data(), 0.0, q.data(), false);
+    double pq = dot(p, q);
+    if (pq == 0.0 || !is_fin(pq)) {
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    double alpha = rho / pq;
+    for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * p[i];
+    for (int64_t i = 0; i < N; ++i) r[i] = r[i] - alpha * q[i];
+    ++it;
+    nr = nrm2(r);
+    if (hist) hist[it] = nr / nb;
+    if (nr <= rtol * nb) {
+      residual(s.A, b.data(), x.data(), r.data(), false);
+      if (nrm2(r) <= rtol * nb) {
+        status = ORC_OK;
+        break;
+      }
+      restart = true;
+      continue;
+    }
+    precond(s, r.data(), z.data());
+    double rho_new = dot(r, z);
+    double beta = rho_new / rho;
+    for (int64_t i = 0; i < N; ++i) p[i] = z[i] + beta * p[i];
+    rho = rho_new;
+  }
+  std::copy(x.begin(), x.end(), xp);
+  rep->iters = it;
+  rep->restarts = 0;
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  rep->relres_true = nrm2(r) / nb;
+  rep->converged = status == ORC_OK;
+  return status;
+}
+
+// Right-preconditioned BiCGStab (van der Vorst), shadow rhat = r0, half-step exit
+// on ||s|| <= rtol ||b||; breakdown (|rho| <= 1e-30 ||b||^2, rhat.v = 0, t.t = 0,
+// omega = 0 or non-finite) -> one restart, then ORC_EBREAKDOWN (C11).
+static int solve_bicgstab(const orc_solver& s, const double* bp, double* xp, double rtol,
+                          orc_report* rep, double* hist) {
+  const int64_t N = (int64_t)s.A.n * s.A.b;
+  vector<double> b(bp, bp + N), x(xp, xp + N), r(N), rh(N), p(N), ph(N), v(N), sv(N), sh(N), t(N);
+  const double nb = nrm2(b);
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  if (hist) hist[0] = nrm2(r) / nb;
+  int it = 0, restarts = 0;
+  int status = ORC_NOT_CONVERGED;
+  if (nrm2(r) <= rtol * nb) status = ORC_OK;
+  rh = r;
+  bool first = true;
+  double rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  auto do_restart = [&]() -> bool {
+    if (restarts >= 1) return false;
+    ++restarts;
+    residual(s.A, b.data(), x.data(), r.data(), false);
+    rh = r;
+    first = true;
+    return true;
+  };
+  auto verify = [&]() -> bool {  // true residual check
+    residual(s.A, b.data(), x.data(), r.data(), false);
+    if (nrm2(r) <= rtol * nb) return true;
+    rh = r;
+    first = true;
+    return false;
+  };
+  while (status != ORC_OK && it < s.p.maxiter) {
+    double rho = dot(rh, r);
+    if (!(std::fabs(rho) > 1e-30 * nb * nb) || !is_fin(rho)) {
+      if (do_restart()) continue;
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    if (first) {
+      p = r;
+      first = false;
+    } else {
+      double beta = (rho / rho_old) * (alpha / omega);
+      for (int64_t i = 0; i < N; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+    }
+    precond(s, p.data(), ph.data());
+    spmv(s.A, 1.0, ph.data(), 0.0, v.data(), false);
+    double rv = dot(rh, v);
+    if (rv == 0.0 || !is_fin(rv)) {
+      if (do_restart()) continue;
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    alpha = rho / rv;
+    for (int64_t i = 0; i < N; ++i) sv[i] = r[i] - alpha * v[i];
+    ++it;
+    double ns = nrm2(sv);
+    if (ns <= rtol * nb) {
+      for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * ph[i];
+      if (hist) hist[it] = ns / nb;
+      if (verify()) {
+        status = ORC_OK;
+        break;
+      }
+      continue;
+    }
+    precond(s, sv.data(), sh.data());
+    spmv(s.A, 1.0, sh.data(), 0.0, t.data(), false);
+    double tt = dot(t, t);
+    if (tt == 0.0 || !is_fin(tt)) {
+      if (do_restart()) continue;
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    omega = dot(t, sv) / tt;
+    for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * ph[i] + omega * sh[i];
+    for (int64_t i = 0; i < N; ++i) r[i] = sv[i] - omega * t[i];
+    rho_old = rho;
+    double nr = nrm2(r);
+    if (hist) hist[it] = nr / nb;
+    if (omega == 0.0 || !is_fin(omega)) {
+      if (do_restart()) continue;
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    if (nr <= rtol * nb && verify()) {
+      status = ORC_OK;
+      break;
+    }
+  }
+  std::copy(x.begin(), x.end(), xp);
+  rep->iters = it;
+  rep->restarts = restarts;
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  rep->relres_true = nrm2(r) / nb;
+  rep->converged = status == ORC_OK;
+  return status;
+}
+
+// Flexible right-preconditioned GMRES(m) (C11): z_j = M v_j, w = A z_j, CGS2 Arnoldi
+// (two classical Gram-Schmidt passes, coefficients summed), Givens rotations, stop
+// when |g_{j+1}| <= rtol ||b||, x += Z y, true residual recomputed at every cycle end.
+// Listing 1 names GMRES; the flexible form is the C11 reading.
+// If hist != NULL, hist[j] = true ||b - A x_j|| / ||b|| for every Arnoldi step j.
+static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double rtol,
+                       orc_report* rep, double* hist) {
+  const int64_t N = (int64_t)s.A.n * s.A.b;
+  const int m = s.p.gmres_m;
+  vector<double> b(bp, bp + N), x(xp, xp + N), r(N), w(N), tmpx(N), tmpr(N);
+  vector<vector<double>> V(m + 1, vector<double>(N)), Z(m, vector<double>(N));
+  vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), h(m + 1), h2(m + 1);
+  const double nb = nrm2(b);
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  double beta = nrm2(r);
+  if (hist) hist[0] = beta / nb;
+  int it = 0, cycles = 0;
+  int status = ORC_NOT_CONVERGED;
+  if (beta <= rtol * nb) status = ORC_OK;
+  while (status != ORC_OK && it < s.p.maxiter) {
+    ++cycles;
+    for (int64_t i = 0; i < N; ++i) V[0][i] = r[i] / beta;
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    bool stop = false;
+    for (; j < m && !stop; ++j) {
+      precond(s, V[j].data(), Z[j].data());
+      spmv(s.A, 1.0, Z[j].data(), 0.0, w.data(), false);
+      for (int i = 0; i <= j; ++i) h[i] = dot(V[i], w);
+      for (int i = 0; i <= j; ++i)
+        for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h[i] * V[i][q];
+      for (int i = 0; i <= j; ++i) h2[i] = dot(V[i], w);
+      for (int i = 0; i <= j; ++i)
+        for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h2[i] * V[i][q];
+      for (int i = 0; i <= j; ++i) h[i] = h[i] + h2[i];
+      double hn = nrm2(w);
+      if (hn != 0.0)
+        for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / hn;
+      h[j + 1] = hn;
+      for (int i = 0; i < j; ++i) {  // previous rotations
+        double t = cs[i] * h[i] + sn[i] * h[i + 1];
+        h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = t;
+      }
+      double rr = std::hypot(h[j], h[j + 1]);
+      if (rr == 0.0 || !is_fin(rr)) {
+        status = ORC_EBREAKDOWN;
+        stop = true;
+        break;
+      }
+      cs[j] = h[j] / rr;
+      sn[j] = h[j + 1] / rr;
+      h[j] = rr;
+      h[j + 1] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = h[i];
+      ++it;
+      if (hist) {  // true residual of the current iterate x + Z y_j
+        for (int i = j; i >= 0; --i) {
+          double t = g[i];
+          for (int k = i + 1; k <= j; ++k) t = t - H[(size_t)i * m + k] * y[k];
+          y[i] = t / H[(size_t)i * m + i];
+        }
+        tmpx = x;
+        for (int i = 0; i <= j; ++i)
+          for (int64_t q = 0; q < N; ++q) tmpx[q] = tmpx[q] + y[i] * Z[i][q];
+        residual(s.A, b.data(), tmpx.data(), tmpr.data(), false);
+        hist[it] = nrm2(tmpr) / nb;
+      }
+      if (std::fabs(g[j + 1]) <= rtol * nb || it >= s.p.maxiter || hn == 0.0) stop = true;
+    }
+    if (status == ORC_EBREAKDOWN) break;
+    int k = j;  // number of Arnoldi steps in this cycle
+    for (int i = k - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int c = i + 1; c < k; ++c) t = t - H[(size_t)i * m + c] * y[c];
+      y[i] = t / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < k; ++i)
+      for (int64_t q = 0; q < N; ++q) x[q] = x[q] + y[i] * Z[i][q];
+    residual(s.A, b.data(), x.data(), r.data(), false);
+    beta = nrm2(r);
+    if (beta <= rtol * nb) status = ORC_OK;
+  }
+  std::copy(x.begin(), x.end(), xp);
+  rep->iters = it;
+  rep->restarts = cycles > 0 ? cycles - 1 : 0;
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  rep->relres_true = nrm2(r) / nb;
+  rep->converged = status == ORC_OK;
+  return status;
+}
+
+extern "C" int orc_solve(const orc_solver* s, const double* b, double* x, double rtol,
+                         orc_report* rep, double* history) {
+  const int64_t N = (int64_t)s->A.n * s->A.b;
+  rep->levels = orc_levels(s);
+  double nb = 0.0;
+  for (int64_t i = 0; i < N; ++i) nb = nb + b[i] * b[i];
+  if (nb == 0.0) {  // ||b|| = 0 -> x = 0, converged, relres 0
+    std::fill(x, x + N, 0.0);
+    rep->iters = 0;
+    rep->converged = 1;
+    rep->restarts = 0;
+    rep->relres_true = 0.0;
+    return ORC_OK;
+  }
+  switch (s->p.solver) {
+    case ORC_CG: return solve_cg(*s, b, x, rtol, rep, history);
+    case ORC_BICGSTAB: return solve_bicgstab(*s, b, x, rtol, rep, history);
+    case ORC_GMRES: return solve_gmres(*s, b, x, rtol, rep, history);
+    default: return ORC_EINVAL;
+  }
+}

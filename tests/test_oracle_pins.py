@@ -1,0 +1,564 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(SURVEY.md §8(c) C0-C12).  None of these re-types an oracle formula: each
+check is a printed value, a closed form, an invariant, a library routine
+(numpy dense linear algebra) or brute force on a tiny input."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import bsr_dense, golden, laplace3_blocks, poisson1d, random_bsr
+
+pytestmark = pytest.mark.filterwarnings("ignore")
+
+
+# ---------------------------------------------------------------- C0 / C1
+def test_worked_example_csr_to_bsr():
+    g = golden("worked_example.json")
+    A = oracle.csr_to_bsr(6, 6, 2, g["csr_ptr"], g["csr_col"], g["csr_val"])
+    ptr, col, val = A.to_arrays()
+    assert ptr.tolist() == g["bsr_ptr"]
+    assert col.tolist() == g["bsr_col"]
+    assert np.array_equal(val, np.array(g["bsr_val"]))
+    # ptr halves, col shrinks 4x
+    assert len(ptr) - 1 == (len(g["csr_ptr"]) - 1) // 2
+    assert len(col) * 4 == len(g["csr_col"])
+
+
+def test_worked_example_spmv():
+    g = golden("worked_example.json")
+    A = oracle.Mat.from_arrays(g["bsr_ptr"], g["bsr_col"], np.array(g["bsr_val"]))
+    y = oracle.spmv(A, np.ones(6))
+    assert np.allclose(y, g["y_ones"], rtol=0, atol=1e-14)
+
+
+def test_csr_to_bsr_explicit_zeros_and_not_divisible(rng):
+    # a tile with one scalar becomes a full block with explicit zeros
+    A = oracle.csr_to_bsr(4, 4, 2, [0, 1, 1, 2, 3], [1, 3, 2], [5.0, 7.0, 9.0])
+    ptr, col, val = A.to_arrays()
+    assert ptr.tolist() == [0, 1, 2] and col.tolist() == [0, 1]
+    assert val[0].tolist() == [[0, 5], [0, 0]] and val[1].tolist() == [[0, 7], [9, 0]]
+    with pytest.raises(ValueError):
+        oracle.csr_to_bsr(3, 3, 2, [0, 0, 0, 0], [], [])
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_spmv_dense(rng, b):
+    for n in (1, 7, 40):
+        ptr, col, val = random_bsr(rng, n, b, density=0.2)
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        x = rng.standard_normal(n * b)
+        y0 = rng.standard_normal(n * b)
+        D = bsr_dense(ptr, col, val)
+        for alpha, beta in ((1.0, 0.0), (-0.5, 2.0), (2.0, 1.0)):
+            y = oracle.spmv(A, x, alpha, beta, y0)
+            ref = alpha * (D @ x) + beta * y0
+            assert np.linalg.norm(y - ref) <= 1e-13 * max(1.0, np.linalg.norm(ref))
+
+
+def test_spmv_beta0_ignores_nan(rng):
+    ptr, col, val = random_bsr(rng, 10, 3)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    y = oracle.spmv(A, np.ones(30), 1.0, 0.0, np.full(30, np.nan))
+    assert np.all(np.isfinite(y))
+
+
+def test_spmv_block_vs_scalar_expansion(rng):
+    # b-blocked vs scalar-expanded equivalence
+    ptr, col, val = random_bsr(rng, 12, 3, density=0.3)
+    D = bsr_dense(ptr, col, val)
+    rows, cols = np.nonzero(D != 0)
+    sptr = np.searchsorted(rows, np.arange(D.shape[0] + 1)).astype(np.int32)
+    As = oracle.Mat.from_arrays(sptr, cols.astype(np.int32), D[rows, cols].reshape(-1, 1, 1))
+    Ab = oracle.Mat.from_arrays(ptr, col, val)
+    x = rng.standard_normal(36)
+    assert np.allclose(oracle.spmv(As, x), oracle.spmv(Ab, x), rtol=0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- block inverse
+def test_block_inverse(rng):
+    assert np.array_equal(oracle.block_inverse(np.diag([2.0, 4.0])), np.diag([0.5, 0.25]))
+    assert np.array_equal(oracle.block_inverse(np.eye(3)), np.eye(3))
+    for b in (1, 2, 3, 4):
+        for _ in range(20):
+            X = rng.standard_normal((b, b)) + 3 * np.eye(b)
+            Xi = oracle.block_inverse(X)
+            assert np.linalg.norm(Xi @ X - np.eye(b)) < 1e-12
+    # a permutation needs pivoting
+    Pm = np.array([[0.0, 1.0], [1.0, 0.0]])
+    assert np.array_equal(oracle.block_inverse(Pm), Pm)
+    with pytest.raises(np.linalg.LinAlgError):
+        oracle.block_inverse(np.array([[1.0, 2.0], [2.0, 4.0]]))
+
+
+# ---------------------------------------------------------------- C2 strength
+def test_strength_eps0_keeps_all_and_diagonal_has_none(rng):
+    ptr, col, val = random_bsr(rng, 30, 3, density=0.2, symmetric_pattern=True, dom=5)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    sp, sc = oracle.strength(A, eps=0.0)
+    offdiag = sum(1 for i in range(30) for k in range(ptr[i], ptr[i + 1]) if col[k] != i)
+    assert len(sc) == offdiag
+    d = np.array([np.eye(3) * (i + 1) for i in range(30)])
+    Ad = oracle.Mat.from_arrays(np.arange(31, dtype=np.int32), np.arange(30, dtype=np.int32), d)
+    sp, sc = oracle.strength(Ad, 1e-3)
+    assert len(sc) == 0
+    agg, nc = oracle.aggregate(Ad)
+    assert nc == 0 and np.all(agg == -1)
+
+
+def test_strength_constructed_strong_weak(rng):
+    # off-diagonal blocks are either O(1) ("strong") or O(1e-9) ("weak"): the graph must be
+    # exactly the symmetrised set of O(1) blocks, whatever the exact threshold arithmetic.
+    n, b = 25, 2
+    ptr, col, val = random_bsr(rng, n, b, density=0.25, dom=4)
+    strong_set = set()
+    for i in range(n):
+        for k in range(ptr[i], ptr[i + 1]):
+            j = col[k]
+            if j == i:
+                continue
+            if rng.random() < 0.5:
+                val[k] *= 1e-9
+            else:
+                strong_set.add((i, j))
+                strong_set.add((j, i))
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    sp, sc = oracle.strength(A, 1e-3)
+    got = {(i, int(sc[k])) for i in range(n) for k in range(sp[i], sp[i + 1])}
+    assert got == strong_set
+
+
+def test_strength_1d_poisson_all_strong():
+    A = oracle.Mat.from_arrays(*poisson1d(9))
+    sp, sc = oracle.strength(A, 1e-3)  # |-1|^2 > 1e-6*2*2
+    assert len(sc) == 16
+
+
+def test_strength_slabs_drop_cross_edges():
+    A = oracle.Mat.from_arrays(*poisson1d(10))
+    sp, sc = oracle.strength(A, 1e-3, nparts=2)
+    assert len(sc) == 16  # the edge 4-5 is dropped both ways
+
+
+# ---------------------------------------------------------------- C3 aggregation
+def test_aggregation_1d_hand_trace():
+    g = golden("aggregation_1d.json")
+    agg, nc = oracle.aggregate(oracle.Mat.from_arrays(*poisson1d(9)))
+    assert agg.tolist() == g["n9_agg"] and nc == 3
+    agg, nc = oracle.aggregate(oracle.Mat.from_arrays(*poisson1d(729)))
+    assert nc == g["n729_count"]
+
+
+def _graph(sp, sc, n):
+    return [set(sc[sp[i]:sp[i + 1]].tolist()) for i in range(n)]
+
+
+def _dist2(adj, i):
+    d1 = adj[i]
+    d2 = set()
+    for j in d1:
+        d2 |= adj[j]
+    return (d1 | d2) - {i}
+
+
+def _parallel_rounds_roots(adj):
+    """Independent formulation: lexicographically-first MIS of the distance-2 graph by
+    parallel rounds: an undecided node becomes a root when every
+    lower-index node within distance 2 is decided non-root; it is removed when any node
+    within distance 2 is a root."""
+    n = len(adj)
+    UND, ROOT, NOT = 0, 1, 2
+    st = [NOT if not adj[i] else UND for i in range(n)]
+    nb2 = [_dist2(adj, i) for i in range(n)]
+    rounds = 0
+    while UND in st:
+        rounds += 1
+        new = list(st)
+        for i in range(n):
+            if st[i] != UND:
+                continue
+            if any(st[j] == ROOT for j in nb2[i]):
+                new[i] = NOT
+            elif all(st[j] == NOT for j in nb2[i] if j < i):
+                new[i] = ROOT
+        st = new
+    return [1 if s == ROOT else 0 for s in st], rounds
+
+
+def _check_aggregation_invariants(A, adj, agg, nc, roots):
+    n = len(adj)
+    root_ids = [i for i in range(n) if roots[i]]
+    assert len(root_ids) == nc
+    # coarse ids in ascending root order
+    assert [agg[r] for r in root_ids] == list(range(nc))
+    for a in root_ids:  # roots pairwise at distance >= 3
+        assert not (_dist2(adj, a) & set(root_ids))
+    for i in range(n):
+        if not adj[i]:
+            assert agg[i] == -1
+            continue
+        assert 0 <= agg[i] < nc
+        r = root_ids[agg[i]]
+        assert i == r or r in _dist2(adj, i)  # every member within distance 2 of its root
+
+
+def test_aggregation_invariants_and_rounds(rng):
+    for trial in range(6):
+        n = 60
+        ptr, col, val = random_bsr(rng, n, 2, density=0.06, symmetric_pattern=True, dom=3)
+        for i in range(n):  # make a few nodes isolated (weak rows)
+            if rng.random() < 0.1:
+                for k in range(ptr[i], ptr[i + 1]):
+                    if col[k] != i:
+                        val[k] *= 1e-12
+                        # symmetric partner
+                        for kk in range(ptr[col[k]], ptr[col[k] + 1]):
+                            if col[kk] == i:
+                                val[kk] *= 1e-12
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        sp, sc = oracle.strength(A, 1e-3)
+        adj = _graph(sp, sc, n)
+        agg, nc = oracle.aggregate(A)
+        roots = oracle.roots(A)
+        _check_aggregation_invariants(A, adj, agg, nc, roots)
+        pr, _ = _parallel_rounds_roots(adj)
+        assert pr == roots.tolist()
+
+
+def test_aggregation_probe_counts_7pt():
+    # 16^3 7-point -> 514 aggregates
+    ptr, col, val = laplace3_blocks(16)
+    agg, nc = oracle.aggregate(oracle.Mat.from_arrays(ptr, col, val))
+    assert nc == 514
+
+
+def test_aggregation_parallel_rounds_7pt_8():
+    ptr, col, val = laplace3_blocks(8)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    sp, sc = oracle.strength(A, 1e-3)
+    adj = _graph(sp, sc, 512)
+    pr, rounds = _parallel_rounds_roots(adj)
+    assert pr == oracle.roots(A).tolist()
+    assert rounds > 1
+
+
+# ---------------------------------------------------------------- C4-C6 hierarchy
+def _solver(ptr, col, val, **kw):
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    return A, oracle.Solver(A, **kw)
+
+
+def test_tentative_prolongator_omega0():
+    ptr, col, val = laplace3_blocks(6)
+    A, S = _solver(ptr, col, val, sa_omega=0.0, coarse_enough=64, hier_f32=0, vec_f32=0)
+    P = S.level_mat(0, 1).dense()
+    agg = S.level_agg(0)
+    nc = agg.max() + 1
+    sizes = np.bincount(agg[agg >= 0], minlength=nc)
+    assert np.array_equal(P.T @ P, np.kron(np.diag(sizes), np.eye(3)))
+    assert set(np.unique(P)) <= {0.0, 1.0}
+
+
+def test_smoothed_prolongator_partition_of_unity():
+    # interior rows of the 7-point Laplacian tensor I3 have zero row sums; all edges are
+    # strong, so A_F = A and P's row sums equal P_tent's
+    n = 6
+    ptr, col, val = laplace3_blocks(n)
+    A, S = _solver(ptr, col, val, coarse_enough=64, hier_f32=0, vec_f32=0)
+    P = S.level_mat(0, 1).dense()
+    rs = P.reshape(n ** 3, 3, -1, 3).sum(axis=2)  # block row sums
+    for i in range(n ** 3):
+        x, y, z = i % n, (i // n) % n, i // (n * n)
+        if 0 < x < n - 1 and 0 < y < n - 1 and 0 < z < n - 1:
+            assert np.allclose(rs[i], np.eye(3), atol=1e-14)
+
+
+def test_galerkin_identity_and_symmetry(rng):
+    # P^T (A (P u)) = A_c u (north_star) and symmetry preservation
+    ptr, col, val = gen.matrix(gen.POISSON3, 8)
+    A, S = _solver(ptr, col, val, coarse_enough=64, hier_f32=0, vec_f32=0)
+    assert S.levels >= 3
+    for l in range(S.levels - 1):
+        Al, Pl, Rl, Ac = (S.level_mat(l, 0), S.level_mat(l, 1), S.level_mat(l, 2), S.level_mat(l + 1, 0))
+        u = rng.standard_normal(Ac.info()[0] * 3)
+        lhs = oracle.spmv(Rl, oracle.spmv(Al, oracle.spmv(Pl, u)))
+        rhs = oracle.spmv(Ac, u)
+        assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(rhs)
+        D = Ac.dense()
+        assert np.linalg.norm(D - D.T) <= 1e-12 * np.linalg.norm(D)
+        assert np.array_equal(Rl.dense(), Pl.dense().T)
+
+
+def test_galerkin_dense_triple_product(rng):
+    ptr, col, val = random_bsr(rng, 150, 2, density=0.03, symmetric_pattern=True, dom=6)
+    A, S = _solver(ptr, col, val, coarse_enough=40, hier_f32=0, vec_f32=0)
+    assert S.levels >= 2
+    Ad = A.dense()
+    P = S.level_mat(0, 1).dense()
+    Ac = S.level_mat(1, 0).dense()
+    assert np.linalg.norm(P.T @ Ad @ P - Ac) <= 1e-12 * np.linalg.norm(Ac)
+
+
+def test_level_sizes_strictly_decrease():
+    ptr, col, val = gen.matrix(gen.STOKES, 12)
+    A, S = _solver(ptr, col, val, coarse_enough=50)
+    sizes = [S.level_mat(l, 0).info()[0] for l in range(S.levels)]
+    assert all(a > b for a, b in zip(sizes, sizes[1:]))
+
+
+# ---------------------------------------------------------------- C8 smoother
+def test_spai0_is_scaled_block_inverse(rng):
+    # M_I A_II = theta_I I with 0 < theta_I <= 1; with vanishing couplings theta -> 1,
+    # i.e. a diagonal A gets its exact inverse
+    n, b = 40, 3
+    blocks = [rng.standard_normal((b, b)) + 4 * np.eye(b) for _ in range(n)]
+    for scale in (0.5, 1e-2):
+        pp, cc, vv = [0], [], []
+        for i in range(n):
+            for j in (i - 1, i, i + 1):
+                if 0 <= j < n:
+                    cc.append(j)
+                    vv.append(blocks[i] if j == i else -scale * np.eye(b))
+            pp.append(len(cc))
+        A, S = _solver(np.array(pp, np.int32), np.array(cc, np.int32), np.array(vv), coarse_enough=30,
+                       hier_f32=0, vec_f32=0)
+        M = S.level_M(0)
+        for i in range(n):
+            T = M[i] @ blocks[i]
+            theta = T[0, 0]
+            assert np.allclose(T, theta * np.eye(b), atol=1e-13)
+            assert 0 < theta <= 1
+            if scale == 1e-2:
+                assert abs(theta - 1) < 1e-4
+
+
+def test_spai0_closed_form_7pt():
+    # 7-point Laplacian tensor I3: interior theta = 108 / (108 + 6*3) = 6/7
+    n = 6
+    ptr, col, val = laplace3_blocks(n)
+    A, S = _solver(ptr, col, val, coarse_enough=64, hier_f32=0, vec_f32=0)
+    M = S.level_M(0)
+    i = 2 + n * (2 + n * 2)
+    assert np.allclose(M[i], (6.0 / 7.0) * np.eye(3) / 6.0, rtol=1e-15)
+    c = 0  # corner: 3 neighbours -> 108 / (108 + 9)
+    assert np.allclose(M[c], (108.0 / 117.0) * np.eye(3) / 6.0, rtol=1e-15)
+
+
+def test_spai0_scalar_minimiser(rng):
+    # b = 1: m_i = a_ii / sum_j a_ij^2 minimises ||I - M A||_F over diagonal M
+    n = 80
+    ptr, col, val = random_bsr(rng, n, 1, density=0.1, symmetric_pattern=True, dom=3)
+    A, S = _solver(ptr, col, val, coarse_enough=20, hier_f32=0, vec_f32=0)
+    m = S.level_M(0).reshape(-1)
+    Ad = A.dense()
+    best = np.linalg.norm(np.eye(n) - np.diag(m) @ Ad)
+    for _ in range(100):
+        D = m * (1 + 0.05 * rng.standard_normal(n))
+        assert best <= np.linalg.norm(np.eye(n) - np.diag(D) @ Ad) + 1e-12
+
+
+def test_jacobi_smoother_closed_form():
+    n = 6
+    ptr, col, val = laplace3_blocks(n)
+    A, S = _solver(ptr, col, val, coarse_enough=64, smoother=oracle.JACOBI, jacobi_omega=2.0 / 3.0,
+                   hier_f32=0, vec_f32=0)
+    assert np.allclose(S.level_M(0), (2.0 / 3.0) * np.eye(3) / 6.0, rtol=1e-15)
+
+
+# ---------------------------------------------------------------- C9 V-cycle
+def test_vcycle_linear_and_symmetric(rng):
+    ptr, col, val = gen.matrix(gen.POISSON3, 8)
+    A, S = _solver(ptr, col, val, coarse_enough=100, hier_f32=0, vec_f32=0)
+    assert S.levels >= 2
+    N = 512 * 3
+    u, w = rng.standard_normal(N), rng.standard_normal(N)
+    Vu, Vw = S.vcycle(u), S.vcycle(w)
+    assert np.allclose(S.vcycle(2.5 * u), 2.5 * Vu, rtol=0, atol=1e-12 * np.abs(Vu).max())
+    assert abs(Vu @ w - u @ Vw) <= 1e-13 * abs(Vu @ w)  # symmetric on SPD (probe 2e-16)
+
+
+def test_vcycle_single_level_is_exact(rng):
+    ptr, col, val = gen.matrix(gen.POISSON3, 6)
+    A, S = _solver(ptr, col, val, hier_f32=0, vec_f32=0)  # 648 unknowns <= 3000
+    assert S.levels == 1
+    f = rng.standard_normal(648)
+    x = S.vcycle(f)
+    assert np.allclose(x, np.linalg.solve(A.dense(), f), rtol=0, atol=1e-10)
+
+
+def test_vcycle_two_level_dense_replay(rng):
+    ptr, col, val = random_bsr(rng, 60, 2, density=0.06, symmetric_pattern=True, dom=5)
+    A, S = _solver(ptr, col, val, coarse_enough=100, hier_f32=0, vec_f32=0)
+    assert S.levels == 2
+    Ad = A.dense()
+    P, R, Ac = S.level_mat(0, 1).dense(), S.level_mat(0, 2).dense(), S.level_mat(1, 0).dense()
+    M = S.level_M(0)
+    Md = np.zeros_like(Ad)
+    for i in range(60):
+        Md[2 * i:2 * i + 2, 2 * i:2 * i + 2] = M[i]
+    f = rng.standard_normal(120)
+    x = Md @ f
+    r = f - Ad @ x
+    xc = np.linalg.solve(Ac, R @ r)
+    x = x + P @ xc
+    x = x + Md @ (f - Ad @ x)
+    assert np.allclose(S.vcycle(f), x, rtol=0, atol=1e-11 * np.abs(x).max())
+
+
+# ---------------------------------------------------------------- C10 Schur
+def test_schur_eq10_hand_value():
+    g = golden("schur_eq10_hand.json")
+    blk = np.array(g["block"])[None]
+    A = oracle.Mat.from_arrays(np.array([0, 1], np.int32), np.array([0], np.int32), blk)
+    S = oracle.Solver(A, precond=oracle.PC_SCHUR, schur_p_component=g["p_component"], hier_f32=0, vec_f32=0)
+    d, m = S.schur_vectors()
+    assert d[0] == g["Shat"]
+    assert m[0] == 1.0 / g["Shat"]  # SPAI0 of a 1x1 matrix is its inverse
+
+
+def test_schur_shat_interior_closed_form():
+    # Stokes generator: Shat_ii = -6 - (#neighbours) (1/(2h))^2 / (6/h^2) = -6 - k/24
+    n = 6
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, precond=oracle.PC_SCHUR, hier_f32=0, vec_f32=0)
+    d, m = S.schur_vectors()
+    k = np.diff(ptr) - 1
+    assert np.allclose(d, -6.0 - k / 24.0, rtol=1e-15)
+    i = 2 + n * (2 + n * 2)
+    assert d[i] == -6.25
+
+
+def test_schur_block_lu_identity(rng):
+    # exact U-solve (single level): z = apply(r) satisfies (A z)_u = r_u and
+    # (A z)_p - r_p = (S m_S - I)(r_p - B A_u^-1 r_u), S = C - B A_u^-1 B^T (Eq. 9)
+    n = 3
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, precond=oracle.PC_SCHUR, hier_f32=0, vec_f32=0)
+    Ad = A.dense()
+    vel = np.array([q for q in range(4 * n ** 3) if q % 4 != 3])
+    pre = np.array([q for q in range(4 * n ** 3) if q % 4 == 3])
+    Au, Bt, B, C = Ad[np.ix_(vel, vel)], Ad[np.ix_(vel, pre)], Ad[np.ix_(pre, vel)], Ad[np.ix_(pre, pre)]
+    _, mS = S.schur_vectors()
+    Sx = C - B @ np.linalg.solve(Au, Bt)
+    for _ in range(3):
+        r = rng.standard_normal(4 * n ** 3)
+        z = S.precond(r)
+        Az = Ad @ z
+        assert np.allclose(Az[vel], r[vel], atol=1e-10 * np.abs(r).max())
+        expect = (Sx @ np.diag(mS) - np.eye(len(pre))) @ (r[pre] - B @ np.linalg.solve(Au, r[vel]))
+        assert np.allclose(Az[pre] - r[pre], expect, atol=1e-10 * np.abs(r).max())
+
+
+def test_schur_decoupled_exact_one_iteration(rng):
+    # B = 0, C diagonal: Shat = C, m_S = C^-1 exactly, single-level U-solve is exact ->
+    # the preconditioner is A^-1 and GMRES converges in 1 iteration (SURVEY.md C10 pin).
+    n = 3
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    val = val.copy()
+    for i in range(n ** 3):
+        for k in range(ptr[i], ptr[i + 1]):
+            val[k][3, :3] = 0
+            val[k][:3, 3] = 0
+            val[k][3, 3] = -6.0 - 0.1 * i if col[k] == i else 0.0
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, precond=oracle.PC_SCHUR, solver=oracle.GMRES, hier_f32=0, vec_f32=0)
+    res = S.solve(rng.standard_normal(4 * n ** 3), rtol=1e-10)
+    assert res.converged and res.iters == 1
+
+
+# ---------------------------------------------------------------- C11 Krylov
+@pytest.mark.parametrize("solver", [oracle.CG, oracle.BICGSTAB, oracle.GMRES])
+def test_identity_one_iteration(rng, solver):
+    n = 50
+    A = oracle.Mat.from_arrays(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                               np.tile(np.eye(2), (n, 1, 1)))
+    S = oracle.Solver(A, solver=solver, precond=oracle.PC_NONE)
+    b = rng.standard_normal(2 * n)
+    r = S.solve(b, rtol=1e-10)
+    assert r.converged and r.iters == 1 and np.allclose(r.x, b)
+
+
+def test_zero_rhs(rng):
+    ptr, col, val = gen.matrix(gen.POISSON3, 4)
+    A, S = _solver(ptr, col, val, solver=oracle.CG)
+    r = S.solve(np.zeros(192), x0=rng.standard_normal(192))
+    assert r.converged and r.iters == 0 and r.relres_true == 0 and not r.x.any()
+
+
+@pytest.mark.parametrize("solver,kind", [(oracle.CG, gen.POISSON3), (oracle.BICGSTAB, gen.STOKES),
+                                         (oracle.GMRES, gen.STOKES)])
+def test_dense_solve_small(rng, solver, kind):
+    # <= 2000 unknowns, coarse_enough lowered so that a real hierarchy is exercised (C7 caveat)
+    n = 7 if kind == gen.POISSON3 else 6
+    ptr, col, val = gen.matrix(kind, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    pc = oracle.PC_SCHUR if solver == oracle.GMRES else oracle.PC_AMG
+    S = oracle.Solver(A, solver=solver, precond=pc, coarse_enough=64)
+    assert S.levels >= 2
+    b = rng.standard_normal(len(ptr) * 0 + (len(ptr) - 1) * val.shape[-1])
+    r = S.solve(b, rtol=1e-10)
+    xd = np.linalg.solve(A.dense(), b)
+    assert r.converged and r.relres_true <= 1e-10
+    assert np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
+def test_gmres_finite_termination(rng):
+    n = 20
+    ptr, col, val = random_bsr(rng, n, 1, density=1.0, dom=10)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=n, precond=oracle.PC_NONE)
+    r = S.solve(rng.standard_normal(n), rtol=1e-12)
+    assert r.converged and r.iters <= n
+
+
+def test_gmres_true_residual_monotone(rng):
+    ptr, col, val = gen.matrix(gen.STOKES, 8)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, solver=oracle.GMRES, precond=oracle.PC_SCHUR, gmres_m=10, coarse_enough=100)
+    r = S.solve(gen.rhs(gen.RHS_LID_NOISE, 8, 4), rtol=1e-8, history=True)
+    h = r.history
+    assert r.converged and r.iters > 10  # crosses a restart
+    assert np.all(np.diff(h) <= 1e-12 * h[:-1] + 1e-15)
+    assert h[-1] <= 1e-8
+
+
+@pytest.mark.parametrize("kind,solver,pc,rhs", [
+    (gen.POISSON3, oracle.CG, oracle.PC_AMG, gen.RHS_UNIFORM),
+    (gen.STOKES, oracle.BICGSTAB, oracle.PC_AMG, gen.RHS_LID),
+    (gen.STOKES, oracle.GMRES, oracle.PC_SCHUR, gen.RHS_FORCE_NOISE),
+])
+def test_fp32_hierarchy_iteration_parity(kind, solver, pc, rhs):
+    # mixed precision "does not increase the number of iterations"
+    n = 12
+    ptr, col, val = gen.matrix(kind, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    b = gen.rhs(rhs, n, val.shape[-1])
+    its = []
+    for h32 in (0, 1):
+        S = oracle.Solver(A, solver=solver, precond=pc, hier_f32=h32, vec_f32=h32, coarse_enough=200)
+        r = S.solve(b, rtol=1e-8)
+        assert r.converged and r.relres_true <= 1e-8
+        its.append(r.iters)
+    assert abs(its[0] - its[1]) <= 1
+
+
+# ---------------------------------------------------------------- C12 multi-rank
+def test_multirank_aggregates_are_slab_local():
+    n = 8
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    for P in (2, 4):
+        agg, nc = oracle.aggregate(A, nparts=P)
+        rows = n ** 3 // P
+        for r in range(P):
+            a = agg[r * rows:(r + 1) * rows]
+            others = np.concatenate([agg[:r * rows], agg[(r + 1) * rows:]])
+            assert not (set(a.tolist()) & set(others.tolist()))
+        S = oracle.Solver(A, solver=oracle.GMRES, precond=oracle.PC_SCHUR, nparts=P, coarse_enough=100)
+        res = S.solve(gen.rhs(gen.RHS_LID_NOISE, n, 4), rtol=1e-8)
+        assert res.converged and res.relres_true <= 1e-8
+    a1, n1 = oracle.aggregate(A, nparts=1)
+    a0, n0 = oracle.aggregate(A)
+    assert np.array_equal(a1, a0)
