@@ -1,0 +1,159 @@
+/* amg.h -- C ABI of the B200-native solve phase of the AMG-preconditioned Krylov
+ * solver for Stokes saddle-point systems of Demidov, Mu & Wang, "Accelerating
+ * linear solvers for Stokes problems with C++ metaprogramming" (arXiv 2006.06052).
+ *
+ * Problem (Listing 3 "Solver S(A, prm)" then apply):
+ * given a square sparse block matrix A (BSR), a right-hand side
+ * b, an initial guess x0 and a tolerance, return x with ||b - A x||_2 / ||b||_2 <= rtol.
+ *
+ * Conventions for every entry point
+ *  - Pointers are DEVICE pointers unless the comment says "host".
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered on it
+ *    (NULL = legacy default stream).  amg_setup / amg_solve synchronise `stream`
+ *    before returning (setup reads aggregation flags, solve reads one convergence
+ *    scalar per iteration); bsr_spmv never synchronises.
+ *  - Every call returns an int status (AMG_OK = 0, AMG_NOT_CONVERGED = 1, negative
+ *    codes are errors, see amg_status_string()).  On error nothing the caller owns
+ *    is freed; a handle stays valid if it was valid before the call.
+ *  - No call throws, no call prints; CUDA/NCCL failures map to AMG_ECUDA / AMG_ENCCL.
+ *  - Indices are int32 (nnzb < 2^31), value offsets are 64-bit internally.
+ */
+#ifndef AMG_B200_H
+#define AMG_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+enum {
+  AMG_OK = 0,
+  AMG_NOT_CONVERGED = 1,       /* x holds the last iterate, report filled */
+  AMG_EINVAL = -1,             /* bad argument / unsupported option / coarsening stalled */
+  AMG_EDIM = -2,               /* dimension mismatch */
+  AMG_EZERODIAG = -3,          /* missing or zero diagonal block */
+  AMG_ESINGULAR_BLOCK = -4,    /* a diagonal block is singular */
+  AMG_EINDEX_OVERFLOW = -5,    /* nnzb >= 2^31 or n*b overflows int32 */
+  AMG_EBREAKDOWN = -6,         /* Krylov breakdown after one restart */
+  AMG_ECUDA = -7,
+  AMG_ENCCL = -8,
+  AMG_ENOMEM = -9
+};
+
+typedef enum { AMG_F64 = 0, AMG_F32 = 1 } amg_dtype;
+enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2 };
+enum { AMG_PC_AMG = 0, AMG_PC_SCHUR = 1, AMG_PC_NONE = 2 };
+enum { AMG_SPAI0 = 0, AMG_JACOBI = 1 };
+
+/* Block-CSR descriptor (PAPER.md:666-672 layout).  Caller-owned; the library never
+ * frees or retains it beyond the call (amg_setup deep-copies). */
+typedef struct {
+  int32_t n_block_rows;   /* rows of this descriptor (local rows when distributed) */
+  int32_t n_block_cols;   /* block columns (global) */
+  int32_t block_size;     /* b in {1,2,3,4}; the hot path uses 3 and 4 */
+  int32_t _pad;
+  int64_t nnzb;           /* number of stored blocks, < 2^31 */
+  const int32_t* row_ptr; /* [n_block_rows+1], row_ptr[0] = 0, non-decreasing, row_ptr[n] = nnzb */
+  const int32_t* col_idx; /* [nnzb], 0-based, strictly increasing within a row; the diagonal
+                             block must be present for amg_setup */
+  const void* values;     /* [nnzb*b*b] row-major b x b blocks, type `dtype` */
+  int32_t dtype;          /* amg_dtype */
+  int32_t _pad2;
+} amg_bsr;
+
+/* Runtime parameters: a flat version of the paper's nested params structs
+ * (Listings 2-3).  Fill with amg_params_default(). */
+typedef struct {
+  int32_t solver;            /* AMG_CG | AMG_BICGSTAB | AMG_GMRES (flexible GMRES(m)) */
+  int32_t gmres_m;           /* restart length, default 30 (PAPER.md:255 shows M = 50) */
+  int32_t precond;           /* AMG_PC_AMG (monolithic SA-AMG) | AMG_PC_SCHUR (Eq. 9-10) | AMG_PC_NONE */
+  int32_t maxiter;           /* default 1000 */
+  int32_t hier_dtype;        /* values of A_l, P_l, R_l, M_l, coarse inverse, B, B^T, m_S:
+                                AMG_F32 (default, Listing V4) | AMG_F64 */
+  int32_t vcycle_vec_dtype;  /* vectors inside the preconditioner: AMG_F32 (default) | AMG_F64 */
+  int32_t smoother;          /* AMG_SPAI0 (default) | AMG_JACOBI */
+  int32_t coarse_enough;     /* max scalar unknowns of the coarsest level, default 3000 */
+  double jacobi_omega;       /* damped-Jacobi weight, default 2/3 */
+  double sa_omega;           /* prolongator damping, default 2/3 (reading R5) */
+  double eps_strong;         /* strong-connection threshold, default 1e-3 */
+  int32_t max_levels;        /* default 20 */
+  int32_t npre, npost;       /* smoothing sweeps, default 1, 1 */
+  int32_t schur_p_component; /* pressure component inside a block, default 3 for (u,v,w,p) */
+  int32_t use_graphs;        /* 1 (default): replay the preconditioner as a CUDA graph */
+  int32_t _pad;
+} amg_params;
+
+typedef struct {
+  int32_t iters;        /* Krylov iterations (GMRES: Arnoldi steps; BiCGStab: full steps) */
+  int32_t converged;    /* 1 iff relres_true <= rtol */
+  int32_t levels;       /* AMG levels including the coarsest */
+  int32_t restarts;     /* GMRES cycles - 1, or BiCGStab/CG restarts */
+  double relres_true;   /* ||b - A x|| / ||b|| recomputed at exit */
+  double setup_s;       /* wall seconds of amg_setup (device-synchronised) */
+  double solve_s;       /* seconds of this solve: CUDA events on `stream` (max over ranks) */
+  double alg_bytes;     /* algorithmic bytes the solve moved */
+} amg_report;
+
+struct amg_handle;
+struct amg_comm;
+
+int amg_params_default(amg_params* p /* host */);
+const char* amg_status_string(int status);
+
+/* Build the solver for A (device descriptor): Schur split + Eq. 10 (if precond =
+ * SCHUR), the smoothed-aggregation hierarchy on the GPU, the coarse inverse, the
+ * narrowed (fp32) copies and the solve workspace.  A may be freed afterwards. */
+int amg_setup(const amg_bsr* A /* host struct, device arrays */, const amg_params* p /* host */,
+              void* stream, struct amg_handle** out /* host */);
+
+/* Solve A x = b.  b, x: device fp64 [n_block_rows*b]; x is read as x0 and overwritten.
+ * Allocates nothing.  ||b|| = 0 returns x = 0, converged, relres 0. */
+int amg_solve(struct amg_handle* h, const double* b, double* x, double rtol, void* stream,
+              amg_report* rep /* host, may be NULL */);
+
+/* Same as amg_solve with HOST b and x (pageable or pinned); the host<->device copies
+ * are part of the call (the bench's end-to-end number). */
+int amg_solve_host(struct amg_handle* h, const double* b_host, double* x_host, double rtol,
+                   void* stream, amg_report* rep);
+
+/* One application of the preconditioner (z = M r) on outer fp64 device vectors. */
+int amg_apply_precond(struct amg_handle* h, const double* r, double* z, void* stream);
+
+/* y = alpha A x + beta y with fp64 accumulation (C1); beta == 0 overwrites y (NaN
+ * included).  x, y: device vectors of type xt / yt. */
+int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double beta, void* y,
+             int32_t yt, void* stream);
+
+void amg_destroy(struct amg_handle* h);
+
+/* ---- introspection (used by the parity tests; all outputs HOST) ---- */
+/* out[5] = {n_block_rows, block_size, nnzb(A_l), nnzb(P_l) or 0, n_coarse or 0} */
+int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);
+/* which: 0 = A_l, 1 = P_l, 2 = R_l (fp64 setup values); 3 = smoother blocks M_l
+ * (ptr/col ignored, val = n*b*b).  Arrays sized from amg_level_info. */
+int amg_level_export(struct amg_handle* h, int32_t level, int32_t which, int32_t* ptr, int32_t* col,
+                     double* val);
+int amg_level_aggregates(struct amg_handle* h, int32_t level, int32_t* agg);
+/* Schur vectors: Shat diagonal and m_S (n_block_rows each), fp64 setup values */
+int amg_schur_export(struct amg_handle* h, double* shat_diag, double* m_s);
+/* One V-cycle of the hierarchy on fp64 device vectors of the level-0 size. */
+int amg_vcycle(struct amg_handle* h, const double* f, double* x, void* stream);
+/* device bytes held by the handle (hierarchy + workspace) */
+int64_t amg_device_bytes(struct amg_handle* h);
+
+/* ---- multi-GPU: one process per GPU, contiguous block-row slabs ---- */
+/* NCCL unique id (128 bytes, host) generated by rank 0 (amg_comm_unique_id) and
+ * broadcast by the caller (torch.distributed). */
+int amg_comm_unique_id(void* id128 /* host, 128 B */);
+int amg_comm_init(const void* id128 /* host */, int32_t nranks, int32_t rank,
+                  struct amg_comm** out);
+/* A_local: this rank's rows [row_begin, row_begin + n_block_rows) with GLOBAL column
+ * ids.  After this call amg_solve takes the LOCAL slices of b and x. */
+int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_block_rows,
+                   struct amg_comm* c, const amg_params* p, void* stream, struct amg_handle** out);
+void amg_comm_destroy(struct amg_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -633,7 +633,7 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
     A = std::move(Ac);
     s.lv.push_back(std::move(L));
   }
-  if ((int64_t)A.n * A.b > 16384) return ORC_EINVAL;  // coarsening stalled: dense solve too large
+  if ((int64_t)A.n * A.b > 8192) return ORC_EINVAL;  // coarsening stalled: dense solve too large
   s.Acoarse = A;
   int rc = coarse_factor(A, s.coarse);
   if (rc != ORC_OK) return rc;

@@ -1,0 +1,29 @@
+// blas1.h -- K12 vector kernels (fp64 outer vectors), all stream-ordered.
+#pragma once
+
+#include "common.cuh"
+
+namespace amgb {
+
+constexpr int kMaxPartials = 148 * 8;
+
+struct PtrList {
+  const double* p[32];
+};
+
+// out[0] = a . b (or its sqrt); partials: scratch of kMaxPartials doubles
+void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double* partials, double* out,
+                bool sqrt_out, cudaStream_t s);
+// out[j] = V_j . w, j < k <= 32; partials: scratch of 32 * kMaxPartials doubles
+void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* partials, double* out, cudaStream_t s);
+// w -= sum_j coef[j] V_j  (coef: device)
+void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s);
+// x += sum_j y[j] Z_j  (Z of dtype zt, y: device)
+void launch_zupdate(int64_t n, int k, const PtrList& Z, int zt, const double* y, double* x, cudaStream_t s);
+void launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s);
+void launch_axpbypcz(int64_t n, double a, const double* x, double b, const double* y, double c, double* z,
+                     cudaStream_t s);
+// y = x / sdev[0]
+void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s);
+
+}  // namespace amgb

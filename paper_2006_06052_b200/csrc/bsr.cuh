@@ -1,0 +1,266 @@
+// bsr.cuh -- block-row machinery of every SpMV-type kernel (K1, K2, K4-K7, K10, K11).
+//
+// Layout: int32 row_ptr[n+1], int32 col[nnzb] sorted, values
+// [nnzb][b][b] row-major.  A group of G lanes (G = 8 or 32, a power of two) owns
+// one block row.  The row's work is enumerated as items t = (block k, block row r)
+// in storage order, so the G lanes of a group read G consecutive b-value segments
+// of the value stream: every warp load is contiguous (coalesced) and whole
+// sectors are used.  Each lane multiplies its b values with the b entries of x
+// at the block's column (the b lanes of one block hit the same x segment: one
+// L1 broadcast), accumulating in fp64.  A butterfly inside the group produces the
+// b-vector (A x)_I, which the kernel's epilogue consumes.  All arithmetic is fp64
+// with one rounding on store.
+#pragma once
+
+#include "common.cuh"
+
+namespace amgb {
+
+// ---- b contiguous elements -> fp64 registers (128-bit loads where alignment allows) ----
+template <int B, bool STREAM, typename T>
+__device__ __forceinline__ void load_b(const T* __restrict__ p, double (&v)[B]) {
+  if constexpr (B == 4 && std::is_same_v<T, float>) {
+    float4 q = STREAM ? __ldcs(reinterpret_cast<const float4*>(p)) : __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else if constexpr (B == 4 && std::is_same_v<T, double>) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = STREAM ? __ldcs(q) : __ldg(q);
+    double2 c = STREAM ? __ldcs(q + 1) : __ldg(q + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+  } else if constexpr (B == 2 && std::is_same_v<T, float>) {
+    float2 q = STREAM ? __ldcs(reinterpret_cast<const float2*>(p)) : __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else if constexpr (B == 2 && std::is_same_v<T, double>) {
+    double2 q = STREAM ? __ldcs(reinterpret_cast<const double2*>(p)) : __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < B; ++c) v[c] = (double)(STREAM ? __ldcs(p + c) : __ldg(p + c));
+  }
+}
+
+// b contiguous elements in their storage type (keeps fp32 values at 1 register each)
+template <int B, bool STREAM, typename T>
+__device__ __forceinline__ void load_raw(const T* __restrict__ p, T (&v)[B]) {
+  if constexpr (B == 4 && std::is_same_v<T, float>) {
+    float4 q = STREAM ? __ldcs(reinterpret_cast<const float4*>(p)) : __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else if constexpr (B == 4 && std::is_same_v<T, double>) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = STREAM ? __ldcs(q) : __ldg(q);
+    double2 c = STREAM ? __ldcs(q + 1) : __ldg(q + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+  } else if constexpr (B == 2 && std::is_same_v<T, float>) {
+    float2 q = STREAM ? __ldcs(reinterpret_cast<const float2*>(p)) : __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else if constexpr (B == 2 && std::is_same_v<T, double>) {
+    double2 q = STREAM ? __ldcs(reinterpret_cast<const double2*>(p)) : __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < B; ++c) v[c] = STREAM ? __ldcs(p + c) : __ldg(p + c);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T to_out(double v) {
+  return (T)v;  // fp32: round-to-nearest-even, once
+}
+
+// Partial (A x) of block row `row` for lane gl of its group.  The row is walked in
+// chunks of G blocks: one coalesced load brings the chunk's G column indices into
+// the group's registers; the chunk's G*B items are then handled B per lane
+// (item t = gl + i*G, block t / B, block row t % B), with all B value loads and B
+// x loads of a lane issued before any FMA (no col -> x dependency inside the
+// chunk, B independent 16/32-byte loads in flight per lane).  If G % B == 0 the
+// lane always handles block row r = gl % B and accumulates into acc[0]; otherwise
+// acc[r] is used.
+template <int B, int G, typename V, typename X>
+__device__ __forceinline__ void row_partial(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                            const V* __restrict__ val, const X* __restrict__ x, int row,
+                                            int gl, double (&acc)[B]) {
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  // lanes of this group only: other groups of the warp may run a different number of chunks
+  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  for (int kc = k0; kc < k1; kc += G) {
+    const int nbk = min(G, k1 - kc);
+    const int mycol = (gl < nbk) ? __ldg(col + kc + gl) : 0;
+    V a[B][B];
+    X xv[B][B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int t = gl + i * G;
+      const int kb = t / B;
+      const int c = __shfl_sync(gmask, mycol, kb & (G - 1), G);
+      if (kb < nbk) {
+        const int r = t % B;
+        load_raw<B, true>(val + ((int64_t)(kc + kb) * B + r) * B, a[i]);
+        load_raw<B, false>(x + (int64_t)c * B, xv[i]);
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < B; ++cc) a[i][cc] = V(0), xv[i][cc] = X(0);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double s = (double)a[i][0] * (double)xv[i][0];
+#pragma unroll
+      for (int cc = 1; cc < B; ++cc) s = fma((double)a[i][cc], (double)xv[i][cc], s);
+      if constexpr (G % B == 0) {
+        acc[0] += s;
+      } else {
+        const int r = (gl + i * G) % B;
+#pragma unroll
+        for (int rr = 0; rr < B; ++rr)
+          if (rr == r) acc[rr] += s;
+      }
+    }
+  }
+}
+
+// Simple variant: one item per lane per iteration, col loaded per item.
+template <int B, int G, typename V, typename X>
+__device__ __forceinline__ void row_partial_simple(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                                   const V* __restrict__ val, const X* __restrict__ x, int row,
+                                                   int gl, double (&acc)[B]) {
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  const int nitems = (k1 - k0) * B;
+#pragma unroll 2
+  for (int t = gl; t < nitems; t += G) {
+    const int kb = k0 + t / B;
+    const int r = (G % B == 0) ? (gl % B) : (t % B);
+    const int c = __ldg(col + kb);
+    V a[B];
+    X xv[B];
+    load_raw<B, true>(val + ((int64_t)kb * B + r) * B, a);
+    load_raw<B, false>(x + (int64_t)c * B, xv);
+    double s = (double)a[0] * (double)xv[0];
+#pragma unroll
+    for (int cc = 1; cc < B; ++cc) s = fma((double)a[cc], (double)xv[cc], s);
+    if constexpr (G % B == 0) {
+      acc[0] += s;
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < B; ++rr)
+        if (rr == r) acc[rr] += s;
+    }
+  }
+}
+
+// Group reduction: every lane of the group receives the full b-vector y = (A x)_row.
+template <int B, int G>
+__device__ __forceinline__ void group_reduce(double (&acc)[B], double (&y)[B]) {
+  if constexpr (G % B == 0) {
+    double v = acc[0];
+#pragma unroll
+    for (int off = G / 2; off >= B; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
+#pragma unroll
+    for (int c = 0; c < B; ++c) y[c] = __shfl_sync(kFull, v, c, G);
+  } else {
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      double v = acc[c];
+#pragma unroll
+      for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
+      y[c] = v;
+    }
+  }
+}
+
+template <int B>
+__device__ __forceinline__ double pick(const double (&y)[B], int i) {
+  double v = y[0];
+#pragma unroll
+  for (int c = 1; c < B; ++c)
+    if (c == i) v = y[c];
+  return v;
+}
+
+// ---- K1: y = alpha A x + beta y (beta == 0 overwrites) ----
+template <int B, int G, typename V, typename X, typename Y, int VARIANT>
+__global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__ ptr,
+                                              const int32_t* __restrict__ col, const V* __restrict__ val,
+                                              double alpha, const X* __restrict__ x, double beta,
+                                              Y* __restrict__ y) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
+  const bool valid = row < n;
+  double acc[B] = {};
+  if (valid) {
+    if constexpr (VARIANT == 1) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
+    else row_partial_simple<B, G>(ptr, col, val, x, row, gl, acc);
+  }
+  double yv[B];
+  group_reduce<B, G>(acc, yv);
+  if (valid && gl < B) {
+    const int64_t o = (int64_t)row * B + gl;
+    double v = alpha * pick<B>(yv, gl);
+    if (beta != 0.0) v = fma(beta, (double)y[o], v);
+    y[o] = to_out<Y>(v);
+  }
+}
+
+// ---- K2: r = f - A x ----
+template <int B, int G, typename V, typename X>
+__global__ void __launch_bounds__(256) k_residual(int n, const int32_t* __restrict__ ptr,
+                                                  const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                  const X* __restrict__ f, const X* __restrict__ x,
+                                                  X* __restrict__ r) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
+  const bool valid = row < n;
+  double acc[B] = {};
+  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
+  double yv[B];
+  group_reduce<B, G>(acc, yv);
+  if (valid && gl < B) {
+    const int64_t o = (int64_t)row * B + gl;
+    r[o] = to_out<X>((double)f[o] - pick<B>(yv, gl));
+  }
+}
+
+// ---- K5: post-smooth xo = x + M (f - A x), every row from the old x (Jacobi-type) ----
+template <int B, int G, typename V, typename X>
+__global__ void __launch_bounds__(256) k_smooth(int n, const int32_t* __restrict__ ptr,
+                                                const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                const V* __restrict__ M, const X* __restrict__ f,
+                                                const X* __restrict__ x, X* __restrict__ xo) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
+  const bool valid = row < n;
+  double acc[B] = {};
+  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
+  double yv[B];
+  group_reduce<B, G>(acc, yv);
+  if (valid && gl < B) {
+    const int64_t o = (int64_t)row * B;
+    double res[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) res[c] = (double)f[o + c] - yv[c];
+    double m[B];
+    load_b<B, false>(M + ((int64_t)row * B + gl) * B, m);
+    double t = m[0] * res[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) t = fma(m[c], res[c], t);
+    xo[o + gl] = to_out<X>((double)x[o + gl] + t);
+  }
+}
+
+// ---- K4 (first half): x = M f (pre-smoothing from a zero initial guess) ----
+template <int B, typename V, typename X>
+__global__ void __launch_bounds__(256) k_apply_M(int n, const V* __restrict__ M, const X* __restrict__ f,
+                                                 X* __restrict__ x) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * B) return;
+  const int64_t row = t / B;
+  const int r = (int)(t % B);
+  double m[B], fv[B];
+  load_b<B, false>(M + (row * B + r) * B, m);
+  load_b<B, false>(f + row * B, fv);
+  double s = m[0] * fv[0];
+#pragma unroll
+  for (int c = 1; c < B; ++c) s = fma(m[c], fv[c], s);
+  x[t] = to_out<X>(s);
+}
+
+}  // namespace amgb

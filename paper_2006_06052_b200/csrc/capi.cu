@@ -1,0 +1,117 @@
+// capi.cu -- the C ABI (include/amg.h): argument validation, error mapping, and the
+// entry points that need no hierarchy (bsr_spmv, params, status strings).
+#include <cstring>
+
+#include "amg.h"
+#include "common.cuh"
+#include "ops.h"
+
+using namespace amgb;
+
+namespace amgb {
+void set_last_error(const std::string& s);
+
+int validate_bsr(const amg_bsr* A, bool square) {
+  if (!A) return AMG_EINVAL;
+  if (A->block_size < 1 || A->block_size > 4) return AMG_EINVAL;
+  if (A->n_block_rows < 0 || A->n_block_cols < 0 || A->nnzb < 0) return AMG_EINVAL;
+  if (A->nnzb >= (int64_t(1) << 31)) return AMG_EINDEX_OVERFLOW;
+  if ((int64_t)A->n_block_rows * A->block_size >= (int64_t(1) << 31)) return AMG_EINDEX_OVERFLOW;
+  if (A->dtype != AMG_F32 && A->dtype != AMG_F64) return AMG_EINVAL;
+  if (A->n_block_rows > 0 && (!A->row_ptr || (A->nnzb > 0 && (!A->col_idx || !A->values))))
+    return AMG_EINVAL;
+  if (square && A->n_block_rows != A->n_block_cols) return AMG_EDIM;
+  return AMG_OK;
+}
+
+Mat view_of(const amg_bsr* A) {
+  Mat M;
+  M.n = A->n_block_rows;
+  M.m = A->n_block_cols;
+  M.b = A->block_size;
+  M.nnz = A->nnzb;
+  M.ptr = const_cast<int32_t*>(A->row_ptr);
+  M.col = const_cast<int32_t*>(A->col_idx);
+  M.val = const_cast<void*>(A->values);
+  M.vt = A->dtype;
+  M.G = choose_group(M.nnz, M.n, M.b);
+  return M;
+}
+
+}  // namespace amgb
+
+#define AMG_GUARD_BEGIN try {
+#define AMG_GUARD_END                      \
+  }                                        \
+  catch (const ::amgb::Error& e) {         \
+    ::amgb::set_last_error(e.what);        \
+    return e.code;                         \
+  }                                        \
+  catch (const std::bad_alloc&) {          \
+    return AMG_ENOMEM;                     \
+  }                                        \
+  catch (...) {                            \
+    return AMG_EINVAL;                     \
+  }
+
+namespace amgb {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& s) { g_last_error = s; }
+}  // namespace amgb
+
+extern "C" {
+
+const char* amg_last_error(void) { return amgb::g_last_error.c_str(); }
+
+int amg_params_default(amg_params* p) {
+  if (!p) return AMG_EINVAL;
+  std::memset(p, 0, sizeof(*p));
+  p->solver = AMG_GMRES;
+  p->gmres_m = 30;
+  p->precond = AMG_PC_AMG;
+  p->maxiter = 1000;
+  p->hier_dtype = AMG_F32;
+  p->vcycle_vec_dtype = AMG_F32;
+  p->smoother = AMG_SPAI0;
+  p->coarse_enough = 3000;
+  p->jacobi_omega = 2.0 / 3.0;
+  p->sa_omega = 2.0 / 3.0;
+  p->eps_strong = 1e-3;
+  p->max_levels = 20;
+  p->npre = 1;
+  p->npost = 1;
+  p->schur_p_component = 3;
+  p->use_graphs = 1;
+  return AMG_OK;
+}
+
+const char* amg_status_string(int s) {
+  switch (s) {
+    case AMG_OK: return "ok";
+    case AMG_NOT_CONVERGED: return "not converged (x holds the last iterate)";
+    case AMG_EINVAL: return "invalid argument";
+    case AMG_EDIM: return "dimension mismatch";
+    case AMG_EZERODIAG: return "missing or zero diagonal block";
+    case AMG_ESINGULAR_BLOCK: return "singular diagonal block";
+    case AMG_EINDEX_OVERFLOW: return "index overflow (nnzb or n*b >= 2^31)";
+    case AMG_EBREAKDOWN: return "Krylov breakdown after one restart";
+    case AMG_ECUDA: return "CUDA error";
+    case AMG_ENCCL: return "NCCL error";
+    case AMG_ENOMEM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double beta, void* y, int32_t yt,
+             void* stream) {
+  AMG_GUARD_BEGIN
+  int rc = validate_bsr(A, false);
+  if (rc != AMG_OK) return rc;
+  if ((xt != AMG_F32 && xt != AMG_F64) || (yt != AMG_F32 && yt != AMG_F64)) return AMG_EINVAL;
+  if (A->n_block_rows > 0 && (!x || !y)) return AMG_EINVAL;
+  launch_spmv(view_of(A), alpha, x, xt, beta, y, yt, (cudaStream_t)stream);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// common.cuh -- shared host/device plumbing of the B200 library (no method arithmetic).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "amg.h"
+
+namespace amgb {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+// Internal error: thrown inside the library, converted to a status code at the C ABI.
+struct Error {
+  int code;
+  std::string what;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& what) { throw Error{code, what}; }
+
+#define AMG_CK(expr)                                                                       \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      ::amgb::fail(e_ == cudaErrorMemoryAllocation ? AMG_ENOMEM : AMG_ECUDA,               \
+                   std::string(#expr) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+#define AMG_CK_LAUNCH() AMG_CK(cudaGetLastError())
+
+inline size_t dtype_size(int dt) { return dt == AMG_F32 ? 4 : 8; }
+
+// Owning device allocation list: every buffer of a handle lives here and is freed
+// by the destructor.  Solve-phase code never allocates.
+class Arena {
+ public:
+  Arena() = default;
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  ~Arena() { release(); }
+  void* alloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    void* p = nullptr;
+    AMG_CK(cudaMalloc(&p, bytes));
+    ptrs_.push_back(p);
+    total_ += (int64_t)bytes;
+    return p;
+  }
+  template <class T>
+  T* alloc_n(size_t n) {
+    return static_cast<T*>(alloc(n * sizeof(T)));
+  }
+  void release() {
+    for (void* p : ptrs_) cudaFree(p);
+    ptrs_.clear();
+    total_ = 0;
+  }
+  int64_t bytes() const { return total_; }
+
+ private:
+  std::vector<void*> ptrs_;
+  int64_t total_ = 0;
+};
+
+// Device BSR matrix with square b x b blocks (PAPER.md:666-672 layout).
+struct Mat {
+  int32_t n = 0, m = 0, b = 1;
+  int64_t nnz = 0;
+  int32_t* ptr = nullptr;
+  int32_t* col = nullptr;
+  void* val = nullptr;
+  int vt = AMG_F64;
+  int G = 8;  // lanes per block row in the SpMV-type kernels (chosen from the row length)
+};
+
+// Lanes per block row: enough lanes to cover a row's (block, block-row) items in a
+// few passes; 8 for 7-point rows (21-28 items), 32 for longer (coarse / 27-point) rows.
+inline int choose_group(int64_t nnz, int32_t n, int b) {
+  if (n <= 0) return 8;
+  double items = (double)nnz * b / (double)n;
+  return items > 40.0 ? 32 : 8;
+}
+
+inline unsigned grid_for(int64_t threads, int block) {
+  int64_t g = (threads + block - 1) / block;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace amgb

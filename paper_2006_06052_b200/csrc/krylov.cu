@@ -1,0 +1,349 @@
+// krylov.cu -- outer fp64 Krylov solvers: PCG, right-
+// preconditioned BiCGStab (van der Vorst), flexible right-preconditioned GMRES(m)
+// with CGS2 Arnoldi and Givens rotations.  Same steps, scalars and stopping rules as
+// the oracle; the host reads the needed scalars once per step through pinned memory.
+#include <cmath>
+#include <vector>
+
+#include "blas1.h"
+#include "ops.h"
+#include "solver.h"
+
+namespace amgb {
+
+namespace {
+
+struct Ctx {
+  Handle& h;
+  cudaStream_t s;
+  int64_t N;
+  double bytes = 0.0;  // algorithmic bytes of the solve
+  Ctx(Handle& hh, cudaStream_t ss) : h(hh), s(ss), N((int64_t)hh.n * hh.b) {}
+
+  // host copies of device scalars [0, k)
+  void read(int k) {
+    AMG_CK(cudaMemcpyAsync(h.hscal, h.dscal, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    AMG_CK(cudaStreamSynchronize(s));
+  }
+  void dot(const double* a, const double* b, int slot, bool sq = false) {
+    launch_dot(N, a, AMG_F64, b, AMG_F64, h.partials, h.dscal + slot, sq, s);
+    bytes += (a == b ? 8.0 : 16.0) * N;
+  }
+  void spmv(const void* x, int xt, double* y) {
+    launch_spmv(h.A, 1.0, x, xt, 0.0, y, AMG_F64, s);
+    bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0);
+  }
+  void residual(const double* b, const double* x, double* r) {
+    launch_residual(h.A, b, x, r, AMG_F64, s);
+    bytes += h.alg_bytes_spmv + 8.0 * N;
+  }
+  void pc(const double* r, void* z, int zt, double scale = 1.0) {
+    precond_apply(h, r, z, zt, s, scale);
+    bytes += h.alg_bytes_precond + N * ((double)dtype_size(zt) - 8.0);
+  }
+  void axpby(double a, const double* x, double b, double* y) {
+    launch_axpby(N, a, x, b, y, s);
+    bytes += (b == 0.0 ? 16.0 : 24.0) * N;
+  }
+  void axpbypcz(double a, const double* x, double b, const double* y, double c, double* z) {
+    launch_axpbypcz(N, a, x, b, y, c, z, s);
+    bytes += 32.0 * N;
+  }
+};
+
+bool finite(double v) { return std::isfinite(v); }
+
+int finish(Ctx& c, const double* b, double* x, double* r, double nb, int status, int iters, int restarts,
+           amg_report* rep) {
+  c.residual(b, x, r);
+  c.dot(r, r, 0, true);
+  c.read(1);
+  if (rep) {
+    rep->iters = iters;
+    rep->restarts = restarts;
+    rep->relres_true = c.h.hscal[0] / nb;
+    rep->converged = status == AMG_OK;
+    rep->alg_bytes = c.bytes;
+  }
+  return status;
+}
+
+// ---- PCG (cfg 1) ----
+int solve_cg(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  double *r = h.vec[0], *z = h.vec[1], *p = h.vec[2], *q = h.vec[3];
+  c.residual(b, x, r);
+  c.dot(r, r, 0, true);
+  c.read(1);
+  int it = 0, status = AMG_NOT_CONVERGED;
+  if (h.hscal[0] <= rtol * nb) status = AMG_OK;
+  bool restart = true;
+  double rho = 0.0;
+  while (status != AMG_OK && it < h.p.maxiter) {
+    if (restart) {
+      c.pc(r, z, AMG_F64);
+      launch_convert(c.N, z, AMG_F64, p, AMG_F64, 1.0, c.s);
+      c.bytes += 16.0 * c.N;
+      c.dot(r, z, 0);
+      c.read(1);
+      rho = h.hscal[0];
+      restart = false;
+    }
+    c.spmv(p, AMG_F64, q);
+    c.dot(p, q, 0);
+    c.read(1);
+    const double pq = h.hscal[0];
+    if (pq == 0.0 || !finite(pq)) {
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    const double alpha = rho / pq;
+    c.axpby(alpha, p, 1.0, x);
+    c.axpby(-alpha, q, 1.0, r);
+    ++it;
+    c.dot(r, r, 0, true);
+    c.read(1);
+    if (h.hscal[0] <= rtol * nb) {
+      c.residual(b, x, r);
+      c.dot(r, r, 0, true);
+      c.read(1);
+      if (h.hscal[0] <= rtol * nb) {
+        status = AMG_OK;
+        break;
+      }
+      restart = true;
+      continue;
+    }
+    c.pc(r, z, AMG_F64);
+    c.dot(r, z, 0);
+    c.read(1);
+    const double rho_new = h.hscal[0];
+    const double beta = rho_new / rho;
+    c.axpby(1.0, z, beta, p);  // p = z + beta p
+    rho = rho_new;
+  }
+  return finish(c, b, x, r, nb, status, it, 0, rep);
+}
+
+// ---- BiCGStab (cfg 3) ----
+int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  double *r = h.vec[0], *rh = h.vec[1], *p = h.vec[2], *ph = h.vec[3], *v = h.vec[4], *sv = h.vec[5],
+         *sh = h.vec[6], *t = h.vec[7];
+  const int64_t N = c.N;
+  c.residual(b, x, r);
+  c.dot(r, r, 0, true);
+  c.read(1);
+  int it = 0, restarts = 0, status = AMG_NOT_CONVERGED;
+  if (h.hscal[0] <= rtol * nb) status = AMG_OK;
+  launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+  bool first = true;
+  double rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  auto do_restart = [&]() -> bool {
+    if (restarts >= 1) return false;
+    ++restarts;
+    c.residual(b, x, r);
+    launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+    first = true;
+    return true;
+  };
+  auto verify = [&]() -> bool {
+    c.residual(b, x, r);
+    c.dot(r, r, 0, true);
+    c.read(1);
+    if (h.hscal[0] <= rtol * nb) return true;
+    launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+    first = true;
+    return false;
+  };
+  while (status != AMG_OK && it < h.p.maxiter) {
+    c.dot(rh, r, 0);
+    c.read(1);
+    const double rho = h.hscal[0];
+    if (!(std::fabs(rho) > 1e-30 * nb * nb) || !finite(rho)) {
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    if (first) {
+      launch_convert(N, r, AMG_F64, p, AMG_F64, 1.0, c.s);
+      c.bytes += 16.0 * N;
+      first = false;
+    } else {
+      const double beta = (rho / rho_old) * (alpha / omega);
+      // p = r + beta (p - omega v) = r + beta p - beta omega v
+      c.axpbypcz(1.0, r, -beta * omega, v, beta, p);
+    }
+    c.pc(p, ph, AMG_F64);
+    c.spmv(ph, AMG_F64, v);
+    c.dot(rh, v, 0);
+    c.read(1);
+    const double rv = h.hscal[0];
+    if (rv == 0.0 || !finite(rv)) {
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    alpha = rho / rv;
+    launch_convert(N, r, AMG_F64, sv, AMG_F64, 1.0, c.s);
+    c.axpby(-alpha, v, 1.0, sv);  // s = r - alpha v
+    ++it;
+    c.dot(sv, sv, 0, true);
+    c.read(1);
+    if (h.hscal[0] <= rtol * nb) {
+      c.axpby(alpha, ph, 1.0, x);
+      if (verify()) {
+        status = AMG_OK;
+        break;
+      }
+      continue;
+    }
+    c.pc(sv, sh, AMG_F64);
+    c.spmv(sh, AMG_F64, t);
+    c.dot(t, t, 0);
+    c.dot(t, sv, 1);
+    c.read(2);
+    const double tt = h.hscal[0];
+    if (tt == 0.0 || !finite(tt)) {
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    omega = h.hscal[1] / tt;
+    c.axpbypcz(alpha, ph, omega, sh, 1.0, x);  // x += alpha ph + omega sh
+    launch_convert(N, sv, AMG_F64, r, AMG_F64, 1.0, c.s);
+    c.axpby(-omega, t, 1.0, r);  // r = s - omega t
+    rho_old = rho;
+    c.dot(r, r, 0, true);
+    c.read(1);
+    const double nr = h.hscal[0];
+    if (omega == 0.0 || !finite(omega)) {
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    if (nr <= rtol * nb && verify()) {
+      status = AMG_OK;
+      break;
+    }
+  }
+  return finish(c, b, x, r, nb, status, it, restarts, rep);
+}
+
+// ---- flexible GMRES(m) with CGS2 (cfg 4, 5) ----
+int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  const int m = h.p.gmres_m;
+  const int64_t N = c.N;
+  double* r = h.vec[0];
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hh(m + 1);
+  c.residual(b, x, r);
+  c.dot(r, r, 0, true);
+  c.read(1);
+  double beta = h.hscal[0];
+  int it = 0, cycles = 0, status = AMG_NOT_CONVERGED;
+  if (beta <= rtol * nb) status = AMG_OK;
+  const double sx = (double)dtype_size(h.zt);
+  // device scalar slots: [0, 32) h, [32, 64) h2, 64 norm, [96, 128) y
+  while (status != AMG_OK && it < h.p.maxiter) {
+    ++cycles;
+    launch_scale_by_inv(N, r, h.dscal + 64, h.V[0], c.s);  // dscal[64] holds beta (set below)
+    c.bytes += 16.0 * N;
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    bool stop = false;
+    for (; j < m && !stop; ++j) {
+      c.pc(h.V[j], h.Z[j], h.zt);
+      double* w = h.V[j + 1];
+      c.spmv(h.Z[j], h.zt, w);
+      PtrList Vl{};
+      for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
+      // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2
+      launch_mdot(N, j + 1, Vl, w, h.partials, h.dscal, c.s);
+      launch_maxpy(N, j + 1, Vl, h.dscal, w, c.s);
+      launch_mdot(N, j + 1, Vl, w, h.partials, h.dscal + 32, c.s);
+      launch_maxpy(N, j + 1, Vl, h.dscal + 32, w, c.s);
+      c.bytes += 8.0 * N * (4.0 * (j + 1) + 6.0);
+      launch_dot(N, w, AMG_F64, w, AMG_F64, h.partials, h.dscal + 64, true, c.s);
+      launch_scale_by_inv(N, w, h.dscal + 64, w, c.s);
+      c.bytes += 8.0 * N * 3.0;
+      AMG_CK(cudaMemcpyAsync(h.hscal, h.dscal, sizeof(double) * 65, cudaMemcpyDeviceToHost, c.s));
+      AMG_CK(cudaStreamSynchronize(c.s));
+      for (int i = 0; i <= j; ++i) hh[i] = h.hscal[i] + h.hscal[32 + i];
+      const double hn = h.hscal[64];
+      hh[j + 1] = hn;
+      for (int i = 0; i < j; ++i) {
+        double t = cs[i] * hh[i] + sn[i] * hh[i + 1];
+        hh[i + 1] = -sn[i] * hh[i] + cs[i] * hh[i + 1];
+        hh[i] = t;
+      }
+      const double rr = std::hypot(hh[j], hh[j + 1]);
+      if (rr == 0.0 || !finite(rr)) {
+        status = AMG_EBREAKDOWN;
+        stop = true;
+        break;
+      }
+      cs[j] = hh[j] / rr;
+      sn[j] = hh[j + 1] / rr;
+      hh[j] = rr;
+      hh[j + 1] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hh[i];
+      ++it;
+      if (std::fabs(g[j + 1]) <= rtol * nb || it >= h.p.maxiter || hn == 0.0) stop = true;
+    }
+    if (status == AMG_EBREAKDOWN) break;
+    const int k = j;
+    for (int i = k - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int cc = i + 1; cc < k; ++cc) t = t - H[(size_t)i * m + cc] * y[cc];
+      y[i] = t / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < k; ++i) h.hscal[96 + i] = y[i];
+    AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+    PtrList Zl{};
+    for (int i = 0; i < k; ++i) Zl.p[i] = (const double*)h.Z[i];
+    launch_zupdate(N, k, Zl, h.zt, h.dscal + 96, x, c.s);
+    c.bytes += N * (16.0 + sx * k);
+    c.residual(b, x, r);
+    launch_dot(N, r, AMG_F64, r, AMG_F64, h.partials, h.dscal + 64, true, c.s);
+    c.bytes += 8.0 * N;
+    AMG_CK(cudaMemcpyAsync(h.hscal + 64, h.dscal + 64, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    AMG_CK(cudaStreamSynchronize(c.s));
+    beta = h.hscal[64];
+    if (beta <= rtol * nb) status = AMG_OK;
+  }
+  return finish(c, b, x, r, nb, status, it, cycles > 0 ? cycles - 1 : 0, rep);
+}
+
+}  // namespace
+
+int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t s, amg_report* rep) {
+  Ctx c(h, s);
+  // ||b||; ||b|| = 0 -> x = 0, converged, relres 0
+  launch_dot(c.N, b, AMG_F64, b, AMG_F64, h.partials, h.dscal, true, s);
+  c.read(1);
+  const double nb = h.hscal[0];
+  if (rep) rep->levels = h.amg_active ? (int)h.lv.size() + 1 : 0;
+  if (nb == 0.0) {
+    AMG_CK(cudaMemsetAsync(x, 0, sizeof(double) * c.N, s));
+    AMG_CK(cudaStreamSynchronize(s));
+    if (rep) rep->iters = 0, rep->converged = 1, rep->restarts = 0, rep->relres_true = 0.0, rep->alg_bytes = 0.0;
+    return AMG_OK;
+  }
+  switch (h.p.solver) {
+    case AMG_CG: return solve_cg(c, b, x, rtol, nb, rep);
+    case AMG_BICGSTAB: return solve_bicgstab(c, b, x, rtol, nb, rep);
+    case AMG_GMRES: {
+      // the first normalisation reads beta from dscal[64]
+      c.residual(b, x, h.vec[0]);
+      launch_dot(c.N, h.vec[0], AMG_F64, h.vec[0], AMG_F64, h.partials, h.dscal + 64, true, s);
+      return solve_gmres(c, b, x, rtol, nb, rep);
+    }
+    default: fail(AMG_EINVAL, "unknown solver");
+  }
+}
+
+}  // namespace amgb

@@ -1,0 +1,43 @@
+// ops.h -- host launchers of the solve-phase kernels (all stream-ordered, no sync,
+// no allocation).  Vector/value types are AMG_F32 / AMG_F64.
+#pragma once
+
+#include "common.cuh"
+
+namespace amgb {
+
+// K1  y = alpha A x + beta y
+void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
+                 cudaStream_t s);
+// K2  r = f - A x   (f, x, r of type xt)
+void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s);
+// K5  xo = x + M (f - A x)
+void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
+                   cudaStream_t s);
+// K4a x = M f
+void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
+                    cudaStream_t s);
+// K8  x = Ainv f (dense N x N, values vt, vectors xt)
+void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void* x, int xt,
+                       cudaStream_t s);
+
+// K10 p = m_S o (r_p - B u*)   B: [nnz][nu] on A's pattern (nu velocity comps, 1 x nu blocks)
+void launch_schur_p(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* Bv,
+                    const void* mS, int vt, const void* rp, const void* us, void* p, int xt,
+                    int G, cudaStream_t s);
+// K11 ru2 = r_u - B^T p         BT: [nnz][nu] (nu x 1 blocks)
+void launch_schur_u(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* BTv,
+                    int vt, const void* ru, const void* p, void* ru2, int xt, int G, cudaStream_t s);
+
+// K9  split the fp64 interleaved outer vector (b comps per cell) into the velocity part
+// (nu = b-1 comps, type xt) and the pressure part (type xt), narrowing RNE; optional
+// scale (used to fold a GMRES normalisation in).
+void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
+                  cudaStream_t s);
+// K9' join (u, p) -> interleaved fp64 z (exact widening)
+void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt,
+                 cudaStream_t s);
+// convert a whole vector between dtypes (narrowing RNE / exact widening); scale applied in fp64
+void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s);
+
+}  // namespace amgb

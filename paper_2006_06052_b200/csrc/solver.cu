@@ -1,0 +1,279 @@
+// solver.cu -- C ABI of the solver handle: amg_setup / amg_solve / introspection.
+#include <chrono>
+#include <cstring>
+
+#include "amg.h"
+#include "ops.h"
+#include "solver.h"
+
+namespace amgb {
+int validate_bsr(const amg_bsr* A, bool square);
+Mat view_of(const amg_bsr* A);
+void set_last_error(const std::string& s);
+
+Handle::~Handle() {
+  if (pc_graph) cudaGraphExecDestroy(pc_graph);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (hscal) cudaFreeHost(hscal);
+}
+
+namespace {
+
+void alloc_workspace(Handle& h, cudaStream_t s) {
+  const int64_t N = (int64_t)h.n * h.b;
+  const int nv = 8;
+  for (int i = 0; i < nv; ++i) h.vec.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+  if (h.p.solver == AMG_GMRES) {
+    const int m = h.p.gmres_m;
+    // Z is stored in the preconditioner's output precision: the fp32 V-cycle output is
+    // exactly representable in fp32, so storing it narrow is lossless.
+    h.zt = (h.amg_active && h.xt == AMG_F32) ? AMG_F32 : AMG_F64;
+    for (int i = 0; i <= m; ++i) h.V.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+    for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(N, 1) * dtype_size(h.zt)));
+  }
+  h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32);
+  h.dscal = h.arena.alloc_n<double>(256);
+  AMG_CK(cudaMallocHost(&h.hscal, sizeof(double) * 256));
+  if (h.schur) {
+    const size_t xs = dtype_size(h.xt);
+    h.rp = h.arena.alloc(std::max(h.n, 1) * xs);
+    h.pp = h.arena.alloc(std::max(h.n, 1) * xs);
+  }
+  AMG_CK(cudaEventCreate(&h.ev0));
+  AMG_CK(cudaEventCreate(&h.ev1));
+  (void)s;
+}
+
+double mat_bytes(const Mat& A, int vt) {
+  return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(vt)) + 4.0 * (A.n + 1);
+}
+
+}  // namespace
+
+int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle** out, int nparts) {
+  int rc = validate_bsr(A, true);
+  if (rc != AMG_OK) return rc;
+  if (!p || !out) return AMG_EINVAL;
+  if (p->solver < AMG_CG || p->solver > AMG_GMRES) return AMG_EINVAL;
+  if (p->precond < AMG_PC_AMG || p->precond > AMG_PC_NONE) return AMG_EINVAL;
+  if (p->solver == AMG_GMRES && (p->gmres_m < 1 || p->gmres_m > 31)) return AMG_EINVAL;
+  if (p->npre < 1 || p->npost < 0 || p->max_levels < 1 || p->maxiter < 0) return AMG_EINVAL;
+  if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
+      (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
+    return AMG_EINVAL;
+  auto t0 = std::chrono::steady_clock::now();
+  Handle* h = new Handle;
+  try {
+    h->p = *p;
+    h->vt = p->hier_dtype;
+    h->xt = p->vcycle_vec_dtype;
+    h->n = A->n_block_rows;
+    h->b = A->block_size;
+    h->schur = p->precond == AMG_PC_SCHUR;
+    h->pc = p->schur_p_component;
+    h->amg_active = p->precond != AMG_PC_NONE;
+    if (h->schur && (h->pc < 0 || h->pc >= h->b)) fail(AMG_EINVAL, "schur_p_component out of range");
+    // library-owned fp64 copy of A (setup in own structures, then moved)
+    Mat src = view_of(A);
+    Mat& M = h->A;
+    M = src;
+    M.vt = AMG_F64;
+    M.ptr = h->arena.alloc_n<int32_t>(M.n + 1);
+    M.col = h->arena.alloc_n<int32_t>(std::max<int64_t>(M.nnz, 1));
+    M.val = h->arena.alloc_n<double>(std::max<int64_t>(M.nnz, 1) * M.b * M.b);
+    AMG_CK(cudaMemcpyAsync(M.ptr, src.ptr, sizeof(int32_t) * (M.n + 1), cudaMemcpyDeviceToDevice, s));
+    if (M.nnz > 0) {
+      AMG_CK(cudaMemcpyAsync(M.col, src.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToDevice, s));
+      launch_convert(M.nnz * M.b * M.b, src.val, src.vt, M.val, AMG_F64, 1.0, s);
+    }
+    h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
+    if (h->amg_active) setup_build(*h, M, nparts, s);
+    alloc_workspace(*h, s);
+    h->alg_bytes_precond = precond_bytes(*h);
+    AMG_CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = h;
+  return AMG_OK;
+}
+
+}  // namespace amgb
+
+using namespace amgb;
+
+#define AMG_GUARD_BEGIN try {
+#define AMG_GUARD_END                  \
+  }                                    \
+  catch (const ::amgb::Error& e) {     \
+    ::amgb::set_last_error(e.what);    \
+    return e.code;                     \
+  }                                    \
+  catch (const std::bad_alloc&) {      \
+    return AMG_ENOMEM;                 \
+  }                                    \
+  catch (...) {                        \
+    return AMG_EINVAL;                 \
+  }
+
+extern "C" {
+
+int amg_setup(const amg_bsr* A, const amg_params* p, void* stream, struct amg_handle** out) {
+  AMG_GUARD_BEGIN
+  if (!A || !p || !out) return AMG_EINVAL;
+  Handle* h = nullptr;
+  int rc = setup_common(A, p, (cudaStream_t)stream, &h, 1);
+  if (rc != AMG_OK) return rc;
+  *out = reinterpret_cast<amg_handle*>(h);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+void amg_destroy(struct amg_handle* hh) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  delete h;
+}
+
+int amg_solve(struct amg_handle* hh, const double* b, double* x, double rtol, void* stream, amg_report* rep) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || (!b && h->n > 0) || (!x && h->n > 0) || !(rtol > 0.0)) return AMG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  amg_report local{};
+  amg_report* r = rep ? rep : &local;
+  std::memset(r, 0, sizeof(*r));
+  AMG_CK(cudaEventRecord(h->ev0, s));
+  int st = krylov_solve(*h, b, x, rtol, s, r);
+  AMG_CK(cudaEventRecord(h->ev1, s));
+  AMG_CK(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  AMG_CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  r->solve_s = ms * 1e-3;
+  r->setup_s = h->setup_s;
+  if (st == AMG_OK && !r->converged) st = AMG_NOT_CONVERGED;
+  return st;
+  AMG_GUARD_END
+}
+
+int amg_solve_host(struct amg_handle* hh, const double* b_host, double* x_host, double rtol, void* stream,
+                   amg_report* rep) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !b_host || !x_host) return AMG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t N = (int64_t)h->n * h->b;
+  // staging buffers live in the handle's workspace: vec[6], vec[7] are free outside a solve
+  // only for CG; use dedicated ones
+  static_assert(sizeof(double) == 8, "");
+  if (!h->pc_in) {
+    h->pc_in = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
+    h->pc_out = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
+  }
+  AMG_CK(cudaMemcpyAsync(h->pc_in, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  AMG_CK(cudaMemcpyAsync(h->pc_out, x_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  int st = amg_solve(hh, h->pc_in, h->pc_out, rtol, stream, rep);
+  if (st < 0) return st;
+  AMG_CK(cudaMemcpyAsync(x_host, h->pc_out, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  AMG_CK(cudaStreamSynchronize(s));
+  return st;
+  AMG_GUARD_END
+}
+
+int amg_apply_precond(struct amg_handle* hh, const double* r, double* z, void* stream) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || ((!r || !z) && h->n > 0)) return AMG_EINVAL;
+  precond_apply(*h, r, z, AMG_F64, (cudaStream_t)stream, 1.0);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int amg_vcycle(struct amg_handle* hh, const double* f, double* x, void* stream) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !h->amg_active) return AMG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t N0 = h->lv.empty() ? h->coarse.N : (int64_t)h->lv[0].A.n * h->lv[0].A.b;
+  launch_convert(N0, f, AMG_F64, level0_f(*h), h->xt, 1.0, s);
+  void* out = vcycle_run(*h, 0, s);
+  launch_convert(N0, out, h->xt, x, AMG_F64, 1.0, s);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int amg_level_info(struct amg_handle* hh, int32_t level, int64_t* out) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !out || !h->amg_active || level < 0) return AMG_EINVAL;
+  if ((size_t)level < h->lv.size()) {
+    const Level& L = h->lv[level];
+    out[0] = L.A.n, out[1] = L.A.b, out[2] = L.A.nnz, out[3] = L.P.nnz, out[4] = L.nc;
+    return AMG_OK;
+  }
+  if ((size_t)level == h->lv.size()) {
+    out[0] = h->coarse.n, out[1] = h->coarse.b, out[2] = h->coarse.A.nnz, out[3] = 0, out[4] = 0;
+    return AMG_OK;
+  }
+  return AMG_EINVAL;
+}
+
+int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_t* ptr, int32_t* col, double* val) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !val || !h->amg_active || level < 0 || (size_t)level > h->lv.size()) return AMG_EINVAL;
+  const bool coarsest = (size_t)level == h->lv.size();
+  if (which == 3) {
+    if (coarsest) return AMG_EINVAL;
+    const Level& L = h->lv[level];
+    const int64_t cnt = (int64_t)L.A.n * L.A.b * L.A.b;
+    double* tmp = nullptr;
+    AMG_CK(cudaMalloc(&tmp, std::max<int64_t>(cnt, 1) * 8));
+    launch_convert(cnt, L.M, h->vt, tmp, AMG_F64, 1.0, nullptr);
+    AMG_CK(cudaMemcpy(val, tmp, cnt * 8, cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+    return AMG_OK;
+  }
+  if (which < 0 || which > 2 || (coarsest && which != 0) || !ptr || !col) return AMG_EINVAL;
+  const Mat& M = coarsest ? h->coarse.A : (which == 0 ? h->lv[level].A : which == 1 ? h->lv[level].P : h->lv[level].R);
+  AMG_CK(cudaDeviceSynchronize());
+  AMG_CK(cudaMemcpy(ptr, M.ptr, sizeof(int32_t) * (M.n + 1), cudaMemcpyDeviceToHost));
+  if (M.nnz > 0) AMG_CK(cudaMemcpy(col, M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
+  const int64_t cnt = M.nnz * M.b * M.b;
+  double* tmp = nullptr;
+  AMG_CK(cudaMalloc(&tmp, std::max<int64_t>(cnt, 1) * 8));
+  launch_convert(cnt, M.val, M.vt, tmp, AMG_F64, 1.0, nullptr);
+  AMG_CK(cudaMemcpy(val, tmp, cnt * 8, cudaMemcpyDeviceToHost));
+  cudaFree(tmp);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int amg_level_aggregates(struct amg_handle* hh, int32_t level, int32_t* agg) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !agg || level < 0 || (size_t)level >= h->lv.size()) return AMG_EINVAL;
+  AMG_CK(cudaDeviceSynchronize());
+  AMG_CK(cudaMemcpy(agg, h->lv[level].agg, sizeof(int32_t) * h->lv[level].A.n, cudaMemcpyDeviceToHost));
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int amg_schur_export(struct amg_handle* hh, double* shat_diag, double* m_s) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !h->schur || !shat_diag || !m_s) return AMG_EINVAL;
+  AMG_CK(cudaDeviceSynchronize());
+  AMG_CK(cudaMemcpy(shat_diag, h->shat64, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+  AMG_CK(cudaMemcpy(m_s, h->mS64, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int64_t amg_device_bytes(struct amg_handle* hh) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  return h ? h->arena.bytes() : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// vcycle.cu -- the preconditioner applies: SA V(npre,npost) cycle (C9)
+// and the Schur pressure correction (Eq. 9a/9b).  Pure launches on
+// one stream; no allocation, no synchronisation (graph-capturable).
+#include <utility>
+
+#include "ops.h"
+#include "solver.h"
+
+namespace amgb {
+
+void* level0_f(Handle& h) { return h.lv.empty() ? h.coarse.f : h.lv[0].f; }
+
+// V(l, f):  x = M f;  r = f - A x;  f_c = R r;  x_c = V(l+1, f_c);  x += P x_c;
+//           x = x + M (f - A x)            (one kernel per line; fp64 accumulation,
+//                                            one rounding on store)
+void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
+  const int xt = h.xt, vt = h.vt;
+  if (l == h.lv.size()) {
+    launch_dense_gemv(h.coarse.N, h.coarse.inv, vt, h.coarse.f, h.coarse.x, xt, s);  // K8
+    return h.coarse.x;
+  }
+  Level& L = h.lv[l];
+  void* x = L.x;
+  void* t = L.t;
+  launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
+  for (int k = 1; k < h.p.npre; ++k) {
+    launch_smooth(L.A, L.M, L.f, x, t, xt, s);
+    std::swap(x, t);
+  }
+  launch_residual(L.A, L.f, x, L.r, xt, s);  // K4b: r = f - A x
+  void* fc = (l + 1 < h.lv.size()) ? h.lv[l + 1].f : h.coarse.f;
+  launch_spmv(L.R, 1.0, L.r, xt, 0.0, fc, xt, s);  // K6: f_c = R r
+  void* xc = vcycle_run(h, l + 1, s);
+  launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
+  for (int k = 0; k < h.p.npost; ++k) {          // K5: post-smooth (double-buffered)
+    launch_smooth(L.A, L.M, L.f, x, t, xt, s);
+    std::swap(x, t);
+  }
+  return x;
+}
+
+// z = M r.  Monolithic AMG: narrow r once (RNE), V-cycle, widen exactly (C9).
+// Schur (C10): split + narrow; u* = V(r_u); p = m_S o (r_p - B u*); r_u' = r_u - B^T p;
+// u = V(r_u'); z = join(u, p).
+void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale) {
+  const int64_t N = (int64_t)h.n * h.b;
+  if (!h.amg_active) {
+    launch_convert(N, r, AMG_F64, z, zt, scale, s);
+    return;
+  }
+  void* f0 = level0_f(h);
+  if (!h.schur) {
+    launch_convert(N, r, AMG_F64, f0, h.xt, scale, s);
+    void* x = vcycle_run(h, 0, s);
+    launch_convert(N, x, h.xt, z, zt, 1.0, s);
+    return;
+  }
+  launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s);                                 // K9
+  void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
+  launch_schur_p(h.n, h.nu, h.A.ptr, h.A.col, h.Bv, h.mS, h.vt, h.rp, us, h.pp, h.xt, h.A.G, s);  // K10
+  launch_schur_u(h.n, h.nu, h.A.ptr, h.A.col, h.BTv, h.vt, f0, h.pp, f0, h.xt, h.A.G, s);    // K11 (in place)
+  void* u = vcycle_run(h, 0, s);                                                               // u = V(r_u')
+  launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
+}
+
+// Algorithmic bytes of one preconditioner application:
+// every matrix array read once per use, every vector read/written once per kernel.
+static double mat_bytes(const Mat& A, int vt) {
+  return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(vt)) + 4.0 * (A.n + 1);
+}
+
+static double vcycle_bytes(const Handle& h) {
+  const double sx = (double)dtype_size(h.xt), sv = (double)dtype_size(h.vt);
+  double tot = 0.0;
+  for (const Level& L : h.lv) {
+    const double nb = (double)L.A.n * L.A.b;
+    tot += 2.0 * mat_bytes(L.A, h.vt) + mat_bytes(L.P, h.vt) + mat_bytes(L.R, h.vt);
+    tot += 2.0 * nb * L.A.b * sv;  // M read twice
+    // K4a: f, x | K4b: f, x, r | K6: r, f_c | K7: x_c, x rw | K5: f, x, x'
+    tot += nb * sx * (2 + 3 + 1 + 2 + 3);
+    tot += (double)L.nc * L.A.b * sx * 2;  // f_c write, x_c read
+  }
+  tot += (double)h.coarse.N * h.coarse.N * sv + 2.0 * h.coarse.N * sx;
+  return tot;
+}
+
+double precond_bytes(const Handle& h) {
+  const int64_t N = (int64_t)h.n * h.b;
+  const double sx = (double)dtype_size(h.xt), sv = (double)dtype_size(h.vt);
+  if (!h.amg_active) return (double)N * 16.0;
+  if (!h.schur) return vcycle_bytes(h) + (double)N * (8.0 + sx) * 2.0;
+  const double n = (double)h.n, nnz = (double)h.A.nnz;
+  double t = 2.0 * vcycle_bytes(h);
+  t += (double)N * 8.0 + (double)N * sx;                        // split
+  t += nnz * (4.0 + 3.0 * sv) + 4.0 * (n + 1) + n * sv + n * 3 * sx + 2 * n * sx;  // K10
+  t += nnz * (4.0 + 3.0 * sv) + 4.0 * (n + 1) + n * sx + 6.0 * n * sx;           // K11
+  t += (double)N * sx + (double)N * 8.0;                        // join
+  return t;
+}
+
+}  // namespace amgb

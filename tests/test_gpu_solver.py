@@ -1,0 +1,246 @@
+"""GPU setup / V-cycle / Schur / Krylov parity against the CPU oracle, through the C ABI.
+
+Bars (BASELINE.json north_star): aggregates and sparsity patterns
+bit-exact; level values bit-exact in fp64 (== after fp32 rounding for the fp32
+hierarchy); V-cycle / preconditioner outputs norm-wise 1e-10 (fp64; the coarse
+solve is an explicit Gauss-Jordan inverse on the GPU vs LU in the oracle) and 1e-5
+(fp32); solves within +-2 iterations of the oracle with true relres <= 1e-8."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import random_bsr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def amg():
+    import paper_2006_06052_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxiter": "maxiter",
+          "smoother": "smoother", "sa_omega": "sa_omega", "eps_strong": "eps_strong",
+          "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
+          "jacobi_omega": "jacobi_omega"}
+
+
+def make_pair(amg, ptr, col, val, hier32=True, **kw):
+    """Build the GPU solver and the oracle with the same parameters."""
+    A = amg.BSR.from_numpy(ptr, col, val)
+    gp = amg.default_params(hier_dtype=amg.F32 if hier32 else amg.F64,
+                            vcycle_vec_dtype=amg.F32 if hier32 else amg.F64, **kw)
+    S = amg.Solver(A, gp)
+    op = oracle.default_params(hier_f32=int(hier32), vec_f32=int(hier32),
+                               **{ORC_OF[k]: v for k, v in kw.items() if k in ORC_OF})
+    O = oracle.Solver(oracle.Mat.from_arrays(ptr, col, val), op)
+    return A, S, O
+
+
+def r32(a):
+    return a.astype(np.float32).astype(np.float64)
+
+
+def relerr(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def check_hierarchy(S, O, hier32):
+    assert S.levels == O.levels
+    for l in range(O.levels):
+        n, b, nnzA, nnzP, nc = S.level_info(l)
+        oA = O.level_mat(l, 0)
+        optr, ocol, oval = oA.to_arrays()
+        ptr, col, val = S.level_export(l, 0)
+        assert np.array_equal(ptr, optr) and np.array_equal(col, ocol), f"A pattern level {l}"
+        assert np.array_equal(val, r32(oval) if hier32 else oval), f"A values level {l}"
+        if l == O.levels - 1:
+            break
+        assert np.array_equal(S.level_aggregates(l), O.level_agg(l)), f"aggregates level {l}"
+        for which in (1, 2):
+            optr, ocol, oval = O.level_mat(l, which).to_arrays()
+            ptr, col, val = S.level_export(l, which)
+            assert np.array_equal(ptr, optr) and np.array_equal(col, ocol), f"pattern {which} level {l}"
+            assert np.array_equal(val, r32(oval) if hier32 else oval), f"values {which} level {l}"
+        M = S.level_export(l, 3)
+        oM = O.level_M(l)
+        assert np.array_equal(M, r32(oM) if hier32 else oM), f"smoother level {l}"
+
+
+CASES = [
+    ("cfg1-16", gen.POISSON3, 16, dict(precond=0, solver=0), False),
+    ("cfg3-16", gen.STOKES, 16, dict(precond=0, solver=1), True),
+    ("cfg3-24", gen.STOKES, 24, dict(precond=0, solver=1), True),
+    ("cfg4-16", gen.STOKES, 16, dict(precond=1, solver=2), True),
+    ("poisson-lowce", gen.POISSON3, 10, dict(precond=0, solver=0, coarse_enough=40), False),
+    ("stokes-lowce-f64", gen.STOKES, 10, dict(precond=1, solver=2, coarse_enough=40), False),
+]
+
+
+@pytest.mark.parametrize("name,kind,n,kw,h32", CASES, ids=[c[0] for c in CASES])
+def test_hierarchy_bit_exact(amg, name, kind, n, kw, h32):
+    ptr, col, val = gen.matrix(kind, n)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=h32, **kw)
+    check_hierarchy(S, O, h32)
+    if kw.get("precond") == 1:
+        d, m = S.schur_export()
+        od, om = O.schur_vectors()
+        assert np.array_equal(d, od) and np.array_equal(m, om)
+
+
+def test_hierarchy_random_matrices(amg, rng):
+    for b in (1, 2, 3, 4):
+        for trial in range(2):
+            ptr, col, val = random_bsr(rng, 400, b, density=0.012, symmetric_pattern=(trial == 0), dom=6)
+            for h32 in (False, True):
+                A, S, O = make_pair(amg, ptr, col, val, hier32=h32, precond=0, coarse_enough=20 * b)
+                check_hierarchy(S, O, h32)
+
+
+def test_smoother_jacobi_and_omega(amg):
+    ptr, col, val = gen.matrix(gen.POISSON3, 10)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=False, precond=0, smoother=1, sa_omega=0.5,
+                        coarse_enough=100)
+    check_hierarchy(S, O, False)
+
+
+@pytest.mark.parametrize("name,kind,n,kw,h32", CASES, ids=[c[0] for c in CASES])
+def test_precond_parity(amg, rng, name, kind, n, kw, h32):
+    ptr, col, val = gen.matrix(kind, n)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=h32, **kw)
+    N = len(ptr) * 0 + (len(ptr) - 1) * val.shape[-1]
+    for _ in range(2):
+        r = rng.standard_normal(N)
+        z = S.apply_precond(torch.as_tensor(r, device="cuda"), torch.zeros(N, dtype=torch.float64, device="cuda"))
+        torch.cuda.synchronize()
+        assert relerr(z.cpu().numpy(), O.precond(r)) <= (1e-5 if h32 else 1e-10)
+
+
+def _solve(amg, S, bvec, rtol=1e-8):
+    b = torch.as_tensor(bvec, device="cuda")
+    x = torch.zeros_like(b)
+    rep = S.solve(b, x, rtol)
+    return x.cpu().numpy(), rep
+
+
+SOLVE_CASES = [
+    ("cfg1", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(precond=0, solver=0), False),
+    ("cfg1-f32", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(precond=0, solver=0), True),
+    ("cfg3-32", gen.STOKES, 32, gen.RHS_LID, dict(precond=0, solver=1), True),
+    ("cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2), True),
+    ("cfg4-32", gen.STOKES, 32, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2), True),
+    ("cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2), True),
+    ("gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10), False),
+]
+
+
+@pytest.mark.parametrize("name,kind,n,rk,kw,h32", SOLVE_CASES, ids=[c[0] for c in SOLVE_CASES])
+def test_solve_parity(amg, name, kind, n, rk, kw, h32):
+    ptr, col, val = gen.matrix(kind, n)
+    bvec = gen.rhs(rk, n, val.shape[-1])
+    A, S, O = make_pair(amg, ptr, col, val, hier32=h32, **kw)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    assert rep.status == amg.OK and rep.converged
+    assert rep.relres_true <= 1e-8
+    # independent check of the reported relres with the oracle's SpMV
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert true <= 1e-8 and abs(true - rep.relres_true) <= 1e-10
+    assert abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters)
+    assert rep.levels == O.levels
+
+
+def test_cfg3_full_size(amg):
+    # BASELINE configs[2] at its full size (64^3, 1.05M unknowns)
+    n = 64
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID, n, 4)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=0, solver=1)
+    check_hierarchy(S, O, True)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    assert rep.converged and rep.relres_true <= 1e-8 and abs(rep.iters - ro.iters) <= 2
+
+
+def test_zero_rhs_and_x0(amg, rng):
+    ptr, col, val = gen.matrix(gen.POISSON3, 8)
+    A = amg.BSR.from_numpy(ptr, col, val)
+    S = amg.Solver(A, amg.default_params(solver=amg.CG, coarse_enough=100))
+    b = torch.zeros(512 * 3, dtype=torch.float64, device="cuda")
+    x = torch.as_tensor(rng.standard_normal(512 * 3), device="cuda")
+    rep = S.solve(b, x)
+    assert rep.converged and rep.iters == 0 and rep.relres_true == 0 and not x.any()
+    # nonzero x0 is honoured: starting at the solution converges immediately
+    bv = gen.rhs(gen.RHS_UNIFORM, 8, 3)
+    xs = np.linalg.solve(oracle.Mat.from_arrays(ptr, col, val).dense(), bv)
+    rep = S.solve(torch.as_tensor(bv, device="cuda"), torch.as_tensor(xs, device="cuda"))
+    assert rep.converged and rep.iters == 0
+
+
+def test_single_level_exact(amg, rng):
+    ptr, col, val = gen.matrix(gen.POISSON3, 6)  # 648 unknowns <= coarse_enough
+    A = amg.BSR.from_numpy(ptr, col, val)
+    for solver in (amg.CG, amg.BICGSTAB, amg.GMRES):
+        S = amg.Solver(A, amg.default_params(solver=solver, hier_dtype=amg.F64, vcycle_vec_dtype=amg.F64))
+        assert S.levels == 1
+        x, rep = _solve(amg, S, rng.standard_normal(648))
+        assert rep.converged and rep.iters == 1
+
+
+def test_identity_no_precond(amg, rng):
+    n = 100
+    A = amg.BSR.from_numpy(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), np.tile(np.eye(3), (n, 1, 1)))
+    for solver in (amg.CG, amg.BICGSTAB, amg.GMRES):
+        S = amg.Solver(A, amg.default_params(solver=solver, precond=amg.PC_NONE))
+        b = rng.standard_normal(3 * n)
+        x, rep = _solve(amg, S, b)
+        assert rep.converged and rep.iters == 1 and np.allclose(x, b)
+
+
+def test_error_codes(amg):
+    ptr, col, val = gen.matrix(gen.POISSON3, 4)
+    # non-square
+    A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=65)
+    with pytest.raises(amg.AmgError) as e:
+        amg.Solver(A)
+    assert e.value.status == amg.EDIM
+    # missing diagonal block
+    p2 = np.array([0, 1, 2], np.int32)
+    c2 = np.array([1, 0], np.int32)
+    with pytest.raises(amg.AmgError) as e:
+        amg.Solver(amg.BSR.from_numpy(p2, c2, np.ones((2, 3, 3))), coarse_enough=1)
+    assert e.value.status == amg.EZERODIAG
+    # singular diagonal block
+    v = val.copy()
+    for i in range(64):
+        for k in range(ptr[i], ptr[i + 1]):
+            if col[k] == i and i == 5:
+                v[k] = np.array([[1, 2, 3], [2, 4, 6], [0, 0, 1.0]])
+    with pytest.raises(amg.AmgError) as e:
+        amg.Solver(amg.BSR.from_numpy(ptr, col, v), coarse_enough=30)
+    assert e.value.status == amg.ESINGULAR_BLOCK
+    # bad params
+    with pytest.raises(amg.AmgError) as e:
+        amg.Solver(amg.BSR.from_numpy(ptr, col, val), gmres_m=40)
+    assert e.value.status == amg.EINVAL
+
+
+def test_fp32_vs_fp64_iteration_parity(amg):
+    # mixed precision "does not increase the number of iterations"
+    n = 24
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    its = []
+    for h32 in (False, True):
+        A = amg.BSR.from_numpy(ptr, col, val)
+        dt = amg.F32 if h32 else amg.F64
+        S = amg.Solver(A, amg.default_params(solver=amg.GMRES, precond=amg.PC_SCHUR, hier_dtype=dt,
+                                             vcycle_vec_dtype=dt))
+        x, rep = _solve(amg, S, bvec)
+        assert rep.converged
+        its.append(rep.iters)
+    assert abs(its[0] - its[1]) <= 1

@@ -1,0 +1,125 @@
+"""K1 BSR SpMV parity: CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Norm-wise relative error: <= 1e-12 when the
+oracle sees the same (fp32-rounded) values, <= 1e-5 for fp32 values vs the fp64
+oracle (north_star); fp32 outputs add one fp32 rounding (<= 1e-7)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import random_bsr
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def amg():
+    import paper_2006_06052_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def _relerr(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def _r32(a):
+    return a.astype(np.float32).astype(np.float64)
+
+
+def _run(amg, ptr, col, val, x, vt, xt, yt, alpha=1.0, beta=0.0, y0=None):
+    tdt = {amg.F32: torch.float32, amg.F64: torch.float64}
+    A = amg.BSR.from_numpy(ptr, col, val, dtype=tdt[vt])
+    xd = torch.as_tensor(x).to("cuda", tdt[xt])
+    n, b = len(ptr) - 1, val.shape[-1]
+    yd = (torch.zeros(n * b, dtype=tdt[yt], device="cuda") if y0 is None
+          else torch.as_tensor(y0).to("cuda", tdt[yt]))
+    amg.bsr_spmv(A, xd, yd, alpha, beta)
+    torch.cuda.synchronize()
+    return yd.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+@pytest.mark.parametrize("vt,xt,yt", [(0, 0, 0), (1, 0, 0), (1, 1, 1), (1, 1, 0), (0, 1, 0), (1, 0, 1)])
+def test_spmv_random(amg, rng, b, vt, xt, yt):
+    for n, dens in ((1, 1.0), (37, 0.2), (300, 0.02), (1000, 0.05)):  # several tiles + ragged tail
+        ptr, col, val = random_bsr(rng, n, b, density=dens)
+        x = rng.uniform(-1, 1, n * b)
+        y0 = rng.standard_normal(n * b)
+        for alpha, beta in ((1.0, 0.0), (-0.7, 1.3)):
+            y = _run(amg, ptr, col, val, x, vt, xt, yt, alpha, beta, y0)
+            vv = _r32(val) if vt == amg.F32 else val
+            xx = _r32(x) if xt == amg.F32 else x
+            yy = _r32(y0) if yt == amg.F32 else y0
+            ref_same = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, alpha, beta, yy)
+            tol = 1e-12 if yt == amg.F64 else 2e-7
+            assert _relerr(y, ref_same) <= tol
+            if vt == amg.F32:
+                ref64 = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x, alpha, beta, y0)
+                assert _relerr(y, ref64) <= 1e-5
+
+
+def test_spmv_beta0_overwrites_nan(amg, rng):
+    ptr, col, val = random_bsr(rng, 50, 3, density=0.1)
+    y = _run(amg, ptr, col, val, np.ones(150), 0, 0, 0, 1.0, 0.0, np.full(150, np.nan))
+    assert np.all(np.isfinite(y))
+
+
+def test_spmv_empty_rows_and_empty_matrix(amg, rng):
+    # rows without blocks produce 0 (beta = 0); n = 0 is a no-op
+    ptr = np.array([0, 0, 2, 2, 3], np.int32)
+    col = np.array([0, 3, 1], np.int32)
+    val = rng.standard_normal((3, 4, 4))
+    x = rng.standard_normal(16)
+    y = _run(amg, ptr, col, val, x, 0, 0, 0)
+    ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
+    assert _relerr(y, ref) <= 1e-14 and not y[:4].any() and not y[8:12].any()
+    A = amg.BSR.from_numpy(np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros((0, 3, 3)))
+    amg.bsr_spmv(A, torch.zeros(0, dtype=torch.float64, device="cuda"),
+                 torch.zeros(0, dtype=torch.float64, device="cuda"))
+
+
+def test_spmv_worked_example(amg):
+    from conftest import golden
+    g = golden("worked_example.json")
+    y = _run(amg, np.array(g["bsr_ptr"]), np.array(g["bsr_col"]), np.array(g["bsr_val"]), np.ones(6), 0, 0, 0)
+    assert np.allclose(y, g["y_ones"], rtol=0, atol=1e-14)
+
+
+def test_spmv_bad_args(amg):
+    A = amg.BSR.from_numpy(np.array([0, 1], np.int32), np.array([0], np.int32), np.ones((1, 5, 5)))
+    with pytest.raises(amg.AmgError) as e:
+        amg.bsr_spmv(A, torch.ones(5, dtype=torch.float64, device="cuda"),
+                     torch.ones(5, dtype=torch.float64, device="cuda"))
+    assert e.value.status == amg.EINVAL
+
+
+@pytest.mark.parametrize("b", [3, 4])
+@pytest.mark.parametrize("n", [16, 24])
+def test_spmv_cfg2_pattern(amg, b, n):
+    # cfg 2 distribution (27-point, N(0,1) + 30 I) at reduced n: f64/f64 and f32-values/f64-x
+    ptr, col, val = gen.matrix(gen.RAND27, n, b)
+    x = gen.rhs(gen.X_UNIFORM, n, b)
+    ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
+    assert _relerr(_run(amg, ptr, col, val, x, 0, 0, 0), ref) <= 1e-12
+    y32 = _run(amg, ptr, col, val, x, 1, 0, 0)
+    assert _relerr(y32, ref) <= 1e-5
+    ref32 = oracle.spmv(oracle.Mat.from_arrays(ptr, col, _r32(val)), x)
+    assert _relerr(y32, ref32) <= 1e-12
+
+
+@pytest.mark.parametrize("b", [4])
+def test_spmv_cfg2_full_size(amg, b):
+    # BASELINE configs[1] at its full size (128^3, 55.7M blocks), in the bench's launch
+    # configuration (fp32 values x fp64 x); the oracle computes every row
+    n = 128
+    ptr, col, val = gen.matrix(gen.RAND27, n, b)
+    x = gen.rhs(gen.X_UNIFORM, n, b)
+    ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
+    y = _run(amg, ptr, col, val, x, 1, 0, 0)
+    assert _relerr(y, ref) <= 1e-5
+    y = _run(amg, ptr, col, val, x, 0, 0, 0)
+    assert _relerr(y, ref) <= 1e-12
