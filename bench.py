@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 solve phase (BASELINE.json metric: "Stokes solve time & BSR
+SpMV HBM GB/s (4x4 fp32 blocks) at 1/2/4/8 B200").
+
+A step = one full solve (every SURVEY.md §8(a) row: outer SpMV, Schur-PC apply with two
+fp32 SA V-cycles, FGMRES(30) vector work, convergence control) of BASELINE configs[4]
+(cfg 5: stabilised Stokes on 256^3 cells, 67M unknowns, 4x4 BSR), x0 = 0, rtol 1e-8,
+with A, b and the hierarchy resident in HBM.  Setup is timed separately.  The
+matrices (15 GB of values) are far larger than L2, so no L2 flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--cfg 5 --n 256]
+
+Multi-GPU (torchrun, one rank per GPU): z-slab row partition, NCCL halo + allreduce;
+timings are CUDA events on the solve stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+CFG_SOLVER = {  # BASELINE configs -> (rhs kind, solver, precond)
+    1: (gen.RHS_UNIFORM, "cg", "amg"),
+    3: (gen.RHS_LID, "bicgstab", "amg"),
+    4: (gen.RHS_FORCE_NOISE, "gmres", "schur"),
+    5: (gen.RHS_LID_NOISE, "gmres", "schur"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_problem(cfg: int, n: int, row_begin: int, row_end: int):
+    kind = gen.POISSON3 if cfg == 1 else gen.STOKES
+    ptr, col, val = gen.matrix(kind, n, None, row_begin, row_end)
+    b = gen.rhs(CFG_SOLVER[cfg][0], n, val.shape[-1], row_begin, row_end)
+    return ptr, col, val, b
+
+
+def params_for(amg, cfg: int):
+    _, solver, pc = CFG_SOLVER[cfg]
+    hier = amg.F64 if cfg == 1 else amg.F32
+    return amg.default_params(solver={"cg": amg.CG, "bicgstab": amg.BICGSTAB, "gmres": amg.GMRES}[solver],
+                              precond=amg.PC_SCHUR if pc == "schur" else amg.PC_AMG,
+                              hier_dtype=hier, vcycle_vec_dtype=hier)
+
+
+def oracle_sample(cfg: int, n_full: int, n_sample: int, gpu_iters: int | None):
+    """Oracle (single thread, as it stands) solve of the same generator at n_sample^3,
+    scaled to the full workload: seconds x (cells ratio) x (iteration ratio)."""
+    import oracle
+    ptr, col, val, b = make_problem(cfg, n_sample, 0, n_sample ** 3)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    _, solver, pc = CFG_SOLVER[cfg]
+    p = oracle.default_params(solver={"cg": oracle.CG, "bicgstab": oracle.BICGSTAB, "gmres": oracle.GMRES}[solver],
+                              precond=oracle.PC_SCHUR if pc == "schur" else oracle.PC_AMG,
+                              hier_f32=0 if cfg == 1 else 1, vec_f32=0 if cfg == 1 else 1)
+    t0 = time.perf_counter()
+    S = oracle.Solver(A, p)
+    t1 = time.perf_counter()
+    r = S.solve(b, rtol=1e-8)
+    t2 = time.perf_counter()
+    scale = (n_full / n_sample) ** 3
+    it_ratio = (gpu_iters / r.iters) if (gpu_iters and r.iters) else 1.0
+    return {"setup_s": t1 - t0, "solve_s": t2 - t1, "iters": r.iters, "relres": r.relres_true,
+            "value": (t2 - t1) * scale * it_ratio, "n_sample": n_sample, "scale": scale, "it_ratio": it_ratio}
+
+
+def run_reference(args, rank: int):
+    """--impl reference: the CPU oracle as it stands, each step a bounded sample of the
+    workload (n_sample^3 cells), scaled to the full cfg; rank 0 only."""
+    if rank != 0:
+        return
+    n_full = args.n or gen.CONFIGS[args.cfg]["n"]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(args.cfg, n_full, args.ref_n, None)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    line = {
+        "impl": "reference", "metric": metric_name(args.cfg, n_full), "value": v, "unit": "s/solve",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64 outer / f32 hierarchy",
+        "data": "synthetic", "config": config_dict(args.cfg, n_full, args.gpus),
+        "cpu_baseline": {"value": v, "unit": "s/solve", "cores": 1, "kind": "oracle",
+                         "sample": f"oracle solve of the cfg-{args.cfg} generator at {args.ref_n}^3 cells "
+                                   f"(x{vals[0]['scale']:.0f} cells to {n_full}^3; same iteration count assumed), "
+                                   f"{vals[0]['iters']} its, {statistics.median([r['solve_s'] for r in vals]):.2f} s"},
+        "e2e": {"value": v, "unit": "s/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(cfg, n):
+    return f"stokes_solve_time_cfg{cfg}_{n}^3"
+
+
+def config_dict(cfg, n, gpus):
+    _, solver, pc = CFG_SOLVER[cfg]
+    return {"workload": f"cfg{cfg}: {'stabilised Stokes' if cfg != 1 else 'vector Poisson'} {n}^3 cells, "
+                        f"{solver}{'(30) flexible' if solver == 'gmres' else ''} + "
+                        f"{'Schur pressure correction' if pc == 'schur' else 'SA-AMG'}, "
+                        f"{'fp32' if cfg != 1 else 'fp64'} hierarchy, rtol 1e-8, x0 = 0",
+            "unknowns": 4 * n ** 3 if cfg != 1 else 3 * n ** 3, "parallelism": f"z-slabs x{gpus}",
+            "l2": "inputs (15 GB matrix at 256^3) larger than L2; no flush"}
+
+
+def spmv_cfg2(amg, torch, n=128, reps=30):
+    """cfg 2 SpMV microbench, 4x4 fp32 values x fp64 x (the metric's SpMV)."""
+    ptr, col, val = gen.matrix(gen.RAND27, n, 4)
+    x = gen.rhs(gen.X_UNIFORM, n, 4)
+    A = amg.BSR.from_numpy(ptr, col, val, dtype=torch.float32)
+    del val
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.zeros_like(xd)
+    for _ in range(5):
+        amg.bsr_spmv(A, xd, yd)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        amg.bsr_spmv(A, xd, yd)
+        b.record()
+    torch.cuda.synchronize()
+    ms = statistics.median([a.elapsed_time(b) for a, b in ev])
+    Z, nr = len(col), n ** 3
+    byts = 4 * (nr + 1) + Z * (4 + 16 * 4) + nr * 4 * 8 * 2
+    return {"config": "cfg2 27-point 128^3, 4x4 fp32 values x fp64 x", "ms": ms, "GBs": byts / ms / 1e6,
+            "alg_bytes": byts}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=5, choices=[1, 3, 4, 5])
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--ref-n", type=int, default=32, help="grid of the oracle's bounded sample")
+    ap.add_argument("--cpu-n", type=int, default=48, help="grid of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spmv", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import paper_2006_06052_b200 as amg
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.n or gen.CONFIGS[args.cfg]["n"]
+    nrows = n ** 3
+    r0, r1 = rank * nrows // world, (rank + 1) * nrows // world
+    t0 = time.perf_counter()
+    ptr, col, val, bvec = make_problem(args.cfg, n, r0, r1)
+    t_gen = time.perf_counter() - t0
+    A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=nrows)
+    del val
+    params = params_for(amg, args.cfg)
+    comm = amg.Comm(rank, world) if world > 1 else None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    S = amg.Solver(A, params, comm=comm, row_begin=r0, n_global=nrows)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    del A
+    torch.cuda.empty_cache()
+    b = torch.as_tensor(bvec, device="cuda")
+    x = torch.zeros_like(b)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        x.zero_()
+        return S.solve(b, x, 1e-8)
+
+    for _ in range(args.warmup):
+        rep = step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = amg.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        reps = [step() for _ in range(args.steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = (amg.kernel_launches() - l0)
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    rep = reps[-1]
+
+    # end to end through the C ABI with HOST buffers (copies inside the timed region)
+    bh = torch.as_tensor(bvec).pin_memory()
+    xh = torch.zeros_like(bh).pin_memory()
+    S.solve_host(bh, xh, 1e-8)
+    torch.cuda.synchronize()
+    te = []
+    for _ in range(max(1, min(args.steps, 3))):
+        xh.zero_()
+        t0 = time.perf_counter()
+        S.solve_host(bh, xh, 1e-8)
+        te.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(te)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # per-kernel CUDA-event timings of one more solve (outside the timed region)
+    amg.profile_begin()
+    step()
+    prof = amg.profile_end()
+    tot_ms = sum(p["total_ms"] for p in prof)
+    top = max(prof, key=lambda p: p["total_ms"])
+    peak, peak_src = peaks()
+    avg_ms = top["total_ms"] / top["launches"]
+    achieved = top["bytes"] / (avg_ms * 1e-3) / 1e9
+    prof_sorted = sorted(prof, key=lambda p: -p["total_ms"])[:8]
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    out = {
+        "metric": metric_name(args.cfg, n), "value": ms * 1e-3, "unit": "s/solve", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 outer / f32 hierarchy" if args.cfg != 1 else "f64",
+        "data": "synthetic", "config": config_dict(args.cfg, n, world),
+        "iters": rep.iters, "relres_true": rep.relres_true, "converged": rep.converged, "levels": rep.levels,
+        "setup_s": setup_s, "gen_s": t_gen,
+        "solve_alg_bytes": rep.alg_bytes, "solve_alg_GBs": rep.alg_bytes / (ms * 1e-3) / 1e9,
+        "solve_roofline_frac": rep.alg_bytes / (ms * 1e-3) / 1e9 / peak,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_s, "unit": "s/solve", "h2d_bytes_per_step": 2 * bh.numel() * 8,
+                "d2h_bytes_per_step": bh.numel() * 8},
+        "roofline": {"bound": "hbm", "kernel": top["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "share_of_step": top["total_ms"] / tot_ms, "bytes_per_launch": top["bytes"],
+                     "avg_launch_ms": avg_ms},
+        "top_kernels": [{"kernel": p["kernel"], "launches": p["launches"], "ms": round(p["total_ms"], 4),
+                         "GBs": round(p["bytes"] / (p["total_ms"] / p["launches"] * 1e-3) / 1e9, 1)}
+                        for p in prof_sorted],
+        "clocks": clk.summary(),
+    }
+    if not args.no_spmv and world == 1:
+        del S
+        torch.cuda.empty_cache()
+        out["spmv"] = spmv_cfg2(amg, torch)
+        out["spmv"]["frac"] = out["spmv"]["GBs"] / peak
+    if not args.no_cpu_baseline:
+        c = oracle_sample(args.cfg, n, args.cpu_n, rep.iters)
+        out["cpu_baseline"] = {"value": c["value"], "unit": "s/solve", "cores": 1, "kind": "oracle",
+                               "sample": f"oracle (1 thread) solve of the cfg-{args.cfg} generator at {args.cpu_n}^3: "
+                                         f"{c['solve_s']:.2f} s, {c['iters']} its; scaled x{c['scale']:.0f} cells "
+                                         f"and x{c['it_ratio']:.2f} iterations to {n}^3"}
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,18 @@ int amg_vcycle(struct amg_handle* h, const double* f, double* x, void* stream);
 /* device bytes held by the handle (hierarchy + workspace) */
 int64_t amg_device_bytes(struct amg_handle* h);
 
+/* ---- launch accounting / per-kernel timing (diagnostics, host) ---- */
+/* number of library kernels launched by this process so far */
+int64_t amg_kernel_launches(void);
+/* start recording a CUDA-event pair and the algorithmic bytes around every launch */
+int amg_profile_begin(void);
+/* stop recording; writes a JSON list [{"kernel","bytes","launches","total_ms"}, ...]
+ * aggregated per (kernel, bytes per launch) into out (host, capacity cap) and returns the
+ * full length.  Synchronises the device. */
+int64_t amg_profile_end(char* out, int64_t cap);
+/* text of the last error raised on this thread */
+const char* amg_last_error(void);
+
 /* ---- multi-GPU: one process per GPU, contiguous block-row slabs ---- */
 /* NCCL unique id (128 bytes, host) generated by rank 0 (amg_comm_unique_id) and
  * broadcast by the caller (torch.distributed). */

@@ -60,7 +60,8 @@ class amg_report(ctypes.Structure):
 EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", "amg_solve_host",
            "amg_apply_precond", "bsr_spmv", "amg_destroy", "amg_level_info", "amg_level_export",
            "amg_level_aggregates", "amg_schur_export", "amg_vcycle", "amg_device_bytes",
-           "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy"]
+           "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
+           "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error"]
 
 _lib = None
 
@@ -94,6 +95,9 @@ def lib():
             "amg_comm_init": (i32, [P, i32, i32, P]),
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
             "amg_comm_destroy": (None, [P]),
+            "amg_kernel_launches": (i64, []),
+            "amg_profile_begin": (i32, []),
+            "amg_profile_end": (i64, [P, i64]),
         }
         for name, (res, args) in sig.items():
             if not hasattr(L, name):
@@ -103,6 +107,26 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def kernel_launches() -> int:
+    """Library kernels launched by this process so far."""
+    return int(lib().amg_kernel_launches())
+
+
+def profile_begin():
+    _check(lib().amg_profile_begin(), "amg_profile_begin")
+
+
+def profile_end() -> list:
+    """Per-(kernel, bytes/launch) CUDA-event timings recorded since profile_begin()."""
+    import json
+    cap = 1 << 22
+    buf = ctypes.create_string_buffer(cap)
+    n = lib().amg_profile_end(buf, cap)
+    if n >= cap:
+        raise RuntimeError("profile record larger than the buffer")
+    return json.loads(buf.value.decode())
 
 
 def status_string(status: int) -> str:

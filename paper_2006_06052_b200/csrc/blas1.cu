@@ -2,6 +2,7 @@
 // fixed grid for a given length, fixed-order finalisation), multi-dot / multi-axpy
 // for the CGS2 Arnoldi step, linear combinations, and the flexible-GMRES update.
 #include "blas1.h"
+#include "prof.h"
 
 namespace amgb {
 
@@ -140,6 +141,7 @@ inline unsigned ew_grid(int64_t n) {
 void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double* partials, double* out, bool sqrt_out,
                 cudaStream_t s) {
   const int nb = nblocks_for(n);
+  ProfScope ps_(prof_name("dot", 1, at, bt), (double)n * (a == b ? dtype_size(at) : dtype_size(at) + dtype_size(bt)), s);
   if (at == AMG_F64 && bt == AMG_F64)
     k_dot<double, double><<<nb, kT, 0, s>>>(n, (const double*)a, (const double*)b, partials, nb);
   else if (at == AMG_F64 && bt == AMG_F32)
@@ -149,41 +151,49 @@ void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double*
   else
     k_dot<float, float><<<nb, kT, 0, s>>>(n, (const float*)a, (const float*)b, partials, nb);
   AMG_CK_LAUNCH();
+  ++g_launches;
   k_finalize<<<1, kT, 0, s>>>(1, partials, nb, out, sqrt_out ? 1 : 0);
   AMG_CK_LAUNCH();
 }
 
 void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* partials, double* out, cudaStream_t s) {
   const int nb = nblocks_for(n);
+  ProfScope ps_(prof_name("mdot", k, AMG_F64, -1), 8.0 * n * (k + 1), s);
   k_mdot<<<nb, kT, 0, s>>>(n, k, V, w, partials, nb);
   AMG_CK_LAUNCH();
+  ++g_launches;
   k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
   AMG_CK_LAUNCH();
 }
 
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s) {
+  ProfScope ps_(prof_name("maxpy", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
   k_maxpy<<<ew_grid(n), kT, 0, s>>>(n, k, V, coef, w);
   AMG_CK_LAUNCH();
 }
 
 void launch_zupdate(int64_t n, int k, const PtrList& Z, int zt, const double* y, double* x, cudaStream_t s) {
+  ProfScope ps_(prof_name("zupdate", k, zt, -1), (double)n * (16.0 + (double)k * dtype_size(zt)), s);
   if (zt == AMG_F32) k_zupdate<float><<<ew_grid(n), kT, 0, s>>>(n, k, Z, y, x);
   else k_zupdate<double><<<ew_grid(n), kT, 0, s>>>(n, k, Z, y, x);
   AMG_CK_LAUNCH();
 }
 
 void launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s) {
+  ProfScope ps_(prof_name("axpby", 1, AMG_F64, -1), 8.0 * n * (b == 0.0 ? 2.0 : 3.0), s);
   k_axpby<<<ew_grid(n), kT, 0, s>>>(n, a, x, b, y);
   AMG_CK_LAUNCH();
 }
 
 void launch_axpbypcz(int64_t n, double a, const double* x, double b, const double* y, double c, double* z,
                      cudaStream_t s) {
+  ProfScope ps_(prof_name("axpbypcz", 1, AMG_F64, -1), 32.0 * n, s);
   k_axpbypcz<<<ew_grid(n), kT, 0, s>>>(n, a, x, b, y, c, z);
   AMG_CK_LAUNCH();
 }
 
 void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s) {
+  ProfScope ps_(prof_name("scale", 1, AMG_F64, -1), 16.0 * n, s);
   k_scale_by_inv<<<ew_grid(n), kT, 0, s>>>(n, x, sdev, y);
   AMG_CK_LAUNCH();
 }

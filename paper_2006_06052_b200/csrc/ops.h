@@ -6,6 +6,8 @@
 
 namespace amgb {
 
+extern int64_t g_schur_nnz;
+
 // K1  y = alpha A x + beta y
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s);

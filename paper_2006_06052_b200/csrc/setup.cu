@@ -761,6 +761,7 @@ void setup_build(Handle& h, const Mat& A64, int nparts, cudaStream_t s) {
     launch_convert(A64.nnz * nu, btv, AMG_F64, h.BTv, h.vt, 1.0, s);
     launch_convert(A64.n, h.mS64, AMG_F64, h.mS, h.vt, 1.0, s);
     Au.G = choose_group(Au.nnz, Au.n, Au.b);
+    g_schur_nnz = A64.nnz;
     Amg = Au;
   }
   h.bh = Amg.b;

@@ -4,8 +4,11 @@
 
 #include "bsr.cuh"
 #include "ops.h"
+#include "prof.h"
 
 namespace amgb {
+
+int64_t g_schur_nnz = 0;  // nnz of the Schur B / B^T pattern (set by setup)
 
 namespace {
 
@@ -35,11 +38,18 @@ void dispatch_g(int G, F&& f) {
   else f(std::integral_constant<int, 8>{});
 }
 
+double mat_bytes(const Mat& A) {  // algorithmic bytes of one pass over A
+  return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(A.vt)) + 4.0 * (A.n + 1);
+}
+
 }  // namespace
 
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s) {
   if (A.n == 0) return;
+  ProfScope ps_(prof_name("spmv", A.b, A.vt, xt),
+                mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) +
+                    (double)A.n * A.b * dtype_size(yt) * (beta != 0.0 ? 2.0 : 1.0), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_g(A.G, [&](auto Gc) {
@@ -67,6 +77,8 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
 
 void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s) {
   if (A.n == 0) return;
+  ProfScope ps_(prof_name("residual", A.b, A.vt, xt),
+                mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + 2.0 * A.n * A.b * dtype_size(xt), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_g(A.G, [&](auto Gc) {
@@ -87,6 +99,8 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
 void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
                    cudaStream_t s) {
   if (A.n == 0) return;
+  ProfScope ps_(prof_name("smooth", A.b, A.vt, xt),
+                mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 3.0 * A.n * A.b * dtype_size(xt), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_g(A.G, [&](auto Gc) {
@@ -107,6 +121,7 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
                     cudaStream_t s) {
   if (n == 0) return;
+  ProfScope ps_(prof_name("apply_M", b, vt, xt), (double)n * b * b * dtype_size(vt) + 2.0 * n * b * dtype_size(xt), s);
   dispatch_b(b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_t(vt, [&](auto v) {
@@ -139,6 +154,7 @@ __global__ void __launch_bounds__(256) k_dense_gemv(int N, const V* __restrict__
 void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void* x, int xt,
                        cudaStream_t s) {
   if (N == 0) return;
+  ProfScope ps_(prof_name("coarse_gemv", 1, vt, xt), (double)N * N * dtype_size(vt) + 2.0 * N * dtype_size(xt), s);
   dispatch_t(vt, [&](auto v) {
     using V = decltype(v);
     dispatch_t(xt, [&](auto xx) {
@@ -219,6 +235,8 @@ void launch_schur_p(int32_t n, int nu, const int32_t* ptr, const int32_t* col, c
                     cudaStream_t s) {
   if (n == 0) return;
   if (nu != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
+  ProfScope ps_(prof_name("schur_p", 3, vt, xt),
+                ((double)g_schur_nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + (double)n * dtype_size(vt) + 5.0 * n * dtype_size(xt), s);
   dispatch_g(G, [&](auto Gc) {
     constexpr int GG = decltype(Gc)::value;
     dispatch_t(vt, [&](auto v) {
@@ -237,6 +255,7 @@ void launch_schur_u(int32_t n, int nu, const int32_t* ptr, const int32_t* col, c
                     const void* ru, const void* p, void* ru2, int xt, int G, cudaStream_t s) {
   if (n == 0) return;
   if (nu != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
+  ProfScope ps_(prof_name("schur_u", 3, vt, xt), ((double)g_schur_nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + 7.0 * n * dtype_size(xt), s);
   dispatch_g(G, [&](auto Gc) {
     constexpr int GG = decltype(Gc)::value;
     dispatch_t(vt, [&](auto v) {
@@ -283,6 +302,7 @@ __global__ void k_convert(int64_t N, const I* __restrict__ in, O* __restrict__ o
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
                   cudaStream_t s) {
   if (n == 0) return;
+  ProfScope ps_(prof_name("split", b, AMG_F64, xt), (double)n * b * (8.0 + dtype_size(xt)), s);
   dispatch_t(xt, [&](auto xx) {
     using X = decltype(xx);
     k_split<X><<<grid_for((int64_t)n * b, 256), 256, 0, s>>>(n, b, pc, r, scale, (X*)ru, (X*)rp);
@@ -292,6 +312,7 @@ void launch_split(int32_t n, int b, int pc, const double* r, double scale, void*
 
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt, cudaStream_t s) {
   if (n == 0) return;
+  ProfScope ps_(prof_name("join", b, zt, xt), (double)n * b * (dtype_size(zt) + dtype_size(xt)), s);
   dispatch_t(xt, [&](auto xx) {
     using X = decltype(xx);
     dispatch_t(zt, [&](auto zz) {
@@ -304,6 +325,7 @@ void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt,
 
 void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s) {
   if (N == 0) return;
+  ProfScope ps_(prof_name("convert", 1, ot, it), (double)N * (dtype_size(it) + dtype_size(ot)), s);
   unsigned g = grid_for(N, 256);
   if (g > 148u * 16u) g = 148u * 16u;
   dispatch_t(it, [&](auto ii) {
