@@ -126,6 +126,15 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
 
 void amg_destroy(struct amg_handle* h);
 
+/* SpMV plan: analyses A's row tiles once (one reduction + one stream sync) so that
+ * repeated products run the TMA-staged kernel.  The plan keeps A's device pointers:
+ * A's arrays must stay allocated and unchanged while the plan is used. */
+struct bsr_plan;
+int bsr_plan_create(const amg_bsr* A /* host struct, device arrays */, void* stream, struct bsr_plan** out);
+int bsr_plan_spmv(struct bsr_plan* P, double alpha, const void* x, int32_t xt, double beta, void* y,
+                  int32_t yt, void* stream);
+void bsr_plan_destroy(struct bsr_plan* P);
+
 /* ---- introspection (used by the parity tests; all outputs HOST) ---- */
 /* out[5] = {n_block_rows, block_size, nnzb(A_l), nnzb(P_l) or 0, n_coarse or 0} */
 int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);

@@ -61,7 +61,8 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_apply_precond", "bsr_spmv", "amg_destroy", "amg_level_info", "amg_level_export",
            "amg_level_aggregates", "amg_schur_export", "amg_vcycle", "amg_device_bytes",
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
-           "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error"]
+           "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
+           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy"]
 
 _lib = None
 
@@ -96,6 +97,9 @@ def lib():
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
             "amg_comm_destroy": (None, [P]),
             "amg_kernel_launches": (i64, []),
+            "bsr_plan_create": (i32, [P, P, P]),
+            "bsr_plan_spmv": (i32, [P, dbl, P, i32, dbl, P, i32, P]),
+            "bsr_plan_destroy": (None, [P]),
             "amg_profile_begin": (i32, []),
             "amg_profile_end": (i64, [P, i64]),
         }
@@ -198,6 +202,28 @@ def bsr_spmv(A: BSR, x, y, alpha: float = 1.0, beta: float = 0.0, stream=None):
     _check(lib().bsr_spmv(ctypes.byref(d), alpha, ctypes.c_void_p(x.data_ptr()), _dt(x), beta,
                           ctypes.c_void_p(y.data_ptr()), _dt(y), _stream_ptr(stream)), "bsr_spmv")
     return y
+
+
+class SpmvPlan:
+    """bsr_plan_create / bsr_plan_spmv: TMA-staged repeated products with A (A's tensors
+    must stay alive and unchanged)."""
+
+    def __init__(self, A: BSR, stream=None):
+        self.A = A
+        self.d = A.desc()
+        h = ctypes.c_void_p()
+        _check(lib().bsr_plan_create(ctypes.byref(self.d), _stream_ptr(stream), ctypes.byref(h)), "bsr_plan_create")
+        self.h = h
+
+    def __call__(self, x, y, alpha: float = 1.0, beta: float = 0.0, stream=None):
+        _check(lib().bsr_plan_spmv(self.h, alpha, ctypes.c_void_p(x.data_ptr()), _dt(x), beta,
+                                   ctypes.c_void_p(y.data_ptr()), _dt(y), _stream_ptr(stream)), "bsr_plan_spmv")
+        return y
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.bsr_plan_destroy(self.h)
+            self.h = None
 
 
 def default_params(**kw) -> amg_params:

@@ -62,7 +62,61 @@ __global__ void __launch_bounds__(kT) k_mdot(int64_t n, int k, PtrList V, const 
   block_reduce_store<32>(acc, k, partials, nblk);
 }
 
-// out[j] = scale * sum of the nblk partials of reduction j, in a fixed order
+// CGS2 fused update (flexible GMRES).  Basis vectors are stored
+// unnormalised with a scale s_j (v_j = s_j V_j): w_out = w - sum_j c_j s_j V_j, and in the
+// same pass either the next Gram-Schmidt coefficients acc_j = s_j V_j . w_out (DOT) or
+// ||w_out||^2 (acc_0).  V_j[i] is re-read from L1 in the second loop.
+template <bool DOT>
+__global__ void __launch_bounds__(kT) k_cgs_update(int64_t n, int k, PtrList V, const double* __restrict__ sc,
+                                                   const double* __restrict__ coef, const double* w,
+                                                   double* w_out, double* partials, int nblk) {
+  __shared__ double c[32], sv[32];
+  if (threadIdx.x < k) {
+    sv[threadIdx.x] = sc[threadIdx.x];
+    c[threadIdx.x] = coef[threadIdx.x] * sc[threadIdx.x];
+  }
+  __syncthreads();
+  double acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    double v = w[i];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < k) v = fma(-c[j], V.p[j][i], v);
+    w_out[i] = v;
+    if constexpr (DOT) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < k) acc[j] = fma(sv[j] * V.p[j][i], v, acc[j]);
+    } else {
+      acc[0] = fma(v, v, acc[0]);
+    }
+  }
+  block_reduce_store<32>(acc, DOT ? k : 1, partials, nblk);
+}
+
+// scaled multi-dot: out[j] = s_j V_j . w
+__global__ void __launch_bounds__(kT) k_mdot_scaled(int64_t n, int k, PtrList V, const double* __restrict__ sc,
+                                                    const double* __restrict__ w, double* partials, int nblk) {
+  double acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const double wi = w[i];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < k) acc[j] = fma(V.p[j][i], wi, acc[j]);
+  }
+  __shared__ double s2[32];
+  if (threadIdx.x < k) s2[threadIdx.x] = sc[threadIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] *= s2[j < k ? j : 0];
+  block_reduce_store<32>(acc, k, partials, nblk);
+}
+
+// x += sum_j y[j] Z_j ... see k_zupdate; here: out[j] = scale * sum of the nblk partials of reduction j, in a fixed order
 __global__ void k_finalize(int k, const double* partials, int nblk, double* out, int sqrt_out) {
   __shared__ double sh[kT];
   for (int j = 0; j < k; ++j) {
@@ -163,6 +217,29 @@ void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* pa
   AMG_CK_LAUNCH();
   ++g_launches;
   k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
+  AMG_CK_LAUNCH();
+}
+
+void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, const double* w, double* partials,
+                        double* out, cudaStream_t s) {
+  const int nb = nblocks_for(n);
+  ProfScope ps_(prof_name("mdot", k, AMG_F64, -1), 8.0 * n * (k + 1), s);
+  k_mdot_scaled<<<nb, kT, 0, s>>>(n, k, V, sc, w, partials, nb);
+  AMG_CK_LAUNCH();
+  ++g_launches;
+  k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
+  AMG_CK_LAUNCH();
+}
+
+void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
+                       double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s) {
+  const int nb = nblocks_for(n);
+  ProfScope ps_(prof_name(dot_next ? "cgs_update_dot" : "cgs_update_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
+  if (dot_next) k_cgs_update<true><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
+  else k_cgs_update<false><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
+  AMG_CK_LAUNCH();
+  ++g_launches;
+  k_finalize<<<1, kT, 0, s>>>(dot_next ? k : 1, partials, nb, out, dot_next ? 0 : 1);
   AMG_CK_LAUNCH();
 }
 

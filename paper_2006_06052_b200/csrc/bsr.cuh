@@ -62,65 +62,35 @@ __device__ __forceinline__ void load_raw(const T* __restrict__ p, T (&v)[B]) {
   }
 }
 
+// One block-row item: sum_c a[c] x[c], in fp64 (fp32 x fp32 products are exact there).
+// FAST (internal V-cycle on the fp32 hierarchy only, Listing V4's float backend,
+// PAPER.md:703-704): the b-term chain in fp32 FMA, converted once; the row sum over
+// items is still accumulated in fp64 by the caller.
+template <int B, typename V, typename X, bool FAST = false>
+__device__ __forceinline__ double item_dot(const V (&a)[B], const X (&x)[B]) {
+  if constexpr (FAST && std::is_same_v<V, float> && std::is_same_v<X, float>) {
+    float s = a[0] * x[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) s = fmaf(a[c], x[c], s);
+    return (double)s;
+  } else {
+    double s = (double)a[0] * (double)x[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) s = fma((double)a[c], (double)x[c], s);
+    return s;
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T to_out(double v) {
   return (T)v;  // fp32: round-to-nearest-even, once
 }
 
-// Partial (A x) of block row `row` for lane gl of its group.  The row is walked in
-// chunks of G blocks: one coalesced load brings the chunk's G column indices into
-// the group's registers; the chunk's G*B items are then handled B per lane
-// (item t = gl + i*G, block t / B, block row t % B), with all B value loads and B
-// x loads of a lane issued before any FMA (no col -> x dependency inside the
-// chunk, B independent 16/32-byte loads in flight per lane).  If G % B == 0 the
-// lane always handles block row r = gl % B and accumulates into acc[0]; otherwise
-// acc[r] is used.
+// Partial (A x) of block row `row` for lane gl of its group: one (block, block-row)
+// item per lane per iteration, items in storage order.  If G % B == 0 the lane always
+// handles block row r = gl % B and accumulates into acc[0]; otherwise acc[r].
 template <int B, int G, typename V, typename X>
 __device__ __forceinline__ void row_partial(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                                            const V* __restrict__ val, const X* __restrict__ x, int row,
-                                            int gl, double (&acc)[B]) {
-  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
-  // lanes of this group only: other groups of the warp may run a different number of chunks
-  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
-  for (int kc = k0; kc < k1; kc += G) {
-    const int nbk = min(G, k1 - kc);
-    const int mycol = (gl < nbk) ? __ldg(col + kc + gl) : 0;
-    V a[B][B];
-    X xv[B][B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-      const int t = gl + i * G;
-      const int kb = t / B;
-      const int c = __shfl_sync(gmask, mycol, kb & (G - 1), G);
-      if (kb < nbk) {
-        const int r = t % B;
-        load_raw<B, true>(val + ((int64_t)(kc + kb) * B + r) * B, a[i]);
-        load_raw<B, false>(x + (int64_t)c * B, xv[i]);
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < B; ++cc) a[i][cc] = V(0), xv[i][cc] = X(0);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-      double s = (double)a[i][0] * (double)xv[i][0];
-#pragma unroll
-      for (int cc = 1; cc < B; ++cc) s = fma((double)a[i][cc], (double)xv[i][cc], s);
-      if constexpr (G % B == 0) {
-        acc[0] += s;
-      } else {
-        const int r = (gl + i * G) % B;
-#pragma unroll
-        for (int rr = 0; rr < B; ++rr)
-          if (rr == r) acc[rr] += s;
-      }
-    }
-  }
-}
-
-// Simple variant: one item per lane per iteration, col loaded per item.
-template <int B, int G, typename V, typename X>
-__device__ __forceinline__ void row_partial_simple(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                                    const V* __restrict__ val, const X* __restrict__ x, int row,
                                                    int gl, double (&acc)[B]) {
   const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
@@ -134,9 +104,7 @@ __device__ __forceinline__ void row_partial_simple(const int32_t* __restrict__ p
     X xv[B];
     load_raw<B, true>(val + ((int64_t)kb * B + r) * B, a);
     load_raw<B, false>(x + (int64_t)c * B, xv);
-    double s = (double)a[0] * (double)xv[0];
-#pragma unroll
-    for (int cc = 1; cc < B; ++cc) s = fma((double)a[cc], (double)xv[cc], s);
+    const double s = item_dot<B, V, X>(a, xv);
     if constexpr (G % B == 0) {
       acc[0] += s;
     } else {
@@ -177,7 +145,7 @@ __device__ __forceinline__ double pick(const double (&y)[B], int i) {
 }
 
 // ---- K1: y = alpha A x + beta y (beta == 0 overwrites) ----
-template <int B, int G, typename V, typename X, typename Y, int VARIANT>
+template <int B, int G, typename V, typename X, typename Y>
 __global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__ ptr,
                                               const int32_t* __restrict__ col, const V* __restrict__ val,
                                               double alpha, const X* __restrict__ x, double beta,
@@ -186,10 +154,7 @@ __global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__
   const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
   const bool valid = row < n;
   double acc[B] = {};
-  if (valid) {
-    if constexpr (VARIANT == 1) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
-    else row_partial_simple<B, G>(ptr, col, val, x, row, gl, acc);
-  }
+  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
   double yv[B];
   group_reduce<B, G>(acc, yv);
   if (valid && gl < B) {

@@ -114,4 +114,38 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
   AMG_GUARD_END
 }
 
+struct bsr_plan {
+  amgb::Mat A;
+};
+
+int bsr_plan_create(const amg_bsr* A, void* stream, struct bsr_plan** out) {
+  AMG_GUARD_BEGIN
+  int rc = validate_bsr(A, false);
+  if (rc != AMG_OK) return rc;
+  if (!out) return AMG_EINVAL;
+  bsr_plan* p = new bsr_plan;
+  p->A = view_of(A);
+  try {
+    make_tma_plan(p->A, (cudaStream_t)stream);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  *out = p;
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+int bsr_plan_spmv(struct bsr_plan* P, double alpha, const void* x, int32_t xt, double beta, void* y, int32_t yt,
+                  void* stream) {
+  AMG_GUARD_BEGIN
+  if (!P || (xt != AMG_F32 && xt != AMG_F64) || (yt != AMG_F32 && yt != AMG_F64)) return AMG_EINVAL;
+  if (P->A.n > 0 && (!x || !y)) return AMG_EINVAL;
+  launch_spmv(P->A, alpha, x, xt, beta, y, yt, (cudaStream_t)stream);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
+void bsr_plan_destroy(struct bsr_plan* P) { delete P; }
+
 }  // extern "C"

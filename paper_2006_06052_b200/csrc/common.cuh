@@ -78,6 +78,10 @@ struct Mat {
   void* val = nullptr;
   int vt = AMG_F64;
   int G = 8;  // lanes per block row in the SpMV-type kernels (chosen from the row length)
+  // TMA-staged tile plan (bsr_tma.cuh); tma_grid == 0 -> direct kernels
+  int tma_tr = 0, tma_ntiles = 0, tma_ns = 0, tma_stage = 0, tma_col_off = 0, tma_val_off = 0, tma_grid = 0;
+  bool tma_rows = false;  // row-per-lane TMA consumer (short rows)
+  bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
 };
 
 // Lanes per block row: enough lanes to cover a row's (block, block-row) items in a

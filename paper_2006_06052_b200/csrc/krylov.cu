@@ -7,6 +7,7 @@
 
 #include "blas1.h"
 #include "ops.h"
+#include "prof.h"
 #include "solver.h"
 
 namespace amgb {
@@ -231,47 +232,55 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
 }
 
 // ---- flexible GMRES(m) with CGS2 (cfg 4, 5) ----
+// The Arnoldi basis is stored unnormalised, v_j = s_j V_j with s_j = 1/||V_j|| kept on
+// the device: the normalisation pass disappears (the preconditioner's split applies
+// s_j while narrowing, the Gram-Schmidt kernels apply it in registers), and each CGS2
+// step is three passes over the basis: scaled multi-dot, fused update + second
+// multi-dot, fused update + norm.
+__global__ void k_set_inv(double* dst, const double* src) { *dst = 1.0 / *src; }
+
 int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
   Handle& h = c.h;
   const int m = h.p.gmres_m;
   const int64_t N = c.N;
-  double* r = h.vec[0];
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hh(m + 1);
-  c.residual(b, x, r);
-  c.dot(r, r, 0, true);
-  c.read(1);
-  double beta = h.hscal[0];
+  double* sc = h.dscal + 128;  // s_j
+  // r = b - A x straight into V_0
+  c.residual(b, x, h.V[0]);
+  launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s);
+  c.bytes += 8.0 * N;
+  k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
+  AMG_CK_LAUNCH();
+  ++g_launches;
+  c.read(65);
+  double beta = h.hscal[64];
   int it = 0, cycles = 0, status = AMG_NOT_CONVERGED;
   if (beta <= rtol * nb) status = AMG_OK;
   const double sx = (double)dtype_size(h.zt);
-  // device scalar slots: [0, 32) h, [32, 64) h2, 64 norm, [96, 128) y
+  double s_host = 1.0 / beta;
   while (status != AMG_OK && it < h.p.maxiter) {
     ++cycles;
-    launch_scale_by_inv(N, r, h.dscal + 64, h.V[0], c.s);  // dscal[64] holds beta (set below)
-    c.bytes += 16.0 * N;
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int j = 0;
     bool stop = false;
     for (; j < m && !stop; ++j) {
-      c.pc(h.V[j], h.Z[j], h.zt);
+      c.pc(h.V[j], h.Z[j], h.zt, s_host);  // z_j = M(v_j), v_j = s_j V_j
       double* w = h.V[j + 1];
       c.spmv(h.Z[j], h.zt, w);
       PtrList Vl{};
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
-      // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2
-      launch_mdot(N, j + 1, Vl, w, h.partials, h.dscal, c.s);
-      launch_maxpy(N, j + 1, Vl, h.dscal, w, c.s);
-      launch_mdot(N, j + 1, Vl, w, h.partials, h.dscal + 32, c.s);
-      launch_maxpy(N, j + 1, Vl, h.dscal + 32, w, c.s);
-      c.bytes += 8.0 * N * (4.0 * (j + 1) + 6.0);
-      launch_dot(N, w, AMG_F64, w, AMG_F64, h.partials, h.dscal + 64, true, c.s);
-      launch_scale_by_inv(N, w, h.dscal + 64, w, c.s);
-      c.bytes += 8.0 * N * 3.0;
-      AMG_CK(cudaMemcpyAsync(h.hscal, h.dscal, sizeof(double) * 65, cudaMemcpyDeviceToHost, c.s));
-      AMG_CK(cudaStreamSynchronize(c.s));
+      launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s);                 // h1 = v^T w
+      launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s);   // w -= v h1; h2 = v^T w
+      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s);  // w -= v h2; ||w||
+      k_set_inv<<<1, 1, 0, c.s>>>(sc + j + 1, h.dscal + 64);
+      AMG_CK_LAUNCH();
+      ++g_launches;
+      c.bytes += 8.0 * N * (3.0 * (j + 1) + 5.0);
+      c.read(65);
       for (int i = 0; i <= j; ++i) hh[i] = h.hscal[i] + h.hscal[32 + i];
       const double hn = h.hscal[64];
+      s_host = 1.0 / hn;
       hh[j + 1] = hn;
       for (int i = 0; i < j; ++i) {
         double t = cs[i] * hh[i] + sn[i] * hh[i + 1];
@@ -307,15 +316,18 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     for (int i = 0; i < k; ++i) Zl.p[i] = (const double*)h.Z[i];
     launch_zupdate(N, k, Zl, h.zt, h.dscal + 96, x, c.s);
     c.bytes += N * (16.0 + sx * k);
-    c.residual(b, x, r);
-    launch_dot(N, r, AMG_F64, r, AMG_F64, h.partials, h.dscal + 64, true, c.s);
+    c.residual(b, x, h.V[0]);  // true residual = next cycle's V_0
+    launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s);
+    k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
+    AMG_CK_LAUNCH();
+    ++g_launches;
     c.bytes += 8.0 * N;
-    AMG_CK(cudaMemcpyAsync(h.hscal + 64, h.dscal + 64, sizeof(double), cudaMemcpyDeviceToHost, c.s));
-    AMG_CK(cudaStreamSynchronize(c.s));
+    c.read(65);
     beta = h.hscal[64];
+    s_host = 1.0 / beta;
     if (beta <= rtol * nb) status = AMG_OK;
   }
-  return finish(c, b, x, r, nb, status, it, cycles > 0 ? cycles - 1 : 0, rep);
+  return finish(c, b, x, h.V[0], nb, status, it, cycles > 0 ? cycles - 1 : 0, rep);
 }
 
 }  // namespace
@@ -336,12 +348,7 @@ int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_
   switch (h.p.solver) {
     case AMG_CG: return solve_cg(c, b, x, rtol, nb, rep);
     case AMG_BICGSTAB: return solve_bicgstab(c, b, x, rtol, nb, rep);
-    case AMG_GMRES: {
-      // the first normalisation reads beta from dscal[64]
-      c.residual(b, x, h.vec[0]);
-      launch_dot(c.N, h.vec[0], AMG_F64, h.vec[0], AMG_F64, h.partials, h.dscal + 64, true, s);
-      return solve_gmres(c, b, x, rtol, nb, rep);
-    }
+    case AMG_GMRES: return solve_gmres(c, b, x, rtol, nb, rep);
     default: fail(AMG_EINVAL, "unknown solver");
   }
 }

@@ -8,6 +8,9 @@ namespace amgb {
 
 extern int64_t g_schur_nnz;
 
+// build the TMA tile plan of a device matrix (one reduction + one sync); no-op for small n
+void make_tma_plan(Mat& A, cudaStream_t s);
+
 // K1  y = alpha A x + beta y
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s);

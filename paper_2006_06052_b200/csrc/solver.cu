@@ -88,6 +88,7 @@ int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle**
       launch_convert(M.nnz * M.b * M.b, src.val, src.vt, M.val, AMG_F64, 1.0, s);
     }
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
+    make_tma_plan(M, s);
     if (h->amg_active) setup_build(*h, M, nparts, s);
     alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);

@@ -1,8 +1,10 @@
 // spmv.cu -- instantiation + dispatch of the SpMV-type solve kernels (K1, K2, K4, K5,
 // K8, K9, K10, K11).  See bsr.cuh for the block-row design.
+#include <algorithm>
 #include <cstdlib>
 
 #include "bsr.cuh"
+#include "bsr_tma.cuh"
 #include "ops.h"
 #include "prof.h"
 
@@ -44,6 +46,89 @@ double mat_bytes(const Mat& A) {  // algorithmic bytes of one pass over A
 
 }  // namespace
 
+
+// ---------------------------------------------------------------- TMA tile plans
+__global__ void k_tile_max(int n, int tr, const int32_t* ptr, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t * (int64_t)tr >= n) return;
+  const int r0 = t * tr, r1 = min(r0 + tr, n);
+  atomicMax(out, ptr[r1] - ptr[r0]);
+}
+
+template <int B, int G, typename V, typename X, bool FAST, class EPI>
+static void launch_tma_f(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+  TmaArgs a{A.n, A.tma_tr, A.tma_ntiles, A.tma_ns, A.tma_stage, A.tma_col_off, A.tma_val_off};
+  const int smem = A.tma_ns * A.tma_stage;
+  if (A.tma_rows) {
+    static int configured_r = 48 * 1024;
+    if (smem > configured_r) {
+      AMG_CK(cudaFuncSetAttribute(k_bsr_tma_rows<B, V, X, FAST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured_r = smem;
+    }
+    k_bsr_tma_rows<B, V, X, FAST, EPI><<<A.tma_grid, 128, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
+    return;
+  }
+  static int configured = 48 * 1024;
+  if (smem > configured) {
+    AMG_CK(cudaFuncSetAttribute(k_bsr_tma<B, G, V, X, FAST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = smem;
+  }
+  k_bsr_tma<B, G, V, X, FAST, EPI><<<A.tma_grid, 256, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+void make_tma_plan(Mat& A, cudaStream_t s) {
+  A.tma_grid = 0;
+  A.tma_rows = false;
+  if (A.n < 2048 || env_int("AMG_NO_TMA", 0)) return;
+  const double bb = (double)A.b * A.b * dtype_size(A.vt) + 4.0;
+  const double row_bytes = std::max(1.0, (double)A.nnz / A.n * bb);
+  // row-per-lane mode for short rows (<= 12 blocks) when a 128-row tile fits a stage
+  const int mode_rows = env_int("AMG_TMA_ROWS", 1) && (double)A.nnz / A.n <= 12.0 && 128 * row_bytes <= 40 * 1024;
+  int tr = 4;
+  while (tr < 256 && tr * 2 * row_bytes <= env_int("AMG_TMA_TILE_BYTES", 16384)) tr *= 2;
+  if (mode_rows) tr = 128;
+  const int ntiles = (int)((A.n + tr - 1) / tr);
+  int* d = nullptr;
+  AMG_CK(cudaMallocAsync((void**)&d, sizeof(int), s));
+  AMG_CK(cudaMemsetAsync(d, 0, sizeof(int), s));
+  k_tile_max<<<grid_for(ntiles, 256), 256, 0, s>>>(A.n, tr, A.ptr, d);
+  AMG_CK_LAUNCH();
+  int mx = 0;
+  AMG_CK(cudaMemcpyAsync(&mx, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AMG_CK(cudaFreeAsync(d, s));
+  AMG_CK(cudaStreamSynchronize(s));
+  auto a16 = [](int64_t v) { return (int)((v + 15) & ~int64_t(15)); };
+  const int pbytes = a16(4LL * (tr + 1) + 32);
+  const int cbytes = a16(4LL * mx + 32);
+  const int64_t vbytes64 = (int64_t)mx * A.b * A.b * dtype_size(A.vt) + 32;
+  if (vbytes64 > 96 * 1024) return;  // pathological rows: direct kernels
+  const int stage = pbytes + cbytes + a16(vbytes64);
+  const int ns = stage <= 40 * 1024 ? 3 : 2;
+  const int budget = 220 * 1024;
+  int per_sm = budget / (ns * stage);
+  if (per_sm > (mode_rows ? 8 : 4)) per_sm = mode_rows ? 8 : 4;
+  if (per_sm < 1) return;
+  A.tma_rows = mode_rows;
+  A.tma_tr = tr;
+  A.tma_ntiles = ntiles;
+  A.tma_ns = ns;
+  A.tma_stage = stage;
+  A.tma_col_off = pbytes;
+  A.tma_val_off = pbytes + cbytes;
+  A.tma_grid = std::min(ntiles, kSMs * per_sm);
+}
+
+template <int B, int G, typename V, typename X, class EPI>
+static void launch_tma(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+  if (A.fast32) launch_tma_f<B, G, V, X, true>(A, x, epi, s);
+  else launch_tma_f<B, G, V, X, false>(A, x, epi, s);
+}
+
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s) {
   if (A.n == 0) return;
@@ -60,12 +145,10 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
           using X = decltype(xx);
           dispatch_t(yt, [&](auto yy) {
             using Y = decltype(yy);
-            static int variant = getenv("AMG_SPMV_V") ? atoi(getenv("AMG_SPMV_V")) : 0;
-            if (variant == 1)
-              k_spmv<B, G, V, X, Y, 1><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-                  A.n, A.ptr, A.col, (const V*)A.val, alpha, (const X*)x, beta, (Y*)y);
+            if (A.tma_grid > 0)
+              launch_tma<B, G, V, X>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
             else
-              k_spmv<B, G, V, X, Y, 0><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
+              k_spmv<B, G, V, X, Y><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
                   A.n, A.ptr, A.col, (const V*)A.val, alpha, (const X*)x, beta, (Y*)y);
           });
         });
@@ -87,8 +170,11 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
         using V = decltype(v);
         dispatch_t(xt, [&](auto xx) {
           using X = decltype(xx);
-          k_residual<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-              A.n, A.ptr, A.col, (const V*)A.val, (const X*)f, (const X*)x, (X*)r);
+          if (A.tma_grid > 0)
+            launch_tma<B, G, V, X>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
+          else
+            k_residual<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
+                A.n, A.ptr, A.col, (const V*)A.val, (const X*)f, (const X*)x, (X*)r);
         });
       });
     });
@@ -109,8 +195,11 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
         using V = decltype(v);
         dispatch_t(xt, [&](auto xx) {
           using X = decltype(xx);
-          k_smooth<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-              A.n, A.ptr, A.col, (const V*)A.val, (const V*)M, (const X*)f, (const X*)x, (X*)xo);
+          if (A.tma_grid > 0)
+            launch_tma<B, G, V, X>(A, (const X*)x, EpiSmooth<B, V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s);
+          else
+            k_smooth<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
+                A.n, A.ptr, A.col, (const V*)A.val, (const V*)M, (const X*)f, (const X*)x, (X*)xo);
         });
       });
     });

@@ -123,3 +123,70 @@ def test_spmv_cfg2_full_size(amg, b):
     assert _relerr(y, ref) <= 1e-5
     y = _run(amg, ptr, col, val, x, 0, 0, 0)
     assert _relerr(y, ref) <= 1e-12
+
+
+# ---- TMA-staged plan path (bsr_plan_create / bsr_plan_spmv) ----
+def _run_plan(amg, ptr, col, val, x, vt, xt, yt, alpha=1.0, beta=0.0, y0=None):
+    tdt = {amg.F32: torch.float32, amg.F64: torch.float64}
+    A = amg.BSR.from_numpy(ptr, col, val, dtype=tdt[vt])
+    P = amg.SpmvPlan(A)
+    xd = torch.as_tensor(x).to("cuda", tdt[xt])
+    n, b = len(ptr) - 1, val.shape[-1]
+    yd = (torch.zeros(n * b, dtype=tdt[yt], device="cuda") if y0 is None
+          else torch.as_tensor(y0).to("cuda", tdt[yt]))
+    P(xd, yd, alpha, beta)
+    torch.cuda.synchronize()
+    return yd.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+@pytest.mark.parametrize("vt,xt,yt", [(0, 0, 0), (1, 0, 0), (1, 1, 1)])
+def test_plan_spmv_random(amg, rng, b, vt, xt, yt):
+    # n >= 2048 so the TMA tiles are used; ragged last tile, empty rows, long rows
+    for n, dens in ((2049, 0.002), (5000, 0.004)):
+        ptr, col, val = random_bsr(rng, n, b, density=dens)
+        x = rng.uniform(-1, 1, n * b)
+        y0 = rng.standard_normal(n * b)
+        for alpha, beta in ((1.0, 0.0), (0.5, -2.0)):
+            y = _run_plan(amg, ptr, col, val, x, vt, xt, yt, alpha, beta, y0)
+            vv = _r32(val) if vt == amg.F32 else val
+            xx = _r32(x) if xt == amg.F32 else x
+            yy = _r32(y0) if yt == amg.F32 else y0
+            ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, alpha, beta, yy)
+            assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7)
+
+
+def test_plan_spmv_empty_rows(amg, rng):
+    n = 4096
+    ptr = np.zeros(n + 1, np.int32)
+    cols = []
+    for i in range(n):
+        c = [] if i % 7 == 3 else sorted(set(rng.integers(0, n, 3).tolist()))
+        cols.extend(c)
+        ptr[i + 1] = ptr[i] + len(c)
+    col = np.array(cols, np.int32)
+    val = rng.standard_normal((len(col), 3, 3))
+    x = rng.standard_normal(3 * n)
+    y = _run_plan(amg, ptr, col, val, x, 1, 0, 0, 1.0, 0.0, np.full(3 * n, np.nan))
+    ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, _r32(val)), x)
+    assert _relerr(y, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("b", [3, 4])
+def test_plan_spmv_cfg2(amg, b):
+    for n in (16, 24):
+        ptr, col, val = gen.matrix(gen.RAND27, n, b)
+        x = gen.rhs(gen.X_UNIFORM, n, b)
+        ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
+        assert _relerr(_run_plan(amg, ptr, col, val, x, 0, 0, 0), ref) <= 1e-12
+        assert _relerr(_run_plan(amg, ptr, col, val, x, 1, 0, 0), ref) <= 1e-5
+
+
+def test_plan_spmv_cfg2_full_size(amg):
+    # BASELINE configs[1] at full size, the bench's launch configuration (plan, 4x4 fp32 x fp64)
+    n, b = 128, 4
+    ptr, col, val = gen.matrix(gen.RAND27, n, b)
+    x = gen.rhs(gen.X_UNIFORM, n, b)
+    ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
+    assert _relerr(_run_plan(amg, ptr, col, val, x, 1, 0, 0), ref) <= 1e-5
+    assert _relerr(_run_plan(amg, ptr, col, val, x, 0, 0, 0), ref) <= 1e-12
