@@ -250,7 +250,7 @@ namespace amgb {
 // blocks is 63 words: odd stride, conflict-free).  No shuffles; the thread owns the
 // whole b-vector of its row.
 template <int B, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(128) k_bsr_tma_rows(TmaArgs a, const int32_t* __restrict__ ptr,
+__global__ void __launch_bounds__(256) k_bsr_tma_rows(TmaArgs a, const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col, const V* __restrict__ val,
                                                       const X* __restrict__ x, EPI epi) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -312,33 +312,31 @@ __global__ void __launch_bounds__(128) k_bsr_tma_rows(TmaArgs a, const int32_t* 
       const int kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
       double acc[B] = {};
       int kb = kb0;
-      // 4 blocks per pass: 4 column reads, 4*B x-gathers in flight before the FMAs
-      for (; kb + 4 <= kb1; kb += 4) {
-        X xv[4][B];
+      // U blocks per pass: U column reads and U*B x-gathers in flight before the FMAs
+      constexpr int U = (B <= 3) ? 8 : 4;
+      for (; kb < kb1; kb += U) {
+        X xv[U][B];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) load_raw<B, false>(x + (int64_t)sc[kb + u] * B, xv[u]);
+        for (int u = 0; u < U; ++u) {
+          if (kb + u < kb1) {
+            load_raw<B, false>(x + (int64_t)sc[kb + u] * B, xv[u]);
+          } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const V* blk = sv + (int64_t)(kb + u) * B * B;
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            V av[B];
-#pragma unroll
-            for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
-            acc[r] += item_dot<B, V, X, FAST>(av, xv[u]);
+            for (int c = 0; c < B; ++c) xv[u][c] = X(0);
           }
         }
-      }
-      for (; kb < kb1; ++kb) {
-        X xv[B];
-        load_raw<B, false>(x + (int64_t)sc[kb] * B, xv);
-        const V* blk = sv + (int64_t)kb * B * B;
 #pragma unroll
-        for (int r = 0; r < B; ++r) {
-          V av[B];
+        for (int u = 0; u < U; ++u) {
+          if (kb + u < kb1) {
+            const V* blk = sv + (int64_t)(kb + u) * B * B;
 #pragma unroll
-          for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
-          acc[r] += item_dot<B, V, X, FAST>(av, xv);
+            for (int r = 0; r < B; ++r) {
+              V av[B];
+#pragma unroll
+              for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
+              acc[r] += item_dot<B, V, X, FAST>(av, xv[u]);
+            }
+          }
         }
       }
 #pragma unroll

@@ -1,0 +1,132 @@
+// comm.cu -- NcclComm and LocalComm (see comm.h).
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "amg.h"
+#include "comm.h"
+#include "common.cuh"
+
+namespace amgb {
+
+#define AMG_NCCL(expr)                                                                      \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess) ::amgb::fail(AMG_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+class NcclComm : public CommBase {
+ public:
+  ncclComm_t comm = nullptr;
+  NcclComm(const void* id128, int n, int r) {
+    nranks = n;
+    rank = r;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    AMG_NCCL(ncclCommInitRank(&comm, n, id, r));
+  }
+  ~NcclComm() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  void allreduce_sum(double* d, int n, cudaStream_t s) override {
+    if (nranks == 1 || n == 0) return;
+    AMG_NCCL(ncclAllReduce(d, d, n, ncclDouble, ncclSum, comm, s));
+  }
+  void allgather_host(const int64_t* mine, int n_each, int64_t* all) override {
+    int64_t* d = nullptr;
+    AMG_CK(cudaMalloc(&d, sizeof(int64_t) * n_each * (nranks + 1)));
+    AMG_CK(cudaMemcpy(d, mine, sizeof(int64_t) * n_each, cudaMemcpyHostToDevice));
+    AMG_NCCL(ncclAllGather(d, d + n_each, n_each, ncclInt64, comm, nullptr));
+    AMG_CK(cudaStreamSynchronize(nullptr));
+    AMG_CK(cudaMemcpy(all, d + n_each, sizeof(int64_t) * n_each * nranks, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  }
+  void group_begin() override { AMG_NCCL(ncclGroupStart()); }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t s) override {
+    AMG_NCCL(ncclSend(buf, bytes, ncclChar, peer, comm, s));
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t s) override {
+    AMG_NCCL(ncclRecv(buf, bytes, ncclChar, peer, comm, s));
+  }
+  void group_end(cudaStream_t) override { AMG_NCCL(ncclGroupEnd()); }
+  void barrier() override {
+    double* d = nullptr;
+    AMG_CK(cudaMalloc(&d, sizeof(double)));
+    AMG_CK(cudaMemset(d, 0, sizeof(double)));
+    AMG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclSum, comm, nullptr));
+    AMG_CK(cudaStreamSynchronize(nullptr));
+    cudaFree(d);
+  }
+};
+
+class LocalComm : public CommBase {
+ public:
+  LocalGroup* g;
+  struct Pending {
+    void* buf;
+    const void* sbuf;
+    size_t bytes;
+    int peer;
+  };
+  std::vector<Pending> sends, recvs;
+  LocalComm(LocalGroup* grp, int r) : g(grp) {
+    nranks = grp->P;
+    rank = r;
+  }
+  void allreduce_sum(double* d, int n, cudaStream_t s) override {
+    if (nranks == 1 || n == 0) return;
+    std::vector<double> mine(n);
+    AMG_CK(cudaMemcpyAsync(mine.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    AMG_CK(cudaStreamSynchronize(s));
+    g->red[rank] = mine;
+    g->barrier();
+    std::vector<double> tot(n, 0.0);
+    for (int r = 0; r < nranks; ++r)  // rank order: deterministic
+      for (int i = 0; i < n; ++i) tot[i] += g->red[r][i];
+    g->barrier();
+    AMG_CK(cudaMemcpyAsync(d, tot.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    AMG_CK(cudaStreamSynchronize(s));
+  }
+  void allgather_host(const int64_t* mine, int n_each, int64_t* all) override {
+    g->gat[rank].assign(mine, mine + n_each);
+    g->barrier();
+    for (int r = 0; r < nranks; ++r) std::memcpy(all + (size_t)r * n_each, g->gat[r].data(), sizeof(int64_t) * n_each);
+    g->barrier();
+  }
+  void group_begin() override {
+    sends.clear();
+    recvs.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t) override { sends.push_back({nullptr, buf, bytes, peer}); }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t) override { recvs.push_back({buf, nullptr, bytes, peer}); }
+  void group_end(cudaStream_t s) override {
+    AMG_CK(cudaStreamSynchronize(s));  // send buffers complete
+    g->mail[rank].clear();
+    for (auto& p : sends) g->mail[rank].push_back({rank, p.peer, p.sbuf, p.bytes});
+    g->barrier();
+    // the k-th recv from peer p matches the k-th send of p to this rank
+    std::vector<int> seen(nranks, 0);
+    for (auto& rv : recvs) {
+      int k = seen[rv.peer]++;
+      int found = -1;
+      for (size_t m = 0, c = 0; m < g->mail[rv.peer].size(); ++m)
+        if (g->mail[rv.peer][m].dst == rank && (int)c++ == k) {
+          found = (int)m;
+          break;
+        }
+      if (found < 0) fail(AMG_ENCCL, "LocalComm: unmatched recv");
+      const auto& msg = g->mail[rv.peer][found];
+      if (msg.bytes != rv.bytes) fail(AMG_ENCCL, "LocalComm: size mismatch");
+      if (rv.bytes) AMG_CK(cudaMemcpyAsync(rv.buf, msg.ptr, rv.bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    AMG_CK(cudaStreamSynchronize(s));
+    g->barrier();  // senders may reuse their buffers after this
+  }
+  void barrier() override { g->barrier(); }
+};
+
+CommBase* make_nccl_comm(const void* id128, int nranks, int rank) { return new NcclComm(id128, nranks, rank); }
+CommBase* make_local_comm(LocalGroup* g, int rank) { return new LocalComm(g, rank); }
+
+}  // namespace amgb

@@ -65,7 +65,7 @@ static void launch_tma_f(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
       AMG_CK(cudaFuncSetAttribute(k_bsr_tma_rows<B, V, X, FAST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       configured_r = smem;
     }
-    k_bsr_tma_rows<B, V, X, FAST, EPI><<<A.tma_grid, 128, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
+    k_bsr_tma_rows<B, V, X, FAST, EPI><<<A.tma_grid, A.tma_tr, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
     return;
   }
   static int configured = 48 * 1024;
@@ -91,7 +91,7 @@ void make_tma_plan(Mat& A, cudaStream_t s) {
   const int mode_rows = env_int("AMG_TMA_ROWS", 1) && (double)A.nnz / A.n <= 12.0 && 128 * row_bytes <= 40 * 1024;
   int tr = 4;
   while (tr < 256 && tr * 2 * row_bytes <= env_int("AMG_TMA_TILE_BYTES", 16384)) tr *= 2;
-  if (mode_rows) tr = 128;
+  if (mode_rows) tr = env_int("AMG_TMA_ROWS_TR", 128);
   const int ntiles = (int)((A.n + tr - 1) / tr);
   int* d = nullptr;
   AMG_CK(cudaMallocAsync((void**)&d, sizeof(int), s));
@@ -108,10 +108,11 @@ void make_tma_plan(Mat& A, cudaStream_t s) {
   const int64_t vbytes64 = (int64_t)mx * A.b * A.b * dtype_size(A.vt) + 32;
   if (vbytes64 > 96 * 1024) return;  // pathological rows: direct kernels
   const int stage = pbytes + cbytes + a16(vbytes64);
-  const int ns = stage <= 40 * 1024 ? 3 : 2;
+  const int ns = env_int("AMG_TMA_NS", (mode_rows || stage > 40 * 1024) ? 2 : 3);
   const int budget = 220 * 1024;
   int per_sm = budget / (ns * stage);
-  if (per_sm > (mode_rows ? 8 : 4)) per_sm = mode_rows ? 8 : 4;
+  const int cap = mode_rows ? std::min(32, 2048 / tr) : 4;
+  if (per_sm > cap) per_sm = cap;
   if (per_sm < 1) return;
   A.tma_rows = mode_rows;
   A.tma_tr = tr;
