@@ -173,6 +173,13 @@ int amg_comm_init(const void* id128 /* host */, int32_t nranks, int32_t rank,
 int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_block_rows,
                    struct amg_comm* c, const amg_params* p, void* stream, struct amg_handle** out);
 void amg_comm_destroy(struct amg_comm* c);
+/* Thread-emulated communicator (testing the distributed path on ONE device): a group of
+ * nranks host threads of this process, each with its own stream; exchanges are device
+ * copies with host barriers (no kernel ever waits on another rank), reductions are
+ * summed in rank order.  Same semantics as the NCCL communicator. */
+int amg_local_group_create(int32_t nranks, void** group /* host out */);
+void amg_local_group_destroy(void* group);
+int amg_comm_init_local(void* group, int32_t rank, struct amg_comm** out);
 
 #ifdef __cplusplus
 }

@@ -62,7 +62,8 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_level_aggregates", "amg_schur_export", "amg_vcycle", "amg_device_bytes",
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
-           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy"]
+           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy",
+           "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local"]
 
 _lib = None
 
@@ -97,6 +98,9 @@ def lib():
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
             "amg_comm_destroy": (None, [P]),
             "amg_kernel_launches": (i64, []),
+            "amg_local_group_create": (i32, [i32, P]),
+            "amg_local_group_destroy": (None, [P]),
+            "amg_comm_init_local": (i32, [P, i32, P]),
             "bsr_plan_create": (i32, [P, P, P]),
             "bsr_plan_spmv": (i32, [P, dbl, P, i32, dbl, P, i32, P]),
             "bsr_plan_destroy": (None, [P]),
@@ -352,8 +356,33 @@ class Solver:
         return int(lib().amg_device_bytes(self.h))
 
 
+class LocalGroup:
+    """amg_local_group_create: P ranks as P threads of this process on one device."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        _check(lib().amg_local_group_create(nranks, ctypes.byref(h)), "amg_local_group_create")
+        self.h = h
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.amg_local_group_destroy(self.h)
+            self.h = None
+
+
 class Comm:
-    """NCCL communicator for amg_setup_dist (one process per GPU)."""
+    """NCCL communicator for amg_setup_dist (one process per GPU), or with
+    ``Comm.local(group, rank)`` the thread-emulated one."""
+
+    @classmethod
+    def local(cls, group: "LocalGroup", rank: int):
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        _check(lib().amg_comm_init_local(group.h, rank, ctypes.byref(h)), "amg_comm_init_local")
+        self.h = h
+        self.group = group
+        return self
 
     def __init__(self, rank: int, nranks: int, pg=None):
         torch = _torch()

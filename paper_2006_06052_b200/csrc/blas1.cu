@@ -2,6 +2,7 @@
 // fixed grid for a given length, fixed-order finalisation), multi-dot / multi-axpy
 // for the CGS2 Arnoldi step, linear combinations, and the flexible-GMRES update.
 #include "blas1.h"
+#include "comm.h"
 #include "prof.h"
 
 namespace amgb {
@@ -184,6 +185,20 @@ __global__ void k_scale_by_inv(int64_t n, const double* __restrict__ x, const do
   for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) y[i] = x[i] * inv;
 }
 
+__global__ void k_sqrt_vec(double* d, int n) {
+  if (threadIdx.x < n) d[threadIdx.x] = sqrt(d[threadIdx.x]);
+}
+
+// distributed: the partials are local; sum over ranks before the square root
+inline void finalize_global(CommBase* comm, double* out, int k, bool sqrt_out, cudaStream_t s) {
+  if (!comm) return;
+  comm->allreduce_sum(out, k, s);
+  if (sqrt_out) {
+    k_sqrt_vec<<<1, 32, 0, s>>>(out, k);
+    AMG_CK_LAUNCH();
+  }
+}
+
 inline unsigned ew_grid(int64_t n) {
   int64_t g = (n + kT - 1) / kT;
   if (g > kSMs * 16) g = kSMs * 16;
@@ -193,7 +208,7 @@ inline unsigned ew_grid(int64_t n) {
 }  // namespace
 
 void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double* partials, double* out, bool sqrt_out,
-                cudaStream_t s) {
+                cudaStream_t s, CommBase* comm) {
   const int nb = nblocks_for(n);
   ProfScope ps_(prof_name("dot", 1, at, bt), (double)n * (a == b ? dtype_size(at) : dtype_size(at) + dtype_size(bt)), s);
   if (at == AMG_F64 && bt == AMG_F64)
@@ -206,8 +221,9 @@ void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double*
     k_dot<float, float><<<nb, kT, 0, s>>>(n, (const float*)a, (const float*)b, partials, nb);
   AMG_CK_LAUNCH();
   ++g_launches;
-  k_finalize<<<1, kT, 0, s>>>(1, partials, nb, out, sqrt_out ? 1 : 0);
+  k_finalize<<<1, kT, 0, s>>>(1, partials, nb, out, (sqrt_out && !comm) ? 1 : 0);
   AMG_CK_LAUNCH();
+  finalize_global(comm, out, 1, sqrt_out, s);
 }
 
 void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* partials, double* out, cudaStream_t s) {
@@ -221,7 +237,7 @@ void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* pa
 }
 
 void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, const double* w, double* partials,
-                        double* out, cudaStream_t s) {
+                        double* out, cudaStream_t s, CommBase* comm) {
   const int nb = nblocks_for(n);
   ProfScope ps_(prof_name("mdot", k, AMG_F64, -1), 8.0 * n * (k + 1), s);
   k_mdot_scaled<<<nb, kT, 0, s>>>(n, k, V, sc, w, partials, nb);
@@ -229,18 +245,20 @@ void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, co
   ++g_launches;
   k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
   AMG_CK_LAUNCH();
+  finalize_global(comm, out, k, false, s);
 }
 
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
-                       double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s) {
+                       double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s, CommBase* comm) {
   const int nb = nblocks_for(n);
   ProfScope ps_(prof_name(dot_next ? "cgs_update_dot" : "cgs_update_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
   if (dot_next) k_cgs_update<true><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
   else k_cgs_update<false><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
   AMG_CK_LAUNCH();
   ++g_launches;
-  k_finalize<<<1, kT, 0, s>>>(dot_next ? k : 1, partials, nb, out, dot_next ? 0 : 1);
+  k_finalize<<<1, kT, 0, s>>>(dot_next ? k : 1, partials, nb, out, (dot_next || comm) ? 0 : 1);
   AMG_CK_LAUNCH();
+  finalize_global(comm, out, dot_next ? k : 1, !dot_next, s);
 }
 
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s) {

@@ -27,14 +27,22 @@ struct Ctx {
     AMG_CK(cudaStreamSynchronize(s));
   }
   void dot(const double* a, const double* b, int slot, bool sq = false) {
-    launch_dot(N, a, AMG_F64, b, AMG_F64, h.partials, h.dscal + slot, sq, s);
+    launch_dot(N, a, AMG_F64, b, AMG_F64, h.partials, h.dscal + slot, sq, s, h.comm);
     bytes += (a == b ? 8.0 : 16.0) * N;
   }
+  // x: a vector with ghost space (workspace / Z basis); ghosts exchanged first
   void spmv(const void* x, int xt, double* y) {
+    halo_exchange(h, h.halo0, const_cast<void*>(x), xt, h.b, s);
     launch_spmv(h.A, 1.0, x, xt, 0.0, y, AMG_F64, s);
     bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0);
   }
+  // x: the caller's iterate (no ghost space): copied into x_ext when distributed
   void residual(const double* b, const double* x, double* r) {
+    if (h.comm) {
+      AMG_CK(cudaMemcpyAsync(h.x_ext, x, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+      halo_exchange(h, h.halo0, h.x_ext, AMG_F64, h.b, s);
+      x = h.x_ext;
+    }
     launch_residual(h.A, b, x, r, AMG_F64, s);
     bytes += h.alg_bytes_spmv + 8.0 * N;
   }
@@ -247,7 +255,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   double* sc = h.dscal + 128;  // s_j
   // r = b - A x straight into V_0
   c.residual(b, x, h.V[0]);
-  launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s);
+  launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s, h.comm);
   c.bytes += 8.0 * N;
   k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
   AMG_CK_LAUNCH();
@@ -270,9 +278,9 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
       c.spmv(h.Z[j], h.zt, w);
       PtrList Vl{};
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
-      launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s);                 // h1 = v^T w
-      launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s);   // w -= v h1; h2 = v^T w
-      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s);  // w -= v h2; ||w||
+      launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);                 // h1 = v^T w
+      launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s, h.comm);   // w -= v h1; h2 = v^T w
+      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s, h.comm);  // w -= v h2; ||w||
       k_set_inv<<<1, 1, 0, c.s>>>(sc + j + 1, h.dscal + 64);
       AMG_CK_LAUNCH();
       ++g_launches;
@@ -317,7 +325,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     launch_zupdate(N, k, Zl, h.zt, h.dscal + 96, x, c.s);
     c.bytes += N * (16.0 + sx * k);
     c.residual(b, x, h.V[0]);  // true residual = next cycle's V_0
-    launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s);
+    launch_dot(N, h.V[0], AMG_F64, h.V[0], AMG_F64, h.partials, h.dscal + 64, true, c.s, h.comm);
     k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
     AMG_CK_LAUNCH();
     ++g_launches;
@@ -335,7 +343,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
 int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t s, amg_report* rep) {
   Ctx c(h, s);
   // ||b||; ||b|| = 0 -> x = 0, converged, relres 0
-  launch_dot(c.N, b, AMG_F64, b, AMG_F64, h.partials, h.dscal, true, s);
+  launch_dot(c.N, b, AMG_F64, b, AMG_F64, h.partials, h.dscal, true, s, h.comm);
   c.read(1);
   const double nb = h.hscal[0];
   if (rep) rep->levels = h.amg_active ? (int)h.lv.size() + 1 : 0;

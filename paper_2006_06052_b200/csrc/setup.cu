@@ -720,7 +720,7 @@ Mat solve_copy(Handle& h, const Mat& M64, cudaStream_t s) {
 }  // namespace
 
 // ---------------------------------------------------------------- the setup driver
-void setup_build(Handle& h, const Mat& A64, int nparts, cudaStream_t s) {
+void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0, cudaStream_t s) {
   SetupCtx c;
   c.s = s;
   c.err = c.tmp.alloc_n<int>(1);
@@ -769,8 +769,10 @@ void setup_build(Handle& h, const Mat& A64, int nparts, cudaStream_t s) {
   h.bh = Amg.b;
 
   // slab of every row (rank-local aggregation)
-  std::vector<int64_t> bounds(nparts + 1);
-  for (int r = 0; r <= nparts; ++r) bounds[r] = (int64_t)r * Amg.n / nparts;
+  std::vector<int64_t> bounds = bounds0;
+  const int nparts = (int)bounds.size() - 1;
+  h.lbounds.clear();
+  h.lbounds.push_back(bounds);
 
   Mat A = Amg;
   std::vector<Mat> lvA, lvP, lvR;
@@ -849,13 +851,18 @@ void setup_build(Handle& h, const Mat& A64, int nparts, cudaStream_t s) {
     AMG_CK_LAUNCH();
     const int64_t nc = scan(c, rid, n);
     // coarse slab bounds = number of roots before each slab boundary
+    std::vector<int64_t> cb(nparts + 1, 0);
     if (nparts > 1) {
       std::vector<int32_t> hr(n + 1);
       AMG_CK(cudaMemcpyAsync(hr.data(), rid, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
       AMG_CK(cudaStreamSynchronize(s));
-      for (int r = 0; r <= nparts; ++r) bounds[r] = hr[bounds[r]];
+      for (int r = 0; r <= nparts; ++r) cb[r] = hr[bounds[r]];
+    } else {
+      cb[1] = nc;
     }
     if (nc == 0 || nc >= n) break;
+    bounds = cb;
+    h.lbounds.push_back(bounds);
     int32_t* agg1 = c.tmp.alloc_n<int32_t>(n);
     int32_t* agg = c.tmp.alloc_n<int32_t>(n);
     k_pass1<<<grid_for(n, kT), kT, 0, s>>>(n, aptr, adj, state, rid, agg1);

@@ -13,24 +13,26 @@ void set_last_error(const std::string& s);
 
 Handle::~Handle() {
   if (pc_graph) cudaGraphExecDestroy(pc_graph);
+  for (Level& L : lv)
+    if (L.halo.send_buf) L.halo.send_buf = nullptr;  // arena-owned
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (hscal) cudaFreeHost(hscal);
 }
 
-namespace {
-
 void alloc_workspace(Handle& h, cudaStream_t s) {
   const int64_t N = (int64_t)h.n * h.b;
+  const int64_t Nx = (int64_t)(h.n + h.halo0.nghost) * h.b;  // SpMV inputs carry ghosts
   const int nv = 8;
-  for (int i = 0; i < nv; ++i) h.vec.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+  for (int i = 0; i < nv; ++i) h.vec.push_back(h.arena.alloc_n<double>(std::max<int64_t>(Nx, 1)));
+  if (h.comm) h.x_ext = h.arena.alloc_n<double>(std::max<int64_t>(Nx, 1));
   if (h.p.solver == AMG_GMRES) {
     const int m = h.p.gmres_m;
     // Z is stored in the preconditioner's output precision: the fp32 V-cycle output is
     // exactly representable in fp32, so storing it narrow is lossless.
     h.zt = (h.amg_active && h.xt == AMG_F32) ? AMG_F32 : AMG_F64;
     for (int i = 0; i <= m; ++i) h.V.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
-    for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(N, 1) * dtype_size(h.zt)));
+    for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
   }
   h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32);
   h.dscal = h.arena.alloc_n<double>(256);
@@ -38,12 +40,15 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
   if (h.schur) {
     const size_t xs = dtype_size(h.xt);
     h.rp = h.arena.alloc(std::max(h.n, 1) * xs);
-    h.pp = h.arena.alloc(std::max(h.n, 1) * xs);
+    h.pp = h.arena.alloc(std::max(h.n + h.halo0.nghost, 1) * xs);
   }
   AMG_CK(cudaEventCreate(&h.ev0));
   AMG_CK(cudaEventCreate(&h.ev1));
+  (void)N;
   (void)s;
 }
+
+namespace {
 
 double mat_bytes(const Mat& A, int vt) {
   return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(vt)) + 4.0 * (A.n + 1);
@@ -51,10 +56,8 @@ double mat_bytes(const Mat& A, int vt) {
 
 }  // namespace
 
-int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle** out, int nparts) {
-  int rc = validate_bsr(A, true);
-  if (rc != AMG_OK) return rc;
-  if (!p || !out) return AMG_EINVAL;
+int check_params(const amg_params* p) {
+  if (!p) return AMG_EINVAL;
   if (p->solver < AMG_CG || p->solver > AMG_GMRES) return AMG_EINVAL;
   if (p->precond < AMG_PC_AMG || p->precond > AMG_PC_NONE) return AMG_EINVAL;
   if (p->solver == AMG_GMRES && (p->gmres_m < 1 || p->gmres_m > 31)) return AMG_EINVAL;
@@ -62,20 +65,23 @@ int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle**
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;
+  return AMG_OK;
+}
+
+Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s) {
   auto t0 = std::chrono::steady_clock::now();
   Handle* h = new Handle;
   try {
     h->p = *p;
     h->vt = p->hier_dtype;
     h->xt = p->vcycle_vec_dtype;
-    h->n = A->n_block_rows;
-    h->b = A->block_size;
+    h->n = src.n;
+    h->b = src.b;
     h->schur = p->precond == AMG_PC_SCHUR;
     h->pc = p->schur_p_component;
     h->amg_active = p->precond != AMG_PC_NONE;
     if (h->schur && (h->pc < 0 || h->pc >= h->b)) fail(AMG_EINVAL, "schur_p_component out of range");
     // library-owned fp64 copy of A (setup in own structures, then moved)
-    Mat src = view_of(A);
     Mat& M = h->A;
     M = src;
     M.vt = AMG_F64;
@@ -89,7 +95,7 @@ int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle**
     }
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
     make_tma_plan(M, s);
-    if (h->amg_active) setup_build(*h, M, nparts, s);
+    if (h->amg_active) setup_build(*h, M, bounds, s);
     alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));
@@ -98,7 +104,16 @@ int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle**
     throw;
   }
   h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  *out = h;
+  return h;
+}
+
+int setup_common(const amg_bsr* A, const amg_params* p, cudaStream_t s, Handle** out) {
+  int rc = validate_bsr(A, true);
+  if (rc != AMG_OK) return rc;
+  if (!out) return AMG_EINVAL;
+  rc = check_params(p);
+  if (rc != AMG_OK) return rc;
+  *out = build_handle(view_of(A), p, {0, (int64_t)A->n_block_rows}, s);
   return AMG_OK;
 }
 
@@ -126,7 +141,7 @@ int amg_setup(const amg_bsr* A, const amg_params* p, void* stream, struct amg_ha
   AMG_GUARD_BEGIN
   if (!A || !p || !out) return AMG_EINVAL;
   Handle* h = nullptr;
-  int rc = setup_common(A, p, (cudaStream_t)stream, &h, 1);
+  int rc = setup_common(A, p, (cudaStream_t)stream, &h);
   if (rc != AMG_OK) return rc;
   *out = reinterpret_cast<amg_handle*>(h);
   return AMG_OK;
@@ -225,6 +240,7 @@ int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_
   Handle* h = reinterpret_cast<Handle*>(hh);
   if (!h || !val || !h->amg_active || level < 0 || (size_t)level > h->lv.size()) return AMG_EINVAL;
   const bool coarsest = (size_t)level == h->lv.size();
+  if (coarsest && !h->coarse.A.ptr) return AMG_EINVAL;  // distributed: coarsest not kept
   if (which == 3) {
     if (coarsest) return AMG_EINVAL;
     const Level& L = h->lv[level];

@@ -4,14 +4,28 @@
 #include <vector>
 
 #include "blas1.h"
+#include "comm.h"
 #include "common.cuh"
 
 struct ncclComm;
 
 namespace amgb {
 
+// Ghost exchange plan of one row-distributed square matrix.  Local
+// columns are [0, nloc); ghost column g lives at nloc + g, ghosts sorted by global index
+// (hence grouped by owner rank).  Vectors read by the matrix carry (nloc + nghost) blocks.
+struct Halo {
+  int nloc = 0, nghost = 0;
+  std::vector<int> peers;
+  std::vector<int> send_cnt, send_off, recv_cnt, recv_off;  // per peer, in blocks
+  int32_t* send_idx = nullptr;  // device [total_send]: local rows to pack
+  int total_send = 0;
+  void* send_buf = nullptr;     // device, total_send * 4 doubles
+};
+
 struct Level {
   Mat A, P, R;                // solve copies, values in hier dtype
+  Halo halo;                  // distributed: ghost plan of A
   void* M = nullptr;          // smoother blocks [n][b][b], hier dtype
   int32_t* agg = nullptr;     // aggregates (device) [n], -1 = isolated
   int32_t nc = 0;
@@ -19,6 +33,9 @@ struct Level {
 };
 
 struct Coarse {
+  // distributed: the coarsest level is replicated; rank r owns block rows
+  // [off[r], off[r] + cnt[r]) of the coarse right-hand side (allgathered before the GEMV)
+  std::vector<int64_t> cnt, off;
   int32_t N = 0;              // scalar unknowns of the coarsest level
   int32_t n = 0, b = 0;
   void* inv = nullptr;        // dense explicit inverse [N][N], hier dtype
@@ -26,7 +43,6 @@ struct Coarse {
   Mat A;                      // the coarsest matrix (solve copy, for export)
 };
 
-struct DistInfo;              // dist.cu
 
 struct Handle {
   amg_params p{};
@@ -64,13 +80,26 @@ struct Handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double setup_s = 0.0;
   double alg_bytes_precond = 0.0, alg_bytes_spmv = 0.0;
-  DistInfo* dist = nullptr;
+  // distributed (amg_setup_dist): communicator, outer ghost plan, slab bounds per level
+  CommBase* comm = nullptr;
+  Halo halo0;
+  double* x_ext = nullptr;         // fp64 copy of the iterate with ghost space
+  int64_t row_lo = 0;
+  std::vector<std::vector<int64_t>> lbounds;
   Arena arena;
   ~Handle();
 };
 
 // setup.cu
-void setup_build(Handle& h, const Mat& A64 /* device fp64 copy owned by h */, int nparts, cudaStream_t s);
+void setup_build(Handle& h, const Mat& A64 /* device fp64 copy owned by h */, const std::vector<int64_t>& bounds,
+                 cudaStream_t s);
+void alloc_workspace(Handle& h, cudaStream_t s);
+// solver.cu: full single-device build on a device matrix view with slab bounds
+Handle* build_handle(const Mat& view, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s);
+// dist.cu
+void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_t s);
+void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s);
+void coarse_allgather(Handle& h, cudaStream_t s);
 // vcycle.cu
 // V-cycle from level `level` on that level's f buffer; returns the buffer holding x
 void* vcycle_run(Handle& h, size_t level, cudaStream_t s);

@@ -16,6 +16,7 @@ void* level0_f(Handle& h) { return h.lv.empty() ? h.coarse.f : h.lv[0].f; }
 void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   const int xt = h.xt, vt = h.vt;
   if (l == h.lv.size()) {
+    coarse_allgather(h, s);  // distributed: the coarsest level is replicated
     launch_dense_gemv(h.coarse.N, h.coarse.inv, vt, h.coarse.f, h.coarse.x, xt, s);  // K8
     return h.coarse.x;
   }
@@ -24,15 +25,21 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   void* t = L.t;
   launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
   for (int k = 1; k < h.p.npre; ++k) {
+    halo_exchange(h, L.halo, x, xt, L.A.b, s);
     launch_smooth(L.A, L.M, L.f, x, t, xt, s);
     std::swap(x, t);
   }
+  halo_exchange(h, L.halo, x, xt, L.A.b, s);
   launch_residual(L.A, L.f, x, L.r, xt, s);  // K4b: r = f - A x
-  void* fc = (l + 1 < h.lv.size()) ? h.lv[l + 1].f : h.coarse.f;
+  void* fc = (l + 1 < h.lv.size()) ? h.lv[l + 1].f
+                                   : (void*)((char*)h.coarse.f + (h.comm ? h.coarse.off[h.comm->rank] * h.coarse.b *
+                                                                              dtype_size(xt)
+                                                                        : 0));
   launch_spmv(L.R, 1.0, L.r, xt, 0.0, fc, xt, s);  // K6: f_c = R r
   void* xc = vcycle_run(h, l + 1, s);
   launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
   for (int k = 0; k < h.p.npost; ++k) {          // K5: post-smooth (double-buffered)
+    halo_exchange(h, L.halo, x, xt, L.A.b, s);
     launch_smooth(L.A, L.M, L.f, x, t, xt, s);
     std::swap(x, t);
   }
@@ -57,7 +64,9 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   }
   launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s);                                 // K9
   void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
+  halo_exchange(h, h.halo0, us, h.xt, h.nu, s);
   launch_schur_p(h.n, h.nu, h.A.ptr, h.A.col, h.Bv, h.mS, h.vt, h.rp, us, h.pp, h.xt, h.A.G, s);  // K10
+  halo_exchange(h, h.halo0, h.pp, h.xt, 1, s);
   launch_schur_u(h.n, h.nu, h.A.ptr, h.A.col, h.BTv, h.vt, f0, h.pp, f0, h.xt, h.A.G, s);    // K11 (in place)
   void* u = vcycle_run(h, 0, s);                                                               // u = V(r_u')
   launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
