@@ -226,7 +226,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.n or gen.CONFIGS[args.cfg]["n"]
     nrows = n ** 3
-    r0, r1 = rank * nrows // world, (rank + 1) * nrows // world
+    bd = amg.slab_bounds(nrows, world)
+    r0, r1 = bd[rank], bd[rank + 1]
     t0 = time.perf_counter()
     ptr, col, val, bvec = make_problem(args.cfg, n, r0, r1)
     t_gen = time.perf_counter() - t0

@@ -356,6 +356,32 @@ class Solver:
         return int(lib().amg_device_bytes(self.h))
 
 
+def broadcast_unique_id(rank: int, nranks: int, pg=None, make=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL unique id (amg_comm_unique_id), torch.distributed
+    broadcasts it (any backend: nccl, or gloo on CPU)."""
+    if rank == 0:
+        if make is not None:
+            raw = make()
+        else:
+            uid = (ctypes.c_ubyte * 128)()
+            _check(lib().amg_comm_unique_id(uid), "amg_comm_unique_id")
+            raw = bytes(uid)
+    else:
+        raw = None
+    if nranks > 1:
+        import torch.distributed as dist
+        obj = [raw]
+        dist.broadcast_object_list(obj, src=0, group=pg)
+        raw = obj[0]
+    assert isinstance(raw, bytes) and len(raw) == 128
+    return raw
+
+
+def slab_bounds(n_rows: int, nranks: int):
+    """Contiguous block-row slabs (z-slabs for the x-fastest grid ordering)."""
+    return [r * n_rows // nranks for r in range(nranks + 1)]
+
+
 class LocalGroup:
     """amg_local_group_create: P ranks as P threads of this process on one device."""
 
@@ -385,18 +411,8 @@ class Comm:
         return self
 
     def __init__(self, rank: int, nranks: int, pg=None):
-        torch = _torch()
-        import torch.distributed as dist
-        uid = (ctypes.c_ubyte * 128)()
-        if rank == 0:
-            _check(lib().amg_comm_unique_id(uid), "amg_comm_unique_id")
-        t = torch.tensor(bytearray(uid), dtype=torch.uint8)
-        if nranks > 1:
-            obj = [bytes(t.tolist())]
-            dist.broadcast_object_list(obj, src=0, group=pg)
-            t = torch.tensor(bytearray(obj[0]), dtype=torch.uint8)
-        for i in range(128):
-            uid[i] = int(t[i])
+        raw = broadcast_unique_id(rank, nranks, pg)
+        uid = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
         h = ctypes.c_void_p()
         _check(lib().amg_comm_init(uid, nranks, rank, ctypes.byref(h)), "amg_comm_init")
         self.h = h

@@ -298,51 +298,85 @@ __global__ void __launch_bounds__(256) k_bsr_tma_rows(TmaArgs a, const int32_t* 
       nk1 = __ldg(ptr + min(t * a.tr + a.tr, a.n));
     }
   }
-  for (int i = 0; i < my_tiles; ++i) {
+  // software pipeline: while tile i is computed, the x gathers of this thread's row of
+  // tile i+1 are already in flight (tile i+1 landed: ns >= 3 stages)
+  constexpr int U = (B <= 3) ? 8 : 4;
+  auto tile_info = [&](int i, const int32_t*& sp, const int32_t*& sc, const V*& sv, int& k0, int& nr, int& R0) {
     const int s = i % a.ns;
-    mbar_wait(&full[s], (unsigned)((i / a.ns) & 1));
-    const int t = t_begin + i;
-    const int R0 = t * a.tr, nr = min(a.tr, a.n - R0);
     const unsigned char* st = smem + (size_t)s * a.stage_bytes;
-    const int32_t* sp = reinterpret_cast<const int32_t*>(st + meta[s][0]);
-    const int32_t* sc = reinterpret_cast<const int32_t*>(st + a.col_off + meta[s][1]);
-    const V* sv = reinterpret_cast<const V*>(st + a.val_off + meta[s][2]);
-    const int k0 = meta[s][3];
-    for (int lr = tid; lr < nr; lr += blockDim.x) {
+    sp = reinterpret_cast<const int32_t*>(st + meta[s][0]);
+    sc = reinterpret_cast<const int32_t*>(st + a.col_off + meta[s][1]);
+    sv = reinterpret_cast<const V*>(st + a.val_off + meta[s][2]);
+    k0 = meta[s][3];
+    R0 = (t_begin + i) * a.tr;
+    nr = min(a.tr, a.n - R0);
+  };
+  auto prefetch = [&](int i, X (&xb)[U][B]) {
+    const int32_t *sp, *sc;
+    const V* sv;
+    int k0, nr, R0;
+    tile_info(i, sp, sc, sv, k0, nr, R0);
+    const int lr = tid;
+    int kb0 = 0, kb1 = 0;
+    if (lr < nr) kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kb0 + u < kb1) {
+        load_raw<B, false>(x + (int64_t)sc[kb0 + u] * B, xb[u]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < B; ++c) xb[u][c] = X(0);
+      }
+    }
+  };
+  X xa[U][B], xb[U][B];
+  if (my_tiles > 0) {
+    mbar_wait(&full[0], 0u);
+    prefetch(0, xa);
+  }
+  for (int i = 0; i < my_tiles; ++i) {
+    if (i + 1 < my_tiles) {
+      mbar_wait(&full[(i + 1) % a.ns], (unsigned)(((i + 1) / a.ns) & 1));
+      prefetch(i + 1, xb);
+    }
+    const int32_t *sp, *sc;
+    const V* sv;
+    int k0, nr, R0;
+    tile_info(i, sp, sc, sv, k0, nr, R0);
+    const int lr = tid;
+    if (lr < nr) {
       const int kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
       double acc[B] = {};
-      int kb = kb0;
-      // U blocks per pass: U column reads and U*B x-gathers in flight before the FMAs
-      constexpr int U = (B <= 3) ? 8 : 4;
-      for (; kb < kb1; kb += U) {
-        X xv[U][B];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (kb + u < kb1) {
-            load_raw<B, false>(x + (int64_t)sc[kb + u] * B, xv[u]);
-          } else {
+      for (int u = 0; u < U; ++u) {
+        if (kb0 + u < kb1) {
+          const V* blk = sv + (int64_t)(kb0 + u) * B * B;
 #pragma unroll
-            for (int c = 0; c < B; ++c) xv[u][c] = X(0);
+          for (int r = 0; r < B; ++r) {
+            V av[B];
+#pragma unroll
+            for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
+            acc[r] += item_dot<B, V, X, FAST>(av, xa[u]);
           }
         }
+      }
+      for (int kb = kb0 + U; kb < kb1; ++kb) {  // long rows: the rest loaded in place
+        X xv[B];
+        load_raw<B, false>(x + (int64_t)sc[kb] * B, xv);
+        const V* blk = sv + (int64_t)kb * B * B;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (kb + u < kb1) {
-            const V* blk = sv + (int64_t)(kb + u) * B * B;
+        for (int r = 0; r < B; ++r) {
+          V av[B];
 #pragma unroll
-            for (int r = 0; r < B; ++r) {
-              V av[B];
-#pragma unroll
-              for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
-              acc[r] += item_dot<B, V, X, FAST>(av, xv[u]);
-            }
-          }
+          for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
+          acc[r] += item_dot<B, V, X, FAST>(av, xv);
         }
       }
 #pragma unroll
       for (int c = 0; c < B; ++c) epi(R0 + lr, c, acc);
     }
     __syncthreads();
+    const int s = i % a.ns;
     if (tid == 0 && i + a.ns < my_tiles) {
       issue(i + a.ns, s, nk0, nk1);
       if (i + a.ns + 1 < my_tiles) {
@@ -351,6 +385,10 @@ __global__ void __launch_bounds__(256) k_bsr_tma_rows(TmaArgs a, const int32_t* 
         nk1 = __ldg(ptr + min(tn * a.tr + a.tr, a.n));
       }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < B; ++c) xa[u][c] = xb[u][c];
   }
 }
 

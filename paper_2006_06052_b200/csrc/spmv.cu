@@ -85,6 +85,7 @@ void make_tma_plan(Mat& A, cudaStream_t s) {
   A.tma_grid = 0;
   A.tma_rows = false;
   if (A.n < 2048 || env_int("AMG_NO_TMA", 0)) return;
+  if (A.vt == AMG_F64 && !env_int("AMG_TMA_F64", 0)) return;  // direct kernels stream fp64 blocks at ~95 %
   const double bb = (double)A.b * A.b * dtype_size(A.vt) + 4.0;
   const double row_bytes = std::max(1.0, (double)A.nnz / A.n * bb);
   // row-per-lane mode for short rows (<= 12 blocks) when a 128-row tile fits a stage
@@ -108,7 +109,7 @@ void make_tma_plan(Mat& A, cudaStream_t s) {
   const int64_t vbytes64 = (int64_t)mx * A.b * A.b * dtype_size(A.vt) + 32;
   if (vbytes64 > 96 * 1024) return;  // pathological rows: direct kernels
   const int stage = pbytes + cbytes + a16(vbytes64);
-  const int ns = env_int("AMG_TMA_NS", (mode_rows || stage > 40 * 1024) ? 2 : 3);
+  const int ns = env_int("AMG_TMA_NS", mode_rows ? 3 : (stage > 40 * 1024 ? 2 : 3));
   const int budget = 220 * 1024;
   int per_sm = budget / (ns * stage);
   const int cap = mode_rows ? std::min(32, 2048 / tr) : 4;
