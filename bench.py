@@ -258,10 +258,12 @@ def main():
     l0 = amg.kernel_launches()
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off: timed region only
         e0.record(stream)
         reps = [step() for _ in range(args.steps)]
         e1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     launches = (amg.kernel_launches() - l0)
     ms = e0.elapsed_time(e1) / args.steps
     if dist:

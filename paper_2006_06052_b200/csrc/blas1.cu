@@ -5,6 +5,8 @@
 #include "comm.h"
 #include "prof.h"
 
+#include <algorithm>
+
 namespace amgb {
 
 namespace {
@@ -48,76 +50,149 @@ __global__ void __launch_bounds__(kT) k_dot(int64_t n, const TA* __restrict__ a,
   block_reduce_store<1>(acc, 1, partials, nblk);
 }
 
-// acc[j] = sum_i V_j[i] w[i], j < k <= 32
-__global__ void __launch_bounds__(kT) k_mdot(int64_t n, int k, PtrList V, const double* __restrict__ w,
-                                             double* partials, int nblk) {
-  double acc[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const double wi = w[i];
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < k) acc[j] = fma(V.p[j][i], wi, acc[j]);
-  }
-  block_reduce_store<32>(acc, k, partials, nblk);
-}
+// ---- multi-vector kernels of the CGS2 Arnoldi step (flexible GMRES) ----
+// K (the number of basis vectors, 1..32) is a template parameter: every loop over the
+// basis unrolls without predication and the thread's K values of V stay in registers
+// between the update and the dot of the same pass (no L1 re-read).  Each thread handles
+// U elements per grid-stride step (U loads of every vector in flight for small K).  The
+// grid is persistent (occupancy x 148 SMs); block partials are reduced by the LAST block
+// to finish (ticket), in a fixed order -- deterministic, and no second launch.
+constexpr int kTM = 128;
 
-// CGS2 fused update (flexible GMRES).  Basis vectors are stored
-// unnormalised with a scale s_j (v_j = s_j V_j): w_out = w - sum_j c_j s_j V_j, and in the
-// same pass either the next Gram-Schmidt coefficients acc_j = s_j V_j . w_out (DOT) or
-// ||w_out||^2 (acc_0).  V_j[i] is re-read from L1 in the second loop.
-template <bool DOT>
-__global__ void __launch_bounds__(kT) k_cgs_update(int64_t n, int k, PtrList V, const double* __restrict__ sc,
-                                                   const double* __restrict__ coef, const double* w,
-                                                   double* w_out, double* partials, int nblk) {
-  __shared__ double c[32], sv[32];
-  if (threadIdx.x < k) {
-    sv[threadIdx.x] = sc[threadIdx.x];
-    c[threadIdx.x] = coef[threadIdx.x] * sc[threadIdx.x];
-  }
-  __syncthreads();
-  double acc[32];
+template <int K>
+constexpr int cgs_unroll() { return K <= 2 ? 8 : (K <= 4 ? 4 : (K <= 10 ? 2 : 1)); }
+
+// acc[j] (j < kout) of every thread -> partials[j * gridDim.x + block]; the last block sums
+// the gridDim.x partials of each output in a fixed order: out[j] = post(sum_j).
+// post: 0 = plain, 1 = sqrt, 2 = sqrt and inv[0] = 1 / sqrt
+template <int K>
+__device__ __forceinline__ void reduce_finish(double (&acc)[K], int kout, double* partials, unsigned* ticket,
+                                              double* out, int post, double* inv) {
+  __shared__ double sh[K][kTM / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    double v = w[i];
+  for (int j = 0; j < K; ++j) {
+    if (j < kout) {
+      double v = acc[j];
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < k) v = fma(-c[j], V.p[j][i], v);
-    w_out[i] = v;
-    if constexpr (DOT) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < k) acc[j] = fma(sv[j] * V.p[j][i], v, acc[j]);
-    } else {
-      acc[0] = fma(v, v, acc[0]);
+      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+      if (lane == 0) sh[j][warp] = v;
     }
   }
-  block_reduce_store<32>(acc, DOT ? k : 1, partials, nblk);
-}
-
-// scaled multi-dot: out[j] = s_j V_j . w
-__global__ void __launch_bounds__(kT) k_mdot_scaled(int64_t n, int k, PtrList V, const double* __restrict__ sc,
-                                                    const double* __restrict__ w, double* partials, int nblk) {
-  double acc[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const double wi = w[i];
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < k) acc[j] = fma(V.p[j][i], wi, acc[j]);
-  }
-  __shared__ double s2[32];
-  if (threadIdx.x < k) s2[threadIdx.x] = sc[threadIdx.x];
   __syncthreads();
+  if (threadIdx.x < kout) {
+    double v = 0.0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] *= s2[j < k ? j : 0];
-  block_reduce_store<32>(acc, k, partials, nblk);
+    for (int w = 0; w < kTM / 32; ++w) v += sh[threadIdx.x][w];
+    partials[(int64_t)threadIdx.x * nblk + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)nblk - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = warp; j < kout; j += kTM / 32) {
+    double v = 0.0;
+    for (int i = lane; i < nblk; i += 32) v += __ldcg(partials + (int64_t)j * nblk + i);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    if (lane == 0) {
+      if (post >= 1) v = sqrt(v);
+      out[j] = v;
+      if (post == 2 && j == 0) inv[0] = 1.0 / v;
+    }
+  }
+  if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch (graph-safe)
 }
 
-// x += sum_j y[j] Z_j ... see k_zupdate; here: out[j] = scale * sum of the nblk partials of reduction j, in a fixed order
+// MODE 0: out[j] = s_j V_j . w                                   (scaled multi-dot)
+// MODE 1: w_out = w - sum_j c_j s_j V_j;  out[j] = s_j V_j . w_out   (update + next dot)
+// MODE 2: w_out = w - sum_j c_j s_j V_j;  out[0] = ||w_out||        (update + norm)
+// (v_j = s_j V_j: the basis is stored unnormalised with device scales sc)
+template <int K, int MODE>
+__global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double* __restrict__ sc,
+                                             const double* __restrict__ coef, const double* w, double* w_out,
+                                             double* partials, unsigned* ticket, double* out, int post,
+                                             double* inv) {
+  constexpr int U = cgs_unroll<K>();
+  __shared__ double c[K], sv[K];
+  if (threadIdx.x < K) {
+    sv[threadIdx.x] = sc ? sc[threadIdx.x] : 1.0;
+    c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
+  }
+  __syncthreads();
+  constexpr int KA = (MODE == 2) ? 1 : K;
+  double acc[KA];
+#pragma unroll
+  for (int j = 0; j < KA; ++j) acc[j] = 0.0;
+  const int64_t step = (int64_t)gridDim.x * kTM * U;
+  for (int64_t i0 = (int64_t)blockIdx.x * kTM * U + threadIdx.x; i0 < n; i0 += step) {
+    double wv[U], vv[U][K];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kTM;
+      const bool ok = i < n;
+      wv[u] = ok ? w[i] : 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) vv[u][j] = ok ? __ldcs(V.p[j] + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kTM;
+      if constexpr (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fma(vv[u][j], wv[u], acc[j]);
+      } else {
+        double v = wv[u];
+#pragma unroll
+        for (int j = 0; j < K; ++j) v = fma(-c[j], vv[u][j], v);
+        if (i < n) w_out[i] = v;
+        if constexpr (MODE == 1) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[j] = fma(sv[j] * vv[u][j], v, acc[j]);
+        } else {
+          acc[0] = fma(v, v, acc[0]);
+        }
+      }
+    }
+  }
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] *= sv[j];
+  }
+  reduce_finish<KA>(acc, KA, partials, ticket, out, post, inv);
+}
+
+template <int K = 1, class F>
+void dispatch_k(int k, F&& f) {
+  if (k == K) f(std::integral_constant<int, K>{});
+  else if constexpr (K < 32) dispatch_k<K + 1>(k, f);
+  else fail(AMG_EINVAL, "multi-vector kernels take 1..32 vectors");
+}
+
+template <int MODE>
+void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
+                double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s) {
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  dispatch_k(k, [&](auto Kc) {
+    constexpr int K = decltype(Kc)::value;
+    constexpr int U = cgs_unroll<K>();
+    static int occ = 0;  // per (K, MODE) instantiation
+    if (occ == 0) {
+      AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, MODE>, kTM, 0));
+      occ = std::max(occ, 1);
+    }
+    const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)occ * kSMs, (int64_t)kMaxPartials, work}));
+    k_cgs<K, MODE><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv);
+  });
+  AMG_CK_LAUNCH();
+}
+
+// out[j] = sum of the nblk partials of reduction j, in a fixed order
 __global__ void k_finalize(int k, const double* partials, int nblk, double* out, int sqrt_out) {
   __shared__ double sh[kT];
   for (int j = 0; j < k; ++j) {
@@ -227,38 +302,35 @@ void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double*
 }
 
 void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* partials, double* out, cudaStream_t s) {
-  const int nb = nblocks_for(n);
   ProfScope ps_(prof_name("mdot", k, AMG_F64, -1), 8.0 * n * (k + 1), s);
-  k_mdot<<<nb, kT, 0, s>>>(n, k, V, w, partials, nb);
-  AMG_CK_LAUNCH();
-  ++g_launches;
-  k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
-  AMG_CK_LAUNCH();
+  launch_cgs<0>(n, k, V, nullptr, nullptr, w, nullptr, partials, out, 0, nullptr, s);
 }
 
 void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, const double* w, double* partials,
                         double* out, cudaStream_t s, CommBase* comm) {
-  const int nb = nblocks_for(n);
   ProfScope ps_(prof_name("mdot", k, AMG_F64, -1), 8.0 * n * (k + 1), s);
-  k_mdot_scaled<<<nb, kT, 0, s>>>(n, k, V, sc, w, partials, nb);
-  AMG_CK_LAUNCH();
-  ++g_launches;
-  k_finalize<<<1, kT, 0, s>>>(k, partials, nb, out, 0);
-  AMG_CK_LAUNCH();
+  launch_cgs<0>(n, k, V, sc, nullptr, w, nullptr, partials, out, 0, nullptr, s);
   finalize_global(comm, out, k, false, s);
 }
 
+__global__ void k_set_inv1(double* dst, const double* src) { *dst = 1.0 / *src; }
+
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
-                       double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s, CommBase* comm) {
-  const int nb = nblocks_for(n);
+                       double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s, CommBase* comm,
+                       double* inv_out) {
   ProfScope ps_(prof_name(dot_next ? "cgs_update_dot" : "cgs_update_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
-  if (dot_next) k_cgs_update<true><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
-  else k_cgs_update<false><<<nb, kT, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, nb);
-  AMG_CK_LAUNCH();
-  ++g_launches;
-  k_finalize<<<1, kT, 0, s>>>(dot_next ? k : 1, partials, nb, out, (dot_next || comm) ? 0 : 1);
-  AMG_CK_LAUNCH();
-  finalize_global(comm, out, dot_next ? k : 1, !dot_next, s);
+  if (dot_next) {
+    launch_cgs<1>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s);
+    finalize_global(comm, out, k, false, s);
+    return;
+  }
+  const int post = comm ? 0 : (inv_out ? 2 : 1);
+  launch_cgs<2>(n, k, V, sc, coef, w, w_out, partials, out, post, inv_out, s);
+  finalize_global(comm, out, 1, true, s);
+  if (comm && inv_out) {
+    k_set_inv1<<<1, 1, 0, s>>>(inv_out, out);
+    AMG_CK_LAUNCH();
+  }
 }
 
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s) {

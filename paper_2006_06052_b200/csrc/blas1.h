@@ -18,16 +18,19 @@ struct PtrList {
 // out[0] = a . b (or its sqrt); partials: scratch of kMaxPartials doubles
 void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double* partials, double* out,
                 bool sqrt_out, cudaStream_t s, CommBase* comm = nullptr);
-// out[j] = V_j . w, j < k <= 32; partials: scratch of 32 * kMaxPartials doubles
+// out[j] = V_j . w, j < k <= 32; partials: scratch of 32 * kMaxPartials doubles followed
+// by one zero-initialised unsigned ticket (the multi-vector kernels finish their own
+// reduction in the last block and reset the ticket)
 void launch_mdot(int64_t n, int k, const PtrList& V, const double* w, double* partials, double* out, cudaStream_t s);
 // out[j] = sc[j] V_j . w   (basis stored unnormalised with scales sc; device)
 void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, const double* w, double* partials,
                         double* out, cudaStream_t s, CommBase* comm = nullptr);
 // w_out = w - sum_j coef[j] sc[j] V_j, plus out[j] = sc[j] V_j . w_out (dot_next) or
-// out[0] = ||w_out|| -- one pass (CGS2 step of flexible GMRES)
+// out[0] = ||w_out|| and, if inv_out, *inv_out = 1/||w_out|| -- one pass (CGS2 step of
+// flexible GMRES)
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                        double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s,
-                       CommBase* comm = nullptr);
+                       CommBase* comm = nullptr, double* inv_out = nullptr);
 // w -= sum_j coef[j] V_j  (coef: device)
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s);
 // x += sum_j y[j] Z_j  (Z of dtype zt, y: device)

@@ -280,10 +280,8 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
       launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);                 // h1 = v^T w
       launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s, h.comm);   // w -= v h1; h2 = v^T w
-      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s, h.comm);  // w -= v h2; ||w||
-      k_set_inv<<<1, 1, 0, c.s>>>(sc + j + 1, h.dscal + 64);
-      AMG_CK_LAUNCH();
-      ++g_launches;
+      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s, h.comm,
+                        sc + j + 1);  // w -= v h2; ||w||; s_{j+1} = 1/||w||
       c.bytes += 8.0 * N * (3.0 * (j + 1) + 5.0);
       c.read(65);
       for (int i = 0; i <= j; ++i) hh[i] = h.hscal[i] + h.hscal[32 + i];

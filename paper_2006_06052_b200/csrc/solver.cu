@@ -34,7 +34,8 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     for (int i = 0; i <= m; ++i) h.V.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
     for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
   }
-  h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32);
+  h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32 + 8);  // + ticket (blas1.h)
+  AMG_CK(cudaMemset(h.partials + (size_t)kMaxPartials * 32, 0, 8 * sizeof(double)));
   h.dscal = h.arena.alloc_n<double>(256);
   AMG_CK(cudaMallocHost(&h.hscal, sizeof(double) * 256));
   if (h.schur) {
