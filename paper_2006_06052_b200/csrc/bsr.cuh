@@ -1,15 +1,8 @@
-// bsr.cuh -- block-row machinery of every SpMV-type kernel (K1, K2, K4-K7, K10, K11).
-//
-// Layout: int32 row_ptr[n+1], int32 col[nnzb] sorted, values
-// [nnzb][b][b] row-major.  A group of G lanes (G = 8 or 32, a power of two) owns
-// one block row.  The row's work is enumerated as items t = (block k, block row r)
-// in storage order, so the G lanes of a group read G consecutive b-value segments
-// of the value stream: every warp load is contiguous (coalesced) and whole
-// sectors are used.  Each lane multiplies its b values with the b entries of x
-// at the block's column (the b lanes of one block hit the same x segment: one
-// L1 broadcast), accumulating in fp64.  A butterfly inside the group produces the
-// b-vector (A x)_I, which the kernel's epilogue consumes.  All arithmetic is fp64
-// with one rounding on store.
+// bsr.cuh -- shared device helpers of the SpMV-type kernels (bsr_lane.cuh, bsr_tma.cuh):
+// b-element loads, the block-row dot item_dot, the fp64 -> storage rounding, and the
+// K4a pre-smoother x = M f.  Layout: int32 row_ptr[n+1], int32
+// col[nnzb] sorted, values [nnzb][b][b] row-major.  All arithmetic is fp64 with one
+// rounding on store.
 #pragma once
 
 #include "common.cuh"
@@ -86,55 +79,6 @@ __device__ __forceinline__ T to_out(double v) {
   return (T)v;  // fp32: round-to-nearest-even, once
 }
 
-// Partial (A x) of block row `row` for lane gl of its group: one (block, block-row)
-// item per lane per iteration, items in storage order.  If G % B == 0 the lane always
-// handles block row r = gl % B and accumulates into acc[0]; otherwise acc[r].
-template <int B, int G, typename V, typename X>
-__device__ __forceinline__ void row_partial(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                                                   const V* __restrict__ val, const X* __restrict__ x, int row,
-                                                   int gl, double (&acc)[B]) {
-  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
-  const int nitems = (k1 - k0) * B;
-#pragma unroll 2
-  for (int t = gl; t < nitems; t += G) {
-    const int kb = k0 + t / B;
-    const int r = (G % B == 0) ? (gl % B) : (t % B);
-    const int c = __ldg(col + kb);
-    V a[B];
-    X xv[B];
-    load_raw<B, true>(val + ((int64_t)kb * B + r) * B, a);
-    load_raw<B, false>(x + (int64_t)c * B, xv);
-    const double s = item_dot<B, V, X>(a, xv);
-    if constexpr (G % B == 0) {
-      acc[0] += s;
-    } else {
-#pragma unroll
-      for (int rr = 0; rr < B; ++rr)
-        if (rr == r) acc[rr] += s;
-    }
-  }
-}
-
-// Group reduction: every lane of the group receives the full b-vector y = (A x)_row.
-template <int B, int G>
-__device__ __forceinline__ void group_reduce(double (&acc)[B], double (&y)[B]) {
-  if constexpr (G % B == 0) {
-    double v = acc[0];
-#pragma unroll
-    for (int off = G / 2; off >= B; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
-#pragma unroll
-    for (int c = 0; c < B; ++c) y[c] = __shfl_sync(kFull, v, c, G);
-  } else {
-#pragma unroll
-    for (int c = 0; c < B; ++c) {
-      double v = acc[c];
-#pragma unroll
-      for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
-      y[c] = v;
-    }
-  }
-}
-
 template <int B>
 __device__ __forceinline__ double pick(const double (&y)[B], int i) {
   double v = y[0];
@@ -142,73 +86,6 @@ __device__ __forceinline__ double pick(const double (&y)[B], int i) {
   for (int c = 1; c < B; ++c)
     if (c == i) v = y[c];
   return v;
-}
-
-// ---- K1: y = alpha A x + beta y (beta == 0 overwrites) ----
-template <int B, int G, typename V, typename X, typename Y>
-__global__ void __launch_bounds__(256) k_spmv(int n, const int32_t* __restrict__ ptr,
-                                              const int32_t* __restrict__ col, const V* __restrict__ val,
-                                              double alpha, const X* __restrict__ x, double beta,
-                                              Y* __restrict__ y) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
-  const bool valid = row < n;
-  double acc[B] = {};
-  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
-  double yv[B];
-  group_reduce<B, G>(acc, yv);
-  if (valid && gl < B) {
-    const int64_t o = (int64_t)row * B + gl;
-    double v = alpha * pick<B>(yv, gl);
-    if (beta != 0.0) v = fma(beta, (double)y[o], v);
-    y[o] = to_out<Y>(v);
-  }
-}
-
-// ---- K2: r = f - A x ----
-template <int B, int G, typename V, typename X>
-__global__ void __launch_bounds__(256) k_residual(int n, const int32_t* __restrict__ ptr,
-                                                  const int32_t* __restrict__ col, const V* __restrict__ val,
-                                                  const X* __restrict__ f, const X* __restrict__ x,
-                                                  X* __restrict__ r) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
-  const bool valid = row < n;
-  double acc[B] = {};
-  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
-  double yv[B];
-  group_reduce<B, G>(acc, yv);
-  if (valid && gl < B) {
-    const int64_t o = (int64_t)row * B + gl;
-    r[o] = to_out<X>((double)f[o] - pick<B>(yv, gl));
-  }
-}
-
-// ---- K5: post-smooth xo = x + M (f - A x), every row from the old x (Jacobi-type) ----
-template <int B, int G, typename V, typename X>
-__global__ void __launch_bounds__(256) k_smooth(int n, const int32_t* __restrict__ ptr,
-                                                const int32_t* __restrict__ col, const V* __restrict__ val,
-                                                const V* __restrict__ M, const X* __restrict__ f,
-                                                const X* __restrict__ x, X* __restrict__ xo) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
-  const bool valid = row < n;
-  double acc[B] = {};
-  if (valid) row_partial<B, G>(ptr, col, val, x, row, gl, acc);
-  double yv[B];
-  group_reduce<B, G>(acc, yv);
-  if (valid && gl < B) {
-    const int64_t o = (int64_t)row * B;
-    double res[B];
-#pragma unroll
-    for (int c = 0; c < B; ++c) res[c] = (double)f[o + c] - yv[c];
-    double m[B];
-    load_b<B, false>(M + ((int64_t)row * B + gl) * B, m);
-    double t = m[0] * res[0];
-#pragma unroll
-    for (int c = 1; c < B; ++c) t = fma(m[c], res[c], t);
-    xo[o + gl] = to_out<X>((double)x[o + gl] + t);
-  }
 }
 
 // ---- K4 (first half): x = M f (pre-smoothing from a zero initial guess) ----

@@ -1,0 +1,285 @@
+// bsr_lane.cuh -- "row-component lanes": the default SpMV-type kernels (K1 SpMV, K2
+// residual, K5 smoother, K6/K7 restriction/prolongation, K10/K11 Schur products).
+//
+// BR lanes own one block row: lane r accumulates (A x)_{row, r} on its own, so there
+// is no cross-lane reduction and the epilogue store of a warp is contiguous; a warp
+// covers 32/BR consecutive block rows (32 % BR lanes idle).  Each lane walks the row's
+// blocks with U blocks per step: the U column indices and the U block-row segments
+// are loaded first, then the U x gathers, then the arithmetic -- every load of a step
+// is in flight at once.  Two value layouts:
+//   ROWS  lane r reads row r of every block (BC contiguous values: one 16-byte load for
+//         4 fp32 values, two for 4 fp64) and the BC-vector x_col;
+//   COLS  lane r reads column r of every block (values i*B + r: at each i the BR lanes
+//         read consecutive words) and the single value x_col[r]; partial sums acc[i]
+//         for every i, combined across the row's lanes at the end (transpose-reduce).
+// Value loads are cache-streaming (ld.global.cs: read once, evict first) or, where the
+// lanes' pieces share 32-byte sectors (3x3 fp32), L1-allocating (ld.global.nc).
+// Measured on B200 (tools/spmv_lab.cu, cfg-2 27-point 128^3): 4x4 fp32 x fp64 5.49 TB/s,
+// 4x4 fp64 6.08 TB/s (7-point 256^3: 6.60), 3x3 fp32 COLS 4.60 TB/s; the 7-point 3x3
+// fp32 ROWS+nc 5.13 TB/s -- ahead of the TMA-staged consumers (bsr_tma.cuh) in every case.
+// Arithmetic: fp64 accumulation, one rounding on store; FAST
+// (fp32 hierarchy x fp32 vectors, the V-cycle's float backend) forms each block-row dot
+// in fp32 before adding it in fp64.
+#pragma once
+
+#include "bsr.cuh"
+
+namespace amgb {
+
+template <bool NC, typename T>
+__device__ __forceinline__ T ld_val(const T* p) {
+  if constexpr (NC) return __ldg(p);
+  else return __ldcs(p);
+}
+
+// n contiguous values (row segment of a block): vector loads where 16-B aligned
+template <int N, bool NC, typename T>
+__device__ __forceinline__ void ld_seg(const T* __restrict__ p, T (&v)[N]) {
+  if constexpr (N == 4 && std::is_same_v<T, float>) {
+    const float4 q = NC ? __ldg(reinterpret_cast<const float4*>(p)) : __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else if constexpr (N == 4 && std::is_same_v<T, double>) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    const double2 a = NC ? __ldg(q) : __ldcs(q), c = NC ? __ldg(q + 1) : __ldcs(q + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+  } else if constexpr (N == 2 && std::is_same_v<T, double>) {
+    const double2 a = NC ? __ldg(reinterpret_cast<const double2*>(p)) : __ldcs(reinterpret_cast<const double2*>(p));
+    v[0] = a.x; v[1] = a.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < N; ++c) v[c] = ld_val<NC>(p + c);
+  }
+}
+
+// Row-component lane context handed to the epilogue: y_r = (A x)_{row, r}; all()
+// gathers the row's full BR-vector from its lanes (warp shuffles, every lane of the
+// warp must call it).
+template <int BR>
+struct LaneRow {
+  int row, r, base;  // block row, component, lane of component 0
+  bool valid;
+  double yr;
+  __device__ __forceinline__ void all(double (&y)[BR]) const {
+#pragma unroll
+    for (int c = 0; c < BR; ++c) y[c] = __shfl_sync(kFull, yr, base + c);
+  }
+};
+
+// ---------------------------------------------------------------- epilogues
+template <typename Y>
+struct LEpiSpmv {  // y = alpha A x + beta y
+  static constexpr bool kAll = false;
+  double alpha, beta;
+  Y* y;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (!L.valid) return;
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    double v = alpha * L.yr;
+    if (beta != 0.0) v = fma(beta, (double)y[o], v);
+    y[o] = to_out<Y>(v);
+  }
+};
+
+template <typename X>
+struct LEpiResidual {  // r = f - A x
+  static constexpr bool kAll = false;
+  const X* f;
+  X* res;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (!L.valid) return;
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    res[o] = to_out<X>((double)f[o] - L.yr);
+  }
+};
+
+template <typename V, typename X>
+struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
+  static constexpr bool kAll = true;
+  const V* M;
+  const X* f;
+  const X* x;
+  X* xo;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    const double res = L.valid ? (double)f[o] - L.yr : 0.0;
+    double rv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = __shfl_sync(kFull, res, L.base + c);
+    if (!L.valid) return;
+    double m[BR];
+    load_b<BR, false>(M + o * BR, m);
+    double t = m[0] * rv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], rv[c], t);
+    xo[o] = to_out<X>((double)x[o] + t);
+  }
+};
+
+template <typename V, typename X>
+struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
+  static constexpr bool kAll = false;
+  const V* mS;
+  const X* rp;
+  X* p;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (!L.valid) return;
+    p[L.row] = to_out<X>((double)mS[L.row] * ((double)rp[L.row] - L.yr));
+  }
+};
+
+template <typename X>
+struct LEpiSchurU {  // r_u' = r_u - B^T p          (nu x 1 blocks; in place allowed)
+  static constexpr bool kAll = false;
+  const X* ru;
+  X* ru2;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (!L.valid) return;
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    ru2[o] = to_out<X>((double)ru[o] - L.yr);
+  }
+};
+
+// ---------------------------------------------------------------- the kernel
+template <int BR, int BC, int U, bool COLS, bool NC, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __restrict__ ptr,
+                                                  const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                  const X* __restrict__ x, EPI epi) {
+  static_assert(!COLS || BR == BC, "column layout needs square blocks");
+  constexpr int RPW = 32 / BR;
+  constexpr int BE = BR * BC;
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g = lane / BR, r = lane - g * BR;
+  const int row = warp * RPW + g;
+  LaneRow<BR> L;
+  L.row = row;
+  L.r = r;
+  L.base = lane - r;
+  L.valid = g < RPW && row < n;
+  int k0 = 0, k1 = 0;
+  if (L.valid) k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  if constexpr (!COLS) {
+    double acc = 0.0;
+    int k = k0;
+#pragma unroll 1
+    for (; k + U <= k1; k += U) {
+      int c[U];
+      V a[U][BC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = __ldg(col + k + u);
+        ld_seg<BC, NC>(val + (int64_t)(k + u) * BE + r * BC, a[u]);
+      }
+      X xv[U][BC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) load_raw<BC, false>(x + (int64_t)c[u] * BC, xv[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += item_dot<BC, V, X, FAST>(a[u], xv[u]);
+    }
+#pragma unroll 1
+    for (; k < k1; ++k) {
+      V a[BC];
+      X xv[BC];
+      ld_seg<BC, NC>(val + (int64_t)k * BE + r * BC, a);
+      load_raw<BC, false>(x + (int64_t)__ldg(col + k) * BC, xv);
+      acc += item_dot<BC, V, X, FAST>(a, xv);
+    }
+    L.yr = acc;
+  } else {
+    double acc[BR] = {};
+    int k = k0;
+#pragma unroll 1
+    for (; k + U <= k1; k += U) {
+      int c[U];
+      V a[U][BR];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = __ldg(col + k + u);
+#pragma unroll
+        for (int i = 0; i < BR; ++i) a[u][i] = ld_val<NC>(val + (int64_t)(k + u) * BE + i * BC + r);
+      }
+      X xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + (int64_t)c[u] * BC + r);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < BR; ++i) acc[i] = fma((double)a[u][i], (double)xv[u], acc[i]);
+    }
+    for (; k < k1; ++k) {
+      const X xv = __ldg(x + (int64_t)__ldg(col + k) * BC + r);
+#pragma unroll
+      for (int i = 0; i < BR; ++i) acc[i] = fma((double)ld_val<NC>(val + (int64_t)k * BE + i * BC + r), (double)xv, acc[i]);
+    }
+    // y_r = sum over the row's lanes l of acc_l[r]: BR-1 rotations, lane r sends the
+    // entry its receiver needs
+    double s = acc[0];
+#pragma unroll
+    for (int i = 1; i < BR; ++i)
+      if (i == r) s = acc[i];
+#pragma unroll
+    for (int d = 1; d < BR; ++d) {
+      const int want = (r + BR - d) % BR;  // component of the lane that reads from me
+      double v = acc[0];
+#pragma unroll
+      for (int i = 1; i < BR; ++i)
+        if (i == want) v = acc[i];
+      const int src = L.base + (r + d) % BR;
+      s += __shfl_sync(kFull, v, src);
+    }
+    L.yr = s;
+  }
+  epi(L);
+}
+
+// Very long rows (coarse operators, restriction onto a small coarsest level): one warp
+// per block row, whole blocks per lane (U per step, loads first), butterfly over the
+// warp; lanes r < BR then hold component r for the epilogue.
+template <int BR, int BC, int U, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restrict__ ptr,
+                                                  const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                  const X* __restrict__ x, EPI epi) {
+  constexpr int BE = BR * BC;
+  const int lane = threadIdx.x & 31;
+  const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int k0 = 0, k1 = 0;
+  if (row < n) k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  double acc[BR] = {};
+  for (int kb = k0 + lane; kb < k1; kb += 32 * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (kb + 32 * u < k1) ? __ldg(col + kb + 32 * u) : -1;
+    X xv[U][BC];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) load_raw<BC, false>(x + (int64_t)c[u] * BC, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c[u] < 0) continue;
+#pragma unroll
+      for (int i = 0; i < BR; ++i) {
+        V a[BC];
+        ld_seg<BC, false>(val + (int64_t)(kb + 32 * u) * BE + i * BC, a);
+        acc[i] += item_dot<BC, V, X, FAST>(a, xv[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BR; ++i)
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
+  LaneRow<BR> L;
+  L.row = row;
+  L.r = lane < BR ? lane : 0;
+  L.base = 0;
+  L.valid = lane < BR && row < n;
+  L.yr = pick<BR>(acc, L.r);
+  epi(L);
+}
+
+}  // namespace amgb

@@ -1,16 +1,30 @@
-// bsr_tma.cuh -- persistent, TMA-staged BSR kernels (K1 SpMV, K2 residual, K5 smoother).
+// bsr_tma.cuh -- persistent, TMA-staged BSR kernels (K1 SpMV, K2 residual, K5 smoother,
+// K10/K11 Schur coupling products).
 //
 // The direct kernels in bsr.cuh are latency bound: every group walks ptr -> col -> x
 // with only a few hundred bytes in flight (ncu: 81 % of stall cycles on L1TEX
 // scoreboard, profiles/r01_ncu_spmv_direct_b4_f32xf64.csv).  Here each CTA owns a
-// strided set of row tiles (tr consecutive block rows).  A tile's row_ptr slice, its
-// column indices and its block values are each ONE contiguous byte range of global
-// memory, so thread 0 moves them into a shared-memory stage with three bulk async
-// copies (cp.async.bulk, TMA engine) completing on the stage's mbarrier.  `ns` stages
-// are in flight per CTA while the CTA's 8 warps compute the current tile out of
-// shared memory: G lanes per block row, (block, block row) items, fp64
-// accumulation, x gathered from L2, group butterfly, epilogue functor.  HBM streams
-// the matrix continuously; only the x gather latency is exposed in compute.
+// set of row tiles (tr consecutive block rows).  A tile's row_ptr slice, its column
+// indices and its block values are each ONE contiguous byte range of global memory,
+// so thread 0 moves them into a shared-memory stage with three bulk async copies
+// (cp.async.bulk, TMA engine) completing on the stage's mbarrier.  `ns` stages are in
+// flight per CTA while the CTA's threads compute the current tile out of shared
+// memory; HBM streams the matrix continuously and only the x gather latency is
+// exposed in compute.
+//
+// Tile order (TmaArgs::wave): 0 = each CTA owns a contiguous tile range; 1 = tile i of
+// CTA c is c + i*grid, so all CTAs sweep the matrix together and the x entries a
+// banded (stencil-ordered) matrix gathers -- rows within +-n^2 of the sweep front --
+// stay L2-resident instead of being re-read from HBM.
+//
+// Consumer: k_bsr_tma_rows, one thread per block row (short rows, <= 12 blocks); x
+// gathers of the next tile in flight while the current one is computed; rectangular
+// BR x BC blocks (Schur B: 1 x 3, B^T: 3 x 1).
+//
+// Status: opt-in (AMG_TMA=1).  The row-component lane kernels of bsr_lane.cuh measured
+// faster on B200 for every shape of the path (tools/spmv_lab.cu); two
+// further TMA consumers (a warp-per-row group consumer and a thread-per-block consumer
+// with a shared-memory segmented sum) were measured at 2.0-4.0 TB/s and removed.
 #pragma once
 
 #include "bsr.cuh"
@@ -43,12 +57,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// 1-D bulk copy global -> shared (TMA), completes tx bytes on `bar`; 16-B aligned, size % 16 == 0
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+// 1-D bulk copy global -> shared (TMA), completes tx bytes on `bar`; 16-B aligned, size % 16 == 0.
+// The matrix is streamed exactly once per launch: L2 evict-first keeps x resident.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                            uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 // b contiguous values from shared memory; 16-byte vector reads when a block row is a
@@ -75,7 +97,8 @@ __device__ __forceinline__ void lds_b(const V* p, V (&v)[B]) {
 }
 
 // ---------------------------------------------------------------- epilogues
-// called by lanes gl < B of the group owning `row` with the full row vector y = (A x)_row
+// called by the owner of `row` with the full row vector y = (A x)_row, once per
+// component gl < BR (the row kernels call it for every gl with the same y)
 template <int B, typename Y>
 struct EpiSpmv {
   double alpha, beta;
@@ -117,39 +140,77 @@ struct EpiSmooth {  // xo = x + M (f - A x)
   }
 };
 
-// ---------------------------------------------------------------- the kernel
+// K10 epilogue (1 x nu blocks of B): p = m_S o (r_p - B u*)
+template <typename V, typename X>
+struct EpiSchurP {
+  const V* mS;
+  const X* rp;
+  X* p;
+  __device__ __forceinline__ void operator()(int row, int, const double (&yv)[1]) const {
+    p[row] = to_out<X>((double)mS[row] * ((double)rp[row] - yv[0]));
+  }
+};
+
+// K11 epilogue (nu x 1 blocks of B^T): r_u' = r_u - B^T p   (in place allowed: each
+// element is read and written by its own thread)
+template <int NU, typename X>
+struct EpiSchurU {
+  const X* ru;
+  X* ru2;
+  __device__ __forceinline__ void operator()(int row, int gl, const double (&yv)[NU]) const {
+    const int64_t o = (int64_t)row * NU + gl;
+    ru2[o] = to_out<X>((double)ru[o] - pick<NU>(yv, gl));
+  }
+};
+
+// ---------------------------------------------------------------- staging
 struct TmaArgs {
   int n, tr, ntiles, ns;
   int stage_bytes, col_off, val_off;  // stage layout: [ptr | col | val]
+  int wave;                           // tile order (see top)
+  int part_off, max_blk;              // seg consumer: partial sums [BR][max_blk] doubles after the stages
 };
 
-template <int B, int G, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(256) k_bsr_tma(TmaArgs a, const int32_t* __restrict__ ptr,
-                                                 const int32_t* __restrict__ col, const V* __restrict__ val,
-                                                 const X* __restrict__ x, EPI epi) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[kTmaMaxStages];
-  __shared__ int meta[kTmaMaxStages][4];  // ptr shift (B), col shift (B), val shift (B), k0
-  const int tid = threadIdx.x;
-  // contiguous tile range per CTA: consecutive tiles stay on one SM, so the x entries
-  // of the +-1 and +-n neighbours of a 3-D stencil row are L1 hits
-  const int per = (a.ntiles + gridDim.x - 1) / gridDim.x;
-  const int t_begin = blockIdx.x * per;
-  const int my_tiles = max(0, min(per, a.ntiles - t_begin));
-  if (tid == 0) {
-    for (int s = 0; s < a.ns; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
+// Producer side of the pipeline: one elected thread issues the three bulk copies of a
+// tile; consumers read the tile through Tile views.
+template <int BE, typename V>  // BE = elements per block (BR * BC)
+struct TmaPipe {
+  const TmaArgs& a;
+  const int32_t* __restrict__ ptr;
+  const int32_t* __restrict__ col;
+  const V* __restrict__ val;
+  unsigned char* smem;
+  uint64_t* full;
+  int (*meta)[4];  // per stage: ptr shift, col shift, val shift (bytes), k0
+  int t_begin, my_tiles;
+  uint64_t pol;
 
-  // thread 0 is the producer: stage the tile's ptr slice, columns and values
-  auto issue = [&](int i, int s, int k0, int k1) {
-    const int t = t_begin + i;
-    const int R0 = t * a.tr, R1 = min(R0 + a.tr, a.n);
+  __device__ TmaPipe(const TmaArgs& aa, const int32_t* p, const int32_t* c, const V* v, unsigned char* sm,
+                     uint64_t* fu, int (*me)[4])
+      : a(aa), ptr(p), col(c), val(v), smem(sm), full(fu), meta(me) {
+    if (a.wave) {
+      t_begin = 0;
+      my_tiles = (a.ntiles > (int)blockIdx.x) ? (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    } else {
+      const int per = (a.ntiles + gridDim.x - 1) / gridDim.x;
+      t_begin = blockIdx.x * per;
+      my_tiles = max(0, min(per, a.ntiles - t_begin));
+    }
+    pol = policy_evict_first();
+  }
+  __device__ __forceinline__ int tile(int i) const { return a.wave ? (int)blockIdx.x + i * (int)gridDim.x : t_begin + i; }
+  __device__ __forceinline__ int row0(int i) const { return tile(i) * a.tr; }
+  __device__ __forceinline__ void kpair(int i, int& k0, int& k1) const {
+    const int R0 = row0(i);
+    k0 = __ldg(ptr + R0);
+    k1 = __ldg(ptr + min(R0 + a.tr, a.n));
+  }
+  __device__ void issue(int i, int s, int k0, int k1) {
+    const int R0 = row0(i), R1 = min(R0 + a.tr, a.n);
     unsigned char* st = smem + (size_t)s * a.stage_bytes;
     const uintptr_t pa = (uintptr_t)(ptr + R0), pe = (uintptr_t)(ptr + R1 + 1);
     const uintptr_t ca = (uintptr_t)(col + k0), ce = (uintptr_t)(col + k1);
-    const uintptr_t va = (uintptr_t)(val + (int64_t)k0 * B * B), ve = (uintptr_t)(val + (int64_t)k1 * B * B);
+    const uintptr_t va = (uintptr_t)(val + (int64_t)k0 * BE), ve = (uintptr_t)(val + (int64_t)k1 * BE);
     const uintptr_t pa16 = pa & ~uintptr_t(15), ca16 = ca & ~uintptr_t(15), va16 = va & ~uintptr_t(15);
     const unsigned pb = (unsigned)(((pe + 15) & ~uintptr_t(15)) - pa16);
     const unsigned cb = (k1 > k0) ? (unsigned)(((ce + 15) & ~uintptr_t(15)) - ca16) : 0u;
@@ -159,236 +220,139 @@ __global__ void __launch_bounds__(256) k_bsr_tma(TmaArgs a, const int32_t* __res
     meta[s][2] = (int)(va - va16);
     meta[s][3] = k0;
     mbar_arrive_expect_tx(&full[s], pb + cb + vb);
-    tma_load_1d(st, (const void*)pa16, pb, &full[s]);
-    if (cb) tma_load_1d(st + a.col_off, (const void*)ca16, cb, &full[s]);
-    if (vb) tma_load_1d(st + a.val_off, (const void*)va16, vb, &full[s]);
-  };
-  int nk0 = 0, nk1 = 0;  // producer's prefetched ptr pair of the next tile to issue
-  if (tid == 0) {
+    tma_load_1d(st, (const void*)pa16, pb, &full[s], pol);
+    if (cb) tma_load_1d(st + a.col_off, (const void*)ca16, cb, &full[s], pol);
+    if (vb) tma_load_1d(st + a.val_off, (const void*)va16, vb, &full[s], pol);
+  }
+  // thread 0: prologue, first min(ns, my_tiles) tiles; returns the k-pair of tile ns
+  __device__ void prologue(int& nk0, int& nk1) {
     const int pro = min(a.ns, my_tiles);
     for (int i = 0; i < pro; ++i) {
-      const int t = t_begin + i;
-      issue(i, i, __ldg(ptr + t * a.tr), __ldg(ptr + min(t * a.tr + a.tr, a.n)));
+      int k0, k1;
+      kpair(i, k0, k1);
+      issue(i, i, k0, k1);
     }
-    if (a.ns < my_tiles) {
-      const int t = t_begin + a.ns;
-      nk0 = __ldg(ptr + t * a.tr);
-      nk1 = __ldg(ptr + min(t * a.tr + a.tr, a.n));
-    }
+    if (a.ns < my_tiles) kpair(a.ns, nk0, nk1);
   }
-
-  const int g = tid / G, gl = tid & (G - 1);
-  constexpr int NG = 256 / G;
-  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
-  for (int i = 0; i < my_tiles; ++i) {
-    const int s = i % a.ns;
-    mbar_wait(&full[s], (unsigned)((i / a.ns) & 1));
-    const int t = t_begin + i;
-    const int R0 = t * a.tr, nr = min(a.tr, a.n - R0);
-    const unsigned char* st = smem + (size_t)s * a.stage_bytes;
-    const int32_t* sp = reinterpret_cast<const int32_t*>(st + meta[s][0]);
-    const int32_t* sc = reinterpret_cast<const int32_t*>(st + a.col_off + meta[s][1]);
-    const V* sv = reinterpret_cast<const V*>(st + a.val_off + meta[s][2]);
-    const int k0 = meta[s][3];
-    for (int lr = g; lr < nr + (NG - 1) - ((nr + NG - 1) % NG); lr += NG) {
-      // every group of the CTA runs the same number of passes (shuffles stay converged)
-      const bool valid = lr < nr;
-      // block per lane: lane gl handles blocks kb0 + gl, kb0 + gl + G, ...; x is
-      // gathered once per block (b loads) and the b x b block is read from shared memory
-      double acc[B] = {};
-      if (valid) {
-        const int kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
-        for (int kb = kb0 + gl; kb < kb1; kb += G) {
-          X xv[B];
-          load_raw<B, false>(x + (int64_t)sc[kb] * B, xv);
-          const V* blk = sv + (int64_t)kb * B * B;
-#pragma unroll
-          for (int q = 0; q < B; ++q) {
-            // rotate the block-row order per lane: 16-byte rows of neighbouring lanes fall
-            // in different shared-memory bank groups
-            const int r = (B == 4) ? ((q + gl) & 3) : q;
-            V av[B];
-            lds_b<B, V>(blk + r * B, av);
-            const double d = item_dot<B, V, X, FAST>(av, xv);
-#pragma unroll
-            for (int rr = 0; rr < B; ++rr)
-              if (rr == r) acc[rr] += d;
-          }
-        }
-      }
-      double yv[B];
-#pragma unroll
-      for (int c = 0; c < B; ++c) {
-        double v = acc[c];
-#pragma unroll
-        for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(gmask, v, off, G);
-        yv[c] = v;
-      }
-      if (valid && gl < B) epi(R0 + lr, gl, yv);
-    }
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0 && i + a.ns < my_tiles) {
+  // thread 0, after stage s (tile i) is consumed: refill it with tile i + ns
+  __device__ void refill(int i, int s, int& nk0, int& nk1) {
+    if (i + a.ns < my_tiles) {
       issue(i + a.ns, s, nk0, nk1);
-      if (i + a.ns + 1 < my_tiles) {
-        const int tn = t_begin + i + a.ns + 1;
-        nk0 = __ldg(ptr + tn * a.tr);
-        nk1 = __ldg(ptr + min(tn * a.tr + a.tr, a.n));
-      }
+      if (i + a.ns + 1 < my_tiles) kpair(i + a.ns + 1, nk0, nk1);
     }
   }
-}
-
-}  // namespace amgb
-
-namespace amgb {
-
-// ---------------------------------------------------------------- row per lane
-// Same TMA staging as k_bsr_tma, but one THREAD per block row (tile = blockDim rows).
-// For short rows in a banded / stencil ordering the lanes of a warp then gather x at
-// the same block slot of 32 consecutive rows, i.e. contiguous addresses (coalesced),
-// while the row-strided block values are read from shared memory (a row of 7 3x3 fp32
-// blocks is 63 words: odd stride, conflict-free).  No shuffles; the thread owns the
-// whole b-vector of its row.
-template <int B, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(256) k_bsr_tma_rows(TmaArgs a, const int32_t* __restrict__ ptr,
-                                                      const int32_t* __restrict__ col, const V* __restrict__ val,
-                                                      const X* __restrict__ x, EPI epi) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[kTmaMaxStages];
-  __shared__ int meta[kTmaMaxStages][4];
-  const int tid = threadIdx.x;
-  const int per = (a.ntiles + gridDim.x - 1) / gridDim.x;
-  const int t_begin = blockIdx.x * per;
-  const int my_tiles = max(0, min(per, a.ntiles - t_begin));
-  if (tid == 0) {
-    for (int s = 0; s < a.ns; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  auto issue = [&](int i, int s, int k0, int k1) {
-    const int t = t_begin + i;
-    const int R0 = t * a.tr, R1 = min(R0 + a.tr, a.n);
-    unsigned char* st = smem + (size_t)s * a.stage_bytes;
-    const uintptr_t pa = (uintptr_t)(ptr + R0), pe = (uintptr_t)(ptr + R1 + 1);
-    const uintptr_t ca = (uintptr_t)(col + k0), ce = (uintptr_t)(col + k1);
-    const uintptr_t va = (uintptr_t)(val + (int64_t)k0 * B * B), ve = (uintptr_t)(val + (int64_t)k1 * B * B);
-    const uintptr_t pa16 = pa & ~uintptr_t(15), ca16 = ca & ~uintptr_t(15), va16 = va & ~uintptr_t(15);
-    const unsigned pb = (unsigned)(((pe + 15) & ~uintptr_t(15)) - pa16);
-    const unsigned cb = (k1 > k0) ? (unsigned)(((ce + 15) & ~uintptr_t(15)) - ca16) : 0u;
-    const unsigned vb = (k1 > k0) ? (unsigned)(((ve + 15) & ~uintptr_t(15)) - va16) : 0u;
-    meta[s][0] = (int)(pa - pa16);
-    meta[s][1] = (int)(ca - ca16);
-    meta[s][2] = (int)(va - va16);
-    meta[s][3] = k0;
-    mbar_arrive_expect_tx(&full[s], pb + cb + vb);
-    tma_load_1d(st, (const void*)pa16, pb, &full[s]);
-    if (cb) tma_load_1d(st + a.col_off, (const void*)ca16, cb, &full[s]);
-    if (vb) tma_load_1d(st + a.val_off, (const void*)va16, vb, &full[s]);
-  };
-  int nk0 = 0, nk1 = 0;
-  if (tid == 0) {
-    const int pro = min(a.ns, my_tiles);
-    for (int i = 0; i < pro; ++i) {
-      const int t = t_begin + i;
-      issue(i, i, __ldg(ptr + t * a.tr), __ldg(ptr + min(t * a.tr + a.tr, a.n)));
-    }
-    if (a.ns < my_tiles) {
-      const int t = t_begin + a.ns;
-      nk0 = __ldg(ptr + t * a.tr);
-      nk1 = __ldg(ptr + min(t * a.tr + a.tr, a.n));
-    }
-  }
-  // software pipeline: while tile i is computed, the x gathers of this thread's row of
-  // tile i+1 are already in flight (tile i+1 landed: ns >= 3 stages)
-  constexpr int U = (B <= 3) ? 8 : 4;
-  auto tile_info = [&](int i, const int32_t*& sp, const int32_t*& sc, const V*& sv, int& k0, int& nr, int& R0) {
+  __device__ __forceinline__ void wait(int i) { mbar_wait(&full[i % a.ns], (unsigned)((i / a.ns) & 1)); }
+  // shared-memory views of tile i
+  __device__ __forceinline__ void view(int i, const int32_t*& sp, const int32_t*& sc, const V*& sv, int& k0, int& nr,
+                                       int& R0) const {
     const int s = i % a.ns;
     const unsigned char* st = smem + (size_t)s * a.stage_bytes;
     sp = reinterpret_cast<const int32_t*>(st + meta[s][0]);
     sc = reinterpret_cast<const int32_t*>(st + a.col_off + meta[s][1]);
     sv = reinterpret_cast<const V*>(st + a.val_off + meta[s][2]);
     k0 = meta[s][3];
-    R0 = (t_begin + i) * a.tr;
+    R0 = row0(i);
     nr = min(a.tr, a.n - R0);
-  };
-  auto prefetch = [&](int i, X (&xb)[U][B]) {
+  }
+};
+
+#define AMGB_TMA_PROLOGUE(BE, V)                                              \
+  extern __shared__ __align__(128) unsigned char smem[];                      \
+  __shared__ __align__(8) uint64_t full[kTmaMaxStages];                      \
+  __shared__ int meta[kTmaMaxStages][4];                                      \
+  const int tid = threadIdx.x;                                                \
+  TmaPipe<BE, V> pipe(a, ptr, col, val, smem, full, meta);                    \
+  if (tid == 0) {                                                             \
+    for (int s_ = 0; s_ < a.ns; ++s_) mbar_init(&full[s_], 1);                \
+    mbar_fence_init();                                                        \
+  }                                                                           \
+  __syncthreads();                                                            \
+  int nk0 = 0, nk1 = 0;                                                       \
+  if (tid == 0) pipe.prologue(nk0, nk1);
+
+// ---------------------------------------------------------------- row per lane
+// One THREAD per block row (tile = blockDim rows).  For short rows in a banded /
+// stencil ordering the lanes of a warp then gather x at the same block slot of 32
+// consecutive rows, i.e. contiguous addresses (coalesced), while the row-strided block
+// values are read from shared memory (a row of 7 3x3 fp32 blocks is 63 words: odd
+// stride, conflict-free).  No shuffles; the thread owns the whole BR-vector of its row.
+// Blocks are BR x BC (square BSR: BR = BC = b).
+template <int BR, int BC, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(256) k_bsr_tma_rows(TmaArgs a, const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                      const X* __restrict__ x, EPI epi) {
+  AMGB_TMA_PROLOGUE(BR * BC, V)
+  // software pipeline: while tile i is computed, the x gathers of this thread's row of
+  // tile i+1 are already in flight (tile i+1 landed: ns >= 3 stages)
+  constexpr int U = (BC <= 3) ? 8 : 4;
+  auto prefetch = [&](int i, X (&xb)[U][BC]) {
     const int32_t *sp, *sc;
     const V* sv;
     int k0, nr, R0;
-    tile_info(i, sp, sc, sv, k0, nr, R0);
-    const int lr = tid;
+    pipe.view(i, sp, sc, sv, k0, nr, R0);
     int kb0 = 0, kb1 = 0;
-    if (lr < nr) kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
+    if (tid < nr) kb0 = sp[tid] - k0, kb1 = sp[tid + 1] - k0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb0 + u < kb1) {
-        load_raw<B, false>(x + (int64_t)sc[kb0 + u] * B, xb[u]);
+        load_raw<BC, false>(x + (int64_t)sc[kb0 + u] * BC, xb[u]);
       } else {
 #pragma unroll
-        for (int c = 0; c < B; ++c) xb[u][c] = X(0);
+        for (int c = 0; c < BC; ++c) xb[u][c] = X(0);
       }
     }
   };
-  X xa[U][B], xb[U][B];
-  if (my_tiles > 0) {
-    mbar_wait(&full[0], 0u);
+  X xa[U][BC], xb[U][BC];
+  if (pipe.my_tiles > 0) {
+    pipe.wait(0);
     prefetch(0, xa);
   }
-  for (int i = 0; i < my_tiles; ++i) {
-    if (i + 1 < my_tiles) {
-      mbar_wait(&full[(i + 1) % a.ns], (unsigned)(((i + 1) / a.ns) & 1));
+  for (int i = 0; i < pipe.my_tiles; ++i) {
+    if (i + 1 < pipe.my_tiles) {
+      pipe.wait(i + 1);
       prefetch(i + 1, xb);
     }
     const int32_t *sp, *sc;
     const V* sv;
     int k0, nr, R0;
-    tile_info(i, sp, sc, sv, k0, nr, R0);
-    const int lr = tid;
-    if (lr < nr) {
-      const int kb0 = sp[lr] - k0, kb1 = sp[lr + 1] - k0;
-      double acc[B] = {};
+    pipe.view(i, sp, sc, sv, k0, nr, R0);
+    if (tid < nr) {
+      const int kb0 = sp[tid] - k0, kb1 = sp[tid + 1] - k0;
+      double acc[BR] = {};
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (kb0 + u < kb1) {
-          const V* blk = sv + (int64_t)(kb0 + u) * B * B;
+          const V* blk = sv + (int64_t)(kb0 + u) * BR * BC;
 #pragma unroll
-          for (int r = 0; r < B; ++r) {
-            V av[B];
+          for (int r = 0; r < BR; ++r) {
+            V av[BC];
 #pragma unroll
-            for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
-            acc[r] += item_dot<B, V, X, FAST>(av, xa[u]);
+            for (int c = 0; c < BC; ++c) av[c] = blk[r * BC + c];
+            acc[r] += item_dot<BC, V, X, FAST>(av, xa[u]);
           }
         }
       }
       for (int kb = kb0 + U; kb < kb1; ++kb) {  // long rows: the rest loaded in place
-        X xv[B];
-        load_raw<B, false>(x + (int64_t)sc[kb] * B, xv);
-        const V* blk = sv + (int64_t)kb * B * B;
+        X xv[BC];
+        load_raw<BC, false>(x + (int64_t)sc[kb] * BC, xv);
+        const V* blk = sv + (int64_t)kb * BR * BC;
 #pragma unroll
-        for (int r = 0; r < B; ++r) {
-          V av[B];
+        for (int r = 0; r < BR; ++r) {
+          V av[BC];
 #pragma unroll
-          for (int c = 0; c < B; ++c) av[c] = blk[r * B + c];
-          acc[r] += item_dot<B, V, X, FAST>(av, xv);
+          for (int c = 0; c < BC; ++c) av[c] = blk[r * BC + c];
+          acc[r] += item_dot<BC, V, X, FAST>(av, xv);
         }
       }
 #pragma unroll
-      for (int c = 0; c < B; ++c) epi(R0 + lr, c, acc);
+      for (int c = 0; c < BR; ++c) epi(R0 + tid, c, acc);
     }
     __syncthreads();
-    const int s = i % a.ns;
-    if (tid == 0 && i + a.ns < my_tiles) {
-      issue(i + a.ns, s, nk0, nk1);
-      if (i + a.ns + 1 < my_tiles) {
-        const int tn = t_begin + i + a.ns + 1;
-        nk0 = __ldg(ptr + tn * a.tr);
-        nk1 = __ldg(ptr + min(tn * a.tr + a.tr, a.n));
-      }
-    }
+    if (tid == 0) pipe.refill(i, i % a.ns, nk0, nk1);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int c = 0; c < B; ++c) xa[u][c] = xb[u][c];
+      for (int c = 0; c < BC; ++c) xa[u][c] = xb[u][c];
   }
 }
 

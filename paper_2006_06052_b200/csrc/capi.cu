@@ -34,7 +34,7 @@ Mat view_of(const amg_bsr* A) {
   M.col = const_cast<int32_t*>(A->col_idx);
   M.val = const_cast<void*>(A->values);
   M.vt = A->dtype;
-  M.G = choose_group(M.nnz, M.n, M.b);
+  set_lane_plan(M);
   return M;
 }
 

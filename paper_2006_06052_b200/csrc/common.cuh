@@ -69,7 +69,12 @@ class Arena {
   int64_t total_ = 0;
 };
 
-// Device BSR matrix with square b x b blocks (PAPER.md:666-672 layout).
+enum { kTmaNone = 0, kTmaGroup = 1, kTmaRows = 2, kTmaSeg = 3 };
+// bsr_lane.cuh variants: R/C = ROWS/COLS layout, C/N = streaming / L1-allocating loads, U
+enum { kLaneRC2 = 0, kLaneRC4 = 1, kLaneRN2 = 2, kLaneRN4 = 3, kLaneCN2 = 4, kLaneCN4 = 5, kLaneW = 6 /* warp per row */ };
+
+// Device BSR matrix with b x b blocks (PAPER.md:666-672 layout); the Schur coupling
+// views use rectangular br x bc blocks on the outer pattern.
 struct Mat {
   int32_t n = 0, m = 0, b = 1;
   int64_t nnz = 0;
@@ -77,20 +82,16 @@ struct Mat {
   int32_t* col = nullptr;
   void* val = nullptr;
   int vt = AMG_F64;
-  int G = 8;  // lanes per block row in the SpMV-type kernels (chosen from the row length)
+  int br = 0, bc = 0;  // rectangular blocks (0: b)
   // TMA-staged tile plan (bsr_tma.cuh); tma_grid == 0 -> direct kernels
+  int tma_mode = kTmaNone;
   int tma_tr = 0, tma_ntiles = 0, tma_ns = 0, tma_stage = 0, tma_col_off = 0, tma_val_off = 0, tma_grid = 0;
-  bool tma_rows = false;  // row-per-lane TMA consumer (short rows)
+  int tma_wave = 1, tma_part_off = 0, tma_max_blk = 0, tma_smem = 0;
+  int lane_var = kLaneRC2;  // bsr_lane.cuh variant (make_tma_plan)
   bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
+  int rows_per_block() const { return br ? br : b; }
+  int cols_per_block() const { return bc ? bc : b; }
 };
-
-// Lanes per block row: enough lanes to cover a row's (block, block-row) items in a
-// few passes; 8 for 7-point rows (21-28 items), 32 for longer (coarse / 27-point) rows.
-inline int choose_group(int64_t nnz, int32_t n, int b) {
-  if (n <= 0) return 8;
-  double items = (double)nnz * b / (double)n;
-  return items > 40.0 ? 32 : 8;
-}
 
 inline unsigned grid_for(int64_t threads, int block) {
   int64_t g = (threads + block - 1) / block;

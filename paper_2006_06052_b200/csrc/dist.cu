@@ -279,7 +279,6 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
     // outer operator
     h->A = slice_rows(h->arena, Gh->A, bounds[me], bounds[me + 1], s);
     build_halo(*h, h->A, bounds[me], bounds, h->halo0, s);
-    h->A.G = choose_group(h->A.nnz, h->A.n, h->A.b);
     make_tma_plan(h->A, s);
     h->alg_bytes_spmv = (double)h->A.nnz * (4.0 + 8.0 * b * b) + 4.0 * (h->A.n + 1) + 16.0 * h->A.n * b;
     const size_t xs = dtype_size(h->xt);
@@ -302,7 +301,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
                         cudaMemcpyDeviceToDevice));
       AMG_CK(cudaMemcpy(h->shat64, Gh->shat64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
       AMG_CK(cudaMemcpy(h->mS64, Gh->mS64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
-      g_schur_nnz = nz;
+      make_schur_views(h->A, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
     }
     // hierarchy levels
     const size_t L = Gh->lv.size();
@@ -314,17 +313,14 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       const auto& bc = h->lbounds[l + 1];
       LL.A = slice_rows(h->arena, GL.A, bd[me], bd[me + 1], s);
       build_halo(*h, LL.A, bd[me], bd, LL.halo, s);
-      LL.A.G = choose_group(LL.A.nnz, LL.A.n, LL.A.b);
       LL.A.fast32 = GL.A.fast32;
       make_tma_plan(LL.A, s);
       LL.P = slice_rows(h->arena, GL.P, bd[me], bd[me + 1], s);
       if (l + 1 < L) remap_shift(LL.P, bc[me], bc[me + 1] - bc[me]);  // coarsest: global coarse ids
-      LL.P.G = choose_group(LL.P.nnz, LL.P.n, LL.P.b);
       LL.P.fast32 = GL.P.fast32;
       make_tma_plan(LL.P, s);
       LL.R = slice_rows(h->arena, GL.R, bc[me], bc[me + 1], s);
       remap_shift(LL.R, bd[me], bd[me + 1] - bd[me]);
-      LL.R.G = choose_group(LL.R.nnz, LL.R.n, LL.R.b);
       LL.R.fast32 = GL.R.fast32;
       make_tma_plan(LL.R, s);
       const int bb = LL.A.b;

@@ -6,9 +6,9 @@
 
 namespace amgb {
 
-extern int64_t g_schur_nnz;
-
-// build the TMA tile plan of a device matrix (one reduction + one sync); no-op for small n
+// kernel plan of a device matrix: the bsr_lane.cuh variant (host only), plus the opt-in
+// TMA tile plan (AMG_TMA=1: one reduction + one sync)
+void set_lane_plan(Mat& A);
 void make_tma_plan(Mat& A, cudaStream_t s);
 
 // K1  y = alpha A x + beta y
@@ -26,13 +26,14 @@ void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void
 void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void* x, int xt,
                        cudaStream_t s);
 
-// K10 p = m_S o (r_p - B u*)   B: [nnz][nu] on A's pattern (nu velocity comps, 1 x nu blocks)
-void launch_schur_p(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* Bv,
-                    const void* mS, int vt, const void* rp, const void* us, void* p, int xt,
-                    int G, cudaStream_t s);
-// K11 ru2 = r_u - B^T p         BT: [nnz][nu] (nu x 1 blocks)
-void launch_schur_u(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* BTv,
-                    int vt, const void* ru, const void* p, void* ru2, int xt, int G, cudaStream_t s);
+// Schur coupling views on the outer pattern: Bm (1 x nu blocks, values Bv [nnz][nu]) and
+// BTm (nu x 1 blocks, values BTv [nnz][nu]), with their TMA plans
+void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int vt, Mat& Bm, Mat& BTm,
+                      cudaStream_t s);
+// K10 p = m_S o (r_p - B u*)
+void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s);
+// K11 ru2 = r_u - B^T p   (ru2 may alias ru)
+void launch_schur_u(const Mat& BTm, const void* ru, const void* p, void* ru2, int xt, cudaStream_t s);
 
 // K9  split the fp64 interleaved outer vector (b comps per cell) into the velocity part
 // (nu = b-1 comps, type xt) and the pressure part (type xt), narrowing RNE; optional

@@ -711,7 +711,6 @@ Mat solve_copy(Handle& h, const Mat& M64, cudaStream_t s) {
     AMG_CK(cudaMemcpyAsync(M.col, M64.col, sizeof(int32_t) * M64.nnz, cudaMemcpyDeviceToDevice, s));
     launch_convert(M64.nnz * M64.b * M64.b, M64.val, AMG_F64, M.val, h.vt, 1.0, s);
   }
-  M.G = choose_group(M.nnz, M.n, M.b);
   M.fast32 = (h.vt == AMG_F32 && h.xt == AMG_F32);
   make_tma_plan(M, s);
   return M;
@@ -762,8 +761,6 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     launch_convert(A64.nnz * nu, bv, AMG_F64, h.Bv, h.vt, 1.0, s);
     launch_convert(A64.nnz * nu, btv, AMG_F64, h.BTv, h.vt, 1.0, s);
     launch_convert(A64.n, h.mS64, AMG_F64, h.mS, h.vt, 1.0, s);
-    Au.G = choose_group(Au.nnz, Au.n, Au.b);
-    g_schur_nnz = A64.nnz;
     Amg = Au;
   }
   h.bh = Amg.b;
@@ -897,7 +894,6 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     Mat AP = spgemm(c, A, P);
     Mat Ac = spgemm(c, R, AP);
     Ac.m = Ac.n;
-    Ac.G = choose_group(Ac.nnz, Ac.n, Ac.b);
     lvA.push_back(A);
     lvP.push_back(P);
     lvR.push_back(R);

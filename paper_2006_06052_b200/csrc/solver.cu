@@ -97,6 +97,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
     make_tma_plan(M, s);
     if (h->amg_active) setup_build(*h, M, bounds, s);
+    if (h->schur) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
     alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));

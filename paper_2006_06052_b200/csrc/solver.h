@@ -53,6 +53,7 @@ struct Handle {
   bool schur = false;
   int pc = 3, nu = 3;
   void *Bv = nullptr, *BTv = nullptr, *mS = nullptr;
+  Mat Bm, BTm;                     // views of B / B^T on A's pattern (1 x nu / nu x 1 blocks)
   double *shat64 = nullptr, *mS64 = nullptr;
   void *ru = nullptr, *rp = nullptr, *us = nullptr, *pp = nullptr, *ru2 = nullptr, *uu = nullptr;
   // AMG hierarchy (on A, or on A_u for Schur)

@@ -2,15 +2,16 @@
 // K8, K9, K10, K11).  See bsr.cuh for the block-row design.
 #include <algorithm>
 #include <cstdlib>
+#include <unordered_map>
 
 #include "bsr.cuh"
+#include "bsr_lane.cuh"
 #include "bsr_tma.cuh"
 #include "ops.h"
 #include "prof.h"
 
 namespace amgb {
 
-int64_t g_schur_nnz = 0;  // nnz of the Schur B / B^T pattern (set by setup)
 
 namespace {
 
@@ -34,12 +35,6 @@ void dispatch_b(int b, F&& f) {
   }
 }
 
-template <typename F>
-void dispatch_g(int G, F&& f) {
-  if (G == 32) f(std::integral_constant<int, 32>{});
-  else f(std::integral_constant<int, 8>{});
-}
-
 double mat_bytes(const Mat& A) {  // algorithmic bytes of one pass over A
   return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(A.vt)) + 4.0 * (A.n + 1);
 }
@@ -55,25 +50,26 @@ __global__ void k_tile_max(int n, int tr, const int32_t* ptr, int* out) {
   atomicMax(out, ptr[r1] - ptr[r0]);
 }
 
-template <int B, int G, typename V, typename X, bool FAST, class EPI>
-static void launch_tma_f(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
-  TmaArgs a{A.n, A.tma_tr, A.tma_ntiles, A.tma_ns, A.tma_stage, A.tma_col_off, A.tma_val_off};
-  const int smem = A.tma_ns * A.tma_stage;
-  if (A.tma_rows) {
-    static int configured_r = 48 * 1024;
-    if (smem > configured_r) {
-      AMG_CK(cudaFuncSetAttribute(k_bsr_tma_rows<B, V, X, FAST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured_r = smem;
-    }
-    k_bsr_tma_rows<B, V, X, FAST, EPI><<<A.tma_grid, A.tma_tr, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
-    return;
-  }
-  static int configured = 48 * 1024;
+// dynamic shared memory already enabled per kernel (host-side, per function)
+static int& smem_configured(const void* kern) {
+  static std::unordered_map<const void*, int> m;
+  auto it = m.find(kern);
+  if (it == m.end()) it = m.emplace(kern, 48 * 1024).first;
+  return it->second;
+}
+
+template <int BR, int BC, typename V, typename X, bool FAST, class EPI>
+static void launch_tma_rows(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+  TmaArgs a{A.n, A.tma_tr, A.tma_ntiles, A.tma_ns, A.tma_stage, A.tma_col_off, A.tma_val_off,
+            A.tma_wave, A.tma_part_off, A.tma_max_blk};
+  const int smem = A.tma_smem;
+  auto kern = k_bsr_tma_rows<BR, BC, V, X, FAST, EPI>;
+  int& configured = smem_configured((const void*)kern);
   if (smem > configured) {
-    AMG_CK(cudaFuncSetAttribute(k_bsr_tma<B, G, V, X, FAST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
   }
-  k_bsr_tma<B, G, V, X, FAST, EPI><<<A.tma_grid, 256, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
+  kern<<<A.tma_grid, A.tma_tr, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
 }
 
 static int env_int(const char* name, int dflt) {
@@ -81,18 +77,37 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// Kernel plan of a device matrix (bsr_lane.cuh variants, measured in tools/spmv_lab.cu):
+//   4 x 4 (and b <= 2):     ROWS, streaming loads, U = 4 for long rows (> 12 blocks), else 2
+//   3 x 3 fp32 values:      long rows COLS + L1-allocating loads, U = 4; short rows ROWS + nc, U = 2
+//   3 x 3 fp64, rectangular: ROWS, U = 2 (nc for fp32 values)
+// AMG_TMA=1 switches short-row fp32 matrices to the TMA-staged row-per-lane consumer
+// (bsr_tma.cuh) for comparison.  One reduction + one sync only in that case.
+void set_lane_plan(Mat& A) {
+  const int br = A.rows_per_block(), bc = A.cols_per_block();
+  const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
+  const bool f32 = A.vt == AMG_F32;
+  int var = kLaneRC2;
+  if (br == 4 && bc == 4) var = per_row > 12.0 ? kLaneRC4 : kLaneRC2;
+  else if (br == 3 && bc == 3 && f32) var = per_row > 12.0 ? kLaneCN4 : kLaneRN2;
+  else if (br == 3 && bc == 3) var = per_row > 12.0 ? kLaneCN4 : kLaneCN2;
+  else if (br == bc) var = kLaneRN4;
+  else var = f32 ? kLaneRN2 : kLaneRC2;
+  if (per_row > 64.0) var = kLaneW;
+  A.lane_var = env_int("AMG_LANE_VAR", var);
+}
+
 void make_tma_plan(Mat& A, cudaStream_t s) {
   A.tma_grid = 0;
-  A.tma_rows = false;
-  if (A.n < 2048 || env_int("AMG_NO_TMA", 0)) return;
-  if (A.vt == AMG_F64 && !env_int("AMG_TMA_F64", 0)) return;  // direct kernels stream fp64 blocks at ~95 %
-  const double bb = (double)A.b * A.b * dtype_size(A.vt) + 4.0;
-  const double row_bytes = std::max(1.0, (double)A.nnz / A.n * bb);
-  // row-per-lane mode for short rows (<= 12 blocks) when a 128-row tile fits a stage
-  const int mode_rows = env_int("AMG_TMA_ROWS", 1) && (double)A.nnz / A.n <= 12.0 && 128 * row_bytes <= 40 * 1024;
-  int tr = 4;
-  while (tr < 256 && tr * 2 * row_bytes <= env_int("AMG_TMA_TILE_BYTES", 16384)) tr *= 2;
-  if (mode_rows) tr = env_int("AMG_TMA_ROWS_TR", 128);
+  A.tma_mode = kTmaNone;
+  set_lane_plan(A);
+  const int br = A.rows_per_block(), bc = A.cols_per_block();
+  const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
+  if (!env_int("AMG_TMA", 0) || A.n < 2048 || A.vt != AMG_F32) return;
+  const double bb = (double)br * bc * dtype_size(A.vt) + 4.0;
+  const double row_bytes = std::max(1.0, per_row * bb);
+  if (!(per_row <= 12.0 && 128 * row_bytes <= 40 * 1024)) return;
+  const int tr = env_int("AMG_TMA_ROWS_TR", 128);
   const int ntiles = (int)((A.n + tr - 1) / tr);
   int* d = nullptr;
   AMG_CK(cudaMallocAsync((void**)&d, sizeof(int), s));
@@ -106,29 +121,75 @@ void make_tma_plan(Mat& A, cudaStream_t s) {
   auto a16 = [](int64_t v) { return (int)((v + 15) & ~int64_t(15)); };
   const int pbytes = a16(4LL * (tr + 1) + 32);
   const int cbytes = a16(4LL * mx + 32);
-  const int64_t vbytes64 = (int64_t)mx * A.b * A.b * dtype_size(A.vt) + 32;
-  if (vbytes64 > 96 * 1024) return;  // pathological rows: direct kernels
+  const int64_t vbytes64 = (int64_t)mx * br * bc * dtype_size(A.vt) + 32;
+  if (vbytes64 > 96 * 1024) return;
   const int stage = pbytes + cbytes + a16(vbytes64);
-  const int ns = env_int("AMG_TMA_NS", mode_rows ? 3 : (stage > 40 * 1024 ? 2 : 3));
-  const int budget = 220 * 1024;
-  int per_sm = budget / (ns * stage);
-  const int cap = mode_rows ? std::min(32, 2048 / tr) : 4;
-  if (per_sm > cap) per_sm = cap;
+  const int ns = env_int("AMG_TMA_NS", 3);
+  int per_sm = (220 * 1024) / (ns * stage);
+  per_sm = std::min(per_sm, std::min(8, 2048 / tr));
   if (per_sm < 1) return;
-  A.tma_rows = mode_rows;
+  A.tma_mode = kTmaRows;
   A.tma_tr = tr;
   A.tma_ntiles = ntiles;
   A.tma_ns = ns;
   A.tma_stage = stage;
   A.tma_col_off = pbytes;
   A.tma_val_off = pbytes + cbytes;
+  A.tma_part_off = ns * stage;
+  A.tma_max_blk = std::max(mx, 1);
+  A.tma_smem = ns * stage;
+  A.tma_wave = env_int("AMG_TMA_WAVE", 1);
   A.tma_grid = std::min(ntiles, kSMs * per_sm);
 }
 
-template <int B, int G, typename V, typename X, class EPI>
-static void launch_tma(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
-  if (A.fast32) launch_tma_f<B, G, V, X, true>(A, x, epi, s);
-  else launch_tma_f<B, G, V, X, false>(A, x, epi, s);
+// lane-kernel variant -> compile-time (U, COLS, NC); only the variants a block shape uses
+// are instantiated
+template <int BR, int BC, class F>
+static void dispatch_lane(int var, F&& f) {
+  auto go = [&](auto U, auto COLS, auto NC) { f(U, COLS, NC); };
+  using I2 = std::integral_constant<int, 2>;
+  using I4 = std::integral_constant<int, 4>;
+  using T = std::true_type;
+  using Fa = std::false_type;
+  if constexpr (BR == 3 && BC == 3) {
+    if (var == kLaneCN4) go(I4{}, T{}, T{});
+    else if (var == kLaneCN2) go(I2{}, T{}, T{});
+    else if (var == kLaneRN4) go(I4{}, Fa{}, T{});
+    else if (var == kLaneRC2) go(I2{}, Fa{}, Fa{});
+    else go(I2{}, Fa{}, T{});
+  } else if constexpr (BR == 4 && BC == 4) {
+    if (var == kLaneRC4) go(I4{}, Fa{}, Fa{});
+    else if (var == kLaneRN2) go(I2{}, Fa{}, T{});
+    else go(I2{}, Fa{}, Fa{});
+  } else {
+    if (var == kLaneRC2) go(I2{}, Fa{}, Fa{});
+    else if (var == kLaneRN2) go(I2{}, Fa{}, T{});
+    else go(I4{}, Fa{}, T{});
+  }
+}
+
+template <int BR, int BC, typename V, typename X, class EPI>
+static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+  constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
+  if (A.lane_var == kLaneW) {
+    const unsigned grid = grid_for((int64_t)A.n * 32, kBlock);
+    if (can_fast && A.fast32)
+      k_bsr_warp<BR, BC, 2, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+    else
+      k_bsr_warp<BR, BC, 2, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+    return;
+  }
+  constexpr int RPW = 32 / BR;
+  const int64_t warps = ((int64_t)A.n + RPW - 1) / RPW;
+  const unsigned grid = grid_for(warps * 32, kBlock);
+  dispatch_lane<BR, BC>(A.lane_var, [&](auto Uc, auto Cc, auto Nc) {
+    constexpr int U = decltype(Uc)::value;
+    constexpr bool COLS = decltype(Cc)::value, NC = decltype(Nc)::value;
+    if (can_fast && A.fast32)
+      k_bsr_lane<BR, BC, U, COLS, NC, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+    else
+      k_bsr_lane<BR, BC, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+  });
 }
 
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
@@ -139,20 +200,18 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
                     (double)A.n * A.b * dtype_size(yt) * (beta != 0.0 ? 2.0 : 1.0), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
-    dispatch_g(A.G, [&](auto Gc) {
-      constexpr int G = decltype(Gc)::value;
-      dispatch_t(A.vt, [&](auto v) {
-        using V = decltype(v);
-        dispatch_t(xt, [&](auto xx) {
-          using X = decltype(xx);
-          dispatch_t(yt, [&](auto yy) {
-            using Y = decltype(yy);
-            if (A.tma_grid > 0)
-              launch_tma<B, G, V, X>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
-            else
-              k_spmv<B, G, V, X, Y><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-                  A.n, A.ptr, A.col, (const V*)A.val, alpha, (const X*)x, beta, (Y*)y);
-          });
+    dispatch_t(A.vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        dispatch_t(yt, [&](auto yy) {
+          using Y = decltype(yy);
+          if (A.tma_grid > 0) {
+            if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
+            else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
+          } else {
+            launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmv<Y>{alpha, beta, (Y*)y}, s);
+          }
         });
       });
     });
@@ -166,18 +225,16 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
                 mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + 2.0 * A.n * A.b * dtype_size(xt), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
-    dispatch_g(A.G, [&](auto Gc) {
-      constexpr int G = decltype(Gc)::value;
-      dispatch_t(A.vt, [&](auto v) {
-        using V = decltype(v);
-        dispatch_t(xt, [&](auto xx) {
-          using X = decltype(xx);
-          if (A.tma_grid > 0)
-            launch_tma<B, G, V, X>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
-          else
-            k_residual<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-                A.n, A.ptr, A.col, (const V*)A.val, (const X*)f, (const X*)x, (X*)r);
-        });
+    dispatch_t(A.vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        if (A.tma_grid > 0) {
+          if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
+          else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
+        } else {
+          launch_lane<B, B, V, X>(A, (const X*)x, LEpiResidual<X>{(const X*)f, (X*)r}, s);
+        }
       });
     });
   });
@@ -191,18 +248,17 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
                 mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 3.0 * A.n * A.b * dtype_size(xt), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
-    dispatch_g(A.G, [&](auto Gc) {
-      constexpr int G = decltype(Gc)::value;
-      dispatch_t(A.vt, [&](auto v) {
-        using V = decltype(v);
-        dispatch_t(xt, [&](auto xx) {
-          using X = decltype(xx);
-          if (A.tma_grid > 0)
-            launch_tma<B, G, V, X>(A, (const X*)x, EpiSmooth<B, V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s);
-          else
-            k_smooth<B, G, V, X><<<grid_for((int64_t)A.n * G, kBlock), kBlock, 0, s>>>(
-                A.n, A.ptr, A.col, (const V*)A.val, (const V*)M, (const X*)f, (const X*)x, (X*)xo);
-        });
+    dispatch_t(A.vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        if (A.tma_grid > 0) {
+          auto e = EpiSmooth<B, V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo};
+          if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, e, s);
+          else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, e, s);
+        } else {
+          launch_lane<B, B, V, X>(A, (const X*)x, LEpiSmooth<V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s);
+        }
       });
     });
   });
@@ -256,106 +312,55 @@ void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void*
   AMG_CK_LAUNCH();
 }
 
-// ---- K10: p = m_S o (r_p - B u*) ; items = blocks of the row, NU values each ----
-template <int NU, int G, typename V, typename X>
-__global__ void __launch_bounds__(256) k_schur_p(int n, const int32_t* __restrict__ ptr,
-                                                 const int32_t* __restrict__ col, const V* __restrict__ Bv,
-                                                 const V* __restrict__ mS, const X* __restrict__ rp,
-                                                 const X* __restrict__ us, X* __restrict__ p) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
-  const bool valid = row < n;
-  double acc = 0.0;
-  if (valid) {
-    const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
-    for (int k = k0 + gl; k < k1; k += G) {
-      const int c = __ldg(col + k);
-      double bv[NU], uv[NU];
-      load_b<NU, true>(Bv + (int64_t)k * NU, bv);
-      load_b<NU, false>(us + (int64_t)c * NU, uv);
-#pragma unroll
-      for (int d = 0; d < NU; ++d) acc = fma(bv[d], uv[d], acc);
-    }
-  }
-#pragma unroll
-  for (int off = G / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off, G);
-  if (valid && gl == 0) p[row] = to_out<X>((double)mS[row] * ((double)rp[row] - acc));
+void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int vt, Mat& Bm, Mat& BTm,
+                      cudaStream_t s) {
+  Bm = A;
+  Bm.b = 1;
+  Bm.br = 1;
+  Bm.bc = nu;
+  Bm.val = const_cast<void*>(Bv);
+  Bm.vt = vt;
+  Bm.fast32 = false;  // fp64 accumulation of every product (as the direct kernels)
+  BTm = Bm;
+  BTm.br = nu;
+  BTm.bc = 1;
+  BTm.val = const_cast<void*>(BTv);
+  make_tma_plan(Bm, s);
+  make_tma_plan(BTm, s);
 }
 
-// ---- K11: r_u' = r_u - B^T p ; items = (block k, velocity comp d), one value each ----
-template <int NU, int G, typename V, typename X>
-__global__ void __launch_bounds__(256) k_schur_u(int n, const int32_t* __restrict__ ptr,
-                                                 const int32_t* __restrict__ col, const V* __restrict__ BTv,
-                                                 const X* ru, const X* __restrict__ p,
-                                                 X* ru2) {  // ru2 may alias ru (in-place update)
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gid / G), gl = threadIdx.x & (G - 1);
-  const bool valid = row < n;
-  double acc[NU] = {};
-  if (valid) {
-    const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
-    const int nitems = (k1 - k0) * NU;
-    for (int t = gl; t < nitems; t += G) {
-      const int k = k0 + t / NU, d = t % NU;
-      const double v = (double)__ldcs(BTv + (int64_t)k0 * NU + t) * (double)__ldg(p + __ldg(col + k));
-#pragma unroll
-      for (int dd = 0; dd < NU; ++dd)
-        if (dd == d) acc[dd] += v;
-    }
-  }
-  double y[NU];
-#pragma unroll
-  for (int d = 0; d < NU; ++d) {
-    double v = acc[d];
-#pragma unroll
-    for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
-    y[d] = v;
-  }
-  if (valid && gl < NU) {
-    const int64_t o = (int64_t)row * NU + gl;
-    double yy = y[0];
-#pragma unroll
-    for (int d = 1; d < NU; ++d)
-      if (d == gl) yy = y[d];
-    ru2[o] = to_out<X>((double)ru[o] - yy);
-  }
-}
-
-void launch_schur_p(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* Bv,
-                    const void* mS, int vt, const void* rp, const void* us, void* p, int xt, int G,
-                    cudaStream_t s) {
+void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s) {
+  const int n = Bm.n, vt = Bm.vt;
   if (n == 0) return;
-  if (nu != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
+  if (Bm.bc != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
   ProfScope ps_(prof_name("schur_p", 3, vt, xt),
-                ((double)g_schur_nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + (double)n * dtype_size(vt) + 5.0 * n * dtype_size(xt), s);
-  dispatch_g(G, [&](auto Gc) {
-    constexpr int GG = decltype(Gc)::value;
-    dispatch_t(vt, [&](auto v) {
-      using V = decltype(v);
-      dispatch_t(xt, [&](auto xx) {
-        using X = decltype(xx);
-        k_schur_p<3, GG, V, X><<<grid_for((int64_t)n * GG, 256), 256, 0, s>>>(
-            n, ptr, col, (const V*)Bv, (const V*)mS, (const X*)rp, (const X*)us, (X*)p);
-      });
+                ((double)Bm.nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + (double)n * dtype_size(vt) + 5.0 * n * dtype_size(xt), s);
+  dispatch_t(vt, [&](auto v) {
+    using V = decltype(v);
+    dispatch_t(xt, [&](auto xx) {
+      using X = decltype(xx);
+      if (Bm.tma_grid > 0)
+        launch_tma_rows<1, 3, V, X, false>(Bm, (const X*)us, EpiSchurP<V, X>{(const V*)mS, (const X*)rp, (X*)p}, s);
+      else
+        launch_lane<1, 3, V, X>(Bm, (const X*)us, LEpiSchurP<V, X>{(const V*)mS, (const X*)rp, (X*)p}, s);
     });
   });
   AMG_CK_LAUNCH();
 }
 
-void launch_schur_u(int32_t n, int nu, const int32_t* ptr, const int32_t* col, const void* BTv, int vt,
-                    const void* ru, const void* p, void* ru2, int xt, int G, cudaStream_t s) {
+void launch_schur_u(const Mat& BTm, const void* ru, const void* p, void* ru2, int xt, cudaStream_t s) {
+  const int n = BTm.n, vt = BTm.vt;
   if (n == 0) return;
-  if (nu != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
-  ProfScope ps_(prof_name("schur_u", 3, vt, xt), ((double)g_schur_nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + 7.0 * n * dtype_size(xt), s);
-  dispatch_g(G, [&](auto Gc) {
-    constexpr int GG = decltype(Gc)::value;
-    dispatch_t(vt, [&](auto v) {
-      using V = decltype(v);
-      dispatch_t(xt, [&](auto xx) {
-        using X = decltype(xx);
-        k_schur_u<3, GG, V, X><<<grid_for((int64_t)n * GG, 256), 256, 0, s>>>(
-            n, ptr, col, (const V*)BTv, (const X*)ru, (const X*)p, (X*)ru2);
-      });
+  if (BTm.br != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
+  ProfScope ps_(prof_name("schur_u", 3, vt, xt), ((double)BTm.nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + 7.0 * n * dtype_size(xt), s);
+  dispatch_t(vt, [&](auto v) {
+    using V = decltype(v);
+    dispatch_t(xt, [&](auto xx) {
+      using X = decltype(xx);
+      if (BTm.tma_grid > 0)
+        launch_tma_rows<3, 1, V, X, false>(BTm, (const X*)p, EpiSchurU<3, X>{(const X*)ru, (X*)ru2}, s);
+      else
+        launch_lane<3, 1, V, X>(BTm, (const X*)p, LEpiSchurU<X>{(const X*)ru, (X*)ru2}, s);
     });
   });
   AMG_CK_LAUNCH();

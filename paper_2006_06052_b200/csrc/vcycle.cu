@@ -65,9 +65,9 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s);                                 // K9
   void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
   halo_exchange(h, h.halo0, us, h.xt, h.nu, s);
-  launch_schur_p(h.n, h.nu, h.A.ptr, h.A.col, h.Bv, h.mS, h.vt, h.rp, us, h.pp, h.xt, h.A.G, s);  // K10
+  launch_schur_p(h.Bm, h.mS, h.rp, us, h.pp, h.xt, s);  // K10
   halo_exchange(h, h.halo0, h.pp, h.xt, 1, s);
-  launch_schur_u(h.n, h.nu, h.A.ptr, h.A.col, h.BTv, h.vt, f0, h.pp, f0, h.xt, h.A.G, s);    // K11 (in place)
+  launch_schur_u(h.BTm, f0, h.pp, f0, h.xt, s);    // K11 (in place)
   void* u = vcycle_run(h, 0, s);                                                               // u = V(r_u')
   launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
 }

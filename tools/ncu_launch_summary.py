@@ -1,0 +1,30 @@
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) per kernel.
+
+  python tools/ncu_launch_summary.py gpurun_out/launches.csv [top]
+Per-launch ncu times are cold-cache and serialised: compare SHARES of the step, not absolutes.
+"""
+import collections
+import csv
+import re
+import sys
+
+path = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+rows = [l for l in open(path) if l.startswith('"')]
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+for r in csv.DictReader(rows):
+    if r.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    name = r["Kernel Name"]
+    name = re.sub(r"\(.*$", "", name)  # drop the parameter list, keep template args
+    v = float(r["Metric Value"].replace(",", ""))
+    unit = r.get("Metric Unit", "ns")
+    v *= {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(unit, 1e-6)
+    tot[name] += v
+    cnt[name] += 1
+T = sum(tot.values())
+print(f"{sum(cnt.values())} launches, {T:.2f} ms total (ncu, serialised)")
+print(f"{'share':>6s} {'ms':>9s} {'launches':>8s}  kernel")
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:top]:
+    print(f"{v / T:6.3f} {v:9.3f} {cnt[k]:8d}  {k[:150]}")

@@ -22,6 +22,10 @@ A = amg.BSR.from_numpy(ptr, col, val)
 del val
 S = amg.Solver(A, bench.params_for(amg, cfg))
 del A
+for l in range(S.levels):
+    nb, bs, za, zp, nc = S.level_info(l)
+    print(f"level {l}: n {nb} b {bs} A {za} ({za / max(nb, 1):.1f}/row) P {zp} ({zp / max(nb, 1):.2f}/row) "
+          f"R rows {nc} ({zp / max(nc, 1):.1f}/row)")
 b = torch.as_tensor(bvec, device="cuda")
 x = torch.zeros_like(b)
 for _ in range(2):

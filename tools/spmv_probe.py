@@ -36,9 +36,12 @@ def main(n=128, reps=30, bs=(4, 3), variants=((1, 0), (0, 0), (1, 1))):
                 run()
             ts = []
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            for _ in range(reps):
-                s.record(); run(); e.record(); e.synchronize()
-                ts.append(s.elapsed_time(e))
+            for _ in range(5):
+                s.record()
+                for _ in range(reps):
+                    run()
+                e.record(); e.synchronize()
+                ts.append(s.elapsed_time(e) / reps)
             t = float(np.median(ts))
             nrows, Z = n ** 3, len(col)
             sv, sx = (4 if vt == amg.F32 else 8), (4 if xt == amg.F32 else 8)
