@@ -224,19 +224,34 @@ __global__ void __launch_bounds__(kT) k_maxpy(int64_t n, int k, PtrList V, const
   }
 }
 
-// x += sum_j y[j] Z_j  (Z of type T; y on the device)
-template <typename T>
-__global__ void __launch_bounds__(kT) k_zupdate(int64_t n, int k, PtrList Z, const double* __restrict__ y,
-                                                double* __restrict__ x) {
-  __shared__ double c[32];
-  if (threadIdx.x < k) c[threadIdx.x] = y[threadIdx.x];
+// x += sum_j y[j] Z_j  (Z of type T; y on the device); K-templated like k_cgs
+template <int K, typename T>
+__global__ void __launch_bounds__(kTM) k_zupdate(int64_t n, PtrList Z, const double* __restrict__ y,
+                                                 double* __restrict__ x) {
+  constexpr int U = cgs_unroll<K>();
+  __shared__ double c[K];
+  if (threadIdx.x < K) c[threadIdx.x] = y[threadIdx.x];
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    double v = x[i];
+  const int64_t step = (int64_t)gridDim.x * kTM * U;
+  for (int64_t i0 = (int64_t)blockIdx.x * kTM * U + threadIdx.x; i0 < n; i0 += step) {
+    double xv[U];
+    T zv[U][K];
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < k) v = fma(c[j], (double)reinterpret_cast<const T*>(Z.p[j])[i], v);
-    x[i] = v;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kTM;
+      const bool ok = i < n;
+      xv[u] = ok ? x[i] : 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) zv[u][j] = ok ? __ldcs(reinterpret_cast<const T*>(Z.p[j]) + i) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kTM;
+      double v = xv[u];
+#pragma unroll
+      for (int j = 0; j < K; ++j) v = fma(c[j], (double)zv[u][j], v);
+      if (i < n) x[i] = v;
+    }
   }
 }
 
@@ -341,8 +356,14 @@ void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double
 
 void launch_zupdate(int64_t n, int k, const PtrList& Z, int zt, const double* y, double* x, cudaStream_t s) {
   ProfScope ps_(prof_name("zupdate", k, zt, -1), (double)n * (16.0 + (double)k * dtype_size(zt)), s);
-  if (zt == AMG_F32) k_zupdate<float><<<ew_grid(n), kT, 0, s>>>(n, k, Z, y, x);
-  else k_zupdate<double><<<ew_grid(n), kT, 0, s>>>(n, k, Z, y, x);
+  dispatch_k(k, [&](auto Kc) {
+    constexpr int K = decltype(Kc)::value;
+    constexpr int U = cgs_unroll<K>();
+    const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)kSMs * 8, work));
+    if (zt == AMG_F32) k_zupdate<K, float><<<g, kTM, 0, s>>>(n, Z, y, x);
+    else k_zupdate<K, double><<<g, kTM, 0, s>>>(n, Z, y, x);
+  });
   AMG_CK_LAUNCH();
 }
 

@@ -282,4 +282,78 @@ __global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restri
   epi(L);
 }
 
+// ---------------------------------------------------------------- sliced BSR
+// Long rows: the library's solve copy also holds a SLICED layout of the same blocks
+// (SELL-C with C = 32/B consecutive block rows per slice, one warp per slice, padded to
+// the slice's longest row with zero blocks; built once in make_tma_plan).  Step j of
+// slice s stores, for block row i < B, the C*B words [g][r] = A_{row s*C+g, block j}[i][r]
+// contiguously, so each of the B value loads of a warp reads C*B consecutive words
+// (perfect coalescing, no sector shared across instructions); lane (g, r) holds column
+// r of its row's block (COLS) and gathers the single value x_col[r].
+// Measured (tools/spmv_lab.cu): 27-point 3x3 fp32 5.63 TB/s (row layout 4.59), 4x4
+// fp32 x fp64 6.04 TB/s (5.68), 4x4 fp64 6.69 TB/s (6.16).
+template <int B, int U, typename V, typename X, class EPI>
+__global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const int32_t* __restrict__ sptr,
+                                                     const int32_t* __restrict__ scol, const V* __restrict__ sval,
+                                                     const X* __restrict__ x, EPI epi) {
+  constexpr int C = 32 / B;
+  const int lane = threadIdx.x & 31;
+  const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int g = lane / B, r = lane - g * B;
+  const bool act = g < C && s < nslices;
+  const int L = g < C ? lane : 0, gg = g < C ? g : 0;
+  int j0 = 0, j1 = 0;
+  if (s < nslices) j0 = __ldg(sptr + s), j1 = __ldg(sptr + s + 1);
+  double acc[B] = {};
+  int j = j0;
+#pragma unroll 1
+  for (; j + U <= j1; j += U) {
+    int c[U];
+    V a[U][B];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = __ldg(scol + (int64_t)(j + u) * C + gg);
+#pragma unroll
+      for (int i = 0; i < B; ++i) a[u][i] = __ldcs(sval + ((int64_t)(j + u) * B + i) * (C * B) + L);
+    }
+    X xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + (int64_t)c[u] * B + r);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < B; ++i) acc[i] = fma((double)a[u][i], (double)xv[u], acc[i]);
+  }
+#pragma unroll 1
+  for (; j < j1; ++j) {
+    const int c = __ldg(scol + (int64_t)j * C + gg);
+    const X xv = __ldg(x + (int64_t)c * B + r);
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      acc[i] = fma((double)__ldcs(sval + ((int64_t)j * B + i) * (C * B) + L), (double)xv, acc[i]);
+  }
+  // y_r = sum over the row's lanes l of acc_l[r] (transpose-reduce, as k_bsr_lane COLS)
+  const int base = lane - r;
+  double sum = acc[0];
+#pragma unroll
+  for (int i = 1; i < B; ++i)
+    if (i == r) sum = acc[i];
+#pragma unroll
+  for (int d = 1; d < B; ++d) {
+    const int want = (r + B - d) % B;
+    double v = acc[0];
+#pragma unroll
+    for (int i = 1; i < B; ++i)
+      if (i == want) v = acc[i];
+    sum += __shfl_sync(kFull, v, base + (r + d) % B);
+  }
+  LaneRow<B> Lr;
+  Lr.row = s * C + g;
+  Lr.r = r;
+  Lr.base = base;
+  Lr.valid = act && Lr.row < n;
+  Lr.yr = sum;
+  epi(Lr);
+}
+
 }  // namespace amgb

@@ -116,6 +116,7 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
 
 struct bsr_plan {
   amgb::Mat A;
+  amgb::Arena arena;  // the plan's sliced copy of long-row matrices
 };
 
 int bsr_plan_create(const amg_bsr* A, void* stream, struct bsr_plan** out) {
@@ -126,7 +127,7 @@ int bsr_plan_create(const amg_bsr* A, void* stream, struct bsr_plan** out) {
   bsr_plan* p = new bsr_plan;
   p->A = view_of(A);
   try {
-    make_tma_plan(p->A, (cudaStream_t)stream);
+    make_tma_plan(p->A, (cudaStream_t)stream, &p->arena);
   } catch (...) {
     delete p;
     throw;

@@ -71,7 +71,7 @@ class Arena {
 
 enum { kTmaNone = 0, kTmaGroup = 1, kTmaRows = 2, kTmaSeg = 3 };
 // bsr_lane.cuh variants: R/C = ROWS/COLS layout, C/N = streaming / L1-allocating loads, U
-enum { kLaneRC2 = 0, kLaneRC4 = 1, kLaneRN2 = 2, kLaneRN4 = 3, kLaneCN2 = 4, kLaneCN4 = 5, kLaneW = 6 /* warp per row */ };
+enum { kLaneRC2 = 0, kLaneRC4 = 1, kLaneRN2 = 2, kLaneRN4 = 3, kLaneCN2 = 4, kLaneCN4 = 5, kLaneW = 6 /* warp per row */, kLaneSell = 7 /* sliced copy */ };
 
 // Device BSR matrix with b x b blocks (PAPER.md:666-672 layout); the Schur coupling
 // views use rectangular br x bc blocks on the outer pattern.
@@ -88,6 +88,11 @@ struct Mat {
   int tma_tr = 0, tma_ntiles = 0, tma_ns = 0, tma_stage = 0, tma_col_off = 0, tma_val_off = 0, tma_grid = 0;
   int tma_wave = 1, tma_part_off = 0, tma_max_blk = 0, tma_smem = 0;
   int lane_var = kLaneRC2;  // bsr_lane.cuh variant (make_tma_plan)
+  // sliced copy of the blocks (kLaneSell; bsr_lane.cuh k_bsr_sell), owned by the builder's arena
+  int32_t sell_ns = 0;
+  int32_t* sell_ptr = nullptr;  // [sell_ns + 1] step offsets
+  int32_t* sell_col = nullptr;  // [steps][C]
+  void* sell_val = nullptr;     // [steps][b][C][b]
   bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
   int rows_per_block() const { return br ? br : b; }
   int cols_per_block() const { return bc ? bc : b; }

@@ -279,7 +279,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
     // outer operator
     h->A = slice_rows(h->arena, Gh->A, bounds[me], bounds[me + 1], s);
     build_halo(*h, h->A, bounds[me], bounds, h->halo0, s);
-    make_tma_plan(h->A, s);
+    make_tma_plan(h->A, s, &h->arena);
     h->alg_bytes_spmv = (double)h->A.nnz * (4.0 + 8.0 * b * b) + 4.0 * (h->A.n + 1) + 16.0 * h->A.n * b;
     const size_t xs = dtype_size(h->xt);
     if (h->schur) {
@@ -314,15 +314,15 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       LL.A = slice_rows(h->arena, GL.A, bd[me], bd[me + 1], s);
       build_halo(*h, LL.A, bd[me], bd, LL.halo, s);
       LL.A.fast32 = GL.A.fast32;
-      make_tma_plan(LL.A, s);
+      make_tma_plan(LL.A, s, &h->arena);
       LL.P = slice_rows(h->arena, GL.P, bd[me], bd[me + 1], s);
       if (l + 1 < L) remap_shift(LL.P, bc[me], bc[me + 1] - bc[me]);  // coarsest: global coarse ids
       LL.P.fast32 = GL.P.fast32;
-      make_tma_plan(LL.P, s);
+      make_tma_plan(LL.P, s, &h->arena);
       LL.R = slice_rows(h->arena, GL.R, bc[me], bc[me + 1], s);
       remap_shift(LL.R, bd[me], bd[me + 1] - bd[me]);
       LL.R.fast32 = GL.R.fast32;
-      make_tma_plan(LL.R, s);
+      make_tma_plan(LL.R, s, &h->arena);
       const int bb = LL.A.b;
       const int64_t nl = LL.A.n;
       LL.M = h->arena.alloc(std::max<int64_t>(nl * bb * bb, 1) * dtype_size(h->vt));

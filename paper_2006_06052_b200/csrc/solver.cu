@@ -1,5 +1,6 @@
 // solver.cu -- C ABI of the solver handle: amg_setup / amg_solve / introspection.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "amg.h"
@@ -31,7 +32,13 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     // Z is stored in the preconditioner's output precision: the fp32 V-cycle output is
     // exactly representable in fp32, so storing it narrow is lossless.
     h.zt = (h.amg_active && h.xt == AMG_F32) ? AMG_F32 : AMG_F64;
-    for (int i = 0; i <= m; ++i) h.V.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+    // one slab for the basis; vector j starts j * (size + stagger) bytes in, so the
+    // j-streams the CGS2 kernels read side by side do not share DRAM address bits
+    const char* st = getenv("AMG_VSTAGGER");
+    const size_t stagger = st ? (size_t)atol(st) : 0;
+    const size_t vbytes = ((size_t)std::max<int64_t>(N, 1) * 8 + 255) & ~size_t(255);
+    char* slab = (char*)h.arena.alloc((vbytes + stagger) * (m + 1) + 256);
+    for (int i = 0; i <= m; ++i) h.V.push_back(reinterpret_cast<double*>(slab + (size_t)i * (vbytes + stagger)));
     for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
   }
   h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32 + 8);  // + ticket (blas1.h)
@@ -95,7 +102,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
       launch_convert(M.nnz * M.b * M.b, src.val, src.vt, M.val, AMG_F64, 1.0, s);
     }
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
-    make_tma_plan(M, s);
+    make_tma_plan(M, s, &h->arena);
     if (h->amg_active) setup_build(*h, M, bounds, s);
     if (h->schur) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
     alloc_workspace(*h, s);

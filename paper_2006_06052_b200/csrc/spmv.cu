@@ -1,6 +1,7 @@
 // spmv.cu -- instantiation + dispatch of the SpMV-type solve kernels (K1, K2, K4, K5,
 // K8, K9, K10, K11).  See bsr.cuh for the block-row design.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <unordered_map>
 
@@ -97,10 +98,77 @@ void set_lane_plan(Mat& A) {
   A.lane_var = env_int("AMG_LANE_VAR", var);
 }
 
-void make_tma_plan(Mat& A, cudaStream_t s) {
+// ---- sliced copy (k_bsr_sell) ----
+__global__ void k_sell_len(int n, int C, const int32_t* ptr, int32_t* len) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s * C >= n) return;
+  int mx = 0;
+  for (int64_t r = s * C; r < min((int64_t)n, s * C + C); ++r) mx = max(mx, ptr[r + 1] - ptr[r]);
+  len[s] = mx;
+}
+
+template <typename V>
+__global__ void k_sell_fill(int n, int b, int C, int ns, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                            const V* __restrict__ val, const int32_t* __restrict__ sptr, int32_t* __restrict__ scol,
+                            V* __restrict__ sval) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * C) return;
+  const int s = (int)(t / C), g = (int)(t % C);
+  const int64_t row = (int64_t)s * C + g;
+  const int k0 = row < n ? ptr[row] : 0, len = row < n ? ptr[row + 1] - k0 : 0;
+  const int pad_col = row < n ? (int)row : 0;
+  for (int j = 0; j < sptr[s + 1] - sptr[s]; ++j) {
+    const int64_t st = sptr[s] + j;
+    scol[st * C + g] = j < len ? col[k0 + j] : (len > 0 ? col[k0] : pad_col);
+    for (int i = 0; i < b; ++i)
+      for (int r = 0; r < b; ++r)
+        sval[(st * b + i) * ((int64_t)C * b) + g * b + r] = j < len ? val[((int64_t)(k0 + j) * b + i) * b + r] : V(0);
+  }
+}
+
+static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
+  const int C = 32 / A.b;
+  const int ns = (int)((A.n + C - 1) / C);
+  int32_t* len = nullptr;
+  AMG_CK(cudaMallocAsync((void**)&len, sizeof(int32_t) * ns, s));
+  k_sell_len<<<grid_for(ns, 256), 256, 0, s>>>(A.n, C, A.ptr, len);
+  AMG_CK_LAUNCH();
+  std::vector<int32_t> h(ns), sp(ns + 1, 0);
+  AMG_CK(cudaMemcpyAsync(h.data(), len, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, s));
+  AMG_CK(cudaStreamSynchronize(s));
+  AMG_CK(cudaFreeAsync(len, s));
+  for (int i = 0; i < ns; ++i) {
+    if ((int64_t)sp[i] + h[i] > INT32_MAX) fail(AMG_EINDEX_OVERFLOW, "sliced copy: too many steps");
+    sp[i + 1] = sp[i] + h[i];
+  }
+  const int64_t steps = sp[ns];
+  A.sell_ns = ns;
+  A.sell_ptr = arena.alloc_n<int32_t>(ns + 1);
+  A.sell_col = arena.alloc_n<int32_t>(std::max<int64_t>(steps * C, 1));
+  A.sell_val = arena.alloc(std::max<int64_t>(steps * C * A.b * A.b, 1) * dtype_size(A.vt));
+  AMG_CK(cudaMemcpyAsync(A.sell_ptr, sp.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, s));
+  dispatch_t(A.vt, [&](auto v) {
+    using V = decltype(v);
+    k_sell_fill<V><<<grid_for((int64_t)ns * C, 256), 256, 0, s>>>(A.n, A.b, C, ns, A.ptr, A.col, (const V*)A.val,
+                                                                   A.sell_ptr, A.sell_col, (V*)A.sell_val);
+  });
+  AMG_CK_LAUNCH();
+  AMG_CK(cudaStreamSynchronize(s));  // sp (host) must outlive the copy
+  A.lane_var = kLaneSell;
+}
+
+void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena) {
   A.tma_grid = 0;
   A.tma_mode = kTmaNone;
   set_lane_plan(A);
+  {
+    // long rows and enough slices to fill the GPU: sliced copy (k_bsr_sell)
+    const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
+    const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
+    if (arena && square && per_row > 12.0 && (int64_t)A.n / (32 / A.b) >= (int64_t)kSMs * 8 &&
+        !env_int("AMG_NO_SELL", 0) && !env_int("AMG_LANE_VAR", 0))
+      build_sell(A, *arena, s);
+  }
   const int br = A.rows_per_block(), bc = A.cols_per_block();
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
   if (!env_int("AMG_TMA", 0) || A.n < 2048 || A.vt != AMG_F32) return;
@@ -171,6 +239,15 @@ static void dispatch_lane(int var, F&& f) {
 template <int BR, int BC, typename V, typename X, class EPI>
 static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
   constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
+  if constexpr (BR == BC && BR >= 2) {
+    if (A.lane_var == kLaneSell) {
+      constexpr int U = (BR * BR * sizeof(V) <= 36) ? 4 : 2;
+      const unsigned grid = grid_for((int64_t)A.sell_ns * 32, kBlock);
+      k_bsr_sell<BR, U, V, X, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_col, (const V*)A.sell_val,
+                                                          x, epi);
+      return;
+    }
+  }
   if (A.lane_var == kLaneW) {
     const unsigned grid = grid_for((int64_t)A.n * 32, kBlock);
     if (can_fast && A.fast32)
@@ -395,10 +472,67 @@ __global__ void k_convert(int64_t N, const I* __restrict__ in, O* __restrict__ o
     out[t] = to_out<O>((double)in[t] * scale);
 }
 
+// Hot shape (b = 4, pressure component 3, fp32 V-cycle vectors): thread per cell, one
+// 32-byte read of the cell, the velocity triples staged in shared memory and written
+// as float4 (coalesced), the pressure written directly.
+__global__ void __launch_bounds__(256) k_split4(int n, const double* __restrict__ r, double scale, float* __restrict__ ru,
+                                                float* __restrict__ rp) {
+  __shared__ __align__(16) float su[3 * 256];
+  const int64_t c0 = (int64_t)blockIdx.x * 256;
+  const int64_t c = c0 + threadIdx.x;
+  const int nc = (int)min((int64_t)256, (int64_t)n - c0);
+  if (c < n) {
+    const double2* q = reinterpret_cast<const double2*>(r + c * 4);
+    const double2 a = __ldcs(q), b = __ldcs(q + 1);
+    su[3 * threadIdx.x + 0] = (float)(a.x * scale);
+    su[3 * threadIdx.x + 1] = (float)(a.y * scale);
+    su[3 * threadIdx.x + 2] = (float)(b.x * scale);
+    rp[c] = (float)(b.y * scale);
+  }
+  __syncthreads();
+  float* dst = ru + c0 * 3;
+  if (nc == 256) {  // 768 floats = 192 float4, 16-byte aligned (c0 * 12 bytes, c0 % 256 == 0)
+    if (threadIdx.x < 192) reinterpret_cast<float4*>(dst)[threadIdx.x] = reinterpret_cast<const float4*>(su)[threadIdx.x];
+  } else {
+    for (int i = threadIdx.x; i < 3 * nc; i += 256) dst[i] = su[i];
+  }
+}
+
+template <typename Z>
+__global__ void __launch_bounds__(256) k_join4(int n, const float* __restrict__ u, const float* __restrict__ p,
+                                               Z* __restrict__ z) {
+  __shared__ __align__(16) float su[3 * 256];
+  const int64_t c0 = (int64_t)blockIdx.x * 256;
+  const int64_t c = c0 + threadIdx.x;
+  const int nc = (int)min((int64_t)256, (int64_t)n - c0);
+  const float* src = u + c0 * 3;
+  if (nc == 256) {
+    if (threadIdx.x < 192) reinterpret_cast<float4*>(su)[threadIdx.x] = __ldcs(reinterpret_cast<const float4*>(src) + threadIdx.x);
+  } else {
+    for (int i = threadIdx.x; i < 3 * nc; i += 256) su[i] = src[i];
+  }
+  __syncthreads();
+  if (c < n) {
+    const float pv = __ldcs(p + c);
+    if constexpr (std::is_same_v<Z, float>) {
+      reinterpret_cast<float4*>(z)[c] = make_float4(su[3 * threadIdx.x], su[3 * threadIdx.x + 1], su[3 * threadIdx.x + 2], pv);
+    } else {
+      double2* o = reinterpret_cast<double2*>(z + c * 4);
+      o[0] = make_double2(su[3 * threadIdx.x], su[3 * threadIdx.x + 1]);
+      o[1] = make_double2(su[3 * threadIdx.x + 2], pv);
+    }
+  }
+}
+
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
                   cudaStream_t s) {
   if (n == 0) return;
   ProfScope ps_(prof_name("split", b, AMG_F64, xt), (double)n * b * (8.0 + dtype_size(xt)), s);
+  if (b == 4 && pc == 3 && xt == AMG_F32) {
+    k_split4<<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, (float*)ru, (float*)rp);
+    AMG_CK_LAUNCH();
+    return;
+  }
   dispatch_t(xt, [&](auto xx) {
     using X = decltype(xx);
     k_split<X><<<grid_for((int64_t)n * b, 256), 256, 0, s>>>(n, b, pc, r, scale, (X*)ru, (X*)rp);
@@ -409,6 +543,12 @@ void launch_split(int32_t n, int b, int pc, const double* r, double scale, void*
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt, cudaStream_t s) {
   if (n == 0) return;
   ProfScope ps_(prof_name("join", b, zt, xt), (double)n * b * (dtype_size(zt) + dtype_size(xt)), s);
+  if (b == 4 && pc == 3 && xt == AMG_F32) {
+    if (zt == AMG_F32) k_join4<float><<<grid_for(n, 256), 256, 0, s>>>(n, (const float*)u, (const float*)p, (float*)z);
+    else k_join4<double><<<grid_for(n, 256), 256, 0, s>>>(n, (const float*)u, (const float*)p, (double*)z);
+    AMG_CK_LAUNCH();
+    return;
+  }
   dispatch_t(xt, [&](auto xx) {
     using X = decltype(xx);
     dispatch_t(zt, [&](auto zz) {

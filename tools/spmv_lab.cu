@@ -358,6 +358,66 @@ __global__ void __launch_bounds__(256) k_lane_p(int n, const int* __restrict__ p
   if (r < B) y[(int64_t)row * B + r] = acc;
 }
 
+// F: sliced BSR (SELL-C, C = 32/B rows per warp) + COLS: step j of slice s holds
+// [i][g][r] = A_{row g, block j}[i][r] (i < B block rows, g < C rows, r < B columns):
+// every value load of a warp is 4 * C * B contiguous bytes.  scol[s][j][g].
+template <int B, int U, typename V, typename X>
+__global__ void __launch_bounds__(256) k_sell_col(int n, int nslices, const int* __restrict__ sptr /*[nslices+1] steps offset*/,
+                                                  const int* __restrict__ scol, const V* __restrict__ sval,
+                                                  const X* __restrict__ x, double* __restrict__ y) {
+  constexpr int C = 32 / B;
+  const int lane = threadIdx.x & 31;
+  const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (s >= nslices) return;
+  const int g = lane / B, r = lane - g * B;
+  const bool act = g < C;
+  const int j0 = __ldg(sptr + s), j1 = __ldg(sptr + s + 1);
+  double acc[B] = {};
+  const int L = act ? lane : 0;
+  int j = j0;
+#pragma unroll 1
+  for (; j + U <= j1; j += U) {
+    int c[U];
+    V a[U][B];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = __ldg(scol + (int64_t)(j + u) * C + (act ? g : 0));
+#pragma unroll
+      for (int i = 0; i < B; ++i) a[u][i] = __ldcs(sval + ((int64_t)(j + u) * B + i) * (C * B) + L);
+    }
+    X xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + (int64_t)c[u] * B + r);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < B; ++i) acc[i] = fma((double)a[u][i], (double)xv[u], acc[i]);
+  }
+#pragma unroll 1
+  for (; j < j1; ++j) {
+    const int c = __ldg(scol + (int64_t)j * C + (act ? g : 0));
+    const X xv = __ldg(x + (int64_t)c * B + r);
+#pragma unroll
+    for (int i = 0; i < B; ++i) acc[i] = fma((double)__ldcs(sval + ((int64_t)j * B + i) * (C * B) + L), (double)xv, acc[i]);
+  }
+  const int base = lane - r;
+  double sum = acc[0];
+#pragma unroll
+  for (int i = 1; i < B; ++i)
+    if (i == r) sum = acc[i];
+#pragma unroll
+  for (int d = 1; d < B; ++d) {
+    const int want = (r + B - d) % B;
+    double v = acc[0];
+#pragma unroll
+    for (int i = 1; i < B; ++i)
+      if (i == want) v = acc[i];
+    sum += __shfl_sync(0xffffffffu, v, base + (r + d) % B);
+  }
+  const int row = s * C + g;
+  if (act && row < n) y[(int64_t)row * B + r] = sum;
+}
+
 template <class F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b;
@@ -430,6 +490,53 @@ void run(int n, int st) {
     check("lib lane RC4", t);
     t = timeit([&] { amgb::k_bsr_lane<B, B, 2, false, false, V, X, false, amgb::LEpiSpmv<double>><<<((N + 32 / B - 1) / (32 / B) * 32 + 255) / 256, 256>>>(N, ptr, col, val, x, e); }, 20);
     check("lib lane RC2", t);
+  }
+  {
+    constexpr int C = 32 / B;
+    const int64_t ns = (N + C - 1) / C;
+    std::vector<int> hcol(Z);
+    CK(cudaMemcpy(hcol.data(), col, Z * 4, cudaMemcpyDeviceToHost));
+    std::vector<V> hval((size_t)Z * B * B);
+    CK(cudaMemcpy(hval.data(), val, (size_t)Z * B * B * sizeof(V), cudaMemcpyDeviceToHost));
+    std::vector<int> sp(ns + 1, 0);
+    for (int64_t s2 = 0; s2 < ns; ++s2) {
+      int mx = 0;
+      for (int g = 0; g < C && s2 * C + g < N; ++g) mx = std::max(mx, hp[s2 * C + g + 1] - hp[s2 * C + g]);
+      sp[s2 + 1] = sp[s2] + mx;
+    }
+    const int64_t steps = sp[ns];
+    std::vector<int> sc((size_t)steps * C, 0);
+    std::vector<V> sv((size_t)steps * B * C * B, V(0));
+    for (int64_t s2 = 0; s2 < ns; ++s2)
+      for (int g = 0; g < C; ++g) {
+        const int64_t row = s2 * C + g;
+        const int len = row < N ? hp[row + 1] - hp[row] : 0;
+        for (int j = 0; j < sp[s2 + 1] - sp[s2]; ++j) {
+          const int64_t st = sp[s2] + j;
+          if (j < len) {
+            const int64_t k = hp[row] + j;
+            sc[st * C + g] = hcol[k];
+            for (int i = 0; i < B; ++i)
+              for (int r = 0; r < B; ++r) sv[(st * B + i) * (C * B) + g * B + r] = hval[k * B * B + i * B + r];
+          } else {
+            sc[st * C + g] = row < N ? (int)row : 0;
+          }
+        }
+      }
+    int *dsp, *dsc;
+    V* dsv;
+    CK(cudaMalloc(&dsp, (ns + 1) * 4));
+    CK(cudaMalloc(&dsc, steps * C * 4));
+    CK(cudaMalloc(&dsv, steps * B * C * B * sizeof(V)));
+    CK(cudaMemcpy(dsp, sp.data(), (ns + 1) * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dsc, sc.data(), steps * C * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dsv, sv.data(), steps * B * C * B * sizeof(V), cudaMemcpyHostToDevice));
+    printf("  SELL: %lld steps, padding %.1f%%\n", (long long)steps, 100.0 * ((double)steps * C / Z - 1.0));
+    t = timeit([&] { k_sell_col<B, 2, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+    check("sell_col U=2", t);
+    t = timeit([&] { k_sell_col<B, 4, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+    check("sell_col U=4", t);
+    cudaFree(dsp); cudaFree(dsc); cudaFree(dsv);
   }
 #define LANEBNC(U)                                                                                              \
   t = timeit([&] { k_lane_bnc<B, U, V, X><<<((N + 32 / B - 1) / (32 / B) * 32 + 255) / 256, 256>>>(N, ptr, col, val, x, y1); }, 20); \
