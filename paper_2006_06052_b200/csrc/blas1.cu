@@ -6,6 +6,7 @@
 #include "prof.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace amgb {
 
@@ -166,6 +167,139 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
   reduce_finish<KA>(acc, KA, partials, ticket, out, post, inv);
 }
 
+// ---- wide variant for many basis vectors (k > 12) ----
+// The K-templated k_cgs keeps all k values of an element in one thread: past k ~ 13 the
+// compiler no longer issues all loads before the arithmetic (measured 2.6-4.5 TB/s at
+// k = 16..29).  Here the 8 warps of a 256-thread block split the VECTORS (warp w owns
+// j = w + 8q, q < NJ) and the block walks chunks of 256 elements: every lane holds NJ x 8
+// values in registers, each load of a warp is 256 contiguous bytes, and the update
+// sum_j c_j s_j V_j is combined across warps through shared memory in a fixed order.
+constexpr int kTW = 256, kCW = 256;  // threads, elements per chunk
+
+__device__ __forceinline__ void finish_partials(int kout, double* partials, unsigned* ticket, double* out, int post,
+                                                double* inv) {
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)nblk - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = warp; j < kout; j += blockDim.x / 32) {
+    double v = 0.0;
+    for (int i = lane; i < nblk; i += 32) v += __ldcg(partials + (int64_t)j * nblk + i);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    if (lane == 0) {
+      if (post >= 1) v = sqrt(v);
+      out[j] = v;
+      if (post == 2 && j == 0) inv[0] = 1.0 / v;
+    }
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+template <int NJ, int MODE>
+__global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V, const double* __restrict__ sc,
+                                                     const double* __restrict__ coef, const double* w, double* w_out,
+                                                     double* partials, unsigned* ticket, double* out, int post,
+                                                     double* inv) {
+  constexpr int T = kCW / 32;  // elements per lane per chunk
+  __shared__ double c[32], sv[32];
+  __shared__ double part[8][kCW + 1];
+  __shared__ double vs[kCW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < k) {
+    sv[threadIdx.x] = sc ? sc[threadIdx.x] : 1.0;
+    c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
+  }
+  __syncthreads();
+  const double* vp[NJ];
+  bool own[NJ];
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) {
+    const int j = warp + 8 * q;
+    own[q] = j < k;
+    vp[q] = own[q] ? V.p[j] : V.p[0];
+  }
+  double acc[NJ];
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) acc[q] = 0.0;
+  double nrm = 0.0;
+  for (int64_t i0 = (int64_t)blockIdx.x * kCW; i0 < n; i0 += (int64_t)gridDim.x * kCW) {
+    const bool full = i0 + kCW <= n;
+    double val[NJ][T];
+#pragma unroll
+    for (int q = 0; q < NJ; ++q)
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int64_t i = i0 + lane + 32 * t;
+        val[q][t] = (own[q] && (full || i < n)) ? __ldcs(vp[q] + i) : 0.0;
+      }
+    const int64_t it = i0 + threadIdx.x;
+    const double wv = (it < n) ? w[it] : 0.0;
+    if constexpr (MODE == 0) {
+      vs[threadIdx.x] = wv;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NJ; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[q] = fma(val[q][t], vs[lane + 32 * t], acc[q]);
+      __syncthreads();
+    } else {
+      // partial update of this warp's vectors, element e = lane + 32 t
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        double p = 0.0;
+#pragma unroll
+        for (int q = 0; q < NJ; ++q) p = fma(c[own[q] ? warp + 8 * q : 0] * (own[q] ? 1.0 : 0.0), val[q][t], p);
+        part[warp][lane + 32 * t] = p;
+      }
+      __syncthreads();
+      double v = wv;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) v -= part[ww][threadIdx.x];
+      if (it < n) w_out[it] = v;
+      if constexpr (MODE == 2) {
+        nrm = fma(v, v, nrm);
+      } else {
+        vs[threadIdx.x] = v;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NJ; ++q)
+#pragma unroll
+          for (int t = 0; t < T; ++t) acc[q] = fma(val[q][t], vs[lane + 32 * t], acc[q]);
+      }
+      __syncthreads();  // part / vs reused by the next chunk
+    }
+  }
+  if constexpr (MODE == 2) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
+    if (lane == 0) part[0][warp] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += part[0][ww];
+      partials[blockIdx.x] = s;
+    }
+    finish_partials(1, partials, ticket, out, post, inv);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      double v = acc[q];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+      const int j = warp + 8 * q;
+      if (lane == 0 && own[q]) partials[(int64_t)j * gridDim.x + blockIdx.x] = v * sv[j];
+    }
+    finish_partials(k, partials, ticket, out, post, inv);
+  }
+}
+
 template <int K = 1, class F>
 void dispatch_k(int k, F&& f) {
   if (k == K) f(std::integral_constant<int, K>{});
@@ -177,6 +311,20 @@ template <int MODE>
 void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                 double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s) {
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  static const int wide_from = [] {
+    const char* e = getenv("AMG_CGS_WIDE");
+    return e ? atoi(e) : 13;
+  }();
+  if (k >= wide_from) {
+    const int64_t work = (n + kCW - 1) / kCW;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * kSMs, (int64_t)kMaxPartials, work}));
+    auto go = [&](auto kern) { kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv); };
+    if (k <= 16) go(k_cgs_wide<2, MODE>);
+    else if (k <= 24) go(k_cgs_wide<3, MODE>);
+    else go(k_cgs_wide<4, MODE>);
+    AMG_CK_LAUNCH();
+    return;
+  }
   dispatch_k(k, [&](auto Kc) {
     constexpr int K = decltype(Kc)::value;
     constexpr int U = cgs_unroll<K>();

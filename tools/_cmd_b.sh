@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for v in "4 1 0" "3 1 0" "4 0 0" "3 0 0" "4 1 1" "3 1 1"; do python tools/spmv_probe.py $v 20; done 2>&1 | grep GBs
-python tools/solve_profile.py 5 256 > gpurun_out/prof5.txt 2>&1; head -30 gpurun_out/prof5.txt
+timeout 900 python -m pytest tests/test_gpu_solver.py tests/test_gpu_dist.py -x -q 2>&1 | tail -2
+python tools/solve_profile.py 5 256 > gpurun_out/prof5.txt 2>&1; head -5 gpurun_out/prof5.txt | tail -1
+grep -E "^(mdot|cgs)" gpurun_out/prof5.txt | sort -t_ -k3 | awk '{printf "%s:%s ", $1, $6}'; echo
+AMG_CGS_WIDE=9 python tools/solve_profile.py 5 256 > gpurun_out/prof5w9.txt 2>&1; head -5 gpurun_out/prof5w9.txt | tail -1
+grep -E "^(mdot|cgs)" gpurun_out/prof5w9.txt | sort -t_ -k3 | awk '{printf "%s:%s ", $1, $6}'; echo
