@@ -95,6 +95,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def ncu_traffic(key: str):
+    """DRAM bytes per launch (read + write) of a kernel from the committed `ncu --set full`
+    capture (profiles/traffic.json, written from tools/_bench_evidence.sh), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[key]["traffic"]
+    except Exception:
+        return None
+
+
 def make_problem(cfg: int, n: int, row_begin: int, row_end: int):
     kind = gen.POISSON3 if cfg == 1 else gen.STOKES
     ptr, col, val = gen.matrix(kind, n, None, row_begin, row_end)
@@ -323,7 +333,8 @@ def main():
         "e2e": {"value": e2e_s, "unit": "s/solve", "h2d_bytes_per_step": 2 * bh.numel() * 8,
                 "d2h_bytes_per_step": bh.numel() * 8},
         "roofline": {"bound": "hbm", "kernel": top["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": ncu_traffic(f"{top['kernel']}@cfg{args.cfg}") if n == 256 else None,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, one launch)", "peak_source": peak_src,
                      "share_of_step": top["total_ms"] / tot_ms, "bytes_per_launch": top["bytes"],
                      "avg_launch_ms": avg_ms},
         "top_kernels": [{"kernel": p["kernel"], "launches": p["launches"], "ms": round(p["total_ms"], 4),
@@ -336,6 +347,7 @@ def main():
         torch.cuda.empty_cache()
         out["spmv"] = spmv_cfg2(amg, torch)
         out["spmv"]["frac"] = out["spmv"]["GBs"] / peak
+        out["spmv"]["traffic"] = ncu_traffic("spmv_cfg2_b4_f32xf64")
     if not args.no_cpu_baseline:
         c = oracle_sample(args.cfg, n, args.cpu_n, rep.iters)
         out["cpu_baseline"] = {"value": c["value"], "unit": "s/solve", "cores": 1, "kind": "oracle",

@@ -126,9 +126,15 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
 
 void amg_destroy(struct amg_handle* h);
 
-/* SpMV plan: analyses A's row tiles once (one reduction + one stream sync) so that
- * repeated products run the TMA-staged kernel.  The plan keeps A's device pointers:
- * A's arrays must stay allocated and unchanged while the plan is used. */
+/* SpMV plan for repeated products y = alpha A x + beta y (same semantics and errors as
+ * bsr_spmv; §4 block layout PAPER.md:644-682).  Creation picks the
+ * kernel from the block shape and row length and, for long rows (> 12 blocks per row,
+ * enough rows to fill the GPU, square b = 2..4), builds a SLICED copy of A's blocks
+ * (32/b consecutive block rows per slice, zero-padded to the slice's longest row) that
+ * the plan owns and frees in bsr_plan_destroy (device memory ~= A's values + columns;
+ * one stream sync).  The plan also keeps A's device pointers: A's arrays must stay
+ * allocated and unchanged while the plan is used.  Errors: AMG_EINVAL (bad A / NULL
+ * out), AMG_EINDEX_OVERFLOW (sliced copy beyond 2^31 steps), AMG_ENOMEM, AMG_ECUDA. */
 struct bsr_plan;
 int bsr_plan_create(const amg_bsr* A /* host struct, device arrays */, void* stream, struct bsr_plan** out);
 int bsr_plan_spmv(struct bsr_plan* P, double alpha, const void* x, int32_t xt, double beta, void* y,
@@ -138,7 +144,7 @@ void bsr_plan_destroy(struct bsr_plan* P);
 /* ---- introspection (used by the parity tests; all outputs HOST) ---- */
 /* out[5] = {n_block_rows, block_size, nnzb(A_l), nnzb(P_l) or 0, n_coarse or 0} */
 int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);
-/* which: 0 = A_l, 1 = P_l, 2 = R_l (fp64 setup values); 3 = smoother blocks M_l
+/* which: 0 = A_l, 1 = P_l, 2 = R_l (the solve copies in the hierarchy dtype, widened to fp64); 3 = smoother blocks M_l
  * (ptr/col ignored, val = n*b*b).  Arrays sized from amg_level_info. */
 int amg_level_export(struct amg_handle* h, int32_t level, int32_t which, int32_t* ptr, int32_t* col,
                      double* val);
