@@ -166,7 +166,8 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena) {
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     const double lo = env_int("AMG_SELL_MIN_ROW", 12), hi = env_int("AMG_SELL_MAX_ROW", 64);
-    if (arena && square && per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= (int64_t)kSMs * 8 &&
+    const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 8);
+    if (arena && square && per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices &&
         !env_int("AMG_NO_SELL", 0) && !env_int("AMG_LANE_VAR", 0))
       build_sell(A, *arena, s);
   }

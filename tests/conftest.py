@@ -85,3 +85,20 @@ def laplace3_blocks(n, b=3, noise=None):
         for k in range(ptr[i], ptr[i + 1]):
             val[k] = (6.0 if col[k] == i else -1.0) * np.eye(b)
     return ptr, col, val
+
+
+@pytest.fixture
+def envvars():
+    """Set library tuning switches (read at plan / launch time) for one test."""
+    saved = {}
+
+    def set_(**kv):
+        for k, v in kv.items():
+            saved.setdefault(k, os.environ.get(k))
+            os.environ[k] = str(v)
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v

@@ -244,3 +244,18 @@ def test_fp32_vs_fp64_iteration_parity(amg):
         assert rep.converged
         its.append(rep.iters)
     assert abs(its[0] - its[1]) <= 1
+
+
+@pytest.mark.parametrize("wide", [1, 99])
+def test_solve_forced_kernel_paths(amg, envvars, wide):
+    # sliced copies on every long-row level (small grid: lower the slice-count gate) and
+    # the wide (wide=1) or K-templated (wide=99) CGS2 kernels at every k
+    envvars(AMG_SELL_MIN_SLICES=1, AMG_CGS_WIDE=wide)
+    n = 24
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)

@@ -190,3 +190,52 @@ def test_plan_spmv_cfg2_full_size(amg):
     ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
     assert _relerr(_run_plan(amg, ptr, col, val, x, 1, 0, 0), ref) <= 1e-5
     assert _relerr(_run_plan(amg, ptr, col, val, x, 0, 0, 0), ref) <= 1e-12
+
+
+# ---- every kernel variant of bsr_lane.cuh, forced (the plan picks one per shape) ----
+def _ragged_bsr(rng, n, b):
+    """rows of 0, 1..5 and 20..90 blocks (empty, short and long rows in one matrix)"""
+    ptr = np.zeros(n + 1, np.int32)
+    cols = []
+    for i in range(n):
+        r = i % 9
+        L = 0 if r == 4 else (int(rng.integers(1, 6)) if r < 6 else int(rng.integers(20, 91)))
+        c = np.unique(np.concatenate([[i], rng.integers(0, n, L)]))[:max(L, 0)] if L else np.zeros(0, int)
+        cols.append(np.sort(c))
+        ptr[i + 1] = ptr[i] + len(c)
+    col = np.concatenate(cols).astype(np.int32)
+    return ptr, col, rng.standard_normal((len(col), b, b))
+
+
+@pytest.mark.parametrize("var", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_spmv_lane_variants(amg, rng, envvars, var, b):
+    envvars(AMG_LANE_VAR=var)
+    ptr, col, val = _ragged_bsr(rng, 700, b)
+    x = rng.uniform(-1, 1, 700 * b)
+    y0 = rng.standard_normal(700 * b)
+    for vt, xt, yt in ((0, 0, 0), (1, 0, 0), (1, 1, 1)):
+        y = _run(amg, ptr, col, val, x, vt, xt, yt, -0.5, 2.0, y0)
+        vv = _r32(val) if vt == amg.F32 else val
+        xx = _r32(x) if xt == amg.F32 else x
+        yy = _r32(y0) if yt == amg.F32 else y0
+        ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, -0.5, 2.0, yy)
+        assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (var, b, vt, xt, yt)
+
+
+@pytest.mark.parametrize("b", [2, 3, 4])
+def test_spmv_sliced_copy(amg, rng, envvars, b):
+    # force the sliced copy (k_bsr_sell) on a small ragged matrix: empty, short and long
+    # rows in one slice, ragged last slice
+    envvars(AMG_SELL_MIN_ROW=0, AMG_SELL_MAX_ROW=100000, AMG_SELL_MIN_SLICES=1)
+    n = 1003
+    ptr, col, val = _ragged_bsr(rng, n, b)
+    x = rng.uniform(-1, 1, n * b)
+    y0 = rng.standard_normal(n * b)
+    for vt, xt, yt in ((0, 0, 0), (1, 0, 0), (1, 1, 1)):
+        y = _run_plan(amg, ptr, col, val, x, vt, xt, yt, 0.75, -1.0, y0)
+        vv = _r32(val) if vt == amg.F32 else val
+        xx = _r32(x) if xt == amg.F32 else x
+        yy = _r32(y0) if yt == amg.F32 else y0
+        ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, 0.75, -1.0, yy)
+        assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (b, vt, xt, yt)
