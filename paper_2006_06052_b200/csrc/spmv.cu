@@ -94,7 +94,10 @@ void set_lane_plan(Mat& A) {
   else if (br == 3 && bc == 3) var = per_row > 12.0 ? kLaneCN4 : kLaneCN2;
   else if (br == bc) var = kLaneRN4;
   else var = f32 ? kLaneRN2 : kLaneRC2;
-  if (per_row > 64.0) var = kLaneW;
+  // very long rows, or long rows on a matrix too small to fill the GPU with row-lane
+  // warps (coarse levels): one warp per row
+  const double lane_warps = (double)A.n / (32 / std::max(br, 1));
+  if (per_row > 64.0 || (per_row > 12.0 && lane_warps < (double)kSMs * 64)) var = kLaneW;
   A.lane_var = env_int("AMG_LANE_VAR", var);
 }
 
@@ -166,7 +169,9 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena) {
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     const double lo = env_int("AMG_SELL_MIN_ROW", 12), hi = env_int("AMG_SELL_MAX_ROW", 64);
-    const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 8);
+    // >= 64 slices per SM: below that the per-slice step chains are latency bound and
+    // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
+    const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
     if (arena && square && per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices &&
         !env_int("AMG_NO_SELL", 0) && !env_int("AMG_LANE_VAR", 0))
       build_sell(A, *arena, s);

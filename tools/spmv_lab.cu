@@ -314,6 +314,43 @@ __global__ void __launch_bounds__(256) k_lane_col(int n, const int* __restrict__
   if (valid) y[(int64_t)row * B + r] = s;
 }
 
+// G: B lanes per row, whole short row (<= UMAX blocks) loaded in ONE round: predicated
+// col/value loads, then predicated x gathers; MINB = min blocks/SM for the register budget
+template <int B, int UMAX, int MINB, typename V, typename X>
+__global__ void __launch_bounds__(256, MINB) k_lane_pre(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                                                   const V* __restrict__ val, const X* __restrict__ x, double* __restrict__ y) {
+  constexpr int RPW = 32 / B;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int row = warp * RPW + lane / B, r = lane % B;
+  if (lane >= RPW * B || row >= n) return;
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  double acc = 0.0;
+  for (int k = k0; k < k1; k += UMAX) {
+    int c[UMAX];
+    V a[UMAX][B];
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      const bool ok = k + u < k1;
+      c[u] = ok ? __ldg(col + k + u) : 0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) a[u][q] = ok ? __ldg(val + ((int64_t)(k + u) * B + r) * B + q) : V(0);
+    }
+    X xv[UMAX][B];
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u)
+#pragma unroll
+      for (int q = 0; q < B; ++q) xv[u][q] = (k + u < k1) ? __ldg(x + (int64_t)c[u] * B + q) : X(0);
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      float s2 = 0.f;
+#pragma unroll
+      for (int q = 0; q < B; ++q) s2 = fmaf((float)a[u][q], (float)xv[u][q], s2);
+      acc += (double)s2;
+    }
+  }
+  y[(int64_t)row * B + r] = acc;
+}
+
 // D: lane_r with the col/val loads of the next U-chunk issued before the current chunk's
 // x gathers are consumed (software pipelined)
 template <int B, int U, typename V, typename X>
@@ -538,6 +575,10 @@ void run(int n, int st) {
     check("sell_col U=4", t);
     cudaFree(dsp); cudaFree(dsc); cudaFree(dsv);
   }
+#define LANEPRE(U, M)                                                                                              \
+  t = timeit([&] { k_lane_pre<B, U, M, V, X><<<((N + 32 / B - 1) / (32 / B) * 32 + 255) / 256, 256>>>(N, ptr, col, val, x, y1); }, 20); \
+  check("lane_pre U=" #U " minb=" #M, t);
+  LANEPRE(4, 8) LANEPRE(4, 4) LANEPRE(8, 4) LANEPRE(8, 2) LANEPRE(7, 4)
 #define LANEBNC(U)                                                                                              \
   t = timeit([&] { k_lane_bnc<B, U, V, X><<<((N + 32 / B - 1) / (32 / B) * 32 + 255) / 256, 256>>>(N, ptr, col, val, x, y1); }, 20); \
   check("lane_bnc U=" #U, t);
