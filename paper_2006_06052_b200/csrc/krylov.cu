@@ -46,8 +46,9 @@ struct Ctx {
     launch_residual(h.A, b, x, r, AMG_F64, s);
     bytes += h.alg_bytes_spmv + 8.0 * N;
   }
-  void pc(const double* r, void* z, int zt, double scale = 1.0) {
-    precond_apply(h, r, z, zt, s, scale);
+  // scale_dev (device, optional): r is scaled by *scale_dev while narrowing (GMRES's 1/||V_j||)
+  void pc(const double* r, void* z, int zt, const double* scale_dev = nullptr) {
+    precond_apply_graphed(h, r, z, zt, s, scale_dev);
     bytes += h.alg_bytes_precond + N * ((double)dtype_size(zt) - 8.0);
   }
   void axpby(double a, const double* x, double b, double* y) {
@@ -273,7 +274,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     int j = 0;
     bool stop = false;
     for (; j < m && !stop; ++j) {
-      c.pc(h.V[j], h.Z[j], h.zt, s_host);  // z_j = M(v_j), v_j = s_j V_j
+      c.pc(h.V[j], h.Z[j], h.zt, sc + j);  // z_j = M(v_j), v_j = s_j V_j (s_j on the device)
       double* w = h.V[j + 1];
       c.spmv(h.Z[j], h.zt, w);
       PtrList Vl{};
@@ -338,7 +339,24 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
 
 }  // namespace
 
-int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t s, amg_report* rep) {
+int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t caller, amg_report* rep) {
+  // the solve runs on the handle's own non-blocking stream (graph capture is not allowed on
+  // the legacy default stream), ordered after / before the caller's stream by two events
+  cudaStream_t s = h.work ? h.work : caller;
+  if (s != caller) {
+    AMG_CK(cudaEventRecord(h.ev_in, caller));
+    AMG_CK(cudaStreamWaitEvent(s, h.ev_in, 0));
+  }
+  struct Join {
+    Handle& h;
+    cudaStream_t s, caller;
+    ~Join() {
+      if (s != caller) {
+        cudaEventRecord(h.ev_out, s);
+        cudaStreamWaitEvent(caller, h.ev_out, 0);
+      }
+    }
+  } join{h, s, caller};
   Ctx c(h, s);
   // ||b||; ||b|| = 0 -> x = 0, converged, relres 0
   launch_dot(c.N, b, AMG_F64, b, AMG_F64, h.partials, h.dscal, true, s, h.comm);

@@ -40,11 +40,13 @@ void launch_schur_u(const Mat& BTm, const void* ru, const void* p, void* ru2, in
 // (nu = b-1 comps, type xt) and the pressure part (type xt), narrowing RNE; optional
 // scale (used to fold a GMRES normalisation in).
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
-                  cudaStream_t s);
+                  cudaStream_t s, const double* scale_dev = nullptr);
 // K9' join (u, p) -> interleaved fp64 z (exact widening)
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt,
                  cudaStream_t s);
 // convert a whole vector between dtypes (narrowing RNE / exact widening); scale applied in fp64
-void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s);
+// scale_dev (device, optional) replaces scale: graph-replayable scaling
+void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s,
+                    const double* scale_dev = nullptr);
 
 }  // namespace amgb

@@ -13,7 +13,11 @@ Mat view_of(const amg_bsr* A);
 void set_last_error(const std::string& s);
 
 Handle::~Handle() {
-  if (pc_graph) cudaGraphExecDestroy(pc_graph);
+  for (PcGraph& G : pc_graphs)
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+  if (work) cudaStreamDestroy(work);
+  if (ev_in) cudaEventDestroy(ev_in);
+  if (ev_out) cudaEventDestroy(ev_out);
   for (Level& L : lv)
     if (L.halo.send_buf) L.halo.send_buf = nullptr;  // arena-owned
   if (ev0) cudaEventDestroy(ev0);
@@ -50,6 +54,9 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     h.rp = h.arena.alloc(std::max(h.n, 1) * xs);
     h.pp = h.arena.alloc(std::max(h.n + h.halo0.nghost, 1) * xs);
   }
+  AMG_CK(cudaStreamCreateWithFlags(&h.work, cudaStreamNonBlocking));
+  AMG_CK(cudaEventCreateWithFlags(&h.ev_in, cudaEventDisableTiming));
+  AMG_CK(cudaEventCreateWithFlags(&h.ev_out, cudaEventDisableTiming));
   AMG_CK(cudaEventCreate(&h.ev0));
   AMG_CK(cudaEventCreate(&h.ev1));
   (void)N;
@@ -193,15 +200,15 @@ int amg_solve_host(struct amg_handle* hh, const double* b_host, double* x_host, 
   // staging buffers live in the handle's workspace: vec[6], vec[7] are free outside a solve
   // only for CG; use dedicated ones
   static_assert(sizeof(double) == 8, "");
-  if (!h->pc_in) {
-    h->pc_in = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
-    h->pc_out = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
+  if (!h->stage_b) {
+    h->stage_b = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
+    h->stage_x = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
   }
-  AMG_CK(cudaMemcpyAsync(h->pc_in, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-  AMG_CK(cudaMemcpyAsync(h->pc_out, x_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-  int st = amg_solve(hh, h->pc_in, h->pc_out, rtol, stream, rep);
+  AMG_CK(cudaMemcpyAsync(h->stage_b, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  AMG_CK(cudaMemcpyAsync(h->stage_x, x_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  int st = amg_solve(hh, h->stage_b, h->stage_x, rtol, stream, rep);
   if (st < 0) return st;
-  AMG_CK(cudaMemcpyAsync(x_host, h->pc_out, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  AMG_CK(cudaMemcpyAsync(x_host, h->stage_x, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
   AMG_CK(cudaStreamSynchronize(s));
   return st;
   AMG_GUARD_END

@@ -44,6 +44,15 @@ struct Coarse {
 };
 
 
+struct PcGraph {
+  const double* r;
+  void* z;
+  int zt;
+  const double* sd;
+  cudaGraphExec_t exec;
+  int64_t kernels;
+};
+
 struct Handle {
   amg_params p{};
   int vt = AMG_F32, xt = AMG_F32;  // hier value dtype, V-cycle vector dtype
@@ -72,11 +81,11 @@ struct Handle {
   double* partials = nullptr;      // [kMaxPartials * 32]
   double* dscal = nullptr;         // device scalars [64]
   double* hscal = nullptr;         // pinned host mirror [64]
-  // CUDA graph of one preconditioner application (input/output = fixed buffers)
-  cudaGraphExec_t pc_graph = nullptr;
-  cudaStream_t pc_graph_stream = nullptr;
-  double* pc_in = nullptr;
-  double* pc_out = nullptr;
+  // CUDA graphs of the preconditioner application, one per (input, output, dtype, scale)
+  std::vector<PcGraph> pc_graphs;
+  cudaStream_t work = nullptr;     // non-blocking stream the Krylov solve runs on (graph capture)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  double *stage_b = nullptr, *stage_x = nullptr;  // amg_solve_host staging (allocated on first use)
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double setup_s = 0.0;
@@ -105,8 +114,11 @@ void coarse_allgather(Handle& h, cudaStream_t s);
 // V-cycle from level `level` on that level's f buffer; returns the buffer holding x
 void* vcycle_run(Handle& h, size_t level, cudaStream_t s);
 void* level0_f(Handle& h);
-// z = M r (outer fp64 r scaled by `scale`, z of dtype zt)
-void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale = 1.0);
+// z = M r (outer fp64 r scaled by `scale` or by *scale_dev when given, z of dtype zt)
+void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale = 1.0,
+                   const double* scale_dev = nullptr);
+// the same, replayed from a per-(r, z, zt, scale_dev) CUDA graph (s must not be the legacy stream)
+void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStream_t s, const double* scale_dev);
 double precond_bytes(const Handle& h);
 // krylov.cu
 int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t s, amg_report* rep);

@@ -452,8 +452,9 @@ void launch_schur_u(const Mat& BTm, const void* ru, const void* p, void* ru2, in
 
 // ---- K9: split / join of the interleaved outer vector ----
 template <typename X>
-__global__ void k_split(int n, int b, int pc, const double* __restrict__ r, double scale, X* __restrict__ ru,
-                        X* __restrict__ rp) {
+__global__ void k_split(int n, int b, int pc, const double* __restrict__ r, double scale_v, const double* scale_d,
+                        X* __restrict__ ru, X* __restrict__ rp) {
+  const double scale = scale_d ? *scale_d : scale_v;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * b) return;
   const int64_t I = t / b;
@@ -474,7 +475,8 @@ __global__ void k_join(int n, int b, int pc, const X* __restrict__ u, const X* _
 }
 
 template <typename I, typename O>
-__global__ void k_convert(int64_t N, const I* __restrict__ in, O* __restrict__ out, double scale) {
+__global__ void k_convert(int64_t N, const I* __restrict__ in, O* __restrict__ out, double scale_v, const double* scale_d) {
+  const double scale = scale_d ? *scale_d : scale_v;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
     out[t] = to_out<O>((double)in[t] * scale);
 }
@@ -482,8 +484,9 @@ __global__ void k_convert(int64_t N, const I* __restrict__ in, O* __restrict__ o
 // Hot shape (b = 4, pressure component 3, fp32 V-cycle vectors): thread per cell, one
 // 32-byte read of the cell, the velocity triples staged in shared memory and written
 // as float4 (coalesced), the pressure written directly.
-__global__ void __launch_bounds__(256) k_split4(int n, const double* __restrict__ r, double scale, float* __restrict__ ru,
-                                                float* __restrict__ rp) {
+__global__ void __launch_bounds__(256) k_split4(int n, const double* __restrict__ r, double scale_v,
+                                                const double* scale_d, float* __restrict__ ru, float* __restrict__ rp) {
+  const double scale = scale_d ? *scale_d : scale_v;
   __shared__ __align__(16) float su[3 * 256];
   const int64_t c0 = (int64_t)blockIdx.x * 256;
   const int64_t c = c0 + threadIdx.x;
@@ -532,17 +535,17 @@ __global__ void __launch_bounds__(256) k_join4(int n, const float* __restrict__ 
 }
 
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
-                  cudaStream_t s) {
+                  cudaStream_t s, const double* scale_dev) {
   if (n == 0) return;
   ProfScope ps_(prof_name("split", b, AMG_F64, xt), (double)n * b * (8.0 + dtype_size(xt)), s);
   if (b == 4 && pc == 3 && xt == AMG_F32) {
-    k_split4<<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, (float*)ru, (float*)rp);
+    k_split4<<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, scale_dev, (float*)ru, (float*)rp);
     AMG_CK_LAUNCH();
     return;
   }
   dispatch_t(xt, [&](auto xx) {
     using X = decltype(xx);
-    k_split<X><<<grid_for((int64_t)n * b, 256), 256, 0, s>>>(n, b, pc, r, scale, (X*)ru, (X*)rp);
+    k_split<X><<<grid_for((int64_t)n * b, 256), 256, 0, s>>>(n, b, pc, r, scale, scale_dev, (X*)ru, (X*)rp);
   });
   AMG_CK_LAUNCH();
 }
@@ -566,7 +569,8 @@ void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt,
   AMG_CK_LAUNCH();
 }
 
-void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s) {
+void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double scale, cudaStream_t s,
+                    const double* scale_dev) {
   if (N == 0) return;
   ProfScope ps_(prof_name("convert", 1, ot, it), (double)N * (dtype_size(it) + dtype_size(ot)), s);
   unsigned g = grid_for(N, 256);
@@ -575,7 +579,7 @@ void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double
     using I = decltype(ii);
     dispatch_t(ot, [&](auto oo) {
       using O = decltype(oo);
-      k_convert<I, O><<<g, 256, 0, s>>>(N, (const I*)in, (O*)out, scale);
+      k_convert<I, O><<<g, 256, 0, s>>>(N, (const I*)in, (O*)out, scale, scale_dev);
     });
   });
   AMG_CK_LAUNCH();

@@ -1,9 +1,11 @@
 // vcycle.cu -- the preconditioner applies: SA V(npre,npost) cycle (C9)
 // and the Schur pressure correction (Eq. 9a/9b).  Pure launches on
 // one stream; no allocation, no synchronisation (graph-capturable).
+#include <cstdlib>
 #include <utility>
 
 #include "ops.h"
+#include "prof.h"
 #include "solver.h"
 
 namespace amgb {
@@ -49,20 +51,21 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
 // z = M r.  Monolithic AMG: narrow r once (RNE), V-cycle, widen exactly (C9).
 // Schur (C10): split + narrow; u* = V(r_u); p = m_S o (r_p - B u*); r_u' = r_u - B^T p;
 // u = V(r_u'); z = join(u, p).
-void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale) {
+void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale,
+                   const double* scale_dev) {
   const int64_t N = (int64_t)h.n * h.b;
   if (!h.amg_active) {
-    launch_convert(N, r, AMG_F64, z, zt, scale, s);
+    launch_convert(N, r, AMG_F64, z, zt, scale, s, scale_dev);
     return;
   }
   void* f0 = level0_f(h);
   if (!h.schur) {
-    launch_convert(N, r, AMG_F64, f0, h.xt, scale, s);
+    launch_convert(N, r, AMG_F64, f0, h.xt, scale, s, scale_dev);
     void* x = vcycle_run(h, 0, s);
     launch_convert(N, x, h.xt, z, zt, 1.0, s);
     return;
   }
-  launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s);                                 // K9
+  launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s, scale_dev);                      // K9
   void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
   halo_exchange(h, h.halo0, us, h.xt, h.nu, s);
   launch_schur_p(h.Bm, h.mS, h.rp, us, h.pp, h.xt, s);  // K10
@@ -70,6 +73,45 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   launch_schur_u(h.BTm, f0, h.pp, f0, h.xt, s);    // K11 (in place)
   void* u = vcycle_run(h, 0, s);                                                               // u = V(r_u')
   launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
+}
+
+// The same application replayed from a CUDA graph: one graph per (r, z, zt, scale_dev)
+// (the Krylov solvers use a handful of fixed workspace buffers: GMRES(m) has m), captured
+// on first use on the handle's work stream and kept for the handle's life.  Eager when a
+// communicator is attached (NCCL halo exchanges), while the per-kernel profiler is on, or
+// with AMG_NO_GRAPH=1.  The library launch counter advances by the graph's kernel count.
+void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStream_t s, const double* scale_dev) {
+  static const bool off = getenv("AMG_NO_GRAPH") != nullptr;
+  if (off || h.comm || g_prof || h.pc_graphs.size() >= 256) {
+    precond_apply(h, r, z, zt, s, 1.0, scale_dev);
+    return;
+  }
+  for (const PcGraph& G : h.pc_graphs)
+    if (G.r == r && G.z == z && G.zt == zt && G.sd == scale_dev) {
+      AMG_CK(cudaGraphLaunch(G.exec, s));
+      g_launches += G.kernels;
+      return;
+    }
+  PcGraph G{r, z, zt, scale_dev, nullptr, 0};
+  const int64_t l0 = g_launches;
+  cudaGraph_t graph = nullptr;
+  AMG_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    precond_apply(h, r, z, zt, s, 1.0, scale_dev);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  AMG_CK(cudaStreamEndCapture(s, &graph));
+  G.kernels = g_launches - l0;
+  g_launches = l0;
+  cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  AMG_CK(e);
+  h.pc_graphs.push_back(G);
+  AMG_CK(cudaGraphLaunch(G.exec, s));
+  g_launches += G.kernels;
 }
 
 // Algorithmic bytes of one preconditioner application:
