@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
-CG, BICGSTAB, GMRES = 0, 1, 2
+CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
 SPAI0, JACOBI = 0, 1
 OK, NOT_CONVERGED, EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EBREAKDOWN = 0, 1, -1, -2, -3, -4, -6
@@ -42,7 +42,7 @@ class Params(ctypes.Structure):
         ("smoother", ctypes.c_int32), ("jacobi_omega", ctypes.c_double), ("sa_omega", ctypes.c_double),
         ("eps_strong", ctypes.c_double), ("coarse_enough", ctypes.c_int32), ("max_levels", ctypes.c_int32),
         ("npre", ctypes.c_int32), ("npost", ctypes.c_int32), ("schur_p_component", ctypes.c_int32),
-        ("nparts", ctypes.c_int32),
+        ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
     ]
 
 
@@ -85,6 +85,7 @@ def lib():
             "orc_vcycle": (i32, [P, P, P]),
             "orc_precond": (i32, [P, P, P]),
             "orc_solve": (i32, [P, P, P, dbl, P, P]),
+            "orc_idrs_shadow": (i32, [i64, i32, i64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -196,6 +197,13 @@ def roots(A: Mat, eps=1e-3, nparts=1):
     r = np.empty(n, dtype=np.int32)
     lib().orc_roots(A.h, eps, nparts, _p(r))
     return r
+
+
+def idrs_shadow(n: int, s: int, base: int) -> np.ndarray:
+    """IDR(s) shadow space [s][n] (counter RNG stream 6, MGS-orthonormalised)."""
+    out = np.zeros((s, n))
+    lib().orc_idrs_shadow(n, s, base, _p(out))
+    return out
 
 
 def block_inverse(blk):

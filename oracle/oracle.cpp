@@ -49,6 +49,8 @@ extern "C" void orc_params_default(orc_params* p) {
   p->npost = 1;
   p->schur_p_component = 3;
   p->nparts = 1;
+  p->idrs_s = 5;
+  p->idrs_seed = 1234;
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -1149,6 +1151,176 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
   return status;
 }
 
+// ---- IDR(s) (Table 1: the paper's outer solver for V1-V4, s = 5;
+// "We use the IDR(s) solver [sonneveld2009idr]").  Reading R17: the
+// bi-orthogonal IDR(s) of van Gijzen & Sonneveld (ACM TOMS 38(1) 5, 2011, "an elegant
+// IDR(s) variant that efficiently exploits bi-orthogonality properties"), right
+// preconditioned, omega by "maintaining the convergence" with kappa = 0.7,
+// no residual smoothing.  Shadow space P: s vectors of N(0,1) draws of the
+// counter RNG (below; stream 6, idx = (64 seed + s restarts + j) N + i), orthonormalised
+// by modified Gram-Schmidt.  One iteration = one product with A (and one preconditioner
+// application): s per IDR cycle plus the dimension-reduction step.  Stop on the
+// recurrence ||r|| <= rtol ||b||, then verify the true residual; if it fails, restart
+// the cycle from r = b - A x.  Breakdown (M_kk = 0, omega = 0, non-finite) -> one restart
+// with a fresh shadow space, then ORC_EBREAKDOWN.
+//
+// Counter RNG (written out here, independently of gen/): SplitMix64
+// finaliser mix, R(stream, idx) = mix(mix(SEED ^ (stream << 56)) ^ idx), SEED = 200606052,
+// U01 = (R >> 11) 2^-53, N01 = sqrt(-2 ln(1 - U01(2 idx))) cos(2 pi U01(2 idx + 1)).
+static uint64_t rng_mix(uint64_t z) {  // the SplitMix64 finaliser (no increment)
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static double rng_u01(uint64_t stream, uint64_t idx) {
+  const uint64_t r = rng_mix(rng_mix(200606052ULL ^ (stream << 56)) ^ idx);
+  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
+}
+static double rng_n01(uint64_t stream, uint64_t idx) {
+  const double u1 = 1.0 - rng_u01(stream, 2 * idx), u2 = rng_u01(stream, 2 * idx + 1);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+static void idrs_shadow(int64_t N, int sdim, uint64_t base, vector<vector<double>>& P) {
+  P.assign(sdim, vector<double>(N));
+  for (int j = 0; j < sdim; ++j) {
+    for (int64_t i = 0; i < N; ++i) P[j][i] = rng_n01(6, (base + (uint64_t)j) * (uint64_t)N + (uint64_t)i);
+    for (int l = 0; l < j; ++l) {  // modified Gram-Schmidt
+      const double d = dot(P[l], P[j]);
+      for (int64_t i = 0; i < N; ++i) P[j][i] = P[j][i] - d * P[l][i];
+    }
+    const double nr = nrm2(P[j]);
+    for (int64_t i = 0; i < N; ++i) P[j][i] = P[j][i] / nr;
+  }
+}
+
+static int solve_idrs(const orc_solver& s, const double* bp, double* xp, double rtol, orc_report* rep,
+                      double* hist) {
+  const int64_t N = (int64_t)s.A.n * s.A.b;
+  const int sd = s.p.idrs_s;
+  const double kappa = 0.7;
+  vector<double> b(bp, bp + N), x(xp, xp + N), r(N), v(N), vh(N), t(N);
+  const double nb = nrm2(b);
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  double nr = nrm2(r);
+  if (hist) hist[0] = nr / nb;
+  int it = 0, restarts = 0, status = ORC_NOT_CONVERGED;
+  if (nr <= rtol * nb) status = ORC_OK;
+  vector<vector<double>> P, G(sd, vector<double>(N, 0.0)), U(sd, vector<double>(N, 0.0));
+  vector<double> M((size_t)sd * sd, 0.0), f(sd), c(sd);
+  uint64_t base = 64ULL * (uint64_t)s.p.idrs_seed;
+  idrs_shadow(N, sd, base, P);
+  auto reset = [&]() {
+    for (int j = 0; j < sd; ++j) std::fill(G[j].begin(), G[j].end(), 0.0), std::fill(U[j].begin(), U[j].end(), 0.0);
+    std::fill(M.begin(), M.end(), 0.0);
+    for (int j = 0; j < sd; ++j) M[(size_t)j * sd + j] = 1.0;
+  };
+  reset();
+  double om = 1.0;
+  // true-residual check after the recurrence converged; false -> restart the cycle
+  auto converged_true = [&]() -> bool {
+    residual(s.A, b.data(), x.data(), r.data(), false);
+    if (nrm2(r) <= rtol * nb) return true;
+    reset();
+    om = 1.0;
+    return false;
+  };
+  auto breakdown = [&]() -> bool {  // true -> restarted, false -> give up
+    if (restarts >= 1) return false;
+    ++restarts;
+    residual(s.A, b.data(), x.data(), r.data(), false);
+    base += (uint64_t)sd;
+    idrs_shadow(N, sd, base, P);
+    reset();
+    om = 1.0;
+    return true;
+  };
+  while (status != ORC_OK && it < s.p.maxiter) {
+    for (int i = 0; i < sd; ++i) f[i] = dot(P[i], r);
+    bool restart_cycle = false;
+    for (int k = 0; k < sd && status != ORC_OK && it < s.p.maxiter; ++k) {
+      // lower-triangular solve M[k:s, k:s] c = f[k:s]
+      for (int i = k; i < sd; ++i) {
+        double a = f[i];
+        for (int l = k; l < i; ++l) a = a - M[(size_t)i * sd + l] * c[l];
+        c[i] = a / M[(size_t)i * sd + i];
+      }
+      for (int64_t q = 0; q < N; ++q) {
+        double a = r[q];
+        for (int i = k; i < sd; ++i) a = a - c[i] * G[i][q];
+        v[q] = a;
+      }
+      precond(s, v.data(), vh.data());
+      for (int64_t q = 0; q < N; ++q) {
+        double a = om * vh[q];
+        for (int i = k; i < sd; ++i) a = a + c[i] * U[i][q];
+        U[k][q] = a;
+      }
+      spmv(s.A, 1.0, U[k].data(), 0.0, G[k].data(), false);
+      for (int i = 0; i < k; ++i) {  // bi-orthogonalise G_k against P_0..P_{k-1}
+        const double alpha = dot(P[i], G[k]) / M[(size_t)i * sd + i];
+        for (int64_t q = 0; q < N; ++q) G[k][q] = G[k][q] - alpha * G[i][q];
+        for (int64_t q = 0; q < N; ++q) U[k][q] = U[k][q] - alpha * U[i][q];
+      }
+      for (int i = k; i < sd; ++i) M[(size_t)i * sd + k] = dot(P[i], G[k]);
+      const double mkk = M[(size_t)k * sd + k];
+      if (mkk == 0.0 || !is_fin(mkk)) {
+        if (breakdown()) {
+          restart_cycle = true;
+          break;
+        }
+        status = ORC_EBREAKDOWN;
+        break;
+      }
+      const double beta = f[k] / mkk;
+      for (int64_t q = 0; q < N; ++q) r[q] = r[q] - beta * G[k][q];
+      for (int64_t q = 0; q < N; ++q) x[q] = x[q] + beta * U[k][q];
+      ++it;
+      nr = nrm2(r);
+      if (hist) hist[it] = nr / nb;
+      if (nr <= rtol * nb) {
+        if (converged_true()) status = ORC_OK;
+        restart_cycle = true;
+        break;
+      }
+      for (int i = k + 1; i < sd; ++i) f[i] = f[i] - beta * M[(size_t)i * sd + k];
+    }
+    if (status == ORC_OK || status == ORC_EBREAKDOWN || restart_cycle || it >= s.p.maxiter) continue;
+    // dimension reduction: v = M^-1 r, t = A v, omega ("maintaining the convergence")
+    precond(s, r.data(), vh.data());
+    spmv(s.A, 1.0, vh.data(), 0.0, t.data(), false);
+    const double tr = dot(t, r), tt = dot(t, t), nt = std::sqrt(tt);
+    om = tr / tt;
+    const double rho = std::fabs(tr) / (nt * nr);
+    if (rho < kappa) om = om * kappa / rho;
+    if (om == 0.0 || !is_fin(om)) {
+      if (breakdown()) continue;
+      status = ORC_EBREAKDOWN;
+      break;
+    }
+    for (int64_t q = 0; q < N; ++q) r[q] = r[q] - om * t[q];
+    for (int64_t q = 0; q < N; ++q) x[q] = x[q] + om * vh[q];
+    ++it;
+    nr = nrm2(r);
+    if (hist) hist[it] = nr / nb;
+    if (nr <= rtol * nb && converged_true()) status = ORC_OK;
+  }
+  std::copy(x.begin(), x.end(), xp);
+  rep->iters = it;
+  rep->restarts = restarts;
+  residual(s.A, b.data(), x.data(), r.data(), false);
+  rep->relres_true = nrm2(r) / nb;
+  rep->converged = status == ORC_OK;
+  return status;
+}
+
+extern "C" int orc_idrs_shadow(int64_t n, int32_t sdim, int64_t base, double* out) {
+  vector<vector<double>> P;
+  idrs_shadow(n, sdim, (uint64_t)base, P);
+  for (int j = 0; j < sdim; ++j) std::copy(P[j].begin(), P[j].end(), out + (int64_t)j * n);
+  return ORC_OK;
+}
+
 extern "C" int orc_solve(const orc_solver* s, const double* b, double* x, double rtol,
                          orc_report* rep, double* history) {
   const int64_t N = (int64_t)s->A.n * s->A.b;
@@ -1167,6 +1339,7 @@ extern "C" int orc_solve(const orc_solver* s, const double* b, double* x, double
     case ORC_CG: return solve_cg(*s, b, x, rtol, rep, history);
     case ORC_BICGSTAB: return solve_bicgstab(*s, b, x, rtol, rep, history);
     case ORC_GMRES: return solve_gmres(*s, b, x, rtol, rep, history);
+    case ORC_IDRS: return solve_idrs(*s, b, x, rtol, rep, history);
     default: return ORC_EINVAL;
   }
 }

@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-enum { ORC_CG = 0, ORC_BICGSTAB = 1, ORC_GMRES = 2 };
+enum { ORC_CG = 0, ORC_BICGSTAB = 1, ORC_GMRES = 2, ORC_IDRS = 3 };
 enum { ORC_PC_AMG = 0, ORC_PC_SCHUR = 1, ORC_PC_NONE = 2 };
 enum { ORC_SPAI0 = 0, ORC_JACOBI = 1 };
 
@@ -42,6 +42,8 @@ typedef struct {
   int32_t npre, npost;   /* 1, 1 */
   int32_t schur_p_component; /* 3 */
   int32_t nparts;        /* rank-local aggregation: number of contiguous block-row slabs (1 = global) */
+  int32_t idrs_s;        /* IDR(s) shadow-space dimension (5, PAPER.md Listing V1-V4 "prm.solver.s = 5") */
+  int32_t idrs_seed;     /* IDR(s) shadow-space seed (1234) */
 } orc_params;
 
 typedef struct {
@@ -104,6 +106,8 @@ int orc_vcycle(const orc_solver* s, const double* f, double* x);
 int orc_precond(const orc_solver* s, const double* r, double* z);
 /* solve A x = b to relres rtol from the given x (x0), fills rep.  history (optional,
  * length maxiter+1) receives the per-iteration residual estimate ||r||/||b||. */
+/* IDR(s) shadow space (tests): s orthonormal vectors [sdim][n] of the counter RNG, stream 6 */
+int orc_idrs_shadow(int64_t n, int32_t sdim, int64_t base, double* out);
 int orc_solve(const orc_solver* s, const double* b, double* x, double rtol, orc_report* rep,
               double* history);
 

@@ -469,7 +469,7 @@ def test_schur_decoupled_exact_one_iteration(rng):
 
 
 # ---------------------------------------------------------------- C11 Krylov
-@pytest.mark.parametrize("solver", [oracle.CG, oracle.BICGSTAB, oracle.GMRES])
+@pytest.mark.parametrize("solver", [oracle.CG, oracle.BICGSTAB, oracle.GMRES, oracle.IDRS])
 def test_identity_one_iteration(rng, solver):
     n = 50
     A = oracle.Mat.from_arrays(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
@@ -488,13 +488,13 @@ def test_zero_rhs(rng):
 
 
 @pytest.mark.parametrize("solver,kind", [(oracle.CG, gen.POISSON3), (oracle.BICGSTAB, gen.STOKES),
-                                         (oracle.GMRES, gen.STOKES)])
+                                         (oracle.GMRES, gen.STOKES), (oracle.IDRS, gen.STOKES)])
 def test_dense_solve_small(rng, solver, kind):
     # <= 2000 unknowns, coarse_enough lowered so that a real hierarchy is exercised (C7 caveat)
     n = 7 if kind == gen.POISSON3 else 6
     ptr, col, val = gen.matrix(kind, n)
     A = oracle.Mat.from_arrays(ptr, col, val)
-    pc = oracle.PC_SCHUR if solver == oracle.GMRES else oracle.PC_AMG
+    pc = oracle.PC_SCHUR if solver in (oracle.GMRES, oracle.IDRS) else oracle.PC_AMG
     S = oracle.Solver(A, solver=solver, precond=pc, coarse_enough=64)
     assert S.levels >= 2
     b = rng.standard_normal(len(ptr) * 0 + (len(ptr) - 1) * val.shape[-1])
@@ -513,6 +513,55 @@ def test_gmres_finite_termination(rng):
     assert r.converged and r.iters <= n
 
 
+# ---- IDR(s) (Table 1: the paper's outer solver; reading R17) ----
+def test_idrs_shadow_space_rng_and_orthonormal():
+    # the oracle's own counter RNG equals gen/'s (same formula, written twice) and the
+    # shadow space is orthonormal; P_0 is the normalised draw vector
+    n, s, base = 300, 5, 64 * 1234
+    P = oracle.idrs_shadow(n, s, base)
+    assert np.abs(P @ P.T - np.eye(s)).max() <= 1e-14
+    d0 = np.array([gen.n01(6, base * n + i) for i in range(n)])
+    assert np.allclose(P[0], d0 / np.linalg.norm(d0), rtol=0, atol=1e-15)
+    d1 = np.array([gen.n01(6, (base + 1) * n + i) for i in range(n)])
+    q = d1 - (P[0] @ d1) * P[0]
+    assert np.allclose(P[1], q / np.linalg.norm(q), rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8])
+def test_idrs_finite_termination(rng, s):
+    # IDR(s) reaches the exact solution in at most N + N/s products with A (Sonneveld &
+    # van Gijzen 2008, Theorem 2.2 / the dimension argument); nonsymmetric dense A
+    n = 16
+    ptr, col, val = random_bsr(rng, n, 1, density=1.0, dom=6)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, solver=oracle.IDRS, idrs_s=s, precond=oracle.PC_NONE)
+    b = rng.standard_normal(n)
+    r = S.solve(b, rtol=1e-11)
+    assert r.converged and r.iters <= n + n // s
+    assert np.allclose(r.x, np.linalg.solve(A.dense(), b), rtol=0, atol=1e-9 * np.abs(r.x).max())
+
+
+def test_idrs_1d_poisson_dense(rng):
+    # SPEC.md:325 example: 1-D Poisson n = 50, no preconditioner, vs a dense solve
+    ptr, col, val = poisson1d(50)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S = oracle.Solver(A, solver=oracle.IDRS, precond=oracle.PC_NONE)
+    b = rng.standard_normal(50)
+    r = S.solve(b, rtol=1e-10)
+    xd = np.linalg.solve(A.dense(), b)
+    assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
+def test_idrs_deterministic_and_seeded(rng):
+    ptr, col, val = gen.matrix(gen.STOKES, 6)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    b = gen.rhs(gen.RHS_LID_NOISE, 6, 4)
+    runs = [oracle.Solver(A, solver=oracle.IDRS, precond=oracle.PC_SCHUR, coarse_enough=100, idrs_seed=sd).solve(b)
+            for sd in (1234, 1234, 99)]
+    assert np.array_equal(runs[0].x, runs[1].x) and runs[0].iters == runs[1].iters
+    assert not np.array_equal(runs[0].x, runs[2].x) and all(r.converged for r in runs)
+
+
 def test_gmres_true_residual_monotone(rng):
     ptr, col, val = gen.matrix(gen.STOKES, 8)
     A = oracle.Mat.from_arrays(ptr, col, val)
@@ -528,6 +577,7 @@ def test_gmres_true_residual_monotone(rng):
     (gen.POISSON3, oracle.CG, oracle.PC_AMG, gen.RHS_UNIFORM),
     (gen.STOKES, oracle.BICGSTAB, oracle.PC_AMG, gen.RHS_LID),
     (gen.STOKES, oracle.GMRES, oracle.PC_SCHUR, gen.RHS_FORCE_NOISE),
+    (gen.STOKES, oracle.IDRS, oracle.PC_SCHUR, gen.RHS_FORCE_NOISE),  # V3 -> V4 of Table 1
 ])
 def test_fp32_hierarchy_iteration_parity(kind, solver, pc, rhs):
     # mixed precision "does not increase the number of iterations"
