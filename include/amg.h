@@ -41,7 +41,7 @@ enum {
 };
 
 typedef enum { AMG_F64 = 0, AMG_F32 = 1 } amg_dtype;
-enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2 };
+enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2, AMG_IDRS = 3 };
 enum { AMG_PC_AMG = 0, AMG_PC_SCHUR = 1, AMG_PC_NONE = 2 };
 enum { AMG_SPAI0 = 0, AMG_JACOBI = 1 };
 
@@ -64,7 +64,8 @@ typedef struct {
 /* Runtime parameters: a flat version of the paper's nested params structs
  * (Listings 2-3).  Fill with amg_params_default(). */
 typedef struct {
-  int32_t solver;            /* AMG_CG | AMG_BICGSTAB | AMG_GMRES (flexible GMRES(m)) */
+  int32_t solver;            /* AMG_CG | AMG_BICGSTAB | AMG_GMRES (flexible GMRES(m)) | AMG_IDRS
+                                (IDR(s), the paper's outer solver, Table 1) */
   int32_t gmres_m;           /* restart length, default 30 (PAPER.md:255 shows M = 50) */
   int32_t precond;           /* AMG_PC_AMG (monolithic SA-AMG) | AMG_PC_SCHUR (Eq. 9-10) | AMG_PC_NONE */
   int32_t maxiter;           /* default 1000 */
@@ -80,11 +81,14 @@ typedef struct {
   int32_t npre, npost;       /* smoothing sweeps, default 1, 1 */
   int32_t schur_p_component; /* pressure component inside a block, default 3 for (u,v,w,p) */
   int32_t use_graphs;        /* 1 (default): replay the preconditioner as a CUDA graph */
+  int32_t idrs_s;            /* IDR(s) shadow-space dimension, default 5 (Listings V1-V4 "s = 5") */
+  int32_t idrs_seed;         /* IDR(s) shadow-space seed, default 1234 (reading R17) */
   int32_t _pad;
 } amg_params;
 
 typedef struct {
-  int32_t iters;        /* Krylov iterations (GMRES: Arnoldi steps; BiCGStab: full steps) */
+  int32_t iters;        /* Krylov iterations (GMRES: Arnoldi steps; BiCGStab: full steps;
+                           IDR(s): products with A, s + 1 per cycle) */
   int32_t converged;    /* 1 iff relres_true <= rtol */
   int32_t levels;       /* AMG levels including the coarsest */
   int32_t restarts;     /* GMRES cycles - 1, or BiCGStab/CG restarts */

@@ -21,7 +21,7 @@ OK, NOT_CONVERGED = 0, 1
 EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EINDEX_OVERFLOW, EBREAKDOWN, ECUDA, ENCCL, ENOMEM = (
     -1, -2, -3, -4, -5, -6, -7, -8, -9)
 F64, F32 = 0, 1
-CG, BICGSTAB, GMRES = 0, 1, 2
+CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
 SPAI0, JACOBI = 0, 1
 
@@ -47,7 +47,7 @@ class amg_params(ctypes.Structure):
                 ("sa_omega", ctypes.c_double), ("eps_strong", ctypes.c_double),
                 ("max_levels", ctypes.c_int32), ("npre", ctypes.c_int32), ("npost", ctypes.c_int32),
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("_pad", ctypes.c_int32)]
+                ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class amg_report(ctypes.Structure):

@@ -532,4 +532,62 @@ void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double*
   AMG_CK_LAUNCH();
 }
 
+// ---- IDR(s) helpers ----
+// out = sum_t c_t in_t  (t < L.n <= 12 terms, host coefficients; out may alias an input:
+// every element is read before it is written, by the same thread)
+__global__ void __launch_bounds__(kT) k_lincomb(int64_t n, LinComb L, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    double v = L.c[0] * L.p[0][i];
+    for (int t = 1; t < L.n; ++t) v = fma(L.c[t], L.p[t][i], v);
+    out[i] = v;
+  }
+}
+
+void launch_lincomb(int64_t n, const LinComb& L, double* out, cudaStream_t s) {
+  if (n == 0 || L.n == 0) return;
+  ProfScope ps_(prof_name("lincomb", L.n, AMG_F64, -1), 8.0 * n * (L.n + 1), s);
+  k_lincomb<<<ew_grid(n), kT, 0, s>>>(n, L, out);
+  AMG_CK_LAUNCH();
+}
+
+// IDR(s) shadow vector: p[i] = N01(stream 6, idx = row * n_global + off + i) with the
+// counter RNG of SURVEY.md §8(d): SplitMix64 finaliser mix, R = mix(mix(SEED ^ (6 << 56)) ^ idx),
+// U01 = (R >> 11) 2^-53, Box-Muller on (1 - U01(2 idx), U01(2 idx + 1))
+__device__ __forceinline__ uint64_t rng_mix_d(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double rng_u01_d(uint64_t key, uint64_t idx) {
+  return (double)(rng_mix_d(key ^ idx) >> 11) * (1.0 / 9007199254740992.0);
+}
+__global__ void k_shadow(int64_t n, uint64_t row, uint64_t n_global, uint64_t off, double* p) {
+  const uint64_t key = rng_mix_d(200606052ULL ^ (6ULL << 56));
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const uint64_t idx = row * n_global + off + (uint64_t)i;
+    const double u1 = 1.0 - rng_u01_d(key, 2 * idx), u2 = rng_u01_d(key, 2 * idx + 1);
+    p[i] = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+  }
+}
+
+__global__ void k_axpy_dev(int64_t n, const double* __restrict__ d, const double* __restrict__ x, double* y) {
+  const double a = d[0];
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) y[i] = y[i] - a * x[i];
+}
+
+void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, uint64_t off, double* const* P,
+                       double* partials, double* dscal, cudaStream_t s, CommBase* comm) {
+  for (int j = 0; j < sdim; ++j) {
+    k_shadow<<<ew_grid(n), kT, 0, s>>>(n, base + (uint64_t)j, n_global, off, P[j]);
+    AMG_CK_LAUNCH();
+    for (int l = 0; l < j; ++l) {  // modified Gram-Schmidt
+      launch_dot(n, P[l], AMG_F64, P[j], AMG_F64, partials, dscal, false, s, comm);
+      k_axpy_dev<<<ew_grid(n), kT, 0, s>>>(n, dscal, P[l], P[j]);
+      AMG_CK_LAUNCH();
+    }
+    launch_dot(n, P[j], AMG_F64, P[j], AMG_F64, partials, dscal, true, s, comm);
+    launch_scale_by_inv(n, P[j], dscal, P[j], s);
+  }
+}
+
 }  // namespace amgb

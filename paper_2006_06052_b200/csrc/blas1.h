@@ -38,6 +38,17 @@ void launch_zupdate(int64_t n, int k, const PtrList& Z, int zt, const double* y,
 void launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s);
 void launch_axpbypcz(int64_t n, double a, const double* x, double b, const double* y, double c, double* z,
                      cudaStream_t s);
+// out = sum_t c[t] p[t]  (t < n <= 12; host coefficients; out may alias an input)
+struct LinComb {
+  int n;
+  double c[12];
+  const double* p[12];
+};
+void launch_lincomb(int64_t n, const LinComb& L, double* out, cudaStream_t s);
+// IDR(s) shadow space: P[j] = MGS-orthonormalised N(0,1) draws of the counter RNG
+// (stream 6, idx = (base + j) * n_global + off + i); dots over ranks via comm
+void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, uint64_t off, double* const* P,
+                       double* partials, double* dscal, cudaStream_t s, CommBase* comm);
 // y = x / sdev[0]
 void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s);
 

@@ -82,6 +82,8 @@ int amg_params_default(amg_params* p) {
   p->npost = 1;
   p->schur_p_component = 3;
   p->use_graphs = 1;
+  p->idrs_s = 5;
+  p->idrs_seed = 1234;
   return AMG_OK;
 }
 

@@ -275,6 +275,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
     h->bh = Gh->bh;
     h->comm = comm;
     h->row_lo = bounds[me];
+    h->n_global_rows = n_global;
     h->lbounds = Gh->lbounds;
     // outer operator
     h->A = slice_rows(h->arena, Gh->A, bounds[me], bounds[me + 1], s);

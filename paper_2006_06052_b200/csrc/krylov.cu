@@ -337,6 +337,171 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   return finish(c, b, x, h.V[0], nb, status, it, cycles > 0 ? cycles - 1 : 0, rep);
 }
 
+// ---- IDR(s) (the paper's outer solver, Table 1; reading R17) ----
+// Bi-orthogonal IDR(s) (van Gijzen & Sonneveld 2011), right preconditioned, omega by
+// "maintaining the convergence" (kappa = 0.7), the oracle's steps and stopping rules
+// (oracle.cpp solve_idrs).  The s x s matrix M = P^T G, f = P^T r and all small solves
+// live on the host; per inner step the device does: v = r - G c (lincomb), vh = M^-1 v
+// (graphed preconditioner), U_k = om vh + U c, G_k = A U_k, one multi-dot P^T G_k (the
+// bi-orthogonalisation coefficients follow from it and M by forward substitution, so the
+// sequential Gram-Schmidt dots of the oracle need no extra passes), the G_k / U_k / r / x
+// updates and ||r||.  Two host reads per inner step.
+int solve_idrs(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  const int sd = h.p.idrs_s;
+  const int64_t N = c.N;
+  const double kappa = 0.7;
+  double *r = h.vec[0], *v = h.vec[1], *vh = h.vec[2], *t = h.vec[3];
+  std::vector<double> M((size_t)sd * sd, 0.0), f(sd), cc(sd), al(sd), pg(sd);
+  const uint64_t n_global = (uint64_t)h.n_global_rows * h.b, off = (uint64_t)h.row_lo * h.b;
+  auto shadow = [&](uint64_t base) {
+    idrs_shadow_space(N, sd, base, n_global, off, h.Pi.data(), h.partials, h.dscal + 200, c.s, h.comm);
+    c.bytes += 8.0 * N * (1.0 + sd);
+  };
+  uint64_t base = 64ULL * (uint64_t)h.p.idrs_seed;
+  if (!h.idrs_ready || h.idrs_base != base) {  // the shadow space depends only on (seed, n): keep it
+    shadow(base);
+    h.idrs_base = base;
+    h.idrs_ready = true;
+  }
+  auto reset = [&]() {
+    for (int j = 0; j < sd; ++j) {
+      AMG_CK(cudaMemsetAsync(h.Gi[j], 0, sizeof(double) * N, c.s));
+      AMG_CK(cudaMemsetAsync(h.Ui[j], 0, sizeof(double) * N, c.s));
+    }
+    std::fill(M.begin(), M.end(), 0.0);
+    for (int j = 0; j < sd; ++j) M[(size_t)j * sd + j] = 1.0;
+  };
+  auto nrm_r = [&]() {
+    c.dot(r, r, 0, true);
+    c.read(1);
+    return h.hscal[0];
+  };
+  c.residual(b, x, r);
+  double nr = nrm_r();
+  int it = 0, restarts = 0, status = AMG_NOT_CONVERGED;
+  if (nr <= rtol * nb) status = AMG_OK;
+  reset();
+  double om = 1.0;
+  auto converged_true = [&]() -> bool {
+    c.residual(b, x, r);
+    if (nrm_r() <= rtol * nb) return true;
+    reset();
+    om = 1.0;
+    return false;
+  };
+  auto breakdown = [&]() -> bool {
+    if (restarts >= 1) return false;
+    ++restarts;
+    c.residual(b, x, r);
+    base += (uint64_t)sd;
+    shadow(base);
+    h.idrs_ready = false;  // the handle's next solve regenerates the seed's own space
+    reset();
+    om = 1.0;
+    return true;
+  };
+  PtrList Pl{};
+  for (int j = 0; j < sd; ++j) Pl.p[j] = h.Pi[j];
+  while (status != AMG_OK && it < h.p.maxiter) {
+    launch_mdot_scaled(N, sd, Pl, nullptr, r, h.partials, h.dscal, c.s, h.comm);  // f = P^T r
+    c.bytes += 8.0 * N * (sd + 1);
+    c.read(sd);
+    for (int i = 0; i < sd; ++i) f[i] = h.hscal[i];
+    bool restart_cycle = false;
+    for (int k = 0; k < sd && status != AMG_OK && it < h.p.maxiter; ++k) {
+      for (int i = k; i < sd; ++i) {  // M[k:s, k:s] c = f[k:s]
+        double a = f[i];
+        for (int l = k; l < i; ++l) a = a - M[(size_t)i * sd + l] * cc[l];
+        cc[i] = a / M[(size_t)i * sd + i];
+      }
+      LinComb L{};  // v = r - G[k:s] c
+      L.n = 0;
+      L.c[L.n] = 1.0, L.p[L.n++] = r;
+      for (int i = k; i < sd; ++i) L.c[L.n] = -cc[i], L.p[L.n++] = h.Gi[i];
+      launch_lincomb(N, L, v, c.s);
+      c.bytes += 8.0 * N * (L.n + 1);
+      c.pc(v, vh, AMG_F64);
+      L.n = 0;  // U_k = om vh + U[k:s] c   (U_k is read before it is written)
+      L.c[L.n] = om, L.p[L.n++] = vh;
+      for (int i = k; i < sd; ++i) L.c[L.n] = cc[i], L.p[L.n++] = h.Ui[i];
+      launch_lincomb(N, L, h.Ui[k], c.s);
+      c.bytes += 8.0 * N * (L.n + 1);
+      c.spmv(h.Ui[k], AMG_F64, h.Gi[k]);  // G_k = A U_k
+      launch_mdot_scaled(N, sd, Pl, nullptr, h.Gi[k], h.partials, h.dscal, c.s, h.comm);  // P^T G_k
+      c.bytes += 8.0 * N * (sd + 1);
+      c.read(sd);
+      for (int i = 0; i < sd; ++i) pg[i] = h.hscal[i];
+      // bi-orthogonalise: alpha_i = (P_i.G_k - sum_{l<i} alpha_l M_il) / M_ii, i < k
+      for (int i = 0; i < k; ++i) {
+        double a = pg[i];
+        for (int l = 0; l < i; ++l) a = a - al[l] * M[(size_t)i * sd + l];
+        al[i] = a / M[(size_t)i * sd + i];
+      }
+      if (k > 0) {
+        L.n = 0;
+        L.c[L.n] = 1.0, L.p[L.n++] = h.Gi[k];
+        for (int i = 0; i < k; ++i) L.c[L.n] = -al[i], L.p[L.n++] = h.Gi[i];
+        launch_lincomb(N, L, h.Gi[k], c.s);
+        L.p[0] = h.Ui[k];
+        for (int i = 0; i < k; ++i) L.p[1 + i] = h.Ui[i];
+        launch_lincomb(N, L, h.Ui[k], c.s);
+        c.bytes += 2.0 * 8.0 * N * (L.n + 1);
+      }
+      for (int i = k; i < sd; ++i) {  // M[i][k] = P_i . G_k after the update
+        double a = pg[i];
+        for (int l = 0; l < k; ++l) a = a - al[l] * M[(size_t)i * sd + l];
+        M[(size_t)i * sd + k] = a;
+      }
+      const double mkk = M[(size_t)k * sd + k];
+      if (mkk == 0.0 || !finite(mkk)) {
+        if (breakdown()) {
+          restart_cycle = true;
+          break;
+        }
+        status = AMG_EBREAKDOWN;
+        break;
+      }
+      const double beta = f[k] / mkk;
+      c.axpby(-beta, h.Gi[k], 1.0, r);  // r -= beta G_k
+      c.axpby(beta, h.Ui[k], 1.0, x);   // x += beta U_k
+      ++it;
+      nr = nrm_r();
+      if (nr <= rtol * nb) {
+        if (converged_true()) status = AMG_OK;
+        restart_cycle = true;
+        break;
+      }
+      for (int i = k + 1; i < sd; ++i) f[i] = f[i] - beta * M[(size_t)i * sd + k];
+    }
+    if (status == AMG_OK || status == AMG_EBREAKDOWN || restart_cycle || it >= h.p.maxiter) continue;
+    // dimension reduction: vh = M^-1 r, t = A vh, omega
+    c.pc(r, vh, AMG_F64);
+    c.spmv(vh, AMG_F64, t);
+    PtrList TR{};
+    TR.p[0] = t;
+    TR.p[1] = r;
+    launch_mdot_scaled(N, 2, TR, nullptr, t, h.partials, h.dscal, c.s, h.comm);  // t.t, r.t
+    c.bytes += 8.0 * N * 3;
+    c.read(2);
+    const double tt = h.hscal[0], tr = h.hscal[1], nt = std::sqrt(tt);
+    om = tr / tt;
+    const double rho = std::fabs(tr) / (nt * nr);
+    if (rho < kappa) om = om * kappa / rho;
+    if (om == 0.0 || !finite(om)) {
+      if (breakdown()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    c.axpby(-om, t, 1.0, r);
+    c.axpby(om, vh, 1.0, x);
+    ++it;
+    nr = nrm_r();
+    if (nr <= rtol * nb && converged_true()) status = AMG_OK;
+  }
+  return finish(c, b, x, r, nb, status, it, restarts, rep);
+}
+
 }  // namespace
 
 int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_t caller, amg_report* rep) {
@@ -373,6 +538,7 @@ int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_
     case AMG_CG: return solve_cg(c, b, x, rtol, nb, rep);
     case AMG_BICGSTAB: return solve_bicgstab(c, b, x, rtol, nb, rep);
     case AMG_GMRES: return solve_gmres(c, b, x, rtol, nb, rep);
+    case AMG_IDRS: return solve_idrs(c, b, x, rtol, nb, rep);
     default: fail(AMG_EINVAL, "unknown solver");
   }
 }

@@ -45,6 +45,15 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     for (int i = 0; i <= m; ++i) h.V.push_back(reinterpret_cast<double*>(slab + (size_t)i * (vbytes + stagger)));
     for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
   }
+  if (h.p.solver == AMG_IDRS) {
+    // IDR(s): shadow space P (N), G (N), U (with ghost space: U_k feeds the SpMV)
+    const int sd = h.p.idrs_s;
+    for (int i = 0; i < sd; ++i) {
+      h.Pi.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+      h.Gi.push_back(h.arena.alloc_n<double>(std::max<int64_t>(N, 1)));
+      h.Ui.push_back(h.arena.alloc_n<double>(std::max<int64_t>(Nx, 1)));
+    }
+  }
   h.partials = h.arena.alloc_n<double>((size_t)kMaxPartials * 32 + 8);  // + ticket (blas1.h)
   AMG_CK(cudaMemset(h.partials + (size_t)kMaxPartials * 32, 0, 8 * sizeof(double)));
   h.dscal = h.arena.alloc_n<double>(256);
@@ -73,7 +82,8 @@ double mat_bytes(const Mat& A, int vt) {
 
 int check_params(const amg_params* p) {
   if (!p) return AMG_EINVAL;
-  if (p->solver < AMG_CG || p->solver > AMG_GMRES) return AMG_EINVAL;
+  if (p->solver < AMG_CG || p->solver > AMG_IDRS) return AMG_EINVAL;
+  if (p->solver == AMG_IDRS && (p->idrs_s < 1 || p->idrs_s > 8)) return AMG_EINVAL;
   if (p->precond < AMG_PC_AMG || p->precond > AMG_PC_NONE) return AMG_EINVAL;
   if (p->solver == AMG_GMRES && (p->gmres_m < 1 || p->gmres_m > 31)) return AMG_EINVAL;
   if (p->npre < 1 || p->npost < 0 || p->max_levels < 1 || p->maxiter < 0) return AMG_EINVAL;
@@ -91,6 +101,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     h->vt = p->hier_dtype;
     h->xt = p->vcycle_vec_dtype;
     h->n = src.n;
+    h->n_global_rows = src.n;
     h->b = src.b;
     h->schur = p->precond == AMG_PC_SCHUR;
     h->pc = p->schur_p_component;

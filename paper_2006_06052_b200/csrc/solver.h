@@ -77,6 +77,10 @@ struct Handle {
   std::vector<double*> V;
   std::vector<void*> Z;
   int zt = AMG_F64;
+  // IDR(s) (AMG_IDRS): shadow space, G = A U, U (search directions); shadow seed base
+  std::vector<double*> Pi, Gi, Ui;
+  uint64_t idrs_base = 0;
+  bool idrs_ready = false;
   // reductions
   double* partials = nullptr;      // [kMaxPartials * 32]
   double* dscal = nullptr;         // device scalars [64]
@@ -95,6 +99,7 @@ struct Handle {
   Halo halo0;
   double* x_ext = nullptr;         // fp64 copy of the iterate with ghost space
   int64_t row_lo = 0;
+  int64_t n_global_rows = 0;       // global block rows (== n when not distributed)
   std::vector<std::vector<int64_t>> lbounds;
   Arena arena;
   ~Handle();

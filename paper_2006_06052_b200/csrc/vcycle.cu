@@ -82,7 +82,7 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
 // with AMG_NO_GRAPH=1.  The library launch counter advances by the graph's kernel count.
 void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStream_t s, const double* scale_dev) {
   static const bool off = getenv("AMG_NO_GRAPH") != nullptr;
-  if (off || h.comm || g_prof || h.pc_graphs.size() >= 256) {
+  if (off || !h.p.use_graphs || h.comm || g_prof || h.pc_graphs.size() >= 256) {
     precond_apply(h, r, z, zt, s, 1.0, scale_dev);
     return;
   }

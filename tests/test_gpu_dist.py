@@ -69,6 +69,7 @@ CASES = [
     ("amg-bicgstab", gen.STOKES, 16, gen.RHS_LID, dict(solver=1, precond=0)),
     ("amg-cg-f64", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=0, precond=0, hier_dtype=0, vcycle_vec_dtype=0,
                                                             coarse_enough=200)),
+    ("schur-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1)),
 ]
 
 

@@ -26,7 +26,7 @@ def amg():
 ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxiter": "maxiter",
           "smoother": "smoother", "sa_omega": "sa_omega", "eps_strong": "eps_strong",
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
-          "jacobi_omega": "jacobi_omega"}
+          "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed"}
 
 
 def make_pair(amg, ptr, col, val, hier32=True, **kw):
@@ -135,6 +135,12 @@ SOLVE_CASES = [
     ("cfg4-32", gen.STOKES, 32, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2), True),
     ("cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2), True),
     ("gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10), False),
+    # IDR(s): the paper's outer solver (Table 1), V4 = Schur PC + fp32 hierarchy
+    ("idrs5-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3), True),
+    ("idrs5-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=3), True),
+    ("idrs5-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=3), True),
+    ("idrs2-poisson-f64", gen.POISSON3, 12, gen.RHS_UNIFORM, dict(precond=0, solver=3, idrs_s=2), False),
+    ("idrs8-stokes-f64", gen.STOKES, 10, gen.RHS_LID_NOISE, dict(precond=1, solver=3, idrs_s=8, idrs_seed=7), False),
 ]
 
 
@@ -194,7 +200,7 @@ def test_single_level_exact(amg, rng):
 def test_identity_no_precond(amg, rng):
     n = 100
     A = amg.BSR.from_numpy(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), np.tile(np.eye(3), (n, 1, 1)))
-    for solver in (amg.CG, amg.BICGSTAB, amg.GMRES):
+    for solver in (amg.CG, amg.BICGSTAB, amg.GMRES, amg.IDRS):
         S = amg.Solver(A, amg.default_params(solver=solver, precond=amg.PC_NONE))
         b = rng.standard_normal(3 * n)
         x, rep = _solve(amg, S, b)
