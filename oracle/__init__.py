@@ -43,6 +43,7 @@ class Params(ctypes.Structure):
         ("eps_strong", ctypes.c_double), ("coarse_enough", ctypes.c_int32), ("max_levels", ctypes.c_int32),
         ("npre", ctypes.c_int32), ("npost", ctypes.c_int32), ("schur_p_component", ctypes.c_int32),
         ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
+        ("schur_u_scalar", ctypes.c_int32),
     ]
 
 
@@ -80,6 +81,7 @@ def lib():
             "orc_level_agg": (P, [P, i32]),
             "orc_level_M": (P, [P, i32]),
             "orc_schur_Au": (P, [P]),
+            "orc_schur_Au_amg": (P, [P]),
             "orc_schur_Shat_diag": (P, [P]),
             "orc_schur_mS": (P, [P]),
             "orc_vcycle": (i32, [P, P, P]),
@@ -266,6 +268,11 @@ class Solver:
 
     def schur_Au(self) -> Mat | None:
         h = lib().orc_schur_Au(self.h)
+        return Mat(h, owned=False) if h else None
+
+    def schur_Au_amg(self) -> Mat | None:
+        """The matrix the U-solver hierarchy is built on (A_u or its scalar expansion)."""
+        h = lib().orc_schur_Au_amg(self.h)
         return Mat(h, owned=False) if h else None
 
     def schur_vectors(self):

@@ -51,6 +51,7 @@ extern "C" void orc_params_default(orc_params* p) {
   p->nparts = 1;
   p->idrs_s = 5;
   p->idrs_seed = 1234;
+  p->schur_u_scalar = 0;
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -545,7 +546,7 @@ struct orc_solver {
   orc_mat Acoarse;          // coarsest matrix (fp64)
   Coarse coarse;
   // Schur split (C10) on A's block pattern
-  orc_mat Au;
+  orc_mat Au, Au_s;  // velocity block; its scalar expansion (schur_u_scalar)
   vector<double> Bv, BTv;   // nnz * 3 (row pc, cols vel) and (rows vel, col pc)
   vector<double> Shat_diag, mS;
   vector<double> Bs, BTs, mSs;
@@ -774,6 +775,35 @@ static int schur_setup(orc_solver& s) {
   return ORC_OK;
 }
 
+// Scalar expansion of A_u for the V2 U-solver (Listing V2: the scalar builtin<double>
+// backend; PAPER.md:660-672 shows the same matrix in both forms): block (I, J) entry
+// (r, c) becomes scalar (bu I + r, bu J + c); entries that are exactly zero inside a
+// stored block are not stored (the scalar CSR holds the structural non-zeros), the
+// diagonal always is.  Rows stay sorted (J ascending, then c).  Reading R18.
+static orc_mat scalar_expansion(const orc_mat& A) {
+  const int b = A.b;
+  orc_mat S;
+  S.n = A.n * b;
+  S.m = A.m * b;
+  S.b = 1;
+  S.ptr.assign((size_t)S.n + 1, 0);
+  for (int32_t I = 0; I < A.n; ++I)
+    for (int r = 0; r < b; ++r) {
+      const int32_t row = I * b + r;
+      for (int32_t k = A.ptr[I]; k < A.ptr[I + 1]; ++k)
+        for (int c = 0; c < b; ++c) {
+          const double v = A.blk(k)[r * b + c];
+          const int32_t colj = A.col[k] * b + c;
+          if (v != 0.0 || colj == row) {
+            S.col.push_back(colj);
+            S.val.push_back(v);
+          }
+        }
+      S.ptr[row + 1] = (int32_t)S.col.size();
+    }
+  return S;
+}
+
 // Eq. 9a then 9b with one application each:
 //   u* = V_u(r_u);  p = m_S o (r_p - B u*);  u = V_u(r_u - B^T p);  z = (u, p)
 static void schur_apply(const orc_solver& s, const double* r, double* z) {
@@ -844,7 +874,8 @@ extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out
   if (p->precond == ORC_PC_SCHUR) {
     s->schur = true;
     rc = schur_setup(*s);
-    if (rc == ORC_OK) rc = build_hierarchy(*s, s->Au);
+    if (rc == ORC_OK && p->schur_u_scalar) s->Au_s = scalar_expansion(s->Au);
+    if (rc == ORC_OK) rc = build_hierarchy(*s, p->schur_u_scalar ? s->Au_s : s->Au);
   } else if (p->precond == ORC_PC_AMG) {
     rc = build_hierarchy(*s, s->A);
   }
@@ -877,6 +908,9 @@ extern "C" const double* orc_level_M(const orc_solver* s, int32_t level) {
   return s->lv[level].M.data();
 }
 extern "C" const orc_mat* orc_schur_Au(const orc_solver* s) { return s->schur ? &s->Au : nullptr; }
+extern "C" const orc_mat* orc_schur_Au_amg(const orc_solver* s) {
+  return s->schur ? (s->p.schur_u_scalar ? &s->Au_s : &s->Au) : nullptr;
+}
 extern "C" const double* orc_schur_Shat_diag(const orc_solver* s) {
   return s->schur ? s->Shat_diag.data() : nullptr;
 }

@@ -44,6 +44,8 @@ typedef struct {
   int32_t nparts;        /* rank-local aggregation: number of contiguous block-row slabs (1 = global) */
   int32_t idrs_s;        /* IDR(s) shadow-space dimension (5, PAPER.md Listing V1-V4 "prm.solver.s = 5") */
   int32_t idrs_seed;     /* IDR(s) shadow-space seed (1234) */
+  int32_t schur_u_scalar; /* 1: the U-solver hierarchy is built on the SCALAR expansion of A_u
+                             (AMGCL V2, Listing V2); 0: on 3x3 blocks (V3/V4, Listing V3) */
 } orc_params;
 
 typedef struct {
@@ -95,6 +97,8 @@ const int32_t* orc_level_agg(const orc_solver* s, int32_t level);
 const double* orc_level_M(const orc_solver* s, int32_t level);
 /* Schur pieces: velocity matrix A_u (3x3 BSR), Shat diagonal (n), m_S (n); NULL if not Schur */
 const orc_mat* orc_schur_Au(const orc_solver* s);
+/* the matrix the U-solver hierarchy is built on (A_u, or its scalar expansion) */
+const orc_mat* orc_schur_Au_amg(const orc_solver* s);
 const double* orc_schur_Shat_diag(const orc_solver* s);
 const double* orc_schur_mS(const orc_solver* s);
 

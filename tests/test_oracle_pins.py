@@ -468,6 +468,29 @@ def test_schur_decoupled_exact_one_iteration(rng):
     assert res.converged and res.iters == 1
 
 
+def test_schur_scalar_u_solver_expansion(rng):
+    # V2 (Listing V2): the U-solver hierarchy on the scalar expansion of A_u -- the same
+    # operator (dense equality), zero entries inside stored blocks not stored (R18), and
+    # the V2 / V3 preconditioned solves both reach the dense solution
+    n = 5
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    S2 = oracle.Solver(A, precond=oracle.PC_SCHUR, solver=oracle.GMRES, schur_u_scalar=1, coarse_enough=40,
+                       hier_f32=0, vec_f32=0)
+    Au, As = S2.schur_Au(), S2.schur_Au_amg()
+    assert As.info()[2] == 1 and As.info()[0] == 3 * n ** 3
+    assert np.array_equal(As.dense(), Au.dense())
+    sp, sc, sv = As.to_arrays()
+    assert np.count_nonzero(sv.reshape(-1) == 0.0) == 0  # Laplacian x I3: only the diagonal couplings
+    assert S2.levels >= 2
+    b = rng.standard_normal(4 * n ** 3)
+    xd = np.linalg.solve(A.dense(), b)
+    for S in (S2, oracle.Solver(A, precond=oracle.PC_SCHUR, solver=oracle.GMRES, coarse_enough=40,
+                                hier_f32=0, vec_f32=0)):
+        r = S.solve(b, rtol=1e-10)
+        assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
 # ---------------------------------------------------------------- C11 Krylov
 @pytest.mark.parametrize("solver", [oracle.CG, oracle.BICGSTAB, oracle.GMRES, oracle.IDRS])
 def test_identity_one_iteration(rng, solver):
