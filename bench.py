@@ -141,18 +141,32 @@ def oracle_sample(cfg: int, n_full: int, n_sample: int, gpu_iters: int | None):
             "value": (t2 - t1) * scale * it_ratio, "n_sample": n_sample, "scale": scale, "it_ratio": it_ratio}
 
 
+def oracle_full_size(cfg: int):
+    """The oracle's own full-size run (tests/golden/oracle_full_size.json, written by
+    tools/oracle_reference_runs.py on the GPU box's host), or None."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "oracle_full_size.json")) as f:
+            return json.load(f).get(f"cfg{cfg}")
+    except Exception:
+        return None
+
+
 def run_reference(args, rank: int):
-    """--impl reference: the CPU oracle as it stands, each step a bounded sample of the
-    workload (n_sample^3 cells), scaled to the full cfg; rank 0 only."""
+    """--impl reference: the CPU oracle as it stands (1 thread), each step a bounded sample
+    of the workload (ref_n^3 cells), scaled to the full cfg by the cell count and by the
+    iteration count of the oracle's own full-size run when it is on record; rank 0 only."""
     if rank != 0:
         return
     n_full = args.n or gen.CONFIGS[args.cfg]["n"]
+    full = oracle_full_size(args.cfg) if n_full == gen.CONFIGS[args.cfg]["n"] else None
     vals = []
     for i in range(args.warmup + args.steps):
-        r = oracle_sample(args.cfg, n_full, args.ref_n, None)
+        r = oracle_sample(args.cfg, n_full, args.ref_n, full["iters"] if full else None)
         if i >= args.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
+    note = (f"; iterations scaled x{vals[0]['it_ratio']:.2f} to the oracle's full-size count {full['iters']} "
+            f"(its measured full-size solve: {full['solve_s']:.0f} s)" if full else "; same iteration count assumed")
     line = {
         "impl": "reference", "metric": metric_name(args.cfg, n_full), "value": v, "unit": "s/solve",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
@@ -160,7 +174,7 @@ def run_reference(args, rank: int):
         "data": "synthetic", "config": config_dict(args.cfg, n_full, args.gpus),
         "cpu_baseline": {"value": v, "unit": "s/solve", "cores": 1, "kind": "oracle",
                          "sample": f"oracle solve of the cfg-{args.cfg} generator at {args.ref_n}^3 cells "
-                                   f"(x{vals[0]['scale']:.0f} cells to {n_full}^3; same iteration count assumed), "
+                                   f"(x{vals[0]['scale']:.0f} cells to {n_full}^3{note}), "
                                    f"{vals[0]['iters']} its, {statistics.median([r['solve_s'] for r in vals]):.2f} s"},
         "e2e": {"value": v, "unit": "s/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

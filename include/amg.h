@@ -83,7 +83,9 @@ typedef struct {
   int32_t use_graphs;        /* 1 (default): replay the preconditioner as a CUDA graph */
   int32_t idrs_s;            /* IDR(s) shadow-space dimension, default 5 (Listings V1-V4 "s = 5") */
   int32_t idrs_seed;         /* IDR(s) shadow-space seed, default 1234 (reading R17) */
-  int32_t _pad;
+  int32_t schur_u_scalar;    /* 1: the Schur U-solver hierarchy is built on the SCALAR expansion of
+                                A_u (the paper's V2, Listing V2; R18); 0 (default): on
+                                3x3 blocks (V3, Listing V3; fp32 values = V4, Listing V4) */
 } amg_params;
 
 typedef struct {

@@ -47,7 +47,7 @@ class amg_params(ctypes.Structure):
                 ("sa_omega", ctypes.c_double), ("eps_strong", ctypes.c_double),
                 ("max_levels", ctypes.c_int32), ("npre", ctypes.c_int32), ("npost", ctypes.c_int32),
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32)]
 
 
 class amg_report(ctypes.Structure):

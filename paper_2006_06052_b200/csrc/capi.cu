@@ -84,6 +84,7 @@ int amg_params_default(amg_params* p) {
   p->use_graphs = 1;
   p->idrs_s = 5;
   p->idrs_seed = 1234;
+  p->schur_u_scalar = 0;
   return AMG_OK;
 }
 

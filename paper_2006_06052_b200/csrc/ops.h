@@ -10,7 +10,7 @@ namespace amgb {
 // long-row matrices also get the sliced copy (k_bsr_sell, allocated in the arena: one
 // sync); the opt-in TMA tile plan (AMG_TMA=1: one reduction + one sync)
 void set_lane_plan(Mat& A);
-void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena = nullptr);
+void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena = nullptr, bool want_tma = false);
 
 // K1  y = alpha A x + beta y
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,

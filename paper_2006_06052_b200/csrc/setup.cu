@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "ops.h"
@@ -626,6 +627,37 @@ void check_err(SetupCtx& c, const char* where) {
   if (e != 0) fail(e, where);
 }
 
+// Scalar expansion of a BSR matrix (the V2 U-solver, reading R18): block (I, J) entry
+// (r, c) -> scalar (b I + r, b J + c); exact zeros inside stored blocks dropped, the
+// diagonal kept; rows stay sorted (J ascending, then c).  Thread per scalar row.
+__global__ void k_expand_count(int n, int b, const int32_t* ptr, const int32_t* col, const double* val, int32_t* cnt) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= (int64_t)n * b) return;
+  const int I = (int)(row / b), r = (int)(row % b);
+  int32_t c0 = 0;
+  for (int32_t k = ptr[I]; k < ptr[I + 1]; ++k)
+    for (int c = 0; c < b; ++c)
+      if (val[((int64_t)k * b + r) * b + c] != 0.0 || (int64_t)col[k] * b + c == row) ++c0;
+  cnt[row] = c0;
+}
+__global__ void k_expand_fill(int n, int b, const int32_t* ptr, const int32_t* col, const double* val,
+                              const int32_t* sptr, int32_t* scol, double* sval) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= (int64_t)n * b) return;
+  const int I = (int)(row / b), r = (int)(row % b);
+  int32_t o = sptr[row];
+  for (int32_t k = ptr[I]; k < ptr[I + 1]; ++k)
+    for (int c = 0; c < b; ++c) {
+      const double v = val[((int64_t)k * b + r) * b + c];
+      const int64_t j = (int64_t)col[k] * b + c;
+      if (v != 0.0 || j == row) {
+        scol[o] = (int32_t)j;
+        sval[o] = v;
+        ++o;
+      }
+    }
+}
+
 // in-place exclusive scan of cnt[0..n] (cnt[n] := 0 first); returns the total
 int64_t scan(SetupCtx& c, int32_t* cnt, int n) {
   AMG_CK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t), c.s));
@@ -762,11 +794,33 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     launch_convert(A64.nnz * nu, btv, AMG_F64, h.BTv, h.vt, 1.0, s);
     launch_convert(A64.n, h.mS64, AMG_F64, h.mS, h.vt, 1.0, s);
     Amg = Au;
+    if (p.schur_u_scalar) {  // V2: the U-solver hierarchy on the scalar expansion of A_u
+      const int64_t ns = (int64_t)Au.n * nu;
+      if (ns >= INT32_MAX) fail(AMG_EINDEX_OVERFLOW, "scalar expansion of A_u");
+      int32_t* sptr = c.tmp.alloc_n<int32_t>(ns + 1);
+      if (ns > 0)
+        k_expand_count<<<grid_for(ns, kT), kT, 0, s>>>(Au.n, nu, Au.ptr, Au.col, (const double*)Au.val, sptr);
+      AMG_CK_LAUNCH();
+      const int64_t snnz = scan(c, sptr, (int)ns);
+      Mat As;
+      As.n = (int32_t)ns, As.m = (int32_t)((int64_t)Au.m * nu), As.b = 1, As.nnz = snnz, As.vt = AMG_F64;
+      As.ptr = sptr;
+      As.col = c.tmp.alloc_n<int32_t>(std::max<int64_t>(snnz, 1));
+      As.val = c.tmp.alloc_n<double>(std::max<int64_t>(snnz, 1));
+      if (ns > 0)
+        k_expand_fill<<<grid_for(ns, kT), kT, 0, s>>>(Au.n, nu, Au.ptr, Au.col, (const double*)Au.val, As.ptr,
+                                                       As.col, (double*)As.val);
+      AMG_CK_LAUNCH();
+      Amg = As;
+    }
   }
   h.bh = Amg.b;
 
-  // slab of every row (rank-local aggregation)
+  // slab of every row (rank-local aggregation); a scalar U-solver
+  // hierarchy has nu scalar rows per block row
   std::vector<int64_t> bounds = bounds0;
+  if (h.schur && p.schur_u_scalar)
+    for (int64_t& v : bounds) v *= h.nu;
   const int nparts = (int)bounds.size() - 1;
   h.lbounds.clear();
   h.lbounds.push_back(bounds);

@@ -26,7 +26,8 @@ def amg():
 ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxiter": "maxiter",
           "smoother": "smoother", "sa_omega": "sa_omega", "eps_strong": "eps_strong",
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
-          "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed"}
+          "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed",
+          "schur_u_scalar": "schur_u_scalar"}
 
 
 def make_pair(amg, ptr, col, val, hier32=True, **kw):
@@ -78,6 +79,9 @@ CASES = [
     ("cfg4-16", gen.STOKES, 16, dict(precond=1, solver=2), True),
     ("poisson-lowce", gen.POISSON3, 10, dict(precond=0, solver=0, coarse_enough=40), False),
     ("stokes-lowce-f64", gen.STOKES, 10, dict(precond=1, solver=2, coarse_enough=40), False),
+    # V2 of the paper's ladder: the U-solver hierarchy on the scalar expansion of A_u
+    ("stokes-v2-scalar-f64", gen.STOKES, 10, dict(precond=1, solver=3, schur_u_scalar=1, coarse_enough=40), False),
+    ("stokes-v2-scalar-16", gen.STOKES, 16, dict(precond=1, solver=3, schur_u_scalar=1), True),
 ]
 
 
@@ -141,6 +145,9 @@ SOLVE_CASES = [
     ("idrs5-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=3), True),
     ("idrs2-poisson-f64", gen.POISSON3, 12, gen.RHS_UNIFORM, dict(precond=0, solver=3, idrs_s=2), False),
     ("idrs8-stokes-f64", gen.STOKES, 10, gen.RHS_LID_NOISE, dict(precond=1, solver=3, idrs_s=8, idrs_seed=7), False),
+    # the paper's ladder: V2 (scalar fp64 U-solver), V3 (3x3 fp64), V4 (3x3 fp32), IDR(5) outer
+    ("ladder-v2", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3, schur_u_scalar=1), False),
+    ("ladder-v3", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3), False),
 ]
 
 

@@ -1,6 +1,6 @@
 """Per-kernel breakdown of one solve (library CUDA-event profiler, not a bench number).
 
-  python tools/solve_profile.py [cfg] [n]     e.g. 5 256 | 4 128 | 3 64
+  python tools/solve_profile.py [cfg] [n] [idrs]     e.g. 5 256 | 4 128 | 3 64 | 5 256 idrs
 Prints every (kernel, bytes/launch) record: launches, total ms, GB/s, share of the solve.
 """
 import os
@@ -20,7 +20,10 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else gen.CONFIGS[cfg]["n"]
 ptr, col, val, bvec = bench.make_problem(cfg, n, 0, n ** 3)
 A = amg.BSR.from_numpy(ptr, col, val)
 del val
-S = amg.Solver(A, bench.params_for(amg, cfg))
+prm = bench.params_for(amg, cfg)
+if len(sys.argv) > 3 and sys.argv[3] == "idrs":
+    prm.solver = amg.IDRS  # the paper's outer solver (Table 1), s = 5
+S = amg.Solver(A, prm)
 del A
 for l in range(S.levels):
     nb, bs, za, zp, nc = S.level_info(l)
