@@ -182,9 +182,11 @@ def test_plan_spmv_cfg2(amg, b):
         assert _relerr(_run_plan(amg, ptr, col, val, x, 1, 0, 0), ref) <= 1e-5
 
 
-def test_plan_spmv_cfg2_full_size(amg):
-    # BASELINE configs[1] at full size, the bench's launch configuration (plan, 4x4 fp32 x fp64)
-    n, b = 128, 4
+@pytest.mark.parametrize("b", [3, 4])
+def test_plan_spmv_cfg2_full_size(amg, b):
+    # BASELINE configs[1] at full size, the bench's launch configuration (plan: the sliced
+    # copy), fp32 values x fp64 x and fp64 x fp64, both block sizes the config names
+    n = 128
     ptr, col, val = gen.matrix(gen.RAND27, n, b)
     x = gen.rhs(gen.X_UNIFORM, n, b)
     ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)
