@@ -192,7 +192,7 @@ def config_dict(cfg, n, gpus):
                         f"{'Schur pressure correction' if pc == 'schur' else 'SA-AMG'}, "
                         f"{'fp32' if cfg != 1 else 'fp64'} hierarchy, rtol 1e-8, x0 = 0",
             "unknowns": 4 * n ** 3 if cfg != 1 else 3 * n ** 3, "parallelism": f"z-slabs x{gpus}",
-            "l2": f"inputs larger than L2 (outer matrix {27 * n ** 3 * 132 / 7 / 1e9 * 7 / 27:.1f} GB fp64, 126 MB L2); no flush"}
+            "l2": f"inputs larger than L2 (outer matrix {7 * n ** 3 * 132 / 1e9:.1f} GB fp64, 126 MB L2); no flush"}
 
 
 def spmv_cfg2(amg, torch, n=128, reps=30):
