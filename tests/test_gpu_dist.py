@@ -105,3 +105,23 @@ def test_dist_p1_equals_single(amg):
     out, x, relres, _ = run_dist(amg, 1, gen.STOKES, n, gen.RHS_LID_NOISE, solver=2, precond=1)
     assert out[0][0].iters == r1.iters
     assert np.array_equal(x, x1.cpu().numpy())
+
+
+def test_nccl_communicator_single_rank(amg):
+    # the NCCL communicator itself (ncclCommInitRank from amg_comm_unique_id) on one rank:
+    # amg_setup_dist + solve through it equals the single-device solve
+    n = 12
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    N = n ** 3
+    comm = amg.Comm(0, 1)
+    A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=N)
+    S = amg.Solver(A, amg.default_params(solver=2, precond=1), comm=comm, row_begin=0, n_global=N)
+    b = torch.as_tensor(bvec, device="cuda")
+    x = torch.zeros_like(b)
+    rep = S.solve(b, x, 1e-8)
+    S1 = amg.Solver(amg.BSR.from_numpy(ptr, col, val), amg.default_params(solver=2, precond=1))
+    x1 = torch.zeros_like(b)
+    rep1 = S1.solve(b, x1, 1e-8)
+    assert rep.converged and rep.iters == rep1.iters
+    assert torch.allclose(x, x1, rtol=0, atol=1e-12 * float(x1.abs().max()))
