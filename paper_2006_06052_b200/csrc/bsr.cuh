@@ -74,6 +74,34 @@ __device__ __forceinline__ double item_dot(const V (&a)[B], const X (&x)[B]) {
   }
 }
 
+// Three consecutive fp32 values (a 3x3 fp32 block row, or x of one block column) in TWO
+// loads instead of three: one 8-byte load at the even-aligned pair and one 4-byte load
+// for the remaining value.  Every lane issues the same two instructions; only the
+// addresses depend on the parity of p.
+template <bool NC>
+__device__ __forceinline__ void ld3f(const float* __restrict__ p, float (&v)[3]) {
+  const bool even = ((reinterpret_cast<uintptr_t>(p) >> 2) & 1) == 0;
+  const float2* q2 = reinterpret_cast<const float2*>(even ? p : p + 1);
+  const float* q1 = even ? p + 2 : p;
+  const float2 a = NC ? __ldg(q2) : __ldcs(q2);
+  const float b = NC ? __ldg(q1) : __ldcs(q1);
+  v[0] = even ? a.x : b;
+  v[1] = even ? a.y : a.x;
+  v[2] = even ? b : a.y;
+}
+
+// b values -> fp64 registers; 3 fp32 values in two loads (ld3f)
+template <int B, typename T>
+__device__ __forceinline__ void load_bd(const T* __restrict__ p, double (&v)[B]) {
+  if constexpr (B == 3 && std::is_same_v<T, float>) {
+    float f[3];
+    ld3f<true>(p, f);
+    v[0] = f[0]; v[1] = f[1]; v[2] = f[2];
+  } else {
+    load_b<B, false>(p, v);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T to_out(double v) {
   return (T)v;  // fp32: round-to-nearest-even, once

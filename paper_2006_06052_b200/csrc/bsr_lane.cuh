@@ -51,6 +51,17 @@ __device__ __forceinline__ void ld_seg(const T* __restrict__ p, T (&v)[N]) {
   }
 }
 
+template <int BC, bool NC, typename T>
+__device__ __forceinline__ void ld_row(const T* __restrict__ p, T (&v)[BC]) {
+  if constexpr (BC == 3 && std::is_same_v<T, float>) ld3f<NC>(p, v);
+  else ld_seg<BC, NC>(p, v);
+}
+template <int BC, typename T>
+__device__ __forceinline__ void ld_x(const T* __restrict__ p, T (&v)[BC]) {
+  if constexpr (BC == 3 && std::is_same_v<T, float>) ld3f<true>(p, v);
+  else load_raw<BC, false>(p, v);
+}
+
 // Row-component lane context handed to the epilogue: y_r = (A x)_{row, r}; all()
 // gathers the row's full BR-vector from its lanes (warp shuffles, every lane of the
 // warp must call it).
@@ -173,11 +184,11 @@ __global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __res
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         c[u] = __ldg(col + k + u);
-        ld_seg<BC, NC>(val + (int64_t)(k + u) * BE + r * BC, a[u]);
+        ld_row<BC, NC>(val + (int64_t)(k + u) * BE + r * BC, a[u]);
       }
       X xv[U][BC];
 #pragma unroll
-      for (int u = 0; u < U; ++u) load_raw<BC, false>(x + (int64_t)c[u] * BC, xv[u]);
+      for (int u = 0; u < U; ++u) ld_x<BC>(x + (int64_t)c[u] * BC, xv[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) acc += item_dot<BC, V, X, FAST>(a[u], xv[u]);
     }
@@ -185,8 +196,8 @@ __global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __res
     for (; k < k1; ++k) {
       V a[BC];
       X xv[BC];
-      ld_seg<BC, NC>(val + (int64_t)k * BE + r * BC, a);
-      load_raw<BC, false>(x + (int64_t)__ldg(col + k) * BC, xv);
+      ld_row<BC, NC>(val + (int64_t)k * BE + r * BC, a);
+      ld_x<BC>(x + (int64_t)__ldg(col + k) * BC, xv);
       acc += item_dot<BC, V, X, FAST>(a, xv);
     }
     L.yr = acc;
