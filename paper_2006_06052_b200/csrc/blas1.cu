@@ -590,4 +590,30 @@ void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, ui
   }
 }
 
+// IDR(s) step update in one pass: r -= a g; x += a u; out[0] = ||r||  (deterministic
+// block partials + last-block finish, as k_cgs)
+__global__ void __launch_bounds__(kTM) k_idr_update(int64_t n, double a, const double* __restrict__ g,
+                                                    const double* __restrict__ u, double* r, double* x,
+                                                    double* partials, unsigned* ticket, double* out, int post) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+    const double ri = fma(-a, g[i], r[i]);
+    r[i] = ri;
+    x[i] = fma(a, u[i], x[i]);
+    acc[0] = fma(ri, ri, acc[0]);
+  }
+  reduce_finish<1>(acc, 1, partials, ticket, out, post, nullptr);
+}
+
+void launch_idr_update(int64_t n, double a, const double* g, const double* u, double* r, double* x,
+                       double* partials, double* out, cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("idr_update", 1, AMG_F64, -1), 8.0 * n * 6, s);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  const int64_t work = (n + kTM - 1) / kTM;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)kMaxPartials, work));
+  k_idr_update<<<grid, kTM, 0, s>>>(n, a, g, u, r, x, partials, ticket, out, comm ? 0 : 1);
+  AMG_CK_LAUNCH();
+  finalize_global(comm, out, 1, true, s);
+}
+
 }  // namespace amgb

@@ -49,6 +49,9 @@ void launch_lincomb(int64_t n, const LinComb& L, double* out, cudaStream_t s);
 // (stream 6, idx = (base + j) * n_global + off + i); dots over ranks via comm
 void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, uint64_t off, double* const* P,
                        double* partials, double* dscal, cudaStream_t s, CommBase* comm);
+// IDR(s) step: r -= a g; x += a u; out[0] = ||r|| (one pass, deterministic)
+void launch_idr_update(int64_t n, double a, const double* g, const double* u, double* r, double* x,
+                       double* partials, double* out, cudaStream_t s, CommBase* comm = nullptr);
 // y = x / sdev[0]
 void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s);
 

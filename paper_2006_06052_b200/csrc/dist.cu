@@ -253,7 +253,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
   allgatherv_bytes(comm, (char*)G.val, o, c, s);
 
   // 2. the global hierarchy (identical on every rank), rank-local aggregation
-  Handle* Gh = build_handle(G, p, bounds, s);
+  Handle* Gh = build_handle(G, p, bounds, s, /*workspace=*/false);
   tmp.release();
   if (Gh->amg_active && Gh->lv.empty() && P > 1) {
     delete Gh;

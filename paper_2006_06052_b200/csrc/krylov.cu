@@ -463,10 +463,11 @@ int solve_idrs(Ctx& c, const double* b, double* x, double rtol, double nb, amg_r
         break;
       }
       const double beta = f[k] / mkk;
-      c.axpby(-beta, h.Gi[k], 1.0, r);  // r -= beta G_k
-      c.axpby(beta, h.Ui[k], 1.0, x);   // x += beta U_k
+      launch_idr_update(N, beta, h.Gi[k], h.Ui[k], r, x, h.partials, h.dscal, c.s, h.comm);  // r, x, ||r||
+      c.bytes += 8.0 * N * 6;
+      c.read(1);
       ++it;
-      nr = nrm_r();
+      nr = h.hscal[0];
       if (nr <= rtol * nb) {
         if (converged_true()) status = AMG_OK;
         restart_cycle = true;
@@ -493,10 +494,11 @@ int solve_idrs(Ctx& c, const double* b, double* x, double rtol, double nb, amg_r
       status = AMG_EBREAKDOWN;
       break;
     }
-    c.axpby(-om, t, 1.0, r);
-    c.axpby(om, vh, 1.0, x);
+    launch_idr_update(N, om, t, vh, r, x, h.partials, h.dscal, c.s, h.comm);  // r -= om t, x += om vh
+    c.bytes += 8.0 * N * 6;
+    c.read(1);
     ++it;
-    nr = nrm_r();
+    nr = h.hscal[0];
     if (nr <= rtol * nb && converged_true()) status = AMG_OK;
   }
   return finish(c, b, x, r, nb, status, it, restarts, rep);

@@ -93,7 +93,8 @@ int check_params(const amg_params* p) {
   return AMG_OK;
 }
 
-Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s) {
+Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s,
+                     bool workspace) {
   auto t0 = std::chrono::steady_clock::now();
   Handle* h = new Handle;
   try {
@@ -123,7 +124,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     make_tma_plan(M, s, &h->arena);
     if (h->amg_active) setup_build(*h, M, bounds, s);
     if (h->schur) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
-    alloc_workspace(*h, s);
+    if (workspace) alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));
   } catch (...) {

@@ -110,7 +110,10 @@ void setup_build(Handle& h, const Mat& A64 /* device fp64 copy owned by h */, co
                  cudaStream_t s);
 void alloc_workspace(Handle& h, cudaStream_t s);
 // solver.cu: full single-device build on a device matrix view with slab bounds
-Handle* build_handle(const Mat& view, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s);
+// workspace = false: hierarchy only (the replicated global handle of amg_setup_dist, whose
+// slabs are copied out: no global Krylov basis on every rank)
+Handle* build_handle(const Mat& view, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s,
+                     bool workspace = true);
 // dist.cu
 void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_t s);
 void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s);
