@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restri
 // fp32 x fp64 6.04 TB/s (5.68), 4x4 fp64 6.69 TB/s (6.16).
 template <int B, int U, typename V, typename X, class EPI>
 __global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const int32_t* __restrict__ sptr,
+                                                     const int32_t* __restrict__ perm,
                                                      const int32_t* __restrict__ scol, const V* __restrict__ sval,
                                                      const X* __restrict__ x, EPI epi) {
   constexpr int C = 32 / B;
@@ -360,9 +361,10 @@ __global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const i
   }
   LaneRow<B> Lr;
   Lr.row = s * C + g;
+  if (perm && act) Lr.row = __ldg(perm + (int64_t)s * C + g);  // sorted windows: slot -> row (-1: padding)
   Lr.r = r;
   Lr.base = base;
-  Lr.valid = act && Lr.row < n;
+  Lr.valid = act && Lr.row >= 0 && Lr.row < n;
   Lr.yr = sum;
   epi(Lr);
 }

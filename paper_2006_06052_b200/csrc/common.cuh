@@ -93,6 +93,7 @@ struct Mat {
   int32_t* sell_ptr = nullptr;  // [sell_ns + 1] step offsets
   int32_t* sell_col = nullptr;  // [steps][C]
   void* sell_val = nullptr;     // [steps][b][C][b]
+  int32_t* sell_perm = nullptr; // [sell_ns * C] slot -> row (-1: padding slot), or nullptr (in order)
   bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
   int rows_per_block() const { return br ? br : b; }
   int cols_per_block() const { return bc ? bc : b; }

@@ -103,22 +103,15 @@ void set_lane_plan(Mat& A) {
 }
 
 // ---- sliced copy (k_bsr_sell) ----
-__global__ void k_sell_len(int n, int C, const int32_t* ptr, int32_t* len) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s * C >= n) return;
-  int mx = 0;
-  for (int64_t r = s * C; r < min((int64_t)n, s * C + C); ++r) mx = max(mx, ptr[r + 1] - ptr[r]);
-  len[s] = mx;
-}
-
 template <typename V>
 __global__ void k_sell_fill(int n, int b, int C, int ns, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                            const V* __restrict__ val, const int32_t* __restrict__ sptr, int32_t* __restrict__ scol,
-                            V* __restrict__ sval) {
+                            const V* __restrict__ val, const int32_t* __restrict__ sptr, const int32_t* __restrict__ perm,
+                            int32_t* __restrict__ scol, V* __restrict__ sval) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)ns * C) return;
   const int s = (int)(t / C), g = (int)(t % C);
-  const int64_t row = (int64_t)s * C + g;
+  int64_t row = (int64_t)s * C + g;
+  if (perm) row = perm[t] >= 0 ? perm[t] : n;  // slot -> row (sorted windows), n = padding slot
   const int k0 = row < n ? ptr[row] : 0, len = row < n ? ptr[row + 1] - k0 : 0;
   const int pad_col = row < n ? (int)row : 0;
   for (int j = 0; j < sptr[s + 1] - sptr[s]; ++j) {
@@ -130,17 +123,47 @@ __global__ void k_sell_fill(int n, int b, int C, int ns, const int32_t* __restri
   }
 }
 
+// Rows are taken in order, or -- when that cuts the zero padding by more than 3 % of the
+// blocks -- sorted by length (descending, stable) inside windows of 32 slices (SELL-C-sigma,
+// sigma = 32 C): a slot -> row permutation kept on the device, the epilogue writes row
+// perm[slot].  Only rows inside one window are reordered, so the output stays local.
 static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
   const int C = 32 / A.b;
   const int ns = (int)((A.n + C - 1) / C);
-  int32_t* len = nullptr;
-  AMG_CK(cudaMallocAsync((void**)&len, sizeof(int32_t) * ns, s));
-  k_sell_len<<<grid_for(ns, 256), 256, 0, s>>>(A.n, C, A.ptr, len);
-  AMG_CK_LAUNCH();
-  std::vector<int32_t> h(ns), sp(ns + 1, 0);
-  AMG_CK(cudaMemcpyAsync(h.data(), len, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> hp((size_t)A.n + 1);
+  AMG_CK(cudaMemcpyAsync(hp.data(), A.ptr, sizeof(int32_t) * (A.n + 1), cudaMemcpyDeviceToHost, s));
   AMG_CK(cudaStreamSynchronize(s));
-  AMG_CK(cudaFreeAsync(len, s));
+  auto len_of = [&](int64_t r) { return r < A.n ? hp[r + 1] - hp[r] : 0; };
+  std::vector<int32_t> h(ns), sp(ns + 1, 0);
+  int64_t pad_plain = 0;
+  for (int i = 0; i < ns; ++i) {
+    int mx = 0;
+    for (int g = 0; g < C; ++g) mx = std::max(mx, len_of((int64_t)i * C + g));
+    h[i] = mx;
+    pad_plain += (int64_t)mx * C;
+  }
+  const int W = 32 * C;
+  std::vector<int32_t> perm((size_t)ns * C, -1), hs(ns);
+  int64_t pad_sorted = 0;
+  for (int64_t w0 = 0; w0 < (int64_t)ns * C; w0 += W) {
+    const int64_t w1 = std::min<int64_t>(w0 + W, (int64_t)ns * C);
+    std::vector<int32_t> rows;
+    for (int64_t r = w0; r < std::min<int64_t>(w1, A.n); ++r) rows.push_back((int32_t)r);
+    std::stable_sort(rows.begin(), rows.end(), [&](int32_t a, int32_t b) { return len_of(a) > len_of(b); });
+    for (size_t q = 0; q < rows.size(); ++q) perm[w0 + q] = rows[q];
+    for (int64_t sl = w0 / C; sl < w1 / C; ++sl) {
+      int mx = 0;
+      for (int g = 0; g < C; ++g) {
+        const int32_t r = perm[sl * C + g];
+        if (r >= 0) mx = std::max(mx, len_of(r));
+      }
+      hs[sl] = mx;
+      pad_sorted += (int64_t)mx * C;
+    }
+  }
+  const bool sorted = (double)(pad_plain - pad_sorted) > 0.03 * (double)std::max<int64_t>(A.nnz, 1) &&
+                      !env_int("AMG_SELL_NO_SORT", 0);
+  if (sorted) h = hs;
   for (int i = 0; i < ns; ++i) {
     if ((int64_t)sp[i] + h[i] > INT32_MAX) fail(AMG_EINDEX_OVERFLOW, "sliced copy: too many steps");
     sp[i + 1] = sp[i] + h[i];
@@ -151,10 +174,15 @@ static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
   A.sell_col = arena.alloc_n<int32_t>(std::max<int64_t>(steps * C, 1));
   A.sell_val = arena.alloc(std::max<int64_t>(steps * C * A.b * A.b, 1) * dtype_size(A.vt));
   AMG_CK(cudaMemcpyAsync(A.sell_ptr, sp.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, s));
+  A.sell_perm = nullptr;
+  if (sorted) {
+    A.sell_perm = arena.alloc_n<int32_t>((size_t)ns * C);
+    AMG_CK(cudaMemcpyAsync(A.sell_perm, perm.data(), sizeof(int32_t) * ns * C, cudaMemcpyHostToDevice, s));
+  }
   dispatch_t(A.vt, [&](auto v) {
     using V = decltype(v);
     k_sell_fill<V><<<grid_for((int64_t)ns * C, 256), 256, 0, s>>>(A.n, A.b, C, ns, A.ptr, A.col, (const V*)A.val,
-                                                                   A.sell_ptr, A.sell_col, (V*)A.sell_val);
+                                                                   A.sell_ptr, A.sell_perm, A.sell_col, (V*)A.sell_val);
   });
   AMG_CK_LAUNCH();
   AMG_CK(cudaStreamSynchronize(s));  // sp (host) must outlive the copy
@@ -251,8 +279,8 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
     if (A.lane_var == kLaneSell) {
       constexpr int U = (BR * BR * sizeof(V) <= 36) ? 4 : 2;
       const unsigned grid = grid_for((int64_t)A.sell_ns * 32, kBlock);
-      k_bsr_sell<BR, U, V, X, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_col, (const V*)A.sell_val,
-                                                          x, epi);
+      k_bsr_sell<BR, U, V, X, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_perm, A.sell_col,
+                                                          (const V*)A.sell_val, x, epi);
       return;
     }
   }
