@@ -237,6 +237,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the IDR(5) secondary measurement")
+    ap.add_argument("--no-other", action="store_true", help="skip the cfg 1/3/4 secondary measurements")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -396,6 +397,34 @@ def main():
                             "solve_alg_GBs": r2.alg_bytes / statistics.median(ts) / 1e9}
         del S2
         torch.cuda.empty_cache()
+    if not args.no_other and world == 1 and args.cfg == 5 and not args.n:
+        # the other solve configs of BASELINE.json at their full sizes ("also
+        # report cfgs 1, 3, 4 at P = 1"): device-timed median of 3 solves after one warm-up
+        out["other_configs"] = {}
+        for oc in (1, 3, 4):
+            on = gen.CONFIGS[oc]["n"]
+            p_, c_, v_, b_ = make_problem(oc, on, 0, on ** 3)
+            So = amg.Solver(amg.BSR.from_numpy(p_, c_, v_), params_for(amg, oc))
+            del v_
+            bo = torch.as_tensor(b_, device="cuda")
+            xo = torch.zeros_like(bo)
+            So.solve(bo, xo, 1e-8)
+            ts = []
+            for _ in range(3):
+                xo.zero_()
+                a_, b2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                ro = So.solve(bo, xo, 1e-8)
+                b2_.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a_.elapsed_time(b2_) * 1e-3)
+            t_ = statistics.median(ts)
+            out["other_configs"][f"cfg{oc}"] = {
+                "workload": config_dict(oc, on, 1)["workload"], "value": t_, "unit": "s/solve", "iters": ro.iters,
+                "relres_true": ro.relres_true, "converged": ro.converged, "levels": ro.levels,
+                "solve_alg_GBs": ro.alg_bytes / t_ / 1e9, "solve_roofline_frac": ro.alg_bytes / t_ / 1e9 / peak}
+            del So, bo, xo
+            torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
         c = oracle_sample(args.cfg, n, args.cpu_n, rep.iters)
         out["cpu_baseline"] = {"value": c["value"], "unit": "s/solve", "cores": 1, "kind": "oracle",

@@ -616,4 +616,57 @@ void launch_idr_update(int64_t n, double a, const double* g, const double* u, do
   finalize_global(comm, out, 1, true, s);
 }
 
+// ---- BiCGStab fused steps (one pass, deterministic reductions, last-block finish) ----
+// out = r - (num / den[0]) v;  dst[0] = out . out          (s = r - alpha v, alpha on the device)
+__global__ void __launch_bounds__(kTM) k_sub_div_nrm(int64_t n, double num, const double* __restrict__ den,
+                                                     const double* __restrict__ v, const double* __restrict__ r,
+                                                     double* __restrict__ out, double* partials, unsigned* ticket,
+                                                     double* dst) {
+  const double a = num / den[0];
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+    const double o = fma(-a, v[i], r[i]);
+    out[i] = o;
+    acc[0] = fma(o, o, acc[0]);
+  }
+  reduce_finish<1>(acc, 1, partials, ticket, dst, 0, nullptr);
+}
+
+// out = s - c t;  dst[0] = out . out,  dst[1] = rh . out     (r = s - omega t, next rho)
+__global__ void __launch_bounds__(kTM) k_axpy_2dot(int64_t n, double c, const double* __restrict__ t,
+                                                   const double* __restrict__ s, double* __restrict__ out,
+                                                   const double* __restrict__ rh, double* partials, unsigned* ticket,
+                                                   double* dst) {
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+    const double o = fma(-c, t[i], s[i]);
+    out[i] = o;
+    acc[0] = fma(o, o, acc[0]);
+    acc[1] = fma(rh[i], o, acc[1]);
+  }
+  reduce_finish<2>(acc, 2, partials, ticket, dst, 0, nullptr);
+}
+
+static int fused_grid(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)kMaxPartials, (n + kTM - 1) / kTM));
+}
+
+void launch_sub_div_nrm(int64_t n, double num, const double* den, const double* v, const double* r, double* out,
+                        double* partials, double* dst, cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("sub_div_nrm", 1, AMG_F64, -1), 8.0 * n * 3, s);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  k_sub_div_nrm<<<fused_grid(n), kTM, 0, s>>>(n, num, den, v, r, out, partials, ticket, dst);
+  AMG_CK_LAUNCH();
+  finalize_global(comm, dst, 1, false, s);
+}
+
+void launch_axpy_2dot(int64_t n, double c, const double* t, const double* s_, double* out, const double* rh,
+                      double* partials, double* dst, cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("axpy_2dot", 2, AMG_F64, -1), 8.0 * n * 4, s);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  k_axpy_2dot<<<fused_grid(n), kTM, 0, s>>>(n, c, t, s_, out, rh, partials, ticket, dst);
+  AMG_CK_LAUNCH();
+  finalize_global(comm, dst, 2, false, s);
+}
+
 }  // namespace amgb

@@ -52,6 +52,12 @@ void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, ui
 // IDR(s) step: r -= a g; x += a u; out[0] = ||r|| (one pass, deterministic)
 void launch_idr_update(int64_t n, double a, const double* g, const double* u, double* r, double* x,
                        double* partials, double* out, cudaStream_t s, CommBase* comm = nullptr);
+// BiCGStab: out = r - (num / den[0]) v, dst[0] = out.out   (den on the device)
+void launch_sub_div_nrm(int64_t n, double num, const double* den, const double* v, const double* r, double* out,
+                        double* partials, double* dst, cudaStream_t s, CommBase* comm = nullptr);
+// BiCGStab: out = s - c t, dst[0] = out.out, dst[1] = rh.out
+void launch_axpy_2dot(int64_t n, double c, const double* t, const double* s_, double* out, const double* rh,
+                      double* partials, double* dst, cudaStream_t s, CommBase* comm = nullptr);
 // y = x / sdev[0]
 void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s);
 

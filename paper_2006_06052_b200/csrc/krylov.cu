@@ -1,7 +1,9 @@
 // krylov.cu -- outer fp64 Krylov solvers: PCG, right-
 // preconditioned BiCGStab (van der Vorst), flexible right-preconditioned GMRES(m)
-// with CGS2 Arnoldi and Givens rotations.  Same steps, scalars and stopping rules as
-// the oracle; the host reads the needed scalars once per step through pinned memory.
+// with CGS2 Arnoldi and Givens rotations, and the paper's IDR(s) (reading R17).  Same
+// steps, scalars and stopping rules as the oracle; the host reads the scalars it
+// branches on through pinned memory (fused into as few reads per step as the data
+// dependencies allow).
 #include <cmath>
 #include <vector>
 
@@ -166,10 +168,18 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
     first = true;
     return false;
   };
+  // rho = rh . r for the next step comes with ||r|| out of the fused r update (one host
+  // read per half step instead of two); recomputed after a restart / failed verify
+  bool have_rho = false;
+  double rho_next = 0.0;
   while (status != AMG_OK && it < h.p.maxiter) {
-    c.dot(rh, r, 0);
-    c.read(1);
-    const double rho = h.hscal[0];
+    if (!have_rho) {
+      c.dot(rh, r, 0);
+      c.read(1);
+      rho_next = h.hscal[0];
+    }
+    have_rho = false;
+    const double rho = rho_next;
     if (!(std::fabs(rho) > 1e-30 * nb * nb) || !finite(rho)) {
       if (do_restart()) continue;
       status = AMG_EBREAKDOWN;
@@ -187,7 +197,10 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
     c.pc(p, ph, AMG_F64);
     c.spmv(ph, AMG_F64, v);
     c.dot(rh, v, 0);
-    c.read(1);
+    // s = r - (rho / rv) v with rv still on the device, ||s||^2 in the same pass
+    launch_sub_div_nrm(N, rho, h.dscal, v, r, sv, h.partials, h.dscal + 1, c.s, h.comm);
+    c.bytes += 24.0 * N;
+    c.read(2);
     const double rv = h.hscal[0];
     if (rv == 0.0 || !finite(rv)) {
       if (do_restart()) continue;
@@ -195,12 +208,8 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
       break;
     }
     alpha = rho / rv;
-    launch_convert(N, r, AMG_F64, sv, AMG_F64, 1.0, c.s);
-    c.axpby(-alpha, v, 1.0, sv);  // s = r - alpha v
     ++it;
-    c.dot(sv, sv, 0, true);
-    c.read(1);
-    if (h.hscal[0] <= rtol * nb) {
+    if (std::sqrt(h.hscal[1]) <= rtol * nb) {
       c.axpby(alpha, ph, 1.0, x);
       if (verify()) {
         status = AMG_OK;
@@ -210,8 +219,11 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
     }
     c.pc(sv, sh, AMG_F64);
     c.spmv(sh, AMG_F64, t);
-    c.dot(t, t, 0);
-    c.dot(t, sv, 1);
+    PtrList TS{};
+    TS.p[0] = t;
+    TS.p[1] = sv;
+    launch_mdot_scaled(N, 2, TS, nullptr, t, h.partials, h.dscal, c.s, h.comm);  // t.t, s.t
+    c.bytes += 24.0 * N;
     c.read(2);
     const double tt = h.hscal[0];
     if (tt == 0.0 || !finite(tt)) {
@@ -221,20 +233,27 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
     }
     omega = h.hscal[1] / tt;
     c.axpbypcz(alpha, ph, omega, sh, 1.0, x);  // x += alpha ph + omega sh
-    launch_convert(N, sv, AMG_F64, r, AMG_F64, 1.0, c.s);
-    c.axpby(-omega, t, 1.0, r);  // r = s - omega t
+    launch_axpy_2dot(N, omega, t, sv, r, rh, h.partials, h.dscal, c.s, h.comm);  // r = s - omega t; r.r, rh.r
+    c.bytes += 32.0 * N;
+    c.read(2);
     rho_old = rho;
-    c.dot(r, r, 0, true);
-    c.read(1);
-    const double nr = h.hscal[0];
+    const double nr = std::sqrt(h.hscal[0]);
+    rho_next = h.hscal[1];
+    have_rho = true;
     if (omega == 0.0 || !finite(omega)) {
-      if (do_restart()) continue;
+      if (do_restart()) {
+        have_rho = false;
+        continue;
+      }
       status = AMG_EBREAKDOWN;
       break;
     }
-    if (nr <= rtol * nb && verify()) {
-      status = AMG_OK;
-      break;
+    if (nr <= rtol * nb) {
+      if (verify()) {
+        status = AMG_OK;
+        break;
+      }
+      have_rho = false;  // r was replaced by the true residual
     }
   }
   return finish(c, b, x, r, nb, status, it, restarts, rep);
