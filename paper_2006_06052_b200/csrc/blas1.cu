@@ -457,6 +457,7 @@ void launch_dot(int64_t n, const void* a, int at, const void* b, int bt, double*
     k_dot<float, float><<<nb, kT, 0, s>>>(n, (const float*)a, (const float*)b, partials, nb);
   AMG_CK_LAUNCH();
   ++g_launches;
+  ++t_launches;
   k_finalize<<<1, kT, 0, s>>>(1, partials, nb, out, (sqrt_out && !comm) ? 1 : 0);
   AMG_CK_LAUNCH();
   finalize_global(comm, out, 1, sqrt_out, s);

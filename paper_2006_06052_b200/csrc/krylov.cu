@@ -280,6 +280,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
   AMG_CK_LAUNCH();
   ++g_launches;
+  ++t_launches;
   c.read(65);
   double beta = h.hscal[64];
   int it = 0, cycles = 0, status = AMG_NOT_CONVERGED;
@@ -347,6 +348,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
     AMG_CK_LAUNCH();
     ++g_launches;
+  ++t_launches;
     c.bytes += 8.0 * N;
     c.read(65);
     beta = h.hscal[64];

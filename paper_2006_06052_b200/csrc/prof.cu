@@ -8,7 +8,8 @@
 
 namespace amgb {
 
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
+thread_local int64_t t_launches = 0;
 bool g_prof = false;
 
 namespace {
@@ -48,7 +49,7 @@ using namespace amgb;
 
 extern "C" {
 
-int64_t amg_kernel_launches(void) { return g_launches; }
+int64_t amg_kernel_launches(void) { return g_launches.load(); }
 
 int amg_profile_begin(void) {
   g_recs.clear();

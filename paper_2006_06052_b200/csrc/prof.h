@@ -5,11 +5,13 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace amgb {
 
-extern int64_t g_launches;
+extern std::atomic<int64_t> g_launches;      // all library launches of the process
+extern thread_local int64_t t_launches;      // this thread's (graph capture counts its own)
 extern bool g_prof;
 
 void prof_record(const char* name, double bytes, cudaEvent_t a, cudaEvent_t b);
@@ -21,6 +23,7 @@ class ProfScope {
  public:
   ProfScope(const char* name, double bytes, cudaStream_t s) : name_(name), bytes_(bytes), s_(s) {
     ++g_launches;
+    ++t_launches;
     if (g_prof) {
       a_ = prof_event();
       cudaEventRecord(a_, s_);

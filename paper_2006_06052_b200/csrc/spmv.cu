@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <mutex>
 #include <unordered_map>
 
 #include "bsr.cuh"
@@ -52,11 +53,17 @@ __global__ void k_tile_max(int n, int tr, const int32_t* ptr, int* out) {
 }
 
 // dynamic shared memory already enabled per kernel (host-side, per function)
-static int& smem_configured(const void* kern) {
+// (thread safe: ranks of the thread-emulated communicator launch concurrently)
+static void ensure_smem(const void* kern, int smem) {
+  static std::mutex mu;
   static std::unordered_map<const void*, int> m;
+  std::lock_guard<std::mutex> lk(mu);
   auto it = m.find(kern);
   if (it == m.end()) it = m.emplace(kern, 48 * 1024).first;
-  return it->second;
+  if (smem > it->second) {
+    AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    it->second = smem;
+  }
 }
 
 template <int BR, int BC, typename V, typename X, bool FAST, class EPI>
@@ -65,11 +72,7 @@ static void launch_tma_rows(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
             A.tma_wave, A.tma_part_off, A.tma_max_blk};
   const int smem = A.tma_smem;
   auto kern = k_bsr_tma_rows<BR, BC, V, X, FAST, EPI>;
-  int& configured = smem_configured((const void*)kern);
-  if (smem > configured) {
-    AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = smem;
-  }
+  ensure_smem((const void*)kern, smem);
   kern<<<A.tma_grid, A.tma_tr, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
 }
 

@@ -90,10 +90,11 @@ void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStre
     if (G.r == r && G.z == z && G.zt == zt && G.sd == scale_dev) {
       AMG_CK(cudaGraphLaunch(G.exec, s));
       g_launches += G.kernels;
+      t_launches += G.kernels;
       return;
     }
   PcGraph G{r, z, zt, scale_dev, nullptr, 0};
-  const int64_t l0 = g_launches;
+  const int64_t l0 = t_launches;
   cudaGraph_t graph = nullptr;
   AMG_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
@@ -104,14 +105,16 @@ void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStre
     throw;
   }
   AMG_CK(cudaStreamEndCapture(s, &graph));
-  G.kernels = g_launches - l0;
-  g_launches = l0;
+  G.kernels = t_launches - l0;  // kernels captured (not launched): undo the count
+  t_launches = l0;
+  g_launches -= G.kernels;
   cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
   cudaGraphDestroy(graph);
   AMG_CK(e);
   h.pc_graphs.push_back(G);
   AMG_CK(cudaGraphLaunch(G.exec, s));
   g_launches += G.kernels;
+  t_launches += G.kernels;
 }
 
 // Algorithmic bytes of one preconditioner application:

@@ -573,6 +573,10 @@ void run(int n, int st) {
     check("sell_col U=2", t);
     t = timeit([&] { k_sell_col<B, 4, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
     check("sell_col U=4", t);
+    t = timeit([&] { k_sell_col<B, 7, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+    check("sell_col U=7", t);
+    t = timeit([&] { k_sell_col<B, 8, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+    check("sell_col U=8", t);
     cudaFree(dsp); cudaFree(dsc); cudaFree(dsv);
   }
 #define LANEPRE(U, M)                                                                                              \
