@@ -372,9 +372,12 @@ __global__ void __launch_bounds__(kT) k_maxpy(int64_t n, int k, PtrList V, const
 
 // x += sum_j y[j] Z_j  (Z of type T; y on the device); K-templated like k_cgs
 template <int K, typename T>
+constexpr int zupdate_unroll() { return (sizeof(T) == 4 && K > 10) ? 2 : cgs_unroll<K>(); }
+
+template <int K, typename T>
 __global__ void __launch_bounds__(kTM) k_zupdate(int64_t n, PtrList Z, const double* __restrict__ y,
                                                  double* __restrict__ x) {
-  constexpr int U = cgs_unroll<K>();
+  constexpr int U = zupdate_unroll<K, T>();
   __shared__ double c[K];
   if (threadIdx.x < K) c[threadIdx.x] = y[threadIdx.x];
   __syncthreads();
@@ -505,11 +508,20 @@ void launch_zupdate(int64_t n, int k, const PtrList& Z, int zt, const double* y,
   ProfScope ps_(prof_name("zupdate", k, zt, -1), (double)n * (16.0 + (double)k * dtype_size(zt)), s);
   dispatch_k(k, [&](auto Kc) {
     constexpr int K = decltype(Kc)::value;
-    constexpr int U = cgs_unroll<K>();
-    const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)kSMs * 8, work));
-    if (zt == AMG_F32) k_zupdate<K, float><<<g, kTM, 0, s>>>(n, Z, y, x);
-    else k_zupdate<K, double><<<g, kTM, 0, s>>>(n, Z, y, x);
+    auto go = [&](auto T) {
+      using TT = decltype(T);
+      constexpr int U = zupdate_unroll<K, TT>();
+      static int occ = 0;  // per instantiation
+      if (occ == 0) {
+        AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zupdate<K, TT>, kTM, 0));
+        occ = std::max(occ, 1);
+      }
+      const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
+      const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)kSMs * occ, work));
+      k_zupdate<K, TT><<<g, kTM, 0, s>>>(n, Z, y, x);
+    };
+    if (zt == AMG_F32) go(float{});
+    else go(double{});
   });
   AMG_CK_LAUNCH();
 }
