@@ -94,7 +94,7 @@ void set_lane_plan(Mat& A) {
   int var = kLaneRC2;
   if (br == 4 && bc == 4) var = per_row > 12.0 ? kLaneRC4 : kLaneRC2;
   else if (br == 3 && bc == 3 && f32)  // very short rows (prolongators, ~3.6 blocks): COLS lanes
-    var = per_row > 12.0 ? kLaneCN4 : (per_row < 5.0 ? kLaneCN2 : kLaneRN2);
+    var = per_row > 12.0 ? kLaneCN4 : (per_row < 6.5 ? kLaneCN2 : kLaneRN2);
   else if (br == 3 && bc == 3) var = per_row > 12.0 ? kLaneCN4 : kLaneCN2;
   else if (br == bc) var = kLaneRN4;
   else var = f32 ? kLaneRN2 : kLaneRC2;
