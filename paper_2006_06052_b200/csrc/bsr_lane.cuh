@@ -268,14 +268,14 @@ __global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restri
     X xv[U][BC];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) load_raw<BC, false>(x + (int64_t)c[u] * BC, xv[u]);
+      if (c[u] >= 0) ld_x<BC>(x + (int64_t)c[u] * BC, xv[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (c[u] < 0) continue;
 #pragma unroll
       for (int i = 0; i < BR; ++i) {
         V a[BC];
-        ld_seg<BC, false>(val + (int64_t)(kb + 32 * u) * BE + i * BC, a);
+        ld_row<BC, false>(val + (int64_t)(kb + 32 * u) * BE + i * BC, a);
         acc[i] += item_dot<BC, V, X, FAST>(a, xv[u]);
       }
     }
