@@ -455,6 +455,59 @@ __global__ void __launch_bounds__(256) k_sell_col(int n, int nslices, const int*
   if (act && row < n) y[(int64_t)row * B + r] = sum;
 }
 
+// H: sliced copy with ROW layout: step j of slice s stores the C blocks [g][B][B] row-major
+// (the BSR blocks of the slice's rows, contiguous); lane (g, r) reads row r of its block with
+// the two-load triple (fp32 B = 3) and x_col with the same trick
+template <int B, int U, typename V, typename X>
+__global__ void __launch_bounds__(256) k_sell_rows(int n, int nslices, const int* __restrict__ sptr,
+                                                   const int* __restrict__ scol, const V* __restrict__ sval,
+                                                   const X* __restrict__ x, double* __restrict__ y) {
+  constexpr int C = 32 / B;
+  const int lane = threadIdx.x & 31;
+  const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (s >= nslices) return;
+  const int g = lane / B, r = lane - g * B;
+  const bool act = g < C;
+  const int gg = act ? g : 0;
+  const int j0 = __ldg(sptr + s), j1 = __ldg(sptr + s + 1);
+  double acc = 0.0;
+  int j = j0;
+#pragma unroll 1
+  for (; j + U <= j1; j += U) {
+    int c[U];
+    V a[U][B];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = __ldg(scol + (int64_t)(j + u) * C + gg);
+      amgb::ld_row<B, false>(sval + ((int64_t)(j + u) * C + gg) * B * B + r * B, a[u]);
+    }
+    X xv[U][B];
+#pragma unroll
+    for (int u = 0; u < U; ++u) amgb::ld_x<B>(x + (int64_t)c[u] * B, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float s2 = 0.f;
+#pragma unroll
+      for (int q = 0; q < B; ++q) s2 = fmaf((float)a[u][q], (float)xv[u][q], s2);
+      acc += (double)s2;
+    }
+  }
+#pragma unroll 1
+  for (; j < j1; ++j) {
+    const int c = __ldg(scol + (int64_t)j * C + gg);
+    V a[B];
+    X xv[B];
+    amgb::ld_row<B, false>(sval + ((int64_t)j * C + gg) * B * B + r * B, a);
+    amgb::ld_x<B>(x + (int64_t)c * B, xv);
+    float s2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < B; ++q) s2 = fmaf((float)a[q], (float)xv[q], s2);
+    acc += (double)s2;
+  }
+  const int row = s * C + g;
+  if (act && row < n) y[(int64_t)row * B + r] = acc;
+}
+
 template <class F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b;
@@ -577,6 +630,26 @@ void run(int n, int st) {
     check("sell_col U=7", t);
     t = timeit([&] { k_sell_col<B, 8, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
     check("sell_col U=8", t);
+    // row-layout slice steps: [step][g][B][B]
+    std::vector<V> sv2((size_t)steps * C * B * B, V(0));
+    for (int64_t s2 = 0; s2 < ns; ++s2)
+      for (int g = 0; g < C; ++g) {
+        const int64_t row = s2 * C + g;
+        const int len = row < N ? hp[row + 1] - hp[row] : 0;
+        for (int j = 0; j < sp[s2 + 1] - sp[s2] && j < len; ++j) {
+          const int64_t st = sp[s2] + j, k = hp[row] + j;
+          for (int q = 0; q < B * B; ++q) sv2[(st * C + g) * B * B + q] = hval[k * B * B + q];
+        }
+      }
+    CK(cudaMemcpy(dsv, sv2.data(), steps * B * C * B * sizeof(V), cudaMemcpyHostToDevice));
+    if constexpr (sizeof(V) == 4 && sizeof(X) == 4) {
+      t = timeit([&] { k_sell_rows<B, 2, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+      check("sell_rows U=2", t);
+      t = timeit([&] { k_sell_rows<B, 4, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+      check("sell_rows U=4", t);
+      t = timeit([&] { k_sell_rows<B, 7, V, X><<<(ns * 32 + 255) / 256, 256>>>(N, ns, dsp, dsc, dsv, x, y1); }, 20);
+      check("sell_rows U=7", t);
+    }
     cudaFree(dsp); cudaFree(dsc); cudaFree(dsv);
   }
 #define LANEPRE(U, M)                                                                                              \
