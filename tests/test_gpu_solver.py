@@ -272,3 +272,22 @@ def test_solve_forced_kernel_paths(amg, envvars, wide):
     x, rep = _solve(amg, S, bvec)
     true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
     assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
+
+
+@pytest.mark.parametrize("solver", [0, 1, 2, 3])
+def test_maxiter_not_converged(amg, solver):
+    # maxiter reached: AMG_NOT_CONVERGED, the report filled, x the last iterate -- the same
+    # iteration count and (to the precision bar) the same residual as the oracle
+    n = 12
+    kind = gen.POISSON3 if solver == 0 else gen.STOKES
+    ptr, col, val = gen.matrix(kind, n)
+    bvec = gen.rhs(gen.RHS_UNIFORM if solver == 0 else gen.RHS_LID_NOISE, n, val.shape[-1])
+    pc = 1 if solver in (2, 3) else 0
+    A, S, O = make_pair(amg, ptr, col, val, hier32=False, precond=pc, solver=solver, maxiter=3, coarse_enough=100)
+    ro = O.solve(bvec, rtol=1e-12)
+    x, rep = _solve(amg, S, bvec, rtol=1e-12)
+    assert rep.status == amg.NOT_CONVERGED and not rep.converged
+    assert rep.iters == ro.iters == 3
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert abs(true - rep.relres_true) <= 1e-10 * max(true, 1.0)
+    assert abs(rep.relres_true - ro.relres_true) <= 1e-6 * ro.relres_true
