@@ -132,6 +132,19 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
 
 void amg_destroy(struct amg_handle* h);
 
+/* Scalar CSR -> BSR on the device (S1; the §4 worked example PAPER.md:658-672):
+ * one b x b block per non-empty tile of the scalar matrix; scalars absent inside a stored
+ * tile become explicit zeros; duplicate scalar entries are summed in CSR order.  n and m
+ * (scalar rows / columns) must be multiples of b; columns need not be sorted.  Inputs:
+ * ptr[n+1], col[nnz], val[nnz] of `dtype` (DEVICE).  Two calls: with bptr == NULL only
+ * *nnzb_out (host) is written; then, with caller-allocated DEVICE arrays bptr[n/b+1],
+ * bcol[nnzb], bval[nnzb*b*b] (same dtype), the BSR is filled (columns sorted per block
+ * row).  Synchronises `stream`.  Errors: AMG_EINVAL (b < 1, n or m not divisible, a
+ * column outside [0, m)), AMG_EINDEX_OVERFLOW (nnz >= 2^31), AMG_ENOMEM, AMG_ECUDA. */
+int amg_csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                   const void* val, int32_t dtype, int32_t* bptr, int32_t* bcol, void* bval, int64_t* nnzb_out,
+                   void* stream);
+
 /* SpMV plan for repeated products y = alpha A x + beta y (same semantics and errors as
  * bsr_spmv; §4 block layout PAPER.md:644-682).  Creation picks the
  * kernel from the block shape and row length and, for long rows (> 12 blocks per row,

@@ -62,7 +62,7 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_level_aggregates", "amg_schur_export", "amg_vcycle", "amg_device_bytes",
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
-           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy",
+           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr",
            "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local"]
 
 _lib = None
@@ -106,6 +106,7 @@ def lib():
             "bsr_plan_destroy": (None, [P]),
             "amg_profile_begin": (i32, []),
             "amg_profile_end": (i64, [P, i64]),
+            "amg_csr_to_bsr": (i32, [i32, i32, i32, i64, P, P, P, i32, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             if not hasattr(L, name):
@@ -206,6 +207,25 @@ def bsr_spmv(A: BSR, x, y, alpha: float = 1.0, beta: float = 0.0, stream=None):
     _check(lib().bsr_spmv(ctypes.byref(d), alpha, ctypes.c_void_p(x.data_ptr()), _dt(x), beta,
                           ctypes.c_void_p(y.data_ptr()), _dt(y), _stream_ptr(stream)), "bsr_spmv")
     return y
+
+
+def csr_to_bsr(n: int, m: int, b: int, ptr, col, val, stream=None):
+    """amg_csr_to_bsr: scalar CSR (device tensors) -> BSR (ptr, col, val[nnzb, b, b])."""
+    import torch
+    dt = _dt(val)
+    nnzb = ctypes.c_int64()
+    nnz = int(col.numel())
+    args = (n, m, b, nnz, ctypes.c_void_p(ptr.data_ptr()), ctypes.c_void_p(col.data_ptr() if nnz else 0),
+            ctypes.c_void_p(val.data_ptr() if nnz else 0), dt)
+    _check(lib().amg_csr_to_bsr(*args, None, None, None, ctypes.byref(nnzb), _stream_ptr(stream)), "amg_csr_to_bsr")
+    nb = nnzb.value
+    bptr = torch.zeros(n // b + 1, dtype=torch.int32, device=ptr.device)
+    bcol = torch.zeros(max(nb, 1), dtype=torch.int32, device=ptr.device)
+    bval = torch.zeros((max(nb, 1), b, b), dtype=val.dtype, device=ptr.device)
+    _check(lib().amg_csr_to_bsr(*args, ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(bcol.data_ptr()),
+                                ctypes.c_void_p(bval.data_ptr()), ctypes.byref(nnzb), _stream_ptr(stream)),
+           "amg_csr_to_bsr")
+    return bptr, bcol[:nb], bval[:nb]
 
 
 class SpmvPlan:

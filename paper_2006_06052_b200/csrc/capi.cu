@@ -117,6 +117,18 @@ int bsr_spmv(const amg_bsr* A, double alpha, const void* x, int32_t xt, double b
   AMG_GUARD_END
 }
 
+int amg_csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                   const void* val, int32_t dtype, int32_t* bptr, int32_t* bcol, void* bval, int64_t* nnzb_out,
+                   void* stream) {
+  AMG_GUARD_BEGIN
+  if (!nnzb_out || (n > 0 && !ptr) || (nnz > 0 && (!col || !val)) || nnz < 0) return AMG_EINVAL;
+  if (dtype != AMG_F32 && dtype != AMG_F64) return AMG_EINVAL;
+  if (bptr && nnz > 0 && (!bcol || !bval)) return AMG_EINVAL;
+  *nnzb_out = csr_to_bsr(n, m, b, nnz, ptr, col, val, dtype, bptr, bcol, bval, (cudaStream_t)stream);
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
 struct bsr_plan {
   amgb::Mat A;
   amgb::Arena arena;  // the plan's sliced copy of long-row matrices

@@ -12,6 +12,10 @@ namespace amgb {
 void set_lane_plan(Mat& A);
 void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena = nullptr, bool want_tma = false);
 
+// S1: scalar CSR -> BSR (convert.cu); returns nnzb, fills bptr/bcol/bval when bptr != nullptr
+int64_t csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                   const void* val, int dtype, int32_t* bptr, int32_t* bcol, void* bval, cudaStream_t s);
+
 // K1  y = alpha A x + beta y
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s);

@@ -241,3 +241,57 @@ def test_spmv_sliced_copy(amg, rng, envvars, b):
         yy = _r32(y0) if yt == amg.F32 else y0
         ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, 0.75, -1.0, yy)
         assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (b, vt, xt, yt)
+
+
+# ---- S1: scalar CSR -> BSR on the device (amg_csr_to_bsr) vs the oracle: bit-exact ----
+def _rand_csr(rng, n, m, dens, dup=True):
+    ptr = [0]
+    cols, vals = [], []
+    for i in range(n):
+        k = rng.binomial(m, dens)
+        c = rng.integers(0, m, k)  # unsorted, duplicates allowed (summed in CSR order)
+        if not dup:
+            c = np.unique(c)
+            rng.shuffle(c)
+        cols.extend(c.tolist())
+        vals.extend(rng.standard_normal(len(c)).tolist())
+        ptr.append(len(cols))
+    return np.array(ptr, np.int32), np.array(cols, np.int32), np.array(vals)
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_csr_to_bsr_parity(amg, rng, b, dt):
+    for nb_rows, dens in ((1, 0.5), (7, 0.3), (333, 0.01)):
+        n = m = nb_rows * b
+        ptr, col, val = _rand_csr(rng, n, m, dens)
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        vv = val if dt == "f64" else _r32(val)
+        bp, bc, bv = amg.csr_to_bsr(n, m, b, torch.as_tensor(ptr, device="cuda"), torch.as_tensor(col, device="cuda"),
+                                    torch.as_tensor(vv, device="cuda", dtype=tdt))
+        O = oracle.csr_to_bsr(n, m, b, ptr, col, vv)
+        op, oc, ov = O.to_arrays()
+        assert np.array_equal(bp.cpu().numpy(), op) and np.array_equal(bc.cpu().numpy(), oc)
+        if dt == "f64":
+            assert np.array_equal(bv.cpu().numpy(), ov)  # same summation order: bit-exact
+        else:  # fp32 sums of duplicates (the oracle sums in fp64): equal to 1 ulp-level
+            assert np.allclose(bv.double().cpu().numpy(), ov, rtol=1e-6, atol=1e-6)
+
+
+def test_csr_to_bsr_worked_example_and_errors(amg):
+    from conftest import golden
+    g = golden("worked_example.json")
+    bp, bc, bv = amg.csr_to_bsr(6, 6, 2, torch.as_tensor(np.array(g["csr_ptr"], np.int32), device="cuda"),
+                                torch.as_tensor(np.array(g["csr_col"], np.int32), device="cuda"),
+                                torch.as_tensor(np.array(g["csr_val"], np.float64), device="cuda"))
+    assert bp.cpu().tolist() == g["bsr_ptr"] and bc.cpu().tolist() == g["bsr_col"]
+    assert np.array_equal(bv.cpu().numpy(), np.array(g["bsr_val"]))
+    with pytest.raises(amg.AmgError) as e:  # not divisible
+        amg.csr_to_bsr(3, 3, 2, torch.zeros(4, dtype=torch.int32, device="cuda"),
+                       torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert e.value.status == amg.EINVAL
+    with pytest.raises(amg.AmgError) as e:  # column out of range
+        amg.csr_to_bsr(2, 2, 1, torch.as_tensor(np.array([0, 1, 1], np.int32), device="cuda"),
+                       torch.as_tensor(np.array([5], np.int32), device="cuda"),
+                       torch.ones(1, dtype=torch.float64, device="cuda"))
+    assert e.value.status == amg.EINVAL
