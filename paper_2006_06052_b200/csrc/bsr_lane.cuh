@@ -23,6 +23,7 @@
 #pragma once
 
 #include "bsr.cuh"
+#include "reduce.cuh"
 
 namespace amgb {
 
@@ -79,7 +80,7 @@ struct LaneRow {
 // ---------------------------------------------------------------- epilogues
 template <typename Y>
 struct LEpiSpmv {  // y = alpha A x + beta y
-  static constexpr bool kAll = false;
+  static constexpr int kDots = 0;
   double alpha, beta;
   Y* y;
   template <int BR>
@@ -94,7 +95,7 @@ struct LEpiSpmv {  // y = alpha A x + beta y
 
 template <typename X>
 struct LEpiResidual {  // r = f - A x
-  static constexpr bool kAll = false;
+  static constexpr int kDots = 0;
   const X* f;
   X* res;
   template <int BR>
@@ -107,7 +108,7 @@ struct LEpiResidual {  // r = f - A x
 
 template <typename V, typename X>
 struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
-  static constexpr bool kAll = true;
+  static constexpr int kDots = 0;
   const V* M;
   const X* f;
   const X* x;
@@ -131,7 +132,7 @@ struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
 
 template <typename V, typename X>
 struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
-  static constexpr bool kAll = false;
+  static constexpr int kDots = 0;
   const V* mS;
   const X* rp;
   X* p;
@@ -144,7 +145,7 @@ struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
 
 template <typename X>
 struct LEpiSchurU {  // r_u' = r_u - B^T p          (nu x 1 blocks; in place allowed)
-  static constexpr bool kAll = false;
+  static constexpr int kDots = 0;
   const X* ru;
   X* ru2;
   template <int BR>
@@ -152,6 +153,46 @@ struct LEpiSchurU {  // r_u' = r_u - B^T p          (nu x 1 blocks; in place all
     if (!L.valid) return;
     const int64_t o = (int64_t)L.row * BR + L.r;
     ru2[o] = to_out<X>((double)ru[o] - L.yr);
+  }
+};
+
+// fused SpMV + dot(s) (K3): y = A x (fp64); d_j += w_j[o] y_o, w_j == nullptr meaning y
+template <int ND>
+struct LEpiSpmvDot {
+  static constexpr int kDots = ND;
+  double* y;
+  const double* w[2];
+  double *partials, *out;
+  unsigned* ticket;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (L.valid) y[(int64_t)L.row * BR + L.r] = L.yr;
+  }
+  template <int BR>
+  __device__ __forceinline__ void dots(const LaneRow<BR>& L, double (&d)[ND]) const {
+    if (!L.valid) return;
+    const int64_t o = (int64_t)L.row * BR + L.r;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) d[j] = fma(w[j] ? w[j][o] : L.yr, L.yr, d[j]);
+  }
+};
+
+// fused residual + norm (K2): r = f - A x; d_0 += r_o^2
+struct LEpiResidualNrm {
+  static constexpr int kDots = 1;
+  const double* f;
+  double* r;
+  double *partials, *out;
+  unsigned* ticket;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    if (L.valid) r[(int64_t)L.row * BR + L.r] = f[(int64_t)L.row * BR + L.r] - L.yr;
+  }
+  template <int BR>
+  __device__ __forceinline__ void dots(const LaneRow<BR>& L, double (&d)[1]) const {
+    if (!L.valid) return;
+    const double v = f[(int64_t)L.row * BR + L.r] - L.yr;
+    d[0] = fma(v, v, d[0]);
   }
 };
 
@@ -163,8 +204,14 @@ __global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __res
   static_assert(!COLS || BR == BC, "column layout needs square blocks");
   constexpr int RPW = 32 / BR;
   constexpr int BE = BR * BC;
+  constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
   const int lane = threadIdx.x & 31;
-  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  // virtual blocks of 8 warps: one per CUDA block, or -- fused dots -- a persistent grid
+  // (at most kMaxPartials blocks) walks them, accumulating its dot partials
+  const int64_t nvb = ((int64_t)n + RPW * 8 - 1) / (RPW * 8);
+  double dacc[ND] = {};
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+  const int warp = (int)(vb * (blockDim.x >> 5) + (threadIdx.x >> 5));
   const int g = lane / BR, r = lane - g * BR;
   const int row = warp * RPW + g;
   LaneRow<BR> L;
@@ -246,6 +293,10 @@ __global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __res
     L.yr = s;
   }
   epi(L);
+  if constexpr (EPI::kDots > 0) epi.dots(L, dacc);
+  }  // virtual blocks
+  if constexpr (EPI::kDots > 0)
+    block_reduce_finish<EPI::kDots, 256>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out, 0, nullptr);
 }
 
 // Very long rows (coarse operators, restriction onto a small coarsest level): one warp

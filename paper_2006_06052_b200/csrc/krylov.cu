@@ -48,6 +48,34 @@ struct Ctx {
     launch_residual(h.A, b, x, r, AMG_F64, s);
     bytes += h.alg_bytes_spmv + 8.0 * N;
   }
+  // y = A x with dscal[j] = w_j . y (w_j == nullptr: y . y), j < nd: one fused pass when the
+  // operator's plan allows it (K3), else the SpMV and the dots
+  void spmv_dot(const void* x, int xt, double* y, const double* w0, const double* w1, int nd) {
+    halo_exchange(h, h.halo0, const_cast<void*>(x), xt, h.b, s);
+    if (launch_spmv_dot(h.A, x, xt, y, w0, w1, nd, h.partials, h.dscal, s, h.comm)) {
+      bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0) + 8.0 * N * ((w0 ? 1 : 0) + (w1 ? 1 : 0));
+      return;
+    }
+    launch_spmv(h.A, 1.0, x, xt, 0.0, y, AMG_F64, s);
+    bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0);
+    dot(w0 ? w0 : y, y, 0);
+    if (nd > 1) dot(w1 ? w1 : y, y, 1);
+  }
+  // r = b - A x with dscal[0] = r . r (K2 fused when the plan allows it)
+  void residual_nrm(const double* b, const double* x, double* r) {
+    if (h.comm) {
+      AMG_CK(cudaMemcpyAsync(h.x_ext, x, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+      halo_exchange(h, h.halo0, h.x_ext, AMG_F64, h.b, s);
+      x = h.x_ext;
+    }
+    if (launch_residual_nrm(h.A, b, x, AMG_F64, r, h.partials, h.dscal, s, h.comm)) {
+      bytes += h.alg_bytes_spmv + 8.0 * N;
+      return;
+    }
+    launch_residual(h.A, b, x, r, AMG_F64, s);
+    bytes += h.alg_bytes_spmv + 8.0 * N;
+    dot(r, r, 0);
+  }
   // scale_dev (device, optional): r is scaled by *scale_dev while narrowing (GMRES's 1/||V_j||)
   void pc(const double* r, void* z, int zt, const double* scale_dev = nullptr) {
     precond_apply_graphed(h, r, z, zt, s, scale_dev);
@@ -67,13 +95,12 @@ bool finite(double v) { return std::isfinite(v); }
 
 int finish(Ctx& c, const double* b, double* x, double* r, double nb, int status, int iters, int restarts,
            amg_report* rep) {
-  c.residual(b, x, r);
-  c.dot(r, r, 0, true);
+  c.residual_nrm(b, x, r);
   c.read(1);
   if (rep) {
     rep->iters = iters;
     rep->restarts = restarts;
-    rep->relres_true = c.h.hscal[0] / nb;
+    rep->relres_true = std::sqrt(c.h.hscal[0]) / nb;
     rep->converged = status == AMG_OK;
     rep->alg_bytes = c.bytes;
   }
@@ -84,11 +111,10 @@ int finish(Ctx& c, const double* b, double* x, double* r, double nb, int status,
 int solve_cg(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
   Handle& h = c.h;
   double *r = h.vec[0], *z = h.vec[1], *p = h.vec[2], *q = h.vec[3];
-  c.residual(b, x, r);
-  c.dot(r, r, 0, true);
+  c.residual_nrm(b, x, r);
   c.read(1);
   int it = 0, status = AMG_NOT_CONVERGED;
-  if (h.hscal[0] <= rtol * nb) status = AMG_OK;
+  if (std::sqrt(h.hscal[0]) <= rtol * nb) status = AMG_OK;
   bool restart = true;
   double rho = 0.0;
   while (status != AMG_OK && it < h.p.maxiter) {
@@ -101,8 +127,7 @@ int solve_cg(Ctx& c, const double* b, double* x, double rtol, double nb, amg_rep
       rho = h.hscal[0];
       restart = false;
     }
-    c.spmv(p, AMG_F64, q);
-    c.dot(p, q, 0);
+    c.spmv_dot(p, AMG_F64, q, p, nullptr, 1);  // q = A p, p . q
     c.read(1);
     const double pq = h.hscal[0];
     if (pq == 0.0 || !finite(pq)) {
@@ -110,16 +135,14 @@ int solve_cg(Ctx& c, const double* b, double* x, double rtol, double nb, amg_rep
       break;
     }
     const double alpha = rho / pq;
-    c.axpby(alpha, p, 1.0, x);
-    c.axpby(-alpha, q, 1.0, r);
+    launch_idr_update(c.N, alpha, q, p, r, x, h.partials, h.dscal, c.s, h.comm);  // r -= a q, x += a p, ||r||
+    c.bytes += 48.0 * c.N;
     ++it;
-    c.dot(r, r, 0, true);
     c.read(1);
     if (h.hscal[0] <= rtol * nb) {
-      c.residual(b, x, r);
-      c.dot(r, r, 0, true);
+      c.residual_nrm(b, x, r);
       c.read(1);
-      if (h.hscal[0] <= rtol * nb) {
+      if (std::sqrt(h.hscal[0]) <= rtol * nb) {
         status = AMG_OK;
         break;
       }
@@ -143,11 +166,10 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
   double *r = h.vec[0], *rh = h.vec[1], *p = h.vec[2], *ph = h.vec[3], *v = h.vec[4], *sv = h.vec[5],
          *sh = h.vec[6], *t = h.vec[7];
   const int64_t N = c.N;
-  c.residual(b, x, r);
-  c.dot(r, r, 0, true);
+  c.residual_nrm(b, x, r);
   c.read(1);
   int it = 0, restarts = 0, status = AMG_NOT_CONVERGED;
-  if (h.hscal[0] <= rtol * nb) status = AMG_OK;
+  if (std::sqrt(h.hscal[0]) <= rtol * nb) status = AMG_OK;
   launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
   bool first = true;
   double rho_old = 1.0, alpha = 1.0, omega = 1.0;
@@ -160,10 +182,9 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
     return true;
   };
   auto verify = [&]() -> bool {
-    c.residual(b, x, r);
-    c.dot(r, r, 0, true);
+    c.residual_nrm(b, x, r);
     c.read(1);
-    if (h.hscal[0] <= rtol * nb) return true;
+    if (std::sqrt(h.hscal[0]) <= rtol * nb) return true;
     launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
     first = true;
     return false;
@@ -195,8 +216,7 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
       c.axpbypcz(1.0, r, -beta * omega, v, beta, p);
     }
     c.pc(p, ph, AMG_F64);
-    c.spmv(ph, AMG_F64, v);
-    c.dot(rh, v, 0);
+    c.spmv_dot(ph, AMG_F64, v, rh, nullptr, 1);  // v = A ph, rh . v
     // s = r - (rho / rv) v with rv still on the device, ||s||^2 in the same pass
     launch_sub_div_nrm(N, rho, h.dscal, v, r, sv, h.partials, h.dscal + 1, c.s, h.comm);
     c.bytes += 24.0 * N;
@@ -218,12 +238,7 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
       continue;
     }
     c.pc(sv, sh, AMG_F64);
-    c.spmv(sh, AMG_F64, t);
-    PtrList TS{};
-    TS.p[0] = t;
-    TS.p[1] = sv;
-    launch_mdot_scaled(N, 2, TS, nullptr, t, h.partials, h.dscal, c.s, h.comm);  // t.t, s.t
-    c.bytes += 24.0 * N;
+    c.spmv_dot(sh, AMG_F64, t, nullptr, sv, 2);  // t = A sh, t . t, s . t
     c.read(2);
     const double tt = h.hscal[0];
     if (tt == 0.0 || !finite(tt)) {
@@ -393,20 +408,18 @@ int solve_idrs(Ctx& c, const double* b, double* x, double rtol, double nb, amg_r
     std::fill(M.begin(), M.end(), 0.0);
     for (int j = 0; j < sd; ++j) M[(size_t)j * sd + j] = 1.0;
   };
-  auto nrm_r = [&]() {
-    c.dot(r, r, 0, true);
+  auto res_nrm = [&]() {  // r = b - A x, ||r||
+    c.residual_nrm(b, x, r);
     c.read(1);
-    return h.hscal[0];
+    return std::sqrt(h.hscal[0]);
   };
-  c.residual(b, x, r);
-  double nr = nrm_r();
+  double nr = res_nrm();
   int it = 0, restarts = 0, status = AMG_NOT_CONVERGED;
   if (nr <= rtol * nb) status = AMG_OK;
   reset();
   double om = 1.0;
   auto converged_true = [&]() -> bool {
-    c.residual(b, x, r);
-    if (nrm_r() <= rtol * nb) return true;
+    if (res_nrm() <= rtol * nb) return true;
     reset();
     om = 1.0;
     return false;

@@ -19,6 +19,15 @@ int64_t csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* 
 // K1  y = alpha A x + beta y
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
                  cudaStream_t s);
+class CommBase;
+// K3  y = A x (fp64 y) with out[j] = w_j . y (w_j == nullptr: y.y), j < nd <= 2, in ONE pass
+// (row-lane plans; false: not fused, the caller runs the SpMV and the dots); partials as
+// blas1.h (with the ticket); comm: the sums are allreduced
+bool launch_spmv_dot(const Mat& A, const void* x, int xt, double* y, const double* w0, const double* w1, int nd,
+                     double* partials, double* out, cudaStream_t s, CommBase* comm);
+// K2  r = f - A x with out[0] = r.r in one pass (fp64 f, r); false: not fused
+bool launch_residual_nrm(const Mat& A, const double* f, const void* x, int xt, double* r, double* partials,
+                         double* out, cudaStream_t s, CommBase* comm);
 // K2  r = f - A x   (f, x, r of type xt)
 void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s);
 // K5  xo = x + M (f - A x)

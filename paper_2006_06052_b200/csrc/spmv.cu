@@ -9,6 +9,8 @@
 #include "bsr.cuh"
 #include "bsr_lane.cuh"
 #include "bsr_tma.cuh"
+#include "blas1.h"
+#include "comm.h"
 #include "ops.h"
 #include "prof.h"
 
@@ -333,6 +335,62 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
     });
   });
   AMG_CK_LAUNCH();
+}
+
+// K3 / K2 fused forms (row-lane plans only; false -> the caller runs the unfused pair)
+template <class EPI>
+static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaStream_t s) {
+  if (A.tma_grid > 0 || A.lane_var > kLaneCN4 || A.n == 0) return false;
+  bool done = false;
+  dispatch_b(A.b, [&](auto Bc) {
+    constexpr int B = decltype(Bc)::value;
+    constexpr int RPW = 32 / B;
+    const int64_t nvb = ((int64_t)A.n + RPW * 8 - 1) / (RPW * 8);
+    const unsigned grid = (unsigned)std::min<int64_t>(nvb, kMaxPartials);
+    dispatch_t(A.vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        dispatch_lane<B, B>(A.lane_var, [&](auto Uc, auto Cc, auto Nc) {
+          constexpr int U = decltype(Uc)::value;
+          constexpr bool COLS = decltype(Cc)::value, NC = decltype(Nc)::value;
+          k_bsr_lane<B, B, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val,
+                                                                                  (const X*)x, epi);
+          done = true;
+        });
+      });
+    });
+  });
+  AMG_CK_LAUNCH();
+  return done;
+}
+
+bool launch_spmv_dot(const Mat& A, const void* x, int xt, double* y, const double* w0, const double* w1, int nd,
+                     double* partials, double* out, cudaStream_t s, CommBase* comm) {
+  if (nd < 1 || nd > 2) return false;
+  const double mb = mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + (double)A.n * A.b * 8.0 * (1 + nd);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  bool ok;
+  {
+    ProfScope ps_(prof_name("spmv_dot", A.b, A.vt, xt), mb, s);
+    if (nd == 1) ok = launch_lane_dot(A, x, xt, LEpiSpmvDot<1>{y, {w0, nullptr}, partials, out, ticket}, s);
+    else ok = launch_lane_dot(A, x, xt, LEpiSpmvDot<2>{y, {w0, w1}, partials, out, ticket}, s);
+  }
+  if (ok && comm) comm->allreduce_sum(out, nd, s);
+  return ok;
+}
+
+bool launch_residual_nrm(const Mat& A, const double* f, const void* x, int xt, double* r, double* partials,
+                         double* out, cudaStream_t s, CommBase* comm) {
+  const double mb = mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + (double)A.n * A.b * 16.0;
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  bool ok;
+  {
+    ProfScope ps_(prof_name("residual_nrm", A.b, A.vt, xt), mb, s);
+    ok = launch_lane_dot(A, x, xt, LEpiResidualNrm{f, r, partials, out, ticket}, s);
+  }
+  if (ok && comm) comm->allreduce_sum(out, 1, s);
+  return ok;
 }
 
 void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s) {
