@@ -198,7 +198,7 @@ struct LEpiResidualNrm {
 
 // ---------------------------------------------------------------- the kernel
 template <int BR, int BC, int U, bool COLS, bool NC, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __restrict__ ptr,
+__global__ void __launch_bounds__(256, 8) k_bsr_lane(int r0, int n, const int32_t* __restrict__ ptr,
                                                   const int32_t* __restrict__ col, const V* __restrict__ val,
                                                   const X* __restrict__ x, EPI epi) {
   static_assert(!COLS || BR == BC, "column layout needs square blocks");
@@ -208,12 +208,12 @@ __global__ void __launch_bounds__(256, 8) k_bsr_lane(int n, const int32_t* __res
   const int lane = threadIdx.x & 31;
   // virtual blocks of 8 warps: one per CUDA block, or -- fused dots -- a persistent grid
   // (at most kMaxPartials blocks) walks them, accumulating its dot partials
-  const int64_t nvb = ((int64_t)n + RPW * 8 - 1) / (RPW * 8);
+  const int64_t nvb = ((int64_t)(n - r0) + RPW * 8 - 1) / (RPW * 8);  // rows [r0, n)
   double dacc[ND] = {};
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
   const int warp = (int)(vb * (blockDim.x >> 5) + (threadIdx.x >> 5));
   const int g = lane / BR, r = lane - g * BR;
-  const int row = warp * RPW + g;
+  const int row = r0 + warp * RPW + g;
   LaneRow<BR> L;
   L.row = row;
   L.r = r;

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "amg.h"
@@ -72,6 +73,48 @@ void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_
     if (H.recv_cnt[i]) h.comm->recv(xc + ((size_t)H.nloc + H.recv_off[i]) * es, (size_t)H.recv_cnt[i] * es, p, s);
   }
   h.comm->group_end(s);
+}
+
+void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, int b, cudaStream_t s,
+                     const std::function<void(int, int)>& launch) {
+  const bool off = getenv("AMG_NO_OVERLAP") != nullptr;  // A/B switch (tests)
+  if (!h.comm || H.peers.empty()) {
+    launch(0, A.n);
+    return;
+  }
+  if (off || H.int_hi <= H.int_lo || A.lane_var > kLaneCN4 || A.tma_grid > 0 || !h.comm_s) {
+    halo_exchange(h, H, x, dt, b, s);
+    launch(0, A.n);
+    return;
+  }
+  const size_t es = dtype_size(dt) * b;
+  if (H.total_send > 0) {
+    ProfScope ps_("halo_pack", (double)H.total_send * es * 2.0, s);
+    if (dt == AMG_F32)
+      k_pack<float><<<grid_for((int64_t)H.total_send * b, 256), 256, 0, s>>>(H.total_send, b, H.send_idx,
+                                                                            (const float*)x, (float*)H.send_buf);
+    else
+      k_pack<double><<<grid_for((int64_t)H.total_send * b, 256), 256, 0, s>>>(H.total_send, b, H.send_idx,
+                                                                             (const double*)x, (double*)H.send_buf);
+    AMG_CK_LAUNCH();
+  }
+  AMG_CK(cudaEventRecord(h.ev_pack, s));
+  AMG_CK(cudaStreamWaitEvent(h.comm_s, h.ev_pack, 0));
+  char* xc = static_cast<char*>(x);
+  h.comm->group_begin();
+  for (size_t i = 0; i < H.peers.size(); ++i) {
+    const int p = H.peers[i];
+    if (H.send_cnt[i])
+      h.comm->send((char*)H.send_buf + (size_t)H.send_off[i] * es, (size_t)H.send_cnt[i] * es, p, h.comm_s);
+    if (H.recv_cnt[i])
+      h.comm->recv(xc + ((size_t)H.nloc + H.recv_off[i]) * es, (size_t)H.recv_cnt[i] * es, p, h.comm_s);
+  }
+  h.comm->group_end(h.comm_s);
+  AMG_CK(cudaEventRecord(h.ev_halo, h.comm_s));
+  launch(H.int_lo, H.int_hi);  // interior rows: no ghost read
+  AMG_CK(cudaStreamWaitEvent(s, h.ev_halo, 0));
+  launch(0, H.int_lo);
+  launch(H.int_hi, A.n);
 }
 
 void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s) {
@@ -150,6 +193,21 @@ void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bound
   H = Halo{};
   H.nloc = M.n;
   H.nghost = (int)ghosts.size();
+  {  // the longest run of rows without a ghost column (>= a quarter of the rows): overlap window
+    std::vector<int32_t> hp((size_t)M.n + 1);
+    AMG_CK(cudaMemcpy(hp.data(), M.ptr, sizeof(int32_t) * (M.n + 1), cudaMemcpyDeviceToHost));
+    int32_t best_lo = 0, best_hi = 0, run_lo = 0;
+    for (int32_t r = 0; r <= M.n; ++r) {
+      bool ghost_row = r == M.n;
+      if (r < M.n)
+        for (int32_t k = hp[r]; k < hp[r + 1] && !ghost_row; ++k) ghost_row = c[k] >= M.n;
+      if (ghost_row) {
+        if (r - run_lo > best_hi - best_lo) best_lo = run_lo, best_hi = r;
+        run_lo = r + 1;
+      }
+    }
+    if ((int64_t)(best_hi - best_lo) * 4 >= M.n && H.nghost > 0) H.int_lo = best_lo, H.int_hi = best_hi;
+  }
   M.m = M.n + H.nghost;
   // how many ghosts I need from every rank; everybody learns the full P x P matrix
   std::vector<int64_t> need(P, 0), all((size_t)P * P);

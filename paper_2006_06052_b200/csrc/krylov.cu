@@ -34,24 +34,29 @@ struct Ctx {
   }
   // x: a vector with ghost space (workspace / Z basis); ghosts exchanged first
   void spmv(const void* x, int xt, double* y) {
-    halo_exchange(h, h.halo0, const_cast<void*>(x), xt, h.b, s);
-    launch_spmv(h.A, 1.0, x, xt, 0.0, y, AMG_F64, s);
+    halo_overlapped(h, h.halo0, h.A, const_cast<void*>(x), xt, h.b, s,
+                    [&](int r0, int r1) { launch_spmv(h.A, 1.0, x, xt, 0.0, y, AMG_F64, s, r0, r1); });
     bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0);
   }
   // x: the caller's iterate (no ghost space): copied into x_ext when distributed
   void residual(const double* b, const double* x, double* r) {
     if (h.comm) {
       AMG_CK(cudaMemcpyAsync(h.x_ext, x, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-      halo_exchange(h, h.halo0, h.x_ext, AMG_F64, h.b, s);
       x = h.x_ext;
     }
-    launch_residual(h.A, b, x, r, AMG_F64, s);
+    halo_overlapped(h, h.halo0, h.A, const_cast<double*>(x), AMG_F64, h.b, s,
+                    [&](int r0, int r1) { launch_residual(h.A, b, x, r, AMG_F64, s, r0, r1); });
     bytes += h.alg_bytes_spmv + 8.0 * N;
   }
   // y = A x with dscal[j] = w_j . y (w_j == nullptr: y . y), j < nd: one fused pass when the
   // operator's plan allows it (K3), else the SpMV and the dots
   void spmv_dot(const void* x, int xt, double* y, const double* w0, const double* w1, int nd) {
-    halo_exchange(h, h.halo0, const_cast<void*>(x), xt, h.b, s);
+    if (h.comm) {  // distributed: the exchange overlaps the interior rows, dots separate
+      spmv(x, xt, y);
+      dot(w0 ? w0 : y, y, 0);
+      if (nd > 1) dot(w1 ? w1 : y, y, 1);
+      return;
+    }
     if (launch_spmv_dot(h.A, x, xt, y, w0, w1, nd, h.partials, h.dscal, s, h.comm)) {
       bytes += h.alg_bytes_spmv + N * ((double)dtype_size(xt) - 8.0) + 8.0 * N * ((w0 ? 1 : 0) + (w1 ? 1 : 0));
       return;
@@ -63,10 +68,10 @@ struct Ctx {
   }
   // r = b - A x with dscal[0] = r . r (K2 fused when the plan allows it)
   void residual_nrm(const double* b, const double* x, double* r) {
-    if (h.comm) {
-      AMG_CK(cudaMemcpyAsync(h.x_ext, x, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-      halo_exchange(h, h.halo0, h.x_ext, AMG_F64, h.b, s);
-      x = h.x_ext;
+    if (h.comm) {  // distributed: overlapped residual, then the norm
+      residual(b, x, r);
+      dot(r, r, 0);
+      return;
     }
     if (launch_residual_nrm(h.A, b, x, AMG_F64, r, h.partials, h.dscal, s, h.comm)) {
       bytes += h.alg_bytes_spmv + 8.0 * N;

@@ -17,8 +17,9 @@ int64_t csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* 
                    const void* val, int dtype, int32_t* bptr, int32_t* bcol, void* bval, cudaStream_t s);
 
 // K1  y = alpha A x + beta y
+// (r0, r1): only block rows [r0, r1) (row-lane plans; r1 < 0 = all rows)
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
-                 cudaStream_t s);
+                 cudaStream_t s, int r0 = 0, int r1 = -1);
 class CommBase;
 // K3  y = A x (fp64 y) with out[j] = w_j . y (w_j == nullptr: y.y), j < nd <= 2, in ONE pass
 // (row-lane plans; false: not fused, the caller runs the SpMV and the dots); partials as
@@ -29,10 +30,11 @@ bool launch_spmv_dot(const Mat& A, const void* x, int xt, double* y, const doubl
 bool launch_residual_nrm(const Mat& A, const double* f, const void* x, int xt, double* r, double* partials,
                          double* out, cudaStream_t s, CommBase* comm);
 // K2  r = f - A x   (f, x, r of type xt)
-void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s);
+void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s, int r0 = 0,
+                     int r1 = -1);
 // K5  xo = x + M (f - A x)
 void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
-                   cudaStream_t s);
+                   cudaStream_t s, int r0 = 0, int r1 = -1);
 // K4a x = M f
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
                     cudaStream_t s);

@@ -16,6 +16,9 @@ Handle::~Handle() {
   for (PcGraph& G : pc_graphs)
     if (G.exec) cudaGraphExecDestroy(G.exec);
   if (work) cudaStreamDestroy(work);
+  if (comm_s) cudaStreamDestroy(comm_s);
+  if (ev_pack) cudaEventDestroy(ev_pack);
+  if (ev_halo) cudaEventDestroy(ev_halo);
   if (ev_in) cudaEventDestroy(ev_in);
   if (ev_out) cudaEventDestroy(ev_out);
   for (Level& L : lv)
@@ -64,6 +67,11 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     h.pp = h.arena.alloc(std::max(h.n + h.halo0.nghost, 1) * xs);
   }
   AMG_CK(cudaStreamCreateWithFlags(&h.work, cudaStreamNonBlocking));
+  if (h.comm) {
+    AMG_CK(cudaStreamCreateWithFlags(&h.comm_s, cudaStreamNonBlocking));
+    AMG_CK(cudaEventCreateWithFlags(&h.ev_pack, cudaEventDisableTiming));
+    AMG_CK(cudaEventCreateWithFlags(&h.ev_halo, cudaEventDisableTiming));
+  }
   AMG_CK(cudaEventCreateWithFlags(&h.ev_in, cudaEventDisableTiming));
   AMG_CK(cudaEventCreateWithFlags(&h.ev_out, cudaEventDisableTiming));
   AMG_CK(cudaEventCreate(&h.ev0));

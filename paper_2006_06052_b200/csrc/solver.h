@@ -1,6 +1,7 @@
 // solver.h -- the solver handle: hierarchy, Schur pieces, Krylov workspace.
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "blas1.h"
@@ -21,6 +22,9 @@ struct Halo {
   int32_t* send_idx = nullptr;  // device [total_send]: local rows to pack
   int total_send = 0;
   void* send_buf = nullptr;     // device, total_send * 4 doubles
+  // rows [int_lo, int_hi) reference no ghost: computed while the exchange is in flight
+  // (empty: no overlap)
+  int32_t int_lo = 0, int_hi = 0;
 };
 
 struct Level {
@@ -98,6 +102,8 @@ struct Handle {
   CommBase* comm = nullptr;
   Halo halo0;
   double* x_ext = nullptr;         // fp64 copy of the iterate with ghost space
+  cudaStream_t comm_s = nullptr;   // halo exchanges overlapped with the interior rows
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   int64_t row_lo = 0;
   int64_t n_global_rows = 0;       // global block rows (== n when not distributed)
   std::vector<std::vector<int64_t>> lbounds;
@@ -116,6 +122,11 @@ Handle* build_handle(const Mat& view, const amg_params* p, const std::vector<int
                      bool workspace = true);
 // dist.cu
 void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_t s);
+// launch(r0, r1) over all block rows of A, x's ghosts exchanged first -- on the handle's
+// comm stream while the interior rows [H.int_lo, H.int_hi) run, then the
+// boundary rows.  Row-lane plans only; otherwise exchange, then one launch.
+void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, int b, cudaStream_t s,
+                     const std::function<void(int, int)>& launch);
 void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s);
 void coarse_allgather(Handle& h, cudaStream_t s);
 // vcycle.cu

@@ -278,7 +278,11 @@ static void dispatch_lane(int var, F&& f) {
 }
 
 template <int BR, int BC, typename V, typename X, class EPI>
-static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r0 = 0, int r1 = -1) {
+  if (r1 < 0) r1 = A.n;
+  if (r1 <= r0) return;
+  if ((r0 > 0 || r1 < A.n) && (A.lane_var > kLaneCN4 || A.tma_grid > 0))
+    fail(AMG_EINVAL, "row ranges need a row-lane plan");
   constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
   if constexpr (BR == BC && BR >= 2) {
     if (A.lane_var == kLaneSell) {
@@ -298,24 +302,26 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
     return;
   }
   constexpr int RPW = 32 / BR;
-  const int64_t warps = ((int64_t)A.n + RPW - 1) / RPW;
+  const int64_t warps = ((int64_t)(r1 - r0) + RPW - 1) / RPW;
   const unsigned grid = grid_for(warps * 32, kBlock);
   dispatch_lane<BR, BC>(A.lane_var, [&](auto Uc, auto Cc, auto Nc) {
     constexpr int U = decltype(Uc)::value;
     constexpr bool COLS = decltype(Cc)::value, NC = decltype(Nc)::value;
     if (can_fast && A.fast32)
-      k_bsr_lane<BR, BC, U, COLS, NC, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+      k_bsr_lane<BR, BC, U, COLS, NC, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(r0, r1, A.ptr, A.col, (const V*)A.val, x, epi);
     else
-      k_bsr_lane<BR, BC, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+      k_bsr_lane<BR, BC, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(r0, r1, A.ptr, A.col, (const V*)A.val, x, epi);
   });
 }
 
 void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta, void* y, int yt,
-                 cudaStream_t s) {
-  if (A.n == 0) return;
+                 cudaStream_t s, int r0, int r1) {
+  if (r1 < 0) r1 = A.n;
+  if (A.n == 0 || r1 <= r0) return;
+  const double frac = (double)(r1 - r0) / A.n;
   ProfScope ps_(prof_name("spmv", A.b, A.vt, xt),
-                mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) +
-                    (double)A.n * A.b * dtype_size(yt) * (beta != 0.0 ? 2.0 : 1.0), s);
+                frac * (mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) +
+                        (double)A.n * A.b * dtype_size(yt) * (beta != 0.0 ? 2.0 : 1.0)), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_t(A.vt, [&](auto v) {
@@ -328,7 +334,7 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
             if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
             else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
           } else {
-            launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmv<Y>{alpha, beta, (Y*)y}, s);
+            launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmv<Y>{alpha, beta, (Y*)y}, s, r0, r1);
           }
         });
       });
@@ -354,8 +360,8 @@ static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaSt
         dispatch_lane<B, B>(A.lane_var, [&](auto Uc, auto Cc, auto Nc) {
           constexpr int U = decltype(Uc)::value;
           constexpr bool COLS = decltype(Cc)::value, NC = decltype(Nc)::value;
-          k_bsr_lane<B, B, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val,
-                                                                                  (const X*)x, epi);
+          k_bsr_lane<B, B, U, COLS, NC, V, X, false, EPI><<<grid, kBlock, 0, s>>>(0, A.n, A.ptr, A.col,
+                                                                                  (const V*)A.val, (const X*)x, epi);
           done = true;
         });
       });
@@ -393,10 +399,12 @@ bool launch_residual_nrm(const Mat& A, const double* f, const void* x, int xt, d
   return ok;
 }
 
-void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s) {
-  if (A.n == 0) return;
+void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt, cudaStream_t s, int r0, int r1) {
+  if (r1 < 0) r1 = A.n;
+  if (A.n == 0 || r1 <= r0) return;
+  const double frac = (double)(r1 - r0) / A.n;
   ProfScope ps_(prof_name("residual", A.b, A.vt, xt),
-                mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + 2.0 * A.n * A.b * dtype_size(xt), s);
+                frac * (mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + 2.0 * A.n * A.b * dtype_size(xt)), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_t(A.vt, [&](auto v) {
@@ -407,7 +415,7 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
           if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
           else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, EpiResidual<B, X>{(const X*)f, (X*)r}, s);
         } else {
-          launch_lane<B, B, V, X>(A, (const X*)x, LEpiResidual<X>{(const X*)f, (X*)r}, s);
+          launch_lane<B, B, V, X>(A, (const X*)x, LEpiResidual<X>{(const X*)f, (X*)r}, s, r0, r1);
         }
       });
     });
@@ -416,10 +424,12 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
 }
 
 void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
-                   cudaStream_t s) {
-  if (A.n == 0) return;
+                   cudaStream_t s, int r0, int r1) {
+  if (r1 < 0) r1 = A.n;
+  if (A.n == 0 || r1 <= r0) return;
+  const double frac = (double)(r1 - r0) / A.n;
   ProfScope ps_(prof_name("smooth", A.b, A.vt, xt),
-                mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 3.0 * A.n * A.b * dtype_size(xt), s);
+                frac * (mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 3.0 * A.n * A.b * dtype_size(xt)), s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_t(A.vt, [&](auto v) {
@@ -431,7 +441,8 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
           if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, e, s);
           else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, e, s);
         } else {
-          launch_lane<B, B, V, X>(A, (const X*)x, LEpiSmooth<V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s);
+          launch_lane<B, B, V, X>(A, (const X*)x, LEpiSmooth<V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s,
+                                  r0, r1);
         }
       });
     });

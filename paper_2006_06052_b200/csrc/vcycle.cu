@@ -27,12 +27,12 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   void* t = L.t;
   launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
   for (int k = 1; k < h.p.npre; ++k) {
-    halo_exchange(h, L.halo, x, xt, L.A.b, s);
-    launch_smooth(L.A, L.M, L.f, x, t, xt, s);
+    halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
+                    [&](int r0, int r1) { launch_smooth(L.A, L.M, L.f, x, t, xt, s, r0, r1); });
     std::swap(x, t);
   }
-  halo_exchange(h, L.halo, x, xt, L.A.b, s);
-  launch_residual(L.A, L.f, x, L.r, xt, s);  // K4b: r = f - A x
+  halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
+                  [&](int r0, int r1) { launch_residual(L.A, L.f, x, L.r, xt, s, r0, r1); });  // K4b: r = f - A x
   void* fc = (l + 1 < h.lv.size()) ? h.lv[l + 1].f
                                    : (void*)((char*)h.coarse.f + (h.comm ? h.coarse.off[h.comm->rank] * h.coarse.b *
                                                                               dtype_size(xt)
@@ -41,8 +41,8 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   void* xc = vcycle_run(h, l + 1, s);
   launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
   for (int k = 0; k < h.p.npost; ++k) {          // K5: post-smooth (double-buffered)
-    halo_exchange(h, L.halo, x, xt, L.A.b, s);
-    launch_smooth(L.A, L.M, L.f, x, t, xt, s);
+    halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
+                    [&](int r0, int r1) { launch_smooth(L.A, L.M, L.f, x, t, xt, s, r0, r1); });
     std::swap(x, t);
   }
   return x;

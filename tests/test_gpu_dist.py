@@ -125,3 +125,16 @@ def test_nccl_communicator_single_rank(amg):
     rep1 = S1.solve(b, x1, 1e-8)
     assert rep.converged and rep.iters == rep1.iters
     assert torch.allclose(x, x1, rtol=0, atol=1e-12 * float(x1.abs().max()))
+
+
+def test_halo_overlap_is_exact(amg, envvars):
+    # the interior rows computed while the exchange is in flight, then the boundary rows:
+    # the same per-row arithmetic as exchange-then-compute -> bit-identical iterates
+    runs = []
+    for off in (False, True):
+        if off:
+            envvars(AMG_NO_OVERLAP=1)
+        out, x, relres, _ = run_dist(amg, 2, gen.STOKES, 16, gen.RHS_LID_NOISE, solver=2, precond=1)
+        runs.append((x, out[0][0].iters))
+    assert runs[0][1] == runs[1][1]
+    assert np.array_equal(runs[0][0], runs[1][0])
