@@ -174,6 +174,13 @@ int amg_schur_export(struct amg_handle* h, double* shat_diag, double* m_s);
 int amg_vcycle(struct amg_handle* h, const double* f, double* x, void* stream);
 /* device bytes held by the handle (hierarchy + workspace) */
 int64_t amg_device_bytes(struct amg_handle* h);
+/* Memory footprint per component (the paper's memory comparisons, PAPER.md:717-718,
+ * 836-857), bytes, out[n >= 8] (host): [0] outer operator (BSR + sliced copy),
+ * [1] hierarchy A_l/P_l/R_l (BSR), [2] their sliced copies, [3] smoother blocks M_l,
+ * [4] Schur B, B^T, m_S, [5] coarse inverse, [6] Krylov workspace vectors, [7] total
+ * allocated by the handle (includes halo buffers, aggregates, padding).  AMG_EINVAL on a
+ * NULL handle / out or n < 8. */
+int amg_memory_report(struct amg_handle* h, int64_t* out, int32_t n);
 
 /* ---- launch accounting / per-kernel timing (diagnostics, host) ---- */
 /* number of library kernels launched by this process so far */

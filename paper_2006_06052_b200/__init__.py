@@ -62,7 +62,7 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_level_aggregates", "amg_schur_export", "amg_vcycle", "amg_device_bytes",
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
-           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr",
+           "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr", "amg_memory_report",
            "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local"]
 
 _lib = None
@@ -93,6 +93,7 @@ def lib():
             "amg_schur_export": (i32, [P, P, P]),
             "amg_vcycle": (i32, [P, P, P, P]),
             "amg_device_bytes": (i64, [P]),
+            "amg_memory_report": (i32, [P, P, i32]),
             "amg_comm_unique_id": (i32, [P]),
             "amg_comm_init": (i32, [P, i32, i32, P]),
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
@@ -370,6 +371,14 @@ class Solver:
         _check(lib().amg_schur_export(self.h, d.ctypes.data_as(ctypes.c_void_p), m.ctypes.data_as(ctypes.c_void_p)),
                "amg_schur_export")
         return d, m
+
+    def memory_report(self) -> dict:
+        """amg_memory_report: device bytes per component."""
+        import numpy as np
+        out = np.zeros(8, dtype=np.int64)
+        _check(lib().amg_memory_report(self.h, out.ctypes.data_as(ctypes.c_void_p), 8), "amg_memory_report")
+        keys = ["outer_A", "hierarchy", "sliced_copies", "smoothers", "schur", "coarse_inverse", "krylov", "total"]
+        return dict(zip(keys, (int(v) for v in out)))
 
     @property
     def device_bytes(self) -> int:

@@ -329,4 +329,40 @@ int64_t amg_device_bytes(struct amg_handle* hh) {
   return h ? h->arena.bytes() : 0;
 }
 
+int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
+  AMG_GUARD_BEGIN
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !out || n < 8) return AMG_EINVAL;
+  auto mat = [&](const Mat& M) -> int64_t {
+    if (!M.ptr) return 0;
+    return 4LL * (M.n + 1) + M.nnz * (4LL + (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt));
+  };
+  auto sell = [&](const Mat& M) -> int64_t {
+    if (M.lane_var != kLaneSell || !M.sell_ptr) return 0;
+    const int C = 32 / M.b;
+    std::vector<int32_t> last(1);
+    AMG_CK(cudaMemcpy(last.data(), M.sell_ptr + M.sell_ns, 4, cudaMemcpyDeviceToHost));
+    const int64_t steps = last[0];
+    return 4LL * (M.sell_ns + 1) + steps * C * (4LL + (int64_t)M.b * M.b * dtype_size(M.vt)) +
+           (M.sell_perm ? 4LL * M.sell_ns * C : 0);
+  };
+  int64_t v[8] = {};
+  v[0] = mat(h->A) + sell(h->A);
+  for (const Level& L : h->lv) {
+    v[1] += mat(L.A) + mat(L.P) + mat(L.R);
+    v[2] += sell(L.A) + sell(L.P) + sell(L.R);
+    v[3] += (int64_t)L.A.n * L.A.b * L.A.b * dtype_size(h->vt);
+  }
+  if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
+  v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
+  const int64_t N = (int64_t)h->n * h->b;
+  v[6] = 8LL * N * ((int64_t)h->vec.size() + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
+                    (int64_t)h->Ui.size()) +
+         (int64_t)h->Z.size() * N * dtype_size(h->zt);
+  v[7] = h->arena.bytes();
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  return AMG_OK;
+  AMG_GUARD_END
+}
+
 }  // extern "C"

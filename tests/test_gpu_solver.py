@@ -291,3 +291,13 @@ def test_maxiter_not_converged(amg, solver):
     true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
     assert abs(true - rep.relres_true) <= 1e-10 * max(true, 1.0)
     assert abs(rep.relres_true - ro.relres_true) <= 1e-6 * ro.relres_true
+
+
+def test_memory_report(amg):
+    ptr, col, val = gen.matrix(gen.STOKES, 16)
+    S = amg.Solver(amg.BSR.from_numpy(ptr, col, val), amg.default_params(solver=2, precond=1))
+    m = S.memory_report()
+    nnz = len(col)
+    assert m["outer_A"] >= nnz * (4 + 16 * 8)  # 4x4 fp64 library copy
+    assert m["hierarchy"] > 0 and m["smoothers"] > 0 and m["schur"] > 0 and m["krylov"] > 0
+    assert sum(v for k, v in m.items() if k != "total") <= m["total"] == S.device_bytes

@@ -60,7 +60,7 @@ def main():
                     ts.append(e0.elapsed_time(e1) / 1e3)
                 r = {"n": n, "cfg": cfg, "solver": sname, "variant": vname, "setup_s": setup_s,
                      "solve_s": sorted(ts)[1], "iters": rep.iters, "relres_true": rep.relres_true,
-                     "converged": bool(rep.converged), "levels": rep.levels, "device_bytes": S.device_bytes,
+                     "converged": bool(rep.converged), "levels": rep.levels, "device_bytes": S.device_bytes, "memory": S.memory_report(),
                      "alg_bytes": rep.alg_bytes}
                 rows.append(r)
                 print(json.dumps(r), flush=True)
