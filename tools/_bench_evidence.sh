@@ -13,6 +13,11 @@ ncu -f --set full --clock-control none --import-source on --kernel-name-base dem
 tail -2 /tmp/ncu_top.log
 ncu -i /tmp/top.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_top_details.csv
 ncu -i /tmp/top.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_top_raw.csv
+rm -f /tmp/smooth.ncu-rep
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_lane.*LEpiSmooth<float, float>" -c 1 -o /tmp/smooth python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_smooth.log 2>&1
+tail -2 /tmp/ncu_smooth.log
+ncu -i /tmp/smooth.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_smooth_details.csv
+ncu -i /tmp/smooth.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_smooth_raw.csv
 python tools/spmv_probe.py 4 1 0 5 > gpurun_out/${TAG}_spmv_plain.log 2>&1 || exit 1
 ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sell" -s 2 -c 1 -o /tmp/spmv python tools/spmv_probe.py 4 1 0 5 > /tmp/ncu_spmv.log 2>&1
 tail -2 /tmp/ncu_spmv.log
