@@ -91,6 +91,20 @@ struct LEpiSpmv {  // y = alpha A x + beta y
     if (beta != 0.0) v = fma(beta, (double)y[o], v);
     y[o] = to_out<Y>(v);
   }
+  // row-per-lane form (k_bsr_sellr): the lane holds the row's BR results
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double v[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) v[c] = beta != 0.0 ? (double)y[o + c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < BR; ++c) {
+      double t = alpha * yr[c];
+      if (beta != 0.0) t = fma(beta, v[c], t);
+      y[o + c] = to_out<Y>(t);
+    }
+  }
 };
 
 template <typename X>
@@ -103,6 +117,15 @@ struct LEpiResidual {  // r = f - A x
     if (!L.valid) return;
     const int64_t o = (int64_t)L.row * BR + L.r;
     res[o] = to_out<X>((double)f[o] - L.yr);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double fv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) fv[c] = (double)f[o + c];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) res[o + c] = to_out<X>(fv[c] - yr[c]);
   }
 };
 
@@ -127,6 +150,22 @@ struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
 #pragma unroll
     for (int c = 1; c < BR; ++c) t = fma(m[c], rv[c], t);
     xo[o] = to_out<X>((double)x[o] + t);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double rv[BR], xv[BR], m[BR][BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = (double)f[o + c] - yr[c], xv[c] = (double)x[o + c];
+#pragma unroll
+    for (int i = 0; i < BR; ++i) load_b<BR, false>(M + (o + i) * BR, m[i]);
+#pragma unroll
+    for (int i = 0; i < BR; ++i) {
+      double t = m[i][0] * rv[0];
+#pragma unroll
+      for (int c = 1; c < BR; ++c) t = fma(m[i][c], rv[c], t);
+      xo[o + i] = to_out<X>(xv[i] + t);
+    }
   }
 };
 
@@ -175,6 +214,19 @@ struct LEpiSpmvDot {
 #pragma unroll
     for (int j = 0; j < ND; ++j) d[j] = fma(w[j] ? w[j][o] : L.yr, L.yr, d[j]);
   }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+#pragma unroll
+    for (int c = 0; c < BR; ++c) y[(int64_t)row * BR + c] = yr[c];
+  }
+  template <int BR>
+  __device__ __forceinline__ void row_dots(int row, const double (&yr)[BR], double (&d)[ND]) const {
+    const int64_t o = (int64_t)row * BR;
+#pragma unroll
+    for (int j = 0; j < ND; ++j)
+#pragma unroll
+      for (int c = 0; c < BR; ++c) d[j] = fma(w[j] ? w[j][o + c] : yr[c], yr[c], d[j]);
+  }
 };
 
 // fused residual + norm (K2): r = f - A x; d_0 += r_o^2
@@ -193,6 +245,21 @@ struct LEpiResidualNrm {
     if (!L.valid) return;
     const double v = f[(int64_t)L.row * BR + L.r] - L.yr;
     d[0] = fma(v, v, d[0]);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+#pragma unroll
+    for (int c = 0; c < BR; ++c) r[o + c] = f[o + c] - yr[c];
+  }
+  template <int BR>
+  __device__ __forceinline__ void row_dots(int row, const double (&yr)[BR], double (&d)[1]) const {
+    const int64_t o = (int64_t)row * BR;
+#pragma unroll
+    for (int c = 0; c < BR; ++c) {
+      const double v = f[o + c] - yr[c];
+      d[0] = fma(v, v, d[0]);
+    }
   }
 };
 
@@ -418,6 +485,127 @@ __global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const i
   Lr.valid = act && Lr.row >= 0 && Lr.row < n;
   Lr.yr = sum;
   epi(Lr);
+}
+
+// ---------------------------------------------------------------- interleaved row-per-lane
+// Opt-in (AMG_SELLR=1/2 or AMG_LANE_VAR=8; measured slower than the row-component lanes
+// and the sliced copy on every level of the cfg-5 hierarchy).  The solve
+// copy interleaves 32 consecutive block rows (one slice, one warp; lane = row).  Each
+// row's blocks are flattened ([block][i][c], padded to the slice's longest row with zero
+// blocks) and cut into W-element vectors (W = 16 bytes / sizeof(V)); vector t of lane l
+// sits at (vptr[s] + t) * 32 + l, so every value load of the warp is 32 x 16 contiguous
+// bytes (4 L1 wavefronts, no sector shared between instructions) and column index j of
+// the slice is one 128-byte load.  GB blocks (the least multiple of the block that fills
+// whole vectors: 4 for 3x3 fp32, 2 for 3x3 fp64, 1 for 4x4) are loaded per step, all
+// loads first, the next step's column indices one step ahead.  The lane owns its row's
+// BR results and runs the epilogue's row-per-lane form (row(), row_dots()).
+// Arithmetic: the block-row dots of k_bsr_lane's ROWS layout in the same block order --
+// bit-identical to it.
+template <int B, int W>
+struct SellrShape {
+  static constexpr int E = B * B;
+  static constexpr int gcd(int a, int b) { return b == 0 ? a : gcd(b, a % b); }
+  static constexpr int GB = W / gcd(E, W);  // blocks per step: lcm(E, W) / E
+  static constexpr int NV = GB * E / W;     // vectors per step
+};
+// resident blocks per SM: a step's values take NV * W registers; above 16 words the
+// kernel needs more than 64 registers per thread (3 blocks: 85; fp64 products of 36
+// fp32 values, 2 blocks: 128)
+template <int B, int W, typename V, bool FAST>
+constexpr int sellr_min_blocks() {
+  constexpr int words = SellrShape<B, W>::NV * W * (int)sizeof(V) / 4;
+  return words <= 16 ? 4 : (FAST || words <= 18 ? 3 : 2);
+}
+
+template <int W, typename V>
+__device__ __forceinline__ void ld_vec(const V* __restrict__ p, V* v) {
+  if constexpr (W == 4 && std::is_same_v<V, float>) {
+    const float4 q = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else if constexpr (W == 2 && std::is_same_v<V, float>) {
+    const float2 q = __ldcs(reinterpret_cast<const float2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else if constexpr (W == 2 && std::is_same_v<V, double>) {
+    const double2 q = __ldcs(reinterpret_cast<const double2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else {
+    static_assert(W == 1, "vector width");
+    v[0] = __ldcs(p);
+  }
+}
+
+// One step: GB blocks of the lane's row.  c holds this step's column indices (loaded one
+// step ahead); the value loads, the x gathers and the next step's column loads are all
+// issued before any arithmetic.
+template <int B, int W, bool TAIL, typename V, typename X, bool FAST>
+__device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32_t* __restrict__ cpn,
+                                           const X* __restrict__ x, int nb, int nbn, int (&c)[SellrShape<B, W>::GB],
+                                           double (&acc)[B]) {
+  using S = SellrShape<B, W>;
+  V a[S::NV * W];
+  const int nv = TAIL ? (S::E * nb + W - 1) / W : S::NV;
+#pragma unroll
+  for (int q = 0; q < S::NV; ++q)
+    if (!TAIL || q < nv) ld_vec<W>(vp + (int64_t)q * 32 * W, a + q * W);
+  X xv[S::GB][B];
+#pragma unroll
+  for (int u = 0; u < S::GB; ++u)
+    if (!TAIL || u < nb) ld_x<B>(x + (int64_t)c[u] * B, xv[u]);
+  if constexpr (!TAIL) {
+#pragma unroll
+    for (int u = 0; u < S::GB; ++u) c[u] = u < nbn ? __ldcs(cpn + u * 32) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < S::GB; ++u) {
+    if (TAIL && u >= nb) continue;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      V ar[B];
+#pragma unroll
+      for (int cc = 0; cc < B; ++cc) ar[cc] = a[u * S::E + i * B + cc];
+      acc[i] += item_dot<B, V, X, FAST>(ar, xv[u]);
+    }
+  }
+}
+
+template <int B, int W, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(256, (sellr_min_blocks<B, W, V, FAST>())) k_bsr_sellr(
+    int n, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
+    const int32_t* __restrict__ perm, const int32_t* __restrict__ scol, const V* __restrict__ sval,
+    const X* __restrict__ x, EPI epi) {
+  using S = SellrShape<B, W>;
+  constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nvb = ((int64_t)nslices + 7) / 8;
+  double dacc[ND] = {};
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int s = (int)(vb * 8 + w);
+    double acc[B] = {};
+    if (s < nslices) {
+      const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;
+      const V* vp = sval + ((int64_t)__ldg(vptr + s) * 32 + lane) * W;
+      const int32_t* cp = scol + (int64_t)j0 * 32 + lane;
+      int c[S::GB];
+#pragma unroll
+      for (int u = 0; u < S::GB; ++u) c[u] = u < L ? __ldcs(cp + u * 32) : 0;
+      int j = 0;
+#pragma unroll 1
+      for (; j + S::GB <= L; j += S::GB) {
+        cp += S::GB * 32;
+        sellr_step<B, W, false, V, X, FAST>(vp, cp, x, S::GB, min(S::GB, L - j - S::GB), c, acc);
+        vp += (int64_t)S::NV * 32 * W;
+      }
+      if (j < L) sellr_step<B, W, true, V, X, FAST>(vp, cp, x, L - j, 0, c, acc);
+    }
+    int row = s * 32 + lane;
+    if (perm && s < nslices) row = __ldg(perm + (int64_t)s * 32 + lane);  // sorted windows (-1: padding)
+    if (s < nslices && row >= 0 && row < n) {
+      epi.template row<B>(row, acc);
+      if constexpr (EPI::kDots > 0) epi.template row_dots<B>(row, acc, dacc);
+    }
+  }
+  if constexpr (EPI::kDots > 0)
+    block_reduce_finish<EPI::kDots, 256>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out, 0, nullptr);
 }
 
 }  // namespace amgb

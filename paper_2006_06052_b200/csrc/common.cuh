@@ -71,7 +71,8 @@ class Arena {
 
 enum { kTmaNone = 0, kTmaGroup = 1, kTmaRows = 2, kTmaSeg = 3 };
 // bsr_lane.cuh variants: R/C = ROWS/COLS layout, C/N = streaming / L1-allocating loads, U
-enum { kLaneRC2 = 0, kLaneRC4 = 1, kLaneRN2 = 2, kLaneRN4 = 3, kLaneCN2 = 4, kLaneCN4 = 5, kLaneW = 6 /* warp per row */, kLaneSell = 7 /* sliced copy */ };
+enum { kLaneRC2 = 0, kLaneRC4 = 1, kLaneRN2 = 2, kLaneRN4 = 3, kLaneCN2 = 4, kLaneCN4 = 5, kLaneW = 6 /* warp per row */, kLaneSell = 7 /* sliced copy */,
+       kLaneSellR = 8 /* interleaved row-per-lane copy */ };
 
 // Device BSR matrix with b x b blocks (PAPER.md:666-672 layout); the Schur coupling
 // views use rectangular br x bc blocks on the outer pattern.
@@ -94,6 +95,10 @@ struct Mat {
   int32_t* sell_col = nullptr;  // [steps][C]
   void* sell_val = nullptr;     // [steps][b][C][b]
   int32_t* sell_perm = nullptr; // [sell_ns * C] slot -> row (-1: padding slot), or nullptr (in order)
+  // kLaneSellR (k_bsr_sellr, C = 32): sell_col [steps][32], sell_val [vectors][32][sell_w],
+  // sell_vptr [sell_ns + 1] vector offsets
+  int32_t* sell_vptr = nullptr;
+  int sell_w = 0;
   bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
   int rows_per_block() const { return br ? br : b; }
   int cols_per_block() const { return bc ? bc : b; }

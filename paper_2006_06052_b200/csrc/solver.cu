@@ -338,13 +338,17 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
     return 4LL * (M.n + 1) + M.nnz * (4LL + (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt));
   };
   auto sell = [&](const Mat& M) -> int64_t {
-    if (M.lane_var != kLaneSell || !M.sell_ptr) return 0;
-    const int C = 32 / M.b;
-    std::vector<int32_t> last(1);
-    AMG_CK(cudaMemcpy(last.data(), M.sell_ptr + M.sell_ns, 4, cudaMemcpyDeviceToHost));
-    const int64_t steps = last[0];
-    return 4LL * (M.sell_ns + 1) + steps * C * (4LL + (int64_t)M.b * M.b * dtype_size(M.vt)) +
-           (M.sell_perm ? 4LL * M.sell_ns * C : 0);
+    if ((M.lane_var != kLaneSell && M.lane_var != kLaneSellR) || !M.sell_ptr) return 0;
+    const int C = M.lane_var == kLaneSellR ? 32 : 32 / M.b;
+    int32_t last = 0;
+    AMG_CK(cudaMemcpy(&last, M.sell_ptr + M.sell_ns, 4, cudaMemcpyDeviceToHost));
+    const int64_t steps = last;
+    const int64_t perm = M.sell_perm ? 4LL * M.sell_ns * C : 0;
+    if (M.lane_var == kLaneSell)
+      return 4LL * (M.sell_ns + 1) + steps * C * (4LL + (int64_t)M.b * M.b * dtype_size(M.vt)) + perm;
+    int32_t nvec = 0;
+    AMG_CK(cudaMemcpy(&nvec, M.sell_vptr + M.sell_ns, 4, cudaMemcpyDeviceToHost));
+    return 8LL * (M.sell_ns + 1) + steps * C * 4LL + (int64_t)nvec * C * M.sell_w * dtype_size(M.vt) + perm;
   };
   int64_t v[8] = {};
   v[0] = mat(h->A) + sell(h->A);

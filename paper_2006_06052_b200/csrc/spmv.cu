@@ -132,14 +132,20 @@ __global__ void k_sell_fill(int n, int b, int C, int ns, const int32_t* __restri
 // blocks -- sorted by length (descending, stable) inside windows of 32 slices (SELL-C-sigma,
 // sigma = 32 C): a slot -> row permutation kept on the device, the epilogue writes row
 // perm[slot].  Only rows inside one window are reordered, so the output stays local.
-static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
-  const int C = 32 / A.b;
+struct Slicing {
+  int ns = 0;
+  std::vector<int32_t> h, perm;  // steps per slice; slot -> row (empty: in order)
+};
+
+static Slicing slice_rows(const Mat& A, int C, cudaStream_t s) {
+  Slicing out;
   const int ns = (int)((A.n + C - 1) / C);
+  out.ns = ns;
   std::vector<int32_t> hp((size_t)A.n + 1);
   AMG_CK(cudaMemcpyAsync(hp.data(), A.ptr, sizeof(int32_t) * (A.n + 1), cudaMemcpyDeviceToHost, s));
   AMG_CK(cudaStreamSynchronize(s));
   auto len_of = [&](int64_t r) { return r < A.n ? hp[r + 1] - hp[r] : 0; };
-  std::vector<int32_t> h(ns), sp(ns + 1, 0);
+  std::vector<int32_t> h(ns);
   int64_t pad_plain = 0;
   for (int i = 0; i < ns; ++i) {
     int mx = 0;
@@ -168,22 +174,39 @@ static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
   }
   const bool sorted = (double)(pad_plain - pad_sorted) > 0.03 * (double)std::max<int64_t>(A.nnz, 1) &&
                       !env_int("AMG_SELL_NO_SORT", 0);
-  if (sorted) h = hs;
-  for (int i = 0; i < ns; ++i) {
-    if ((int64_t)sp[i] + h[i] > INT32_MAX) fail(AMG_EINDEX_OVERFLOW, "sliced copy: too many steps");
+  out.h = sorted ? hs : h;
+  if (sorted) out.perm = std::move(perm);
+  return out;
+}
+
+static std::vector<int32_t> prefix32(const std::vector<int32_t>& h, const char* what) {
+  std::vector<int32_t> sp(h.size() + 1, 0);
+  for (size_t i = 0; i < h.size(); ++i) {
+    if ((int64_t)sp[i] + h[i] > INT32_MAX) fail(AMG_EINDEX_OVERFLOW, what);
     sp[i + 1] = sp[i] + h[i];
   }
+  return sp;
+}
+
+static int32_t* upload_perm(const Slicing& sl, int C, Arena& arena, cudaStream_t s) {
+  if (sl.perm.empty()) return nullptr;
+  int32_t* d = arena.alloc_n<int32_t>((size_t)sl.ns * C);
+  AMG_CK(cudaMemcpyAsync(d, sl.perm.data(), sizeof(int32_t) * sl.ns * C, cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
+  const int C = 32 / A.b;
+  const Slicing sl = slice_rows(A, C, s);
+  const int ns = sl.ns;
+  const std::vector<int32_t> sp = prefix32(sl.h, "sliced copy: too many steps");
   const int64_t steps = sp[ns];
   A.sell_ns = ns;
   A.sell_ptr = arena.alloc_n<int32_t>(ns + 1);
   A.sell_col = arena.alloc_n<int32_t>(std::max<int64_t>(steps * C, 1));
   A.sell_val = arena.alloc(std::max<int64_t>(steps * C * A.b * A.b, 1) * dtype_size(A.vt));
   AMG_CK(cudaMemcpyAsync(A.sell_ptr, sp.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, s));
-  A.sell_perm = nullptr;
-  if (sorted) {
-    A.sell_perm = arena.alloc_n<int32_t>((size_t)ns * C);
-    AMG_CK(cudaMemcpyAsync(A.sell_perm, perm.data(), sizeof(int32_t) * ns * C, cudaMemcpyHostToDevice, s));
-  }
+  A.sell_perm = upload_perm(sl, C, arena, s);
   dispatch_t(A.vt, [&](auto v) {
     using V = decltype(v);
     k_sell_fill<V><<<grid_for((int64_t)ns * C, 256), 256, 0, s>>>(A.n, A.b, C, ns, A.ptr, A.col, (const V*)A.val,
@@ -194,21 +217,84 @@ static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
   A.lane_var = kLaneSell;
 }
 
+// ---- interleaved row-per-lane copy (k_bsr_sellr) ----
+template <typename V>
+__global__ void k_sellr_fill(int n, int b, int W, int ns, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ col, const V* __restrict__ val,
+                             const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
+                             const int32_t* __restrict__ perm, int32_t* __restrict__ scol, V* __restrict__ sval) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * 32) return;
+  const int s = (int)(t / 32), g = (int)(t % 32);
+  int64_t row = t;
+  if (perm) row = perm[t] >= 0 ? perm[t] : n;
+  const int k0 = row < n ? ptr[row] : 0, len = row < n ? ptr[row + 1] - k0 : 0;
+  const int pad_col = row < n ? (int)row : 0;
+  const int E = b * b;
+  for (int j = 0; j < sptr[s + 1] - sptr[s]; ++j)
+    scol[((int64_t)sptr[s] + j) * 32 + g] = j < len ? col[k0 + j] : (len > 0 ? col[k0] : pad_col);
+  const int64_t nv = vptr[s + 1] - vptr[s];
+  for (int64_t e = 0; e < nv * W; ++e) {
+    const int64_t q = e / W, jb = e / E;
+    sval[(((int64_t)vptr[s] + q) * 32 + g) * W + (e % W)] = jb < len ? val[(k0 + jb) * E + (e % E)] : V(0);
+  }
+}
+
+static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
+  const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 ? 4 : 2);
+  if (!(W == 4 && A.vt == AMG_F32) && W != 2) fail(AMG_EINVAL, "AMG_SELLR_W: 4 (fp32) or 2");
+  const int E = A.b * A.b;
+  const Slicing sl = slice_rows(A, 32, s);
+  const int ns = sl.ns;
+  const std::vector<int32_t> sp = prefix32(sl.h, "interleaved copy: too many steps");
+  std::vector<int32_t> nvec(ns);
+  for (int i = 0; i < ns; ++i) nvec[i] = (int32_t)(((int64_t)E * sl.h[i] + W - 1) / W);
+  const std::vector<int32_t> vp = prefix32(nvec, "interleaved copy: too many vectors");
+  A.sell_ns = ns;
+  A.sell_w = W;
+  A.sell_ptr = arena.alloc_n<int32_t>(ns + 1);
+  A.sell_vptr = arena.alloc_n<int32_t>(ns + 1);
+  A.sell_col = arena.alloc_n<int32_t>(std::max<int64_t>((int64_t)sp[ns] * 32, 1));
+  A.sell_val = arena.alloc(std::max<int64_t>((int64_t)vp[ns] * 32 * W, 1) * dtype_size(A.vt));
+  AMG_CK(cudaMemcpyAsync(A.sell_ptr, sp.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, s));
+  AMG_CK(cudaMemcpyAsync(A.sell_vptr, vp.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, s));
+  A.sell_perm = upload_perm(sl, 32, arena, s);
+  dispatch_t(A.vt, [&](auto v) {
+    using V = decltype(v);
+    k_sellr_fill<V><<<grid_for((int64_t)ns * 32, 256), 256, 0, s>>>(A.n, A.b, W, ns, A.ptr, A.col, (const V*)A.val,
+                                                                     A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col,
+                                                                     (V*)A.sell_val);
+  });
+  AMG_CK_LAUNCH();
+  AMG_CK(cudaStreamSynchronize(s));
+  A.lane_var = kLaneSellR;
+}
+
 void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
   A.tma_grid = 0;
   A.tma_mode = kTmaNone;
   set_lane_plan(A);
   {
-    // long rows and enough slices to fill the GPU: sliced copy (k_bsr_sell)
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
-    const double lo = env_int("AMG_SELL_MIN_ROW", 12), hi = env_int("AMG_SELL_MAX_ROW", 64);
-    // >= 64 slices per SM: below that the per-slice step chains are latency bound and
-    // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
-    const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
-    if (arena && square && per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices &&
-        !env_int("AMG_NO_SELL", 0) && !env_int("AMG_LANE_VAR", 0))
+    const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
+    const int sellr_mode = env_int("AMG_SELLR", 0);  // 0: never (default, measured slower), 1: fp32 hierarchy, 2: every square matrix
+    // sliced copies need the builder's arena and square b x b blocks
+    if (arena && square && forced == kLaneSellR) {
+      build_sellr(A, *arena, s);
+    } else if (arena && square && forced == kLaneSell) {
       build_sell(A, *arena, s);
+    } else if (arena && square && forced < 0) {
+      const double lo = env_int("AMG_SELL_MIN_ROW", 12), hi = env_int("AMG_SELL_MAX_ROW", 64);
+      // >= 64 slices per SM: below that the per-slice step chains are latency bound and
+      // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
+      const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
+      const bool many = (int64_t)A.n / 32 >= min_slices;
+      if (sellr_mode == 2 || (sellr_mode == 1 && many && per_row <= hi && A.vt == AMG_F32 && A.fast32))
+        build_sellr(A, *arena, s);
+      else if (per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices && !env_int("AMG_NO_SELL", 0))
+        build_sell(A, *arena, s);
+    }
   }
   const int br = A.rows_per_block(), bc = A.cols_per_block();
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
@@ -277,6 +363,26 @@ static void dispatch_lane(int var, F&& f) {
   }
 }
 
+template <int B, typename V, typename X, class EPI>
+static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, unsigned grid) {
+  auto go = [&](auto Wc) {
+    constexpr int W = decltype(Wc)::value;
+    constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
+    if (can_fast && fast)
+      k_bsr_sellr<B, W, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_vptr, A.sell_perm,
+                                                                    A.sell_col, (const V*)A.sell_val, x, epi);
+    else
+      k_bsr_sellr<B, W, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_vptr, A.sell_perm,
+                                                                  A.sell_col, (const V*)A.sell_val, x, epi);
+  };
+  if constexpr (std::is_same_v<V, float>) {
+    if (A.sell_w == 4) go(std::integral_constant<int, 4>{});
+    else go(std::integral_constant<int, 2>{});
+  } else {
+    go(std::integral_constant<int, 2>{});
+  }
+}
+
 template <int BR, int BC, typename V, typename X, class EPI>
 static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r0 = 0, int r1 = -1) {
   if (r1 < 0) r1 = A.n;
@@ -285,6 +391,10 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r
     fail(AMG_EINVAL, "row ranges need a row-lane plan");
   constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
   if constexpr (BR == BC && BR >= 2) {
+    if (A.lane_var == kLaneSellR) {
+      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, (unsigned)((A.sell_ns + 7) / 8));
+      return;
+    }
     if (A.lane_var == kLaneSell) {
       constexpr int U = (BR * BR * sizeof(V) <= 36) ? 4 : 2;
       const unsigned grid = grid_for((int64_t)A.sell_ns * 32, kBlock);
@@ -346,7 +456,27 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
 // K3 / K2 fused forms (row-lane plans only; false -> the caller runs the unfused pair)
 template <class EPI>
 static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaStream_t s) {
-  if (A.tma_grid > 0 || A.lane_var > kLaneCN4 || A.n == 0) return false;
+  if (A.tma_grid > 0 || A.n == 0) return false;
+  if (A.lane_var == kLaneSellR) {
+    bool done = false;
+    dispatch_b(A.b, [&](auto Bc) {
+      constexpr int B = decltype(Bc)::value;
+      if constexpr (B >= 2) {
+        done = true;
+        dispatch_t(A.vt, [&](auto v) {
+          using V = decltype(v);
+          dispatch_t(xt, [&](auto xx) {
+            using X = decltype(xx);
+            const unsigned grid = (unsigned)std::min<int64_t>((A.sell_ns + 7) / 8, kMaxPartials);
+            launch_sellr<B, V, X>(A, (const X*)x, epi, s, false, grid);
+          });
+        });
+      }
+    });
+    AMG_CK_LAUNCH();
+    return done;
+  }
+  if (A.lane_var > kLaneCN4) return false;
   bool done = false;
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;

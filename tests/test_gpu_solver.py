@@ -274,6 +274,21 @@ def test_solve_forced_kernel_paths(amg, envvars, wide):
     assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
 
 
+@pytest.mark.parametrize("solver", [1, 2])
+def test_solve_interleaved_copies_everywhere(amg, envvars, solver):
+    # every square-block matrix of the handle (outer operator: fused SpMV+dot and
+    # residual+norm; hierarchy A, P, R) on the interleaved row-per-lane copy
+    envvars(AMG_LANE_VAR=8)
+    n = 20
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=solver)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
+
+
 @pytest.mark.parametrize("solver", [0, 1, 2, 3])
 def test_maxiter_not_converged(amg, solver):
     # maxiter reached: AMG_NOT_CONVERGED, the report filled, x the last iterate -- the same

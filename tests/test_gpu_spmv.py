@@ -243,6 +243,40 @@ def test_spmv_sliced_copy(amg, rng, envvars, b):
         assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (b, vt, xt, yt)
 
 
+@pytest.mark.parametrize("b", [2, 3, 4])
+@pytest.mark.parametrize("w,nosort", [(4, 0), (2, 0), (4, 1)])
+def test_spmv_interleaved_copy(amg, rng, envvars, b, w, nosort):
+    # force the interleaved row-per-lane copy (k_bsr_sellr): empty, short and long rows
+    # in one slice, ragged last slice, tail steps of every length, sorted windows or not
+    envvars(AMG_LANE_VAR=8, AMG_SELLR_W=w, AMG_SELL_NO_SORT=nosort)
+    n = 1003
+    ptr, col, val = _ragged_bsr(rng, n, b)
+    x = rng.uniform(-1, 1, n * b)
+    y0 = rng.standard_normal(n * b)
+    for vt, xt, yt in ((0, 0, 0), (1, 0, 0), (1, 1, 1), (0, 1, 0)):
+        if vt == amg.F64 and w == 4:
+            continue  # fp64 values: 2-wide vectors only
+        y = _run_plan(amg, ptr, col, val, x, vt, xt, yt, 0.75, -1.0, y0)
+        vv = _r32(val) if vt == amg.F32 else val
+        xx = _r32(x) if xt == amg.F32 else x
+        yy = _r32(y0) if yt == amg.F32 else y0
+        ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv), xx, 0.75, -1.0, yy)
+        assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (b, vt, xt, yt)
+
+
+@pytest.mark.parametrize("b", [3, 4])
+def test_spmv_interleaved_matches_row_lanes_bitwise(amg, rng, envvars, b):
+    # same block-row dots in the same block order as the ROWS lane kernel: identical bits
+    n = 777
+    ptr, col, val = _ragged_bsr(rng, n, b)
+    x = rng.uniform(-1, 1, n * b)
+    out = []
+    for var in (2, 8):
+        envvars(AMG_LANE_VAR=var)
+        out.append(_run_plan(amg, ptr, col, val, x, 1, 0, 0))
+    assert np.array_equal(out[0], out[1])
+
+
 # ---- S1: scalar CSR -> BSR on the device (amg_csr_to_bsr) vs the oracle: bit-exact ----
 def _rand_csr(rng, n, m, dens, dup=True):
     ptr = [0]

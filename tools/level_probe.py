@@ -2,7 +2,7 @@
 of a cfg-4/5 Schur hierarchy), fp32 values x fp32 vectors, y = A x and y += A x.
 
   python tools/level_probe.py <n> <level> <which 0=A 1=P 2=R> [reps]
-Prints one line per AMG_LANE_VAR variant (and the default plan): ms, GB/s.
+Prints one line per AMG_LANE_VAR variant (and the default plan; 7 sliced, 8 interleaved w4/w2): ms, GB/s.
 """
 import os
 import statistics
@@ -30,9 +30,13 @@ torch.cuda.empty_cache()
 nr, b = len(p) - 1, v.shape[-1]
 print(f"level {level} which {which}: rows {nr} blocks {len(c)} ({len(c) / nr:.2f}/row) b {b}")
 x = torch.rand(ncol * b, dtype=torch.float32, device="cuda")
-for var in [None, 0, 1, 2, 3, 4, 5, 6]:
+for var in [None, 0, 1, 2, 3, 4, 5, 6, 7, "8w4", "8w2"]:
+    os.environ.pop("AMG_SELLR_W", None)
     if var is None:
         os.environ.pop("AMG_LANE_VAR", None)
+    elif isinstance(var, str):
+        os.environ["AMG_LANE_VAR"] = "8"
+        os.environ["AMG_SELLR_W"] = var[2:]
     else:
         os.environ["AMG_LANE_VAR"] = str(var)
     A = amg.BSR.from_numpy(p, c, v, dtype=torch.float32, n_block_cols=ncol)
