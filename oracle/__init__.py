@@ -22,6 +22,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
 SPAI0, JACOBI = 0, 1
+SA, PLAIN = 0, 1  # coarsening
 OK, NOT_CONVERGED, EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EBREAKDOWN = 0, 1, -1, -2, -3, -4, -6
 
 
@@ -43,7 +44,8 @@ class Params(ctypes.Structure):
         ("eps_strong", ctypes.c_double), ("coarse_enough", ctypes.c_int32), ("max_levels", ctypes.c_int32),
         ("npre", ctypes.c_int32), ("npost", ctypes.c_int32), ("schur_p_component", ctypes.c_int32),
         ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
-        ("schur_u_scalar", ctypes.c_int32),
+        ("schur_u_scalar", ctypes.c_int32), ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32),
+        ("over_interp", ctypes.c_double),
     ]
 
 

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <vector>
 
 using std::vector;
@@ -52,6 +53,9 @@ extern "C" void orc_params_default(orc_params* p) {
   p->idrs_s = 5;
   p->idrs_seed = 1234;
   p->schur_u_scalar = 0;
+  p->coarsening = ORC_SA;
+  p->schur_shat = 1;
+  p->over_interp = 1.5;
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -497,6 +501,26 @@ static int smoothed_prolongator(const orc_mat& A, const vector<vector<int32_t>>&
   return ORC_OK;
 }
 
+// Plain aggregation (Listings V2-V4, "amgcl::coarsening::aggregation"): P = P_tent,
+// one identity block per aggregated row at its aggregate (C4); isolated rows empty.
+static orc_mat tentative_prolongator(const orc_mat& A, const vector<int32_t>& agg, int32_t nc) {
+  const int b = A.b;
+  orc_mat Pt;
+  Pt.n = A.n;
+  Pt.m = nc;
+  Pt.b = b;
+  Pt.ptr.assign(A.n + 1, 0);
+  for (int32_t I = 0; I < A.n; ++I) {
+    if (agg[I] >= 0) {
+      Pt.col.push_back(agg[I]);
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) Pt.val.push_back(r == c ? 1.0 : 0.0);
+    }
+    Pt.ptr[I + 1] = (int32_t)Pt.col.size();
+  }
+  return Pt;
+}
+
 // ---------------------------------------------------------------- C8 smoother
 // SPAI0: M_I = theta_I A_II^-1, theta_I = ||A_II||_F^2 / sum_J ||A_IJ||_F^2
 // (block generalisation of Broker-Grote SPAI(0)).
@@ -617,13 +641,22 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
     vector<int32_t> roots;
     L.nc = aggregate(adj, L.agg, &roots);
     if (L.nc == 0 || L.nc >= A.n) break;
-    rc = smoothed_prolongator(A, adj, L.agg, L.nc, p.sa_omega, L.P);
+    if (p.coarsening == ORC_PLAIN)
+      L.P = tentative_prolongator(A, L.agg, L.nc);
+    else
+      rc = smoothed_prolongator(A, adj, L.agg, L.nc, p.sa_omega, L.P);
     if (rc != ORC_OK) return rc;
     L.R = transpose(L.P);
     rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
     if (rc != ORC_OK) return rc;
     orc_mat AP = spgemm(A, L.P);
     orc_mat Ac = spgemm(L.R, AP);
+    if (p.coarsening == ORC_PLAIN && p.over_interp != 1.0) {
+      // over-interpolation (reading R19): the coarse correction scaled by alpha, i.e.
+      // the Galerkin operator by 1 / alpha
+      const double inv = 1.0 / p.over_interp;
+      for (double& v : Ac.val) v = v * inv;
+    }
     // coarse slab bounds: aggregates are numbered in ascending root order (C3, C12)
     vector<int32_t> nb(bd.size(), 0);
     for (size_t r = 1; r < bd.size(); ++r) {
@@ -709,6 +742,46 @@ static void vcycle(const orc_solver& s, size_t l, const vector<double>& f, vecto
 // pc), C (pc,pc).  Shat = C - diag(B diag(A_u)^-1 B^T) (Eq. 10, PAPER.md:541-543,
 // adjust_p = 1 PAPER.md:622; diag(A_u) the scalar diagonal).  m_S = SPAI0(Shat):
 // m_i = Shat_ii / sum_j Shat_ij^2.
+// schur_shat = 2: the explicitly assembled S_hat = C - B diag(A_u)^-1 B^T (the PETSc
+// variant), row i over the union of C's row and the rows of B^T reached
+// through B's row; every sum_ij accumulated over k (row i's blocks ascending), then d,
+// S_hat_ij = C_ij - sum_ij (C_ij = 0 off C's pattern), m_S,i = S_hat_ii / sum_j S_hat_ij^2
+// (j ascending).  Same bars as Eq. 10 otherwise.
+static int schur_shat_full(orc_solver& s, const orc_mat& A, const vector<double>& Cv) {
+  const int bu = A.b - 1;
+  const orc_mat& Au = s.Au;
+  for (int32_t i = 0; i < A.n; ++i) {
+    std::map<int32_t, double> sum, crow;
+    for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) crow[A.col[k]] = Cv[k];
+    if (crow.find(i) == crow.end()) return ORC_EZERODIAG;
+    for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      const int32_t K = A.col[k];
+      const int64_t kKK = find_block(A, K, K);
+      if (kKK < 0) return ORC_EZERODIAG;
+      for (int d = 0; d < bu; ++d) {
+        const double diag = Au.val[kKK * bu * bu + d * bu + d];
+        if (diag == 0.0) return ORC_EZERODIAG;
+        const double t = s.Bv[k * bu + d] * (1.0 / diag);
+        for (int32_t kk = A.ptr[K]; kk < A.ptr[K + 1]; ++kk) {
+          double& acc = sum[A.col[kk]];  // value-initialised 0.0 on first use
+          acc = acc + t * s.BTv[kk * bu + d];
+        }
+      }
+    }
+    double den = 0.0, sii = 0.0;
+    for (const auto& e : sum) {  // pattern(B B^T) contains C's (diagonal blocks present)
+      const auto c = crow.find(e.first);
+      const double v = (c == crow.end() ? 0.0 : c->second) - e.second;
+      if (e.first == i) sii = v;
+      den = den + v * v;
+    }
+    if (den == 0.0) return ORC_EZERODIAG;
+    s.Shat_diag[i] = sii;
+    s.mS[i] = sii / den;
+  }
+  return ORC_OK;
+}
+
 static int schur_setup(orc_solver& s) {
   const orc_mat& A = s.A;
   const int b = A.b, pc = s.p.schur_p_component;
@@ -739,10 +812,15 @@ static int schur_setup(orc_solver& s) {
   }
   s.Shat_diag.assign(A.n, 0.0);
   s.mS.assign(A.n, 0.0);
-  for (int32_t i = 0; i < A.n; ++i) {
+  if (s.p.schur_shat == 2) {
+    int rc = schur_shat_full(s, A, Cv);
+    if (rc != ORC_OK) return rc;
+  }
+  for (int32_t i = 0; i < A.n && s.p.schur_shat != 2; ++i) {
     int64_t kd = find_block(A, i, i);
     if (kd < 0) return ORC_EZERODIAG;
     double sum = 0.0;
+    if (s.p.schur_shat == 1)
     for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
       int32_t J = A.col[k];
       int64_t kJJ = find_block(A, J, J), kJi = find_block(A, J, i);

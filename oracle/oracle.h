@@ -23,6 +23,7 @@ extern "C" {
 enum { ORC_CG = 0, ORC_BICGSTAB = 1, ORC_GMRES = 2, ORC_IDRS = 3 };
 enum { ORC_PC_AMG = 0, ORC_PC_SCHUR = 1, ORC_PC_NONE = 2 };
 enum { ORC_SPAI0 = 0, ORC_JACOBI = 1 };
+enum { ORC_SA = 0, ORC_PLAIN = 1 };
 
 enum {
   ORC_OK = 0, ORC_NOT_CONVERGED = 1, ORC_EINVAL = -1, ORC_EDIM = -2, ORC_EZERODIAG = -3,
@@ -46,6 +47,12 @@ typedef struct {
   int32_t idrs_seed;     /* IDR(s) shadow-space seed (1234) */
   int32_t schur_u_scalar; /* 1: the U-solver hierarchy is built on the SCALAR expansion of A_u
                              (AMGCL V2, Listing V2); 0: on 3x3 blocks (V3/V4, Listing V3) */
+  int32_t coarsening;    /* ORC_SA: smoothed aggregation; ORC_PLAIN: plain
+                            aggregation, P = P_tent (Listings V2-V4 "coarsening::aggregation") */
+  int32_t schur_shat;    /* P-solver matrix: 0 = C; 1 = Eq. 10 C - diag(B diag(A_u)^-1 B^T)
+                            (adjust_p = 1); 2 = the explicitly
+                            assembled C - B diag(A_u)^-1 B^T (the PETSc variant) */
+  double over_interp;    /* plain aggregation: A_c = (1/over_interp) P^T A P (reading R19, 1.5) */
 } orc_params;
 
 typedef struct {

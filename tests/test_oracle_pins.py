@@ -299,6 +299,40 @@ def test_galerkin_dense_triple_product(rng):
     assert np.linalg.norm(P.T @ Ad @ P - Ac) <= 1e-12 * np.linalg.norm(Ac)
 
 
+@pytest.mark.parametrize("alpha", [1.0, 1.5])
+def test_plain_aggregation_is_tentative_with_scaled_galerkin(rng, alpha):
+    # plain aggregation (Listings V2-V4 "coarsening::aggregation"): P = P_tent exactly (one
+    # identity block per aggregated row, at its aggregate), A_c = (1/alpha) P^T A P
+    # (over-interpolation, reading R19) -- numpy dense triple product, every level
+    ptr, col, val = random_bsr(rng, 300, 3, density=0.02, symmetric_pattern=True, dom=6)
+    A, S = _solver(ptr, col, val, coarse_enough=60, coarsening=oracle.PLAIN, over_interp=alpha,
+                   hier_f32=0, vec_f32=0)
+    assert S.levels >= 2
+    for l in range(S.levels - 1):
+        Al, P, Ac = S.level_mat(l, 0).dense(), S.level_mat(l, 1).dense(), S.level_mat(l + 1, 0).dense()
+        agg = S.level_agg(l)
+        Pt = np.zeros_like(P)
+        for i, a in enumerate(agg):
+            if a >= 0:
+                Pt[3 * i:3 * i + 3, 3 * a:3 * a + 3] = np.eye(3)
+        assert np.array_equal(P, Pt)
+        assert np.array_equal(S.level_mat(l, 2).dense(), P.T)
+        assert np.linalg.norm(P.T @ Al @ P / alpha - Ac) <= 1e-13 * np.linalg.norm(Ac)
+
+
+def test_plain_aggregation_solves_to_dense_solution(rng):
+    for kind, pc, solver in ((gen.POISSON3, oracle.PC_AMG, oracle.CG), (gen.STOKES, oracle.PC_SCHUR, oracle.GMRES)):
+        ptr, col, val = gen.matrix(kind, 8)
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        S = oracle.Solver(A, precond=pc, solver=solver, coarsening=oracle.PLAIN, coarse_enough=60,
+                          hier_f32=0, vec_f32=0)
+        assert S.levels >= 2
+        b = rng.standard_normal(len(ptr) * 0 + (len(ptr) - 1) * val.shape[-1])
+        r = S.solve(b, rtol=1e-10)
+        xd = np.linalg.solve(A.dense(), b)
+        assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
 def test_level_sizes_strictly_decrease():
     ptr, col, val = gen.matrix(gen.STOKES, 12)
     A, S = _solver(ptr, col, val, coarse_enough=50)
@@ -414,6 +448,34 @@ def test_schur_eq10_hand_value():
     d, m = S.schur_vectors()
     assert d[0] == g["Shat"]
     assert m[0] == 1.0 / g["Shat"]  # SPAI0 of a 1x1 matrix is its inverse
+
+
+def _stokes_split(n):
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    Ad = A.dense()
+    vel = np.array([q for q in range(4 * n ** 3) if q % 4 != 3])
+    pre = np.array([q for q in range(4 * n ** 3) if q % 4 == 3])
+    return A, Ad[np.ix_(vel, vel)], Ad[np.ix_(vel, pre)], Ad[np.ix_(pre, vel)], Ad[np.ix_(pre, pre)]
+
+
+def test_schur_shat_variants_dense():
+    # schur_shat = 0: S_hat = C; 1: Eq. 10 C - diag(B diag(A_u)^-1 B^T); 2: the explicitly
+    # assembled C - B diag(A_u)^-1 B^T (PETSc variant).  m_S = SPAI0:
+    # m_i = S_ii / sum_j S_ij^2 -- all three from numpy dense products
+    n = 4
+    A, Au, Bt, B, C = _stokes_split(n)
+    X = B @ np.diag(1.0 / np.diag(Au)) @ Bt
+    want = {0: C, 1: C - np.diag(np.diag(X)), 2: C - X}
+    diags = {}
+    for mode, Sh in want.items():
+        S = oracle.Solver(A, precond=oracle.PC_SCHUR, schur_shat=mode, hier_f32=0, vec_f32=0)
+        d, m = S.schur_vectors()
+        assert np.allclose(d, np.diag(Sh), rtol=1e-14, atol=0), mode
+        assert np.allclose(m, np.diag(Sh) / (Sh ** 2).sum(axis=1), rtol=1e-13, atol=0), mode
+        diags[mode] = d
+    assert np.array_equal(diags[1], diags[2])  # same diagonal terms, same order
+    assert not np.allclose(want[2], np.diag(np.diag(want[2])))  # the full S_hat has off-diagonal fill
 
 
 def test_schur_shat_interior_closed_form():
