@@ -44,6 +44,9 @@ typedef enum { AMG_F64 = 0, AMG_F32 = 1 } amg_dtype;
 enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2, AMG_IDRS = 3 };
 enum { AMG_PC_AMG = 0, AMG_PC_SCHUR = 1, AMG_PC_NONE = 2 };
 enum { AMG_SPAI0 = 0, AMG_JACOBI = 1 };
+/* coarsening: smoothed aggregation | plain aggregation, P = P_tent
+   (Listings V2-V4, "amgcl::coarsening::aggregation") */
+enum { AMG_SA = 0, AMG_PLAIN_AGG = 1 };
 
 /* Block-CSR descriptor (PAPER.md:666-672 layout).  Caller-owned; the library never
  * frees or retains it beyond the call (amg_setup deep-copies). */
@@ -86,6 +89,13 @@ typedef struct {
   int32_t schur_u_scalar;    /* 1: the Schur U-solver hierarchy is built on the SCALAR expansion of
                                 A_u (the paper's V2, Listing V2; R18); 0 (default): on
                                 3x3 blocks (V3, Listing V3; fp32 values = V4, Listing V4) */
+  int32_t coarsening;        /* AMG_SA (default) | AMG_PLAIN_AGG */
+  int32_t schur_shat;        /* matrix of the Schur P-solver's SPAI0: 0 = C; 1 (default) = Eq. 10
+                                C - diag(B diag(A_u)^-1 B^T) (adjust_p = 1);
+                                2 = the explicitly assembled C - B diag(A_u)^-1 B^T (the PETSc
+                                variant) */
+  double over_interp;        /* AMG_PLAIN_AGG: A_c = (1/over_interp) P^T A P, default 1.5
+                                (over-interpolation, reading R19); ignored for AMG_SA */
 } amg_params;
 
 typedef struct {

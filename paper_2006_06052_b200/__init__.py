@@ -24,6 +24,7 @@ F64, F32 = 0, 1
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
 SPAI0, JACOBI = 0, 1
+SA, PLAIN_AGG = 0, 1  # coarsening
 
 
 class AmgError(RuntimeError):
@@ -47,7 +48,8 @@ class amg_params(ctypes.Structure):
                 ("sa_omega", ctypes.c_double), ("eps_strong", ctypes.c_double),
                 ("max_levels", ctypes.c_int32), ("npre", ctypes.c_int32), ("npost", ctypes.c_int32),
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32)]
+                ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32),
+                ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32), ("over_interp", ctypes.c_double)]
 
 
 class amg_report(ctypes.Structure):

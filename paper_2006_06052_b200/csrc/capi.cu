@@ -85,6 +85,9 @@ int amg_params_default(amg_params* p) {
   p->idrs_s = 5;
   p->idrs_seed = 1234;
   p->schur_u_scalar = 0;
+  p->coarsening = AMG_SA;
+  p->schur_shat = 1;
+  p->over_interp = 1.5;
   return AMG_OK;
 }
 

@@ -355,6 +355,26 @@ __global__ void k_p_fill(int n, const int32_t* ptr, const int32_t* col, const do
   }
 }
 
+// plain aggregation (Listings V2-V4): P = P_tent, one identity block per aggregated row
+__global__ void k_ptent_count(int n, const int32_t* agg, int32_t* cnt) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I < n) cnt[I] = agg[I] >= 0 ? 1 : 0;
+}
+template <int B>
+__global__ void k_ptent_fill(int n, const int32_t* agg, const int32_t* pptr, int32_t* pcol, double* pval) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= n || agg[I] < 0) return;
+  const int i = pptr[I];
+  pcol[i] = agg[I];
+  for (int r = 0; r < B; ++r)
+    for (int c = 0; c < B; ++c) pval[(int64_t)i * B * B + r * B + c] = (r == c) ? 1.0 : 0.0;
+}
+// over-interpolation (reading R19): A_c values times 1 / alpha
+__global__ void k_scale_vals(int64_t m, double inv, double* v) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < m) v[e] = v[e] * inv;
+}
+
 // ---------------------------------------------------------------- S7 transpose
 __global__ void k_count_cols(int64_t nnz, const int32_t* col, int32_t* cnt) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -489,15 +509,16 @@ __global__ void k_schur_split(int64_t nnz, int b, int pc, const double* val, dou
   cv[k] = a[pc * b + pc];
 }
 
-// Shat_ii = C_ii - sum_J sum_d B_iJ[d] (1/A_u,JJ[d][d]) B^T_Ji[d]  (Eq. 10)
-// m_S,i = Shat_ii / sum_j Shat_ij^2 (SPAI0 of Shat)
-__global__ void k_schur_shat(int n, int nu, const int32_t* ptr, const int32_t* col, const int32_t* diag,
+// Shat_ii = C_ii - sum_J sum_d B_iJ[d] (1/A_u,JJ[d][d]) B^T_Ji[d]  (Eq. 10, PAPER.md:541-543;
+// mode 1) or C_ii (mode 0: S_hat = C); m_S,i = Shat_ii / sum_j Shat_ij^2 over C's pattern
+// (SPAI0 of Shat)
+__global__ void k_schur_shat(int n, int nu, int mode, const int32_t* ptr, const int32_t* col, const int32_t* diag,
                              const double* au, const double* bv, const double* btv, const double* cv, double* shat,
                              double* ms, int* err) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double sum = 0.0;
-  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+  for (int k = ptr[i]; k < ptr[i + 1] && mode == 1; ++k) {
     int J = col[k];
     int kJJ = diag[J];
     int kJi = bsearch(col, ptr[J], ptr[J + 1], i);
@@ -525,6 +546,51 @@ __global__ void k_schur_shat(int n, int nu, const int32_t* ptr, const int32_t* c
   }
   shat[i] = s;
   ms[i] = s / den;
+}
+
+// mode 2, the explicitly assembled S_hat = C - B diag(A_u)^-1 B^T (the PETSc variant,
+// PAPER.md:558-561) on pattern(A A) (spgemm symbolic, sorted rows): sum_ij accumulated
+// over k (row i's blocks ascending), then d; S_hat_ij = C_ij - sum_ij (C_ij = 0 off C's
+// pattern); m_S,i = S_hat_ii / sum_j S_hat_ij^2 (j ascending).  Thread per pressure row.
+__global__ void k_schur_shat_full(int n, int nu, const int32_t* ptr, const int32_t* col, const int32_t* diag,
+                                  const double* au, const double* bv, const double* btv, const double* cv,
+                                  const int32_t* sptr, const int32_t* scol, double* ssum, double* shat, double* ms,
+                                  int* err) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c0 = sptr[i], c1 = sptr[i + 1];
+  for (int q = c0; q < c1; ++q) ssum[q] = 0.0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int K = col[k], kKK = diag[K];
+    for (int d = 0; d < nu; ++d) {
+      const double dg = au[(int64_t)kKK * nu * nu + d * nu + d];
+      if (dg == 0.0) {
+        set_err(err, AMG_EZERODIAG);
+        return;
+      }
+      const double t = bv[(int64_t)k * nu + d] * (1.0 / dg);
+      for (int kk = ptr[K]; kk < ptr[K + 1]; ++kk) {
+        const int q = bsearch(scol, c0, c1, col[kk]);
+        ssum[q] = ssum[q] + t * btv[(int64_t)kk * nu + d];
+      }
+    }
+  }
+  double den = 0.0, sii = 0.0;
+  int k = ptr[i];
+  for (int q = c0; q < c1; ++q) {
+    const int j = scol[q];
+    while (k < ptr[i + 1] && col[k] < j) ++k;
+    const double c = (k < ptr[i + 1] && col[k] == j) ? cv[k] : 0.0;
+    const double v = c - ssum[q];
+    if (j == i) sii = v;
+    den = den + v * v;
+  }
+  if (den == 0.0) {
+    set_err(err, AMG_EZERODIAG);
+    return;
+  }
+  shat[i] = sii;
+  ms[i] = sii / den;
 }
 
 // ---------------------------------------------------------------- S11 coarse inverse
@@ -782,9 +848,23 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     AMG_CK_LAUNCH();
     h.shat64 = h.arena.alloc_n<double>(std::max(A64.n, 1));
     h.mS64 = h.arena.alloc_n<double>(std::max(A64.n, 1));
-    if (A64.n > 0)
-      k_schur_shat<<<grid_for(A64.n, kT), kT, 0, s>>>(A64.n, nu, A64.ptr, A64.col, diag0, (const double*)Au.val, bv,
-                                                      btv, cv, h.shat64, h.mS64, c.err);
+    if (A64.n > 0 && p.schur_shat == 2) {
+      int32_t* heads = c.tmp.alloc_n<int32_t>(std::max<int64_t>(A64.nnz, 1));
+      int32_t* sptr = c.tmp.alloc_n<int32_t>(A64.n + 1);
+      k_spgemm_sym<<<grid_for(A64.n, kT), kT, 0, s>>>(A64.n, A64.ptr, A64.col, A64.ptr, A64.col, heads, nullptr,
+                                                       nullptr, sptr);
+      AMG_CK_LAUNCH();
+      const int64_t snnz = scan(c, sptr, A64.n);
+      int32_t* scol = c.tmp.alloc_n<int32_t>(std::max<int64_t>(snnz, 1));
+      double* ssum = c.tmp.alloc_n<double>(std::max<int64_t>(snnz, 1));
+      k_spgemm_sym<<<grid_for(A64.n, kT), kT, 0, s>>>(A64.n, A64.ptr, A64.col, A64.ptr, A64.col, heads, sptr, scol,
+                                                       nullptr);
+      k_schur_shat_full<<<grid_for(A64.n, kT), kT, 0, s>>>(A64.n, nu, A64.ptr, A64.col, diag0, (const double*)Au.val,
+                                                            bv, btv, cv, sptr, scol, ssum, h.shat64, h.mS64, c.err);
+    } else if (A64.n > 0) {
+      k_schur_shat<<<grid_for(A64.n, kT), kT, 0, s>>>(A64.n, nu, p.schur_shat, A64.ptr, A64.col, diag0,
+                                                      (const double*)Au.val, bv, btv, cv, h.shat64, h.mS64, c.err);
+    }
     AMG_CK_LAUNCH();
     check_err(c, "Schur complement approximation");
     h.Bv = h.arena.alloc(std::max<int64_t>(A64.nnz, 1) * nu * dtype_size(h.vt));
@@ -920,10 +1000,12 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     k_pass2<<<grid_for(n, kT), kT, 0, s>>>(n, aptr, adj, agg1, agg);
     AMG_CK_LAUNCH();
 
-    // smoothed prolongator
+    // smoothed prolongator (plain aggregation: the tentative one)
+    const bool plain = p.coarsening == AMG_PLAIN_AGG;
     int32_t* cand = c.tmp.alloc_n<int32_t>(std::max<int64_t>(nnz, 1));
     int32_t* pcnt = c.tmp.alloc_n<int32_t>(n + 1);
-    k_p_cand<<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, diag, sym, agg, cand, pcnt);
+    if (plain) k_ptent_count<<<grid_for(n, kT), kT, 0, s>>>(n, agg, pcnt);
+    else k_p_cand<<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, diag, sym, agg, cand, pcnt);
     AMG_CK_LAUNCH();
     const int64_t pnnz = scan(c, pcnt, n);
     Mat P;
@@ -933,11 +1015,15 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     P.val = c.tmp.alloc_n<double>(std::max<int64_t>(pnnz, 1) * A.b * A.b);
     dispatch_bs(A.b, [&](auto Bc) {
       constexpr int BB = decltype(Bc)::value;
-      k_filtered_diag<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, (const double*)A.val, diag, sym, D, Dinv,
-                                                         c.err);
-      AMG_CK_LAUNCH();
-      k_p_fill<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, (const double*)A.val, diag, sym, agg, D, Dinv,
-                                                  cand, P.ptr, P.col, (double*)P.val, p.sa_omega);
+      if (plain) {
+        k_ptent_fill<BB><<<grid_for(n, kT), kT, 0, s>>>(n, agg, P.ptr, P.col, (double*)P.val);
+      } else {
+        k_filtered_diag<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, (const double*)A.val, diag, sym, D,
+                                                           Dinv, c.err);
+        AMG_CK_LAUNCH();
+        k_p_fill<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, (const double*)A.val, diag, sym, agg, D, Dinv,
+                                                    cand, P.ptr, P.col, (double*)P.val, p.sa_omega);
+      }
       AMG_CK_LAUNCH();
       k_smoother<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, (const double*)A.val, diag, p.smoother == AMG_SPAI0,
                                                     p.jacobi_omega, M, c.err);
@@ -948,6 +1034,11 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     Mat AP = spgemm(c, A, P);
     Mat Ac = spgemm(c, R, AP);
     Ac.m = Ac.n;
+    if (plain && p.over_interp != 1.0 && Ac.nnz > 0) {
+      const int64_t m = Ac.nnz * Ac.b * Ac.b;
+      k_scale_vals<<<grid_for(m, kT), kT, 0, s>>>(m, 1.0 / p.over_interp, (double*)Ac.val);
+      AMG_CK_LAUNCH();
+    }
     lvA.push_back(A);
     lvP.push_back(P);
     lvR.push_back(R);

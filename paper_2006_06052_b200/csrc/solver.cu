@@ -95,6 +95,8 @@ int check_params(const amg_params* p) {
   if (p->precond < AMG_PC_AMG || p->precond > AMG_PC_NONE) return AMG_EINVAL;
   if (p->solver == AMG_GMRES && (p->gmres_m < 1 || p->gmres_m > 31)) return AMG_EINVAL;
   if (p->npre < 1 || p->npost < 0 || p->max_levels < 1 || p->maxiter < 0) return AMG_EINVAL;
+  if (p->coarsening != AMG_SA && p->coarsening != AMG_PLAIN_AGG) return AMG_EINVAL;
+  if (p->schur_shat < 0 || p->schur_shat > 2 || !(p->over_interp > 0.0)) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;

@@ -27,7 +27,8 @@ ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxit
           "smoother": "smoother", "sa_omega": "sa_omega", "eps_strong": "eps_strong",
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
           "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed",
-          "schur_u_scalar": "schur_u_scalar"}
+          "schur_u_scalar": "schur_u_scalar", "coarsening": "coarsening", "schur_shat": "schur_shat",
+          "over_interp": "over_interp"}
 
 
 def make_pair(amg, ptr, col, val, hier32=True, **kw):
@@ -82,6 +83,14 @@ CASES = [
     # V2 of the paper's ladder: the U-solver hierarchy on the scalar expansion of A_u
     ("stokes-v2-scalar-f64", gen.STOKES, 10, dict(precond=1, solver=3, schur_u_scalar=1, coarse_enough=40), False),
     ("stokes-v2-scalar-16", gen.STOKES, 16, dict(precond=1, solver=3, schur_u_scalar=1), True),
+    # plain aggregation (Listings V2-V4) and the S_hat variants
+    ("plain-agg-poisson", gen.POISSON3, 10, dict(precond=0, solver=0, coarsening=1, coarse_enough=40), False),
+    ("plain-agg-stokes-16", gen.STOKES, 16, dict(precond=1, solver=3, coarsening=1), True),
+    ("plain-agg-alpha1-f64", gen.STOKES, 10, dict(precond=1, solver=2, coarsening=1, over_interp=1.0,
+                                                  coarse_enough=40), False),
+    ("shat-C-f64", gen.STOKES, 10, dict(precond=1, solver=2, schur_shat=0, coarse_enough=40), False),
+    ("shat-full-f64", gen.STOKES, 12, dict(precond=1, solver=2, schur_shat=2, coarse_enough=40), False),
+    ("shat-full-plain-16", gen.STOKES, 16, dict(precond=1, solver=3, schur_shat=2, coarsening=1), True),
 ]
 
 
@@ -148,6 +157,12 @@ SOLVE_CASES = [
     # the paper's ladder: V2 (scalar fp64 U-solver), V3 (3x3 fp64), V4 (3x3 fp32), IDR(5) outer
     ("ladder-v2", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3, schur_u_scalar=1), False),
     ("ladder-v3", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3), False),
+    # plain aggregation + the S_hat variants
+    ("plain-agg-idrs5-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3, coarsening=1), True),
+    ("plain-agg-cg-poisson", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(precond=0, solver=0, coarsening=1), False),
+    ("plain-agg-bicgstab-cfg3", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, coarsening=1), True),
+    ("shat-full-gmres-cfg5-16", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(precond=1, solver=2, schur_shat=2), True),
+    ("shat-C-gmres-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, schur_shat=0), False),
 ]
 
 
@@ -237,9 +252,10 @@ def test_error_codes(amg):
         amg.Solver(amg.BSR.from_numpy(ptr, col, v), coarse_enough=30)
     assert e.value.status == amg.ESINGULAR_BLOCK
     # bad params
-    with pytest.raises(amg.AmgError) as e:
-        amg.Solver(amg.BSR.from_numpy(ptr, col, val), gmres_m=40)
-    assert e.value.status == amg.EINVAL
+    for bad in (dict(gmres_m=40), dict(coarsening=2), dict(schur_shat=3), dict(over_interp=0.0)):
+        with pytest.raises(amg.AmgError) as e:
+            amg.Solver(amg.BSR.from_numpy(ptr, col, val), **bad)
+        assert e.value.status == amg.EINVAL, bad
 
 
 def test_fp32_vs_fp64_iteration_parity(amg):
