@@ -21,7 +21,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
-SPAI0, JACOBI = 0, 1
+SPAI0, JACOBI, ILU0 = 0, 1, 2
 SA, PLAIN = 0, 1  # coarsening
 OK, NOT_CONVERGED, EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EBREAKDOWN = 0, 1, -1, -2, -3, -4, -6
 
@@ -45,7 +45,7 @@ class Params(ctypes.Structure):
         ("npre", ctypes.c_int32), ("npost", ctypes.c_int32), ("schur_p_component", ctypes.c_int32),
         ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
         ("schur_u_scalar", ctypes.c_int32), ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32),
-        ("over_interp", ctypes.c_double),
+        ("over_interp", ctypes.c_double), ("ilu_sweeps", ctypes.c_int32), ("_pad", ctypes.c_int32),
     ]
 
 
@@ -82,6 +82,7 @@ def lib():
             "orc_level_mat": (P, [P, i32, i32]),
             "orc_level_agg": (P, [P, i32]),
             "orc_level_M": (P, [P, i32]),
+            "orc_level_smooth": (i32, [P, i32, P, P]),
             "orc_schur_Au": (P, [P]),
             "orc_schur_Au_amg": (P, [P]),
             "orc_schur_Shat_diag": (P, [P]),
@@ -267,6 +268,13 @@ class Solver:
         n, _, b, _ = A.info()
         p = lib().orc_level_M(self.h, level)
         return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(n, b, b)).copy()
+
+    def level_smooth(self, level: int, f) -> np.ndarray:
+        """x = S_l(f), the level's pre-smoother from zero (M f, or the sweep-solved ILU(0))."""
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        x = np.zeros_like(f)
+        assert lib().orc_level_smooth(self.h, level, _p(f), _p(x)) == 0
+        return x
 
     def schur_Au(self) -> Mat | None:
         h = lib().orc_schur_Au(self.h)

@@ -56,6 +56,8 @@ extern "C" void orc_params_default(orc_params* p) {
   p->coarsening = ORC_SA;
   p->schur_shat = 1;
   p->over_interp = 1.5;
+  p->ilu_sweeps = 2;
+  p->_pad = 0;
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -521,6 +523,59 @@ static orc_mat tentative_prolongator(const orc_mat& A, const vector<int32_t>& ag
   return Pt;
 }
 
+// ---------------------------------------------------------------- C8b ILU(0)
+// Block ILU(0) on A's pattern (no fill; SURVEY.md §8(f) #3 -- the paper's U-solver
+// smoother is ILU-type; Saad, Iterative Methods, Alg. 10.4 "IKJ"):
+// for each row i ascending, for each k < i in row i ascending:
+//   a_ik <- a_ik D_k^-1;  a_ij <- a_ij - a_ik a_kj for every later j of row i with (k,j) in A.
+// Then D_i^-1 = inverse(a_ii) (error if singular).  L = I + strictly lower a_ik,
+// U = D + strictly upper a_ij.  Reading R20.
+static int ilu0_factor(const orc_mat& A, orc_mat& Lo, orc_mat& Up, vector<double>& Dinv) {
+  const int b = A.b, bb = b * b;
+  vector<double> a = A.val;
+  Dinv.assign((size_t)A.n * bb, 0.0);
+  vector<double> tmp(bb);
+  for (int32_t i = 0; i < A.n; ++i) {
+    int64_t kd = -1;
+    for (int32_t kk = A.ptr[i]; kk < A.ptr[i + 1]; ++kk) {
+      const int32_t k = A.col[kk];
+      if (k == i) kd = kk;
+      if (k >= i) continue;
+      blk_mul(b, &a[(size_t)kk * bb], &Dinv[(size_t)k * bb], tmp.data());
+      std::copy(tmp.begin(), tmp.end(), a.begin() + (size_t)kk * bb);
+      for (int32_t jj = kk + 1; jj < A.ptr[i + 1]; ++jj) {
+        const int64_t kj = find_block(A, k, A.col[jj]);
+        if (kj < 0) continue;
+        blk_mul(b, &a[(size_t)kk * bb], &a[(size_t)kj * bb], tmp.data());
+        for (int e = 0; e < bb; ++e) a[(size_t)jj * bb + e] = a[(size_t)jj * bb + e] - tmp[e];
+      }
+    }
+    if (kd < 0) return ORC_EZERODIAG;
+    int rc = block_inverse(b, &a[(size_t)kd * bb], &Dinv[(size_t)i * bb]);
+    if (rc != ORC_OK) return rc;
+  }
+  for (orc_mat* F : {&Lo, &Up}) {
+    F->n = A.n;
+    F->m = A.m;
+    F->b = b;
+    F->ptr.assign(A.n + 1, 0);
+    F->col.clear();
+    F->val.clear();
+  }
+  for (int32_t i = 0; i < A.n; ++i) {
+    for (int32_t kk = A.ptr[i]; kk < A.ptr[i + 1]; ++kk) {
+      const int32_t j = A.col[kk];
+      if (j == i) continue;
+      orc_mat& F = j < i ? Lo : Up;
+      F.col.push_back(j);
+      F.val.insert(F.val.end(), a.begin() + (size_t)kk * bb, a.begin() + (size_t)(kk + 1) * bb);
+    }
+    Lo.ptr[i + 1] = (int32_t)Lo.col.size();
+    Up.ptr[i + 1] = (int32_t)Up.col.size();
+  }
+  return ORC_OK;
+}
+
 // ---------------------------------------------------------------- C8 smoother
 // SPAI0: M_I = theta_I A_II^-1, theta_I = ||A_II||_F^2 / sum_J ||A_IJ||_F^2
 // (block generalisation of Broker-Grote SPAI(0)).
@@ -550,8 +605,9 @@ struct Level {
   orc_mat A, P, R;          // fp64 setup values
   vector<int32_t> agg;
   int32_t nc = 0;
-  vector<double> M;         // fp64 setup values
-  orc_mat As, Ps, Rs;       // solve copies (narrowed when hier_f32)
+  vector<double> M;         // fp64 setup values (ILU(0): the inverted pivot blocks D^-1)
+  orc_mat L, U;             // ILU(0): strictly lower / strictly upper factor blocks
+  orc_mat As, Ps, Rs, Ls, Us;  // solve copies (narrowed when hier_f32)
   vector<double> Ms;
 };
 
@@ -647,7 +703,10 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
       rc = smoothed_prolongator(A, adj, L.agg, L.nc, p.sa_omega, L.P);
     if (rc != ORC_OK) return rc;
     L.R = transpose(L.P);
-    rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
+    if (p.smoother == ORC_ILU0)
+      rc = ilu0_factor(A, L.L, L.U, L.M);
+    else
+      rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
     if (rc != ORC_OK) return rc;
     orc_mat AP = spgemm(A, L.P);
     orc_mat Ac = spgemm(L.R, AP);
@@ -677,6 +736,8 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
     L.As = p.hier_f32 ? narrowed(L.A) : L.A;
     L.Ps = p.hier_f32 ? narrowed(L.P) : L.P;
     L.Rs = p.hier_f32 ? narrowed(L.R) : L.R;
+    L.Ls = p.hier_f32 ? narrowed(L.L) : L.L;
+    L.Us = p.hier_f32 ? narrowed(L.U) : L.U;
     L.Ms = L.M;
     if (p.hier_f32)
       for (double& v : L.Ms) v = f32r(v);
@@ -714,6 +775,50 @@ static void smooth_step(const orc_mat& A, const vector<double>& M, const double*
   x.swap(xn);
 }
 
+// ILU(0) smoothing (R20): z = (LU)^-1 g with k = ilu_sweeps Jacobi sweeps per triangular
+// solve (Anzt, Chow & Dongarra 2015): y_0 = g, y_m = g - L_s y_(m-1) (m = 1..k);
+// z_0 = D^-1 y_k, z_m = D^-1 (y_k - U_s z_(m-1)) (m = 1..k); every sweep one stored vector.
+// The last U sweep adds z_k into x (x0 == nullptr: from zero).  Exact once k reaches the
+// depth of the factors' dependency graph.
+static void ilu_into(const Level& L, int k, const double* g, const double* x0, double* xo, bool rf) {
+  const int b = L.As.b, bb = b * b;
+  const int32_t n = L.As.n;
+  const size_t N = (size_t)n * b;
+  vector<double> y(g, g + N), yn(N), z(N), zn(N), uz(N);
+  for (int m = 1; m <= k; ++m) {
+    residual(L.Ls, g, y.data(), yn.data(), rf);
+    y.swap(yn);
+  }
+  apply_M(L.Ms, b, n, y.data(), z.data(), rf);
+  for (int m = 1; m <= k; ++m) {
+    residual(L.Us, y.data(), z.data(), uz.data(), false);  // y - U_s z, fp64 (fused in the sweep)
+    const bool last = m == k;
+    for (int32_t I = 0; I < n; ++I)
+      for (int r = 0; r < b; ++r) {
+        double t = 0.0;
+        for (int c = 0; c < b; ++c) t = t + L.Ms[(size_t)I * bb + r * b + c] * uz[(size_t)I * b + c];
+        const double v = (last && x0) ? x0[(size_t)I * b + r] + t : t;
+        (last ? xo : zn.data())[(size_t)I * b + r] = rf ? f32r(v) : v;
+      }
+    if (!last) z.swap(zn);
+  }
+}
+
+// x = S(f) from zero (K4a) and x <- x + S(f - A x) (K5) for the level's smoother
+static void pre_smooth(const orc_solver& s, const Level& L, const double* f, double* x, bool rf) {
+  if (s.p.smoother == ORC_ILU0) ilu_into(L, s.p.ilu_sweeps, f, nullptr, x, rf);
+  else apply_M(L.Ms, L.As.b, L.As.n, f, x, rf);
+}
+static void post_smooth(const orc_solver& s, const Level& L, const double* f, vector<double>& x, bool rf) {
+  if (s.p.smoother != ORC_ILU0) {
+    smooth_step(L.As, L.Ms, f, x, rf);
+    return;
+  }
+  vector<double> r(x.size());
+  residual(L.As, f, x.data(), r.data(), rf);
+  ilu_into(L, s.p.ilu_sweeps, r.data(), x.data(), x.data(), rf);
+}
+
 static void vcycle(const orc_solver& s, size_t l, const vector<double>& f, vector<double>& x) {
   const bool rf = s.p.vec_f32 != 0;
   if (l == s.lv.size()) {
@@ -725,15 +830,15 @@ static void vcycle(const orc_solver& s, size_t l, const vector<double>& f, vecto
   const int b = L.As.b;
   const int32_t n = L.As.n;
   x.assign((size_t)n * b, 0.0);
-  apply_M(L.Ms, b, n, f.data(), x.data(), rf);
-  for (int k = 1; k < s.p.npre; ++k) smooth_step(L.As, L.Ms, f.data(), x, rf);
+  pre_smooth(s, L, f.data(), x.data(), rf);
+  for (int k = 1; k < s.p.npre; ++k) post_smooth(s, L, f.data(), x, rf);
   vector<double> r((size_t)n * b);
   residual(L.As, f.data(), x.data(), r.data(), rf);
   vector<double> fc((size_t)L.nc * b), xc;
   spmv(L.Rs, 1.0, r.data(), 0.0, fc.data(), rf);
   vcycle(s, l + 1, fc, xc);
   spmv(L.Ps, 1.0, xc.data(), 1.0, x.data(), rf);
-  for (int k = 0; k < s.p.npost; ++k) smooth_step(L.As, L.Ms, f.data(), x, rf);
+  for (int k = 0; k < s.p.npost; ++k) post_smooth(s, L, f.data(), x, rf);
 }
 
 // ---------------------------------------------------------------- C10 Schur
@@ -945,6 +1050,7 @@ static void precond(const orc_solver& s, const double* r, double* z) {
 
 extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out) {
   if (!A || !p || !out || A->n != A->m) return ORC_EINVAL;
+  if (p->smoother == ORC_ILU0 && p->ilu_sweeps < 1) return ORC_EINVAL;
   orc_solver* s = new orc_solver;
   s->p = *p;
   s->A = *A;
@@ -975,7 +1081,14 @@ extern "C" const orc_mat* orc_level_mat(const orc_solver* s, int32_t level, int3
   if ((size_t)level == s->lv.size()) return which == 0 ? &s->Acoarse : nullptr;
   if ((size_t)level > s->lv.size()) return nullptr;
   const Level& L = s->lv[level];
-  return which == 0 ? &L.A : which == 1 ? &L.P : which == 2 ? &L.R : nullptr;
+  return which == 0 ? &L.A : which == 1 ? &L.P : which == 2 ? &L.R
+       : which == 4 ? (L.L.n ? &L.L : nullptr) : which == 5 ? (L.U.n ? &L.U : nullptr) : nullptr;
+}
+extern "C" int orc_level_smooth(const orc_solver* s, int32_t level, const double* f, double* x) {
+  if (level < 0 || (size_t)level >= s->lv.size()) return ORC_EINVAL;
+  const Level& L = s->lv[level];
+  pre_smooth(*s, L, f, x, s->p.vec_f32 != 0);
+  return ORC_OK;
 }
 extern "C" const int32_t* orc_level_agg(const orc_solver* s, int32_t level) {
   if (level < 0 || (size_t)level >= s->lv.size()) return nullptr;

@@ -22,7 +22,7 @@ extern "C" {
 
 enum { ORC_CG = 0, ORC_BICGSTAB = 1, ORC_GMRES = 2, ORC_IDRS = 3 };
 enum { ORC_PC_AMG = 0, ORC_PC_SCHUR = 1, ORC_PC_NONE = 2 };
-enum { ORC_SPAI0 = 0, ORC_JACOBI = 1 };
+enum { ORC_SPAI0 = 0, ORC_JACOBI = 1, ORC_ILU0 = 2 };
 enum { ORC_SA = 0, ORC_PLAIN = 1 };
 
 enum {
@@ -34,7 +34,7 @@ typedef struct {
   int32_t solver, gmres_m, precond, maxiter;
   int32_t hier_f32;      /* hierarchy values (A_l, P_l, R_l, M_l, coarse, B, B^T, m_S) rounded to fp32 */
   int32_t vec_f32;       /* V-cycle / Schur inner vectors rounded to fp32 at every store */
-  int32_t smoother;      /* ORC_SPAI0 | ORC_JACOBI */
+  int32_t smoother;      /* ORC_SPAI0 | ORC_JACOBI | ORC_ILU0 (block ILU(0), sweep-solved, R20) */
   double jacobi_omega;   /* 2/3 */
   double sa_omega;       /* 2/3 */
   double eps_strong;     /* 1e-3 */
@@ -53,6 +53,8 @@ typedef struct {
                             (adjust_p = 1); 2 = the explicitly
                             assembled C - B diag(A_u)^-1 B^T (the PETSc variant) */
   double over_interp;    /* plain aggregation: A_c = (1/over_interp) P^T A P (reading R19, 1.5) */
+  int32_t ilu_sweeps;    /* ORC_ILU0: Jacobi sweeps per triangular solve (>= 1, default 2, R20) */
+  int32_t _pad;
 } orc_params;
 
 typedef struct {
@@ -79,6 +81,11 @@ orc_mat* orc_csr_to_bsr(int32_t n, int32_t m, int32_t b, const int32_t* ptr, con
 
 /* ---- C1 SpMV: y = alpha A x + beta y (beta == 0 overwrites y, NaN included) ---- */
 int orc_spmv(const orc_mat* A, double alpha, const double* x, double beta, double* y);
+
+/* ---- smoother pieces (for pins) ---- */
+/* x = S_l(f): the pre-smoother of level l from a zero initial guess (SPAI0 / Jacobi:
+ * x = M f; ILU(0): the sweep-solved (LU)^-1 f), vectors at the solver's precision. */
+int orc_level_smooth(const orc_solver* s, int32_t level, const double* f, double* x);
 
 /* ---- C2 / C3 one-level pieces (for pins) ---- */
 /* strength graph after symmetric closure, as CSR without diagonal: returns number of

@@ -391,6 +391,100 @@ def test_spai0_scalar_minimiser(rng):
         assert best <= np.linalg.norm(np.eye(n) - np.diag(D) @ Ad) + 1e-12
 
 
+# ---- C8b block ILU(0) smoother (reading R20) ----
+def _ilu_dense(S, level=0):
+    """L = I + L_s, U = blockdiag(pivots) + U_s as dense arrays (pivots = inverse of D^-1)."""
+    Ls, Us = S.level_mat(level, 4), S.level_mat(level, 5)
+    Dinv = S.level_M(level)
+    n, _, b, _ = Ls.info()
+    L = np.eye(n * b) + Ls.dense()
+    U = Us.dense()
+    for i in range(n):
+        U[i * b:(i + 1) * b, i * b:(i + 1) * b] = np.linalg.inv(Dinv[i])
+    return L, U
+
+
+def _ilu_solver(ptr, col, val, **kw):
+    kw.setdefault("hier_f32", 0)
+    kw.setdefault("vec_f32", 0)
+    return _solver(ptr, col, val, smoother=oracle.ILU0, precond=oracle.PC_AMG, **kw)
+
+
+def test_ilu0_factors_reproduce_A_on_its_pattern(rng):
+    # the defining property of ILU(0) (Saad §10.3): (L U)_ij = a_ij for every stored (i, j)
+    for b, dom in ((3, 6), (2, 3), (1, 4)):
+        ptr, col, val = random_bsr(rng, 200, b, density=0.03, dom=dom)
+        A, S = _ilu_solver(ptr, col, val, coarse_enough=30 * b)
+        assert S.levels >= 2
+        L, U = _ilu_dense(S)
+        Ad = A.dense()
+        mask = bsr_dense(ptr, col, np.ones_like(val)) != 0
+        LU = L @ U
+        assert np.abs(LU[mask] - Ad[mask]).max() <= 1e-12 * np.abs(Ad).max()
+        for which, side in ((4, -1), (5, 1)):  # no fill: strictly lower / upper blocks of A's pattern
+            fp, fc, _ = S.level_mat(0, which).to_arrays()
+            rows = np.repeat(np.arange(200), np.diff(fp))
+            assert np.all(np.sign(fc - rows) == side)
+            assert not (S.level_mat(0, which).dense() != 0)[~mask].any()
+
+
+def test_ilu0_without_fill_is_exact_lu(rng):
+    # a block-tridiagonal chain has no fill: ILU(0) = LU, and with sweeps >= the chain depth
+    # the sweep-solved smoother is A^-1 (numpy dense solve)
+    n, b = 40, 3
+    ptr = np.zeros(n + 1, np.int32)
+    cols = []
+    for i in range(n):
+        c = [j for j in (i - 1, i, i + 1) if 0 <= j < n]
+        cols.extend(c)
+        ptr[i + 1] = len(cols)
+    col = np.array(cols, np.int32)
+    val = rng.standard_normal((len(col), b, b))
+    for i in range(n):
+        for k in range(ptr[i], ptr[i + 1]):
+            if col[k] == i:
+                val[k] += 8.0 * np.eye(b)
+    A, S = _ilu_solver(ptr, col, val, coarse_enough=30, ilu_sweeps=n)
+    assert S.levels >= 2
+    L, U = _ilu_dense(S)
+    Ad = A.dense()
+    assert np.linalg.norm(L @ U - Ad) <= 1e-12 * np.linalg.norm(Ad)
+    f = rng.standard_normal(n * b)
+    x = S.level_smooth(0, f)
+    xd = np.linalg.solve(Ad, f)
+    assert np.linalg.norm(x - xd) <= 1e-10 * np.linalg.norm(xd)
+
+
+def test_ilu0_sweeps_converge_to_triangular_solves(rng):
+    # k >= the dependency depth: the Jacobi sweeps equal the exact forward / backward
+    # substitutions with the dense factors (numpy); k = 1 is a different, coarser operator
+    n, b = 120, 3
+    ptr, col, val = random_bsr(rng, n, b, density=0.04, dom=6)
+    f = rng.standard_normal(n * b)
+    A, S = _ilu_solver(ptr, col, val, coarse_enough=60, ilu_sweeps=n)
+    L, U = _ilu_dense(S)
+    want = np.linalg.solve(U, np.linalg.solve(L, f))
+    x = S.level_smooth(0, f)
+    assert np.linalg.norm(x - want) <= 1e-10 * np.linalg.norm(want)
+    _, S1 = _ilu_solver(ptr, col, val, coarse_enough=60, ilu_sweeps=1)
+    x1 = S1.level_smooth(0, f)
+    assert np.linalg.norm(x1 - want) > 1e-6 * np.linalg.norm(want)
+
+
+def test_ilu0_smoothed_solves_reach_dense_solution(rng):
+    for kind, pc, solver in ((gen.STOKES, oracle.PC_SCHUR, oracle.GMRES), (gen.STOKES, oracle.PC_AMG, oracle.BICGSTAB),
+                             (gen.POISSON3, oracle.PC_AMG, oracle.IDRS)):
+        ptr, col, val = gen.matrix(kind, 8)
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        S = oracle.Solver(A, precond=pc, solver=solver, smoother=oracle.ILU0, coarse_enough=60,
+                          hier_f32=0, vec_f32=0)
+        assert S.levels >= 2
+        b = rng.standard_normal((len(ptr) - 1) * val.shape[-1])
+        r = S.solve(b, rtol=1e-10)
+        xd = np.linalg.solve(A.dense(), b)
+        assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd), (kind, solver)
+
+
 def test_jacobi_smoother_closed_form():
     n = 6
     ptr, col, val = laplace3_blocks(n)
