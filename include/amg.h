@@ -43,7 +43,7 @@ enum {
 typedef enum { AMG_F64 = 0, AMG_F32 = 1 } amg_dtype;
 enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2, AMG_IDRS = 3 };
 enum { AMG_PC_AMG = 0, AMG_PC_SCHUR = 1, AMG_PC_NONE = 2 };
-enum { AMG_SPAI0 = 0, AMG_JACOBI = 1 };
+enum { AMG_SPAI0 = 0, AMG_JACOBI = 1, AMG_ILU0 = 2 /* block ILU(0), Jacobi-sweep solves (R20) */ };
 /* coarsening: smoothed aggregation | plain aggregation, P = P_tent
    (Listings V2-V4, "amgcl::coarsening::aggregation") */
 enum { AMG_SA = 0, AMG_PLAIN_AGG = 1 };
@@ -75,7 +75,9 @@ typedef struct {
   int32_t hier_dtype;        /* values of A_l, P_l, R_l, M_l, coarse inverse, B, B^T, m_S:
                                 AMG_F32 (default, Listing V4) | AMG_F64 */
   int32_t vcycle_vec_dtype;  /* vectors inside the preconditioner: AMG_F32 (default) | AMG_F64 */
-  int32_t smoother;          /* AMG_SPAI0 (default) | AMG_JACOBI */
+  int32_t smoother;          /* AMG_SPAI0 (default) | AMG_JACOBI | AMG_ILU0
+                                (single device; the paper's U-solver smoother is ILU-type,
+                                PAPER.md:551-553) */
   int32_t coarse_enough;     /* max scalar unknowns of the coarsest level, default 3000 */
   double jacobi_omega;       /* damped-Jacobi weight, default 2/3 */
   double sa_omega;           /* prolongator damping, default 2/3 (reading R5) */
@@ -96,6 +98,8 @@ typedef struct {
                                 variant) */
   double over_interp;        /* AMG_PLAIN_AGG: A_c = (1/over_interp) P^T A P, default 1.5
                                 (over-interpolation, reading R19); ignored for AMG_SA */
+  int32_t ilu_sweeps;        /* AMG_ILU0: Jacobi sweeps per triangular solve, 1..16, default 2 */
+  int32_t _reserved;
 } amg_params;
 
 typedef struct {
@@ -174,7 +178,9 @@ void bsr_plan_destroy(struct bsr_plan* P);
 /* out[5] = {n_block_rows, block_size, nnzb(A_l), nnzb(P_l) or 0, n_coarse or 0} */
 int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);
 /* which: 0 = A_l, 1 = P_l, 2 = R_l (the solve copies in the hierarchy dtype, widened to fp64); 3 = smoother blocks M_l
- * (ptr/col ignored, val = n*b*b).  Arrays sized from amg_level_info. */
+ * (ptr/col ignored, val = n*b*b; AMG_ILU0: the pivot inverses D^-1); 4 / 5 = the ILU(0) strictly lower / upper
+ * factors (AMG_ILU0 only, else AMG_EINVAL; at most nnz(A_l) - n_l blocks, ptr[n] gives the count).  Arrays sized
+ * from amg_level_info. */
 int amg_level_export(struct amg_handle* h, int32_t level, int32_t which, int32_t* ptr, int32_t* col,
                      double* val);
 int amg_level_aggregates(struct amg_handle* h, int32_t level, int32_t* agg);

@@ -23,7 +23,7 @@ EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EINDEX_OVERFLOW, EBREAKDOWN, ECUDA, EN
 F64, F32 = 0, 1
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
-SPAI0, JACOBI = 0, 1
+SPAI0, JACOBI, ILU0 = 0, 1, 2
 SA, PLAIN_AGG = 0, 1  # coarsening
 
 
@@ -49,7 +49,8 @@ class amg_params(ctypes.Structure):
                 ("max_levels", ctypes.c_int32), ("npre", ctypes.c_int32), ("npost", ctypes.c_int32),
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
                 ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32),
-                ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32), ("over_interp", ctypes.c_double)]
+                ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32), ("over_interp", ctypes.c_double),
+                ("ilu_sweeps", ctypes.c_int32), ("_reserved", ctypes.c_int32)]
 
 
 class amg_report(ctypes.Structure):
@@ -340,7 +341,8 @@ class Solver:
         return n
 
     def level_export(self, level: int, which: int):
-        """which 0/1/2: (ptr, col, val[nnz,b,b]) of A_l/P_l/R_l; 3: M_l [n,b,b] (fp64 host numpy)."""
+        """which 0/1/2: (ptr, col, val[nnz,b,b]) of A_l/P_l/R_l; 3: M_l [n,b,b] (fp64 host numpy);
+        4/5: the ILU(0) strictly lower / upper factors (AMG_ILU0)."""
         import numpy as np
         n, b, nnzA, nnzP, nc = self.level_info(level)
         if which == 3:
@@ -348,14 +350,15 @@ class Solver:
             _check(lib().amg_level_export(self.h, level, 3, None, None, val.ctypes.data_as(ctypes.c_void_p)),
                    "amg_level_export")
             return val
-        rows = {0: n, 1: n, 2: nc}[which]
-        nnz = nnzA if which == 0 else nnzP
+        rows = {0: n, 1: n, 2: nc, 4: n, 5: n}[which]
+        nnz = nnzA if which in (0, 4, 5) else nnzP  # the factors: at most nnz(A) - n blocks
         ptr = np.zeros(rows + 1, dtype=np.int32)
         col = np.zeros(max(nnz, 1), dtype=np.int32)
         val = np.zeros((max(nnz, 1), b, b))
         _check(lib().amg_level_export(self.h, level, which, ptr.ctypes.data_as(ctypes.c_void_p),
                                       col.ctypes.data_as(ctypes.c_void_p), val.ctypes.data_as(ctypes.c_void_p)),
                "amg_level_export")
+        nnz = int(ptr[-1])
         return ptr, col[:nnz], val[:nnz]
 
     def level_aggregates(self, level: int):

@@ -130,7 +130,7 @@ struct LEpiResidual {  // r = f - A x
 };
 
 template <typename V, typename X>
-struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
+struct LEpiSmooth {  // xo = x + M (f - A g), M block-diagonal; g the gathered vector (usually x)
   static constexpr int kDots = 0;
   const V* M;
   const X* f;
@@ -149,14 +149,14 @@ struct LEpiSmooth {  // xo = x + M (f - A x), M block-diagonal
     double t = m[0] * rv[0];
 #pragma unroll
     for (int c = 1; c < BR; ++c) t = fma(m[c], rv[c], t);
-    xo[o] = to_out<X>((double)x[o] + t);
+    xo[o] = to_out<X>((x ? (double)x[o] : 0.0) + t);  // x == nullptr: from zero (ILU(0) U sweeps)
   }
   template <int BR>
   __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
     const int64_t o = (int64_t)row * BR;
     double rv[BR], xv[BR], m[BR][BR];
 #pragma unroll
-    for (int c = 0; c < BR; ++c) rv[c] = (double)f[o + c] - yr[c], xv[c] = (double)x[o + c];
+    for (int c = 0; c < BR; ++c) rv[c] = (double)f[o + c] - yr[c], xv[c] = x ? (double)x[o + c] : 0.0;
 #pragma unroll
     for (int i = 0; i < BR; ++i) load_b<BR, false>(M + (o + i) * BR, m[i]);
 #pragma unroll

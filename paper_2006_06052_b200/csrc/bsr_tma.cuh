@@ -136,7 +136,7 @@ struct EpiSmooth {  // xo = x + M (f - A x)
     double t = m[0] * res[0];
 #pragma unroll
     for (int c = 1; c < B; ++c) t = fma(m[c], res[c], t);
-    xo[o + gl] = to_out<X>((double)x[o + gl] + t);
+    xo[o + gl] = to_out<X>((x ? (double)x[o + gl] : 0.0) + t);  // x == nullptr: from zero
   }
 };
 

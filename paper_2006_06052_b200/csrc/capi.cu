@@ -88,6 +88,8 @@ int amg_params_default(amg_params* p) {
   p->coarsening = AMG_SA;
   p->schur_shat = 1;
   p->over_interp = 1.5;
+  p->ilu_sweeps = 2;
+  p->_reserved = 0;
   return AMG_OK;
 }
 

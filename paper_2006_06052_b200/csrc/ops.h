@@ -35,6 +35,9 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
 // K5  xo = x + M (f - A x)
 void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
                    cudaStream_t s, int r0 = 0, int r1 = -1);
+// ILU(0) U sweep (R20): xo = xb + D^-1 (y - U_s z); xb == nullptr: from zero
+void launch_ilu_usweep(const Mat& U, const void* Dinv, const void* y, const void* z, const void* xb, void* xo, int xt,
+                       cudaStream_t s);
 // K4a x = M f
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
                     cudaStream_t s);

@@ -489,6 +489,66 @@ __global__ void k_smoother(int n, const int32_t* ptr, const double* val, const i
   for (int e = 0; e < B * B; ++e) M[(int64_t)I * B * B + e] = theta * inv[e];
 }
 
+// ---------------------------------------------------------------- S8b block ILU(0)
+// Row i of the IKJ factorisation on A's pattern (reading R20; the oracle's ilu0_factor, same
+// operation order): for k < i ascending: a_ik <- a_ik D_k^-1, a_ij <- a_ij - a_ik a_kj for the
+// later j of row i present in row k; then D_i^-1 = inverse(a_ii).  Rows of one dependency
+// level run in parallel (their k < i rows are final).
+template <int B>
+__global__ void k_ilu_rows(int cnt, const int32_t* rows, const int32_t* ptr, const int32_t* col, double* a,
+                           double* Dinv, int* err) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int i = rows[t];
+  double tmp[B * B];
+  int kd = -1;
+  for (int kk = ptr[i]; kk < ptr[i + 1]; ++kk) {
+    const int k = col[kk];
+    if (k == i) kd = kk;
+    if (k >= i) continue;
+    double* aik = a + (int64_t)kk * B * B;
+    blk_mul<B>(aik, Dinv + (int64_t)k * B * B, tmp);
+    for (int e = 0; e < B * B; ++e) aik[e] = tmp[e];
+    for (int jj = kk + 1; jj < ptr[i + 1]; ++jj) {
+      const int kj = bsearch(col, ptr[k], ptr[k + 1], col[jj]);
+      if (kj < 0) continue;
+      blk_mul<B>(aik, a + (int64_t)kj * B * B, tmp);
+      double* aij = a + (int64_t)jj * B * B;
+      for (int e = 0; e < B * B; ++e) aij[e] = aij[e] - tmp[e];
+    }
+  }
+  if (kd < 0) {
+    set_err(err, AMG_EZERODIAG);
+    return;
+  }
+  if (!block_inverse<B>(a + (int64_t)kd * B * B, Dinv + (int64_t)i * B * B)) set_err(err, AMG_ESINGULAR_BLOCK);
+}
+
+__global__ void k_tri_count(int n, const int32_t* ptr, const int32_t* col, int32_t* lc, int32_t* uc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int l = 0, u = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) l += col[k] < i, u += col[k] > i;
+  lc[i] = l;
+  uc[i] = u;
+}
+template <int B>
+__global__ void k_tri_fill(int n, const int32_t* ptr, const int32_t* col, const double* a, const int32_t* lp,
+                           int32_t* lcol, double* lval, const int32_t* up, int32_t* ucol, double* uval) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int l = lp[i], u = up[i];
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int j = col[k];
+    if (j == i) continue;
+    const int o = j < i ? l++ : u++;
+    int32_t* dc = j < i ? lcol : ucol;
+    double* dv = j < i ? lval : uval;
+    dc[o] = j;
+    for (int e = 0; e < B * B; ++e) dv[(int64_t)o * B * B + e] = a[(int64_t)k * B * B + e];
+  }
+}
+
 // ---------------------------------------------------------------- S9 Schur split
 // A (b x b, fp64) -> A_u (nu x nu), B (row pc, vel cols), B^T (vel rows, col pc), C
 __global__ void k_schur_split(int64_t nnz, int b, int pc, const double* val, double* au, double* bv, double* btv,
@@ -816,6 +876,61 @@ Mat solve_copy(Handle& h, const Mat& M64, cudaStream_t s) {
 
 }  // namespace
 
+// Block ILU(0) of A (fp64): level schedule of the lower-triangular dependency graph on the
+// host (level(i) = 1 + max level(k), k < i in row i), one launch per level, then the
+// strictly lower / upper split.  D^-1 -> Dinv (n b^2).
+void ilu0_factor(SetupCtx& c, const Mat& A, double* Dinv, Mat& Lo, Mat& Up) {
+  const int n = A.n, b = A.b;
+  cudaStream_t s = c.s;
+  std::vector<int32_t> hp((size_t)n + 1), hc((size_t)std::max<int64_t>(A.nnz, 1));
+  AMG_CK(cudaMemcpyAsync(hp.data(), A.ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  if (A.nnz > 0) AMG_CK(cudaMemcpyAsync(hc.data(), A.col, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToHost, s));
+  AMG_CK(cudaStreamSynchronize(s));
+  std::vector<int32_t> lev(n, 0);
+  int nlev = n > 0 ? 1 : 0;
+  for (int i = 0; i < n; ++i) {
+    int l = 0;
+    for (int k = hp[i]; k < hp[i + 1]; ++k)
+      if (hc[k] < i) l = std::max(l, lev[hc[k]] + 1);
+    lev[i] = l;
+    nlev = std::max(nlev, l + 1);
+  }
+  std::vector<int32_t> off(nlev + 1, 0), order(n);
+  for (int i = 0; i < n; ++i) ++off[lev[i] + 1];
+  for (int l = 0; l < nlev; ++l) off[l + 1] += off[l];
+  std::vector<int32_t> cur(off.begin(), off.end() - 1);
+  for (int i = 0; i < n; ++i) order[cur[lev[i]]++] = i;
+  int32_t* dorder = c.tmp.alloc_n<int32_t>(std::max(n, 1));
+  AMG_CK(cudaMemcpyAsync(dorder, order.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+  double* a = c.tmp.alloc_n<double>(std::max<int64_t>(A.nnz, 1) * b * b);
+  AMG_CK(cudaMemcpyAsync(a, A.val, sizeof(double) * A.nnz * b * b, cudaMemcpyDeviceToDevice, s));
+  dispatch_bs(b, [&](auto Bc) {
+    constexpr int BB = decltype(Bc)::value;
+    for (int l = 0; l < nlev; ++l) {
+      const int cnt = off[l + 1] - off[l];
+      k_ilu_rows<BB><<<grid_for(cnt, kT), kT, 0, s>>>(cnt, dorder + off[l], A.ptr, A.col, a, Dinv, c.err);
+    }
+    AMG_CK_LAUNCH();
+  });
+  check_err(c, "ILU(0) factorisation");
+  int32_t* lc = c.tmp.alloc_n<int32_t>(n + 1);
+  int32_t* uc = c.tmp.alloc_n<int32_t>(n + 1);
+  k_tri_count<<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, lc, uc);
+  AMG_CK_LAUNCH();
+  const int64_t ln = scan(c, lc, n), un = scan(c, uc, n);
+  Lo = new_mat(c.tmp, n, A.m, b, ln);
+  Up = new_mat(c.tmp, n, A.m, b, un);
+  AMG_CK(cudaMemcpyAsync(Lo.ptr, lc, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  AMG_CK(cudaMemcpyAsync(Up.ptr, uc, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  dispatch_bs(b, [&](auto Bc) {
+    constexpr int BB = decltype(Bc)::value;
+    k_tri_fill<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, a, Lo.ptr, Lo.col, (double*)Lo.val, Up.ptr,
+                                                   Up.col, (double*)Up.val);
+  });
+  AMG_CK_LAUNCH();
+  AMG_CK(cudaStreamSynchronize(s));
+}
+
 // ---------------------------------------------------------------- the setup driver
 void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0, cudaStream_t s) {
   SetupCtx c;
@@ -906,7 +1021,7 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
   h.lbounds.push_back(bounds);
 
   Mat A = Amg;
-  std::vector<Mat> lvA, lvP, lvR;
+  std::vector<Mat> lvA, lvP, lvR, lvL, lvU;
   std::vector<double*> lvM;
   std::vector<int32_t*> lvAgg;
   std::vector<int32_t> lvNc;
@@ -1025,11 +1140,16 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
                                                     cand, P.ptr, P.col, (double*)P.val, p.sa_omega);
       }
       AMG_CK_LAUNCH();
-      k_smoother<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, (const double*)A.val, diag, p.smoother == AMG_SPAI0,
-                                                    p.jacobi_omega, M, c.err);
+      if (p.smoother != AMG_ILU0)
+        k_smoother<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, (const double*)A.val, diag,
+                                                      p.smoother == AMG_SPAI0, p.jacobi_omega, M, c.err);
       AMG_CK_LAUNCH();
     });
     check_err(c, "prolongator / smoother");
+    Mat Lo, Up;
+    if (p.smoother == AMG_ILU0) ilu0_factor(c, A, M, Lo, Up);  // M <- D^-1
+    lvL.push_back(Lo);
+    lvU.push_back(Up);
     Mat R = transpose(c, P);
     Mat AP = spgemm(c, A, P);
     Mat Ac = spgemm(c, R, AP);
@@ -1089,6 +1209,12 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     L.A = solve_copy(h, lvA[l], s);
     L.P = solve_copy(h, lvP[l], s);
     L.R = solve_copy(h, lvR[l], s);
+    if (lvL[l].ptr) {  // AMG_ILU0: the factors and the sweep vectors
+      L.Lf = solve_copy(h, lvL[l], s);
+      L.Uf = solve_copy(h, lvU[l], s);
+      const int64_t nbw = std::max<int64_t>((int64_t)lvA[l].n * lvA[l].b, 1);
+      for (void*& w : L.w) w = h.arena.alloc(nbw * dtype_size(h.xt));
+    }
     const int64_t nb = (int64_t)lvA[l].n * lvA[l].b;
     L.M = h.arena.alloc(std::max<int64_t>(nb * lvA[l].b, 1) * dtype_size(h.vt));
     launch_convert(nb * lvA[l].b, lvM[l], AMG_F64, L.M, h.vt, 1.0, s);

@@ -97,6 +97,8 @@ int check_params(const amg_params* p) {
   if (p->npre < 1 || p->npost < 0 || p->max_levels < 1 || p->maxiter < 0) return AMG_EINVAL;
   if (p->coarsening != AMG_SA && p->coarsening != AMG_PLAIN_AGG) return AMG_EINVAL;
   if (p->schur_shat < 0 || p->schur_shat > 2 || !(p->over_interp > 0.0)) return AMG_EINVAL;
+  if (p->smoother < AMG_SPAI0 || p->smoother > AMG_ILU0) return AMG_EINVAL;
+  if (p->smoother == AMG_ILU0 && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16)) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;
@@ -290,8 +292,11 @@ int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_
     cudaFree(tmp);
     return AMG_OK;
   }
-  if (which < 0 || which > 2 || (coarsest && which != 0) || !ptr || !col) return AMG_EINVAL;
-  const Mat& M = coarsest ? h->coarse.A : (which == 0 ? h->lv[level].A : which == 1 ? h->lv[level].P : h->lv[level].R);
+  if (which < 0 || which > 5 || (coarsest && which != 0) || !ptr || !col) return AMG_EINVAL;
+  if (which >= 4 && !h->lv[level].Lf.ptr) return AMG_EINVAL;  // ILU(0) factors only with AMG_ILU0
+  const Level& LL = h->lv[std::min(level, (int32_t)h->lv.size() - 1)];
+  const Mat& M = coarsest ? h->coarse.A
+                          : (which == 0 ? LL.A : which == 1 ? LL.P : which == 2 ? LL.R : which == 4 ? LL.Lf : LL.Uf);
   AMG_CK(cudaDeviceSynchronize());
   AMG_CK(cudaMemcpy(ptr, M.ptr, sizeof(int32_t) * (M.n + 1), cudaMemcpyDeviceToHost));
   if (M.nnz > 0) AMG_CK(cudaMemcpy(col, M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
@@ -355,8 +360,8 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   int64_t v[8] = {};
   v[0] = mat(h->A) + sell(h->A);
   for (const Level& L : h->lv) {
-    v[1] += mat(L.A) + mat(L.P) + mat(L.R);
-    v[2] += sell(L.A) + sell(L.P) + sell(L.R);
+    v[1] += mat(L.A) + mat(L.P) + mat(L.R) + mat(L.Lf) + mat(L.Uf);
+    v[2] += sell(L.A) + sell(L.P) + sell(L.R) + sell(L.Lf) + sell(L.Uf);
     v[3] += (int64_t)L.A.n * L.A.b * L.A.b * dtype_size(h->vt);
   }
   if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);

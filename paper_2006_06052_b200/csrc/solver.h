@@ -29,8 +29,10 @@ struct Halo {
 
 struct Level {
   Mat A, P, R;                // solve copies, values in hier dtype
+  Mat Lf, Uf;                 // AMG_ILU0: strictly lower / upper factor blocks (else empty)
   Halo halo;                  // distributed: ghost plan of A
-  void* M = nullptr;          // smoother blocks [n][b][b], hier dtype
+  void* M = nullptr;          // smoother blocks [n][b][b], hier dtype (AMG_ILU0: pivot inverses)
+  void* w[4] = {};            // AMG_ILU0 sweep vectors (y, y', z, z'), vec dtype
   int32_t* agg = nullptr;     // aggregates (device) [n], -1 = isolated
   int32_t nc = 0;
   void *f = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;  // work vectors, vec dtype

@@ -553,13 +553,18 @@ void launch_residual(const Mat& A, const void* f, const void* x, void* r, int xt
   AMG_CK_LAUNCH();
 }
 
-void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
-                   cudaStream_t s, int r0, int r1) {
+// xo = xb + M (f - A g): the smoother (g = xb = x) and the ILU(0) U sweeps (g = z, xb = the
+// smoothed iterate on the last sweep, else nullptr = from zero)
+static void launch_smooth_g(const char* label, const Mat& A, const void* M, const void* f, const void* g,
+                            const void* xb, void* xo, int xt, cudaStream_t s, int r0, int r1) {
   if (r1 < 0) r1 = A.n;
   if (A.n == 0 || r1 <= r0) return;
   const double frac = (double)(r1 - r0) / A.n;
-  ProfScope ps_(prof_name("smooth", A.b, A.vt, xt),
-                frac * (mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 3.0 * A.n * A.b * dtype_size(xt)), s);
+  ProfScope ps_(prof_name(label, A.b, A.vt, xt),
+                frac * (mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) +
+                        (2.0 + (xb ? 1.0 : 0.0)) * A.n * A.b * dtype_size(xt) + (double)A.m * A.b * dtype_size(xt) -
+                        (g == xb ? (double)A.n * A.b * dtype_size(xt) : 0.0)),
+                s);
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
     dispatch_t(A.vt, [&](auto v) {
@@ -567,17 +572,27 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
       dispatch_t(xt, [&](auto xx) {
         using X = decltype(xx);
         if (A.tma_grid > 0) {
-          auto e = EpiSmooth<B, V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo};
-          if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, e, s);
-          else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, e, s);
+          auto e = EpiSmooth<B, V, X>{(const V*)M, (const X*)f, (const X*)xb, (X*)xo};
+          if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)g, e, s);
+          else launch_tma_rows<B, B, V, X, false>(A, (const X*)g, e, s);
         } else {
-          launch_lane<B, B, V, X>(A, (const X*)x, LEpiSmooth<V, X>{(const V*)M, (const X*)f, (const X*)x, (X*)xo}, s,
+          launch_lane<B, B, V, X>(A, (const X*)g, LEpiSmooth<V, X>{(const V*)M, (const X*)f, (const X*)xb, (X*)xo}, s,
                                   r0, r1);
         }
       });
     });
   });
   AMG_CK_LAUNCH();
+}
+
+void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, void* xo, int xt,
+                   cudaStream_t s, int r0, int r1) {
+  launch_smooth_g("smooth", A, M, f, x, x, xo, xt, s, r0, r1);
+}
+
+void launch_ilu_usweep(const Mat& U, const void* Dinv, const void* y, const void* z, const void* xb, void* xo, int xt,
+                       cudaStream_t s) {
+  launch_smooth_g("ilu_u", U, Dinv, y, z, xb, xo, xt, s, 0, -1);
 }
 
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,

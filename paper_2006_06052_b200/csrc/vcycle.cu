@@ -12,6 +12,32 @@ namespace amgb {
 
 void* level0_f(Handle& h) { return h.lv.empty() ? h.coarse.f : h.lv[0].f; }
 
+// ILU(0) smoothing (reading R20), k = ilu_sweeps Jacobi sweeps per triangular solve:
+//   y_0 = g, y_m = g - L_s y_(m-1);  z_0 = D^-1 y_k;  z_m = D^-1 (y_k - U_s z_(m-1)), the last
+//   one written as xo = xb + z_k (xb == nullptr: from zero).  2k + 1 launches; single device.
+static void ilu_apply(Handle& h, Level& L, const void* g, const void* xb, void* xo, cudaStream_t s) {
+  const int xt = h.xt, k = h.p.ilu_sweeps;
+  const void* y = g;
+  for (int m = 0; m < k; ++m) {
+    launch_residual(L.Lf, g, y, L.w[m & 1], xt, s);
+    y = L.w[m & 1];
+  }
+  void* z = L.w[2];
+  launch_apply_M(L.A.n, L.A.b, L.M, h.vt, y, z, xt, s);
+  for (int m = 1; m <= k; ++m) {
+    const bool last = m == k;
+    void* zn = last ? xo : (z == L.w[2] ? L.w[3] : L.w[2]);
+    launch_ilu_usweep(L.Uf, L.M, y, z, last ? xb : nullptr, zn, xt, s);
+    z = zn;
+  }
+}
+
+// x <- x + (LU)^-1 (f - A x)
+static void ilu_step(Handle& h, Level& L, void* x, cudaStream_t s) {
+  launch_residual(L.A, L.f, x, L.r, h.xt, s);
+  ilu_apply(h, L, L.r, x, x, s);
+}
+
 // V(l, f):  x = M f;  r = f - A x;  f_c = R r;  x_c = V(l+1, f_c);  x += P x_c;
 //           x = x + M (f - A x)            (one kernel per line; fp64 accumulation,
 //                                            one rounding on store)
@@ -25,8 +51,14 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   Level& L = h.lv[l];
   void* x = L.x;
   void* t = L.t;
-  launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
+  const bool ilu = L.Lf.ptr != nullptr;
+  if (ilu) ilu_apply(h, L, L.f, nullptr, x, s);  // K4a with ILU(0): x = (LU)^-1 f (sweeps)
+  else launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
   for (int k = 1; k < h.p.npre; ++k) {
+    if (ilu) {
+      ilu_step(h, L, x, s);
+      continue;
+    }
     halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
                     [&](int r0, int r1) { launch_smooth(L.A, L.M, L.f, x, t, xt, s, r0, r1); });
     std::swap(x, t);
@@ -41,6 +73,10 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   void* xc = vcycle_run(h, l + 1, s);
   launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
   for (int k = 0; k < h.p.npost; ++k) {          // K5: post-smooth (double-buffered)
+    if (ilu) {
+      ilu_step(h, L, x, s);
+      continue;
+    }
     halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
                     [&](int r0, int r1) { launch_smooth(L.A, L.M, L.f, x, t, xt, s, r0, r1); });
     std::swap(x, t);
@@ -128,6 +164,16 @@ static double vcycle_bytes(const Handle& h) {
   double tot = 0.0;
   for (const Level& L : h.lv) {
     const double nb = (double)L.A.n * L.A.b;
+    if (L.Lf.ptr) {  // ILU(0): k L sweeps (g, y gathered, y'), z_0 = D^-1 y, k U sweeps (y, z gathered, z' | x rw)
+      const double k = h.p.ilu_sweeps, Msz = nb * L.A.b * sv;
+      const double app = k * (mat_bytes(L.Lf, h.vt) + 3.0 * nb * sx) + (Msz + 2.0 * nb * sx) +
+                         k * (mat_bytes(L.Uf, h.vt) + Msz + 3.0 * nb * sx);
+      tot += 2.0 * app + nb * sx;                                 // pre-smooth, post-smooth (+ x read)
+      tot += 2.0 * (mat_bytes(L.A, h.vt) + 3.0 * nb * sx);       // K4b and the post-smooth residual
+      tot += mat_bytes(L.P, h.vt) + mat_bytes(L.R, h.vt);
+      tot += nb * sx * (1 + 2) + (double)L.nc * L.A.b * sx * 2;  // K6 r read; K7 x rw; f_c, x_c
+      continue;
+    }
     tot += 2.0 * mat_bytes(L.A, h.vt) + mat_bytes(L.P, h.vt) + mat_bytes(L.R, h.vt);
     tot += 2.0 * nb * L.A.b * sv;  // M read twice
     // K4a: f, x | K4b: f, x, r | K6: r, f_c | K7: x_c, x rw | K5: f, x, x'

@@ -28,7 +28,7 @@ ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxit
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
           "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed",
           "schur_u_scalar": "schur_u_scalar", "coarsening": "coarsening", "schur_shat": "schur_shat",
-          "over_interp": "over_interp"}
+          "over_interp": "over_interp", "ilu_sweeps": "ilu_sweeps"}
 
 
 def make_pair(amg, ptr, col, val, hier32=True, **kw):
@@ -71,6 +71,14 @@ def check_hierarchy(S, O, hier32):
         M = S.level_export(l, 3)
         oM = O.level_M(l)
         assert np.array_equal(M, r32(oM) if hier32 else oM), f"smoother level {l}"
+        for which in (4, 5):  # ILU(0) factors (AMG_ILU0)
+            oF = O.level_mat(l, which)
+            if oF is None:
+                continue
+            optr, ocol, oval = oF.to_arrays()
+            ptr, col, val = S.level_export(l, which)
+            assert np.array_equal(ptr, optr) and np.array_equal(col, ocol), f"ILU pattern {which} level {l}"
+            assert np.array_equal(val, r32(oval) if hier32 else oval), f"ILU values {which} level {l}"
 
 
 CASES = [
@@ -91,6 +99,12 @@ CASES = [
     ("shat-C-f64", gen.STOKES, 10, dict(precond=1, solver=2, schur_shat=0, coarse_enough=40), False),
     ("shat-full-f64", gen.STOKES, 12, dict(precond=1, solver=2, schur_shat=2, coarse_enough=40), False),
     ("shat-full-plain-16", gen.STOKES, 16, dict(precond=1, solver=3, schur_shat=2, coarsening=1), True),
+    # block ILU(0) smoothing (R20); plain aggregation + ILU = the paper's V3/V4 U-solver shape
+    ("ilu0-poisson-f64", gen.POISSON3, 10, dict(precond=0, solver=1, smoother=2, coarse_enough=40), False),
+    ("ilu0-stokes-schur-16", gen.STOKES, 16, dict(precond=1, solver=3, smoother=2), True),
+    ("ilu0-plain-agg-f64", gen.STOKES, 12, dict(precond=1, solver=3, smoother=2, coarsening=1, coarse_enough=40),
+     False),
+    ("ilu0-monolithic-4x4-16", gen.STOKES, 16, dict(precond=0, solver=1, smoother=2, ilu_sweeps=3), True),
 ]
 
 
@@ -112,6 +126,16 @@ def test_hierarchy_random_matrices(amg, rng):
             for h32 in (False, True):
                 A, S, O = make_pair(amg, ptr, col, val, hier32=h32, precond=0, coarse_enough=20 * b)
                 check_hierarchy(S, O, h32)
+
+
+def test_ilu0_random_matrices(amg, rng):
+    # block ILU(0) factors bit-exact with the oracle for b = 1..4, fp64 and fp32 hierarchies
+    for b in (1, 2, 3, 4):
+        ptr, col, val = random_bsr(rng, 300, b, density=0.015, dom=6)
+        for h32 in (False, True):
+            A, S, O = make_pair(amg, ptr, col, val, hier32=h32, precond=0, solver=1, smoother=2,
+                                coarse_enough=20 * b)
+            check_hierarchy(S, O, h32)
 
 
 def test_smoother_jacobi_and_omega(amg):
@@ -163,6 +187,13 @@ SOLVE_CASES = [
     ("plain-agg-bicgstab-cfg3", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, coarsening=1), True),
     ("shat-full-gmres-cfg5-16", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(precond=1, solver=2, schur_shat=2), True),
     ("shat-C-gmres-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, schur_shat=0), False),
+    # block ILU(0) smoothing
+    ("ilu0-idrs5-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3, smoother=2), True),
+    ("ilu0-plain-gmres-cfg5-16", gen.STOKES, 16, gen.RHS_LID_NOISE,
+     dict(precond=1, solver=2, smoother=2, coarsening=1), True),
+    ("ilu0-bicgstab-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, smoother=2), True),
+    ("ilu0-sweeps3-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, smoother=2, ilu_sweeps=3),
+     False),
 ]
 
 

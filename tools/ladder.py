@@ -7,7 +7,7 @@ Same outer solver and Schur pressure correction, only the U-solver changes:
 The paper's outer solver is IDR(5) (Table 1); GMRES(30) (the BASELINE cfg 4/5 solver) is
 reported beside it.  Prints one JSON line per (cfg, solver, variant) and a table.
 
-  python tools/ladder.py [n ...]        (default 128)
+  python tools/ladder.py [n ...] [--extra]   (default 128; --extra: the §8(f) #3/#4 variants of V4)
 """
 import json
 import os
@@ -28,11 +28,19 @@ VARIANTS = {
     "V3": dict(schur_u_scalar=0, hier_dtype=amg.F64, vcycle_vec_dtype=amg.F64),
     "V4": dict(schur_u_scalar=0, hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32),
 }
+# SURVEY.md §8(f) #3/#4 variants of the V4 U-solver / P-solver (--extra)
+EXTRA = {
+    "V4-plain": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, coarsening=amg.PLAIN_AGG),
+    "V4-ilu0": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, smoother=amg.ILU0),
+    "V4-plain-ilu0": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, coarsening=amg.PLAIN_AGG, smoother=amg.ILU0),
+    "V4-shat-full": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, schur_shat=2),
+}
 SOLVERS = {"idrs5": amg.IDRS, "gmres30": amg.GMRES}
 
 
 def main():
-    sizes = [int(a) for a in sys.argv[1:]] or [128]
+    sizes = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [128]
+    variants = ({"V4": VARIANTS["V4"], **EXTRA} if "--extra" in sys.argv else VARIANTS)
     rows = []
     for n in sizes:
         cfg = 5 if n == 256 else 4
@@ -40,7 +48,7 @@ def main():
         A = amg.BSR.from_numpy(ptr, col, val)
         b = torch.as_tensor(bvec, device="cuda")
         for sname, solver in SOLVERS.items():
-            for vname, kw in VARIANTS.items():
+            for vname, kw in variants.items():
                 torch.cuda.synchronize()
                 torch.cuda.empty_cache()
                 t0 = time.perf_counter()
