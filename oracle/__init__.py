@@ -77,6 +77,8 @@ def lib():
             "orc_roots": (i32, [P, dbl, i32, P]),
             "orc_block_inverse": (i32, [i32, P, P]),
             "orc_setup": (i32, [P, P, P]),
+            "orc_setup_pmask": (i32, [P, P, P, P]),
+            "orc_schur_np": (i32, [P]),
             "orc_free": (None, [P]),
             "orc_levels": (i32, [P]),
             "orc_level_mat": (P, [P, i32, i32]),
@@ -234,11 +236,17 @@ class SolveResult:
 
 
 class Solver:
-    def __init__(self, A: Mat, params: Params | None = None, **kw):
+    def __init__(self, A: Mat, params: Params | None = None, pmask=None, **kw):
+        """pmask (optional, n_rows*b bools): Schur split by a general scalar pressure mask (R21)."""
         self.A = A
         self.params = params if params is not None else default_params(**kw)
         h = P()
-        rc = lib().orc_setup(A.h, ctypes.byref(self.params), ctypes.byref(h))
+        if pmask is None:
+            rc = lib().orc_setup(A.h, ctypes.byref(self.params), ctypes.byref(h))
+        else:
+            self._pmask = np.ascontiguousarray(pmask, dtype=np.uint8)
+            rc = lib().orc_setup_pmask(A.h, self._pmask.ctypes.data_as(ctypes.c_void_p), ctypes.byref(self.params),
+                                       ctypes.byref(h))
         if rc != OK:
             raise RuntimeError(f"orc_setup failed: {rc}")
         self.h = h
@@ -286,7 +294,7 @@ class Solver:
         return Mat(h, owned=False) if h else None
 
     def schur_vectors(self):
-        n = self.n
+        n = lib().orc_schur_np(self.h)
         dp = lib().orc_schur_Shat_diag(self.h)
         mp = lib().orc_schur_mS(self.h)
         if not dp:

@@ -631,6 +631,11 @@ struct orc_solver {
   vector<double> Shat_diag, mS;
   vector<double> Bs, BTs, mSs;
   vector<int32_t> vel;      // velocity component indices
+  // general scalar pressure mask (R21): index maps and the scalar split of A
+  bool masked = false;
+  vector<int32_t> uidx, pidx;   // scalar unknowns of each class, ascending
+  orc_mat Bm, BTm, Cm;          // B (p rows x u cols), B^T (u rows x p cols), C, b = 1
+  orc_mat Bms, BTms;            // solve copies (narrowed when hier_f32)
 };
 
 static orc_mat narrowed(const orc_mat& A) {
@@ -989,7 +994,115 @@ static orc_mat scalar_expansion(const orc_mat& A) {
 
 // Eq. 9a then 9b with one application each:
 //   u* = V_u(r_u);  p = m_S o (r_p - B u*);  u = V_u(r_u - B^T p);  z = (u, p)
+// ---------------------------------------------------------------- C10b Schur, scalar pmask
+// Reading R21: the scalar expansion As of A (structural non-zeros, diagonal kept; R18) is
+// split by the mask into A_u (u rows, u cols), B (p rows, u cols), B^T (u rows, p cols), C,
+// each renumbered by the ascending position of its unknowns (rows stay sorted).  S_hat by
+// Eq. 10 on the scalar diagonal of A_u (schur_shat 1) or C (0); m_S = SPAI0(S_hat).  With
+// the mask "component pc of every b x b block" this is the V2 split term for term.
+static int schur_setup_pmask(orc_solver& s, const vector<uint8_t>& pm) {
+  const orc_mat As = scalar_expansion(s.A);
+  const int32_t N = As.n;
+  vector<int32_t> nid(N);
+  s.uidx.clear();
+  s.pidx.clear();
+  for (int32_t q = 0; q < N; ++q) {
+    vector<int32_t>& v = pm[q] ? s.pidx : s.uidx;
+    nid[q] = (int32_t)v.size();
+    v.push_back(q);
+  }
+  const int32_t nu = (int32_t)s.uidx.size(), np = (int32_t)s.pidx.size();
+  if (nu == 0 || np == 0) return ORC_EINVAL;
+  auto init = [](orc_mat& M, int32_t n, int32_t m) {
+    M = orc_mat();
+    M.n = n;
+    M.m = m;
+    M.b = 1;
+    M.ptr.assign(n + 1, 0);
+  };
+  init(s.Au, nu, nu);
+  init(s.BTm, nu, np);
+  init(s.Bm, np, nu);
+  init(s.Cm, np, np);
+  for (int32_t q = 0; q < N; ++q) {
+    const bool prow = pm[q] != 0;
+    for (int32_t k = As.ptr[q]; k < As.ptr[q + 1]; ++k) {
+      const int32_t j = As.col[k];
+      const bool pcol = pm[j] != 0;
+      orc_mat& M = prow ? (pcol ? s.Cm : s.Bm) : (pcol ? s.BTm : s.Au);
+      M.col.push_back(nid[j]);
+      M.val.push_back(As.val[k]);
+    }
+    orc_mat& M1 = prow ? s.Bm : s.Au;
+    orc_mat& M2 = prow ? s.Cm : s.BTm;
+    M1.ptr[nid[q] + 1] = (int32_t)M1.col.size();
+    M2.ptr[nid[q] + 1] = (int32_t)M2.col.size();
+  }
+  s.Shat_diag.assign(np, 0.0);
+  s.mS.assign(np, 0.0);
+  for (int32_t i = 0; i < np; ++i) {
+    const int64_t kd = find_block(s.Cm, i, i);
+    if (kd < 0) return ORC_EZERODIAG;
+    double sum = 0.0;
+    if (s.p.schur_shat == 1)
+      for (int32_t k = s.Bm.ptr[i]; k < s.Bm.ptr[i + 1]; ++k) {
+        const int32_t J = s.Bm.col[k];
+        const int64_t kJJ = find_block(s.Au, J, J), kJi = find_block(s.BTm, J, i);
+        if (kJJ < 0) return ORC_EZERODIAG;
+        if (kJi < 0) continue;
+        const double diag = s.Au.val[kJJ];
+        if (diag == 0.0) return ORC_EZERODIAG;
+        const double t = s.Bm.val[k] * (1.0 / diag);
+        sum = sum + t * s.BTm.val[kJi];
+      }
+    s.Shat_diag[i] = s.Cm.val[kd] - sum;
+    double den = 0.0;
+    for (int32_t k = s.Cm.ptr[i]; k < s.Cm.ptr[i + 1]; ++k) {
+      const double v = (k == kd) ? s.Shat_diag[i] : s.Cm.val[k];
+      den = den + v * v;
+    }
+    if (den == 0.0) return ORC_EZERODIAG;
+    s.mS[i] = s.Shat_diag[i] / den;
+  }
+  s.Bms = s.p.hier_f32 ? narrowed(s.Bm) : s.Bm;
+  s.BTms = s.p.hier_f32 ? narrowed(s.BTm) : s.BTm;
+  s.mSs = s.mS;
+  if (s.p.hier_f32)
+    for (double& v : s.mSs) v = f32r(v);
+  return ORC_OK;
+}
+
+// u* = V(r_u);  p = m_S o (r_p - B u*);  r_u' = r_u - B^T p;  u = V(r_u');  z = (u, p) by the maps
+static void schur_apply_pmask(const orc_solver& s, const double* r, double* z) {
+  const bool rf = s.p.vec_f32 != 0;
+  const int32_t nu = (int32_t)s.uidx.size(), np = (int32_t)s.pidx.size();
+  vector<double> ru(nu), rp(np);
+  for (int32_t i = 0; i < nu; ++i) ru[i] = rf ? f32r(r[s.uidx[i]]) : r[s.uidx[i]];
+  for (int32_t i = 0; i < np; ++i) rp[i] = rf ? f32r(r[s.pidx[i]]) : r[s.pidx[i]];
+  vector<double> us, u, p(np), ru2(nu);
+  vcycle(s, 0, ru, us);
+  for (int32_t i = 0; i < np; ++i) {
+    double acc = 0.0;
+    for (int32_t k = s.Bms.ptr[i]; k < s.Bms.ptr[i + 1]; ++k) acc = acc + s.Bms.val[k] * us[s.Bms.col[k]];
+    const double v = s.mSs[i] * (rp[i] - acc);
+    p[i] = rf ? f32r(v) : v;
+  }
+  for (int32_t i = 0; i < nu; ++i) {
+    double acc = 0.0;
+    for (int32_t k = s.BTms.ptr[i]; k < s.BTms.ptr[i + 1]; ++k) acc = acc + s.BTms.val[k] * p[s.BTms.col[k]];
+    const double v = ru[i] - acc;
+    ru2[i] = rf ? f32r(v) : v;
+  }
+  vcycle(s, 0, ru2, u);
+  for (int32_t i = 0; i < nu; ++i) z[s.uidx[i]] = u[i];
+  for (int32_t i = 0; i < np; ++i) z[s.pidx[i]] = p[i];
+}
+
 static void schur_apply(const orc_solver& s, const double* r, double* z) {
+  if (s.masked) {
+    schur_apply_pmask(s, r, z);
+    return;
+  }
   const orc_mat& A = s.A;
   const int b = A.b, pc = s.p.schur_p_component, bu = b - 1;
   const bool rf = s.p.vec_f32 != 0;
@@ -1071,6 +1184,25 @@ extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out
   return ORC_OK;
 }
 
+extern "C" int orc_setup_pmask(const orc_mat* A, const uint8_t* pmask, const orc_params* p, orc_solver** out) {
+  if (!A || !pmask || !p || !out || A->n != A->m || p->precond != ORC_PC_SCHUR) return ORC_EINVAL;
+  if (p->schur_shat == 2 || (p->smoother == ORC_ILU0 && p->ilu_sweeps < 1)) return ORC_EINVAL;
+  orc_solver* s = new orc_solver;
+  s->p = *p;
+  s->A = *A;
+  s->schur = true;
+  s->masked = true;
+  vector<uint8_t> pm(pmask, pmask + (size_t)A->n * A->b);
+  int rc = schur_setup_pmask(*s, pm);
+  if (rc == ORC_OK) rc = build_hierarchy(*s, s->Au);
+  if (rc != ORC_OK) {
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return ORC_OK;
+}
+
 extern "C" void orc_free(orc_solver* s) { delete s; }
 extern "C" int32_t orc_levels(const orc_solver* s) {
   return s->p.precond == ORC_PC_NONE ? 0 : (int32_t)s->lv.size() + 1;
@@ -1106,6 +1238,9 @@ extern "C" const double* orc_schur_Shat_diag(const orc_solver* s) {
   return s->schur ? s->Shat_diag.data() : nullptr;
 }
 extern "C" const double* orc_schur_mS(const orc_solver* s) { return s->schur ? s->mS.data() : nullptr; }
+extern "C" int32_t orc_schur_np(const orc_solver* s) {
+  return s->schur ? (s->masked ? (int32_t)s->pidx.size() : s->A.n) : 0;
+}
 
 extern "C" int orc_vcycle(const orc_solver* s, const double* f, double* x) {
   if (s->p.precond == ORC_PC_NONE) return ORC_EINVAL;

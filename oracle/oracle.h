@@ -82,6 +82,14 @@ orc_mat* orc_csr_to_bsr(int32_t n, int32_t m, int32_t b, const int32_t* ptr, con
 /* ---- C1 SpMV: y = alpha A x + beta y (beta == 0 overwrites y, NaN included) ---- */
 int orc_spmv(const orc_mat* A, double alpha, const double* x, double beta, double* y);
 
+/* Schur pressure correction with a general scalar pressure mask (
+ * SPEC.md:631 pmask): pmask[q] != 0 marks scalar unknown q (of n_rows*b) as pressure.  The
+ * split is taken on the scalar expansion of A (reading R21); the U-solver hierarchy is
+ * scalar (b = 1, as V2).  p->precond must be ORC_PC_SCHUR; schur_shat 0 or 1. */
+int orc_setup_pmask(const orc_mat* A, const uint8_t* pmask, const orc_params* p, orc_solver** out);
+/* number of pressure unknowns of a Schur solver (the length of the S_hat / m_S vectors) */
+int32_t orc_schur_np(const orc_solver* s);
+
 /* ---- smoother pieces (for pins) ---- */
 /* x = S_l(f): the pre-smoother of level l from a zero initial guess (SPAI0 / Jacobi:
  * x = M f; ILU(0): the sweep-solved (LU)^-1 f), vectors at the solver's precision. */

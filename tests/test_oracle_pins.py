@@ -572,6 +572,89 @@ def test_schur_shat_variants_dense():
     assert not np.allclose(want[2], np.diag(np.diag(want[2])))  # the full S_hat has off-diagonal fill
 
 
+# ---- C10b Schur split by a general scalar pressure mask (R21) ----
+def _csr_from_dense(D):
+    ptr = np.zeros(D.shape[0] + 1, np.int32)
+    cols, vals = [], []
+    for i in range(D.shape[0]):
+        nz = np.flatnonzero(D[i])
+        if i not in nz:
+            nz = np.sort(np.append(nz, i))
+        cols.extend(nz.tolist())
+        vals.extend(D[i, nz].tolist())
+        ptr[i + 1] = len(cols)
+    return ptr, np.array(cols, np.int32), np.array(vals).reshape(-1, 1, 1)
+
+
+@pytest.mark.parametrize("h32", [0, 1])
+def test_pmask_interleaved_is_the_v2_split(rng, h32):
+    # mask = component 3 of every (u,v,w,p) block: the scalar split is V2's term for term
+    # (same A_u, same S_hat / m_S, same preconditioner bits)
+    n = 6
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    mask = (np.arange(4 * n ** 3) % 4 == 3)
+    kw = dict(precond=oracle.PC_SCHUR, solver=oracle.GMRES, coarse_enough=60, hier_f32=h32, vec_f32=h32)
+    Sm = oracle.Solver(A, pmask=mask, **kw)
+    S2 = oracle.Solver(A, schur_u_scalar=1, **kw)
+    assert Sm.levels == S2.levels >= 2
+    for a, b in zip(Sm.schur_vectors(), S2.schur_vectors()):
+        assert np.array_equal(a, b)
+    assert np.array_equal(Sm.schur_Au_amg().dense(), S2.schur_Au_amg().dense())
+    for _ in range(2):
+        r = rng.standard_normal(4 * n ** 3)
+        assert np.array_equal(Sm.precond(r), S2.precond(r))
+
+
+def test_pmask_scrambled_ordering_exact_schur_identity(rng):
+    # a scalar matrix whose pressure unknowns sit at random positions: with an exact
+    # (single-level) U-solve the PC satisfies (A z)_u = r_u and
+    # (A z)_p - r_p = (S m_S - I)(r_p - B A_u^-1 r_u), S = C - B A_u^-1 B^T (numpy dense);
+    # m_S is SPAI0 of Eq. 10's S_hat on the scrambled split
+    n = 3
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    Ad0 = oracle.Mat.from_arrays(ptr, col, val).dense()
+    N = Ad0.shape[0]
+    perm = rng.permutation(N)
+    Ad = Ad0[np.ix_(perm, perm)]
+    mask = (perm % 4 == 3)
+    A = oracle.Mat.from_arrays(*_csr_from_dense(Ad))
+    S = oracle.Solver(A, pmask=mask, precond=oracle.PC_SCHUR, hier_f32=0, vec_f32=0)
+    assert S.levels == 1
+    vel, pre = np.flatnonzero(~mask), np.flatnonzero(mask)
+    Au, Bt, B, C = Ad[np.ix_(vel, vel)], Ad[np.ix_(vel, pre)], Ad[np.ix_(pre, vel)], Ad[np.ix_(pre, pre)]
+    X = B @ np.diag(1.0 / np.diag(Au)) @ Bt
+    Sh = C - np.diag(np.diag(X))
+    d, mS = S.schur_vectors()
+    assert np.allclose(d, np.diag(Sh), rtol=1e-14, atol=0)
+    assert np.allclose(mS, np.diag(Sh) / (Sh ** 2).sum(axis=1), rtol=1e-13, atol=0)
+    Sx = C - B @ np.linalg.solve(Au, Bt)
+    for _ in range(3):
+        r = rng.standard_normal(N)
+        z = S.precond(r)
+        Az = Ad @ z
+        assert np.allclose(Az[vel], r[vel], atol=1e-10 * np.abs(r).max())
+        expect = (Sx @ np.diag(mS) - np.eye(len(pre))) @ (r[pre] - B @ np.linalg.solve(Au, r[vel]))
+        assert np.allclose(Az[pre] - r[pre], expect, atol=1e-10 * np.abs(r).max())
+
+
+def test_pmask_scrambled_solve_reaches_dense_solution(rng):
+    n = 6
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    Ad0 = oracle.Mat.from_arrays(ptr, col, val).dense()
+    perm = rng.permutation(Ad0.shape[0])
+    Ad = Ad0[np.ix_(perm, perm)]
+    A = oracle.Mat.from_arrays(*_csr_from_dense(Ad))
+    for solver in (oracle.GMRES, oracle.IDRS):
+        S = oracle.Solver(A, pmask=(perm % 4 == 3), precond=oracle.PC_SCHUR, solver=solver, coarse_enough=60,
+                          hier_f32=0, vec_f32=0)
+        assert S.levels >= 2
+        b = rng.standard_normal(Ad.shape[0])
+        r = S.solve(b, rtol=1e-10)
+        xd = np.linalg.solve(Ad, b)
+        assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
 def test_schur_shat_interior_closed_form():
     # Stokes generator: Shat_ii = -6 - (#neighbours) (1/(2h))^2 / (6/h^2) = -6 - k/24
     n = 6
