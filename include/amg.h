@@ -126,6 +126,16 @@ const char* amg_status_string(int status);
 int amg_setup(const amg_bsr* A /* host struct, device arrays */, const amg_params* p /* host */,
               void* stream, struct amg_handle** out /* host */);
 
+/* Schur pressure correction with a general scalar pressure mask:
+ * pmask (DEVICE, [n_block_rows * block_size] bytes, non-zero = pressure unknown) selects the
+ * pressure unknowns among the scalar unknowns of A in any order; the split is taken on the
+ * scalar expansion of A and the U-solver hierarchy is scalar (b = 1, as the paper's V2;
+ * DESIGN.md reading R21).  p->precond must be AMG_PC_SCHUR, p->schur_shat 0 or 1; single
+ * device (amg_setup_dist has no mask).  The mask may be freed after the call.  Errors as
+ * amg_setup; AMG_EINVAL also for an all-velocity or all-pressure mask. */
+int amg_setup_pmask(const amg_bsr* A, const uint8_t* pmask, const amg_params* p, void* stream,
+                    struct amg_handle** out);
+
 /* Solve A x = b.  b, x: device fp64 [n_block_rows*b]; x is read as x0 and overwritten.
  * Allocates nothing.  ||b|| = 0 returns x = 0, converged, relres 0. */
 int amg_solve(struct amg_handle* h, const double* b, double* x, double rtol, void* stream,
@@ -184,7 +194,8 @@ int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);
 int amg_level_export(struct amg_handle* h, int32_t level, int32_t which, int32_t* ptr, int32_t* col,
                      double* val);
 int amg_level_aggregates(struct amg_handle* h, int32_t level, int32_t* agg);
-/* Schur vectors: Shat diagonal and m_S (n_block_rows each), fp64 setup values */
+/* Schur vectors: Shat diagonal and m_S (n_block_rows each; amg_setup_pmask: one per pressure
+ * unknown, in ascending scalar order), fp64 setup values */
 int amg_schur_export(struct amg_handle* h, double* shat_diag, double* m_s);
 /* One V-cycle of the hierarchy on fp64 device vectors of the level-0 size. */
 int amg_vcycle(struct amg_handle* h, const double* f, double* x, void* stream);

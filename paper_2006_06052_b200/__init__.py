@@ -66,7 +66,7 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
            "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr", "amg_memory_report",
-           "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local"]
+           "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local", "amg_setup_pmask"]
 
 _lib = None
 
@@ -85,6 +85,7 @@ def lib():
             "amg_status_string": (ctypes.c_char_p, [i32]),
             "amg_last_error": (ctypes.c_char_p, []),
             "amg_setup": (i32, [P, P, P, P]),
+            "amg_setup_pmask": (i32, [P, P, P, P, P]),
             "amg_solve": (i32, [P, P, P, dbl, P, P]),
             "amg_solve_host": (i32, [P, P, P, dbl, P, P]),
             "amg_apply_precond": (i32, [P, P, P, P]),
@@ -281,12 +282,20 @@ class Solver:
     """amg_setup / amg_solve on a device BSR matrix (Listing 3: ``Solver S(A, prm)``)."""
 
     def __init__(self, A: BSR, params: amg_params | None = None, stream=None, comm=None,
-                 row_begin: int = 0, n_global: int | None = None, **kw):
+                 row_begin: int = 0, n_global: int | None = None, pmask=None, **kw):
+        """pmask: optional device uint8 tensor [n*b] (non-zero = pressure unknown) -> amg_setup_pmask."""
         self.params = params if params is not None else default_params(**kw)
         self.A = A
         d = A.desc()
         h = ctypes.c_void_p()
-        if comm is None:
+        self.n_pressure = None
+        if pmask is not None:
+            if comm is not None:
+                raise ValueError("pmask: single device only")
+            rc = lib().amg_setup_pmask(ctypes.byref(d), ctypes.c_void_p(pmask.data_ptr()), ctypes.byref(self.params),
+                                       _stream_ptr(stream), ctypes.byref(h))
+            self.n_pressure = int((pmask != 0).sum().item())
+        elif comm is None:
             rc = lib().amg_setup(ctypes.byref(d), ctypes.byref(self.params), _stream_ptr(stream), ctypes.byref(h))
         else:
             rc = lib().amg_setup_dist(ctypes.byref(d), row_begin, A.m if n_global is None else n_global,
@@ -371,7 +380,7 @@ class Solver:
 
     def schur_export(self):
         import numpy as np
-        n = self.A.n
+        n = self.A.n if self.n_pressure is None else self.n_pressure
         d, m = np.zeros(n), np.zeros(n)
         _check(lib().amg_schur_export(self.h, d.ctypes.data_as(ctypes.c_void_p), m.ctypes.data_as(ctypes.c_void_p)),
                "amg_schur_export")

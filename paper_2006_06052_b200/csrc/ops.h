@@ -60,6 +60,10 @@ void launch_schur_u(const Mat& BTm, const void* ru, const void* p, void* ru2, in
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,
                   cudaStream_t s, const double* scale_dev = nullptr);
 // K9' join (u, p) -> interleaved fp64 z (exact widening)
+void launch_mask_split(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const double* r,
+                       double scale, void* ru, void* rp, int xt, cudaStream_t s, const double* scale_dev = nullptr);
+void launch_mask_join(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const void* u, const void* p,
+                      int xt, void* z, int zt, cudaStream_t s);
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt,
                  cudaStream_t s);
 // convert a whole vector between dtypes (narrowing RNE / exact widening); scale applied in fp64

@@ -653,6 +653,95 @@ __global__ void k_schur_shat_full(int n, int nu, const int32_t* ptr, const int32
   ms[i] = sii / den;
 }
 
+// ---------------------------------------------------------------- S9b Schur split by a scalar mask
+// (reading R21) on the scalar expansion As of A: class flags -> exclusive scans give each
+// unknown its position in its class; rows split into A_u / B^T (u rows) and B / C (p rows),
+// columns renumbered, order kept.
+__global__ void k_mask_flags(int64_t N, const uint8_t* m, int32_t* iu, int32_t* ip) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  iu[q] = m[q] ? 0 : 1;
+  ip[q] = m[q] ? 1 : 0;
+}
+__global__ void k_mask_index(int64_t N, const uint8_t* m, const int32_t* iu, const int32_t* ip, int32_t* uidx,
+                             int32_t* pidx) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  if (m[q]) pidx[ip[q]] = (int32_t)q;
+  else uidx[iu[q]] = (int32_t)q;
+}
+__global__ void k_mask_count(int64_t N, const int32_t* sp, const int32_t* sc, const uint8_t* m, const int32_t* iu,
+                             const int32_t* ip, int32_t* cA, int32_t* cBT, int32_t* cB, int32_t* cC) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  int u = 0, p = 0;
+  for (int k = sp[q]; k < sp[q + 1]; ++k) (m[sc[k]] ? p : u) += 1;
+  if (m[q]) cB[ip[q]] = u, cC[ip[q]] = p;
+  else cA[iu[q]] = u, cBT[iu[q]] = p;
+}
+__global__ void k_mask_fill(int64_t N, const int32_t* sp, const int32_t* sc, const double* sv, const uint8_t* m,
+                            const int32_t* iu, const int32_t* ip, const int32_t* Ap, int32_t* Ac, double* Av,
+                            const int32_t* BTp, int32_t* BTc, double* BTv, const int32_t* Bp, int32_t* Bc, double* Bv,
+                            const int32_t* Cp, int32_t* Cc, double* Cv) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  const bool pr = m[q] != 0;
+  const int r = pr ? ip[q] : iu[q];
+  int o1 = pr ? Bp[r] : Ap[r], o2 = pr ? Cp[r] : BTp[r];
+  int32_t* c1 = pr ? Bc : Ac;
+  int32_t* c2 = pr ? Cc : BTc;
+  double* v1 = pr ? Bv : Av;
+  double* v2 = pr ? Cv : BTv;
+  for (int k = sp[q]; k < sp[q + 1]; ++k) {
+    const int j = sc[k];
+    if (m[j]) c2[o2] = ip[j], v2[o2++] = sv[k];
+    else c1[o1] = iu[j], v1[o1++] = sv[k];
+  }
+}
+// Eq. 10 on the scalar split (mode 1) or S_hat = C (mode 0); m_S = SPAI0 (the oracle's order)
+__global__ void k_schur_shat_scalar(int np, int mode, const int32_t* Bp, const int32_t* Bc, const double* Bv,
+                                    const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* BTp,
+                                    const int32_t* BTc, const double* BTv, const int32_t* Cp, const int32_t* Cc,
+                                    const double* Cv, double* shat, double* ms, int* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  const int kd = bsearch(Cc, Cp[i], Cp[i + 1], i);
+  if (kd < 0) {
+    set_err(err, AMG_EZERODIAG);
+    return;
+  }
+  double sum = 0.0;
+  for (int k = Bp[i]; k < Bp[i + 1] && mode == 1; ++k) {
+    const int J = Bc[k];
+    const int kJJ = bsearch(Ac, Ap[J], Ap[J + 1], J);
+    if (kJJ < 0) {
+      set_err(err, AMG_EZERODIAG);
+      return;
+    }
+    const int kJi = bsearch(BTc, BTp[J], BTp[J + 1], i);
+    if (kJi < 0) continue;
+    const double dg = Av[kJJ];
+    if (dg == 0.0) {
+      set_err(err, AMG_EZERODIAG);
+      return;
+    }
+    const double t = Bv[k] * (1.0 / dg);
+    sum = sum + t * BTv[kJi];
+  }
+  const double s = Cv[kd] - sum;
+  double den = 0.0;
+  for (int k = Cp[i]; k < Cp[i + 1]; ++k) {
+    const double v = (k == kd) ? s : Cv[k];
+    den = den + v * v;
+  }
+  if (den == 0.0) {
+    set_err(err, AMG_EZERODIAG);
+    return;
+  }
+  shat[i] = s;
+  ms[i] = s / den;
+}
+
 // ---------------------------------------------------------------- S11 coarse inverse
 template <int B>
 __global__ void k_densify(int n, const int32_t* ptr, const int32_t* col, const double* val, double* W, int N) {
@@ -947,7 +1036,63 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
   check_err(c, "diagonal");
 
   Mat Amg = A64;  // matrix the AMG hierarchy is built on
-  if (h.schur) {
+  if (h.schur && h.pmask_in) {  // general scalar pressure mask (R21)
+    h.masked = true;
+    const int64_t N = (int64_t)A64.n * b;
+    if (N >= INT32_MAX) fail(AMG_EINDEX_OVERFLOW, "scalar expansion of A");
+    int32_t* sp = c.tmp.alloc_n<int32_t>(N + 1);
+    k_expand_count<<<grid_for(N, kT), kT, 0, s>>>(A64.n, b, A64.ptr, A64.col, (const double*)A64.val, sp);
+    AMG_CK_LAUNCH();
+    const int64_t snnz = scan(c, sp, (int)N);
+    int32_t* sc = c.tmp.alloc_n<int32_t>(std::max<int64_t>(snnz, 1));
+    double* sv = c.tmp.alloc_n<double>(std::max<int64_t>(snnz, 1));
+    k_expand_fill<<<grid_for(N, kT), kT, 0, s>>>(A64.n, b, A64.ptr, A64.col, (const double*)A64.val, sp, sc, sv);
+    int32_t* iu = c.tmp.alloc_n<int32_t>(N + 1);
+    int32_t* ip = c.tmp.alloc_n<int32_t>(N + 1);
+    k_mask_flags<<<grid_for(N, kT), kT, 0, s>>>(N, h.pmask_in, iu, ip);
+    AMG_CK_LAUNCH();
+    const int64_t nu = scan(c, iu, (int)N), np = scan(c, ip, (int)N);
+    if (nu == 0 || np == 0) fail(AMG_EINVAL, "pressure mask selects no velocity or no pressure unknown");
+    h.nu_s = (int32_t)nu;
+    h.np_s = (int32_t)np;
+    h.uidx = h.arena.alloc_n<int32_t>(nu);
+    h.pidx = h.arena.alloc_n<int32_t>(np);
+    k_mask_index<<<grid_for(N, kT), kT, 0, s>>>(N, h.pmask_in, iu, ip, h.uidx, h.pidx);
+    int32_t* cA = c.tmp.alloc_n<int32_t>(nu + 1);
+    int32_t* cBT = c.tmp.alloc_n<int32_t>(nu + 1);
+    int32_t* cB = c.tmp.alloc_n<int32_t>(np + 1);
+    int32_t* cC = c.tmp.alloc_n<int32_t>(np + 1);
+    k_mask_count<<<grid_for(N, kT), kT, 0, s>>>(N, sp, sc, h.pmask_in, iu, ip, cA, cBT, cB, cC);
+    AMG_CK_LAUNCH();
+    const int64_t zA = scan(c, cA, (int)nu), zBT = scan(c, cBT, (int)nu), zB = scan(c, cB, (int)np),
+                  zC = scan(c, cC, (int)np);
+    auto mk = [&](int32_t* ptr, int n, int m, int64_t nnz) {
+      Mat M;
+      M.n = n, M.m = m, M.b = 1, M.nnz = nnz, M.vt = AMG_F64, M.ptr = ptr;
+      M.col = c.tmp.alloc_n<int32_t>(std::max<int64_t>(nnz, 1));
+      M.val = c.tmp.alloc_n<double>(std::max<int64_t>(nnz, 1));
+      return M;
+    };
+    Mat Au = mk(cA, (int)nu, (int)nu, zA), BT = mk(cBT, (int)nu, (int)np, zBT), Bq = mk(cB, (int)np, (int)nu, zB),
+        Cq = mk(cC, (int)np, (int)np, zC);
+    k_mask_fill<<<grid_for(N, kT), kT, 0, s>>>(N, sp, sc, sv, h.pmask_in, iu, ip, Au.ptr, Au.col, (double*)Au.val,
+                                                BT.ptr, BT.col, (double*)BT.val, Bq.ptr, Bq.col, (double*)Bq.val,
+                                                Cq.ptr, Cq.col, (double*)Cq.val);
+    AMG_CK_LAUNCH();
+    h.shat64 = h.arena.alloc_n<double>(np);
+    h.mS64 = h.arena.alloc_n<double>(np);
+    k_schur_shat_scalar<<<grid_for(np, kT), kT, 0, s>>>(
+        (int)np, p.schur_shat, Bq.ptr, Bq.col, (const double*)Bq.val, Au.ptr, Au.col, (const double*)Au.val, BT.ptr,
+        BT.col, (const double*)BT.val, Cq.ptr, Cq.col, (const double*)Cq.val, h.shat64, h.mS64, c.err);
+    AMG_CK_LAUNCH();
+    check_err(c, "Schur complement approximation (pressure mask)");
+    h.mS = h.arena.alloc(np * dtype_size(h.vt));
+    launch_convert(np, h.mS64, AMG_F64, h.mS, h.vt, 1.0, s);
+    h.Bm = solve_copy(h, Bq, s);
+    h.BTm = solve_copy(h, BT, s);
+    h.Bm.fast32 = h.BTm.fast32 = false;  // fp64 accumulation of every product (as the block Schur views)
+    Amg = Au;
+  } else if (h.schur) {
     if (b != 4) fail(AMG_EINVAL, "Schur pressure correction needs 4x4 blocks (u,v,w,p)");
     const int nu = b - 1;
     h.nu = nu;
@@ -1014,8 +1159,9 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
   // slab of every row (rank-local aggregation); a scalar U-solver
   // hierarchy has nu scalar rows per block row
   std::vector<int64_t> bounds = bounds0;
-  if (h.schur && p.schur_u_scalar)
+  if (h.schur && p.schur_u_scalar && !h.masked)
     for (int64_t& v : bounds) v *= h.nu;
+  if (h.masked) bounds = {0, (int64_t)h.nu_s};  // single device
   const int nparts = (int)bounds.size() - 1;
   h.lbounds.clear();
   h.lbounds.push_back(bounds);

@@ -63,8 +63,9 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
   AMG_CK(cudaMallocHost(&h.hscal, sizeof(double) * 256));
   if (h.schur) {
     const size_t xs = dtype_size(h.xt);
-    h.rp = h.arena.alloc(std::max(h.n, 1) * xs);
-    h.pp = h.arena.alloc(std::max(h.n + h.halo0.nghost, 1) * xs);
+    const int np = h.masked ? h.np_s : h.n;
+    h.rp = h.arena.alloc(std::max(np, 1) * xs);
+    h.pp = h.arena.alloc(std::max(np + h.halo0.nghost, 1) * xs);
   }
   AMG_CK(cudaStreamCreateWithFlags(&h.work, cudaStreamNonBlocking));
   if (h.comm) {
@@ -106,11 +107,12 @@ int check_params(const amg_params* p) {
 }
 
 Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s,
-                     bool workspace) {
+                     bool workspace, const uint8_t* pmask) {
   auto t0 = std::chrono::steady_clock::now();
   Handle* h = new Handle;
   try {
     h->p = *p;
+    h->pmask_in = pmask;
     h->vt = p->hier_dtype;
     h->xt = p->vcycle_vec_dtype;
     h->n = src.n;
@@ -119,7 +121,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     h->schur = p->precond == AMG_PC_SCHUR;
     h->pc = p->schur_p_component;
     h->amg_active = p->precond != AMG_PC_NONE;
-    if (h->schur && (h->pc < 0 || h->pc >= h->b)) fail(AMG_EINVAL, "schur_p_component out of range");
+    if (h->schur && !pmask && (h->pc < 0 || h->pc >= h->b)) fail(AMG_EINVAL, "schur_p_component out of range");
     // library-owned fp64 copy of A (setup in own structures, then moved)
     Mat& M = h->A;
     M = src;
@@ -135,7 +137,8 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
     make_tma_plan(M, s, &h->arena);
     if (h->amg_active) setup_build(*h, M, bounds, s);
-    if (h->schur) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
+    if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
+    h->pmask_in = nullptr;
     if (workspace) alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));
@@ -176,6 +179,21 @@ using namespace amgb;
   }
 
 extern "C" {
+
+int amg_setup_pmask(const amg_bsr* A, const uint8_t* pmask, const amg_params* p, void* stream,
+                    struct amg_handle** out) {
+  AMG_GUARD_BEGIN
+  if (!A || !p || !out || !pmask) return AMG_EINVAL;
+  int rc = validate_bsr(A, true);
+  if (rc != AMG_OK) return rc;
+  rc = check_params(p);
+  if (rc != AMG_OK) return rc;
+  if (p->precond != AMG_PC_SCHUR || p->schur_shat == 2) return AMG_EINVAL;
+  *out = reinterpret_cast<amg_handle*>(
+      build_handle(view_of(A), p, {0, (int64_t)A->n_block_rows}, (cudaStream_t)stream, true, pmask));
+  return AMG_OK;
+  AMG_GUARD_END
+}
 
 int amg_setup(const amg_bsr* A, const amg_params* p, void* stream, struct amg_handle** out) {
   AMG_GUARD_BEGIN
@@ -325,8 +343,9 @@ int amg_schur_export(struct amg_handle* hh, double* shat_diag, double* m_s) {
   Handle* h = reinterpret_cast<Handle*>(hh);
   if (!h || !h->schur || !shat_diag || !m_s) return AMG_EINVAL;
   AMG_CK(cudaDeviceSynchronize());
-  AMG_CK(cudaMemcpy(shat_diag, h->shat64, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
-  AMG_CK(cudaMemcpy(m_s, h->mS64, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+  const int np = h->masked ? h->np_s : h->n;
+  AMG_CK(cudaMemcpy(shat_diag, h->shat64, sizeof(double) * np, cudaMemcpyDeviceToHost));
+  AMG_CK(cudaMemcpy(m_s, h->mS64, sizeof(double) * np, cudaMemcpyDeviceToHost));
   return AMG_OK;
   AMG_GUARD_END
 }
@@ -364,7 +383,8 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
     v[2] += sell(L.A) + sell(L.P) + sell(L.R) + sell(L.Lf) + sell(L.Uf);
     v[3] += (int64_t)L.A.n * L.A.b * L.A.b * dtype_size(h->vt);
   }
-  if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
+  if (h->schur && h->masked) v[4] = mat(h->Bm) + mat(h->BTm) + (int64_t)h->np_s * dtype_size(h->vt);
+  else if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
   v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
   const int64_t N = (int64_t)h->n * h->b;
   v[6] = 8LL * N * ((int64_t)h->vec.size() + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +

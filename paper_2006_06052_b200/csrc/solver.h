@@ -70,6 +70,12 @@ struct Handle {
   void *Bv = nullptr, *BTv = nullptr, *mS = nullptr;
   Mat Bm, BTm;                     // views of B / B^T on A's pattern (1 x nu / nu x 1 blocks)
   double *shat64 = nullptr, *mS64 = nullptr;
+  // general scalar pressure mask (amg_setup_pmask, R21): Bm / BTm are then scalar (b = 1)
+  // solve copies of B (np x nu) and B^T (nu x np); uidx / pidx the unknowns of each class
+  const uint8_t* pmask_in = nullptr;  // setup only
+  bool masked = false;
+  int32_t np_s = 0, nu_s = 0;
+  int32_t *uidx = nullptr, *pidx = nullptr;
   void *ru = nullptr, *rp = nullptr, *us = nullptr, *pp = nullptr, *ru2 = nullptr, *uu = nullptr;
   // AMG hierarchy (on A, or on A_u for Schur)
   int bh = 0;
@@ -121,7 +127,7 @@ void alloc_workspace(Handle& h, cudaStream_t s);
 // workspace = false: hierarchy only (the replicated global handle of amg_setup_dist, whose
 // slabs are copied out: no global Krylov basis on every rank)
 Handle* build_handle(const Mat& view, const amg_params* p, const std::vector<int64_t>& bounds, cudaStream_t s,
-                     bool workspace = true);
+                     bool workspace = true, const uint8_t* pmask = nullptr);
 // dist.cu
 void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_t s);
 // launch(r0, r1) over all block rows of A, x's ghosts exchanged first -- on the handle's

@@ -664,6 +664,19 @@ void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int
 void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s) {
   const int n = Bm.n, vt = Bm.vt;
   if (n == 0) return;
+  if (Bm.b == 1 && Bm.br == 0) {  // scalar B of the pressure-mask split (R21)
+    ProfScope ps_(prof_name("schur_p", 1, vt, xt),
+                  mat_bytes(Bm) + (double)n * dtype_size(vt) + (double)Bm.m * dtype_size(xt) + 2.0 * n * dtype_size(xt), s);
+    dispatch_t(vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        launch_lane<1, 1, V, X>(Bm, (const X*)us, LEpiSchurP<V, X>{(const V*)mS, (const X*)rp, (X*)p}, s);
+      });
+    });
+    AMG_CK_LAUNCH();
+    return;
+  }
   if (Bm.bc != 3) fail(AMG_EINVAL, "Schur split supports 3 velocity components");
   ProfScope ps_(prof_name("schur_p", 3, vt, xt),
                 ((double)Bm.nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + (double)n * dtype_size(vt) + 5.0 * n * dtype_size(xt), s);
@@ -780,6 +793,52 @@ __global__ void __launch_bounds__(256) k_join4(int n, const float* __restrict__ 
       o[1] = make_double2(su[3 * threadIdx.x + 2], pv);
     }
   }
+}
+
+// pressure-mask split / join (R21): ru[i] = narrow(scale r[uidx[i]]), rp[i] = narrow(scale r[pidx[i]]);
+// z[uidx[i]] = u[i], z[pidx[i]] = p[i]
+template <typename X>
+__global__ void k_mask_split(int nu, int np, const int32_t* __restrict__ uidx, const int32_t* __restrict__ pidx,
+                             const double* __restrict__ r, double scale_v, const double* scale_d, X* __restrict__ ru,
+                             X* __restrict__ rp) {
+  const double scale = scale_d ? *scale_d : scale_v;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nu) ru[t] = to_out<X>(r[uidx[t]] * scale);
+  else if (t < (int64_t)nu + np) rp[t - nu] = to_out<X>(r[pidx[t - nu]] * scale);
+}
+template <typename X, typename Z>
+__global__ void k_mask_join(int nu, int np, const int32_t* __restrict__ uidx, const int32_t* __restrict__ pidx,
+                            const X* __restrict__ u, const X* __restrict__ p, Z* __restrict__ z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nu) z[uidx[t]] = (Z)u[t];
+  else if (t < (int64_t)nu + np) z[pidx[t - nu]] = (Z)p[t - nu];
+}
+
+void launch_mask_split(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const double* r,
+                       double scale, void* ru, void* rp, int xt, cudaStream_t s, const double* scale_dev) {
+  const int64_t N = (int64_t)nu + np;
+  if (N == 0) return;
+  ProfScope ps_(prof_name("split", 1, AMG_F64, xt), (double)N * (8.0 + 4.0 + dtype_size(xt)), s);
+  dispatch_t(xt, [&](auto xx) {
+    using X = decltype(xx);
+    k_mask_split<X><<<grid_for(N, 256), 256, 0, s>>>(nu, np, uidx, pidx, r, scale, scale_dev, (X*)ru, (X*)rp);
+  });
+  AMG_CK_LAUNCH();
+}
+
+void launch_mask_join(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const void* u, const void* p,
+                      int xt, void* z, int zt, cudaStream_t s) {
+  const int64_t N = (int64_t)nu + np;
+  if (N == 0) return;
+  ProfScope ps_(prof_name("join", 1, zt, xt), (double)N * (4.0 + dtype_size(zt) + dtype_size(xt)), s);
+  dispatch_t(xt, [&](auto xx) {
+    using X = decltype(xx);
+    dispatch_t(zt, [&](auto zz) {
+      using Z = decltype(zz);
+      k_mask_join<X, Z><<<grid_for(N, 256), 256, 0, s>>>(nu, np, uidx, pidx, (const X*)u, (const X*)p, (Z*)z);
+    });
+  });
+  AMG_CK_LAUNCH();
 }
 
 void launch_split(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt,

@@ -101,6 +101,15 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
     launch_convert(N, x, h.xt, z, zt, 1.0, s);
     return;
   }
+  if (h.masked) {  // general scalar pressure mask (R21): the same steps on the scalar split
+    launch_mask_split(h.nu_s, h.np_s, h.uidx, h.pidx, r, scale, f0, h.rp, h.xt, s, scale_dev);
+    void* us = vcycle_run(h, 0, s);
+    launch_schur_p(h.Bm, h.mS, h.rp, us, h.pp, h.xt, s);     // p = m_S o (r_p - B u*)
+    launch_residual(h.BTm, f0, h.pp, f0, h.xt, s);           // r_u' = r_u - B^T p (in place)
+    void* u = vcycle_run(h, 0, s);
+    launch_mask_join(h.nu_s, h.np_s, h.uidx, h.pidx, u, h.pp, h.xt, z, zt, s);
+    return;
+  }
   launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s, scale_dev);                      // K9
   void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
   halo_exchange(h, h.halo0, us, h.xt, h.nu, s);
@@ -189,6 +198,13 @@ double precond_bytes(const Handle& h) {
   const double sx = (double)dtype_size(h.xt), sv = (double)dtype_size(h.vt);
   if (!h.amg_active) return (double)N * 16.0;
   if (!h.schur) return vcycle_bytes(h) + (double)N * (8.0 + sx) * 2.0;
+  if (h.masked) {
+    const double nu = h.nu_s, np = h.np_s;
+    double t = 2.0 * vcycle_bytes(h) + (double)N * (12.0 + sx) + (double)N * (4.0 + sx + 8.0);  // split, join
+    t += mat_bytes(h.Bm, h.vt) + np * sv + nu * sx + 2.0 * np * sx;                               // K10
+    t += mat_bytes(h.BTm, h.vt) + np * sx + 2.0 * nu * sx;                                        // K11
+    return t;
+  }
   const double n = (double)h.n, nnz = (double)h.A.nnz;
   double t = 2.0 * vcycle_bytes(h);
   t += (double)N * 8.0 + (double)N * sx;                        // split

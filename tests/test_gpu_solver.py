@@ -336,6 +336,85 @@ def test_solve_interleaved_copies_everywhere(amg, envvars, solver):
     assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
 
 
+# ---- Schur split by a general scalar pressure mask (amg_setup_pmask, R21) ----
+def _csr_from_dense(D):
+    ptr = np.zeros(D.shape[0] + 1, np.int32)
+    cols, vals = [], []
+    for i in range(D.shape[0]):
+        nz = np.flatnonzero(D[i])
+        if i not in nz:
+            nz = np.sort(np.append(nz, i))
+        cols.extend(nz.tolist())
+        vals.extend(D[i, nz].tolist())
+        ptr[i + 1] = len(cols)
+    return ptr, np.array(cols, np.int32), np.array(vals).reshape(-1, 1, 1)
+
+
+def _pmask_pair(amg, ptr, col, val, mask, hier32, **kw):
+    A = amg.BSR.from_numpy(ptr, col, val)
+    gp = amg.default_params(hier_dtype=amg.F32 if hier32 else amg.F64,
+                            vcycle_vec_dtype=amg.F32 if hier32 else amg.F64, precond=1, **kw)
+    S = amg.Solver(A, gp, pmask=torch.as_tensor(mask.astype(np.uint8), device="cuda"))
+    op = oracle.default_params(hier_f32=int(hier32), vec_f32=int(hier32), precond=oracle.PC_SCHUR,
+                               **{ORC_OF[k]: v for k, v in kw.items() if k in ORC_OF})
+    O = oracle.Solver(oracle.Mat.from_arrays(ptr, col, val), op, pmask=mask)
+    return A, S, O
+
+
+def _scrambled_stokes(n, seed=5):
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    Ad0 = oracle.Mat.from_arrays(ptr, col, val).dense()
+    perm = np.random.default_rng(seed).permutation(Ad0.shape[0])
+    Ad = Ad0[np.ix_(perm, perm)]
+    return (*_csr_from_dense(Ad), perm % 4 == 3)
+
+
+PMASK_CASES = [
+    ("interleaved-f64", False, 10, dict(solver=2, coarse_enough=40)),
+    ("interleaved-f32-idrs", True, 16, dict(solver=3)),
+    ("scrambled-f64", False, 8, dict(solver=2, coarse_enough=60, scrambled=True)),
+    ("scrambled-f32-ilu0", True, 10, dict(solver=3, smoother=2, scrambled=True)),
+]
+
+
+@pytest.mark.parametrize("name,h32,n,kw", PMASK_CASES, ids=[c[0] for c in PMASK_CASES])
+def test_pmask_parity(amg, rng, name, h32, n, kw):
+    kw = dict(kw)
+    if kw.pop("scrambled", False):
+        ptr, col, val, mask = _scrambled_stokes(n)
+    else:
+        ptr, col, val = gen.matrix(gen.STOKES, n)
+        mask = np.arange(4 * n ** 3) % 4 == 3
+    A, S, O = _pmask_pair(amg, ptr, col, val, mask, h32, **kw)
+    check_hierarchy(S, O, h32)
+    d, m = S.schur_export()
+    od, om = O.schur_vectors()
+    assert np.array_equal(d, od) and np.array_equal(m, om)
+    N = len(mask)
+    for _ in range(2):
+        r = rng.standard_normal(N)
+        z = S.apply_precond(torch.as_tensor(r, device="cuda"), torch.zeros(N, dtype=torch.float64, device="cuda"))
+        torch.cuda.synchronize()
+        assert relerr(z.cpu().numpy(), O.precond(r)) <= (1e-5 if h32 else 1e-10)
+    bvec = rng.standard_normal(N)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
+
+
+def test_pmask_errors(amg):
+    ptr, col, val = gen.matrix(gen.STOKES, 4)
+    A = amg.BSR.from_numpy(ptr, col, val)
+    N = 4 * 64
+    for mask, kw in ((np.zeros(N), {}), (np.ones(N), {}), (np.arange(N) % 4 == 3, dict(schur_shat=2)),
+                     (np.arange(N) % 4 == 3, dict(precond=0))):
+        gp = amg.default_params(**({"precond": 1} | kw))
+        with pytest.raises(amg.AmgError) as e:
+            amg.Solver(A, gp, pmask=torch.as_tensor(mask.astype(np.uint8), device="cuda"))
+        assert e.value.status == amg.EINVAL
+
+
 @pytest.mark.parametrize("solver", [0, 1, 2, 3])
 def test_maxiter_not_converged(amg, solver):
     # maxiter reached: AMG_NOT_CONVERGED, the report filled, x the last iterate -- the same
