@@ -488,9 +488,8 @@ __global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const i
 }
 
 // ---------------------------------------------------------------- interleaved row-per-lane
-// Opt-in (AMG_SELLR=1/2 or AMG_LANE_VAR=8; measured slower than the row-component lanes
-// and the sliced copy on every level of the cfg-5 hierarchy).  The solve
-// copy interleaves 32 consecutive block rows (one slice, one warp; lane = row).  Each
+// Default for the fp32 hierarchy's 6..64-block rows (spmv.cu make_tma_plan).
+// The solve copy interleaves 32 consecutive block rows (one slice, one warp; lane = row).  Each
 // row's blocks are flattened ([block][i][c], padded to the slice's longest row with zero
 // blocks) and cut into W-element vectors (W = 16 bytes / sizeof(V)); vector t of lane l
 // sits at (vptr[s] + t) * 32 + l, so every value load of the warp is 32 x 16 contiguous
@@ -508,13 +507,14 @@ struct SellrShape {
   static constexpr int GB = W / gcd(E, W);  // blocks per step: lcm(E, W) / E
   static constexpr int NV = GB * E / W;     // vectors per step
 };
-// resident blocks per SM: a step's values take NV * W registers; above 16 words the
-// kernel needs more than 64 registers per thread (3 blocks: 85; fp64 products of 36
-// fp32 values, 2 blocks: 128)
+// resident blocks per SM: a step's values take NV * W registers.  Above 18 words (3x3 fp32,
+// 36 values) the register budget is 128 (2 blocks): with 80 ptxas interleaved each 16-byte
+// load with its FMAs (one load in flight per thread, 4.8 TB/s on A_0); with 128 all loads of
+// a step issue first (5.65 TB/s)
 template <int B, int W, typename V, bool FAST>
 constexpr int sellr_min_blocks() {
   constexpr int words = SellrShape<B, W>::NV * W * (int)sizeof(V) / 4;
-  return words <= 16 ? 4 : (FAST || words <= 18 ? 3 : 2);
+  return words <= 16 ? 4 : (words <= 18 ? 3 : 2);
 }
 
 template <int W, typename V>
@@ -570,16 +570,17 @@ __device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32
 
 template <int B, int W, typename V, typename X, bool FAST, class EPI>
 __global__ void __launch_bounds__(256, (sellr_min_blocks<B, W, V, FAST>())) k_bsr_sellr(
-    int n, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
+    int n, int s0, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
     const int32_t* __restrict__ perm, const int32_t* __restrict__ scol, const V* __restrict__ sval,
     const X* __restrict__ x, EPI epi) {
+  // slices [s0, nslices) (a row range of 32-aligned bounds: the distributed interior / boundary split)
   using S = SellrShape<B, W>;
   constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t nvb = ((int64_t)nslices + 7) / 8;
+  const int64_t nvb = ((int64_t)nslices - s0 + 7) / 8;
   double dacc[ND] = {};
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
-    const int s = (int)(vb * 8 + w);
+    const int s = s0 + (int)(vb * 8 + w);
     double acc[B] = {};
     if (s < nslices) {
       const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;

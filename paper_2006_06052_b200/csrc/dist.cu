@@ -82,7 +82,11 @@ void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, in
     launch(0, A.n);
     return;
   }
-  if (off || H.int_hi <= H.int_lo || A.lane_var > kLaneCN4 || A.tma_grid > 0 || !h.comm_s) {
+  // the interleaved copy computes whole 32-row slices: round the interior inward
+  int lo = H.int_lo, hi = H.int_hi;
+  if (A.lane_var == kLaneSellR) lo = (lo + 31) / 32 * 32, hi = hi / 32 * 32;
+  const bool sellr_ok = A.lane_var == kLaneSellR && hi > lo && sellr_range_ok(A, lo, hi);
+  if (off || hi <= lo || (A.lane_var > kLaneCN4 && !sellr_ok) || A.tma_grid > 0 || !h.comm_s) {
     halo_exchange(h, H, x, dt, b, s);
     launch(0, A.n);
     return;
@@ -111,10 +115,10 @@ void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, in
   }
   h.comm->group_end(h.comm_s);
   AMG_CK(cudaEventRecord(h.ev_halo, h.comm_s));
-  launch(H.int_lo, H.int_hi);  // interior rows: no ghost read
+  launch(lo, hi);  // interior rows: no ghost read
   AMG_CK(cudaStreamWaitEvent(s, h.ev_halo, 0));
-  launch(0, H.int_lo);
-  launch(H.int_hi, A.n);
+  launch(0, lo);
+  launch(hi, A.n);
 }
 
 void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s) {

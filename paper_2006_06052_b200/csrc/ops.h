@@ -38,6 +38,8 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
 // ILU(0) U sweep (R20): xo = xb + D^-1 (y - U_s z); xb == nullptr: from zero
 void launch_ilu_usweep(const Mat& U, const void* Dinv, const void* y, const void* z, const void* xb, void* xo, int xt,
                        cudaStream_t s);
+// the interleaved copy (k_bsr_sellr) runs a row range only on whole unpermuted slices
+bool sellr_range_ok(const Mat& A, int r0, int r1);
 // K4a x = M f
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
                     cudaStream_t s);

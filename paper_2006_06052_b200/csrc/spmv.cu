@@ -278,7 +278,12 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
-    const int sellr_mode = env_int("AMG_SELLR", 0);  // 0: never (default, measured slower), 1: fp32 hierarchy, 2: every square matrix
+    // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) fp32-hierarchy matrices with
+    // 6..64 blocks per row on >= 64 slices per SM (cfg 5: A_0 5.65, A_1 / R_0 6.4-6.5 TB/s vs
+    // 4.8 / 5.4 for the row lanes / sliced copy; the 3.6-block prolongators stay on the COLS
+    // lanes, 3.3 vs 3.8), 2 every square matrix with an arena
+    const int sellr_mode = env_int("AMG_SELLR", 1);
+    const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 6);
     // sliced copies need the builder's arena and square b x b blocks
     if (arena && square && forced == kLaneSellR) {
       build_sellr(A, *arena, s);
@@ -290,7 +295,8 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
       // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
       const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
       const bool many = (int64_t)A.n / 32 >= min_slices;
-      if (sellr_mode == 2 || (sellr_mode == 1 && many && per_row <= hi && A.vt == AMG_F32 && A.fast32))
+      if (sellr_mode == 2 ||
+          (sellr_mode == 1 && many && per_row >= sellr_min_row && per_row <= hi && A.vt == AMG_F32 && A.fast32))
         build_sellr(A, *arena, s);
       else if (per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices && !env_int("AMG_NO_SELL", 0))
         build_sell(A, *arena, s);
@@ -363,16 +369,23 @@ static void dispatch_lane(int var, F&& f) {
   }
 }
 
+bool sellr_range_ok(const Mat& A, int r0, int r1) {
+  return A.lane_var == kLaneSellR && !A.sell_perm && r0 % 32 == 0 && (r1 >= A.n || r1 % 32 == 0);
+}
+
 template <int B, typename V, typename X, class EPI>
-static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, unsigned grid) {
+static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, unsigned grid, int s0 = 0,
+                         int s1 = -1) {
+  if (s1 < 0) s1 = A.sell_ns;
+  if (s1 <= s0) return;
   auto go = [&](auto Wc) {
     constexpr int W = decltype(Wc)::value;
     constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
     if (can_fast && fast)
-      k_bsr_sellr<B, W, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_vptr, A.sell_perm,
+      k_bsr_sellr<B, W, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm,
                                                                     A.sell_col, (const V*)A.sell_val, x, epi);
     else
-      k_bsr_sellr<B, W, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, A.sell_ns, A.sell_ptr, A.sell_vptr, A.sell_perm,
+      k_bsr_sellr<B, W, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm,
                                                                   A.sell_col, (const V*)A.sell_val, x, epi);
   };
   if constexpr (std::is_same_v<V, float>) {
@@ -387,12 +400,16 @@ template <int BR, int BC, typename V, typename X, class EPI>
 static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r0 = 0, int r1 = -1) {
   if (r1 < 0) r1 = A.n;
   if (r1 <= r0) return;
-  if ((r0 > 0 || r1 < A.n) && (A.lane_var > kLaneCN4 || A.tma_grid > 0))
+  const bool ranged = r0 > 0 || r1 < A.n;
+  if (ranged && A.lane_var == kLaneSellR && !sellr_range_ok(A, r0, r1))
+    fail(AMG_EINVAL, "interleaved copy: row ranges must be 32-aligned and unpermuted");
+  if (ranged && ((A.lane_var > kLaneCN4 && A.lane_var != kLaneSellR) || A.tma_grid > 0))
     fail(AMG_EINVAL, "row ranges need a row-lane plan");
   constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
   if constexpr (BR == BC && BR >= 2) {
     if (A.lane_var == kLaneSellR) {
-      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, (unsigned)((A.sell_ns + 7) / 8));
+      const int s0 = r0 / 32, s1 = r1 >= A.n ? A.sell_ns : r1 / 32;
+      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, (unsigned)std::max((s1 - s0 + 7) / 8, 1), s0, s1);
       return;
     }
     if (A.lane_var == kLaneSell) {

@@ -138,3 +138,17 @@ def test_halo_overlap_is_exact(amg, envvars):
         runs.append((x, out[0][0].iters))
     assert runs[0][1] == runs[1][1]
     assert np.array_equal(runs[0][0], runs[1][0])
+
+
+def test_halo_overlap_interleaved_copy_is_exact(amg, envvars):
+    # the same with the interleaved row-per-lane copy on every fp32 level (whole 32-row
+    # slices: the interior rounded inward), unsorted slices so row ranges apply
+    envvars(AMG_SELL_MIN_SLICES=1, AMG_SELL_NO_SORT=1)
+    runs = []
+    for off in (False, True):
+        if off:
+            envvars(AMG_NO_OVERLAP=1)
+        out, x, relres, _ = run_dist(amg, 2, gen.STOKES, 16, gen.RHS_LID_NOISE, solver=2, precond=1)
+        runs.append((x, out[0][0].iters))
+    assert runs[0][1] == runs[1][1]
+    assert np.array_equal(runs[0][0], runs[1][0])
