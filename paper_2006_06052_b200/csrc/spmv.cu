@@ -278,10 +278,11 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
-    // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) fp32-hierarchy matrices with
-    // 6..64 blocks per row on >= 64 slices per SM (cfg 5: A_0 5.65, A_1 / R_0 6.4-6.5 TB/s vs
-    // 4.8 / 5.4 for the row lanes / sliced copy; the 3.6-block prolongators stay on the COLS
-    // lanes, 3.3 vs 3.8), 2 every square matrix with an arena
+    // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) square-block matrices with
+    // 6..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
+    // (cfg 5 / cfg 2): A_0 5.65, A_1 / R_0 6.4-6.5, outer 4x4 fp64 7.07, cfg-2 4x4 fp32 x fp64
+    // 6.85, fp64 7.03 TB/s vs 4.8 / 5.4 / 6.74 / 6.07 / 6.70 for the row lanes / sliced copy;
+    // the 3.6-block prolongators stay on the COLS lanes (3.3 vs 3.8)
     const int sellr_mode = env_int("AMG_SELLR", 1);
     const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 6);
     // sliced copies need the builder's arena and square b x b blocks
@@ -295,8 +296,7 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
       // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
       const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
       const bool many = (int64_t)A.n / 32 >= min_slices;
-      if (sellr_mode == 2 ||
-          (sellr_mode == 1 && many && per_row >= sellr_min_row && per_row <= hi && A.vt == AMG_F32 && A.fast32))
+      if (sellr_mode == 2 || (sellr_mode == 1 && many && per_row >= sellr_min_row && per_row <= hi))
         build_sellr(A, *arena, s);
       else if (per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices && !env_int("AMG_NO_SELL", 0))
         build_sell(A, *arena, s);

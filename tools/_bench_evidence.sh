@@ -9,17 +9,17 @@ python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > gpurun_out/${
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_l.log 2>&1
 tail -2 /tmp/ncu_l.log
 rm -f /tmp/top.ncu-rep /tmp/spmv.ncu-rep
-ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_lane<\(int\)4, \(int\)4.*double, float.*LEpiSpmv<double>" -c 1 -o /tmp/top python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_top.log 2>&1
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr<\(int\)4.*double, float.*LEpiSpmv<double>" -c 1 -o /tmp/top python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_top.log 2>&1
 tail -2 /tmp/ncu_top.log
 ncu -i /tmp/top.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_top_details.csv
 ncu -i /tmp/top.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_top_raw.csv
 rm -f /tmp/smooth.ncu-rep
-ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_lane.*LEpiSmooth<float, float>" -c 1 -o /tmp/smooth python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_smooth.log 2>&1
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr.*LEpiSmooth<float, float>" -s 1 -c 1 -o /tmp/smooth python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_smooth.log 2>&1
 tail -2 /tmp/ncu_smooth.log
 ncu -i /tmp/smooth.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_smooth_details.csv
 ncu -i /tmp/smooth.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_smooth_raw.csv
 python tools/spmv_probe.py 4 1 0 5 > gpurun_out/${TAG}_spmv_plain.log 2>&1 || exit 1
-ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sell" -s 2 -c 1 -o /tmp/spmv python tools/spmv_probe.py 4 1 0 5 > /tmp/ncu_spmv.log 2>&1
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr" -s 2 -c 1 -o /tmp/spmv python tools/spmv_probe.py 4 1 0 5 > /tmp/ncu_spmv.log 2>&1
 tail -2 /tmp/ncu_spmv.log
 ncu -i /tmp/spmv.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_spmv_details.csv
 ncu -i /tmp/spmv.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_spmv_raw.csv
