@@ -2,6 +2,9 @@
 
   python tools/ncu_launch_summary.py gpurun_out/launches.csv [top]
 Per-launch ncu times are cold-cache and serialised: compare SHARES of the step, not absolutes.
+Launches are grouped by kernel AND grid size, so one template instantiation used on two
+hierarchy levels (e.g. the level-0 and level-1 smoother) shows as two lines, as in bench.py's
+per-kernel CUDA-event profile.
 """
 import collections
 import csv
@@ -18,6 +21,7 @@ for r in csv.DictReader(rows):
         continue
     name = r["Kernel Name"]
     name = re.sub(r"\(.*$", "", name)  # drop the parameter list, keep template args
+    name = f"{name}  grid {r.get('Grid Size', '?').split(',')[0].strip('( ')}"
     v = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "ns")
     v *= {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(unit, 1e-6)
@@ -27,4 +31,7 @@ T = sum(tot.values())
 print(f"{sum(cnt.values())} launches, {T:.2f} ms total (ncu, serialised)")
 print(f"{'share':>6s} {'ms':>9s} {'launches':>8s}  kernel")
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{v / T:6.3f} {v:9.3f} {cnt[k]:8d}  {k[:150]}")
+    try:
+        print(f"{v / T:6.3f} {v:9.3f} {cnt[k]:8d}  {k[:170]}")
+    except BrokenPipeError:
+        break
