@@ -241,7 +241,10 @@ __global__ void k_sellr_fill(int n, int b, int W, int ns, const int32_t* __restr
 }
 
 static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
-  const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 ? 4 : 2);
+  // 16-byte vectors; 3x3 fp32 rows of < 6 blocks (prolongators) take 8-byte ones: GB = 2 blocks
+  // per step instead of 4 pads their 3-4-block rows less (P_0: 4.0 vs 3.3 TB/s with W = 4)
+  const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
+  const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 && !(A.b == 3 && per_row < 6.0) ? 4 : 2);
   if (!(W == 4 && A.vt == AMG_F32) && W != 2) fail(AMG_EINVAL, "AMG_SELLR_W: 4 (fp32) or 2");
   const int E = A.b * A.b;
   const Slicing sl = slice_rows(A, 32, s);
@@ -279,12 +282,12 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
     // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) square-block matrices with
-    // 6..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
+    // 3..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
     // (cfg 5 / cfg 2): A_0 5.65, A_1 / R_0 6.4-6.5, outer 4x4 fp64 7.07, cfg-2 4x4 fp32 x fp64
     // 6.85, fp64 7.03 TB/s vs 4.8 / 5.4 / 6.74 / 6.07 / 6.70 for the row lanes / sliced copy;
-    // the 3.6-block prolongators stay on the COLS lanes (3.3 vs 3.8)
+    // the 3.6-block prolongators with 8-byte vectors 4.0 vs 3.9 for the COLS lanes
     const int sellr_mode = env_int("AMG_SELLR", 1);
-    const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 6);
+    const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 3);
     // sliced copies need the builder's arena and square b x b blocks
     if (arena && square && forced == kLaneSellR) {
       build_sellr(A, *arena, s);
