@@ -507,15 +507,21 @@ struct SellrShape {
   static constexpr int GB = W / gcd(E, W);  // blocks per step: lcm(E, W) / E
   static constexpr int NV = GB * E / W;     // vectors per step
 };
-// resident blocks per SM: a step's values take NV * W registers.  Above 18 words (3x3 fp32,
-// 36 values) the register budget is 128 (2 blocks): with 80 ptxas interleaved each 16-byte
-// load with its FMAs (one load in flight per thread, 4.8 TB/s on A_0); with 128 all loads of
-// a step issue first (5.65 TB/s)
+// Launch shape: a step's values take NV * W registers.  Above 18 words (3x3 fp32, 36
+// values) the budget must let ptxas issue every load of a step first: at 80 registers it
+// interleaved each 16-byte load with its FMAs (one load in flight per thread, 4.8 TB/s on
+// A_0), at 128 (256 threads x 2 blocks) all loads issue first (5.65 TB/s).  128 threads x 5
+// blocks (96 registers, 20 warps per SM; -DSELLR_TPB_BIG=128) interleaves again: 5.3 TB/s.
+#ifndef SELLR_TPB_BIG
+#define SELLR_TPB_BIG 256
+#endif
 template <int B, int W, typename V, bool FAST>
-constexpr int sellr_min_blocks() {
-  constexpr int words = SellrShape<B, W>::NV * W * (int)sizeof(V) / 4;
-  return words <= 16 ? 4 : (words <= 18 ? 3 : 2);
-}
+struct SellrCfg {
+  static constexpr int words = SellrShape<B, W>::NV * W * (int)sizeof(V) / 4;
+  static constexpr int TPB = words <= 18 ? 256 : SELLR_TPB_BIG;
+  static constexpr int MINB = words <= 16 ? 4 : (words <= 18 ? 3 : (65536 / TPB) / (TPB == 256 ? 128 : 102));
+  static constexpr int WPB = TPB / 32;
+};
 
 template <int W, typename V>
 __device__ __forceinline__ void ld_vec(const V* __restrict__ p, V* v) {
@@ -569,7 +575,7 @@ __device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32
 }
 
 template <int B, int W, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(256, (sellr_min_blocks<B, W, V, FAST>())) k_bsr_sellr(
+__global__ void __launch_bounds__(SellrCfg<B, W, V, FAST>::TPB, SellrCfg<B, W, V, FAST>::MINB) k_bsr_sellr(
     int n, int s0, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
     const int32_t* __restrict__ perm, const int32_t* __restrict__ scol, const V* __restrict__ sval,
     const X* __restrict__ x, EPI epi) {
@@ -577,10 +583,11 @@ __global__ void __launch_bounds__(256, (sellr_min_blocks<B, W, V, FAST>())) k_bs
   using S = SellrShape<B, W>;
   constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t nvb = ((int64_t)nslices - s0 + 7) / 8;
+  constexpr int WPB = SellrCfg<B, W, V, FAST>::WPB;
+  const int64_t nvb = ((int64_t)nslices - s0 + WPB - 1) / WPB;
   double dacc[ND] = {};
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
-    const int s = s0 + (int)(vb * 8 + w);
+    const int s = s0 + (int)(vb * WPB + w);
     double acc[B] = {};
     if (s < nslices) {
       const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;
@@ -606,7 +613,8 @@ __global__ void __launch_bounds__(256, (sellr_min_blocks<B, W, V, FAST>())) k_bs
     }
   }
   if constexpr (EPI::kDots > 0)
-    block_reduce_finish<EPI::kDots, 256>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out, 0, nullptr);
+    block_reduce_finish<EPI::kDots, SellrCfg<B, W, V, FAST>::TPB>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out,
+                                                                   0, nullptr);
 }
 
 }  // namespace amgb

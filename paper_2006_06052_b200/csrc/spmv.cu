@@ -376,20 +376,26 @@ bool sellr_range_ok(const Mat& A, int r0, int r1) {
   return A.lane_var == kLaneSellR && !A.sell_perm && r0 % 32 == 0 && (r1 >= A.n || r1 % 32 == 0);
 }
 
+// grid: one virtual block per WPB slices (the kernel's launch shape, SellrCfg); fused dots:
+// a persistent grid of at most kMaxPartials blocks
 template <int B, typename V, typename X, class EPI>
-static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, unsigned grid, int s0 = 0,
+static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, bool dots, int s0 = 0,
                          int s1 = -1) {
   if (s1 < 0) s1 = A.sell_ns;
   if (s1 <= s0) return;
   auto go = [&](auto Wc) {
     constexpr int W = decltype(Wc)::value;
     constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
-    if (can_fast && fast)
-      k_bsr_sellr<B, W, V, X, can_fast, EPI><<<grid, kBlock, 0, s>>>(A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm,
-                                                                    A.sell_col, (const V*)A.sell_val, x, epi);
-    else
-      k_bsr_sellr<B, W, V, X, false, EPI><<<grid, kBlock, 0, s>>>(A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm,
-                                                                  A.sell_col, (const V*)A.sell_val, x, epi);
+    auto run = [&](auto Fc) {
+      constexpr bool F = decltype(Fc)::value;
+      using Cfg = SellrCfg<B, W, V, F>;
+      int64_t g = ((int64_t)s1 - s0 + Cfg::WPB - 1) / Cfg::WPB;
+      if (dots) g = std::min<int64_t>(g, kMaxPartials);
+      k_bsr_sellr<B, W, V, X, F, EPI><<<(unsigned)std::max<int64_t>(g, 1), Cfg::TPB, 0, s>>>(
+          A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col, (const V*)A.sell_val, x, epi);
+    };
+    if (can_fast && fast) run(std::integral_constant<bool, can_fast>{});
+    else run(std::false_type{});
   };
   if constexpr (std::is_same_v<V, float>) {
     if (A.sell_w == 4) go(std::integral_constant<int, 4>{});
@@ -412,7 +418,7 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r
   if constexpr (BR == BC && BR >= 2) {
     if (A.lane_var == kLaneSellR) {
       const int s0 = r0 / 32, s1 = r1 >= A.n ? A.sell_ns : r1 / 32;
-      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, (unsigned)std::max((s1 - s0 + 7) / 8, 1), s0, s1);
+      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, false, s0, s1);
       return;
     }
     if (A.lane_var == kLaneSell) {
@@ -487,8 +493,7 @@ static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaSt
           using V = decltype(v);
           dispatch_t(xt, [&](auto xx) {
             using X = decltype(xx);
-            const unsigned grid = (unsigned)std::min<int64_t>((A.sell_ns + 7) / 8, kMaxPartials);
-            launch_sellr<B, V, X>(A, (const X*)x, epi, s, false, grid);
+            launch_sellr<B, V, X>(A, (const X*)x, epi, s, false, true);
           });
         });
       }
