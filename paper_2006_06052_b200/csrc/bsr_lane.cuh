@@ -180,6 +180,10 @@ struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
     if (!L.valid) return;
     p[L.row] = to_out<X>((double)mS[L.row] * ((double)rp[L.row] - L.yr));
   }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    p[row] = to_out<X>((double)mS[row] * ((double)rp[row] - yr[0]));
+  }
 };
 
 template <typename X>
@@ -192,6 +196,15 @@ struct LEpiSchurU {  // r_u' = r_u - B^T p          (nu x 1 blocks; in place all
     if (!L.valid) return;
     const int64_t o = (int64_t)L.row * BR + L.r;
     ru2[o] = to_out<X>((double)ru[o] - L.yr);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double v[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) v[c] = (double)ru[o + c];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) ru2[o + c] = to_out<X>(v[c] - yr[c]);
   }
 };
 
@@ -500,9 +513,9 @@ __global__ void __launch_bounds__(256, 8) k_bsr_sell(int n, int nslices, const i
 // BR results and runs the epilogue's row-per-lane form (row(), row_dots()).
 // Arithmetic: the block-row dots of k_bsr_lane's ROWS layout in the same block order --
 // bit-identical to it.
-template <int B, int W>
+template <int BR, int BC, int W>
 struct SellrShape {
-  static constexpr int E = B * B;
+  static constexpr int E = BR * BC;
   static constexpr int gcd(int a, int b) { return b == 0 ? a : gcd(b, a % b); }
   static constexpr int GB = W / gcd(E, W);  // blocks per step: lcm(E, W) / E
   static constexpr int NV = GB * E / W;     // vectors per step
@@ -515,9 +528,9 @@ struct SellrShape {
 #ifndef SELLR_TPB_BIG
 #define SELLR_TPB_BIG 256
 #endif
-template <int B, int W, typename V, bool FAST>
+template <int BR, int BC, int W, typename V, bool FAST>
 struct SellrCfg {
-  static constexpr int words = SellrShape<B, W>::NV * W * (int)sizeof(V) / 4;
+  static constexpr int words = SellrShape<BR, BC, W>::NV * W * (int)sizeof(V) / 4;
   static constexpr int TPB = words <= 18 ? 256 : SELLR_TPB_BIG;
   static constexpr int MINB = words <= 16 ? 4 : (words <= 18 ? 3 : (65536 / TPB) / (TPB == 256 ? 128 : 102));
   static constexpr int WPB = TPB / 32;
@@ -543,20 +556,20 @@ __device__ __forceinline__ void ld_vec(const V* __restrict__ p, V* v) {
 // One step: GB blocks of the lane's row.  c holds this step's column indices (loaded one
 // step ahead); the value loads, the x gathers and the next step's column loads are all
 // issued before any arithmetic.
-template <int B, int W, bool TAIL, typename V, typename X, bool FAST>
+template <int BR, int BC, int W, bool TAIL, typename V, typename X, bool FAST>
 __device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32_t* __restrict__ cpn,
-                                           const X* __restrict__ x, int nb, int nbn, int (&c)[SellrShape<B, W>::GB],
-                                           double (&acc)[B]) {
-  using S = SellrShape<B, W>;
+                                           const X* __restrict__ x, int nb, int nbn,
+                                           int (&c)[SellrShape<BR, BC, W>::GB], double (&acc)[BR]) {
+  using S = SellrShape<BR, BC, W>;
   V a[S::NV * W];
   const int nv = TAIL ? (S::E * nb + W - 1) / W : S::NV;
 #pragma unroll
   for (int q = 0; q < S::NV; ++q)
     if (!TAIL || q < nv) ld_vec<W>(vp + (int64_t)q * 32 * W, a + q * W);
-  X xv[S::GB][B];
+  X xv[S::GB][BC];
 #pragma unroll
   for (int u = 0; u < S::GB; ++u)
-    if (!TAIL || u < nb) ld_x<B>(x + (int64_t)c[u] * B, xv[u]);
+    if (!TAIL || u < nb) ld_x<BC>(x + (int64_t)c[u] * BC, xv[u]);
   if constexpr (!TAIL) {
 #pragma unroll
     for (int u = 0; u < S::GB; ++u) c[u] = u < nbn ? __ldcs(cpn + u * 32) : 0;
@@ -565,30 +578,30 @@ __device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32
   for (int u = 0; u < S::GB; ++u) {
     if (TAIL && u >= nb) continue;
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-      V ar[B];
+    for (int i = 0; i < BR; ++i) {
+      V ar[BC];
 #pragma unroll
-      for (int cc = 0; cc < B; ++cc) ar[cc] = a[u * S::E + i * B + cc];
-      acc[i] += item_dot<B, V, X, FAST>(ar, xv[u]);
+      for (int cc = 0; cc < BC; ++cc) ar[cc] = a[u * S::E + i * BC + cc];
+      acc[i] += item_dot<BC, V, X, FAST>(ar, xv[u]);
     }
   }
 }
 
-template <int B, int W, typename V, typename X, bool FAST, class EPI>
-__global__ void __launch_bounds__(SellrCfg<B, W, V, FAST>::TPB, SellrCfg<B, W, V, FAST>::MINB) k_bsr_sellr(
+template <int BR, int BC, int W, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(SellrCfg<BR, BC, W, V, FAST>::TPB, SellrCfg<BR, BC, W, V, FAST>::MINB) k_bsr_sellr(
     int n, int s0, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
     const int32_t* __restrict__ perm, const int32_t* __restrict__ scol, const V* __restrict__ sval,
     const X* __restrict__ x, EPI epi) {
   // slices [s0, nslices) (a row range of 32-aligned bounds: the distributed interior / boundary split)
-  using S = SellrShape<B, W>;
+  using S = SellrShape<BR, BC, W>;
   constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  constexpr int WPB = SellrCfg<B, W, V, FAST>::WPB;
+  constexpr int WPB = SellrCfg<BR, BC, W, V, FAST>::WPB;
   const int64_t nvb = ((int64_t)nslices - s0 + WPB - 1) / WPB;
   double dacc[ND] = {};
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
     const int s = s0 + (int)(vb * WPB + w);
-    double acc[B] = {};
+    double acc[BR] = {};
     if (s < nslices) {
       const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;
       const V* vp = sval + ((int64_t)__ldg(vptr + s) * 32 + lane) * W;
@@ -600,20 +613,20 @@ __global__ void __launch_bounds__(SellrCfg<B, W, V, FAST>::TPB, SellrCfg<B, W, V
 #pragma unroll 1
       for (; j + S::GB <= L; j += S::GB) {
         cp += S::GB * 32;
-        sellr_step<B, W, false, V, X, FAST>(vp, cp, x, S::GB, min(S::GB, L - j - S::GB), c, acc);
+        sellr_step<BR, BC, W, false, V, X, FAST>(vp, cp, x, S::GB, min(S::GB, L - j - S::GB), c, acc);
         vp += (int64_t)S::NV * 32 * W;
       }
-      if (j < L) sellr_step<B, W, true, V, X, FAST>(vp, cp, x, L - j, 0, c, acc);
+      if (j < L) sellr_step<BR, BC, W, true, V, X, FAST>(vp, cp, x, L - j, 0, c, acc);
     }
     int row = s * 32 + lane;
     if (perm && s < nslices) row = __ldg(perm + (int64_t)s * 32 + lane);  // sorted windows (-1: padding)
     if (s < nslices && row >= 0 && row < n) {
-      epi.template row<B>(row, acc);
-      if constexpr (EPI::kDots > 0) epi.template row_dots<B>(row, acc, dacc);
+      epi.template row<BR>(row, acc);
+      if constexpr (EPI::kDots > 0) epi.template row_dots<BR>(row, acc, dacc);
     }
   }
   if constexpr (EPI::kDots > 0)
-    block_reduce_finish<EPI::kDots, SellrCfg<B, W, V, FAST>::TPB>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out,
+    block_reduce_finish<EPI::kDots, SellrCfg<BR, BC, W, V, FAST>::TPB>(dacc, EPI::kDots, epi.partials, epi.ticket, epi.out,
                                                                    0, nullptr);
 }
 

@@ -364,7 +364,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
                         cudaMemcpyDeviceToDevice));
       AMG_CK(cudaMemcpy(h->shat64, Gh->shat64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
       AMG_CK(cudaMemcpy(h->mS64, Gh->mS64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
-      make_schur_views(h->A, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
+      make_schur_views(h->A, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
     }
     // hierarchy levels
     const size_t L = Gh->lv.size();

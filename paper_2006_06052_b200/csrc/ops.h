@@ -9,7 +9,7 @@ namespace amgb {
 // kernel plan of a device matrix: the bsr_lane.cuh variant (host only); with an arena,
 // long-row matrices also get the sliced copy (k_bsr_sell, allocated in the arena: one
 // sync); the opt-in TMA tile plan (AMG_TMA=1: one reduction + one sync)
-void set_lane_plan(Mat& A);
+void set_lane_plan(Mat& A, bool use_env = true);
 void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena = nullptr, bool want_tma = false);
 
 // S1: scalar CSR -> BSR (convert.cu); returns nnzb, fills bptr/bcol/bval when bptr != nullptr
@@ -50,7 +50,8 @@ void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void*
 // Schur coupling views on the outer pattern: Bm (1 x nu blocks, values Bv [nnz][nu]) and
 // BTm (nu x 1 blocks, values BTv [nnz][nu]), with their TMA plans
 void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int vt, Mat& Bm, Mat& BTm,
-                      cudaStream_t s);
+                      cudaStream_t s,
+                      Arena* arena = nullptr);
 // K10 p = m_S o (r_p - B u*)
 void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s);
 // K11 ru2 = r_u - B^T p   (ru2 may alias ru)

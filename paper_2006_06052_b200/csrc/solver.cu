@@ -137,7 +137,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
     make_tma_plan(M, s, &h->arena);
     if (h->amg_active) setup_build(*h, M, bounds, s);
-    if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s);
+    if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
     h->pmask_in = nullptr;
     if (workspace) alloc_workspace(*h, s);
     h->alg_bytes_precond = precond_bytes(*h);

@@ -89,7 +89,7 @@ static int env_int(const char* name, int dflt) {
 //   3 x 3 fp64, rectangular: ROWS, U = 2 (nc for fp32 values)
 // AMG_TMA=1 switches short-row fp32 matrices to the TMA-staged row-per-lane consumer
 // (bsr_tma.cuh) for comparison.  One reduction + one sync only in that case.
-void set_lane_plan(Mat& A) {
+void set_lane_plan(Mat& A, bool use_env) {
   const int br = A.rows_per_block(), bc = A.cols_per_block();
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
   const bool f32 = A.vt == AMG_F32;
@@ -104,7 +104,9 @@ void set_lane_plan(Mat& A) {
   // warps (coarse levels): one warp per row
   const double lane_warps = (double)A.n / (32 / std::max(br, 1));
   if (per_row > 64.0 || (per_row > 12.0 && lane_warps < (double)kSMs * 64)) var = kLaneW;
-  A.lane_var = env_int("AMG_LANE_VAR", var);
+  A.lane_var = use_env ? env_int("AMG_LANE_VAR", var) : var;
+  // a forced sliced / interleaved variant needs its copy (make_tma_plan builds it)
+  if ((A.lane_var == kLaneSell && !A.sell_ptr) || (A.lane_var == kLaneSellR && !A.sell_vptr)) A.lane_var = var;
 }
 
 // ---- sliced copy (k_bsr_sell) ----
@@ -219,7 +221,7 @@ static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
 
 // ---- interleaved row-per-lane copy (k_bsr_sellr) ----
 template <typename V>
-__global__ void k_sellr_fill(int n, int b, int W, int ns, const int32_t* __restrict__ ptr,
+__global__ void k_sellr_fill(int n, int E, int W, int ns, const int32_t* __restrict__ ptr,
                              const int32_t* __restrict__ col, const V* __restrict__ val,
                              const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
                              const int32_t* __restrict__ perm, int32_t* __restrict__ scol, V* __restrict__ sval) {
@@ -229,10 +231,8 @@ __global__ void k_sellr_fill(int n, int b, int W, int ns, const int32_t* __restr
   int64_t row = t;
   if (perm) row = perm[t] >= 0 ? perm[t] : n;
   const int k0 = row < n ? ptr[row] : 0, len = row < n ? ptr[row + 1] - k0 : 0;
-  const int pad_col = row < n ? (int)row : 0;
-  const int E = b * b;
-  for (int j = 0; j < sptr[s + 1] - sptr[s]; ++j)
-    scol[((int64_t)sptr[s] + j) * 32 + g] = j < len ? col[k0 + j] : (len > 0 ? col[k0] : pad_col);
+  for (int j = 0; j < sptr[s + 1] - sptr[s]; ++j)  // padding: a column the row reads anyway (or 0)
+    scol[((int64_t)sptr[s] + j) * 32 + g] = j < len ? col[k0 + j] : (len > 0 ? col[k0] : 0);
   const int64_t nv = vptr[s + 1] - vptr[s];
   for (int64_t e = 0; e < nv * W; ++e) {
     const int64_t q = e / W, jb = e / E;
@@ -246,7 +246,7 @@ static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
   const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 && !(A.b == 3 && per_row < 6.0) ? 4 : 2);
   if (!(W == 4 && A.vt == AMG_F32) && W != 2) fail(AMG_EINVAL, "AMG_SELLR_W: 4 (fp32) or 2");
-  const int E = A.b * A.b;
+  const int E = A.rows_per_block() * A.cols_per_block();
   const Slicing sl = slice_rows(A, 32, s);
   const int ns = sl.ns;
   const std::vector<int32_t> sp = prefix32(sl.h, "interleaved copy: too many steps");
@@ -264,7 +264,7 @@ static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
   A.sell_perm = upload_perm(sl, 32, arena, s);
   dispatch_t(A.vt, [&](auto v) {
     using V = decltype(v);
-    k_sellr_fill<V><<<grid_for((int64_t)ns * 32, 256), 256, 0, s>>>(A.n, A.b, W, ns, A.ptr, A.col, (const V*)A.val,
+    k_sellr_fill<V><<<grid_for((int64_t)ns * 32, 256), 256, 0, s>>>(A.n, E, W, ns, A.ptr, A.col, (const V*)A.val,
                                                                      A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col,
                                                                      (V*)A.sell_val);
   });
@@ -280,6 +280,10 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
   {
     const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
+    // Schur B^T (nu x 1 blocks): interleaved copy 5.4 vs 5.15 TB/s (TMA rows); B (1 x nu) stays on
+    // the lane kernel (5.1 vs 4.1 interleaved)
+    const bool rect = (A.br > 0 || A.bc > 0) && A.rows_per_block() > 1 && A.rows_per_block() <= 4 &&
+                      A.cols_per_block() <= 4;
     const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
     // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) square-block matrices with
     // 3..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
@@ -289,7 +293,10 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const int sellr_mode = env_int("AMG_SELLR", 1);
     const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 3);
     // sliced copies need the builder's arena and square b x b blocks
-    if (arena && square && forced == kLaneSellR) {
+    if (arena && rect && forced < 0 && sellr_mode >= 1 && per_row >= 3 && per_row <= 64 &&
+        (int64_t)A.n / 32 >= env_int("AMG_SELL_MIN_SLICES", kSMs * 64)) {
+      build_sellr(A, *arena, s);  // Schur coupling views (1 x nu, nu x 1 blocks on A's pattern)
+    } else if (arena && square && forced == kLaneSellR) {
       build_sellr(A, *arena, s);
     } else if (arena && square && forced == kLaneSell) {
       build_sell(A, *arena, s);
@@ -305,6 +312,7 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
         build_sell(A, *arena, s);
     }
   }
+  if (A.lane_var == kLaneSellR) return;  // the interleaved copy replaces the TMA consumer
   const int br = A.rows_per_block(), bc = A.cols_per_block();
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
   if (!(want_tma || env_int("AMG_TMA", 0)) || A.n < 2048 || A.vt != AMG_F32) return;
@@ -378,7 +386,7 @@ bool sellr_range_ok(const Mat& A, int r0, int r1) {
 
 // grid: one virtual block per WPB slices (the kernel's launch shape, SellrCfg); fused dots:
 // a persistent grid of at most kMaxPartials blocks
-template <int B, typename V, typename X, class EPI>
+template <int BR, int BC, typename V, typename X, class EPI>
 static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool fast, bool dots, int s0 = 0,
                          int s1 = -1) {
   if (s1 < 0) s1 = A.sell_ns;
@@ -388,10 +396,10 @@ static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool
     constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
     auto run = [&](auto Fc) {
       constexpr bool F = decltype(Fc)::value;
-      using Cfg = SellrCfg<B, W, V, F>;
+      using Cfg = SellrCfg<BR, BC, W, V, F>;
       int64_t g = ((int64_t)s1 - s0 + Cfg::WPB - 1) / Cfg::WPB;
       if (dots) g = std::min<int64_t>(g, kMaxPartials);
-      k_bsr_sellr<B, W, V, X, F, EPI><<<(unsigned)std::max<int64_t>(g, 1), Cfg::TPB, 0, s>>>(
+      k_bsr_sellr<BR, BC, W, V, X, F, EPI><<<(unsigned)std::max<int64_t>(g, 1), Cfg::TPB, 0, s>>>(
           A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col, (const V*)A.sell_val, x, epi);
     };
     if (can_fast && fast) run(std::integral_constant<bool, can_fast>{});
@@ -415,12 +423,14 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r
   if (ranged && ((A.lane_var > kLaneCN4 && A.lane_var != kLaneSellR) || A.tma_grid > 0))
     fail(AMG_EINVAL, "row ranges need a row-lane plan");
   constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
-  if constexpr (BR == BC && BR >= 2) {
+  if constexpr (BR != BC || BR >= 2) {
     if (A.lane_var == kLaneSellR) {
       const int s0 = r0 / 32, s1 = r1 >= A.n ? A.sell_ns : r1 / 32;
-      launch_sellr<BR, V, X>(A, x, epi, s, can_fast && A.fast32, false, s0, s1);
+      launch_sellr<BR, BC, V, X>(A, x, epi, s, can_fast && A.fast32, false, s0, s1);
       return;
     }
+  }
+  if constexpr (BR == BC && BR >= 2) {
     if (A.lane_var == kLaneSell) {
       constexpr int U = (BR * BR * sizeof(V) <= 36) ? 4 : 2;
       const unsigned grid = grid_for((int64_t)A.sell_ns * 32, kBlock);
@@ -493,7 +503,7 @@ static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaSt
           using V = decltype(v);
           dispatch_t(xt, [&](auto xx) {
             using X = decltype(xx);
-            launch_sellr<B, V, X>(A, (const X*)x, epi, s, false, true);
+            launch_sellr<B, B, V, X>(A, (const X*)x, epi, s, false, true);
           });
         });
       }
@@ -668,8 +678,9 @@ void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void*
 }
 
 void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int vt, Mat& Bm, Mat& BTm,
-                      cudaStream_t s) {
+                      cudaStream_t s, Arena* arena) {
   Bm = A;
+  Bm.sell_ns = 0, Bm.sell_ptr = Bm.sell_col = Bm.sell_perm = Bm.sell_vptr = nullptr, Bm.sell_val = nullptr;
   Bm.b = 1;
   Bm.br = 1;
   Bm.bc = nu;
@@ -680,10 +691,11 @@ void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int
   BTm.br = nu;
   BTm.bc = 1;
   BTm.val = const_cast<void*>(BTv);
-  make_tma_plan(Bm, s);
-  // B^T (3 x 1 blocks, 4-byte row segments): the TMA-staged row-per-lane consumer
-  // measured 5.2 TB/s against 3.8-4.0 for the lane kernel (cfg 5)
-  make_tma_plan(BTm, s, nullptr, !env_int("AMG_NO_TMA_SCHUR", 0));
+  // B on the lane kernel; B^T (3 x 1 blocks) on the interleaved copy when large enough (5.4
+  // TB/s at cfg 5), else on the TMA-staged row-per-lane consumer (5.2 TB/s against 3.8-4.0
+  // for the lane kernel)
+  make_tma_plan(Bm, s, arena);
+  make_tma_plan(BTm, s, arena, !env_int("AMG_NO_TMA_SCHUR", 0));
 }
 
 void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s) {
