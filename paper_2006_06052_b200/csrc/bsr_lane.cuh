@@ -525,6 +525,8 @@ struct SellrShape {
 // interleaved each 16-byte load with its FMAs (one load in flight per thread, 4.8 TB/s on
 // A_0), at 128 (256 threads x 2 blocks) all loads issue first (5.65 TB/s).  128 threads x 5
 // blocks (96 registers, 20 warps per SM; -DSELLR_TPB_BIG=128) interleaves again: 5.3 TB/s.
+// 18-word steps (3x3 fp32, 8-byte vectors: the prolongators) run 5 blocks per SM (48
+// registers): P_0 4.0 -> 4.3 -> 4.7 TB/s from 3 to 4 to 5 blocks.
 #ifndef SELLR_TPB_BIG
 #define SELLR_TPB_BIG 256
 #endif
@@ -532,7 +534,7 @@ template <int BR, int BC, int W, typename V, bool FAST>
 struct SellrCfg {
   static constexpr int words = SellrShape<BR, BC, W>::NV * W * (int)sizeof(V) / 4;
   static constexpr int TPB = words <= 18 ? 256 : SELLR_TPB_BIG;
-  static constexpr int MINB = words <= 16 ? 4 : (words <= 18 ? 3 : (65536 / TPB) / (TPB == 256 ? 128 : 102));
+  static constexpr int MINB = words <= 16 ? 4 : words <= 18 ? 5 : (65536 / TPB) / (TPB == 256 ? 128 : 102);
   static constexpr int WPB = TPB / 32;
 };
 
