@@ -241,10 +241,13 @@ __global__ void k_sellr_fill(int n, int E, int W, int ns, const int32_t* __restr
 }
 
 static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
-  // 16-byte vectors; 3x3 fp32 rows of < 6 blocks (prolongators) take 8-byte ones: GB = 2 blocks
-  // per step instead of 4 pads their 3-4-block rows less (P_0: 4.0 vs 3.3 TB/s with W = 4)
+  // 16-byte vectors; square 3x3 fp32 rows of < 12 blocks (A_0: 7, prolongators: 3.6) take
+  // 8-byte ones -- GB = 2 blocks per step at 48 registers and 5 blocks per SM instead of 4
+  // blocks per step at 128 registers and 2 (A_0 5.65 -> 6.0, P_0 3.3 -> 4.7 TB/s); long rows
+  // keep 16-byte vectors (A_1 / R_0 6.4-6.5 vs 5.8-6.3)
   const double per_row = A.n > 0 ? (double)A.nnz / A.n : 0.0;
-  const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 && !(A.b == 3 && per_row < 6.0) ? 4 : 2);
+  const bool short3 = A.br == 0 && A.bc == 0 && A.b == 3 && per_row < 12.0;
+  const int W = env_int("AMG_SELLR_W", A.vt == AMG_F32 && !short3 ? 4 : 2);
   if (!(W == 4 && A.vt == AMG_F32) && W != 2) fail(AMG_EINVAL, "AMG_SELLR_W: 4 (fp32) or 2");
   const int E = A.rows_per_block() * A.cols_per_block();
   const Slicing sl = slice_rows(A, 32, s);
