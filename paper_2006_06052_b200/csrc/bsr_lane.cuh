@@ -525,8 +525,10 @@ struct SellrShape {
 // interleaved each 16-byte load with its FMAs (one load in flight per thread, 4.8 TB/s on
 // A_0), at 128 (256 threads x 2 blocks) all loads issue first (5.65 TB/s).  128 threads x 5
 // blocks (96 registers, 20 warps per SM; -DSELLR_TPB_BIG=128) interleaves again: 5.3 TB/s.
-// 18-word steps (3x3 fp32, 8-byte vectors: the prolongators) run 5 blocks per SM (48
-// registers): P_0 4.0 -> 4.3 -> 4.7 TB/s from 3 to 4 to 5 blocks.
+// 18-word steps (3x3 fp32, 8-byte vectors: A_0, the prolongators) run 6 blocks per SM (40
+// registers, 88 bytes of L1-resident spill): P_0 4.0 / 4.3 / 4.7 / 5.1 TB/s at 3 / 4 / 5 / 6
+// blocks, A_0's smoother 5.77 / 5.93 / 6.06 at 4 / 5 / 6; 8 blocks (32 registers) spill
+// 168 bytes and drop to 5.2.  4x4 fp64 (32 words) stays at 2 (uses 72): 4 blocks, 6.90 vs 7.07.
 #ifndef SELLR_TPB_BIG
 #define SELLR_TPB_BIG 256
 #endif
@@ -534,7 +536,7 @@ template <int BR, int BC, int W, typename V, bool FAST>
 struct SellrCfg {
   static constexpr int words = SellrShape<BR, BC, W>::NV * W * (int)sizeof(V) / 4;
   static constexpr int TPB = words <= 18 ? 256 : SELLR_TPB_BIG;
-  static constexpr int MINB = words <= 16 ? 4 : words <= 18 ? 5 : (65536 / TPB) / (TPB == 256 ? 128 : 102);
+  static constexpr int MINB = words <= 16 ? 4 : words <= 18 ? 6 : (65536 / TPB) / (TPB == 256 ? 128 : 102);
   static constexpr int WPB = TPB / 32;
 };
 
