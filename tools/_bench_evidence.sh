@@ -14,7 +14,7 @@ tail -2 /tmp/ncu_top.log
 ncu -i /tmp/top.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_top_details.csv
 ncu -i /tmp/top.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_top_raw.csv
 rm -f /tmp/smooth.ncu-rep
-ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr.*LEpiSmooth<float, float>" -s 1 -c 1 -o /tmp/smooth python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_smooth.log 2>&1
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr<\(int\)3, \(int\)3, \(int\)2, float, float, \(bool\)1, amgb::LEpiSmooth<float, float>>" -c 1 -o /tmp/smooth python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-spmv > /tmp/ncu_smooth.log 2>&1
 tail -2 /tmp/ncu_smooth.log
 ncu -i /tmp/smooth.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_smooth_details.csv
 ncu -i /tmp/smooth.ncu-rep --page raw --csv > gpurun_out/${TAG}_ncu_smooth_raw.csv
