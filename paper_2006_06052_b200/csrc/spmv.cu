@@ -297,7 +297,7 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const double sellr_min_row = env_int("AMG_SELLR_MIN_ROW", 3);
     // sliced copies need the builder's arena and square b x b blocks
     if (arena && rect && forced < 0 && sellr_mode >= 1 && per_row >= 3 && per_row <= 64 &&
-        (int64_t)A.n / 32 >= env_int("AMG_SELL_MIN_SLICES", kSMs * 64)) {
+        (int64_t)A.n / 32 >= env_int("AMG_SELLR_MIN_SLICES", 4096)) {
       build_sellr(A, *arena, s);  // Schur coupling views (1 x nu, nu x 1 blocks on A's pattern)
     } else if (arena && square && forced == kLaneSellR) {
       build_sellr(A, *arena, s);
@@ -308,7 +308,9 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
       // >= 64 slices per SM: below that the per-slice step chains are latency bound and
       // the warp-per-row kernel (set_lane_plan) is faster (cfg 3 level 1: 41 us vs ~10 us)
       const int64_t min_slices = env_int("AMG_SELL_MIN_SLICES", kSMs * 64);
-      const bool many = (int64_t)A.n / 32 >= min_slices;
+      // the interleaved copy pays from >= 4096 slices of 32 rows (cfg 4 level 1, 8,236 slices:
+      // 4.8 -> 5.5-5.6 TB/s; 1024 slices lose at cfg 3)
+      const bool many = (int64_t)A.n / 32 >= env_int("AMG_SELLR_MIN_SLICES", 4096);
       if (sellr_mode == 2 || (sellr_mode == 1 && many && per_row >= sellr_min_row && per_row <= hi))
         build_sellr(A, *arena, s);
       else if (per_row > lo && per_row <= hi && (int64_t)A.n / (32 / A.b) >= min_slices && !env_int("AMG_NO_SELL", 0))

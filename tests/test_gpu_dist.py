@@ -143,7 +143,7 @@ def test_halo_overlap_is_exact(amg, envvars):
 def test_halo_overlap_interleaved_copy_is_exact(amg, envvars):
     # the same with the interleaved row-per-lane copy on every fp32 level (whole 32-row
     # slices: the interior rounded inward), unsorted slices so row ranges apply
-    envvars(AMG_SELL_MIN_SLICES=1, AMG_SELL_NO_SORT=1)
+    envvars(AMG_SELLR_MIN_SLICES=1, AMG_SELL_NO_SORT=1)
     runs = []
     for off in (False, True):
         if off:

@@ -306,11 +306,15 @@ def test_fp32_vs_fp64_iteration_parity(amg):
     assert abs(its[0] - its[1]) <= 1
 
 
-@pytest.mark.parametrize("wide", [1, 99])
-def test_solve_forced_kernel_paths(amg, envvars, wide):
-    # sliced copies on every long-row level (small grid: lower the slice-count gate) and
-    # the wide (wide=1) or K-templated (wide=99) CGS2 kernels at every k
-    envvars(AMG_SELL_MIN_SLICES=1, AMG_CGS_WIDE=wide)
+@pytest.mark.parametrize("wide,copy", [(1, "sell"), (99, "sell"), (1, "sellr")])
+def test_solve_forced_kernel_paths(amg, envvars, wide, copy):
+    # sliced (SELL-C) or interleaved row-per-lane copies on every level they apply to (small
+    # grid: lower the slice-count gates) and the wide (wide=1) or K-templated (wide=99) CGS2
+    # kernels at every k
+    if copy == "sell":
+        envvars(AMG_SELL_MIN_SLICES=1, AMG_SELLR=0, AMG_CGS_WIDE=wide)
+    else:
+        envvars(AMG_SELLR_MIN_SLICES=1, AMG_CGS_WIDE=wide)
     n = 24
     ptr, col, val = gen.matrix(gen.STOKES, n)
     bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
