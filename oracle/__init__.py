@@ -45,7 +45,7 @@ class Params(ctypes.Structure):
         ("npre", ctypes.c_int32), ("npost", ctypes.c_int32), ("schur_p_component", ctypes.c_int32),
         ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
         ("schur_u_scalar", ctypes.c_int32), ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32),
-        ("over_interp", ctypes.c_double), ("ilu_sweeps", ctypes.c_int32), ("_pad", ctypes.c_int32),
+        ("over_interp", ctypes.c_double), ("ilu_sweeps", ctypes.c_int32), ("gmres_ortho", ctypes.c_int32),
     ]
 
 

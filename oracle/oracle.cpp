@@ -57,7 +57,7 @@ extern "C" void orc_params_default(orc_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
-  p->_pad = 0;
+  p->gmres_ortho = 0;
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -1428,6 +1428,7 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
   vector<double> b(bp, bp + N), x(xp, xp + N), r(N), w(N), tmpx(N), tmpr(N);
   vector<vector<double>> V(m + 1, vector<double>(N)), Z(m, vector<double>(N));
   vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), h(m + 1), h2(m + 1);
+  vector<double> Rg((size_t)(m + 1) * (m + 1), 0.0);  // gmres_ortho = 1: Cholesky factor of t^T t
   const double nb = nrm2(b);
   residual(s.A, b.data(), x.data(), r.data(), false);
   double beta = nrm2(r);
@@ -1440,21 +1441,64 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
     for (int64_t i = 0; i < N; ++i) V[0][i] = r[i] / beta;
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
+    std::fill(Rg.begin(), Rg.end(), 0.0);
+    Rg[0] = 1.0;
     int j = 0;
     bool stop = false;
     for (; j < m && !stop; ++j) {
       precond(s, V[j].data(), Z[j].data());
       spmv(s.A, 1.0, Z[j].data(), 0.0, w.data(), false);
-      for (int i = 0; i <= j; ++i) h[i] = dot(V[i], w);
-      for (int i = 0; i <= j; ++i)
-        for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h[i] * V[i][q];
-      for (int i = 0; i <= j; ++i) h2[i] = dot(V[i], w);
-      for (int i = 0; i <= j; ++i)
-        for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h2[i] * V[i][q];
-      for (int i = 0; i <= j; ++i) h[i] = h[i] + h2[i];
-      double hn = nrm2(w);
-      if (hn != 0.0)
-        for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / hn;
+      double hn;
+      if (s.p.gmres_ortho != 1) {  // CGS2 (C11)
+        for (int i = 0; i <= j; ++i) h[i] = dot(V[i], w);
+        for (int i = 0; i <= j; ++i)
+          for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h[i] * V[i][q];
+        for (int i = 0; i <= j; ++i) h2[i] = dot(V[i], w);
+        for (int i = 0; i <= j; ++i)
+          for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h2[i] * V[i][q];
+        for (int i = 0; i <= j; ++i) h[i] = h[i] + h2[i];
+        hn = nrm2(w);
+        if (hn != 0.0)
+          for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / hn;
+      } else {
+        // two-pass Gram/Cholesky orthogonalisation (reading R22).  V holds t_i: once-
+        // orthogonalised unit vectors, t = Q R with Q orthonormal and R the Cholesky factor
+        // of G = t^T t.  p = t^T w; h = R^-T p (= Q^T w); w1 = w - t R^-1 h (= w - Q h);
+        // q = t^T w1, ||w1||; t_{j+1} = w1 / ||w1||; R(:, j+1) = R^-T q / ||w1||,
+        // R(j+1, j+1) = sqrt(1 - |R(0:j, j+1)|^2); H(:, j) = h + ||w1|| R(:, j+1).
+        const int k = j + 1;
+        vector<double> p(k), hv(k), cv(k), qv(k);
+        for (int i = 0; i < k; ++i) p[i] = dot(V[i], w);
+        for (int i = 0; i < k; ++i) {
+          double t = p[i];
+          for (int l = 0; l < i; ++l) t = t - Rg[(size_t)l * (m + 1) + i] * hv[l];
+          hv[i] = t / Rg[(size_t)i * (m + 1) + i];
+        }
+        for (int i = k - 1; i >= 0; --i) {
+          double t = hv[i];
+          for (int l = i + 1; l < k; ++l) t = t - Rg[(size_t)i * (m + 1) + l] * cv[l];
+          cv[i] = t / Rg[(size_t)i * (m + 1) + i];
+        }
+        for (int i = 0; i < k; ++i)
+          for (int64_t q = 0; q < N; ++q) w[q] = w[q] - cv[i] * V[i][q];
+        for (int i = 0; i < k; ++i) qv[i] = dot(V[i], w);
+        const double h0 = nrm2(w);
+        hn = h0;
+        if (h0 != 0.0) {
+          for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / h0;
+          double ss = 0.0;
+          for (int i = 0; i < k; ++i) {
+            double t = qv[i] / h0;
+            for (int l = 0; l < i; ++l) t = t - Rg[(size_t)l * (m + 1) + i] * Rg[(size_t)l * (m + 1) + k];
+            Rg[(size_t)i * (m + 1) + k] = t / Rg[(size_t)i * (m + 1) + i];
+            ss = ss + Rg[(size_t)i * (m + 1) + k] * Rg[(size_t)i * (m + 1) + k];
+          }
+          Rg[(size_t)k * (m + 1) + k] = 1.0 - ss > 0.0 ? std::sqrt(1.0 - ss) : 0.0;
+          for (int i = 0; i < k; ++i) hv[i] = hv[i] + h0 * Rg[(size_t)i * (m + 1) + k];
+          hn = h0 * Rg[(size_t)k * (m + 1) + k];
+        }
+        for (int i = 0; i < k; ++i) h[i] = hv[i];
+      }
       h[j + 1] = hn;
       for (int i = 0; i < j; ++i) {  // previous rotations
         double t = cs[i] * h[i] + sn[i] * h[i + 1];

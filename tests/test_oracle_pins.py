@@ -766,13 +766,43 @@ def test_dense_solve_small(rng, solver, kind):
     assert np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
 
 
-def test_gmres_finite_termination(rng):
+@pytest.mark.parametrize("ortho", [0, 1])
+def test_gmres_finite_termination(rng, ortho):
     n = 20
     ptr, col, val = random_bsr(rng, n, 1, density=1.0, dom=10)
     A = oracle.Mat.from_arrays(ptr, col, val)
-    S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=n, precond=oracle.PC_NONE)
-    r = S.solve(rng.standard_normal(n), rtol=1e-12)
+    S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=n, precond=oracle.PC_NONE, gmres_ortho=ortho)
+    b = rng.standard_normal(n)
+    r = S.solve(b, rtol=1e-12)
     assert r.converged and r.iters <= n
+    xd = np.linalg.solve(A.dense(), b)
+    assert np.linalg.norm(r.x - xd) <= 1e-9 * np.linalg.norm(xd)
+
+
+def test_gmres_two_pass_orthogonalisation_is_arnoldi(rng):
+    # the Gram/Cholesky two-pass orthogonalisation (R22) and CGS2 build the same Arnoldi
+    # process: on a non-normal operator without preconditioning the residual history (the
+    # GMRES minimal residuals, unique in exact arithmetic) agrees step by step, and with the
+    # AMG preconditioners the iteration counts and solutions agree
+    n = 60
+    ptr, col, val = random_bsr(rng, n, 1, density=0.2, dom=3)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    b = rng.standard_normal(n)
+    hs = []
+    for ortho in (0, 1):
+        S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=40, precond=oracle.PC_NONE, gmres_ortho=ortho)
+        hs.append(np.array(S.solve(b, rtol=1e-10, history=True).history))
+    k = min(len(hs[0]), len(hs[1]))
+    assert abs(len(hs[0]) - len(hs[1])) <= 1
+    assert np.allclose(hs[0][:k], hs[1][:k], rtol=1e-6, atol=1e-14)
+    for kind, pc in ((gen.STOKES, oracle.PC_SCHUR), (gen.POISSON3, oracle.PC_AMG)):
+        ptr, col, val = gen.matrix(kind, 8)
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        b = rng.standard_normal((len(ptr) - 1) * val.shape[-1])
+        rs = [oracle.Solver(A, solver=oracle.GMRES, precond=pc, gmres_ortho=o, coarse_enough=60).solve(b, rtol=1e-10)
+              for o in (0, 1)]
+        assert rs[0].iters == rs[1].iters and rs[0].converged and rs[1].converged
+        assert np.linalg.norm(rs[0].x - rs[1].x) <= 1e-8 * np.linalg.norm(rs[0].x)
 
 
 # ---- IDR(s) (Table 1: the paper's outer solver; reading R17) ----
