@@ -99,7 +99,8 @@ typedef struct {
   double over_interp;        /* AMG_PLAIN_AGG: A_c = (1/over_interp) P^T A P, default 1.5
                                 (over-interpolation, reading R19); ignored for AMG_SA */
   int32_t ilu_sweeps;        /* AMG_ILU0: Jacobi sweeps per triangular solve, 1..16, default 2 */
-  int32_t _reserved;
+  int32_t gmres_ortho;       /* AMG_GMRES orthogonalisation: 1 (default) two-pass Gram/Cholesky
+                                (reading R22); 0 CGS2 (three passes over the basis per step) */
 } amg_params;
 
 typedef struct {

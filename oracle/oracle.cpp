@@ -57,7 +57,7 @@ extern "C" void orc_params_default(orc_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
-  p->gmres_ortho = 0;
+  p->gmres_ortho = 1;
 }
 
 // ---------------------------------------------------------------- C0 containers

@@ -50,7 +50,7 @@ class amg_params(ctypes.Structure):
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
                 ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32),
                 ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32), ("over_interp", ctypes.c_double),
-                ("ilu_sweeps", ctypes.c_int32), ("_reserved", ctypes.c_int32)]
+                ("ilu_sweeps", ctypes.c_int32), ("gmres_ortho", ctypes.c_int32)]
 
 
 class amg_report(ctypes.Structure):

@@ -73,6 +73,8 @@ __device__ __forceinline__ void reduce_finish(double (&acc)[K], int kout, double
 // MODE 0: out[j] = s_j V_j . w                                   (scaled multi-dot)
 // MODE 1: w_out = w - sum_j c_j s_j V_j;  out[j] = s_j V_j . w_out   (update + next dot)
 // MODE 2: w_out = w - sum_j c_j s_j V_j;  out[0] = ||w_out||        (update + norm)
+// MODE 3: w_out = w - sum_j c_j s_j V_j;  out[j] = s_j V_j . w_out, out[k] = w_out . w_out
+//         (update + next dots + squared norm: the two-pass Gram/Cholesky orthogonalisation)
 // (v_j = s_j V_j: the basis is stored unnormalised with device scales sc)
 template <int K, int MODE>
 __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double* __restrict__ sc,
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
     c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
   }
   __syncthreads();
-  constexpr int KA = (MODE == 2) ? 1 : K;
+  constexpr int KA = (MODE == 2) ? 1 : (MODE == 3 ? K + 1 : K);
   double acc[KA];
 #pragma unroll
   for (int j = 0; j < KA; ++j) acc[j] = 0.0;
@@ -112,9 +114,10 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
 #pragma unroll
         for (int j = 0; j < K; ++j) v = fma(-c[j], vv[u][j], v);
         if (i < n) w_out[i] = v;
-        if constexpr (MODE == 1) {
+        if constexpr (MODE == 1 || MODE == 3) {
 #pragma unroll
           for (int j = 0; j < K; ++j) acc[j] = fma(sv[j] * vv[u][j], v, acc[j]);
+          if constexpr (MODE == 3) acc[K] = fma(v, v, acc[K]);
         } else {
           acc[0] = fma(v, v, acc[0]);
         }
@@ -223,9 +226,8 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
 #pragma unroll
       for (int ww = 0; ww < 8; ++ww) v -= part[ww][threadIdx.x];
       if (it < n) w_out[it] = v;
-      if constexpr (MODE == 2) {
-        nrm = fma(v, v, nrm);
-      } else {
+      if constexpr (MODE == 2 || MODE == 3) nrm = fma(v, v, nrm);
+      if constexpr (MODE != 2) {
         vs[threadIdx.x] = v;
         __syncthreads();
 #pragma unroll
@@ -257,7 +259,20 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
       const int j = warp + 8 * q;
       if (lane == 0 && own[q]) partials[(int64_t)j * gridDim.x + blockIdx.x] = v * sv[j];
     }
-    finish_partials(k, partials, ticket, out, post, inv);
+    if constexpr (MODE == 3) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
+      __syncthreads();
+      if (lane == 0) part[0][warp] = nrm;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += part[0][ww];
+        partials[(int64_t)k * gridDim.x + blockIdx.x] = s;
+      }
+    }
+    finish_partials(MODE == 3 ? k + 1 : k, partials, ticket, out, post, inv);
   }
 }
 
@@ -440,6 +455,17 @@ void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, co
 }
 
 __global__ void k_set_inv1(double* dst, const double* src) { *dst = 1.0 / *src; }
+
+void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
+                                const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
+                                CommBase* comm) {
+  if (k + 1 > 32) fail(AMG_EINVAL, "update + dots + norm: at most 31 vectors");
+  {
+    ProfScope ps_(prof_name("cgs_update_dots_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
+    launch_cgs<3>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s);
+  }
+  finalize_global(comm, out, k + 1, false, s);
+}
 
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                        double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s, CommBase* comm,

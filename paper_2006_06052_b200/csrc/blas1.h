@@ -31,6 +31,11 @@ void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, co
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                        double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s,
                        CommBase* comm = nullptr, double* inv_out = nullptr);
+// w_out = w - sum_j coef[j] sc[j] V_j, out[j] = sc[j] V_j . w_out (j < k), out[k] = w_out . w_out
+// (one pass; the Gram/Cholesky two-pass orthogonalisation of flexible GMRES)
+void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
+                                const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
+                                CommBase* comm = nullptr);
 // w -= sum_j coef[j] V_j  (coef: device)
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s);
 // x += sum_j y[j] Z_j  (Z of dtype zt, y: device)

@@ -292,6 +292,8 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   const int m = h.p.gmres_m;
   const int64_t N = c.N;
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hh(m + 1);
+  const bool gram = h.p.gmres_ortho == 1;
+  std::vector<double> R((size_t)(m + 1) * (m + 1), 0.0), hv(m + 1), cv(m + 1);  // Gram/Cholesky factor
   double* sc = h.dscal + 128;  // s_j
   // r = b - A x straight into V_0
   c.residual(b, x, h.V[0]);
@@ -311,6 +313,8 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     ++cycles;
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
+    std::fill(R.begin(), R.end(), 0.0);
+    R[0] = 1.0;  // t_0 = v_0 = r / beta
     int j = 0;
     bool stop = false;
     for (; j < m && !stop; ++j) {
@@ -319,14 +323,59 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
       c.spmv(h.Z[j], h.zt, w);
       PtrList Vl{};
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
-      launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);                 // h1 = v^T w
-      launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s, h.comm);   // w -= v h1; h2 = v^T w
-      launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s, h.comm,
-                        sc + j + 1);  // w -= v h2; ||w||; s_{j+1} = 1/||w||
-      c.bytes += 8.0 * N * (3.0 * (j + 1) + 5.0);
-      c.read(65);
-      for (int i = 0; i <= j; ++i) hh[i] = h.hscal[i] + h.hscal[32 + i];
-      const double hn = h.hscal[64];
+      double hn = 0.0;
+      if (!gram) {
+        launch_mdot_scaled(N, j + 1, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);                 // h1 = v^T w
+        launch_cgs_update(N, j + 1, Vl, sc, h.dscal, w, w, true, h.partials, h.dscal + 32, c.s, h.comm);   // w -= v h1; h2 = v^T w
+        launch_cgs_update(N, j + 1, Vl, sc, h.dscal + 32, w, w, false, h.partials, h.dscal + 64, c.s, h.comm,
+                          sc + j + 1);  // w -= v h2; ||w||; s_{j+1} = 1/||w||
+        c.bytes += 8.0 * N * (3.0 * (j + 1) + 5.0);
+        c.read(65);
+        for (int i = 0; i <= j; ++i) hh[i] = h.hscal[i] + h.hscal[32 + i];
+        hn = h.hscal[64];
+      } else {
+        // two-pass Gram/Cholesky orthogonalisation (reading R22): the stored vectors t_i (once
+        // orthogonalised, unit norm) are t = V R with G = t^T t = R^T R.  p = t^T w (pass 1);
+        // h = R^-T p = V^T w; w1 = w - t R^-1 h = w - V h (pass 2, with q = t^T w1, ||w1||^2);
+        // t_{j+1} = w1 / ||w1||; R's new column from G's (R^-T q / ||w1||);
+        // H(:, j) = h + ||w1|| R(:, j+1).
+        const int k = j + 1;
+        launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
+        c.read(k);
+        for (int i = 0; i < k; ++i) {  // h = R^-T p (forward substitution)
+          double t = h.hscal[i];
+          for (int l = 0; l < i; ++l) t -= R[(size_t)l * (m + 1) + i] * hv[l];
+          hv[i] = t / R[(size_t)i * (m + 1) + i];
+        }
+        for (int i = k - 1; i >= 0; --i) {  // c' = R^-1 h (back substitution)
+          double t = hv[i];
+          for (int l = i + 1; l < k; ++l) t -= R[(size_t)i * (m + 1) + l] * cv[l];
+          cv[i] = t / R[(size_t)i * (m + 1) + i];
+        }
+        for (int i = 0; i < k; ++i) h.hscal[96 + i] = cv[i];
+        AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+        launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm);
+        c.bytes += 8.0 * N * (2.0 * k + 4.0);
+        c.read(32 + k + 1);
+        hn = std::sqrt(std::max(h.hscal[32 + k], 0.0));
+        if (hn > 0.0 && finite(hn)) {
+          // R(:, k) = R^-T (q / hn), R(k, k) = sqrt(1 - |R(0:k, k)|^2)
+          double ss = 0.0;
+          for (int i = 0; i < k; ++i) {
+            double t = h.hscal[32 + i] / hn;
+            for (int l = 0; l < i; ++l) t -= R[(size_t)l * (m + 1) + i] * R[(size_t)l * (m + 1) + k];
+            R[(size_t)i * (m + 1) + k] = t / R[(size_t)i * (m + 1) + i];
+            ss += R[(size_t)i * (m + 1) + k] * R[(size_t)i * (m + 1) + k];
+          }
+          const double d2 = 1.0 - ss;
+          R[(size_t)k * (m + 1) + k] = d2 > 0.0 ? std::sqrt(d2) : 0.0;
+          for (int i = 0; i < k; ++i) hv[i] += hn * R[(size_t)i * (m + 1) + k];
+          hn *= R[(size_t)k * (m + 1) + k];
+        }
+        h.hscal[100 + m] = 1.0 / std::sqrt(std::max(h.hscal[32 + k], 0.0));  // s_{j+1}: t_{j+1} = s w1
+        AMG_CK(cudaMemcpyAsync(sc + j + 1, h.hscal + 100 + m, sizeof(double), cudaMemcpyHostToDevice, c.s));
+        for (int i = 0; i < k; ++i) hh[i] = hv[i];
+      }
       s_host = 1.0 / hn;
       hh[j + 1] = hn;
       for (int i = 0; i < j; ++i) {

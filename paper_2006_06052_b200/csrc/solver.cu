@@ -100,6 +100,7 @@ int check_params(const amg_params* p) {
   if (p->schur_shat < 0 || p->schur_shat > 2 || !(p->over_interp > 0.0)) return AMG_EINVAL;
   if (p->smoother < AMG_SPAI0 || p->smoother > AMG_ILU0) return AMG_EINVAL;
   if (p->smoother == AMG_ILU0 && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16)) return AMG_EINVAL;
+  if (p->gmres_ortho < 0 || p->gmres_ortho > 1) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;

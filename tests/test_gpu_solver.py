@@ -28,7 +28,7 @@ ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxit
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
           "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed",
           "schur_u_scalar": "schur_u_scalar", "coarsening": "coarsening", "schur_shat": "schur_shat",
-          "over_interp": "over_interp", "ilu_sweeps": "ilu_sweeps"}
+          "over_interp": "over_interp", "ilu_sweeps": "ilu_sweeps", "gmres_ortho": "gmres_ortho"}
 
 
 def make_pair(amg, ptr, col, val, hier32=True, **kw):
@@ -194,6 +194,12 @@ SOLVE_CASES = [
     ("ilu0-bicgstab-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, smoother=2), True),
     ("ilu0-sweeps3-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, smoother=2, ilu_sweeps=3),
      False),
+    # two-pass Gram/Cholesky orthogonalisation of flexible GMRES (R22)
+    ("gram-gmres-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
+    ("gram-gmres-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
+    ("gram-gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10, gmres_ortho=1),
+     False),
+    ("gram-gmres-poisson", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(precond=0, solver=2, gmres_ortho=1), False),
 ]
 
 
@@ -283,7 +289,7 @@ def test_error_codes(amg):
         amg.Solver(amg.BSR.from_numpy(ptr, col, v), coarse_enough=30)
     assert e.value.status == amg.ESINGULAR_BLOCK
     # bad params
-    for bad in (dict(gmres_m=40), dict(coarsening=2), dict(schur_shat=3), dict(over_interp=0.0)):
+    for bad in (dict(gmres_m=40), dict(coarsening=2), dict(schur_shat=3), dict(over_interp=0.0), dict(gmres_ortho=2)):
         with pytest.raises(amg.AmgError) as e:
             amg.Solver(amg.BSR.from_numpy(ptr, col, val), **bad)
         assert e.value.status == amg.EINVAL, bad
@@ -304,6 +310,20 @@ def test_fp32_vs_fp64_iteration_parity(amg):
         assert rep.converged
         its.append(rep.iters)
     assert abs(its[0] - its[1]) <= 1
+
+
+@pytest.mark.parametrize("wide", [1, 99])
+def test_gram_gmres_kernel_paths(amg, envvars, wide):
+    # the update + dots + norm pass on the wide (wide=1) and K-templated (wide=99) kernels
+    envvars(AMG_CGS_WIDE=wide)
+    n = 16
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2, gmres_ortho=1)
+    ro = O.solve(bvec, rtol=1e-8)
+    x, rep = _solve(amg, S, bvec)
+    true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+    assert rep.converged and true <= 1e-8 and abs(rep.iters - ro.iters) <= 2, (rep.iters, ro.iters, true)
 
 
 @pytest.mark.parametrize("wide,copy", [(1, "sell"), (99, "sell"), (1, "sellr")])

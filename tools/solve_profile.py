@@ -1,6 +1,6 @@
 """Per-kernel breakdown of one solve (library CUDA-event profiler, not a bench number).
 
-  python tools/solve_profile.py [cfg] [n] [idrs]     e.g. 5 256 | 4 128 | 3 64 | 5 256 idrs
+  python tools/solve_profile.py [cfg] [n] [idrs] [field=value ...]     e.g. 5 256 | 4 128 | 3 64 | 5 256 idrs
 Prints every (kernel, bytes/launch) record: launches, total ms, GB/s, share of the solve.
 """
 import os
@@ -21,8 +21,12 @@ ptr, col, val, bvec = bench.make_problem(cfg, n, 0, n ** 3)
 A = amg.BSR.from_numpy(ptr, col, val)
 del val
 prm = bench.params_for(amg, cfg)
-if len(sys.argv) > 3 and sys.argv[3] == "idrs":
-    prm.solver = amg.IDRS  # the paper's outer solver (Table 1), s = 5
+for a in sys.argv[3:]:
+    if a == "idrs":
+        prm.solver = amg.IDRS  # the paper's outer solver (Table 1), s = 5
+    elif "=" in a:  # any amg_params field, e.g. gmres_ortho=1
+        k, v = a.split("=")
+        setattr(prm, k, type(getattr(prm, k))(float(v)) if isinstance(getattr(prm, k), float) else int(v))
 S = amg.Solver(A, prm)
 del A
 for l in range(S.levels):
