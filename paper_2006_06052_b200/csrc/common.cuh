@@ -50,6 +50,7 @@ class Arena {
     void* p = nullptr;
     AMG_CK(cudaMalloc(&p, bytes));
     ptrs_.push_back(p);
+    sizes_.push_back((int64_t)bytes);
     total_ += (int64_t)bytes;
     return p;
   }
@@ -60,12 +61,25 @@ class Arena {
   void release() {
     for (void* p : ptrs_) cudaFree(p);
     ptrs_.clear();
+    sizes_.clear();
     total_ = 0;
+  }
+  // free one allocation of this arena early (no-op for foreign pointers)
+  void release_one(void* p) {
+    for (size_t i = 0; i < ptrs_.size(); ++i)
+      if (ptrs_[i] == p) {
+        cudaFree(p);
+        total_ -= sizes_[i];
+        ptrs_.erase(ptrs_.begin() + i);
+        sizes_.erase(sizes_.begin() + i);
+        return;
+      }
   }
   int64_t bytes() const { return total_; }
 
  private:
   std::vector<void*> ptrs_;
+  std::vector<int64_t> sizes_;
   int64_t total_ = 0;
 };
 

@@ -141,6 +141,15 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
     if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
     h->pmask_in = nullptr;
     if (workspace) alloc_workspace(*h, s);
+    // single-device solve handle: the interleaved copy carries every solve-phase product with
+    // A, so its BSR values (fp64, 15.5 GB at cfg 5) go (the pattern stays: the Schur views
+    // use it).  The distributed setup's global handle (workspace == false) keeps them for
+    // slicing.
+    if (workspace && M.lane_var == kLaneSellR && M.sell_vptr && !getenv("AMG_KEEP_OUTER_VALUES")) {
+      AMG_CK(cudaStreamSynchronize(s));
+      h->arena.release_one(M.val);
+      M.val = nullptr;
+    }
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));
   } catch (...) {
@@ -362,7 +371,8 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   if (!h || !out || n < 8) return AMG_EINVAL;
   auto mat = [&](const Mat& M) -> int64_t {
     if (!M.ptr) return 0;
-    return 4LL * (M.n + 1) + M.nnz * (4LL + (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt));
+    return 4LL * (M.n + 1) +
+           M.nnz * (4LL + (M.val ? (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt) : 0LL));
   };
   auto sell = [&](const Mat& M) -> int64_t {
     if ((M.lane_var != kLaneSell && M.lane_var != kLaneSellR) || !M.sell_ptr) return 0;
