@@ -339,6 +339,11 @@ def test_solve_forced_kernel_paths(amg, envvars, wide, copy):
     ptr, col, val = gen.matrix(gen.STOKES, n)
     bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
     A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2)
+    if copy == "sellr":  # the outer operator's BSR values (fp64) are released once its copy exists
+        envvars(AMG_KEEP_OUTER_VALUES=1)
+        S_keep = amg.Solver(A, S.params)
+        assert S_keep.memory_report()["outer_A"] - S.memory_report()["outer_A"] == len(col) * 16 * 8
+        del S_keep
     ro = O.solve(bvec, rtol=1e-8)
     x, rep = _solve(amg, S, bvec)
     true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
