@@ -57,7 +57,7 @@ extern "C" void orc_params_default(orc_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
-  p->gmres_ortho = 1;
+  p->gmres_ortho = 0;  // CGS2; 1 = the two-pass Gram/Cholesky variant (R22)
 }
 
 // ---------------------------------------------------------------- C0 containers
@@ -733,7 +733,9 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
     A = std::move(Ac);
     s.lv.push_back(std::move(L));
   }
-  if ((int64_t)A.n * A.b > 8192) return ORC_EINVAL;  // coarsening stalled: dense solve too large
+  // coarsening stalled: dense coarse solve too large (reading R7: a coarsest
+  // level above 8192 unknowns is an error on both sides)
+  if ((int64_t)A.n * A.b > 8192) return ORC_EINVAL;
   s.Acoarse = A;
   int rc = coarse_factor(A, s.coarse);
   if (rc != ORC_OK) return rc;

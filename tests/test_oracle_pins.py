@@ -149,6 +149,33 @@ def test_aggregation_1d_hand_trace():
     assert nc == g["n729_count"]
 
 
+def test_aggregation_pass2_lowest_index_neighbour():
+    # Hand-built graph where pass-2 node 3 touches two pass-1 aggregates (
+    # SURVEY.md C3 "lowest-index strong neighbour that was assigned in pass 1").
+    # Edges 0-4, 0-5, 1-2, 2-3, 3-5.  Pass 1: root 0 takes {0,4,5}; root 1 takes {1,2};
+    # node 3 is blocked (neighbours 2 and 5 assigned).  Pass 2: its lowest-index assigned
+    # neighbour is 2 (aggregate 1) -- not 5 (the last neighbour, aggregate 0) and not the
+    # lowest aggregate id (0).
+    n = 6
+    edges = {(0, 4), (0, 5), (1, 2), (2, 3), (3, 5)}
+    Dn = 4.0 * np.eye(n)
+    for i, j in edges:
+        Dn[i, j] = Dn[j, i] = -1.0
+    ptr, col, val = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if Dn[i, j] != 0:
+                col.append(j)
+                val.append(Dn[i, j])
+        ptr.append(len(col))
+    A = oracle.Mat.from_arrays(np.array(ptr, np.int32), np.array(col, np.int32),
+                               np.array(val).reshape(-1, 1, 1))
+    agg, nc = oracle.aggregate(A)
+    assert nc == 2
+    assert agg.tolist() == [0, 1, 1, 1, 0, 0]
+    assert oracle.roots(A).tolist() == [1, 1, 0, 0, 0, 0]
+
+
 def _graph(sp, sc, n):
     return [set(sc[sp[i]:sp[i + 1]].tolist()) for i in range(n)]
 
@@ -271,6 +298,125 @@ def test_smoothed_prolongator_partition_of_unity():
         x, y, z = i % n, (i // n) % n, i // (n * n)
         if 0 < x < n - 1 and 0 < y < n - 1 and 0 < z < n - 1:
             assert np.allclose(rs[i], np.eye(3), atol=1e-14)
+
+
+def test_smoothed_prolongator_1d_closed_form():
+    # 1-D Poisson (2,-1), omega = 2/3, aggregates {0,1},{2,3,4},{5,6,7,8} (C3 hand trace).
+    # P = (I - omega D^-1 A) P_tent written out by hand for this stencil (D = 2, all edges
+    # strong): a row whose both neighbours share its aggregate keeps 1; a row with one
+    # neighbour in another aggregate gets 1 - omega/2 = 2/3 at home and +omega/2 = 1/3 at
+    # the neighbour's aggregate; an end row (one neighbour, same aggregate) keeps 1 - 1/3.
+    ptr, col, val = poisson1d(9)
+    A, S = _solver(ptr, col, val, coarse_enough=2, hier_f32=0, vec_f32=0, max_levels=2)
+    P = S.level_mat(0, 1).dense()
+    t, h = 1.0 / 3.0, 2.0 / 3.0
+    expect = np.array([
+        [1 - t, 0, 0],   # node 0: end row, neighbour 1 in agg 0
+        [h, t, 0],       # node 1: neighbour 2 in agg 1
+        [t, h, 0],       # node 2: neighbour 1 in agg 0
+        [0, 1, 0],       # node 3
+        [0, h, t],       # node 4: neighbour 5 in agg 2
+        [0, t, h],       # node 5: neighbour 4 in agg 1
+        [0, 0, 1],       # node 6
+        [0, 0, 1],       # node 7
+        [0, 0, 1 - t],   # node 8: end row
+    ])
+    assert np.allclose(P, expect, rtol=0, atol=1e-15)
+
+
+def _weak_mix_bsr(rng, n, b, density, scale_share=0.35, scale=1e-4):
+    """Random symmetric-pattern BSR where a share of the off-diagonal block pairs is scaled
+    down so that they are weak at eps = 1e-3 (test input only)."""
+    ptr, col, val = random_bsr(rng, n, b, density=density, symmetric_pattern=True, dom=3 * b)
+    pos = {(i, int(col[k])): k for i in range(n) for k in range(ptr[i], ptr[i + 1])}
+    for (i, j), k in pos.items():
+        if i < j and rng.random() < scale_share:
+            val[k] *= scale
+            if rng.random() < 0.8:  # most pairs weak both ways, some only one way
+                val[pos[(j, i)]] *= scale
+    return ptr, col, val
+
+
+def _brute_strong(ptr, col, val, eps):
+    """Strength by brute force on the dense blocks: ||A_IJ||_F^2 > eps^2 ||A_II||_F ||A_JJ||_F,
+    then symmetric closure."""
+    n = len(ptr) - 1
+    blk = {(i, int(col[k])): val[k] for i in range(n) for k in range(ptr[i], ptr[i + 1])}
+    fro = lambda m: np.sqrt((m * m).sum())
+    s = set()
+    for (i, j), m in blk.items():
+        if i != j and (m * m).sum() > eps * eps * fro(blk[(i, i)]) * fro(blk[(j, j)]):
+            s.add((i, j))
+            s.add((j, i))
+    return blk, s
+
+
+@pytest.mark.parametrize("b", [1, 2, 3])
+def test_smoothed_prolongator_dense_with_weak_blocks(rng, b):
+    # SURVEY.md C5's own pin: a dense (I - omega D_F^-1 A_F) P_tent on random <= 64-row
+    # inputs, with >= 10 % weak blocks so that the lumping of weak blocks into D and the
+    # sign of the smoothing term both change P (PAPER.md:195, 209-211; SPEC.md:506).
+    n, eps, omega = 48, 1e-3, 2.0 / 3.0
+    ptr, col, val = _weak_mix_bsr(rng, n, b, density=0.12)
+    blk, strong = _brute_strong(ptr, col, val, eps)
+    offd = [(i, j) for (i, j) in blk if i != j]
+    weak = [e for e in offd if e not in strong]
+    assert len(weak) >= 0.1 * len(offd)
+    A, S = _solver(ptr, col, val, coarse_enough=b * 8, hier_f32=0, vec_f32=0, eps_strong=eps,
+                   sa_omega=omega)
+    agg = S.level_agg(0)
+    nc = int(agg.max()) + 1
+    # dense A_F: strong and diagonal blocks kept, weak ones added to the diagonal
+    AF = np.zeros((n * b, n * b))
+    for (i, j), m in blk.items():
+        if i == j or (i, j) in strong:
+            AF[i * b:(i + 1) * b, j * b:(j + 1) * b] += m
+        else:
+            AF[i * b:(i + 1) * b, i * b:(i + 1) * b] += m
+    Dinv = np.zeros_like(AF)
+    for i in range(n):
+        Dinv[i * b:(i + 1) * b, i * b:(i + 1) * b] = np.linalg.inv(AF[i * b:(i + 1) * b, i * b:(i + 1) * b])
+    Pt = np.zeros((n * b, nc * b))
+    for i in range(n):
+        if agg[i] >= 0:
+            Pt[i * b:(i + 1) * b, agg[i] * b:(agg[i] + 1) * b] = np.eye(b)
+    expect = (np.eye(n * b) - omega * Dinv @ AF) @ Pt
+    P = S.level_mat(0, 1).dense()
+    assert P.shape == expect.shape
+    assert np.abs(P - expect).max() <= 1e-12 * np.abs(expect).max()
+    # and the lumping is visible: without it P would differ by far more than rounding
+    AF_nolump = AF.copy()
+    for (i, j) in weak:
+        AF_nolump[i * b:(i + 1) * b, i * b:(i + 1) * b] -= blk[(i, j)]
+    assert not np.allclose(AF, AF_nolump, rtol=0, atol=1e-9)
+
+
+def test_smoothed_prolongator_partition_of_unity_with_weak_edges(rng):
+    # A zero-row-sum operator (a graph Laplacian) with weak couplings: lumping the weak
+    # blocks into the diagonal keeps A_F's row sums zero, so P's row sums equal P_tent's on
+    # EVERY row (SPEC.md:506, 510).  Dropping weak blocks without lumping breaks this.
+    n = 40
+    W = np.zeros((n, n))
+    for i in range(n):
+        for j in range(i + 1, n):
+            if rng.random() < 0.15 or j == i + 1:
+                W[i, j] = W[j, i] = (1e-5 if rng.random() < 0.3 else 1.0) * rng.uniform(0.5, 1.5)
+    L = np.diag(W.sum(axis=1)) - W
+    ptr = [0]
+    cols, vals = [], []
+    for i in range(n):
+        for j in range(n):
+            if i == j or W[i, j] != 0:
+                cols.append(j)
+                vals.append(L[i, j])
+        ptr.append(len(cols))
+    ptr, col, val = np.array(ptr, np.int32), np.array(cols, np.int32), np.array(vals).reshape(-1, 1, 1)
+    _, strong = _brute_strong(ptr, col, val, 1e-3)
+    assert sum(1 for i in range(n) for j in range(n) if W[i, j] != 0 and (i, j) not in strong) > 0
+    A, S = _solver(ptr, col, val, coarse_enough=8, hier_f32=0, vec_f32=0)
+    P = S.level_mat(0, 1).dense()
+    agg = S.level_agg(0)
+    assert np.allclose(P.sum(axis=1), (agg >= 0).astype(float), rtol=0, atol=1e-13)
 
 
 def test_galerkin_identity_and_symmetry(rng):

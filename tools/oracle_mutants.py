@@ -1,0 +1,57 @@
+"""Mutation check of the oracle pins (VERDICT r01 "What's weak" #1).
+
+Copies the repo (without .git) to a scratch directory, applies one source mutation
+to oracle/oracle.cpp, rebuilds the oracle there and runs the CPU pins
+(tests/test_oracle_pins.py).  A mutant is KILLED when at least one pin fails.
+Usage: python tools/oracle_mutants.py [name ...]
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# name -> (exact source text, replacement)
+MUTANTS = {
+    "sa_sign": ("p[r * b + c] = pt - omega * dt[r * b + c];",
+                "p[r * b + c] = pt + omega * dt[r * b + c];"),
+    "no_lumping": ("for (int e = 0; e < bb; ++e) D[e] = D[e] + A.blk(k)[e];",
+                   "for (int e = 0; e < bb; ++e) D[e] = D[e] + 0.0 * A.blk(k)[e];"),
+    "pass2_last": ("""      if (pass1[J] >= 0) {
+        agg[I] = pass1[J];
+        break;
+      }""", """      if (pass1[J] >= 0) {
+        agg[I] = pass1[J];
+      }"""),
+}
+DEFAULT = ["sa_sign", "no_lumping", "pass2_last"]
+
+
+def run(name: str) -> bool:
+    old, new = MUTANTS[name]
+    with tempfile.TemporaryDirectory(prefix=f"mut_{name}_") as d:
+        dst = os.path.join(d, "repo")
+        shutil.copytree(ROOT, dst, ignore=shutil.ignore_patterns(".git", "gpurun_out", "build", "*.so",
+                                                                 "__pycache__", "profiles"))
+        src = os.path.join(dst, "oracle", "oracle.cpp")
+        text = open(src).read()
+        assert text.count(old) == 1, f"mutation site for {name} not unique/found"
+        open(src, "w").write(text.replace(old, new))
+        subprocess.check_call([sys.executable, "-c", "import gen, oracle; gen.build(); oracle.build(True)"],
+                              cwd=dst)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_oracle_pins.py"],
+                           cwd=dst, capture_output=True, text=True)
+        tail = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-200:]
+        killed = r.returncode != 0
+        print(f"{name:12s} {'KILLED' if killed else 'SURVIVED'}  ({tail})", flush=True)
+        return killed
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or DEFAULT
+    ok = all([run(n) for n in names])
+    sys.exit(0 if ok else 1)
