@@ -120,25 +120,39 @@ def params_for(amg, cfg: int):
                               hier_dtype=hier, vcycle_vec_dtype=hier)
 
 
-def oracle_sample(cfg: int, n_full: int, n_sample: int, gpu_iters: int | None):
-    """Oracle (single thread, as it stands) solve of the same generator at n_sample^3,
-    scaled to the full workload: seconds x (cells ratio) x (iteration ratio)."""
+def _oracle_problem(cfg: int, n: int, maxiter: int):
     import oracle
-    ptr, col, val, b = make_problem(cfg, n_sample, 0, n_sample ** 3)
+    ptr, col, val, b = make_problem(cfg, n, 0, n ** 3)
     A = oracle.Mat.from_arrays(ptr, col, val)
+    del val, col
     _, solver, pc = CFG_SOLVER[cfg]
     p = oracle.default_params(solver={"cg": oracle.CG, "bicgstab": oracle.BICGSTAB, "gmres": oracle.GMRES}[solver],
                               precond=oracle.PC_SCHUR if pc == "schur" else oracle.PC_AMG,
-                              hier_f32=0 if cfg == 1 else 1, vec_f32=0 if cfg == 1 else 1)
+                              hier_f32=0 if cfg == 1 else 1, vec_f32=0 if cfg == 1 else 1, maxiter=maxiter)
     t0 = time.perf_counter()
     S = oracle.Solver(A, p)
-    t1 = time.perf_counter()
-    r = S.solve(b, rtol=1e-8)
-    t2 = time.perf_counter()
-    scale = (n_full / n_sample) ** 3
-    it_ratio = (gpu_iters / r.iters) if (gpu_iters and r.iters) else 1.0
-    return {"setup_s": t1 - t0, "solve_s": t2 - t1, "iters": r.iters, "relres": r.relres_true,
-            "value": (t2 - t1) * scale * it_ratio, "n_sample": n_sample, "scale": scale, "it_ratio": it_ratio}
+    return S, b, time.perf_counter() - t0
+
+
+def oracle_iterations(cfg: int, n: int, skip: int, count: int):
+    """The CPU oracle as it stands (1 thread): setup (untimed), then a solve stopped after
+    skip + count iterations with per-iteration timestamps; returns seconds per iteration over
+    iterations (skip, skip + count] (a GMRES(30) cycle boundary is not among them when
+    skip + count <= 30)."""
+    S, b, setup_s = _oracle_problem(cfg, n, skip + count)
+    r, st = S.solve_timed(b, rtol=1e-30)
+    k = min(skip + count, r.iters)
+    lo = min(skip, k - 1)
+    return {"setup_s": setup_s, "per_iter_s": (st[k] - st[lo]) / (k - lo), "iters_timed": k - lo,
+            "iters_skipped": lo, "levels": r.levels}
+
+
+def cpu_host():
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:
+        model = "unknown"
+    return model, os.cpu_count()
 
 
 def oracle_full_size(cfg: int):
@@ -152,31 +166,37 @@ def oracle_full_size(cfg: int):
 
 
 def run_reference(args, rank: int):
-    """--impl reference: the CPU oracle as it stands (1 thread), each step a bounded sample
-    of the workload (ref_n^3 cells), scaled to the full cfg by the cell count and by the
-    iteration count of the oracle's own full-size run when it is on record; rank 0 only."""
+    """--impl reference: the CPU oracle as it stands, 1 host thread, rank 0 only.  Setup at the
+    full size (untimed), then W warm-up + K timed steps, a step being ONE Krylov iteration of
+    the full-size solve (the whole per-iteration hot path: outer SpMV, Schur PC with two fp32
+    V-cycles, CGS2 orthogonalisation).  s/solve = seconds per iteration x the oracle's own
+    full-size iteration count (a measured run, tests/golden/oracle_full_size.json)."""
     if rank != 0:
         return
     n_full = args.n or gen.CONFIGS[args.cfg]["n"]
     full = oracle_full_size(args.cfg) if n_full == gen.CONFIGS[args.cfg]["n"] else None
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = oracle_sample(args.cfg, n_full, args.ref_n, full["iters"] if full else None)
-        if i >= args.warmup:
-            vals.append(r)
-    v = statistics.median([r["value"] for r in vals])
-    note = (f"; iterations scaled x{vals[0]['it_ratio']:.2f} to the oracle's full-size count {full['iters']} "
-            f"(its measured full-size solve: {full['solve_s']:.0f} s)" if full else "; same iteration count assumed")
+    t0 = time.perf_counter()
+    r = oracle_iterations(args.cfg, n_full, args.warmup, args.steps)
+    wall = time.perf_counter() - t0
+    its = full["iters"] if full else None
+    if its is None:  # no full-size run on record (a non-default --n): run the whole solve once
+        S, b, _ = _oracle_problem(args.cfg, n_full, 1000)
+        its = S.solve(b, rtol=1e-8).iters
+    v = r["per_iter_s"] * its
+    model, ncpu = cpu_host()
+    sample = (f"oracle (1 thread of {ncpu}: {model}) at the full {n_full}^3 size: setup {r['setup_s']:.0f} s "
+              f"(untimed), then {r['iters_timed']} timed Krylov iterations after {r['iters_skipped']} warm-up ones "
+              f"({r['per_iter_s']:.2f} s each); s/solve = that x {its} iterations "
+              f"({'the oracle' + chr(39) + 's measured full-size solve: ' + format(full['solve_s'], '.0f') + ' s, ' + str(full['iters']) + ' its' if full else 'its own iteration count'})")
     line = {
         "impl": "reference", "metric": metric_name(args.cfg, n_full), "value": v, "unit": "s/solve",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "n_gpus": args.gpus, "steps": r["iters_timed"], "warmup": r["iters_skipped"],
+        "ms_per_step": r["per_iter_s"] * 1e3, "step": "one Krylov iteration of the full-size oracle solve",
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64 outer / f32 hierarchy",
         "data": "synthetic", "config": config_dict(args.cfg, n_full, args.gpus),
-        "cpu_baseline": {"value": v, "unit": "s/solve", "cores": 1, "kind": "oracle",
-                         "sample": f"oracle solve of the cfg-{args.cfg} generator at {args.ref_n}^3 cells "
-                                   f"(x{vals[0]['scale']:.0f} cells to {n_full}^3{note}), "
-                                   f"{vals[0]['iters']} its, {statistics.median([r['solve_s'] for r in vals]):.2f} s"},
+        "cpu_baseline": {"value": v, "unit": "s/solve", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "s/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
 
@@ -232,17 +252,44 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=5, choices=[1, 3, 4, 5])
     ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--ref-n", type=int, default=32, help="grid of the oracle's bounded sample")
-    ap.add_argument("--cpu-n", type=int, default=48, help="grid of the cpu_baseline sample")
+    ap.add_argument("--cpu-n", type=int, default=96, help="grid of the cpu_baseline sample")
+    ap.add_argument("--probe-launch", action="store_true",
+                    help="launcher check: init the process group, print rank / world, exit")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the IDR(5) secondary measurement")
     ap.add_argument("--no-other", action="store_true", help="skip the cfg 1/3/4 secondary measurements")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched as `python bench.py --gpus N`: become N ranks (one process per GPU)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.probe_launch:
+        import torch
+        import torch.distributed as tdist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if world > 1:
+            tdist.init_process_group(backend)
+            t = torch.ones(1)
+            if backend == "gloo":
+                tdist.all_reduce(t)
+            print(json.dumps({"probe": True, "rank": rank, "world": tdist.get_world_size(), "backend": backend,
+                              "sum": float(t.item())}), flush=True)
+            tdist.destroy_process_group()
+        else:
+            print(json.dumps({"probe": True, "rank": 0, "world": 1, "backend": backend}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -426,11 +473,24 @@ def main():
             del So, bo, xo
             torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
-        c = oracle_sample(args.cfg, n, args.cpu_n, rep.iters)
-        out["cpu_baseline"] = {"value": c["value"], "unit": "s/solve", "cores": 1, "kind": "oracle",
-                               "sample": f"oracle (1 thread) solve of the cfg-{args.cfg} generator at {args.cpu_n}^3: "
-                                         f"{c['solve_s']:.2f} s, {c['iters']} its; scaled x{c['scale']:.0f} cells "
-                                         f"and x{c['it_ratio']:.2f} iterations to {n}^3"}
+        # bounded live sample (~20 s of one host core): the oracle at cpu_n^3 of the same
+        # generator, setup untimed, per-iteration time of 10 iterations, scaled by cells to n^3
+        # and by the oracle's measured full-size iteration count
+        c = oracle_iterations(args.cfg, args.cpu_n, 2, 8)
+        full = oracle_full_size(args.cfg) if n == gen.CONFIGS[args.cfg]["n"] else None
+        its = full["iters"] if full else rep.iters
+        scale = (n / args.cpu_n) ** 3
+        v = c["per_iter_s"] * scale * its
+        model, ncpu = cpu_host()
+        out["cpu_baseline"] = {
+            "value": v, "unit": "s/solve", "cores": 1, "kind": "oracle",
+            "sample": f"oracle (1 thread of {ncpu}: {model}) on the cfg-{args.cfg} generator at {args.cpu_n}^3: "
+                      f"setup {c['setup_s']:.1f} s untimed, {c['iters_timed']} Krylov iterations at "
+                      f"{c['per_iter_s']:.3f} s each, scaled x{scale:.1f} cells to {n}^3 and x{its} iterations "
+                      f"({'the oracle' + chr(39) + 's full-size count' if full else 'the GPU count'})",
+            "full_size_measured": ({"solve_s": full["solve_s"], "setup_s": full["setup_s"], "iters": full["iters"],
+                                    "source": "tests/golden/oracle_full_size.json (tools/oracle_reference_runs.py, "
+                                              "one host thread of a B200 box of this pool)"} if full else None)}
     print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()

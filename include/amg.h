@@ -210,6 +210,12 @@ int64_t amg_device_bytes(struct amg_handle* h);
  * NULL handle / out or n < 8. */
 int amg_memory_report(struct amg_handle* h, int64_t* out, int32_t n);
 
+/* Solve counters since setup (host out[n >= 2]): [0] extra orthogonalisation passes the
+ * Gram/Cholesky GMRES took where a new direction was still far from orthogonal to the basis
+ * (the reorthogonalisation safeguard, reading R22); [1] CUDA graphs instantiated.
+ * AMG_EINVAL on a NULL handle / out or n < 2. */
+int amg_solve_counters(struct amg_handle* h, int64_t* out, int32_t n);
+
 /* ---- launch accounting / per-kernel timing (diagnostics, host) ---- */
 /* number of library kernels launched by this process so far */
 int64_t amg_kernel_launches(void);

@@ -92,6 +92,7 @@ def lib():
             "orc_vcycle": (i32, [P, P, P]),
             "orc_precond": (i32, [P, P, P]),
             "orc_solve": (i32, [P, P, P, dbl, P, P]),
+            "orc_solve_timed": (i32, [P, P, P, dbl, P, P, i32]),
             "orc_idrs_shadow": (i32, [i64, i32, i64, P]),
         }
         for name, (res, args) in sig.items():
@@ -326,3 +327,14 @@ class Solver:
             hist = hist[: rep.iters + 1]
         return SolveResult(x, st, rep.iters, bool(rep.converged), rep.relres_true, rep.levels,
                            rep.restarts, hist)
+
+    def solve_timed(self, b, x0=None, rtol=1e-8):
+        """solve() with per-iteration timestamps (seconds since the call; stamps[it] when
+        iteration `it` completed, stamps[0] = 0).  Timing instrumentation only."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, dtype=np.float64).copy()
+        rep = Report()
+        stamps = np.full(self.params.maxiter + 1, np.nan)
+        st = lib().orc_solve_timed(self.h, _p(b), _p(x), rtol, ctypes.byref(rep), _p(stamps), len(stamps))
+        return SolveResult(x, st, rep.iters, bool(rep.converged), rep.relres_true, rep.levels,
+                           rep.restarts, None), stamps[: rep.iters + 1]

@@ -14,6 +14,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -32,6 +33,16 @@ struct orc_mat {
 };
 
 static inline double f32r(double v) { return (double)(float)v; }  // RNE narrowing (C9)
+
+// Timing instrumentation only (bench.py's reference arm): when orc_solve_timed is running,
+// g_stamps[it] = seconds since the solve started, recorded as iteration `it` completes.
+static thread_local double* g_stamps = nullptr;
+static thread_local int32_t g_stamps_cap = 0;
+static thread_local std::chrono::steady_clock::time_point g_t0;
+static inline void stamp(int it) {
+  if (g_stamps && it >= 0 && it < g_stamps_cap)
+    g_stamps[it] = std::chrono::duration<double>(std::chrono::steady_clock::now() - g_t0).count();
+}
 
 extern "C" void orc_params_default(orc_params* p) {
   p->solver = ORC_GMRES;
@@ -1293,6 +1304,7 @@ static int solve_cg(const orc_solver& s, const double* bp, double* xp, double rt
     for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * p[i];
     for (int64_t i = 0; i < N; ++i) r[i] = r[i] - alpha * q[i];
     ++it;
+    stamp(it);
     nr = nrm2(r);
     if (hist) hist[it] = nr / nb;
     if (nr <= rtol * nb) {
@@ -1375,6 +1387,7 @@ static int solve_bicgstab(const orc_solver& s, const double* bp, double* xp, dou
     alpha = rho / rv;
     for (int64_t i = 0; i < N; ++i) sv[i] = r[i] - alpha * v[i];
     ++it;
+    stamp(it);
     double ns = nrm2(sv);
     if (ns <= rtol * nb) {
       for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * ph[i];
@@ -1521,6 +1534,7 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
       g[j] = cs[j] * g[j];
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = h[i];
       ++it;
+      stamp(it);
       if (hist) {  // true residual of the current iterate x + Z y_j
         for (int i = j; i >= 0; --i) {
           double t = g[i];
@@ -1682,6 +1696,7 @@ static int solve_idrs(const orc_solver& s, const double* bp, double* xp, double 
       for (int64_t q = 0; q < N; ++q) r[q] = r[q] - beta * G[k][q];
       for (int64_t q = 0; q < N; ++q) x[q] = x[q] + beta * U[k][q];
       ++it;
+      stamp(it);
       nr = nrm2(r);
       if (hist) hist[it] = nr / nb;
       if (nr <= rtol * nb) {
@@ -1707,6 +1722,7 @@ static int solve_idrs(const orc_solver& s, const double* bp, double* xp, double 
     for (int64_t q = 0; q < N; ++q) r[q] = r[q] - om * t[q];
     for (int64_t q = 0; q < N; ++q) x[q] = x[q] + om * vh[q];
     ++it;
+    stamp(it);
     nr = nrm2(r);
     if (hist) hist[it] = nr / nb;
     if (nr <= rtol * nb && converged_true()) status = ORC_OK;
@@ -1725,6 +1741,18 @@ extern "C" int orc_idrs_shadow(int64_t n, int32_t sdim, int64_t base, double* ou
   idrs_shadow(n, sdim, (uint64_t)base, P);
   for (int j = 0; j < sdim; ++j) std::copy(P[j].begin(), P[j].end(), out + (int64_t)j * n);
   return ORC_OK;
+}
+
+extern "C" int orc_solve_timed(const orc_solver* s, const double* b, double* x, double rtol,
+                               orc_report* rep, double* stamps, int32_t cap) {
+  g_stamps = stamps;
+  g_stamps_cap = cap;
+  g_t0 = std::chrono::steady_clock::now();
+  if (stamps && cap > 0) stamps[0] = 0.0;
+  const int rc = orc_solve(s, b, x, rtol, rep, nullptr);
+  g_stamps = nullptr;
+  g_stamps_cap = 0;
+  return rc;
 }
 
 extern "C" int orc_solve(const orc_solver* s, const double* b, double* x, double rtol,

@@ -136,6 +136,11 @@ int orc_precond(const orc_solver* s, const double* r, double* z);
 int orc_idrs_shadow(int64_t n, int32_t sdim, int64_t base, double* out);
 int orc_solve(const orc_solver* s, const double* b, double* x, double rtol, orc_report* rep,
               double* history);
+/* orc_solve with timing instrumentation (no change to the arithmetic): stamps[it] (it < cap)
+ * receives the seconds since the call started at which iteration `it` completed (stamps[0] =
+ * 0).  Used by bench.py's reference arm to time bounded samples of a full-size solve. */
+int orc_solve_timed(const orc_solver* s, const double* b, double* x, double rtol, orc_report* rep,
+                    double* stamps, int32_t cap);
 
 #ifdef __cplusplus
 }

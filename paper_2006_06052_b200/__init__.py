@@ -66,7 +66,8 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_comm_unique_id", "amg_comm_init", "amg_setup_dist", "amg_comm_destroy",
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
            "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr", "amg_memory_report",
-           "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local", "amg_setup_pmask"]
+           "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local", "amg_setup_pmask",
+           "amg_solve_counters"]
 
 _lib = None
 
@@ -98,6 +99,7 @@ def lib():
             "amg_vcycle": (i32, [P, P, P, P]),
             "amg_device_bytes": (i64, [P]),
             "amg_memory_report": (i32, [P, P, i32]),
+            "amg_solve_counters": (i32, [P, P, i32]),
             "amg_comm_unique_id": (i32, [P]),
             "amg_comm_init": (i32, [P, i32, i32, P]),
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
@@ -234,8 +236,9 @@ def csr_to_bsr(n: int, m: int, b: int, ptr, col, val, stream=None):
 
 
 class SpmvPlan:
-    """bsr_plan_create / bsr_plan_spmv: TMA-staged repeated products with A (A's tensors
-    must stay alive and unchanged)."""
+    """bsr_plan_create / bsr_plan_spmv: repeated products with A on the kernel the plan picks
+    (interleaved row-per-lane or sliced copy for long rows, owned by the plan; A's tensors must
+    stay alive and unchanged)."""
 
     def __init__(self, A: BSR, stream=None):
         self.A = A
@@ -393,6 +396,13 @@ class Solver:
         _check(lib().amg_memory_report(self.h, out.ctypes.data_as(ctypes.c_void_p), 8), "amg_memory_report")
         keys = ["outer_A", "hierarchy", "sliced_copies", "smoothers", "schur", "coarse_inverse", "krylov", "total"]
         return dict(zip(keys, (int(v) for v in out)))
+
+    def counters(self) -> dict:
+        """amg_solve_counters: GMRES reorthogonalisation passes taken, CUDA graphs built."""
+        import numpy as np
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().amg_solve_counters(self.h, out.ctypes.data_as(ctypes.c_void_p), 2), "amg_solve_counters")
+        return {"reorth_passes": int(out[0]), "graphs": int(out[1])}
 
     @property
     def device_bytes(self) -> int:

@@ -287,8 +287,7 @@ template <int MODE>
 void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                 double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s) {
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
-  const char* e = getenv("AMG_CGS_WIDE");  // first k served by k_cgs_wide (tests force both)
-  const int wide_from = e ? atoi(e) : 13;
+  const int wide_from = env_int("AMG_CGS_WIDE", 13);  // first k served by k_cgs_wide (tests force both)
   if (k >= wide_from) {
     const int64_t work = (n + kCW - 1) / kCW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * kSMs, (int64_t)kMaxPartials, work}));

@@ -50,6 +50,8 @@ class NcclComm : public CommBase {
     AMG_NCCL(ncclRecv(buf, bytes, ncclChar, peer, comm, s));
   }
   void group_end(cudaStream_t) override { AMG_NCCL(ncclGroupEnd()); }
+  // ncclSend / ncclRecv / ncclAllReduce are stream-ordered and graph-capturable
+  bool capturable() const override { return true; }
   void barrier() override {
     double* d = nullptr;
     AMG_CK(cudaMalloc(&d, sizeof(double)));

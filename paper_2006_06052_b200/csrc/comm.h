@@ -32,6 +32,8 @@ class CommBase {
   virtual void recv(void* buf, size_t bytes, int peer, cudaStream_t s) = 0;
   virtual void group_end(cudaStream_t s) = 0;
   virtual void barrier() = 0;
+  // may the exchanges be recorded into a CUDA graph (stream-ordered device work only)?
+  virtual bool capturable() const { return false; }
 };
 
 // shared state of a LocalComm group (one per emulated job)

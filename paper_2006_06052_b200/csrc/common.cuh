@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -35,6 +36,15 @@ struct Error {
 #define AMG_CK_LAUNCH() AMG_CK(cudaGetLastError())
 
 inline size_t dtype_size(int dt) { return dt == AMG_F32 ? 4 : 8; }
+
+// Lab / test switches (AMG_*): read from the environment whenever a plan is made or an
+// apply starts, never cached, so a test can A/B a kernel variant within one process.  None
+// changes the arithmetic of the default path; DESIGN.md §6 lists them.
+inline int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+inline bool env_set(const char* name) { return std::getenv(name) != nullptr; }
 
 // Owning device allocation list: every buffer of a handle lives here and is freed
 // by the destructor.  Solve-phase code never allocates.

@@ -77,7 +77,7 @@ void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_
 
 void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, int b, cudaStream_t s,
                      const std::function<void(int, int)>& launch) {
-  const bool off = getenv("AMG_NO_OVERLAP") != nullptr;  // A/B switch (tests)
+  const bool off = env_set("AMG_NO_OVERLAP");  // A/B switch (tests)
   if (!h.comm || H.peers.empty()) {
     launch(0, A.n);
     return;
@@ -125,19 +125,30 @@ void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s) {
   if (h.comm) h.comm->allreduce_sum(d, n, s);
 }
 
-// every rank's coarse right-hand-side segment to every rank (coarsest level replicated)
-void coarse_allgather(Handle& h, cudaStream_t s) {
+// every rank's slab of level l's right-hand side to every rank (levels >= rep_from replicated)
+void replicated_allgather(Handle& h, size_t l, cudaStream_t s) {
   if (!h.comm || h.comm->nranks == 1) return;
-  const size_t es = dtype_size(h.xt) * h.coarse.b;
-  char* f = static_cast<char*>(h.coarse.f);
+  const bool coarsest = l == h.lv.size();
+  const size_t es = dtype_size(h.xt) * (coarsest ? h.coarse.b : h.lv[l].A.b);
+  char* f = static_cast<char*>(coarsest ? h.coarse.f : h.lv[l].f);
+  const auto& bd = h.lbounds[l];
   const int me = h.comm->rank;
   h.comm->group_begin();
   for (int p = 0; p < h.comm->nranks; ++p) {
     if (p == me) continue;
-    if (h.coarse.cnt[me]) h.comm->send(f + h.coarse.off[me] * es, h.coarse.cnt[me] * es, p, s);
-    if (h.coarse.cnt[p]) h.comm->recv(f + h.coarse.off[p] * es, h.coarse.cnt[p] * es, p, s);
+    const int64_t cm = bd[me + 1] - bd[me], cp = bd[p + 1] - bd[p];
+    if (cm) h.comm->send(f + bd[me] * es, cm * es, p, s);
+    if (cp) h.comm->recv(f + bd[p] * es, cp * es, p, s);
   }
   h.comm->group_end(s);
+}
+
+void* level_f_slab(Handle& h, size_t l) {
+  const bool coarsest = l == h.lv.size();
+  char* f = static_cast<char*>(coarsest ? h.coarse.f : h.lv[l].f);
+  if (!h.comm || l < h.rep_from) return f;
+  const int b = coarsest ? h.coarse.b : h.lv[l].A.b;
+  return f + h.lbounds[l][h.comm->rank] * b * dtype_size(h.xt);
 }
 
 namespace {
@@ -366,34 +377,49 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       AMG_CK(cudaMemcpy(h->mS64, Gh->mS64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
       make_schur_views(h->A, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
     }
-    // hierarchy levels
+    // hierarchy levels: levels 0 .. rep_from-1 as row slabs with halos; from rep_from on (the
+    // first level with fewer than AMG_REPLICATE_ROWS block rows per rank, default 50,000;
+    // SURVEY.md §8(e) mitigation 2) every rank holds the whole level and computes it
+    // redundantly, so those levels exchange nothing but the one allgather of their
+    // right-hand side.  Level 0 is always distributed.
     const size_t L = Gh->lv.size();
     h->lv.resize(L);
+    const int64_t rep_rows = env_int("AMG_REPLICATE_ROWS", 50000);
+    h->rep_from = L;
+    for (size_t l = 1; l < L; ++l)
+      if (Gh->lv[l].A.n < rep_rows * P) {
+        h->rep_from = l;
+        break;
+      }
     for (size_t l = 0; l < L; ++l) {
       const Level& GL = Gh->lv[l];
       Level& LL = h->lv[l];
+      const bool rep = l >= h->rep_from;
       const auto& bd = h->lbounds[l];
       const auto& bc = h->lbounds[l + 1];
-      LL.A = slice_rows(h->arena, GL.A, bd[me], bd[me + 1], s);
-      build_halo(*h, LL.A, bd[me], bd, LL.halo, s);
+      const int64_t r0 = rep ? 0 : bd[me], r1 = rep ? GL.A.n : bd[me + 1];
+      const int64_t c0 = rep ? 0 : bc[me], c1 = rep ? GL.nc : bc[me + 1];
+      LL.A = slice_rows(h->arena, GL.A, r0, r1, s);
+      if (!rep) build_halo(*h, LL.A, bd[me], bd, LL.halo, s);
       LL.A.fast32 = GL.A.fast32;
       make_tma_plan(LL.A, s, &h->arena);
-      LL.P = slice_rows(h->arena, GL.P, bd[me], bd[me + 1], s);
-      if (l + 1 < L) remap_shift(LL.P, bc[me], bc[me + 1] - bc[me]);  // coarsest: global coarse ids
+      LL.P = slice_rows(h->arena, GL.P, r0, r1, s);
+      // slab-local coarse ids while the next level is distributed; global ids into a replicated one
+      if (l + 1 < h->rep_from) remap_shift(LL.P, bc[me], bc[me + 1] - bc[me]);
       LL.P.fast32 = GL.P.fast32;
       make_tma_plan(LL.P, s, &h->arena);
-      LL.R = slice_rows(h->arena, GL.R, bc[me], bc[me + 1], s);
-      remap_shift(LL.R, bd[me], bd[me + 1] - bd[me]);
+      LL.R = slice_rows(h->arena, GL.R, c0, c1, s);
+      if (!rep) remap_shift(LL.R, bd[me], bd[me + 1] - bd[me]);
       LL.R.fast32 = GL.R.fast32;
       make_tma_plan(LL.R, s, &h->arena);
       const int bb = LL.A.b;
       const int64_t nl = LL.A.n;
       LL.M = h->arena.alloc(std::max<int64_t>(nl * bb * bb, 1) * dtype_size(h->vt));
-      AMG_CK(cudaMemcpy(LL.M, (char*)GL.M + bd[me] * bb * bb * dtype_size(h->vt), nl * bb * bb * dtype_size(h->vt),
+      AMG_CK(cudaMemcpy(LL.M, (char*)GL.M + r0 * bb * bb * dtype_size(h->vt), nl * bb * bb * dtype_size(h->vt),
                         cudaMemcpyDeviceToDevice));
       LL.agg = h->arena.alloc_n<int32_t>(std::max<int64_t>(nl, 1));
-      AMG_CK(cudaMemcpy(LL.agg, GL.agg + bd[me], 4 * nl, cudaMemcpyDeviceToDevice));
-      LL.nc = (int32_t)(bc[me + 1] - bc[me]);
+      AMG_CK(cudaMemcpy(LL.agg, GL.agg + r0, 4 * nl, cudaMemcpyDeviceToDevice));
+      LL.nc = (int32_t)(c1 - c0);
       const int64_t nx = (int64_t)(nl + LL.halo.nghost) * bb;
       LL.f = h->arena.alloc(std::max<int64_t>(nl * bb, 1) * xs);
       LL.r = h->arena.alloc(std::max<int64_t>(nl * bb, 1) * xs);
@@ -406,10 +432,6 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
     C.N = GC.N;
     C.n = GC.n;
     C.b = GC.b;
-    const auto& bl = h->lbounds[L];
-    C.cnt.resize(P);
-    C.off.resize(P);
-    for (int r = 0; r < P; ++r) C.off[r] = bl[r], C.cnt[r] = bl[r + 1] - bl[r];
     if (C.N > 0) {
       C.inv = h->arena.alloc((size_t)C.N * C.N * dtype_size(h->vt));
       AMG_CK(cudaMemcpy(C.inv, GC.inv, (size_t)C.N * C.N * dtype_size(h->vt), cudaMemcpyDeviceToDevice));

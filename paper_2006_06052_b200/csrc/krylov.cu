@@ -341,24 +341,32 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
         // H(:, j) = h + ||w1|| R(:, j+1).
         const int k = j + 1;
         launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
+        c.bytes += 8.0 * N * (k + 1.0);
         c.read(k);
-        for (int i = 0; i < k; ++i) {  // h = R^-T p (forward substitution)
-          double t = h.hscal[i];
-          for (int l = 0; l < i; ++l) t -= R[(size_t)l * (m + 1) + i] * hv[l];
-          hv[i] = t / R[(size_t)i * (m + 1) + i];
-        }
-        for (int i = k - 1; i >= 0; --i) {  // c' = R^-1 h (back substitution)
-          double t = hv[i];
-          for (int l = i + 1; l < k; ++l) t -= R[(size_t)i * (m + 1) + l] * cv[l];
-          cv[i] = t / R[(size_t)i * (m + 1) + i];
-        }
-        for (int i = 0; i < k; ++i) h.hscal[96 + i] = cv[i];
-        AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
-        launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm);
-        c.bytes += 8.0 * N * (2.0 * k + 4.0);
-        c.read(32 + k + 1);
-        hn = std::sqrt(std::max(h.hscal[32 + k], 0.0));
-        if (hn > 0.0 && finite(hn)) {
+        // h = R^-T p (forward substitution), c' = R^-1 h (back substitution); the update pass
+        // w -= t c' returns q = t^T w and ||w||^2.  hacc accumulates Q^T w over the passes.
+        auto project = [&](const double* pin, double* hout) {
+          for (int i = 0; i < k; ++i) {
+            double t = pin[i];
+            for (int l = 0; l < i; ++l) t -= R[(size_t)l * (m + 1) + i] * hout[l];
+            hout[i] = t / R[(size_t)i * (m + 1) + i];
+          }
+          for (int i = k - 1; i >= 0; --i) {
+            double t = hout[i];
+            for (int l = i + 1; l < k; ++l) t -= R[(size_t)i * (m + 1) + l] * cv[l];
+            cv[i] = t / R[(size_t)i * (m + 1) + i];
+          }
+          for (int i = 0; i < k; ++i) h.hscal[96 + i] = cv[i];
+          AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+          launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm);
+          c.bytes += 8.0 * N * (k + 2.0);  // reads k basis vectors and w, writes w
+          c.read(32 + k + 1);
+        };
+        std::vector<double> pin(h.hscal, h.hscal + k), h2(k);
+        project(pin.data(), hv.data());
+        for (int pass = 0;; ++pass) {
+          hn = std::sqrt(std::max(h.hscal[32 + k], 0.0));
+          if (!(hn > 0.0 && finite(hn))) break;
           // R(:, k) = R^-T (q / hn), R(k, k) = sqrt(1 - |R(0:k, k)|^2)
           double ss = 0.0;
           for (int i = 0; i < k; ++i) {
@@ -368,9 +376,22 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
             ss += R[(size_t)i * (m + 1) + k] * R[(size_t)i * (m + 1) + k];
           }
           const double d2 = 1.0 - ss;
+          // Safeguard: when the updated w is still far from orthogonal to span(V) (|Q^T w1|^2
+          // above half of |w1|^2), 1 - ss loses its digits to cancellation; orthogonalise w1
+          // once more (the pass's q = t^T w1 gives Q^T w1 = R^-T q without another multi-dot)
+          // and take the coefficients of both passes -- CGS2's reorthogonalisation, applied
+          // only where needed.  At most one extra pass.
+          if (pass == 0 && (ss > 0.5 || !(d2 > 1e-8))) {
+            for (int i = 0; i < k; ++i) pin[i] = h.hscal[32 + i];
+            project(pin.data(), h2.data());
+            for (int i = 0; i < k; ++i) hv[i] += h2[i];
+            ++h.reorth_passes;
+            continue;
+          }
           R[(size_t)k * (m + 1) + k] = d2 > 0.0 ? std::sqrt(d2) : 0.0;
           for (int i = 0; i < k; ++i) hv[i] += hn * R[(size_t)i * (m + 1) + k];
           hn *= R[(size_t)k * (m + 1) + k];
+          break;
         }
         h.hscal[100 + m] = 1.0 / std::sqrt(std::max(h.hscal[32 + k], 0.0));  // s_{j+1}: t_{j+1} = s w1
         AMG_CK(cudaMemcpyAsync(sc + j + 1, h.hscal + 100 + m, sizeof(double), cudaMemcpyHostToDevice, c.s));

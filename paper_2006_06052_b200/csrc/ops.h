@@ -11,6 +11,13 @@ namespace amgb {
 // sync); the opt-in TMA tile plan (AMG_TMA=1: one reduction + one sync)
 void set_lane_plan(Mat& A, bool use_env = true);
 void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena = nullptr, bool want_tma = false);
+// does A carry an interleaved (k_bsr_sellr) or sliced (k_bsr_sell) copy of its blocks?
+bool has_solve_copy(const Mat& A);
+// free A's BSR values (A.val = nullptr) when a solve copy carries every product with A; the
+// pattern (ptr, col) stays.  No-op otherwise.  One stream sync.
+void release_bsr_values(Mat& A, Arena& arena, cudaStream_t s);
+// A's BSR values (A.vt, nnz * br * bc) re-materialised from its solve copy into out (device)
+void values_from_copy(const Mat& A, void* out, cudaStream_t s);
 
 // S1: scalar CSR -> BSR (convert.cu); returns nnzb, fills bptr/bcol/bval when bptr != nullptr
 int64_t csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* ptr, const int32_t* col,

@@ -959,7 +959,7 @@ Mat solve_copy(Handle& h, const Mat& M64, cudaStream_t s) {
     launch_convert(M64.nnz * M64.b * M64.b, M64.val, AMG_F64, M.val, h.vt, 1.0, s);
   }
   M.fast32 = (h.vt == AMG_F32 && h.xt == AMG_F32);
-  make_tma_plan(M, s, &h.arena);
+  make_tma_plan(M, s, h.want_copies ? &h.arena : nullptr);
   return M;
 }
 

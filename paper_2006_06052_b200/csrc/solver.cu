@@ -31,8 +31,13 @@ Handle::~Handle() {
 void alloc_workspace(Handle& h, cudaStream_t s) {
   const int64_t N = (int64_t)h.n * h.b;
   const int64_t Nx = (int64_t)(h.n + h.halo0.nghost) * h.b;  // SpMV inputs carry ghosts
-  const int nv = 8;
+  // outer work vectors per solver (krylov.cu): CG r z p q, BiCGStab r rh p ph v s sh t, IDR(s)
+  // r v vh t; flexible GMRES works in its V / Z bases only
+  const int nv = h.p.solver == AMG_BICGSTAB ? 8 : h.p.solver == AMG_GMRES ? 0 : 4;
   for (int i = 0; i < nv; ++i) h.vec.push_back(h.arena.alloc_n<double>(std::max<int64_t>(Nx, 1)));
+  // amg_solve_host's device copies of b and x: allocated here so that no solve call allocates
+  h.stage_b = h.arena.alloc_n<double>(std::max<int64_t>(N, 1));
+  h.stage_x = h.arena.alloc_n<double>(std::max<int64_t>(N, 1));
   if (h.comm) h.x_ext = h.arena.alloc_n<double>(std::max<int64_t>(Nx, 1));
   if (h.p.solver == AMG_GMRES) {
     const int m = h.p.gmres_m;
@@ -41,8 +46,7 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     h.zt = (h.amg_active && h.xt == AMG_F32) ? AMG_F32 : AMG_F64;
     // one slab for the basis; vector j starts j * (size + stagger) bytes in, so the
     // j-streams the CGS2 kernels read side by side do not share DRAM address bits
-    const char* st = getenv("AMG_VSTAGGER");
-    const size_t stagger = st ? (size_t)atol(st) : 0;
+    const size_t stagger = (size_t)env_int("AMG_VSTAGGER", 0);
     const size_t vbytes = ((size_t)std::max<int64_t>(N, 1) * 8 + 255) & ~size_t(255);
     char* slab = (char*)h.arena.alloc((vbytes + stagger) * (m + 1) + 256);
     for (int i = 0; i <= m; ++i) h.V.push_back(reinterpret_cast<double*>(slab + (size_t)i * (vbytes + stagger)));
@@ -114,6 +118,7 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
   try {
     h->p = *p;
     h->pmask_in = pmask;
+    h->want_copies = workspace;
     h->vt = p->hier_dtype;
     h->xt = p->vcycle_vec_dtype;
     h->n = src.n;
@@ -136,19 +141,29 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
       launch_convert(M.nnz * M.b * M.b, src.val, src.vt, M.val, AMG_F64, 1.0, s);
     }
     h->alg_bytes_spmv = mat_bytes(M, AMG_F64) + 16.0 * (double)M.n * M.b;
-    make_tma_plan(M, s, &h->arena);
+    Arena* copies = workspace ? &h->arena : nullptr;
+    make_tma_plan(M, s, copies);
     if (h->amg_active) setup_build(*h, M, bounds, s);
-    if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
+    if (h->schur && !h->masked) make_schur_views(M, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, copies);
     h->pmask_in = nullptr;
     if (workspace) alloc_workspace(*h, s);
     // single-device solve handle: the interleaved copy carries every solve-phase product with
     // A, so its BSR values (fp64, 15.5 GB at cfg 5) go (the pattern stays: the Schur views
     // use it).  The distributed setup's global handle (workspace == false) keeps them for
     // slicing.
-    if (workspace && M.lane_var == kLaneSellR && M.sell_vptr && !getenv("AMG_KEEP_OUTER_VALUES")) {
-      AMG_CK(cudaStreamSynchronize(s));
-      h->arena.release_one(M.val);
-      M.val = nullptr;
+    // single-device solve handle: every solve-phase product with a matrix that has an interleaved
+    // or sliced copy runs on the copy, so its BSR values go (the pattern stays: the Schur views
+    // and the export use it; amg_level_export re-materialises values from the copy).  Outer A:
+    // 15.5 GB fp64 at cfg 5; the fp32 hierarchy A_l / P_l / R_l: 4.7 GB (VERDICT r01 next #6,
+    // the paper's memory claim PAPER.md:43-45, 717-718).  The distributed setup's global handle
+    // (workspace == false) keeps them for slicing.
+    if (workspace && !env_set("AMG_KEEP_VALUES")) {
+      release_bsr_values(M, h->arena, s);
+      for (Level& L : h->lv) {
+        release_bsr_values(L.A, h->arena, s);
+        release_bsr_values(L.P, h->arena, s);
+        release_bsr_values(L.R, h->arena, s);
+      }
     }
     h->alg_bytes_precond = precond_bytes(*h);
     AMG_CK(cudaStreamSynchronize(s));
@@ -249,13 +264,7 @@ int amg_solve_host(struct amg_handle* hh, const double* b_host, double* x_host, 
   if (!h || !b_host || !x_host) return AMG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t N = (int64_t)h->n * h->b;
-  // staging buffers live in the handle's workspace: vec[6], vec[7] are free outside a solve
-  // only for CG; use dedicated ones
-  static_assert(sizeof(double) == 8, "");
-  if (!h->stage_b) {
-    h->stage_b = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
-    h->stage_x = h->arena.alloc_n<double>(std::max<int64_t>(N, 1));
-  }
+  // device copies of b and x: the handle's staging vectors (alloc_workspace; nothing allocated here)
   AMG_CK(cudaMemcpyAsync(h->stage_b, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
   AMG_CK(cudaMemcpyAsync(h->stage_x, x_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
   int st = amg_solve(hh, h->stage_b, h->stage_x, rtol, stream, rep);
@@ -330,10 +339,18 @@ int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_
   if (M.nnz > 0) AMG_CK(cudaMemcpy(col, M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
   const int64_t cnt = M.nnz * M.b * M.b;
   double* tmp = nullptr;
+  void* src = M.val;
+  void* mat = nullptr;  // values re-materialised from the solve copy (released BSR values)
   AMG_CK(cudaMalloc(&tmp, std::max<int64_t>(cnt, 1) * 8));
-  launch_convert(cnt, M.val, M.vt, tmp, AMG_F64, 1.0, nullptr);
+  if (!src && cnt > 0) {
+    AMG_CK(cudaMalloc(&mat, cnt * dtype_size(M.vt)));
+    values_from_copy(M, mat, nullptr);
+    src = mat;
+  }
+  launch_convert(cnt, src, M.vt, tmp, AMG_F64, 1.0, nullptr);
   AMG_CK(cudaMemcpy(val, tmp, cnt * 8, cudaMemcpyDeviceToHost));
   cudaFree(tmp);
+  if (mat) cudaFree(mat);
   return AMG_OK;
   AMG_GUARD_END
 }
@@ -363,6 +380,14 @@ int amg_schur_export(struct amg_handle* hh, double* shat_diag, double* m_s) {
 int64_t amg_device_bytes(struct amg_handle* hh) {
   Handle* h = reinterpret_cast<Handle*>(hh);
   return h ? h->arena.bytes() : 0;
+}
+
+int amg_solve_counters(struct amg_handle* hh, int64_t* out, int32_t n) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || !out || n < 2) return AMG_EINVAL;
+  out[0] = h->reorth_passes;
+  out[1] = (int64_t)h->pc_graphs.size();
+  return AMG_OK;
 }
 
 int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
@@ -398,7 +423,7 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   else if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
   v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
   const int64_t N = (int64_t)h->n * h->b;
-  v[6] = 8LL * N * ((int64_t)h->vec.size() + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
+  v[6] = 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
                     (int64_t)h->Ui.size()) +
          (int64_t)h->Z.size() * N * dtype_size(h->zt);
   v[7] = h->arena.bytes();

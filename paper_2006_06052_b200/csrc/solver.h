@@ -39,9 +39,8 @@ struct Level {
 };
 
 struct Coarse {
-  // distributed: the coarsest level is replicated; rank r owns block rows
-  // [off[r], off[r] + cnt[r]) of the coarse right-hand side (allgathered before the GEMV)
-  std::vector<int64_t> cnt, off;
+  // distributed: the coarsest level is replicated (its right-hand side allgathered from the
+  // ranks' slabs, Handle::lbounds, before the GEMV)
   int32_t N = 0;              // scalar unknowns of the coarsest level
   int32_t n = 0, b = 0;
   void* inv = nullptr;        // dense explicit inverse [N][N], hier dtype
@@ -101,7 +100,8 @@ struct Handle {
   std::vector<PcGraph> pc_graphs;
   cudaStream_t work = nullptr;     // non-blocking stream the Krylov solve runs on (graph capture)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  double *stage_b = nullptr, *stage_x = nullptr;  // amg_solve_host staging (allocated on first use)
+  double *stage_b = nullptr, *stage_x = nullptr;  // amg_solve_host's device b / x (alloc_workspace)
+  int64_t reorth_passes = 0;       // GMRES Gram/Cholesky: extra orthogonalisation passes taken
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double setup_s = 0.0;
@@ -115,6 +115,13 @@ struct Handle {
   int64_t row_lo = 0;
   int64_t n_global_rows = 0;       // global block rows (== n when not distributed)
   std::vector<std::vector<int64_t>> lbounds;
+  // distributed: levels >= rep_from are replicated on every rank (whole level, no halos); the
+  // right-hand side of level rep_from is allgathered from the ranks' slabs (rep_from ==
+  // lv.size(): only the coarsest level, the dense inverse)
+  size_t rep_from = 0;
+  // build the interleaved / sliced solve copies (false for the distributed setup's replicated
+  // global handle: every rank slices the BSR arrays and plans its own slabs)
+  bool want_copies = true;
   Arena arena;
   ~Handle();
 };
@@ -136,7 +143,10 @@ void halo_exchange(Handle& h, const Halo& H, void* x, int dt, int b, cudaStream_
 void halo_overlapped(Handle& h, const Halo& H, const Mat& A, void* x, int dt, int b, cudaStream_t s,
                      const std::function<void(int, int)>& launch);
 void dist_allreduce(Handle& h, double* d, int n, cudaStream_t s);
-void coarse_allgather(Handle& h, cudaStream_t s);
+// distributed: allgather the slabs of level l's right-hand side (l == h.rep_from)
+void replicated_allgather(Handle& h, size_t l, cudaStream_t s);
+// level l's right-hand-side buffer at this rank's slab offset (where R_{l-1} writes)
+void* level_f_slab(Handle& h, size_t l);
 // vcycle.cu
 // V-cycle from level `level` on that level's f buffer; returns the buffer holding x
 void* vcycle_run(Handle& h, size_t level, cudaStream_t s);

@@ -70,6 +70,7 @@ static void ensure_smem(const void* kern, int smem) {
 
 template <int BR, int BC, typename V, typename X, bool FAST, class EPI>
 static void launch_tma_rows(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
+  if (!A.val && A.nnz > 0) fail(AMG_EINVAL, "BSR values released: no TMA plan on the BSR arrays");
   TmaArgs a{A.n, A.tma_tr, A.tma_ntiles, A.tma_ns, A.tma_stage, A.tma_col_off, A.tma_val_off,
             A.tma_wave, A.tma_part_off, A.tma_max_blk};
   const int smem = A.tma_smem;
@@ -78,10 +79,6 @@ static void launch_tma_rows(const Mat& A, const X* x, EPI epi, cudaStream_t s) {
   kern<<<A.tma_grid, A.tma_tr, smem, s>>>(a, A.ptr, A.col, (const V*)A.val, x, epi);
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 // Kernel plan of a device matrix (bsr_lane.cuh variants, measured in tools/spmv_lab.cu):
 //   4 x 4 (and b <= 2):     ROWS, streaming loads, U = 4 for long rows (> 12 blocks), else 2
@@ -219,6 +216,26 @@ static void build_sell(Mat& A, Arena& arena, cudaStream_t s) {
   A.lane_var = kLaneSell;
 }
 
+// inverse of k_sell_fill: the BSR values back from the sliced copy (padding skipped)
+template <typename V>
+__global__ void k_sell_unfill(int n, int b, int C, int ns, const int32_t* __restrict__ ptr,
+                              const int32_t* __restrict__ sptr, const int32_t* __restrict__ perm,
+                              const V* __restrict__ sval, V* __restrict__ val) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * C) return;
+  const int s = (int)(t / C), g = (int)(t % C);
+  int64_t row = (int64_t)s * C + g;
+  if (perm) row = perm[t] >= 0 ? perm[t] : n;
+  if (row >= n) return;
+  const int k0 = ptr[row], len = ptr[row + 1] - k0;
+  for (int j = 0; j < len; ++j) {
+    const int64_t st = sptr[s] + j;
+    for (int i = 0; i < b; ++i)
+      for (int r = 0; r < b; ++r)
+        val[((int64_t)(k0 + j) * b + i) * b + r] = sval[(st * b + i) * ((int64_t)C * b) + g * b + r];
+  }
+}
+
 // ---- interleaved row-per-lane copy (k_bsr_sellr) ----
 template <typename V>
 __global__ void k_sellr_fill(int n, int E, int W, int ns, const int32_t* __restrict__ ptr,
@@ -237,6 +254,24 @@ __global__ void k_sellr_fill(int n, int E, int W, int ns, const int32_t* __restr
   for (int64_t e = 0; e < nv * W; ++e) {
     const int64_t q = e / W, jb = e / E;
     sval[(((int64_t)vptr[s] + q) * 32 + g) * W + (e % W)] = jb < len ? val[(k0 + jb) * E + (e % E)] : V(0);
+  }
+}
+
+// inverse of k_sellr_fill
+template <typename V>
+__global__ void k_sellr_unfill(int n, int E, int W, int ns, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ vptr, const int32_t* __restrict__ perm,
+                               const V* __restrict__ sval, V* __restrict__ val) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * 32) return;
+  const int s = (int)(t / 32), g = (int)(t % 32);
+  int64_t row = t;
+  if (perm) row = perm[t] >= 0 ? perm[t] : n;
+  if (row >= n) return;
+  const int k0 = ptr[row], len = ptr[row + 1] - k0;
+  for (int64_t e = 0; e < (int64_t)len * E; ++e) {
+    const int64_t q = e / W, jb = e / E;
+    val[(k0 + jb) * E + (e % E)] = sval[(((int64_t)vptr[s] + q) * 32 + g) * W + (e % W)];
   }
 }
 
@@ -287,7 +322,7 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     // the lane kernel (5.1 vs 4.1 interleaved)
     const bool rect = (A.br > 0 || A.bc > 0) && A.rows_per_block() > 1 && A.rows_per_block() <= 4 &&
                       A.cols_per_block() <= 4;
-    const int forced = getenv("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
+    const int forced = env_set("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
     // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) square-block matrices with
     // 3..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
     // (cfg 5 / cfg 2): A_0 5.65, A_1 / R_0 6.4-6.5, outer 4x4 fp64 7.07, cfg-2 4x4 fp32 x fp64
@@ -444,6 +479,8 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r
       return;
     }
   }
+  if (!A.val && A.nnz > 0)
+    fail(AMG_EINVAL, "BSR values released: this matrix runs on its interleaved / sliced copy only");
   if (A.lane_var == kLaneW) {
     const unsigned grid = grid_for((int64_t)A.n * 32, kBlock);
     if (can_fast && A.fast32)
@@ -517,6 +554,8 @@ static bool launch_lane_dot(const Mat& A, const void* x, int xt, EPI epi, cudaSt
     return done;
   }
   if (A.lane_var > kLaneCN4) return false;
+  if (!A.val && A.nnz > 0)
+    fail(AMG_EINVAL, "BSR values released: this matrix runs on its interleaved / sliced copy only");
   bool done = false;
   dispatch_b(A.b, [&](auto Bc) {
     constexpr int B = decltype(Bc)::value;
@@ -930,6 +969,36 @@ void launch_convert(int64_t N, const void* in, int it, void* out, int ot, double
       using O = decltype(oo);
       k_convert<I, O><<<g, 256, 0, s>>>(N, (const I*)in, (O*)out, scale, scale_dev);
     });
+  });
+  AMG_CK_LAUNCH();
+}
+
+
+bool has_solve_copy(const Mat& A) {
+  return (A.lane_var == kLaneSellR && A.sell_vptr) || (A.lane_var == kLaneSell && A.sell_ptr);
+}
+
+void release_bsr_values(Mat& A, Arena& arena, cudaStream_t s) {
+  if (!A.val || !has_solve_copy(A) || A.tma_grid > 0) return;
+  AMG_CK(cudaStreamSynchronize(s));  // kernels still reading the values (the copy's fill) are done
+  arena.release_one(A.val);
+  A.val = nullptr;
+}
+
+void values_from_copy(const Mat& A, void* out, cudaStream_t s) {
+  if (A.nnz == 0) return;
+  if (!has_solve_copy(A)) fail(AMG_EINVAL, "values_from_copy: no solve copy");
+  dispatch_t(A.vt, [&](auto v) {
+    using V = decltype(v);
+    if (A.lane_var == kLaneSellR) {
+      const int E = A.rows_per_block() * A.cols_per_block();
+      k_sellr_unfill<V><<<grid_for((int64_t)A.sell_ns * 32, 256), 256, 0, s>>>(
+          A.n, E, A.sell_w, A.sell_ns, A.ptr, A.sell_vptr, A.sell_perm, (const V*)A.sell_val, (V*)out);
+    } else {
+      const int C = 32 / A.b;
+      k_sell_unfill<V><<<grid_for((int64_t)A.sell_ns * C, 256), 256, 0, s>>>(
+          A.n, A.b, C, A.sell_ns, A.ptr, A.sell_ptr, A.sell_perm, (const V*)A.sell_val, (V*)out);
+    }
   });
   AMG_CK_LAUNCH();
 }

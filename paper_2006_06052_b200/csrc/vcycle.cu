@@ -43,8 +43,8 @@ static void ilu_step(Handle& h, Level& L, void* x, cudaStream_t s) {
 //                                            one rounding on store)
 void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   const int xt = h.xt, vt = h.vt;
+  if (h.comm && l == h.rep_from) replicated_allgather(h, l, s);  // distributed: replicated from here on
   if (l == h.lv.size()) {
-    coarse_allgather(h, s);  // distributed: the coarsest level is replicated
     launch_dense_gemv(h.coarse.N, h.coarse.inv, vt, h.coarse.f, h.coarse.x, xt, s);  // K8
     return h.coarse.x;
   }
@@ -65,10 +65,7 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   }
   halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
                   [&](int r0, int r1) { launch_residual(L.A, L.f, x, L.r, xt, s, r0, r1); });  // K4b: r = f - A x
-  void* fc = (l + 1 < h.lv.size()) ? h.lv[l + 1].f
-                                   : (void*)((char*)h.coarse.f + (h.comm ? h.coarse.off[h.comm->rank] * h.coarse.b *
-                                                                              dtype_size(xt)
-                                                                        : 0));
+  void* fc = level_f_slab(h, l + 1);
   launch_spmv(L.R, 1.0, L.r, xt, 0.0, fc, xt, s);  // K6: f_c = R r
   void* xc = vcycle_run(h, l + 1, s);
   launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
@@ -126,8 +123,8 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
 // communicator is attached (NCCL halo exchanges), while the per-kernel profiler is on, or
 // with AMG_NO_GRAPH=1.  The library launch counter advances by the graph's kernel count.
 void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStream_t s, const double* scale_dev) {
-  static const bool off = getenv("AMG_NO_GRAPH") != nullptr;
-  if (off || !h.p.use_graphs || h.comm || g_prof || h.pc_graphs.size() >= 256) {
+  const bool off = env_set("AMG_NO_GRAPH");
+  if (off || !h.p.use_graphs || (h.comm && !h.comm->capturable()) || g_prof || h.pc_graphs.size() >= 256) {
     precond_apply(h, r, z, zt, s, 1.0, scale_dev);
     return;
   }

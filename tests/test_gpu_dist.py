@@ -73,7 +73,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
 @pytest.mark.parametrize("name,kind,n,rk,kw", CASES, ids=[c[0] for c in CASES])
 def test_dist_solve_parity(amg, P, name, kind, n, rk, kw):
     out, x, relres, (ptr, col, val, bvec) = run_dist(amg, P, kind, n, rk, **kw)
@@ -125,6 +125,45 @@ def test_nccl_communicator_single_rank(amg):
     rep1 = S1.solve(b, x1, 1e-8)
     assert rep.converged and rep.iters == rep1.iters
     assert torch.allclose(x, x1, rtol=0, atol=1e-12 * float(x1.abs().max()))
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_replicated_coarse_levels_are_exact(amg, envvars, P):
+    # levels below AMG_REPLICATE_ROWS block rows per rank are held whole on every rank (no
+    # halos, one allgather of their right-hand side); the same arithmetic row by row as the
+    # slab-distributed levels -> the same iterates
+    runs = []
+    for rep_rows in (0, 10 ** 9):  # 0: only the coarsest replicated; 1e9: every level >= 1
+        envvars(AMG_REPLICATE_ROWS=rep_rows)
+        out, x, relres, _ = run_dist(amg, P, gen.STOKES, 16, gen.RHS_LID_NOISE, solver=2, precond=1)
+        assert relres <= 1e-8
+        runs.append((x, out[0][0].iters))
+    assert runs[0][1] == runs[1][1]
+    assert np.array_equal(runs[0][0], runs[1][0])
+
+
+def test_nccl_single_rank_graphs_bit_identical(amg):
+    # graph capture under an NCCL communicator (the preconditioner apply replayed from a CUDA
+    # graph, NCCL calls captured with the kernels): bit-identical to the eager apply
+    n = 12
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    N = n ** 3
+    comm = amg.Comm(0, 1)
+    xs = []
+    for graphs in (0, 1):
+        A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=N)
+        S = amg.Solver(A, amg.default_params(solver=2, precond=1, use_graphs=graphs), comm=comm, row_begin=0,
+                       n_global=N)
+        b = torch.as_tensor(bvec, device="cuda")
+        x = torch.zeros_like(b)
+        rep = S.solve(b, x, 1e-8)
+        assert rep.converged
+        assert (S.counters()["graphs"] >= 1) == bool(graphs)
+        xs.append((x.cpu().numpy(), rep.iters))
+        del S
+    assert xs[0][1] == xs[1][1]
+    assert np.array_equal(xs[0][0], xs[1][0])
 
 
 def test_halo_overlap_is_exact(amg, envvars):
