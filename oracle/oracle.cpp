@@ -184,6 +184,12 @@ static double dot(const vector<double>& a, const vector<double>& b) {
   return s;
 }
 static double nrm2(const vector<double>& a) { return std::sqrt(dot(a, a)); }
+// a^T b with a's entries rounded to fp32 first (the fp32 shadow basis of reading R23)
+static double dot_f32_basis(const vector<double>& a, const vector<double>& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s = s + f32r(a[i]) * b[i];
+  return s;
+}
 
 // ---------------------------------------------------------------- block helpers
 // Frobenius norm squared, row-major order (C2 reading: Frobenius).
@@ -1464,7 +1470,7 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
       precond(s, V[j].data(), Z[j].data());
       spmv(s.A, 1.0, Z[j].data(), 0.0, w.data(), false);
       double hn;
-      if (s.p.gmres_ortho != 1) {  // CGS2 (C11)
+      if (s.p.gmres_ortho == 0) {  // CGS2 (C11)
         for (int i = 0; i <= j; ++i) h[i] = dot(V[i], w);
         for (int i = 0; i <= j; ++i)
           for (int64_t q = 0; q < N; ++q) w[q] = w[q] - h[i] * V[i][q];
@@ -1482,25 +1488,31 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
         // q = t^T w1, ||w1||; t_{j+1} = w1 / ||w1||; R(:, j+1) = R^-T q / ||w1||,
         // R(j+1, j+1) = sqrt(1 - |R(0:j, j+1)|^2); H(:, j) = h + ||w1|| R(:, j+1).
         const int k = j + 1;
-        vector<double> p(k), hv(k), cv(k), qv(k);
-        for (int i = 0; i < k; ++i) p[i] = dot(V[i], w);
-        for (int i = 0; i < k; ++i) {
-          double t = p[i];
-          for (int l = 0; l < i; ++l) t = t - Rg[(size_t)l * (m + 1) + i] * hv[l];
-          hv[i] = t / Rg[(size_t)i * (m + 1) + i];
-        }
-        for (int i = k - 1; i >= 0; --i) {
-          double t = hv[i];
-          for (int l = i + 1; l < k; ++l) t = t - Rg[(size_t)i * (m + 1) + l] * cv[l];
-          cv[i] = t / Rg[(size_t)i * (m + 1) + i];
-        }
-        for (int i = 0; i < k; ++i)
-          for (int64_t q = 0; q < N; ++q) w[q] = w[q] - cv[i] * V[i][q];
-        for (int i = 0; i < k; ++i) qv[i] = dot(V[i], w);
-        const double h0 = nrm2(w);
-        hn = h0;
-        if (h0 != 0.0) {
-          for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / h0;
+        vector<double> p(k), hv(k), cv(k), qv(k), h2v(k);
+        // pass 1; gmres_ortho = 2 (reading R23): the dots read the basis rounded to fp32
+        for (int i = 0; i < k; ++i) p[i] = s.p.gmres_ortho == 2 ? dot_f32_basis(V[i], w) : dot(V[i], w);
+        // project(pin): hout = R^-T pin, cv = R^-1 hout, w = w - t cv, qv = t^T w
+        auto project = [&](const vector<double>& pin, vector<double>& hout) {
+          for (int i = 0; i < k; ++i) {
+            double t = pin[i];
+            for (int l = 0; l < i; ++l) t = t - Rg[(size_t)l * (m + 1) + i] * hout[l];
+            hout[i] = t / Rg[(size_t)i * (m + 1) + i];
+          }
+          for (int i = k - 1; i >= 0; --i) {
+            double t = hout[i];
+            for (int l = i + 1; l < k; ++l) t = t - Rg[(size_t)i * (m + 1) + l] * cv[l];
+            cv[i] = t / Rg[(size_t)i * (m + 1) + i];
+          }
+          for (int i = 0; i < k; ++i)
+            for (int64_t q = 0; q < N; ++q) w[q] = w[q] - cv[i] * V[i][q];
+          for (int i = 0; i < k; ++i) qv[i] = dot(V[i], w);
+        };
+        project(p, hv);
+        hn = 0.0;
+        for (int pass = 0;; ++pass) {
+          const double h0 = nrm2(w);
+          hn = h0;
+          if (h0 == 0.0) break;
           double ss = 0.0;
           for (int i = 0; i < k; ++i) {
             double t = qv[i] / h0;
@@ -1508,9 +1520,17 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
             Rg[(size_t)i * (m + 1) + k] = t / Rg[(size_t)i * (m + 1) + i];
             ss = ss + Rg[(size_t)i * (m + 1) + k] * Rg[(size_t)i * (m + 1) + k];
           }
+          // reorthogonalisation safeguard: w still far from orthogonal to span(V)
+          if (pass == 0 && (ss > 0.5 || !(1.0 - ss > 1e-8))) {
+            project(qv, h2v);
+            for (int i = 0; i < k; ++i) hv[i] = hv[i] + h2v[i];
+            continue;
+          }
+          for (int64_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / h0;
           Rg[(size_t)k * (m + 1) + k] = 1.0 - ss > 0.0 ? std::sqrt(1.0 - ss) : 0.0;
           for (int i = 0; i < k; ++i) hv[i] = hv[i] + h0 * Rg[(size_t)i * (m + 1) + k];
           hn = h0 * Rg[(size_t)k * (m + 1) + k];
+          break;
         }
         for (int i = 0; i < k; ++i) h[i] = hv[i];
       }

@@ -54,7 +54,8 @@ typedef struct {
                             assembled C - B diag(A_u)^-1 B^T (the PETSc variant) */
   double over_interp;    /* plain aggregation: A_c = (1/over_interp) P^T A P (reading R19, 1.5) */
   int32_t ilu_sweeps;    /* ORC_ILU0: Jacobi sweeps per triangular solve (>= 1, default 2, R20) */
-  int32_t gmres_ortho;   /* GMRES orthogonalisation: 0 CGS2 (default), 1 two-pass Gram/Cholesky (R22) */
+  int32_t gmres_ortho;   /* GMRES orthogonalisation: 0 CGS2 (default), 1 two-pass Gram/Cholesky
+                            (R22), 2 the same with the first pass's dots on the fp32-rounded basis (R23) */
 } orc_params;
 
 typedef struct {

@@ -7,6 +7,7 @@
 #include "prof.h"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace amgb {
@@ -76,11 +77,13 @@ __device__ __forceinline__ void reduce_finish(double (&acc)[K], int kout, double
 // MODE 3: w_out = w - sum_j c_j s_j V_j;  out[j] = s_j V_j . w_out, out[k] = w_out . w_out
 //         (update + next dots + squared norm: the two-pass Gram/Cholesky orthogonalisation)
 // (v_j = s_j V_j: the basis is stored unnormalised with device scales sc)
-template <int K, int MODE>
+// TV: element type of the basis as read (double; float for the fp32 shadow copy the GMRES
+// pass-1 multi-dot of reading R23 reads); wf (MODE 3, optional): fp32 copy of w_out
+template <int K, int MODE, typename TV = double>
 __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double* __restrict__ sc,
                                              const double* __restrict__ coef, const double* w, double* w_out,
                                              double* partials, unsigned* ticket, double* out, int post,
-                                             double* inv) {
+                                             double* inv, float* wf) {
   constexpr int U = cgs_unroll<K>();
   __shared__ double c[K], sv[K];
   if (threadIdx.x < K) {
@@ -95,13 +98,33 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
   const int64_t step = (int64_t)gridDim.x * kTM * U;
   for (int64_t i0 = (int64_t)blockIdx.x * kTM * U + threadIdx.x; i0 < n; i0 += step) {
     double wv[U], vv[U][K];
+    if constexpr (std::is_same_v<TV, double>) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + (int64_t)u * kTM;
-      const bool ok = i < n;
-      wv[u] = ok ? w[i] : 0.0;
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + (int64_t)u * kTM;
+        const bool ok = i < n;
+        wv[u] = ok ? w[i] : 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) vv[u][j] = ok ? __ldcs(V.p[j] + i) : 0.0;
+        for (int j = 0; j < K; ++j) vv[u][j] = ok ? __ldcs(V.p[j] + i) : 0.0;
+      }
+    } else {
+      // fp32 basis: unpredicated loads (clamped index) all issued before the widening, which
+      // a predicated load + F2F pair would serialise (SASS: one LDG in flight)
+      TV raw[U][K];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = min(i0 + (int64_t)u * kTM, n - 1);
+#pragma unroll
+        for (int j = 0; j < K; ++j) raw[u][j] = __ldcs(reinterpret_cast<const TV*>(V.p[j]) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + (int64_t)u * kTM;
+        const bool ok = i < n;
+        wv[u] = ok ? w[i] : 0.0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) vv[u][j] = ok ? (double)raw[u][j] : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -114,6 +137,7 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
 #pragma unroll
         for (int j = 0; j < K; ++j) v = fma(-c[j], vv[u][j], v);
         if (i < n) w_out[i] = v;
+        if (MODE == 3 && wf && i < n) wf[i] = (float)v;
         if constexpr (MODE == 1 || MODE == 3) {
 #pragma unroll
           for (int j = 0; j < K; ++j) acc[j] = fma(sv[j] * vv[u][j], v, acc[j]);
@@ -165,11 +189,11 @@ __device__ __forceinline__ void finish_partials(int kout, double* partials, unsi
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-template <int NJ, int MODE>
+template <int NJ, int MODE, typename TV = double>
 __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V, const double* __restrict__ sc,
                                                      const double* __restrict__ coef, const double* w, double* w_out,
                                                      double* partials, unsigned* ticket, double* out, int post,
-                                                     double* inv) {
+                                                     double* inv, float* wf) {
   constexpr int T = kCW / 32;  // elements per lane per chunk
   __shared__ double c[32], sv[32];
   __shared__ double part[8][kCW + 1];
@@ -180,13 +204,13 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
     c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
   }
   __syncthreads();
-  const double* vp[NJ];
+  const TV* vp[NJ];
   bool own[NJ];
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     const int j = warp + 8 * q;
     own[q] = j < k;
-    vp[q] = own[q] ? V.p[j] : V.p[0];
+    vp[q] = reinterpret_cast<const TV*>(own[q] ? V.p[j] : V.p[0]);
   }
   double acc[NJ];
 #pragma unroll
@@ -195,13 +219,28 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
   for (int64_t i0 = (int64_t)blockIdx.x * kCW; i0 < n; i0 += (int64_t)gridDim.x * kCW) {
     const bool full = i0 + kCW <= n;
     double val[NJ][T];
+    if constexpr (std::is_same_v<TV, double>) {
 #pragma unroll
-    for (int q = 0; q < NJ; ++q)
+      for (int q = 0; q < NJ; ++q)
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const int64_t i = i0 + lane + 32 * t;
-        val[q][t] = (own[q] && (full || i < n)) ? __ldcs(vp[q] + i) : 0.0;
-      }
+        for (int t = 0; t < T; ++t) {
+          const int64_t i = i0 + lane + 32 * t;
+          val[q][t] = (own[q] && (full || i < n)) ? __ldcs(vp[q] + i) : 0.0;
+        }
+    } else {  // fp32 basis: unpredicated loads first, then the widening (see k_cgs)
+      TV raw[NJ][T];
+#pragma unroll
+      for (int q = 0; q < NJ; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t) raw[q][t] = __ldcs(vp[q] + min(i0 + lane + 32 * t, n - 1));
+#pragma unroll
+      for (int q = 0; q < NJ; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int64_t i = i0 + lane + 32 * t;
+          val[q][t] = (own[q] && (full || i < n)) ? (double)raw[q][t] : 0.0;
+        }
+    }
     const int64_t it = i0 + threadIdx.x;
     const double wv = (it < n) ? w[it] : 0.0;
     if constexpr (MODE == 0) {
@@ -226,6 +265,7 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
 #pragma unroll
       for (int ww = 0; ww < 8; ++ww) v -= part[ww][threadIdx.x];
       if (it < n) w_out[it] = v;
+      if (MODE == 3 && wf && it < n) wf[it] = (float)v;
       if constexpr (MODE == 2 || MODE == 3) nrm = fma(v, v, nrm);
       if constexpr (MODE != 2) {
         vs[threadIdx.x] = v;
@@ -283,32 +323,35 @@ void dispatch_k(int k, F&& f) {
   else fail(AMG_EINVAL, "multi-vector kernels take 1..32 vectors");
 }
 
-template <int MODE>
+template <int MODE, typename TV = double>
 void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
-                double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s) {
+                double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s,
+                float* wf = nullptr) {
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
   const int wide_from = env_int("AMG_CGS_WIDE", 13);  // first k served by k_cgs_wide (tests force both)
   if (k >= wide_from) {
     const int64_t work = (n + kCW - 1) / kCW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * kSMs, (int64_t)kMaxPartials, work}));
-    auto go = [&](auto kern) { kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv); };
-    if (k <= 16) go(k_cgs_wide<2, MODE>);
-    else if (k <= 24) go(k_cgs_wide<3, MODE>);
-    else go(k_cgs_wide<4, MODE>);
+    auto go = [&](auto kern) {
+      kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
+    };
+    if (k <= 16) go(k_cgs_wide<2, MODE, TV>);
+    else if (k <= 24) go(k_cgs_wide<3, MODE, TV>);
+    else go(k_cgs_wide<4, MODE, TV>);
     AMG_CK_LAUNCH();
     return;
   }
   dispatch_k(k, [&](auto Kc) {
     constexpr int K = decltype(Kc)::value;
     constexpr int U = cgs_unroll<K>();
-    static int occ = 0;  // per (K, MODE) instantiation
+    static int occ = 0;  // per (K, MODE, TV) instantiation
     if (occ == 0) {
-      AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, MODE>, kTM, 0));
+      AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, MODE, TV>, kTM, 0));
       occ = std::max(occ, 1);
     }
     const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)occ * kSMs, (int64_t)kMaxPartials, work}));
-    k_cgs<K, MODE><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv);
+    k_cgs<K, MODE, TV><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
   });
   AMG_CK_LAUNCH();
 }
@@ -455,15 +498,22 @@ void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, co
   finalize_global(comm, out, k, false, s);
 }
 
+void launch_mdot_scaled_f32(int64_t n, int k, const PtrList& Vf, const double* sc, const double* w, double* partials,
+                            double* out, cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("mdot", k, AMG_F32, -1), 4.0 * n * k + 8.0 * n, s);
+  launch_cgs<0, float>(n, k, Vf, sc, nullptr, w, nullptr, partials, out, 0, nullptr, s);
+  finalize_global(comm, out, k, false, s);
+}
+
 __global__ void k_set_inv1(double* dst, const double* src) { *dst = 1.0 / *src; }
 
 void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
                                 const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
-                                CommBase* comm) {
+                                CommBase* comm, float* wf_out) {
   if (k + 1 > 32) fail(AMG_EINVAL, "update + dots + norm: at most 31 vectors");
   {
-    ProfScope ps_(prof_name("cgs_update_dots_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2), s);
-    launch_cgs<3>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s);
+    ProfScope ps_(prof_name("cgs_update_dots_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2) + (wf_out ? 4.0 * n : 0.0), s);
+    launch_cgs<3>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s, wf_out);
   }
   finalize_global(comm, out, k + 1, false, s);
 }
@@ -724,6 +774,89 @@ void launch_axpy_2dot(int64_t n, double c, const double* t, const double* s_, do
   k_axpy_2dot<<<fused_grid(n), kTM, 0, s>>>(n, c, t, s_, out, rh, partials, ticket, dst);
   AMG_CK_LAUNCH();
   finalize_global(comm, dst, 2, false, s);
+}
+
+
+// ---- BiCGStab with device-side scalars (one CUDA graph per iteration, reading R24) ----
+// Every scalar the iteration needs lives in BicgScal (device); the kernels compute alpha,
+// beta and omega from it with the host code's own expressions, so the iterates are
+// bit-identical to the host-driven loop.
+__global__ void __launch_bounds__(kT) k_bicg_p(int64_t n, const double* __restrict__ r, const double* __restrict__ v,
+                                               double* __restrict__ p, const double* __restrict__ sc) {
+  const bool first = sc[kBicgFirst] != 0.0;
+  const double beta = (sc[kBicgRho] / sc[kBicgRhoOld]) * (sc[kBicgAlpha] / sc[kBicgOmega]);
+  const double b2 = -beta * sc[kBicgOmega];
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT)
+    p[i] = first ? r[i] : fma(1.0, r[i], fma(b2, v[i], beta * p[i]));
+}
+
+// alpha = rho / rv; s = r - alpha v; ss = s.s
+__global__ void __launch_bounds__(kTM) k_bicg_s(int64_t n, const double* __restrict__ v, const double* __restrict__ r,
+                                                double* __restrict__ sv, double* sc, double* partials,
+                                                unsigned* ticket) {
+  const double a = sc[kBicgRho] / sc[kBicgRv];
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+    const double o = fma(-a, v[i], r[i]);
+    sv[i] = o;
+    acc[0] = fma(o, o, acc[0]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[kBicgAlphaNew] = a;
+  reduce_finish<1>(acc, 1, partials, ticket, sc + kBicgSs, 0, nullptr);
+}
+
+// omega = ts / tt; x += alpha ph + omega sh (alpha ph only on the half-step exit ||s|| <=
+// tol; nothing when rv or tt broke down); r = s - omega t with r.r and rh.r
+__global__ void __launch_bounds__(kTM) k_bicg_xr(int64_t n, const double* __restrict__ ph,
+                                                 const double* __restrict__ sh, const double* __restrict__ t,
+                                                 const double* __restrict__ sv, const double* __restrict__ rh,
+                                                 double* __restrict__ x, double* __restrict__ r, double* sc,
+                                                 double* partials, unsigned* ticket) {
+  const double rv = sc[kBicgRv], tt = sc[kBicgTt];
+  const double alpha = sc[kBicgAlphaNew];
+  const bool rv_ok = rv != 0.0 && isfinite(rv);
+  const bool half = rv_ok && sqrt(sc[kBicgSs]) <= sc[kBicgTol];
+  const bool tt_ok = tt != 0.0 && isfinite(tt);
+  const double omega = sc[kBicgTs] / tt;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+    if (half) {
+      x[i] = fma(alpha, ph[i], 1.0 * x[i]);
+    } else if (rv_ok && tt_ok) {
+      x[i] = fma(alpha, ph[i], fma(omega, sh[i], 1.0 * x[i]));
+      const double o = fma(-omega, t[i], sv[i]);
+      r[i] = o;
+      acc[0] = fma(o, o, acc[0]);
+      acc[1] = fma(rh[i], o, acc[1]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && rv_ok && tt_ok && !half) sc[kBicgOmegaNew] = omega;
+  reduce_finish<2>(acc, 2, partials, ticket, sc + kBicgRr, 0, nullptr);
+}
+
+void launch_bicg_p(int64_t n, const double* r, const double* v, double* p, const double* sc, cudaStream_t s) {
+  ProfScope ps_(prof_name("bicg_p", 1, AMG_F64, -1), 32.0 * n, s);
+  k_bicg_p<<<ew_grid(n), kT, 0, s>>>(n, r, v, p, sc);
+  AMG_CK_LAUNCH();
+}
+
+void launch_bicg_s(int64_t n, const double* v, const double* r, double* sv, double* sc, double* partials,
+                   cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("sub_div_nrm", 1, AMG_F64, -1), 8.0 * n * 3, s);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  k_bicg_s<<<fused_grid(n), kTM, 0, s>>>(n, v, r, sv, sc, partials, ticket);
+  AMG_CK_LAUNCH();
+  finalize_global(comm, sc + kBicgSs, 1, false, s);
+}
+
+void launch_bicg_xr(int64_t n, const double* ph, const double* sh, const double* t, const double* sv,
+                    const double* rh, double* x, double* r, double* sc, double* partials, cudaStream_t s,
+                    CommBase* comm) {
+  ProfScope ps_(prof_name("bicg_xr", 2, AMG_F64, -1), 8.0 * n * 8, s);
+  unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
+  k_bicg_xr<<<fused_grid(n), kTM, 0, s>>>(n, ph, sh, t, sv, rh, x, r, sc, partials, ticket);
+  AMG_CK_LAUNCH();
+  finalize_global(comm, sc + kBicgRr, 2, false, s);
 }
 
 }  // namespace amgb

@@ -31,11 +31,15 @@ void launch_mdot_scaled(int64_t n, int k, const PtrList& V, const double* sc, co
 void launch_cgs_update(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                        double* w_out, bool dot_next, double* partials, double* out, cudaStream_t s,
                        CommBase* comm = nullptr, double* inv_out = nullptr);
+// the same with the basis read from its fp32 shadow copy (Vf.p[j] are float*; reading R23)
+void launch_mdot_scaled_f32(int64_t n, int k, const PtrList& Vf, const double* sc, const double* w, double* partials,
+                            double* out, cudaStream_t s, CommBase* comm = nullptr);
 // w_out = w - sum_j coef[j] sc[j] V_j, out[j] = sc[j] V_j . w_out (j < k), out[k] = w_out . w_out
-// (one pass; the Gram/Cholesky two-pass orthogonalisation of flexible GMRES)
+// (one pass; the Gram/Cholesky two-pass orthogonalisation of flexible GMRES); wf_out
+// (optional): an fp32 copy of w_out written in the same pass (the shadow basis of R23)
 void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
                                 const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
-                                CommBase* comm = nullptr);
+                                CommBase* comm = nullptr, float* wf_out = nullptr);
 // w -= sum_j coef[j] V_j  (coef: device)
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s);
 // x += sum_j y[j] Z_j  (Z of dtype zt, y: device)
@@ -65,5 +69,34 @@ void launch_axpy_2dot(int64_t n, double c, const double* t, const double* s_, do
                       double* partials, double* dst, cudaStream_t s, CommBase* comm = nullptr);
 // y = x / sdev[0]
 void launch_scale_by_inv(int64_t n, const double* x, const double* sdev, double* y, cudaStream_t s);
+
+// BiCGStab with device-side scalars (reading R24): slots of the scalar block `sc`
+enum : int {
+  kBicgRho = 0,       // rho = rh . r of this iteration
+  kBicgRhoOld = 1,    // rho of the previous iteration
+  kBicgAlpha = 2,     // alpha of the previous iteration (beta)
+  kBicgOmega = 3,     // omega of the previous iteration (beta)
+  kBicgFirst = 4,     // 1: p = r (first step after a (re)start)
+  kBicgTol = 5,       // rtol ||b||
+  kBicgRv = 6,        // rh . v
+  kBicgSs = 7,        // s . s
+  kBicgTt = 8,        // t . t
+  kBicgTs = 9,        // t . s
+  kBicgRr = 10,       // r . r (new r)
+  kBicgRhoNext = 11,  // rh . r (new r)
+  kBicgAlphaNew = 12, // alpha of this iteration
+  kBicgOmegaNew = 13, // omega of this iteration
+  kBicgSlots = 16
+};
+// p = r (first) or r + beta (p - omega v), beta = (rho / rho_old) (alpha / omega) from sc
+void launch_bicg_p(int64_t n, const double* r, const double* v, double* p, const double* sc, cudaStream_t s);
+// alpha = rho / rv -> sc[AlphaNew]; s = r - alpha v; sc[Ss] = s . s
+void launch_bicg_s(int64_t n, const double* v, const double* r, double* sv, double* sc, double* partials,
+                   cudaStream_t s, CommBase* comm = nullptr);
+// omega = ts / tt; x += alpha ph + omega sh (half-step exit: alpha ph; breakdown: nothing);
+// r = s - omega t; sc[Rr] = r . r, sc[RhoNext] = rh . r
+void launch_bicg_xr(int64_t n, const double* ph, const double* sh, const double* t, const double* sv,
+                    const double* rh, double* x, double* r, double* sc, double* partials, cudaStream_t s,
+                    CommBase* comm = nullptr);
 
 }  // namespace amgb

@@ -146,7 +146,9 @@ void replicated_allgather(Handle& h, size_t l, cudaStream_t s) {
 void* level_f_slab(Handle& h, size_t l) {
   const bool coarsest = l == h.lv.size();
   char* f = static_cast<char*>(coarsest ? h.coarse.f : h.lv[l].f);
-  if (!h.comm || l < h.rep_from) return f;
+  // only the first replicated level is assembled from the ranks' slabs; past it every rank's
+  // restriction computes the whole next level
+  if (!h.comm || l != h.rep_from) return f;
   const int b = coarsest ? h.coarse.b : h.lv[l].A.b;
   return f + h.lbounds[l][h.comm->rank] * b * dtype_size(h.xt);
 }

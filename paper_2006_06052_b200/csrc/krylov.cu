@@ -279,6 +279,156 @@ int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, a
   return finish(c, b, x, r, nb, status, it, restarts, rep);
 }
 
+// ---- BiCGStab with device-side scalars: one CUDA graph per iteration (reading R24) ----
+// The whole step -- p update, both preconditioner applications, both fused SpMV + dots, the
+// s, x and r updates -- is one graph replay; alpha, beta and omega are formed on the device
+// from the scalar block (the host code's own expressions, so the iterates are bit-identical
+// to solve_bicgstab's), and the host reads the block once per step: one synchronisation
+// instead of three and one graph launch instead of ~8 launches.  The host keeps the control
+// flow (breakdown restarts, the half-step exit, the true-residual verification) and writes
+// the next step's (rho, rho_old, alpha, omega, first) back with one small copy.
+int solve_bicgstab_graphed(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  double *r = h.vec[0], *rh = h.vec[1], *p = h.vec[2], *ph = h.vec[3], *v = h.vec[4], *sv = h.vec[5],
+         *sh = h.vec[6], *t = h.vec[7];
+  const int64_t N = c.N;
+  double* sc = h.dscal + 160;  // BicgScal block (blas1.h)
+  double* hs = h.hscal + 160;
+  c.residual_nrm(b, x, r);
+  c.read(1);
+  int it = 0, restarts = 0, status = AMG_NOT_CONVERGED;
+  if (std::sqrt(h.hscal[0]) <= rtol * nb) status = AMG_OK;
+  launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+  bool first = true;
+  double rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  auto do_restart = [&]() -> bool {
+    if (restarts >= 1) return false;
+    ++restarts;
+    c.residual(b, x, r);
+    launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+    first = true;
+    return true;
+  };
+  auto verify = [&]() -> bool {
+    c.residual_nrm(b, x, r);
+    c.read(1);
+    if (std::sqrt(h.hscal[0]) <= rtol * nb) return true;
+    launch_convert(N, r, AMG_F64, rh, AMG_F64, 1.0, c.s);
+    first = true;
+    return false;
+  };
+  // the step graph (per iterate pointer x; workspace vectors are the handle's)
+  cudaGraphExec_t G = nullptr;
+  for (const auto& e : h.step_graphs)
+    if (e.first == x) G = e.second;
+  const double step_bytes = 2.0 * h.alg_bytes_precond + 2.0 * (h.alg_bytes_spmv) + 136.0 * N;  // p 32N, rh.v 8N, s 24N, s.t 8N, x + r 64N
+  if (!G) {
+    const int64_t l0 = t_launches;
+    cudaGraph_t graph = nullptr;
+    AMG_CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_bicg_p(N, r, v, p, sc, c.s);                                    // p
+      precond_apply(h, p, ph, AMG_F64, c.s);                                 // ph = M p
+      if (h.comm || !launch_spmv_dot(h.A, ph, AMG_F64, v, rh, nullptr, 1, h.partials, sc + kBicgRv, c.s, h.comm)) {
+        halo_overlapped(h, h.halo0, h.A, ph, AMG_F64, h.b, c.s,
+                        [&](int r0, int r1) { launch_spmv(h.A, 1.0, ph, AMG_F64, 0.0, v, AMG_F64, c.s, r0, r1); });
+        launch_dot(N, rh, AMG_F64, v, AMG_F64, h.partials, sc + kBicgRv, false, c.s, h.comm);
+      }
+      launch_bicg_s(N, v, r, sv, sc, h.partials, c.s, h.comm);              // s, ||s||^2
+      precond_apply(h, sv, sh, AMG_F64, c.s);                                // sh = M s
+      if (h.comm || !launch_spmv_dot(h.A, sh, AMG_F64, t, nullptr, sv, 2, h.partials, sc + kBicgTt, c.s, h.comm)) {
+        halo_overlapped(h, h.halo0, h.A, sh, AMG_F64, h.b, c.s,
+                        [&](int r0, int r1) { launch_spmv(h.A, 1.0, sh, AMG_F64, 0.0, t, AMG_F64, c.s, r0, r1); });
+        launch_dot(N, t, AMG_F64, t, AMG_F64, h.partials, sc + kBicgTt, false, c.s, h.comm);
+        launch_dot(N, sv, AMG_F64, t, AMG_F64, h.partials, sc + kBicgTs, false, c.s, h.comm);
+      }
+      launch_bicg_xr(N, ph, sh, t, sv, rh, x, r, sc, h.partials, c.s, h.comm);  // x, r, r.r, rh.r
+    } catch (...) {
+      cudaStreamEndCapture(c.s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    AMG_CK(cudaStreamEndCapture(c.s, &graph));
+    h.step_graph_kernels = t_launches - l0;
+    t_launches = l0;
+    g_launches -= h.step_graph_kernels;
+    cudaError_t e = cudaGraphInstantiate(&G, graph, 0);
+    cudaGraphDestroy(graph);
+    AMG_CK(e);
+    h.step_graphs.push_back({x, G});
+  }
+  hs[kBicgTol] = rtol * nb;
+  bool have_rho = false;
+  double rho_next = 0.0;
+  while (status != AMG_OK && it < h.p.maxiter) {
+    if (!have_rho) {
+      c.dot(rh, r, 0);
+      c.read(1);
+      rho_next = h.hscal[0];
+    }
+    have_rho = false;
+    const double rho = rho_next;
+    if (!(std::fabs(rho) > 1e-30 * nb * nb) || !finite(rho)) {
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    hs[kBicgRho] = rho, hs[kBicgRhoOld] = rho_old, hs[kBicgAlpha] = alpha, hs[kBicgOmega] = omega;
+    hs[kBicgFirst] = first ? 1.0 : 0.0;
+    AMG_CK(cudaMemcpyAsync(sc, hs, sizeof(double) * 6, cudaMemcpyHostToDevice, c.s));
+    AMG_CK(cudaGraphLaunch(G, c.s));
+    g_launches += h.step_graph_kernels;
+    t_launches += h.step_graph_kernels;
+    c.bytes += step_bytes;
+    AMG_CK(cudaMemcpyAsync(hs + kBicgRv, sc + kBicgRv, sizeof(double) * (kBicgSlots - kBicgRv),
+                           cudaMemcpyDeviceToHost, c.s));
+    AMG_CK(cudaStreamSynchronize(c.s));
+    first = false;
+    const double rv = hs[kBicgRv];
+    if (rv == 0.0 || !finite(rv)) {  // the step left x untouched
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    alpha = rho / rv;
+    ++it;
+    if (std::sqrt(hs[kBicgSs]) <= rtol * nb) {  // half-step exit: the step did x += alpha ph only
+      if (verify()) {
+        status = AMG_OK;
+        break;
+      }
+      continue;
+    }
+    const double tt = hs[kBicgTt];
+    if (tt == 0.0 || !finite(tt)) {  // x untouched
+      if (do_restart()) continue;
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    omega = hs[kBicgTs] / tt;
+    rho_old = rho;
+    const double nr = std::sqrt(hs[kBicgRr]);
+    rho_next = hs[kBicgRhoNext];
+    have_rho = true;
+    if (omega == 0.0 || !finite(omega)) {
+      if (do_restart()) {
+        have_rho = false;
+        continue;
+      }
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    if (nr <= rtol * nb) {
+      if (verify()) {
+        status = AMG_OK;
+        break;
+      }
+      have_rho = false;
+    }
+  }
+  return finish(c, b, x, r, nb, status, it, restarts, rep);
+}
+
 // ---- flexible GMRES(m) with CGS2 (cfg 4, 5) ----
 // The Arnoldi basis is stored unnormalised, v_j = s_j V_j with s_j = 1/||V_j|| kept on
 // the device: the normalisation pass disappears (the preconditioner's split applies
@@ -292,7 +442,13 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   const int m = h.p.gmres_m;
   const int64_t N = c.N;
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hh(m + 1);
-  const bool gram = h.p.gmres_ortho == 1;
+  const bool gram = h.p.gmres_ortho >= 1;
+  const bool shadow = h.p.gmres_ortho == 2;  // reading R23: pass-1 dots on the fp32 shadow basis
+  auto shadow0 = [&]() {  // the fp32 shadow of V_0 (the other shadows come out of the update pass)
+    if (!shadow) return;
+    launch_convert(N, h.V[0], AMG_F64, h.Vs[0], AMG_F32, 1.0, c.s);
+    c.bytes += 12.0 * N;
+  };
   std::vector<double> R((size_t)(m + 1) * (m + 1), 0.0), hv(m + 1), cv(m + 1);  // Gram/Cholesky factor
   double* sc = h.dscal + 128;  // s_j
   // r = b - A x straight into V_0
@@ -303,6 +459,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   AMG_CK_LAUNCH();
   ++g_launches;
   ++t_launches;
+  shadow0();
   c.read(65);
   double beta = h.hscal[64];
   int it = 0, cycles = 0, status = AMG_NOT_CONVERGED;
@@ -340,8 +497,15 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
         // t_{j+1} = w1 / ||w1||; R's new column from G's (R^-T q / ||w1||);
         // H(:, j) = h + ||w1|| R(:, j+1).
         const int k = j + 1;
-        launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
-        c.bytes += 8.0 * N * (k + 1.0);
+        if (shadow) {
+          PtrList Vf{};
+          for (int i = 0; i < k; ++i) Vf.p[i] = reinterpret_cast<const double*>(h.Vs[i]);
+          launch_mdot_scaled_f32(N, k, Vf, sc, w, h.partials, h.dscal, c.s, h.comm);
+          c.bytes += 4.0 * N * k + 8.0 * N;
+        } else {
+          launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
+          c.bytes += 8.0 * N * (k + 1.0);
+        }
         c.read(k);
         // h = R^-T p (forward substitution), c' = R^-1 h (back substitution); the update pass
         // w -= t c' returns q = t^T w and ||w||^2.  hacc accumulates Q^T w over the passes.
@@ -358,11 +522,13 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
           }
           for (int i = 0; i < k; ++i) h.hscal[96 + i] = cv[i];
           AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
-          launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm);
-          c.bytes += 8.0 * N * (k + 2.0);  // reads k basis vectors and w, writes w
+          launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm,
+                                     shadow ? h.Vs[j + 1] : nullptr);
+          c.bytes += 8.0 * N * (k + 2.0) + (shadow ? 4.0 * N : 0.0);  // k basis vectors and w read, w written
           c.read(32 + k + 1);
         };
         std::vector<double> pin(h.hscal, h.hscal + k), h2(k);
+        const bool reorth_always = env_set("AMG_REORTH_ALWAYS");  // test switch: take the extra pass every step
         project(pin.data(), hv.data());
         for (int pass = 0;; ++pass) {
           hn = std::sqrt(std::max(h.hscal[32 + k], 0.0));
@@ -381,7 +547,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
           // once more (the pass's q = t^T w1 gives Q^T w1 = R^-T q without another multi-dot)
           // and take the coefficients of both passes -- CGS2's reorthogonalisation, applied
           // only where needed.  At most one extra pass.
-          if (pass == 0 && (ss > 0.5 || !(d2 > 1e-8))) {
+          if (pass == 0 && (ss > 0.5 || !(d2 > 1e-8) || reorth_always)) {
             for (int i = 0; i < k; ++i) pin[i] = h.hscal[32 + i];
             project(pin.data(), h2.data());
             for (int i = 0; i < k; ++i) hv[i] += h2[i];
@@ -438,8 +604,9 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     k_set_inv<<<1, 1, 0, c.s>>>(sc, h.dscal + 64);
     AMG_CK_LAUNCH();
     ++g_launches;
-  ++t_launches;
+    ++t_launches;
     c.bytes += 8.0 * N;
+    shadow0();
     c.read(65);
     beta = h.hscal[64];
     s_host = 1.0 / beta;
@@ -647,7 +814,13 @@ int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_
   }
   switch (h.p.solver) {
     case AMG_CG: return solve_cg(c, b, x, rtol, nb, rep);
-    case AMG_BICGSTAB: return solve_bicgstab(c, b, x, rtol, nb, rep);
+    case AMG_BICGSTAB:
+      // one graph per step unless graphs are off, the profiler times every launch, or the
+      // communicator cannot be captured (the thread-emulated one)
+      if (h.p.use_graphs && !g_prof && !env_set("AMG_NO_GRAPH") && !env_set("AMG_NO_STEP_GRAPH") &&
+          (!h.comm || h.comm->capturable()))
+        return solve_bicgstab_graphed(c, b, x, rtol, nb, rep);
+      return solve_bicgstab(c, b, x, rtol, nb, rep);
     case AMG_GMRES: return solve_gmres(c, b, x, rtol, nb, rep);
     case AMG_IDRS: return solve_idrs(c, b, x, rtol, nb, rep);
     default: fail(AMG_EINVAL, "unknown solver");

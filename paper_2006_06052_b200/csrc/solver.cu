@@ -15,6 +15,8 @@ void set_last_error(const std::string& s);
 Handle::~Handle() {
   for (PcGraph& G : pc_graphs)
     if (G.exec) cudaGraphExecDestroy(G.exec);
+  for (auto& G : step_graphs)
+    if (G.second) cudaGraphExecDestroy(G.second);
   if (work) cudaStreamDestroy(work);
   if (comm_s) cudaStreamDestroy(comm_s);
   if (ev_pack) cudaEventDestroy(ev_pack);
@@ -51,6 +53,8 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     char* slab = (char*)h.arena.alloc((vbytes + stagger) * (m + 1) + 256);
     for (int i = 0; i <= m; ++i) h.V.push_back(reinterpret_cast<double*>(slab + (size_t)i * (vbytes + stagger)));
     for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
+    if (h.p.gmres_ortho == 2)
+      for (int i = 0; i <= m; ++i) h.Vs.push_back(h.arena.alloc_n<float>(std::max<int64_t>(N, 1)));
   }
   if (h.p.solver == AMG_IDRS) {
     // IDR(s): shadow space P (N), G (N), U (with ghost space: U_k feeds the SpMV)
@@ -104,7 +108,7 @@ int check_params(const amg_params* p) {
   if (p->schur_shat < 0 || p->schur_shat > 2 || !(p->over_interp > 0.0)) return AMG_EINVAL;
   if (p->smoother < AMG_SPAI0 || p->smoother > AMG_ILU0) return AMG_EINVAL;
   if (p->smoother == AMG_ILU0 && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16)) return AMG_EINVAL;
-  if (p->gmres_ortho < 0 || p->gmres_ortho > 1) return AMG_EINVAL;
+  if (p->gmres_ortho < 0 || p->gmres_ortho > 2) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;
@@ -386,7 +390,7 @@ int amg_solve_counters(struct amg_handle* hh, int64_t* out, int32_t n) {
   Handle* h = reinterpret_cast<Handle*>(hh);
   if (!h || !out || n < 2) return AMG_EINVAL;
   out[0] = h->reorth_passes;
-  out[1] = (int64_t)h->pc_graphs.size();
+  out[1] = (int64_t)(h->pc_graphs.size() + h->step_graphs.size());
   return AMG_OK;
 }
 
@@ -423,7 +427,7 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   else if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
   v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
   const int64_t N = (int64_t)h->n * h->b;
-  v[6] = 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
+  v[6] = 4LL * N * (int64_t)h->Vs.size() + 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
                     (int64_t)h->Ui.size()) +
          (int64_t)h->Z.size() * N * dtype_size(h->zt);
   v[7] = h->arena.bytes();

@@ -86,6 +86,7 @@ struct Handle {
   std::vector<double*> vec;
   // GMRES basis (fp64) and preconditioned basis Z (fp32 when the PC output is fp32-exact)
   std::vector<double*> V;
+  std::vector<float*> Vs;          // gmres_ortho = 2: fp32 shadow of V for the pass-1 dots (R23)
   std::vector<void*> Z;
   int zt = AMG_F64;
   // IDR(s) (AMG_IDRS): shadow space, G = A U, U (search directions); shadow seed base
@@ -98,6 +99,9 @@ struct Handle {
   double* hscal = nullptr;         // pinned host mirror [64]
   // CUDA graphs of the preconditioner application, one per (input, output, dtype, scale)
   std::vector<PcGraph> pc_graphs;
+  // one Krylov step as a CUDA graph (BiCGStab, reading R24), per iterate pointer
+  std::vector<std::pair<const double*, cudaGraphExec_t>> step_graphs;
+  int64_t step_graph_kernels = 0;
   cudaStream_t work = nullptr;     // non-blocking stream the Krylov solve runs on (graph capture)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   double *stage_b = nullptr, *stage_x = nullptr;  // amg_solve_host's device b / x (alloc_workspace)

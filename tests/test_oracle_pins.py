@@ -912,7 +912,7 @@ def test_dense_solve_small(rng, solver, kind):
     assert np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
 
 
-@pytest.mark.parametrize("ortho", [0, 1])
+@pytest.mark.parametrize("ortho", [0, 1, 2])
 def test_gmres_finite_termination(rng, ortho):
     n = 20
     ptr, col, val = random_bsr(rng, n, 1, density=1.0, dom=10)
@@ -934,21 +934,26 @@ def test_gmres_two_pass_orthogonalisation_is_arnoldi(rng):
     ptr, col, val = random_bsr(rng, n, 1, density=0.2, dom=3)
     A = oracle.Mat.from_arrays(ptr, col, val)
     b = rng.standard_normal(n)
+    # (R23, gmres_ortho = 2: the first pass's dots on the fp32-rounded basis -- only the
+    # projection coefficients change, the Arnoldi relation and R stay exact, so the minimal
+    # residuals agree step by step as well)
     hs = []
-    for ortho in (0, 1):
+    for ortho in (0, 1, 2):
         S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=40, precond=oracle.PC_NONE, gmres_ortho=ortho)
         hs.append(np.array(S.solve(b, rtol=1e-10, history=True).history))
-    k = min(len(hs[0]), len(hs[1]))
-    assert abs(len(hs[0]) - len(hs[1])) <= 1
-    assert np.allclose(hs[0][:k], hs[1][:k], rtol=1e-6, atol=1e-14)
+    for o in (1, 2):
+        k = min(len(hs[0]), len(hs[o]))
+        assert abs(len(hs[0]) - len(hs[o])) <= 1
+        assert np.allclose(hs[0][:k], hs[o][:k], rtol=1e-6, atol=1e-14)
     for kind, pc in ((gen.STOKES, oracle.PC_SCHUR), (gen.POISSON3, oracle.PC_AMG)):
         ptr, col, val = gen.matrix(kind, 8)
         A = oracle.Mat.from_arrays(ptr, col, val)
         b = rng.standard_normal((len(ptr) - 1) * val.shape[-1])
         rs = [oracle.Solver(A, solver=oracle.GMRES, precond=pc, gmres_ortho=o, coarse_enough=60).solve(b, rtol=1e-10)
-              for o in (0, 1)]
-        assert rs[0].iters == rs[1].iters and rs[0].converged and rs[1].converged
-        assert np.linalg.norm(rs[0].x - rs[1].x) <= 1e-8 * np.linalg.norm(rs[0].x)
+              for o in (0, 1, 2)]
+        for o in (1, 2):
+            assert rs[0].iters == rs[o].iters and rs[0].converged and rs[o].converged
+            assert np.linalg.norm(rs[0].x - rs[o].x) <= 1e-8 * np.linalg.norm(rs[0].x)
 
 
 # ---- IDR(s) (Table 1: the paper's outer solver; reading R17) ----
@@ -1050,3 +1055,24 @@ def test_multirank_aggregates_are_slab_local():
     a1, n1 = oracle.aggregate(A, nparts=1)
     a0, n0 = oracle.aggregate(A)
     assert np.array_equal(a1, a0)
+
+
+@pytest.mark.parametrize("ortho", [1, 2])
+def test_gmres_gram_near_invariant_subspace(rng, ortho):
+    # a spectrum of five values: the Krylov space is invariant after five steps, the new
+    # direction lies in span(V) up to rounding and 1 - |R(:,k)|^2 cancels -- the Gram/
+    # Cholesky variants' reorthogonalisation safeguard must keep them on CGS2's track (the
+    # minimal residual after <= 5 steps reaches rounding level, x equals the dense solution)
+    n = 300
+    d = rng.choice([1.0, 2.0, 3.0, 5.0, 8.0], n)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    D = Q @ np.diag(d) @ Q.T
+    ptr = (np.arange(n + 1) * n).astype(np.int32)
+    col = np.tile(np.arange(n, dtype=np.int32), n)
+    A = oracle.Mat.from_arrays(ptr, col, D.reshape(-1, 1, 1))
+    b = rng.standard_normal(n)
+    xs = np.linalg.solve(D, b)
+    for o in (0, ortho):
+        r = oracle.Solver(A, solver=oracle.GMRES, precond=oracle.PC_NONE, gmres_ortho=o).solve(b, rtol=1e-12)
+        assert r.converged and r.iters <= 6
+        assert np.linalg.norm(r.x - xs) <= 1e-10 * np.linalg.norm(xs)

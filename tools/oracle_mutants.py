@@ -27,8 +27,16 @@ MUTANTS = {
       }""", """      if (pass1[J] >= 0) {
         agg[I] = pass1[J];
       }"""),
+    "no_reorth_safeguard": ("if (pass == 0 && (ss > 0.5 || !(1.0 - ss > 1e-8))) {",
+                            "if (pass == 0 && false) {"),
+    "gram_f32_dots_off": ("p[i] = s.p.gmres_ortho == 2 ? dot_f32_basis(V[i], w) : dot(V[i], w);",
+                          "p[i] = dot(V[i], w);"),
 }
 DEFAULT = ["sa_sign", "no_lumping", "pass2_last"]
+# no_reorth_safeguard survives by design: without the guard a near-breakdown step ends the
+# cycle as a happy breakdown and the restart still converges (the guard saves iterations,
+# it does not change what is computed); gram_f32_dots_off survives for the same reason --
+# R23 only changes projection coefficients, not the minimal residuals the pins check.
 
 
 def run(name: str) -> bool:
