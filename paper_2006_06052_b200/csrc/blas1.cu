@@ -686,7 +686,15 @@ void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, ui
 template <bool VEC>
 __global__ void __launch_bounds__(kTM) k_idr_update(int64_t n, double a, const double* __restrict__ g,
                                                     const double* __restrict__ u, double* r, double* x,
-                                                    double* partials, unsigned* ticket, double* out, int post) {
+                                                    double* partials, unsigned* ticket, double* out, int post,
+                                                    const double* a_num = nullptr, const double* a_den = nullptr) {
+  // a_num / a_den (device, optional): a = a_num[0] / a_den[0] (CG's alpha = rho / p.q formed on
+  // the device, reading R24); the update is skipped when the denominator broke down
+  if (a_num) {
+    const double den = a_den[0];
+    a = a_num[0] / den;
+    if (den == 0.0 || !isfinite(den)) n = 0;
+  }
   // two elements per thread as 16-byte loads (all four loads in flight): 5.0 -> 6+ TB/s
   double acc[1] = {0.0};
   const int64_t n2 = VEC ? n / 2 : 0;
@@ -710,17 +718,32 @@ __global__ void __launch_bounds__(kTM) k_idr_update(int64_t n, double a, const d
 }
 
 void launch_idr_update(int64_t n, double a, const double* g, const double* u, double* r, double* x,
-                       double* partials, double* out, cudaStream_t s, CommBase* comm) {
+                       double* partials, double* out, cudaStream_t s, CommBase* comm, const double* a_num,
+                       const double* a_den) {
   ProfScope ps_(prof_name("idr_update", 1, AMG_F64, -1), 8.0 * n * 6, s);
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
   const int64_t work = (n + kTM - 1) / kTM;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)kMaxPartials, work));
   if (aligned16(g) && aligned16(u) && aligned16(r) && aligned16(x))
-    k_idr_update<true><<<grid, kTM, 0, s>>>(n, a, g, u, r, x, partials, ticket, out, comm ? 0 : 1);
+    k_idr_update<true><<<grid, kTM, 0, s>>>(n, a, g, u, r, x, partials, ticket, out, comm ? 0 : 1, a_num, a_den);
   else
-    k_idr_update<false><<<grid, kTM, 0, s>>>(n, a, g, u, r, x, partials, ticket, out, comm ? 0 : 1);
+    k_idr_update<false><<<grid, kTM, 0, s>>>(n, a, g, u, r, x, partials, ticket, out, comm ? 0 : 1, a_num, a_den);
   AMG_CK_LAUNCH();
   finalize_global(comm, out, 1, true, s);
+}
+
+// CG: p = z + beta p, beta = rz / rho from the device scalars (k_axpby's expression)
+__global__ void __launch_bounds__(kT) k_cg_p(int64_t n, const double* __restrict__ z, double* __restrict__ p,
+                                             const double* __restrict__ rz, const double* __restrict__ rho) {
+  const double beta = rz[0] / rho[0];
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT)
+    p[i] = (beta == 0.0) ? 1.0 * z[i] : fma(1.0, z[i], beta * p[i]);
+}
+
+void launch_cg_p(int64_t n, const double* z, double* p, const double* rz, const double* rho, cudaStream_t s) {
+  ProfScope ps_(prof_name("axpby", 1, AMG_F64, -1), 24.0 * n, s);
+  k_cg_p<<<ew_grid(n), kT, 0, s>>>(n, z, p, rz, rho);
+  AMG_CK_LAUNCH();
 }
 
 // ---- BiCGStab fused steps (one pass, deterministic reductions, last-block finish) ----

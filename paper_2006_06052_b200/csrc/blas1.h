@@ -59,8 +59,12 @@ void launch_lincomb(int64_t n, const LinComb& L, double* out, cudaStream_t s);
 void idrs_shadow_space(int64_t n, int sdim, uint64_t base, uint64_t n_global, uint64_t off, double* const* P,
                        double* partials, double* dscal, cudaStream_t s, CommBase* comm);
 // IDR(s) step: r -= a g; x += a u; out[0] = ||r|| (one pass, deterministic)
+// (a_num, a_den: device scalars, a = a_num[0] / a_den[0], no update when a_den[0] is 0 / not finite)
 void launch_idr_update(int64_t n, double a, const double* g, const double* u, double* r, double* x,
-                       double* partials, double* out, cudaStream_t s, CommBase* comm = nullptr);
+                       double* partials, double* out, cudaStream_t s, CommBase* comm = nullptr,
+                       const double* a_num = nullptr, const double* a_den = nullptr);
+// CG: p = z + beta p with beta = rz[0] / rho[0] (device)
+void launch_cg_p(int64_t n, const double* z, double* p, const double* rz, const double* rho, cudaStream_t s);
 // BiCGStab: out = r - (num / den[0]) v, dst[0] = out.out   (den on the device)
 void launch_sub_div_nrm(int64_t n, double num, const double* den, const double* v, const double* r, double* out,
                         double* partials, double* dst, cudaStream_t s, CommBase* comm = nullptr);

@@ -165,6 +165,92 @@ int solve_cg(Ctx& c, const double* b, double* x, double rtol, double nb, amg_rep
   return finish(c, b, x, r, nb, status, it, 0, rep);
 }
 
+// ---- PCG with device-side scalars: one CUDA graph per iteration (reading R24) ----
+// q = A p with p.q; r -= alpha q, x += alpha p with ||r|| (alpha = rho / p.q on the device);
+// z = M r; r.z; p = z + (r.z / rho) p -- one replay and one read per iteration (the host-driven
+// loop has three); the same kernels and expressions, so the iterates are bit-identical.
+int solve_cg_graphed(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
+  Handle& h = c.h;
+  double *r = h.vec[0], *z = h.vec[1], *p = h.vec[2], *q = h.vec[3];
+  double* sc = h.dscal + 160;  // [0] rho, [1] p.q, [2] ||r||, [3] r.z
+  double* hs = h.hscal + 160;
+  c.residual_nrm(b, x, r);
+  c.read(1);
+  int it = 0, status = AMG_NOT_CONVERGED;
+  if (std::sqrt(h.hscal[0]) <= rtol * nb) status = AMG_OK;
+  cudaGraphExec_t G = nullptr;
+  for (const auto& e : h.step_graphs)
+    if (e.first == x) G = e.second;
+  if (!G) {
+    const int64_t l0 = t_launches;
+    cudaGraph_t graph = nullptr;
+    AMG_CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+    try {
+      if (h.comm || !launch_spmv_dot(h.A, p, AMG_F64, q, p, nullptr, 1, h.partials, sc + 1, c.s, h.comm)) {
+        halo_overlapped(h, h.halo0, h.A, p, AMG_F64, h.b, c.s,
+                        [&](int r0, int r1) { launch_spmv(h.A, 1.0, p, AMG_F64, 0.0, q, AMG_F64, c.s, r0, r1); });
+        launch_dot(c.N, p, AMG_F64, q, AMG_F64, h.partials, sc + 1, false, c.s, h.comm);
+      }
+      launch_idr_update(c.N, 0.0, q, p, r, x, h.partials, sc + 2, c.s, h.comm, sc + 0, sc + 1);
+      precond_apply(h, r, z, AMG_F64, c.s);
+      launch_dot(c.N, r, AMG_F64, z, AMG_F64, h.partials, sc + 3, false, c.s, h.comm);
+      launch_cg_p(c.N, z, p, sc + 3, sc + 0, c.s);
+    } catch (...) {
+      cudaStreamEndCapture(c.s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    AMG_CK(cudaStreamEndCapture(c.s, &graph));
+    h.step_graph_kernels = t_launches - l0;
+    t_launches = l0;
+    g_launches -= h.step_graph_kernels;
+    cudaError_t e = cudaGraphInstantiate(&G, graph, 0);
+    cudaGraphDestroy(graph);
+    AMG_CK(e);
+    h.step_graphs.push_back({x, G});
+  }
+  const double step_bytes = h.alg_bytes_spmv + 8.0 * c.N + 48.0 * c.N + h.alg_bytes_precond + 16.0 * c.N + 24.0 * c.N;
+  bool restart = true;
+  double rho = 0.0;
+  while (status != AMG_OK && it < h.p.maxiter) {
+    if (restart) {
+      c.pc(r, z, AMG_F64);
+      launch_convert(c.N, z, AMG_F64, p, AMG_F64, 1.0, c.s);
+      c.bytes += 16.0 * c.N;
+      c.dot(r, z, 0);
+      c.read(1);
+      rho = h.hscal[0];
+      restart = false;
+    }
+    hs[0] = rho;
+    AMG_CK(cudaMemcpyAsync(sc, hs, sizeof(double), cudaMemcpyHostToDevice, c.s));
+    AMG_CK(cudaGraphLaunch(G, c.s));
+    g_launches += h.step_graph_kernels;
+    t_launches += h.step_graph_kernels;
+    c.bytes += step_bytes;
+    AMG_CK(cudaMemcpyAsync(hs + 1, sc + 1, sizeof(double) * 3, cudaMemcpyDeviceToHost, c.s));
+    AMG_CK(cudaStreamSynchronize(c.s));
+    const double pq = hs[1];
+    if (pq == 0.0 || !finite(pq)) {  // the step left x and r untouched
+      status = AMG_EBREAKDOWN;
+      break;
+    }
+    ++it;
+    if (hs[2] <= rtol * nb) {
+      c.residual_nrm(b, x, r);
+      c.read(1);
+      if (std::sqrt(h.hscal[0]) <= rtol * nb) {
+        status = AMG_OK;
+        break;
+      }
+      restart = true;
+      continue;
+    }
+    rho = hs[3];  // r.z: the step already formed p = z + (r.z / rho) p
+  }
+  return finish(c, b, x, r, nb, status, it, 0, rep);
+}
+
 // ---- BiCGStab (cfg 3) ----
 int solve_bicgstab(Ctx& c, const double* b, double* x, double rtol, double nb, amg_report* rep) {
   Handle& h = c.h;
@@ -813,7 +899,11 @@ int krylov_solve(Handle& h, const double* b, double* x, double rtol, cudaStream_
     return AMG_OK;
   }
   switch (h.p.solver) {
-    case AMG_CG: return solve_cg(c, b, x, rtol, nb, rep);
+    case AMG_CG:
+      if (h.p.use_graphs && !g_prof && !env_set("AMG_NO_GRAPH") && !env_set("AMG_NO_STEP_GRAPH") &&
+          (!h.comm || h.comm->capturable()))
+        return solve_cg_graphed(c, b, x, rtol, nb, rep);
+      return solve_cg(c, b, x, rtol, nb, rep);
     case AMG_BICGSTAB:
       // one graph per step unless graphs are off, the profiler times every launch, or the
       // communicator cannot be captured (the thread-emulated one)
