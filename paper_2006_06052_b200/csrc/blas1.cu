@@ -95,6 +95,34 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
   double acc[KA];
 #pragma unroll
   for (int j = 0; j < KA; ++j) acc[j] = 0.0;
+  if constexpr (MODE == 0 && std::is_same_v<TV, float>) {
+    // fp32 shadow basis (reading R23): four consecutive elements per thread, one 16-byte load
+    // per vector (the scalar form kept one 4-byte load per vector in flight: 2-4 TB/s)
+    const int64_t n4 = n / 4;
+    for (int64_t i4 = (int64_t)blockIdx.x * kTM + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * kTM) {
+      float4 raw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) raw[j] = __ldcs(reinterpret_cast<const float4*>(V.p[j]) + i4);
+      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
+      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        acc[j] = fma((double)raw[j].x, w0.x, acc[j]);
+        acc[j] = fma((double)raw[j].y, w0.y, acc[j]);
+        acc[j] = fma((double)raw[j].z, w1.x, acc[j]);
+        acc[j] = fma((double)raw[j].w, w1.y, acc[j]);
+      }
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+      const double wi = w[i];
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] = fma((double)reinterpret_cast<const TV*>(V.p[j])[i], wi, acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] *= sv[j];
+    reduce_finish<KA>(acc, KA, partials, ticket, out, post, inv);
+    return;
+  }
   const int64_t step = (int64_t)gridDim.x * kTM * U;
   for (int64_t i0 = (int64_t)blockIdx.x * kTM * U + threadIdx.x; i0 < n; i0 += step) {
     double wv[U], vv[U][K];
@@ -218,6 +246,49 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
   double nrm = 0.0;
   for (int64_t i0 = (int64_t)blockIdx.x * kCW; i0 < n; i0 += (int64_t)gridDim.x * kCW) {
     const bool full = i0 + kCW <= n;
+    if constexpr (MODE == 0 && std::is_same_v<TV, float>) {
+      // fp32 shadow basis (reading R23): lane owns elements i0 + 128 h + 4 lane + e (h, e < 2, 4)
+      // -- two 16-byte loads per vector and four for w (L1 serves the other warps' reads of
+      // the same w chunk), so a warp keeps as many bytes in flight as the fp64 kernel
+      if (full) {
+        float4 raw[NJ][2];
+#pragma unroll
+        for (int q = 0; q < NJ; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            raw[q][hh] = __ldcs(reinterpret_cast<const float4*>(vp[q] + i0 + 128 * hh + 4 * lane));
+        double2 wv[2][2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            wv[hh][e] = __ldg(reinterpret_cast<const double2*>(w + i0 + 128 * hh + 4 * lane) + e);
+#pragma unroll
+        for (int q = 0; q < NJ; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            acc[q] = fma((double)raw[q][hh].x, wv[hh][0].x, acc[q]);
+            acc[q] = fma((double)raw[q][hh].y, wv[hh][0].y, acc[q]);
+            acc[q] = fma((double)raw[q][hh].z, wv[hh][1].x, acc[q]);
+            acc[q] = fma((double)raw[q][hh].w, wv[hh][1].y, acc[q]);
+          }
+#pragma unroll
+        for (int q = 0; q < NJ; ++q)
+          if (!own[q]) acc[q] = 0.0;
+      } else {
+        for (int hh = 0; hh < 2; ++hh)
+          for (int e = 0; e < 4; ++e) {
+            const int64_t i = i0 + 128 * hh + 4 * lane + e;
+            if (i < n) {
+              const double wi = w[i];
+#pragma unroll
+              for (int q = 0; q < NJ; ++q)
+                if (own[q]) acc[q] = fma((double)vp[q][i], wi, acc[q]);
+            }
+          }
+      }
+      continue;
+    }
     double val[NJ][T];
     if constexpr (std::is_same_v<TV, double>) {
 #pragma unroll
@@ -737,7 +808,7 @@ __global__ void __launch_bounds__(kT) k_cg_p(int64_t n, const double* __restrict
                                              const double* __restrict__ rz, const double* __restrict__ rho) {
   const double beta = rz[0] / rho[0];
   for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT)
-    p[i] = (beta == 0.0) ? 1.0 * z[i] : fma(1.0, z[i], beta * p[i]);
+    p[i] = (beta == 0.0) ? z[i] : fma(1.0, z[i], __dmul_rn(beta, p[i]));  // __dmul_rn: no contraction
 }
 
 void launch_cg_p(int64_t n, const double* z, double* p, const double* rz, const double* rho, cudaStream_t s) {

@@ -89,7 +89,7 @@ int amg_params_default(amg_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
-  p->gmres_ortho = 1;
+  p->gmres_ortho = 2;
   return AMG_OK;
 }
 

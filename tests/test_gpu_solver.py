@@ -270,7 +270,8 @@ SOLVE_CASES = [
     ("ilu0-sweeps3-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, smoother=2, ilu_sweeps=3),
      False),
     # GPU orthogonalisation variants of flexible GMRES, each against the oracle's CGS2:
-    # two-pass Gram/Cholesky (R22) and the GPU's CGS2
+    # two-pass Gram/Cholesky (R22) and the GPU's CGS2 (every case above without gmres_ortho
+    # runs the GPU default, R23: the fp32-shadow first pass)
     ("gram-gmres-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
     ("gram-gmres-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
     ("gram-gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10, gmres_ortho=1),
@@ -392,14 +393,16 @@ def test_fp32_vs_fp64_iteration_parity(amg):
     assert abs(its[0] - its[1]) <= 1
 
 
+@pytest.mark.parametrize("ortho", [1, 2])
 @pytest.mark.parametrize("wide", [1, 99])
-def test_gram_gmres_kernel_paths(amg, envvars, wide):
-    # the update + dots + norm pass on the wide (wide=1) and K-templated (wide=99) kernels
+def test_gram_gmres_kernel_paths(amg, envvars, wide, ortho):
+    # the update + dots + norm pass (and, ortho = 2, the fp32-shadow multi-dot) on the wide
+    # (wide=1) and K-templated (wide=99) kernels
     envvars(AMG_CGS_WIDE=wide)
     n = 16
     ptr, col, val = gen.matrix(gen.STOKES, n)
     bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
-    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2, gmres_ortho=1)
+    A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2, gmres_ortho=ortho)
     ro = O.solve(bvec, rtol=1e-8)
     x, rep = _solve(amg, S, bvec)
     true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
@@ -579,18 +582,20 @@ def test_gram_gmres_reorthogonalisation_safeguard(amg, envvars, eigs, force):
     ptr, col, val = _block_diag_matrix(np.array(eigs), 2000, 3, rng)
     bvec = rng.standard_normal(6000)
     res = {}
-    for ortho in (0, 1):
+    for ortho in (0, 1, 2):
         A = amg.BSR.from_numpy(ptr, col, val)
         S = amg.Solver(A, amg.default_params(solver=amg.GMRES, precond=amg.PC_NONE, gmres_ortho=ortho,
                                              maxiter=1000))
         x, rep = _solve(amg, S, bvec)
         true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
         res[ortho] = (rep, true, S.counters()["reorth_passes"])
-    (r0, t0, _), (r1, t1, reorth) = res[0], res[1]
-    assert r0.converged and r1.converged and t0 <= 1e-8 and t1 <= 1e-8, (t0, t1)
-    assert abs(r0.iters - r1.iters) <= 2, (r0.iters, r1.iters)
-    if force:
-        assert reorth >= r1.iters
+    r0, t0, _ = res[0]
+    for o in (1, 2):
+        r1, t1, reorth = res[o]
+        assert r0.converged and r1.converged and t0 <= 1e-8 and t1 <= 1e-8, (o, t0, t1)
+        assert abs(r0.iters - r1.iters) <= 2, (o, r0.iters, r1.iters)
+        if force:
+            assert reorth >= r1.iters
     O = oracle.Solver(oracle.Mat.from_arrays(ptr, col, val), oracle.default_params(
         solver=oracle.GMRES, precond=oracle.PC_NONE, maxiter=1000))
     assert abs(O.solve(bvec, rtol=1e-8).iters - r1.iters) <= 2

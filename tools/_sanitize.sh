@@ -6,9 +6,9 @@ out=gpurun_out/r2/sanitizer.txt
 for tool in memcheck racecheck synccheck initcheck; do
   for c in cfg3 cfg4 cfg5 cg idrs dist2; do
     timeout 900 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize.py $c \
-      > /tmp/san_${tool}_$c.log 2>&1
+      > gpurun_out/r2/san_${tool}_$c.log 2>&1
     rc=$?
-    echo "$tool $c rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' /tmp/san_${tool}_$c.log | tail -1)" >> $out
+    echo "$tool $c rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' gpurun_out/r2/san_${tool}_$c.log | tail -1)" >> $out
   done
 done
 cat $out
