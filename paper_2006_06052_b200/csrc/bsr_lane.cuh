@@ -591,12 +591,22 @@ __device__ __forceinline__ void sellr_step(const V* __restrict__ vp, const int32
   }
 }
 
+// k_bsr_sellr's prefetch flags (pf): the low 16 bits cap one prefetch in KiB.  Measured and
+// dropped: prefetching the warp's NEXT slice with a persistent one-wave grid (cfg 5: A_0
+// smoother 6.1 -> 3.3 TB/s -- the prefetched wave evicts itself from L2), and per-lane L2
+// prefetches of the epilogue's operands (f, x, M) at the slice start (6.4 -> 6.2 TB/s: the
+// row index held across the loop adds spill)
+constexpr int kPfRest = 1 << 30;  // the rest of the current slice past its first step
+
 template <int BR, int BC, int W, typename V, typename X, bool FAST, class EPI>
 __global__ void __launch_bounds__(SellrCfg<BR, BC, W, V, FAST>::TPB, SellrCfg<BR, BC, W, V, FAST>::MINB) k_bsr_sellr(
     int n, int s0, int nslices, const int32_t* __restrict__ sptr, const int32_t* __restrict__ vptr,
     const int32_t* __restrict__ perm, const int32_t* __restrict__ scol, const V* __restrict__ sval,
-    const X* __restrict__ x, EPI epi) {
+    const X* __restrict__ x, EPI epi, int pf) {
   // slices [s0, nslices) (a row range of 32-aligned bounds: the distributed interior / boundary split)
+  // pf: at the start of a slice, lane 0 requests the slice's values past its first step into L2
+  // with one bulk (TMA) prefetch, so the per-step loads find them there instead of each step
+  // waiting a full DRAM round trip (the warp's steps are a dependent chain)
   using S = SellrShape<BR, BC, W>;
   constexpr int ND = EPI::kDots > 0 ? EPI::kDots : 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -608,7 +618,16 @@ __global__ void __launch_bounds__(SellrCfg<BR, BC, W, V, FAST>::TPB, SellrCfg<BR
     double acc[BR] = {};
     if (s < nslices) {
       const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;
-      const V* vp = sval + ((int64_t)__ldg(vptr + s) * 32 + lane) * W;
+      const int64_t v0 = __ldg(vptr + s);
+      const V* vp = sval + (v0 * 32 + lane) * W;
+      const uint32_t cap = (uint32_t)(pf & 0xffff) << 10;  // at most this many bytes per prefetch
+      if ((pf & kPfRest) && lane == 0 && L > S::GB) {
+        const int64_t first = (int64_t)S::NV * 32 * W;                     // the first step's values
+        const int64_t tot = ((int64_t)__ldg(vptr + s + 1) - v0) * 32 * W;  // the slice's values
+        const char* a = reinterpret_cast<const char*>(sval + v0 * 32 * W + first);
+        const uint32_t bytes = min((uint32_t)((tot - first) * (int64_t)sizeof(V)), cap) & ~15u;
+        if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+      }
       const int32_t* cp = scol + (int64_t)j0 * 32 + lane;
       int c[S::GB];
 #pragma unroll

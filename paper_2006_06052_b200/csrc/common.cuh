@@ -123,6 +123,7 @@ struct Mat {
   // sell_vptr [sell_ns + 1] vector offsets
   int32_t* sell_vptr = nullptr;
   int sell_w = 0;
+  int sell_pf = 0;      // k_bsr_sellr bulk L2 prefetch flags (bsr_lane.cuh kPfRest | KiB cap)
   bool fast32 = false;  // internal fp32-hierarchy matrices: fp32 block-row dots (bsr.cuh item_dot)
   int rows_per_block() const { return br ? br : b; }
   int cols_per_block() const { return bc ? bc : b; }

@@ -309,6 +309,11 @@ static void build_sellr(Mat& A, Arena& arena, cudaStream_t s) {
   AMG_CK_LAUNCH();
   AMG_CK(cudaStreamSynchronize(s));
   A.lane_var = kLaneSellR;
+  // bulk L2 prefetch of each slice past its first step (kPfRest): the 8-byte-vector 3x3 fp32
+  // rows of >= 5 blocks -- 2-4 dependent steps per slice at 40 registers (cfg 5 A_0: smoother
+  // 6.08 -> 6.42-6.53, residual 5.95 -> 6.39-6.42 TB/s); the 16-byte-vector / fp64 shapes lose
+  // 1-3 % with it (outer 4x4 fp64 7.07 -> 6.97, R_0 6.34 -> 6.07-6.16 TB/s)
+  A.sell_pf = (short3 && W == 2 && per_row >= 5.0) ? (kPfRest | 64) : 0;
 }
 
 void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
@@ -431,6 +436,8 @@ static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool
                          int s1 = -1) {
   if (s1 < 0) s1 = A.sell_ns;
   if (s1 <= s0) return;
+  // L2 prefetches (plan: Mat::sell_pf; AMG_SELLR_PF overrides): kPfRest | KiB cap
+  const int pf = env_set("AMG_SELLR_PF") ? env_int("AMG_SELLR_PF", 0) : A.sell_pf;
   auto go = [&](auto Wc) {
     constexpr int W = decltype(Wc)::value;
     constexpr bool can_fast = std::is_same_v<V, float> && std::is_same_v<X, float>;
@@ -440,7 +447,7 @@ static void launch_sellr(const Mat& A, const X* x, EPI epi, cudaStream_t s, bool
       int64_t g = ((int64_t)s1 - s0 + Cfg::WPB - 1) / Cfg::WPB;
       if (dots) g = std::min<int64_t>(g, kMaxPartials);
       k_bsr_sellr<BR, BC, W, V, X, F, EPI><<<(unsigned)std::max<int64_t>(g, 1), Cfg::TPB, 0, s>>>(
-          A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col, (const V*)A.sell_val, x, epi);
+          A.n, s0, s1, A.sell_ptr, A.sell_vptr, A.sell_perm, A.sell_col, (const V*)A.sell_val, x, epi, pf);
     };
     if (can_fast && fast) run(std::integral_constant<bool, can_fast>{});
     else run(std::false_type{});
