@@ -21,7 +21,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
-SPAI0, JACOBI, ILU0 = 0, 1, 2
+SPAI0, JACOBI, ILU0, ILUT = 0, 1, 2, 3
 SA, PLAIN = 0, 1  # coarsening
 OK, NOT_CONVERGED, EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EBREAKDOWN = 0, 1, -1, -2, -3, -4, -6
 
@@ -46,6 +46,7 @@ class Params(ctypes.Structure):
         ("nparts", ctypes.c_int32), ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32),
         ("schur_u_scalar", ctypes.c_int32), ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32),
         ("over_interp", ctypes.c_double), ("ilu_sweeps", ctypes.c_int32), ("gmres_ortho", ctypes.c_int32),
+        ("ilut_tau", ctypes.c_double), ("ilut_p", ctypes.c_int32),
     ]
 
 

@@ -68,6 +68,8 @@ extern "C" void orc_params_default(orc_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
+  p->ilut_tau = 1e-2;  // SPEC.md:443 (the paper gives none)
+  p->ilut_p = 2;
   p->gmres_ortho = 0;  // CGS2; 1 = the two-pass Gram/Cholesky variant (R22)
 }
 
@@ -593,6 +595,86 @@ static int ilu0_factor(const orc_mat& A, orc_mat& Lo, orc_mat& Up, vector<double
   return ORC_OK;
 }
 
+// ---------------------------------------------------------------- C8c ILUT(tau, p)
+// Block ILUT -- the paper's U-solver smoother, "amgcl::relaxation::ilut" (Listing V2,
+// PAPER.md:599; "AMG with ILU as a smoother has the best performance");
+// the paper gives no (tau, p), SPEC.md:443 fixes the defaults tau = 1e-2, p = 2.  Saad's
+// threshold IKJ factorisation (Iterative Methods, Alg. 10.6, ILUT) on blocks, reading R25:
+//   w = row i of A;  tau_i = tau * ||row i of A||_2 (all its scalars)
+//   for k < i in w, ascending (fill entries created on the way included):
+//     w_k <- w_k D_k^-1;  if ||w_k||_F < tau_i: drop w_k (no update)
+//     else w_j <- w_j - w_k U_kj for every stored U_kj of row k (new entries start at 0)
+//   drop every w_j, j != i, with ||w_j||_F < tau_i;  of the surviving entries, L (j < i) and
+//   U (j > i) each keep those on A's pattern and the p largest fill entries (||.||_F
+//   descending, lower column first on ties);  D_i = w_i (error if singular).
+// The factors are stored as ILU(0)'s are: L_s = the kept w_j, j < i; U_s = the kept w_j,
+// j > i; Dinv = D_i^-1 -- applied by the same sweeps (R20).
+static int ilut_factor(const orc_mat& A, double tau, int p, orc_mat& Lo, orc_mat& Up, vector<double>& Dinv) {
+  const int b = A.b, bb = b * b;
+  Dinv.assign((size_t)A.n * bb, 0.0);
+  for (orc_mat* F : {&Lo, &Up}) {
+    F->n = A.n;
+    F->m = A.m;
+    F->b = b;
+    F->ptr.assign(A.n + 1, 0);
+    F->col.clear();
+    F->val.clear();
+  }
+  vector<double> tmp(bb);
+  for (int32_t i = 0; i < A.n; ++i) {
+    std::map<int32_t, vector<double>> w;
+    double nrm2 = 0.0;
+    for (int32_t kk = A.ptr[i]; kk < A.ptr[i + 1]; ++kk) {
+      w[A.col[kk]] = vector<double>(A.blk(kk), A.blk(kk) + bb);
+      nrm2 = nrm2 + fro2(A.blk(kk), b);
+    }
+    const double tau_i = tau * std::sqrt(nrm2);
+    for (auto it = w.begin(); it != w.end() && it->first < i;) {
+      const int32_t k = it->first;
+      blk_mul(b, it->second.data(), &Dinv[(size_t)k * bb], tmp.data());
+      if (std::sqrt(fro2(tmp.data(), b)) < tau_i) {
+        it = w.erase(it);
+        continue;
+      }
+      it->second = tmp;
+      for (int32_t kj = Up.ptr[k]; kj < Up.ptr[k + 1]; ++kj) {
+        auto jt = w.find(Up.col[kj]);
+        if (jt == w.end()) jt = w.emplace(Up.col[kj], vector<double>(bb, 0.0)).first;
+        blk_mul(b, it->second.data(), Up.blk(kj), tmp.data());
+        for (int e = 0; e < bb; ++e) jt->second[e] = jt->second[e] - tmp[e];
+      }
+      ++it;
+    }
+    auto dt = w.find(i);
+    if (dt == w.end()) return ORC_EZERODIAG;
+    int rc = block_inverse(b, dt->second.data(), &Dinv[(size_t)i * bb]);
+    if (rc != ORC_OK) return rc;
+    for (int side = 0; side < 2; ++side) {  // 0: L (j < i), 1: U (j > i)
+      vector<std::pair<double, int32_t>> fill;
+      vector<int32_t> keep;
+      for (auto& [j, v] : w) {
+        if (j == i || (side == 0) != (j < i)) continue;
+        const double nv = std::sqrt(fro2(v.data(), b));
+        if (nv < tau_i) continue;
+        if (find_block(A, i, j) >= 0) keep.push_back(j);
+        else fill.push_back({nv, j});
+      }
+      std::sort(fill.begin(), fill.end(), [](const std::pair<double, int32_t>& x, const std::pair<double, int32_t>& y) {
+        return x.first > y.first || (x.first == y.first && x.second < y.second);
+      });
+      for (size_t q = 0; q < fill.size() && (int)q < p; ++q) keep.push_back(fill[q].second);
+      std::sort(keep.begin(), keep.end());
+      orc_mat& F = side == 0 ? Lo : Up;
+      for (int32_t j : keep) {
+        F.col.push_back(j);
+        F.val.insert(F.val.end(), w[j].begin(), w[j].end());
+      }
+      F.ptr[i + 1] = (int32_t)F.col.size();
+    }
+  }
+  return ORC_OK;
+}
+
 // ---------------------------------------------------------------- C8 smoother
 // SPAI0: M_I = theta_I A_II^-1, theta_I = ||A_II||_F^2 / sum_J ||A_IJ||_F^2
 // (block generalisation of Broker-Grote SPAI(0)).
@@ -727,6 +809,8 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
     L.R = transpose(L.P);
     if (p.smoother == ORC_ILU0)
       rc = ilu0_factor(A, L.L, L.U, L.M);
+    else if (p.smoother == ORC_ILUT)
+      rc = ilut_factor(A, p.ilut_tau, p.ilut_p, L.L, L.U, L.M);
     else
       rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
     if (rc != ORC_OK) return rc;
@@ -830,11 +914,11 @@ static void ilu_into(const Level& L, int k, const double* g, const double* x0, d
 
 // x = S(f) from zero (K4a) and x <- x + S(f - A x) (K5) for the level's smoother
 static void pre_smooth(const orc_solver& s, const Level& L, const double* f, double* x, bool rf) {
-  if (s.p.smoother == ORC_ILU0) ilu_into(L, s.p.ilu_sweeps, f, nullptr, x, rf);
+  if (s.p.smoother == ORC_ILU0 || s.p.smoother == ORC_ILUT) ilu_into(L, s.p.ilu_sweeps, f, nullptr, x, rf);
   else apply_M(L.Ms, L.As.b, L.As.n, f, x, rf);
 }
 static void post_smooth(const orc_solver& s, const Level& L, const double* f, vector<double>& x, bool rf) {
-  if (s.p.smoother != ORC_ILU0) {
+  if (s.p.smoother != ORC_ILU0 && s.p.smoother != ORC_ILUT) {
     smooth_step(L.As, L.Ms, f, x, rf);
     return;
   }
@@ -1182,7 +1266,8 @@ static void precond(const orc_solver& s, const double* r, double* z) {
 
 extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out) {
   if (!A || !p || !out || A->n != A->m) return ORC_EINVAL;
-  if (p->smoother == ORC_ILU0 && p->ilu_sweeps < 1) return ORC_EINVAL;
+  if ((p->smoother == ORC_ILU0 || p->smoother == ORC_ILUT) && p->ilu_sweeps < 1) return ORC_EINVAL;
+  if (p->smoother == ORC_ILUT && (!(p->ilut_tau >= 0.0) || p->ilut_p < 0)) return ORC_EINVAL;
   orc_solver* s = new orc_solver;
   s->p = *p;
   s->A = *A;
@@ -1205,7 +1290,8 @@ extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out
 
 extern "C" int orc_setup_pmask(const orc_mat* A, const uint8_t* pmask, const orc_params* p, orc_solver** out) {
   if (!A || !pmask || !p || !out || A->n != A->m || p->precond != ORC_PC_SCHUR) return ORC_EINVAL;
-  if (p->schur_shat == 2 || (p->smoother == ORC_ILU0 && p->ilu_sweeps < 1)) return ORC_EINVAL;
+  if (p->schur_shat == 2 || ((p->smoother == ORC_ILU0 || p->smoother == ORC_ILUT) && p->ilu_sweeps < 1)) return ORC_EINVAL;
+  if (p->smoother == ORC_ILUT && (!(p->ilut_tau >= 0.0) || p->ilut_p < 0)) return ORC_EINVAL;
   orc_solver* s = new orc_solver;
   s->p = *p;
   s->A = *A;

@@ -22,7 +22,7 @@ extern "C" {
 
 enum { ORC_CG = 0, ORC_BICGSTAB = 1, ORC_GMRES = 2, ORC_IDRS = 3 };
 enum { ORC_PC_AMG = 0, ORC_PC_SCHUR = 1, ORC_PC_NONE = 2 };
-enum { ORC_SPAI0 = 0, ORC_JACOBI = 1, ORC_ILU0 = 2 };
+enum { ORC_SPAI0 = 0, ORC_JACOBI = 1, ORC_ILU0 = 2, ORC_ILUT = 3 };
 enum { ORC_SA = 0, ORC_PLAIN = 1 };
 
 enum {
@@ -34,7 +34,8 @@ typedef struct {
   int32_t solver, gmres_m, precond, maxiter;
   int32_t hier_f32;      /* hierarchy values (A_l, P_l, R_l, M_l, coarse, B, B^T, m_S) rounded to fp32 */
   int32_t vec_f32;       /* V-cycle / Schur inner vectors rounded to fp32 at every store */
-  int32_t smoother;      /* ORC_SPAI0 | ORC_JACOBI | ORC_ILU0 (block ILU(0), sweep-solved, R20) */
+  int32_t smoother;      /* ORC_SPAI0 | ORC_JACOBI | ORC_ILU0 (block ILU(0), sweep-solved, R20) |
+                            ORC_ILUT (block ILUT(tau, p), sweep-solved, R25) */
   double jacobi_omega;   /* 2/3 */
   double sa_omega;       /* 2/3 */
   double eps_strong;     /* 1e-3 */
@@ -53,9 +54,11 @@ typedef struct {
                             (adjust_p = 1); 2 = the explicitly
                             assembled C - B diag(A_u)^-1 B^T (the PETSc variant) */
   double over_interp;    /* plain aggregation: A_c = (1/over_interp) P^T A P (reading R19, 1.5) */
-  int32_t ilu_sweeps;    /* ORC_ILU0: Jacobi sweeps per triangular solve (>= 1, default 2, R20) */
+  int32_t ilu_sweeps;    /* ORC_ILU0 / ORC_ILUT: Jacobi sweeps per triangular solve (>= 1, default 2, R20) */
   int32_t gmres_ortho;   /* GMRES orthogonalisation: 0 CGS2 (default), 1 two-pass Gram/Cholesky
                             (R22), 2 the same with the first pass's dots on the fp32-rounded basis (R23) */
+  double ilut_tau;       /* ORC_ILUT drop tolerance relative to the row's 2-norm (1e-2) */
+  int32_t ilut_p;        /* ORC_ILUT fill entries kept per row in each of L and U (2) */
 } orc_params;
 
 typedef struct {

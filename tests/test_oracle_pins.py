@@ -631,6 +631,154 @@ def test_ilu0_smoothed_solves_reach_dense_solution(rng):
         assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd), (kind, solver)
 
 
+# ---- C8c block ILUT(tau, p) smoother (Listing V2 "relaxation::ilut"; reading R25) ----
+def _ilut(ptr, col, val, tau, p, **kw):
+    kw.setdefault("coarse_enough", 1)
+    kw.setdefault("max_levels", 2)
+    A, S = _solver(ptr, col, val, smoother=oracle.ILUT, precond=oracle.PC_AMG, ilut_tau=tau, ilut_p=p,
+                   hier_f32=0, vec_f32=0, **kw)
+    assert S.levels >= 2
+    return A, S
+
+
+def _factors(S):
+    """(L_s, U_s, D) at level 0 as dicts {(i, j): block} and the list of pivot blocks."""
+    out = []
+    for which in (4, 5):
+        fp, fc, fv = S.level_mat(0, which).to_arrays()
+        out.append({(i, int(fc[k])): fv[k] for i in range(len(fp) - 1) for k in range(fp[i], fp[i + 1])})
+    D = [np.linalg.inv(m) for m in S.level_M(0)]
+    return out[0], out[1], D
+
+
+def _csr3(rows):
+    ptr, col, val = [0], [], []
+    for r in rows:
+        for j, v in enumerate(r):
+            if v != 0:
+                col.append(j)
+                val.append([[v]])
+        ptr.append(len(col))
+    return np.array(ptr, np.int32), np.array(col, np.int32), np.array(val, float)
+
+
+def test_ilut_fill_limit_hand_example():
+    # worked by hand: A = [[1,1,1],[1,3,0],[1,0,3]], tau = 0.  Row 1 eliminates (1,0) with
+    # multiplier 1 and creates fill (1,2) = -1; row 2 creates fill (2,1) = -1, whose multiplier
+    # -1/2 updates (2,2) through U(1,2) only if that fill was kept.
+    #   p = 0: L = {(1,0): 1, (2,0): 1}, U = {(0,1): 1, (0,2): 1}, D = (1, 2, 2)
+    #   p = 1: + L(2,1) = -1/2, U(1,2) = -1, D = (1, 2, 3/2)  (= the exact LU)
+    ptr, col, val = _csr3([[1, 1, 1], [1, 3, 0], [1, 0, 3]])
+    _, S = _ilut(ptr, col, val, 0.0, 0)
+    L, U, D = _factors(S)
+    assert {k: float(v[0, 0]) for k, v in L.items()} == {(1, 0): 1.0, (2, 0): 1.0}
+    assert {k: float(v[0, 0]) for k, v in U.items()} == {(0, 1): 1.0, (0, 2): 1.0}
+    assert np.allclose([d[0, 0] for d in D], [1, 2, 2], rtol=0, atol=1e-15)
+    _, S = _ilut(ptr, col, val, 0.0, 1)
+    L, U, D = _factors(S)
+    assert {k: float(v[0, 0]) for k, v in L.items()} == {(1, 0): 1.0, (2, 0): 1.0, (2, 1): -0.5}
+    assert {k: float(v[0, 0]) for k, v in U.items()} == {(0, 1): 1.0, (0, 2): 1.0, (1, 2): -1.0}
+    assert np.allclose([d[0, 0] for d in D], [1, 2, 1.5], rtol=0, atol=1e-15)
+
+
+def test_ilut_keeps_largest_fill_hand_example():
+    # row 1 of [[1,0,1,3],[1,5,0,0],[0,0,4,0],[0,0,0,4]] eliminates (1,0) (multiplier 1) and
+    # creates two U fills, (1,2) = -1 and (1,3) = -3: p = 1 keeps the larger, (1,3).  With a
+    # tie ((1,2) = (1,3) = -2) the lower column is kept.
+    ptr, col, val = _csr3([[1, 0, 1, 3], [1, 5, 0, 0], [0, 0, 4, 0], [0, 0, 0, 4]])
+    _, S = _ilut(ptr, col, val, 0.0, 1)
+    _, U, _ = _factors(S)
+    assert {k: float(v[0, 0]) for k, v in U.items() if k[0] == 1} == {(1, 3): -3.0}
+    ptr, col, val = _csr3([[1, 0, 2, 2], [1, 5, 0, 0], [0, 0, 4, 0], [0, 0, 0, 4]])
+    _, S = _ilut(ptr, col, val, 0.0, 1)
+    _, U, _ = _factors(S)
+    assert {k: float(v[0, 0]) for k, v in U.items() if k[0] == 1} == {(1, 2): -2.0}
+
+
+def test_ilut_threshold_hand_example():
+    # worked by hand: A = [[10,1,0],[3,10,5],[0,6,10]], tau = 0.05, p = 2.
+    #   row 0: tau_0 = 0.05 sqrt(101) = 0.5025: U(0,1) = 1 kept
+    #   row 1: tau_1 = 0.05 sqrt(134) = 0.5788: multiplier 3/10 = 0.3 dropped, with no update
+    #          (so D_1 = 10, not 10 - 0.3 * 1 = 9.7); U(1,2) = 5 kept
+    #   row 2: tau_2 = 0.05 sqrt(136) = 0.5831: multiplier 6/10 = 0.6 kept, D_2 = 10 - 0.6 * 5 = 7
+    # (a threshold not scaled by the row norm, a drop test on the unscaled w_k, or an update
+    # applied for a dropped multiplier each give D_1 = 9.7)
+    ptr, col, val = _csr3([[10, 1, 0], [3, 10, 5], [0, 6, 10]])
+    _, S = _ilut(ptr, col, val, 0.05, 2)
+    L, U, D = _factors(S)
+    assert set(L) == {(2, 1)} and abs(L[(2, 1)][0, 0] - 0.6) <= 1e-15
+    assert set(U) == {(0, 1), (1, 2)} and U[(0, 1)][0, 0] == 1.0 and U[(1, 2)][0, 0] == 5.0
+    assert np.allclose([d[0, 0] for d in D], [10, 10, 7], rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("b", [1, 2, 3])
+def test_ilut_without_dropping_is_exact_lu(rng, b):
+    # tau = 0 and p >= n (SPEC.md:401): nothing is dropped, ILUT = the exact LU (numpy dense)
+    n = 24
+    ptr, col, val = random_bsr(rng, n, b, density=0.2, dom=4 * b)
+    A, S = _ilut(ptr, col, val, 0.0, n)
+    Ls, Us, D = _factors(S)
+    L = np.eye(n * b)
+    U = np.zeros((n * b, n * b))
+    for (i, j), v in Ls.items():
+        L[i * b:(i + 1) * b, j * b:(j + 1) * b] = v
+    for (i, j), v in Us.items():
+        U[i * b:(i + 1) * b, j * b:(j + 1) * b] = v
+    for i in range(n):
+        U[i * b:(i + 1) * b, i * b:(i + 1) * b] = D[i]
+    Ad = A.dense()
+    assert np.linalg.norm(L @ U - Ad) <= 1e-12 * np.linalg.norm(Ad)
+    # and the sweep-solved smoother with sweeps >= the depth is A^-1
+    _, S2 = _ilut(ptr, col, val, 0.0, n, ilu_sweeps=n)
+    f = rng.standard_normal(n * b)
+    assert np.linalg.norm(S2.level_smooth(0, f) - np.linalg.solve(Ad, f)) <= 1e-10 * np.linalg.norm(f)
+
+
+def test_ilut_limits(rng):
+    # tau = inf: everything off the diagonal is dropped (SPEC.md:403), D_i = A_ii
+    n, b = 30, 3
+    ptr, col, val = random_bsr(rng, n, b, density=0.2, dom=10)
+    A, S = _ilut(ptr, col, val, 1e300, 2)
+    L, U, D = _factors(S)
+    assert not L and not U
+    for i in range(n):
+        k = ptr[i] + int(np.nonzero(col[ptr[i]:ptr[i + 1]] == i)[0][0])
+        assert np.allclose(D[i], val[k], rtol=1e-12)
+
+
+def test_ilut_row_bounds(rng):
+    # every kept off-diagonal block has ||.||_F >= tau ||a_i||_2, and each of L and U keeps at
+    # most p entries outside A's pattern (SPEC.md:401)
+    n, b, tau, p = 80, 3, 0.01, 2
+    ptr, col, val = random_bsr(rng, n, b, density=0.08, dom=4)
+    A, S = _ilut(ptr, col, val, tau, p)
+    L, U, _ = _factors(S)
+    pat = {(i, int(col[k])) for i in range(n) for k in range(ptr[i], ptr[i + 1])}
+    rown = [np.sqrt(sum(np.sum(val[k] ** 2) for k in range(ptr[i], ptr[i + 1]))) for i in range(n)]
+    nfill = 0
+    for F in (L, U):
+        for i in range(n):
+            ent = [(j, v) for (r, j), v in F.items() if r == i]
+            assert all(np.linalg.norm(v) >= tau * rown[i] for _, v in ent)
+            fill = [j for j, _ in ent if (i, j) not in pat]
+            assert len(fill) <= p
+            nfill += len(fill)
+    assert nfill > 0  # the case exercises the fill limit
+
+
+def test_ilut_smoothed_solves_reach_dense_solution(rng):
+    for kind, pc, solver in ((gen.STOKES, oracle.PC_SCHUR, oracle.GMRES), (gen.POISSON3, oracle.PC_AMG, oracle.IDRS)):
+        ptr, col, val = gen.matrix(kind, 8)
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        S = oracle.Solver(A, precond=pc, solver=solver, smoother=oracle.ILUT, coarse_enough=60,
+                          hier_f32=0, vec_f32=0)
+        assert S.levels >= 2
+        b = rng.standard_normal((len(ptr) - 1) * val.shape[-1])
+        r = S.solve(b, rtol=1e-10)
+        xd = np.linalg.solve(A.dense(), b)
+        assert r.converged and np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd), (kind, solver)
+
+
 def test_jacobi_smoother_closed_form():
     n = 6
     ptr, col, val = laplace3_blocks(n)
