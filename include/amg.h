@@ -43,7 +43,8 @@ enum {
 typedef enum { AMG_F64 = 0, AMG_F32 = 1 } amg_dtype;
 enum { AMG_CG = 0, AMG_BICGSTAB = 1, AMG_GMRES = 2, AMG_IDRS = 3 };
 enum { AMG_PC_AMG = 0, AMG_PC_SCHUR = 1, AMG_PC_NONE = 2 };
-enum { AMG_SPAI0 = 0, AMG_JACOBI = 1, AMG_ILU0 = 2 /* block ILU(0), Jacobi-sweep solves (R20) */ };
+enum { AMG_SPAI0 = 0, AMG_JACOBI = 1, AMG_ILU0 = 2 /* block ILU(0), Jacobi-sweep solves (R20) */,
+       AMG_ILUT = 3 /* block ILUT(tau, p), the paper's U-solver smoother (Listing V2), same solves (R25) */ };
 /* coarsening: smoothed aggregation | plain aggregation, P = P_tent
    (Listings V2-V4, "amgcl::coarsening::aggregation") */
 enum { AMG_SA = 0, AMG_PLAIN_AGG = 1 };
@@ -75,9 +76,10 @@ typedef struct {
   int32_t hier_dtype;        /* values of A_l, P_l, R_l, M_l, coarse inverse, B, B^T, m_S:
                                 AMG_F32 (default, Listing V4) | AMG_F64 */
   int32_t vcycle_vec_dtype;  /* vectors inside the preconditioner: AMG_F32 (default) | AMG_F64 */
-  int32_t smoother;          /* AMG_SPAI0 (default) | AMG_JACOBI | AMG_ILU0
-                                (single device; the paper's U-solver smoother is ILU-type,
-                                PAPER.md:551-553) */
+  int32_t smoother;          /* AMG_SPAI0 (default) | AMG_JACOBI | AMG_ILU0 | AMG_ILUT
+                                (ILU: single device; the paper's U-solver smoother is ILUT,
+                                Listing V2, "AMG with ILU as a smoother has the best
+                                performance") */
   int32_t coarse_enough;     /* max scalar unknowns of the coarsest level, default 3000 */
   double jacobi_omega;       /* damped-Jacobi weight, default 2/3 */
   double sa_omega;           /* prolongator damping, default 2/3 (reading R5) */
@@ -98,12 +100,18 @@ typedef struct {
                                 variant) */
   double over_interp;        /* AMG_PLAIN_AGG: A_c = (1/over_interp) P^T A P, default 1.5
                                 (over-interpolation, reading R19); ignored for AMG_SA */
-  int32_t ilu_sweeps;        /* AMG_ILU0: Jacobi sweeps per triangular solve, 1..16, default 2 */
+  int32_t ilu_sweeps;        /* AMG_ILU0 / AMG_ILUT: Jacobi sweeps per triangular solve, 1..16, default 2 */
   int32_t gmres_ortho;       /* AMG_GMRES orthogonalisation: 2 (default) two-pass Gram/Cholesky with the
                                 first pass's dots on an fp32 shadow of the basis (R23; +31 fp32
                                 vectors of workspace); 1 two-pass Gram/Cholesky on the fp64 basis (R22);
                                 0 CGS2 (three passes over the basis per step).  1 and 2 reorthogonalise a
                                 step whose new direction is still far from orthogonal (R22 safeguard) */
+  int32_t fused_presmooth;   /* 1 (default): the pre-smoothing from zero x = M f (K4a) runs in the epilogue of
+                                the kernel that produces f (split, B^T update, restriction; DESIGN.md
+                                "Fused K4"), bit-identical to 0 (a separate x = M f pass per level) */
+  int32_t ilut_p;            /* AMG_ILUT: fill blocks kept per row in each of L and U beyond A's pattern,
+                                >= 0, default 2 (the paper gives none) */
+  double ilut_tau;           /* AMG_ILUT: drop blocks with ||.||_F < tau ||row of A||_2, >= 0, default 1e-2 */
 } amg_params;
 
 typedef struct {
@@ -192,8 +200,9 @@ void bsr_plan_destroy(struct bsr_plan* P);
 /* out[5] = {n_block_rows, block_size, nnzb(A_l), nnzb(P_l) or 0, n_coarse or 0} */
 int amg_level_info(struct amg_handle* h, int32_t level, int64_t* out);
 /* which: 0 = A_l, 1 = P_l, 2 = R_l (the solve copies in the hierarchy dtype, widened to fp64); 3 = smoother blocks M_l
- * (ptr/col ignored, val = n*b*b; AMG_ILU0: the pivot inverses D^-1); 4 / 5 = the ILU(0) strictly lower / upper
- * factors (AMG_ILU0 only, else AMG_EINVAL; at most nnz(A_l) - n_l blocks, ptr[n] gives the count).  Arrays sized
+ * (ptr/col ignored, val = n*b*b; AMG_ILU0: the pivot inverses D^-1); 4 / 5 = the ILU strictly lower / upper
+ * factors (AMG_ILU0 / AMG_ILUT only, else AMG_EINVAL; at most nnz(A_l) - n_l blocks, + ilut_p * n_l with
+ * AMG_ILUT; ptr[n] gives the count).  Arrays sized
  * from amg_level_info. */
 int amg_level_export(struct amg_handle* h, int32_t level, int32_t which, int32_t* ptr, int32_t* col,
                      double* val);

@@ -23,7 +23,7 @@ EINVAL, EDIM, EZERODIAG, ESINGULAR_BLOCK, EINDEX_OVERFLOW, EBREAKDOWN, ECUDA, EN
 F64, F32 = 0, 1
 CG, BICGSTAB, GMRES, IDRS = 0, 1, 2, 3
 PC_AMG, PC_SCHUR, PC_NONE = 0, 1, 2
-SPAI0, JACOBI, ILU0 = 0, 1, 2
+SPAI0, JACOBI, ILU0, ILUT = 0, 1, 2, 3
 SA, PLAIN_AGG = 0, 1  # coarsening
 
 
@@ -50,7 +50,8 @@ class amg_params(ctypes.Structure):
                 ("schur_p_component", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
                 ("idrs_s", ctypes.c_int32), ("idrs_seed", ctypes.c_int32), ("schur_u_scalar", ctypes.c_int32),
                 ("coarsening", ctypes.c_int32), ("schur_shat", ctypes.c_int32), ("over_interp", ctypes.c_double),
-                ("ilu_sweeps", ctypes.c_int32), ("gmres_ortho", ctypes.c_int32)]
+                ("ilu_sweeps", ctypes.c_int32), ("gmres_ortho", ctypes.c_int32),
+                ("fused_presmooth", ctypes.c_int32), ("ilut_p", ctypes.c_int32), ("ilut_tau", ctypes.c_double)]
 
 
 class amg_report(ctypes.Structure):
@@ -354,7 +355,7 @@ class Solver:
 
     def level_export(self, level: int, which: int):
         """which 0/1/2: (ptr, col, val[nnz,b,b]) of A_l/P_l/R_l; 3: M_l [n,b,b] (fp64 host numpy);
-        4/5: the ILU(0) strictly lower / upper factors (AMG_ILU0)."""
+        4/5: the ILU strictly lower / upper factors (AMG_ILU0 / AMG_ILUT)."""
         import numpy as np
         n, b, nnzA, nnzP, nc = self.level_info(level)
         if which == 3:
@@ -363,7 +364,9 @@ class Solver:
                    "amg_level_export")
             return val
         rows = {0: n, 1: n, 2: nc, 4: n, 5: n}[which]
-        nnz = nnzA if which in (0, 4, 5) else nnzP  # the factors: at most nnz(A) - n blocks
+        nnz = nnzA if which in (0, 4, 5) else nnzP  # ILU(0) factors: at most nnz(A) - n blocks
+        if which in (4, 5) and self.params.smoother == ILUT:
+            nnz += self.params.ilut_p * n  # ILUT: + p fill blocks per row on each side
         ptr = np.zeros(rows + 1, dtype=np.int32)
         col = np.zeros(max(nnz, 1), dtype=np.int32)
         val = np.zeros((max(nnz, 1), b, b))

@@ -107,6 +107,38 @@ struct LEpiSpmv {  // y = alpha A x + beta y
   }
 };
 
+// y = A x + y (beta = 1: the prolongation K7) with y[row] loaded BEFORE the row's blocks
+// (k_bsr_sellr only): short-row matrices (P_0: 3.6 blocks per row, two steps) are latency
+// bound on their chain of dependent loads, and the epilogue's y load is independent of it
+template <typename Y>
+struct LEpiSpmvPre : LEpiSpmv<Y> {
+  static constexpr bool kPre = true;
+  using PreT = Y;
+  template <int BR>
+  __device__ __forceinline__ void pre(int row, Y (&v)[BR]) const {
+#pragma unroll
+    for (int c = 0; c < BR; ++c) v[c] = this->y[(int64_t)row * BR + c];
+  }
+  template <int BR>
+  __device__ __forceinline__ void row_pre(int row, const double (&yr)[BR], const Y (&v)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+#pragma unroll
+    for (int c = 0; c < BR; ++c) this->y[o + c] = to_out<Y>(fma(this->beta, (double)v[c], this->alpha * yr[c]));
+  }
+};
+template <class E, class = void>
+struct EpiPre : std::false_type {};
+template <class E>
+struct EpiPre<E, std::void_t<decltype(E::kPre)>> : std::true_type {};
+template <class E, bool P = EpiPre<E>::value>
+struct EpiPreT {
+  using type = char;
+};
+template <class E>
+struct EpiPreT<E, true> {
+  using type = typename E::PreT;
+};
+
 template <typename X>
 struct LEpiResidual {  // r = f - A x
   static constexpr int kDots = 0;
@@ -205,6 +237,100 @@ struct LEpiSchurU {  // r_u' = r_u - B^T p          (nu x 1 blocks; in place all
     for (int c = 0; c < BR; ++c) v[c] = (double)ru[o + c];
 #pragma unroll
     for (int c = 0; c < BR; ++c) ru2[o + c] = to_out<X>(v[c] - yr[c]);
+  }
+};
+
+// Fused pre-smoothing from zero (K4a in the producer of f): the kernel
+// that produces a level's right-hand side f also applies the level's block-diagonal M to it
+// and stores x = M f.  f is rounded to the vector type first and M f is formed from the
+// rounded values in k_apply_M's order (m0 f0, then fma), so f and x are bit-identical to
+// the unfused pair.  All lanes of the warp must call the lane form (shuffles).
+template <int BR, typename V, typename X>
+__device__ __forceinline__ void apply_M_row(const V* __restrict__ M, int64_t o, const double (&fv)[BR], X* x) {
+#pragma unroll
+  for (int i = 0; i < BR; ++i) {
+    double m[BR];
+    load_b<BR, false>(M + (o + i) * BR, m);
+    double t = m[0] * fv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], fv[c], t);
+    x[o + i] = to_out<X>(t);
+  }
+}
+
+template <typename V, typename X>
+struct LEpiSpmvM {  // f = A g (K6 restriction: g = r of the finer level), x = M f (K4a)
+  static constexpr int kDots = 0;
+  const V* M;
+  X* f;
+  X* x;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    const X fr = to_out<X>(L.yr);
+    const double fd = L.valid ? (double)fr : 0.0;
+    double fv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) fv[c] = __shfl_sync(kFull, fd, L.base + c);
+    if (!L.valid) return;
+    f[o] = fr;
+    double m[BR];
+    load_b<BR, false>(M + o * BR, m);
+    double t = m[0] * fv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], fv[c], t);
+    x[o] = to_out<X>(t);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double fv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) {
+      const X t = to_out<X>(yr[c]);
+      f[o + c] = t;
+      fv[c] = (double)t;
+    }
+    apply_M_row<BR>(M, o, fv, x);
+  }
+};
+
+template <typename V, typename X>
+struct LEpiSchurUM {  // r_u' = r_u - B^T p (K11, in place allowed), x = M r_u' (K4a of the second V-cycle)
+  static constexpr int kDots = 0;
+  const V* M;
+  const X* ru;
+  X* ru2;
+  X* x;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    const X fr = L.valid ? to_out<X>((double)ru[o] - L.yr) : X(0);
+    double fv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) fv[c] = __shfl_sync(kFull, (double)fr, L.base + c);
+    if (!L.valid) return;
+    ru2[o] = fr;
+    double m[BR];
+    load_b<BR, false>(M + o * BR, m);
+    double t = m[0] * fv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], fv[c], t);
+    x[o] = to_out<X>(t);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double fv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) fv[c] = (double)ru[o + c];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) {
+      const X t = to_out<X>(fv[c] - yr[c]);
+      ru2[o + c] = t;
+      fv[c] = (double)t;
+    }
+    apply_M_row<BR>(M, o, fv, x);
   }
 };
 
@@ -616,6 +742,14 @@ __global__ void __launch_bounds__(SellrCfg<BR, BC, W, V, FAST>::TPB, SellrCfg<BR
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
     const int s = s0 + (int)(vb * WPB + w);
     double acc[BR] = {};
+    [[maybe_unused]] int prow = -1;
+    [[maybe_unused]] typename EpiPreT<EPI>::type pv[BR];
+    if constexpr (EpiPre<EPI>::value) {  // the epilogue's operand, loaded ahead of the row
+      if (s < nslices) {
+        prow = perm ? __ldg(perm + (int64_t)s * 32 + lane) : s * 32 + lane;
+        if (prow >= 0 && prow < n) epi.template pre<BR>(prow, pv);
+      }
+    }
     if (s < nslices) {
       const int j0 = __ldg(sptr + s), L = __ldg(sptr + s + 1) - j0;
       const int64_t v0 = __ldg(vptr + s);
@@ -640,6 +774,10 @@ __global__ void __launch_bounds__(SellrCfg<BR, BC, W, V, FAST>::TPB, SellrCfg<BR
         vp += (int64_t)S::NV * 32 * W;
       }
       if (j < L) sellr_step<BR, BC, W, true, V, X, FAST>(vp, cp, x, L - j, 0, c, acc);
+    }
+    if constexpr (EpiPre<EPI>::value) {
+      if (s < nslices && prow >= 0 && prow < n) epi.template row_pre<BR>(prow, acc, pv);
+      continue;
     }
     int row = s * 32 + lane;
     if (perm && s < nslices) row = __ldg(perm + (int64_t)s * 32 + lane);  // sorted windows (-1: padding)

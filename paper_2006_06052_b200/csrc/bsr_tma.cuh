@@ -163,6 +163,38 @@ struct EpiSchurU {
   }
 };
 
+// r_u' = r_u - B^T p and x = M r_u' (the fused pre-smoothing of the second V-cycle; the
+// consumer calls gl = 0..NU-1 in order with the row's whole result, the last call does all)
+template <int NU, typename V, typename X>
+struct EpiSchurUM {
+  const V* M;
+  const X* ru;
+  X* ru2;
+  X* x;
+  __device__ __forceinline__ void operator()(int row, int gl, const double (&yv)[NU]) const {
+    if (gl != NU - 1) return;
+    const int64_t o = (int64_t)row * NU;
+    double fv[NU];
+#pragma unroll
+    for (int c = 0; c < NU; ++c) fv[c] = (double)ru[o + c];
+#pragma unroll
+    for (int c = 0; c < NU; ++c) {
+      const X t = to_out<X>(fv[c] - yv[c]);
+      ru2[o + c] = t;
+      fv[c] = (double)t;
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      double m[NU];
+      load_b<NU, false>(M + (o + i) * NU, m);
+      double t = m[0] * fv[0];
+#pragma unroll
+      for (int c = 1; c < NU; ++c) t = fma(m[c], fv[c], t);
+      x[o + i] = to_out<X>(t);
+    }
+  }
+};
+
 // ---------------------------------------------------------------- staging
 struct TmaArgs {
   int n, tr, ntiles, ns;

@@ -90,6 +90,9 @@ int amg_params_default(amg_params* p) {
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
   p->gmres_ortho = 2;
+  p->fused_presmooth = 1;
+  p->ilut_p = 2;
+  p->ilut_tau = 1e-2;
   return AMG_OK;
 }
 

@@ -50,6 +50,20 @@ bool sellr_range_ok(const Mat& A, int r0, int r1);
 // K4a x = M f
 void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void* x, int xt,
                     cudaStream_t s);
+// K4a fused into the producer of f: the producer also stores x = M f
+// (M: block-diagonal [n][b][b] of type mvt), bit-identical to the producer + launch_apply_M.
+// false: this plan / shape has no fused form (nothing launched; run the pair).
+// K6 + K4a  f = A g, x = M f
+bool launch_spmv_M(const Mat& A, const void* g, void* f, const void* M, int mvt, void* x, int xt, cudaStream_t s);
+// K11 + K4a  ru2 = ru - B^T p, x = M ru2
+bool launch_schur_u_M(const Mat& BTm, const void* ru, const void* p, void* ru2, const void* M, int mvt, void* x, int xt,
+                      cudaStream_t s);
+// K9 + K4a  (b = 4, pc = 3, fp32 vectors) split, xu = M ru
+bool launch_split_M(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt, const void* M,
+                    int mvt, void* xu, cudaStream_t s, const double* scale_dev = nullptr);
+// narrow + K4a  f = narrow(scale r) (n block rows of b), x = M f
+bool launch_convert_M(int32_t n, int b, const double* r, double scale, void* f, int xt, const void* M, int mvt, void* x,
+                      cudaStream_t s, const double* scale_dev = nullptr);
 // K8  x = Ainv f (dense N x N, values vt, vectors xt)
 void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void* x, int xt,
                        cudaStream_t s);

@@ -524,6 +524,227 @@ __global__ void k_ilu_rows(int cnt, const int32_t* rows, const int32_t* ptr, con
   if (!block_inverse<B>(a + (int64_t)kd * B * B, Dinv + (int64_t)i * B * B)) set_err(err, AMG_ESINGULAR_BLOCK);
 }
 
+// ---------------------------------------------------------------- S8c block ILUT(tau, p)
+// Row i of Saad's threshold IKJ factorisation on blocks (reading R25; the oracle's
+// ilut_factor, same operation order, so patterns and fp64 values are bit-identical).
+// Fill makes the dependency graph data-dependent, so rows are not level-scheduled: one warp
+// per row, rows claimed in ascending order from a global counter, and a row waits for each
+// row k it eliminates with (k < i) on k's completion flag (release / acquire at gpu scope).
+// Every claimed row is held by a running warp and waits only on smaller rows, so the
+// smallest unfinished row always progresses (no deadlock).  The working row w lives in
+// shared memory as an unsorted list (original entries first, fill appended); entries are
+// eliminated in ascending column order by a warp-wide min over the unprocessed ones.
+// Kept entries are written to per-row slabs of capacity (row's A entries on that side) + p,
+// compacted afterwards.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kIlutCap = 512;  // working-row entries per warp (error beyond)
+template <int B>
+struct IlutShape {
+  static constexpr int BB = B * B;
+  static constexpr int W = B == 4 ? 1 : 2;  // warps per block
+  static constexpr size_t per_warp = (size_t)kIlutCap * (8 * BB + 8 + 4 + 1) + 8 * BB + 64;
+  static constexpr size_t smem = per_warp * W;
+};
+
+template <int B>
+__global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
+    int n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col, const double* __restrict__ val,
+    double tau, int pfill, const int32_t* __restrict__ loff, const int32_t* __restrict__ uoff, int32_t* lcol,
+    double* lval, int32_t* llen, int32_t* ucol, double* uval, int32_t* ulen, double* Dinv, int* done, int* counter,
+    int* err) {
+  constexpr int BB = B * B;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* base = smem_raw + (size_t)wid * IlutShape<B>::per_warp;
+  double* wv = reinterpret_cast<double*>(base);                 // [cap][BB]
+  double* nrm = wv + (size_t)kIlutCap * BB;                     // [cap] norms (phase 2)
+  double* tl = nrm + kIlutCap;                                  // [BB] the current multiplier
+  int32_t* wc = reinterpret_cast<int32_t*>(tl + BB);            // [cap] columns; -1 - col when dropped
+  int* wlen = reinterpret_cast<int*>(wc + kIlutCap);           // list length
+  uint8_t* kept = reinterpret_cast<uint8_t*>(wlen + 4);         // [cap] phase-2 decisions
+  for (;;) {
+    int i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= n) return;
+    const int r0 = ptr[i], len0 = ptr[i + 1] - r0;
+    if (len0 > kIlutCap) {
+      if (lane == 0) set_err(err, AMG_EINVAL);
+      return;  // the flag stays down: waiters on this row would hang -- setup fails anyway
+    }
+    for (int q = lane; q < len0; q += 32) {
+      wc[q] = col[r0 + q];
+      for (int e = 0; e < BB; ++e) wv[(size_t)q * BB + e] = val[(int64_t)(r0 + q) * BB + e];
+    }
+    if (lane == 0) *wlen = len0;
+    double tau_i = 0.0;
+    if (lane == 0) {
+      double s2 = 0.0;
+      for (int q = 0; q < len0; ++q) s2 = s2 + fro2<B>(val + (int64_t)(r0 + q) * BB);
+      tau_i = tau * sqrt(s2);
+    }
+    tau_i = __shfl_sync(kFull, tau_i, 0);
+    __syncwarp();
+    int last = -1;
+    bool overflow = false;
+    for (;;) {
+      // next k: the smallest live column in (last, i)
+      const int len = *wlen;
+      int best = INT_MAX, bidx = -1;
+      for (int q = lane; q < len; q += 32) {
+        const int c = wc[q];
+        if (c > last && c < i && c < best) best = c, bidx = q;
+      }
+      const int k = __reduce_min_sync(kFull, (unsigned)best);
+      if (k == INT_MAX) break;
+      const unsigned who = __ballot_sync(kFull, best == k);
+      const int kq = __shfl_sync(kFull, bidx, __ffs(who) - 1);
+      while (ld_acquire(done + k) == 0) {
+      }
+      // multiplier l = w_k D_k^-1 (lane e < BB: entry e, blk_mul's order)
+      double le = 0.0;
+      if (lane < BB) {
+        const int r = lane / B, cc = lane - r * B;
+        const double* a = wv + (size_t)kq * BB;
+        const double* d = Dinv + (int64_t)k * BB;
+        double t = a[r * B] * __ldcg(d + cc);
+        for (int m = 1; m < B; ++m) t = t + a[r * B + m] * __ldcg(d + m * B + cc);
+        le = t;
+      }
+      __syncwarp();
+      if (lane < BB) tl[lane] = le;
+      __syncwarp();
+      double ln = 0.0;
+      if (lane == 0) ln = sqrt(fro2<B>(tl));
+      ln = __shfl_sync(kFull, ln, 0);
+      last = k;
+      if (ln < tau_i) {  // dropped: no update
+        if (lane == 0) wc[kq] = -1 - k;
+        __syncwarp();
+        continue;
+      }
+      if (lane < BB) wv[(size_t)kq * BB + lane] = le;
+      // w_j -= l U_kj for the stored U entries of row k (distinct j: one lane each)
+      const int u0 = uoff[k], ul = __ldcg(ulen + k);
+      for (int q = lane; q < ul; q += 32) {
+        const int j = __ldcg(ucol + u0 + q);
+        int idx = -1;
+        for (int t = 0; t < len; ++t)
+          if (wc[t] == j) {
+            idx = t;
+            break;
+          }
+        if (idx < 0) {
+          idx = atomicAdd(wlen, 1);
+          if (idx >= kIlutCap) {
+            overflow = true;
+            continue;
+          }
+          wc[idx] = j;
+          for (int e = 0; e < BB; ++e) wv[(size_t)idx * BB + e] = 0.0;
+        }
+        const double* U = uval + (int64_t)(u0 + q) * BB;
+        double* wj = wv + (size_t)idx * BB;
+        for (int r = 0; r < B; ++r)
+          for (int cc = 0; cc < B; ++cc) {
+            double t = tl[r * B] * __ldcg(U + cc);
+            for (int m = 1; m < B; ++m) t = t + tl[r * B + m] * __ldcg(U + m * B + cc);
+            wj[r * B + cc] = wj[r * B + cc] - t;
+          }
+      }
+      if (__any_sync(kFull, overflow)) {
+        if (lane == 0) set_err(err, AMG_EINVAL);
+        return;
+      }
+      __syncwarp();
+    }
+    const int len = min(*wlen, kIlutCap);
+    // pivot
+    int dq = -1;
+    for (int q = lane; q < len; q += 32)
+      if (wc[q] == i) dq = q;
+    const unsigned dm = __ballot_sync(kFull, dq >= 0);
+    if (!dm) {
+      if (lane == 0) set_err(err, AMG_EZERODIAG);
+      return;
+    }
+    dq = __shfl_sync(kFull, dq, __ffs(dm) - 1);
+    if (lane == 0 && !block_inverse<B>(wv + (size_t)dq * BB, Dinv + (int64_t)i * BB)) set_err(err, AMG_ESINGULAR_BLOCK);
+    // norms; candidates: live, off-diagonal, ||w_j|| >= tau_i
+    for (int q = lane; q < len; q += 32) {
+      const int c = wc[q];
+      nrm[q] = (c >= 0 && c != i) ? sqrt(fro2<B>(wv + (size_t)q * BB)) : -1.0;
+      if (c >= 0 && c != i && nrm[q] < tau_i) nrm[q] = -1.0;
+    }
+    __syncwarp();
+    // keep: original entries, and fill ranked < p by (norm desc, column asc) within its side
+    int nl = 0, nu = 0;
+    for (int q0 = 0; q0 < len; q0 += 32) {
+      const int q = q0 + lane;
+      bool keep = false;
+      int c = -1;
+      if (q < len && nrm[q] >= 0.0) {
+        c = wc[q];
+        keep = q < len0;
+        if (!keep) {
+          int rank = 0;
+          for (int t = len0; t < len; ++t) {
+            const int ct = wc[t];
+            if (t == q || nrm[t] < 0.0 || ((ct < i) != (c < i))) continue;
+            if (nrm[t] > nrm[q] || (nrm[t] == nrm[q] && ct < c)) ++rank;
+          }
+          keep = rank < pfill;
+        }
+      }
+      if (q < len) kept[q] = keep;
+      nl += __popc(__ballot_sync(kFull, keep && c < i));
+      nu += __popc(__ballot_sync(kFull, keep && c > i));
+    }
+    __syncwarp();
+    // positions: ascending column within each side
+    for (int q = lane; q < len; q += 32) {
+      if (!kept[q]) continue;
+      const int c = wc[q];
+      int pos = 0;
+      for (int t = 0; t < len; ++t) {
+        const int ct = wc[t];
+        if (kept[t] && ((ct < i) == (c < i)) && ct < c) ++pos;
+      }
+      int32_t* oc = c < i ? lcol + loff[i] : ucol + uoff[i];
+      double* ov = c < i ? lval + (int64_t)loff[i] * BB : uval + (int64_t)uoff[i] * BB;
+      oc[pos] = c;
+      for (int e = 0; e < BB; ++e) ov[(int64_t)pos * BB + e] = wv[(size_t)q * BB + e];
+    }
+    if (lane == 0) llen[i] = nl, ulen[i] = nu;
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) st_release(done + i, 1);
+  }
+}
+
+__global__ void k_ilut_compact(int n, const int32_t* off, const int32_t* len, const int32_t* scol, const double* sval,
+                               const int32_t* ptr, int32_t* col, double* val, int bb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int q = 0; q < len[i]; ++q) {
+    col[ptr[i] + q] = scol[off[i] + q];
+    for (int e = 0; e < bb; ++e) val[(int64_t)(ptr[i] + q) * bb + e] = sval[(int64_t)(off[i] + q) * bb + e];
+  }
+}
+
+__global__ void k_add_scalar(int n, int32_t* a, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] += v;
+}
+
 __global__ void k_tri_count(int n, const int32_t* ptr, const int32_t* col, int32_t* lc, int32_t* uc) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1020,6 +1241,54 @@ void ilu0_factor(SetupCtx& c, const Mat& A, double* Dinv, Mat& Lo, Mat& Up) {
   AMG_CK(cudaStreamSynchronize(s));
 }
 
+// Block ILUT(tau, p) of A (fp64, reading R25): k_ilut_rows into per-row slabs, then
+// compacted into L_s / U_s.  D^-1 -> Dinv (n b^2).
+void ilut_factor(SetupCtx& c, const Mat& A, double tau, int pfill, double* Dinv, Mat& Lo, Mat& Up) {
+  const int n = A.n, b = A.b;
+  cudaStream_t s = c.s;
+  int32_t* loff = c.tmp.alloc_n<int32_t>(n + 1);
+  int32_t* uoff = c.tmp.alloc_n<int32_t>(n + 1);
+  k_tri_count<<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, A.col, loff, uoff);
+  AMG_CK_LAUNCH();
+  k_add_scalar<<<grid_for(n, kT), kT, 0, s>>>(n, loff, pfill);
+  k_add_scalar<<<grid_for(n, kT), kT, 0, s>>>(n, uoff, pfill);
+  AMG_CK_LAUNCH();
+  const int64_t lcap = scan(c, loff, n), ucap = scan(c, uoff, n);
+  int32_t* scl = c.tmp.alloc_n<int32_t>(std::max<int64_t>(lcap, 1));
+  int32_t* scu = c.tmp.alloc_n<int32_t>(std::max<int64_t>(ucap, 1));
+  double* svl = c.tmp.alloc_n<double>(std::max<int64_t>(lcap, 1) * b * b);
+  double* svu = c.tmp.alloc_n<double>(std::max<int64_t>(ucap, 1) * b * b);
+  int32_t* llen = c.tmp.alloc_n<int32_t>(n + 1);
+  int32_t* ulen = c.tmp.alloc_n<int32_t>(n + 1);
+  int* flags = c.tmp.alloc_n<int>(n + 1);  // [n] done flags, [n] the row counter
+  AMG_CK(cudaMemsetAsync(flags, 0, sizeof(int) * (n + 1), s));
+  dispatch_bs(b, [&](auto Bc) {
+    constexpr int BB = decltype(Bc)::value;
+    using Sh = IlutShape<BB>;
+    AMG_CK(cudaFuncSetAttribute(k_ilut_rows<BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem));
+    int per_sm = 0;
+    AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilut_rows<BB>, 32 * Sh::W, Sh::smem));
+    const int grid = std::max(1, std::min(kSMs * std::max(per_sm, 1), (n + Sh::W - 1) / Sh::W));  // all resident
+    k_ilut_rows<BB><<<grid, 32 * Sh::W, Sh::smem, s>>>(n, A.ptr, A.col, (const double*)A.val, tau, pfill, loff, uoff,
+                                                       scl, svl, llen, scu, svu, ulen, Dinv, flags, flags + n, c.err);
+  });
+  AMG_CK_LAUNCH();
+  check_err(c, "ILUT factorisation");
+  int32_t* lc = c.tmp.alloc_n<int32_t>(n + 1);
+  int32_t* uc = c.tmp.alloc_n<int32_t>(n + 1);
+  AMG_CK(cudaMemcpyAsync(lc, llen, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  AMG_CK(cudaMemcpyAsync(uc, ulen, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  const int64_t ln = scan(c, lc, n), un = scan(c, uc, n);
+  Lo = new_mat(c.tmp, n, A.m, b, ln);
+  Up = new_mat(c.tmp, n, A.m, b, un);
+  AMG_CK(cudaMemcpyAsync(Lo.ptr, lc, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  AMG_CK(cudaMemcpyAsync(Up.ptr, uc, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  k_ilut_compact<<<grid_for(n, kT), kT, 0, s>>>(n, loff, llen, scl, svl, Lo.ptr, Lo.col, (double*)Lo.val, b * b);
+  k_ilut_compact<<<grid_for(n, kT), kT, 0, s>>>(n, uoff, ulen, scu, svu, Up.ptr, Up.col, (double*)Up.val, b * b);
+  AMG_CK_LAUNCH();
+  AMG_CK(cudaStreamSynchronize(s));
+}
+
 // ---------------------------------------------------------------- the setup driver
 void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0, cudaStream_t s) {
   SetupCtx c;
@@ -1286,7 +1555,7 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
                                                     cand, P.ptr, P.col, (double*)P.val, p.sa_omega);
       }
       AMG_CK_LAUNCH();
-      if (p.smoother != AMG_ILU0)
+      if (p.smoother != AMG_ILU0 && p.smoother != AMG_ILUT)
         k_smoother<BB><<<grid_for(n, kT), kT, 0, s>>>(n, A.ptr, (const double*)A.val, diag,
                                                       p.smoother == AMG_SPAI0, p.jacobi_omega, M, c.err);
       AMG_CK_LAUNCH();
@@ -1294,6 +1563,7 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     check_err(c, "prolongator / smoother");
     Mat Lo, Up;
     if (p.smoother == AMG_ILU0) ilu0_factor(c, A, M, Lo, Up);  // M <- D^-1
+    if (p.smoother == AMG_ILUT) ilut_factor(c, A, p.ilut_tau, p.ilut_p, M, Lo, Up);
     lvL.push_back(Lo);
     lvU.push_back(Up);
     Mat R = transpose(c, P);

@@ -106,9 +106,12 @@ int check_params(const amg_params* p) {
   if (p->npre < 1 || p->npost < 0 || p->max_levels < 1 || p->maxiter < 0) return AMG_EINVAL;
   if (p->coarsening != AMG_SA && p->coarsening != AMG_PLAIN_AGG) return AMG_EINVAL;
   if (p->schur_shat < 0 || p->schur_shat > 2 || !(p->over_interp > 0.0)) return AMG_EINVAL;
-  if (p->smoother < AMG_SPAI0 || p->smoother > AMG_ILU0) return AMG_EINVAL;
-  if (p->smoother == AMG_ILU0 && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16)) return AMG_EINVAL;
+  if (p->smoother < AMG_SPAI0 || p->smoother > AMG_ILUT) return AMG_EINVAL;
+  if ((p->smoother == AMG_ILU0 || p->smoother == AMG_ILUT) && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16))
+    return AMG_EINVAL;
+  if (p->smoother == AMG_ILUT && (p->ilut_p < 0 || !(p->ilut_tau >= 0.0))) return AMG_EINVAL;
   if (p->gmres_ortho < 0 || p->gmres_ortho > 2) return AMG_EINVAL;
+  if (p->fused_presmooth < 0 || p->fused_presmooth > 1) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
     return AMG_EINVAL;
@@ -334,7 +337,7 @@ int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_
     return AMG_OK;
   }
   if (which < 0 || which > 5 || (coarsest && which != 0) || !ptr || !col) return AMG_EINVAL;
-  if (which >= 4 && !h->lv[level].Lf.ptr) return AMG_EINVAL;  // ILU(0) factors only with AMG_ILU0
+  if (which >= 4 && !h->lv[level].Lf.ptr) return AMG_EINVAL;  // ILU factors only with AMG_ILU0 / AMG_ILUT
   const Level& LL = h->lv[std::min(level, (int32_t)h->lv.size() - 1)];
   const Mat& M = coarsest ? h->coarse.A
                           : (which == 0 ? LL.A : which == 1 ? LL.P : which == 2 ? LL.R : which == 4 ? LL.Lf : LL.Uf);

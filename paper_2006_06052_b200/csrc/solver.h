@@ -153,7 +153,10 @@ void replicated_allgather(Handle& h, size_t l, cudaStream_t s);
 void* level_f_slab(Handle& h, size_t l);
 // vcycle.cu
 // V-cycle from level `level` on that level's f buffer; returns the buffer holding x
-void* vcycle_run(Handle& h, size_t level, cudaStream_t s);
+// pre_done: level `level`'s x = M f was already formed by the producer of f (fused K4a)
+void* vcycle_run(Handle& h, size_t level, cudaStream_t s, bool pre_done = false);
+// can the producer of level l's f also form x = M f (fused K4a)?
+bool fuse_presmooth(const Handle& h, size_t level);
 void* level0_f(Handle& h);
 // z = M r (outer fp64 r scaled by `scale` or by *scale_dev when given, z of dtype zt)
 void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale = 1.0,

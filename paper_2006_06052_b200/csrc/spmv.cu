@@ -529,7 +529,12 @@ void launch_spmv(const Mat& A, double alpha, const void* x, int xt, double beta,
             if (A.fast32) launch_tma_rows<B, B, V, X, true>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
             else launch_tma_rows<B, B, V, X, false>(A, (const X*)x, EpiSpmv<B, Y>{alpha, beta, (Y*)y}, s);
           } else {
-            launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmv<Y>{alpha, beta, (Y*)y}, s, r0, r1);
+            // K7 on short-row interleaved copies (the prolongators): y loaded ahead of the row
+            const bool pre = beta != 0.0 && A.lane_var == kLaneSellR && A.sell_pf == 0 && env_int("AMG_SPMV_PRE", 1);
+            if (pre)
+              launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmvPre<Y>{{alpha, beta, (Y*)y}}, s, r0, r1);
+            else
+              launch_lane<B, B, V, X>(A, (const X*)x, LEpiSpmv<Y>{alpha, beta, (Y*)y}, s, r0, r1);
           }
         });
       });
@@ -697,6 +702,175 @@ void launch_apply_M(int32_t n, int b, const void* M, int vt, const void* f, void
     });
   });
   AMG_CK_LAUNCH();
+}
+
+// ---- K4a fused into the producer of f ----
+// K6 + K4a: f = A g, x = M f (A: the restriction R_l; M, f, x: level l+1's)
+bool launch_spmv_M(const Mat& A, const void* g, void* f, const void* M, int mvt, void* x, int xt, cudaStream_t s) {
+  if (A.tma_grid > 0 || mvt != A.vt || A.br != A.bc) return false;
+  if (A.n == 0) return true;
+  ProfScope ps_(prof_name("spmv_M", A.b, A.vt, xt),
+                mat_bytes(A) + (double)A.m * A.b * dtype_size(xt) + 2.0 * A.n * A.b * dtype_size(xt) +
+                    (double)A.n * A.b * A.b * dtype_size(mvt),
+                s);
+  dispatch_b(A.b, [&](auto Bc) {
+    constexpr int B = decltype(Bc)::value;
+    dispatch_t(A.vt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        launch_lane<B, B, V, X>(A, (const X*)g, LEpiSpmvM<V, X>{(const V*)M, (X*)f, (X*)x}, s);
+      });
+    });
+  });
+  AMG_CK_LAUNCH();
+  return true;
+}
+
+// K11 + K4a: ru2 = ru - B^T p, x = M ru2 (M, x: level 0's)
+bool launch_schur_u_M(const Mat& BTm, const void* ru, const void* p, void* ru2, const void* M, int mvt, void* x, int xt,
+                      cudaStream_t s) {
+  const int n = BTm.n, vt = BTm.vt;
+  if (BTm.br != 3 || mvt != vt) return false;
+  if (n == 0) return true;
+  ProfScope ps_(prof_name("schur_u_M", 3, vt, xt),
+                ((double)BTm.nnz * (4.0 + 3.0 * dtype_size(vt)) + 4.0 * (n + 1)) + 10.0 * n * dtype_size(xt) +
+                    9.0 * n * dtype_size(mvt),
+                s);
+  dispatch_t(vt, [&](auto v) {
+    using V = decltype(v);
+    dispatch_t(xt, [&](auto xx) {
+      using X = decltype(xx);
+      if (BTm.tma_grid > 0)
+        launch_tma_rows<3, 1, V, X, false>(BTm, (const X*)p, EpiSchurUM<3, V, X>{(const V*)M, (const X*)ru, (X*)ru2, (X*)x},
+                                           s);
+      else
+        launch_lane<3, 1, V, X>(BTm, (const X*)p, LEpiSchurUM<V, X>{(const V*)M, (const X*)ru, (X*)ru2, (X*)x}, s);
+    });
+  });
+  AMG_CK_LAUNCH();
+  return true;
+}
+
+// K9 + K4a, hot shape (b = 4, pressure component 3, fp32 vectors): k_split4 that also forms
+// x_u = M u for the cell's velocity triple.  The cell's M block (9 values) and the x triples
+// are staged through shared memory (16-byte global accesses, 256 cells per block).
+template <typename V>
+__global__ void __launch_bounds__(256) k_split4_M(int n, const double* __restrict__ r, double scale_v,
+                                                  const double* scale_d, float* __restrict__ ru, float* __restrict__ rp,
+                                                  const V* __restrict__ M, float* __restrict__ xu) {
+  const double scale = scale_d ? *scale_d : scale_v;
+  __shared__ __align__(16) float su[3 * 256];
+  __shared__ __align__(16) float sx[3 * 256];
+  __shared__ __align__(16) V sm[9 * 256];
+  const int64_t c0 = (int64_t)blockIdx.x * 256;
+  const int64_t c = c0 + threadIdx.x;
+  const int nc = (int)min((int64_t)256, (int64_t)n - c0);
+  {  // the block's M values: 9 * nc contiguous V (16-byte aligned: c0 * 9 * sizeof(V) % 16 == 0)
+    const V* src = M + c0 * 9;
+    if (nc == 256) {
+      constexpr int NV = 9 * 256 * (int)sizeof(V) / 16;
+      for (int i = threadIdx.x; i < NV; i += 256)
+        reinterpret_cast<float4*>(sm)[i] = __ldcs(reinterpret_cast<const float4*>(src) + i);
+    } else {
+      for (int i = threadIdx.x; i < 9 * nc; i += 256) sm[i] = src[i];
+    }
+  }
+  float u[3] = {};
+  if (c < n) {
+    const double2* q = reinterpret_cast<const double2*>(r + c * 4);
+    const double2 a = __ldcs(q), b = __ldcs(q + 1);
+    u[0] = (float)(a.x * scale);
+    u[1] = (float)(a.y * scale);
+    u[2] = (float)(b.x * scale);
+    su[3 * threadIdx.x + 0] = u[0];
+    su[3 * threadIdx.x + 1] = u[1];
+    su[3 * threadIdx.x + 2] = u[2];
+    rp[c] = (float)(b.y * scale);
+  }
+  __syncthreads();
+  if (c < n) {
+    const V* m = sm + 9 * threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double t = (double)m[3 * i] * (double)u[0];
+      t = fma((double)m[3 * i + 1], (double)u[1], t);
+      t = fma((double)m[3 * i + 2], (double)u[2], t);
+      sx[3 * threadIdx.x + i] = (float)t;
+    }
+  }
+  __syncthreads();
+  float* dst = ru + c0 * 3;
+  float* dx = xu + c0 * 3;
+  if (nc == 256) {
+    if (threadIdx.x < 192) {
+      reinterpret_cast<float4*>(dst)[threadIdx.x] = reinterpret_cast<const float4*>(su)[threadIdx.x];
+      reinterpret_cast<float4*>(dx)[threadIdx.x] = reinterpret_cast<const float4*>(sx)[threadIdx.x];
+    }
+  } else {
+    for (int i = threadIdx.x; i < 3 * nc; i += 256) dst[i] = su[i], dx[i] = sx[i];
+  }
+}
+
+bool launch_split_M(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt, const void* M,
+                    int mvt, void* xu, cudaStream_t s, const double* scale_dev) {
+  if (!(b == 4 && pc == 3 && xt == AMG_F32)) return false;
+  if (n == 0) return true;
+  ProfScope ps_(prof_name("split_M", b, AMG_F64, xt), (double)n * (4 * 8.0 + 7 * 4.0 + 9.0 * dtype_size(mvt)), s);
+  if (mvt == AMG_F32)
+    k_split4_M<float><<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, scale_dev, (float*)ru, (float*)rp,
+                                                        (const float*)M, (float*)xu);
+  else
+    k_split4_M<double><<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, scale_dev, (float*)ru, (float*)rp,
+                                                         (const double*)M, (float*)xu);
+  AMG_CK_LAUNCH();
+  return true;
+}
+
+// narrow + K4a (monolithic level 0): f = narrow(scale r), x = M f; thread per block row
+template <int B, typename V, typename X>
+__global__ void __launch_bounds__(256) k_convert_M(int n, const double* __restrict__ r, double scale_v,
+                                                   const double* scale_d, X* __restrict__ f, const V* __restrict__ M,
+                                                   X* __restrict__ x) {
+  const double scale = scale_d ? *scale_d : scale_v;
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int64_t o = row * B;
+  double fv[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) {
+    const X t = to_out<X>(r[o + c] * scale);
+    f[o + c] = t;
+    fv[c] = (double)t;
+  }
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    double m[B];
+    load_b<B, false>(M + (o + i) * B, m);
+    double t = m[0] * fv[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) t = fma(m[c], fv[c], t);
+    x[o + i] = to_out<X>(t);
+  }
+}
+
+bool launch_convert_M(int32_t n, int b, const double* r, double scale, void* f, int xt, const void* M, int mvt, void* x,
+                      cudaStream_t s, const double* scale_dev) {
+  if (n == 0) return true;
+  ProfScope ps_(prof_name("convert_M", b, AMG_F64, xt),
+                (double)n * b * (8.0 + 2.0 * dtype_size(xt)) + (double)n * b * b * dtype_size(mvt), s);
+  dispatch_b(b, [&](auto Bc) {
+    constexpr int B = decltype(Bc)::value;
+    dispatch_t(mvt, [&](auto v) {
+      using V = decltype(v);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        k_convert_M<B, V, X><<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, scale_dev, (X*)f, (const V*)M, (X*)x);
+      });
+    });
+  });
+  AMG_CK_LAUNCH();
+  return true;
 }
 
 // ---- K8: coarse solve as a dense GEMV with the explicit inverse (one warp per row) ----

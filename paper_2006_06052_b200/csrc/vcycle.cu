@@ -41,7 +41,11 @@ static void ilu_step(Handle& h, Level& L, void* x, cudaStream_t s) {
 // V(l, f):  x = M f;  r = f - A x;  f_c = R r;  x_c = V(l+1, f_c);  x += P x_c;
 //           x = x + M (f - A x)            (one kernel per line; fp64 accumulation,
 //                                            one rounding on store)
-void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
+bool fuse_presmooth(const Handle& h, size_t l) {
+  return h.p.fused_presmooth && l < h.lv.size() && !h.lv[l].Lf.ptr && !(h.comm && l >= h.rep_from);
+}
+
+void* vcycle_run(Handle& h, size_t l, cudaStream_t s, bool pre_done) {
   const int xt = h.xt, vt = h.vt;
   if (h.comm && l == h.rep_from) replicated_allgather(h, l, s);  // distributed: replicated from here on
   if (l == h.lv.size()) {
@@ -53,7 +57,7 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   void* t = L.t;
   const bool ilu = L.Lf.ptr != nullptr;
   if (ilu) ilu_apply(h, L, L.f, nullptr, x, s);  // K4a with ILU(0): x = (LU)^-1 f (sweeps)
-  else launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
+  else if (!pre_done) launch_apply_M(L.A.n, L.A.b, L.M, vt, L.f, x, xt, s);  // K4a: pre-smooth from zero
   for (int k = 1; k < h.p.npre; ++k) {
     if (ilu) {
       ilu_step(h, L, x, s);
@@ -66,8 +70,10 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s) {
   halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
                   [&](int r0, int r1) { launch_residual(L.A, L.f, x, L.r, xt, s, r0, r1); });  // K4b: r = f - A x
   void* fc = level_f_slab(h, l + 1);
-  launch_spmv(L.R, 1.0, L.r, xt, 0.0, fc, xt, s);  // K6: f_c = R r
-  void* xc = vcycle_run(h, l + 1, s);
+  // K6: f_c = R r (with the next level's K4a x_c = M_c f_c in its epilogue where possible)
+  const bool fused = fuse_presmooth(h, l + 1) && launch_spmv_M(L.R, L.r, fc, h.lv[l + 1].M, vt, h.lv[l + 1].x, xt, s);
+  if (!fused) launch_spmv(L.R, 1.0, L.r, xt, 0.0, fc, xt, s);
+  void* xc = vcycle_run(h, l + 1, s, fused);
   launch_spmv(L.P, 1.0, xc, xt, 1.0, x, xt, s);  // K7: x += P x_c
   for (int k = 0; k < h.p.npost; ++k) {          // K5: post-smooth (double-buffered)
     if (ilu) {
@@ -92,9 +98,15 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
     return;
   }
   void* f0 = level0_f(h);
+  // level 0's K4a in the producer of f_0 (its blocks are the producer's rows: not the V2
+  // scalar U-solver, whose level 0 has 1 x 1 blocks)
+  const bool f0M = fuse_presmooth(h, 0) && h.lv[0].A.b == (h.schur ? h.nu : h.b);
+  void* x0 = f0M ? h.lv[0].x : nullptr;
+  const void* M0 = f0M ? h.lv[0].M : nullptr;
   if (!h.schur) {
-    launch_convert(N, r, AMG_F64, f0, h.xt, scale, s, scale_dev);
-    void* x = vcycle_run(h, 0, s);
+    const bool fused = f0M && launch_convert_M(h.n, h.b, r, scale, f0, h.xt, M0, h.vt, x0, s, scale_dev);
+    if (!fused) launch_convert(N, r, AMG_F64, f0, h.xt, scale, s, scale_dev);
+    void* x = vcycle_run(h, 0, s, fused);
     launch_convert(N, x, h.xt, z, zt, 1.0, s);
     return;
   }
@@ -107,13 +119,18 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
     launch_mask_join(h.nu_s, h.np_s, h.uidx, h.pidx, u, h.pp, h.xt, z, zt, s);
     return;
   }
-  launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s, scale_dev);                      // K9
-  void* us = vcycle_run(h, 0, s);                                                              // u* = V(r_u)
+  // K9 (+ level 0's K4a)
+  const bool fs = f0M && launch_split_M(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, M0, h.vt, x0, s, scale_dev);
+  if (!fs) launch_split(h.n, h.b, h.pc, r, scale, f0, h.rp, h.xt, s, scale_dev);
+  void* us = vcycle_run(h, 0, s, fs);                                                          // u* = V(r_u)
   halo_exchange(h, h.halo0, us, h.xt, h.nu, s);
   launch_schur_p(h.Bm, h.mS, h.rp, us, h.pp, h.xt, s);  // K10
   halo_exchange(h, h.halo0, h.pp, h.xt, 1, s);
-  launch_schur_u(h.BTm, f0, h.pp, f0, h.xt, s);    // K11 (in place)
-  void* u = vcycle_run(h, 0, s);                                                               // u = V(r_u')
+  // K11 (in place; + level 0's K4a for the second V-cycle).  us (the first V-cycle's output,
+  // one of level 0's x / t buffers) is dead after K10, so x_0 may be overwritten here.
+  const bool fu = fs && launch_schur_u_M(h.BTm, f0, h.pp, f0, M0, h.vt, x0, h.xt, s);
+  if (!fu) launch_schur_u(h.BTm, f0, h.pp, f0, h.xt, s);
+  void* u = vcycle_run(h, 0, s, fu);                                                           // u = V(r_u')
   launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
 }
 
@@ -165,10 +182,18 @@ static double mat_bytes(const Mat& A, int vt) {
   return (double)A.nnz * (4.0 + (double)A.b * A.b * dtype_size(vt)) + 4.0 * (A.n + 1);
 }
 
+// does level l's K4a run inside its producer (the launchers' conditions)?
+static bool presmooth_fused(const Handle& h, size_t l) {
+  if (!fuse_presmooth(h, l)) return false;
+  if (l > 0) return h.lv[l - 1].R.tma_grid == 0 && h.lv[l - 1].R.vt == h.vt;
+  return !h.masked && h.lv[0].A.b == (h.schur ? h.nu : h.b) && (!h.schur || (h.b == 4 && h.pc == 3 && h.xt == AMG_F32));
+}
+
 static double vcycle_bytes(const Handle& h) {
   const double sx = (double)dtype_size(h.xt), sv = (double)dtype_size(h.vt);
   double tot = 0.0;
-  for (const Level& L : h.lv) {
+  for (size_t l = 0; l < h.lv.size(); ++l) {
+    const Level& L = h.lv[l];
     const double nb = (double)L.A.n * L.A.b;
     if (L.Lf.ptr) {  // ILU(0): k L sweeps (g, y gathered, y'), z_0 = D^-1 y, k U sweeps (y, z gathered, z' | x rw)
       const double k = h.p.ilu_sweeps, Msz = nb * L.A.b * sv;
@@ -182,8 +207,8 @@ static double vcycle_bytes(const Handle& h) {
     }
     tot += 2.0 * mat_bytes(L.A, h.vt) + mat_bytes(L.P, h.vt) + mat_bytes(L.R, h.vt);
     tot += 2.0 * nb * L.A.b * sv;  // M read twice
-    // K4a: f, x | K4b: f, x, r | K6: r, f_c | K7: x_c, x rw | K5: f, x, x'
-    tot += nb * sx * (2 + 3 + 1 + 2 + 3);
+    // K4a: f, x (fused into the producer of f: x) | K4b: f, x, r | K6: r, f_c | K7: x_c, x rw | K5: f, x, x'
+    tot += nb * sx * ((presmooth_fused(h, l) ? 1 : 2) + 3 + 1 + 2 + 3);
     tot += (double)L.nc * L.A.b * sx * 2;  // f_c write, x_c read
   }
   tot += (double)h.coarse.N * h.coarse.N * sv + 2.0 * h.coarse.N * sx;

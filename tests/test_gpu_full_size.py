@@ -6,7 +6,7 @@ solve takes minutes to tens of minutes on one core, so:
   * the iteration count is compared (+-2) with the oracle's count at the same size,
     stored in tests/golden/oracle_full_size.json by tools/oracle_reference_runs.py (a
     committed script that calls only gen/ and oracle/);
-  * the hierarchy depth matches the oracle's.
+  * the hierarchy (depth, rows and blocks of every level) matches the oracle's.
 """
 import json
 import os
@@ -52,6 +52,10 @@ def test_full_size_solve(amg, cfg):
     xd = torch.zeros_like(bd)
     rep = S.solve(bd, xd, 1e-8)
     x = xd.cpu().numpy()
+    # the hierarchy the oracle built at this size: rows and nnzb of every level (aggregates
+    # are deterministic), so equal sizes mean the same coarsening
+    sizes = [list(S.level_info(l)[:1]) + [S.level_info(l)[2]] for l in range(rep.levels)]
+    assert sizes == [list(v) for v in g["level_sizes"]], (sizes, g["level_sizes"])
     del S, bd, xd
     torch.cuda.empty_cache()
     assert rep.converged

@@ -28,7 +28,7 @@ ORC_OF = {"solver": "solver", "gmres_m": "gmres_m", "precond": "precond", "maxit
           "coarse_enough": "coarse_enough", "npre": "npre", "npost": "npost", "max_levels": "max_levels",
           "jacobi_omega": "jacobi_omega", "idrs_s": "idrs_s", "idrs_seed": "idrs_seed",
           "schur_u_scalar": "schur_u_scalar", "coarsening": "coarsening", "schur_shat": "schur_shat",
-          "over_interp": "over_interp", "ilu_sweeps": "ilu_sweeps"}
+          "over_interp": "over_interp", "ilu_sweeps": "ilu_sweeps", "ilut_tau": "ilut_tau", "ilut_p": "ilut_p"}
 # gmres_ortho is deliberately NOT forwarded: the oracle always runs its default CGS2
 # (SURVEY.md C11), so every GPU GMRES case -- whatever orthogonalisation the GPU uses --
 # is checked against the plain reading (VERDICT r01 "What's weak" #2).
@@ -74,7 +74,7 @@ def check_hierarchy(S, O, hier32):
         M = S.level_export(l, 3)
         oM = O.level_M(l)
         assert np.array_equal(M, r32(oM) if hier32 else oM), f"smoother level {l}"
-        for which in (4, 5):  # ILU(0) factors (AMG_ILU0)
+        for which in (4, 5):  # ILU factors (AMG_ILU0 / AMG_ILUT)
             oF = O.level_mat(l, which)
             if oF is None:
                 continue
@@ -108,6 +108,13 @@ CASES = [
     ("ilu0-plain-agg-f64", gen.STOKES, 12, dict(precond=1, solver=3, smoother=2, coarsening=1, coarse_enough=40),
      False),
     ("ilu0-monolithic-4x4-16", gen.STOKES, 16, dict(precond=0, solver=1, smoother=2, ilu_sweeps=3), True),
+    # block ILUT(tau, p) (reading R25): the paper's U-solver smoother, Listing V2 = plain aggregation + ILUT
+    ("ilut-stokes-schur-16", gen.STOKES, 16, dict(precond=1, solver=3, smoother=3), True),
+    ("ilut-plain-agg-f64", gen.STOKES, 12, dict(precond=1, solver=3, smoother=3, coarsening=1, coarse_enough=40),
+     False),
+    ("ilut-p0-tau0-poisson-f64", gen.POISSON3, 10, dict(precond=0, solver=1, smoother=3, ilut_p=0, ilut_tau=0.0,
+                                                         coarse_enough=40), False),
+    ("ilut-monolithic-4x4-16", gen.STOKES, 16, dict(precond=0, solver=1, smoother=3, ilut_p=4, ilut_tau=1e-3), True),
 ]
 
 
@@ -213,6 +220,29 @@ def test_ilu0_random_matrices(amg, rng):
             check_hierarchy(S, O, h32)
 
 
+@pytest.mark.parametrize("tau,p", [(1e-2, 2), (0.0, 0), (0.05, 1), (0.0, 40), (1e-3, 6)])
+def test_ilut_random_matrices(amg, rng, tau, p):
+    # block ILUT factors (patterns and fp64 values) bit-exact with the oracle for b = 1..4
+    # (R25: the same elimination order, threshold and fill-ranking decisions in fp64)
+    for b in (1, 2, 3, 4):
+        ptr, col, val = random_bsr(rng, 300, b, density=0.015, dom=3 * b)
+        for h32 in (False, True):
+            A, S, O = make_pair(amg, ptr, col, val, hier32=h32, precond=0, solver=1, smoother=3, ilut_tau=tau,
+                                ilut_p=p, coarse_enough=20 * b)
+            check_hierarchy(S, O, h32)
+
+
+def test_ilut_stencil_levels(amg):
+    # every level of a 3x3 SA hierarchy (7-point stencil rows, then aggregated rows with 20-60
+    # blocks and their fill) factorised on the GPU equals the oracle's factorisation
+    ptr, col, val = gen.matrix(gen.POISSON3, 16)
+    for tau, p in ((1e-2, 2), (1e-4, 8)):
+        A, S, O = make_pair(amg, ptr, col, val, hier32=False, precond=0, solver=0, smoother=3, ilut_tau=tau, ilut_p=p,
+                            coarse_enough=100)
+        assert S.levels >= 3
+        check_hierarchy(S, O, False)
+
+
 def test_smoother_jacobi_and_omega(amg):
     ptr, col, val = gen.matrix(gen.POISSON3, 10)
     A, S, O = make_pair(amg, ptr, col, val, hier32=False, precond=0, smoother=1, sa_omega=0.5,
@@ -269,6 +299,13 @@ SOLVE_CASES = [
     ("ilu0-bicgstab-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, smoother=2), True),
     ("ilu0-sweeps3-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, smoother=2, ilu_sweeps=3),
      False),
+    # block ILUT (reading R25): Listing V2's U-solver (plain aggregation + ILUT) and SA + ILUT
+    ("ilut-idrs5-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=3, smoother=3), True),
+    ("ilut-plain-idrs5-cfg5-16", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(precond=1, solver=3, smoother=3,
+                                                                         coarsening=1), True),
+    ("ilut-gmres-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, smoother=3, ilut_p=3,
+                                                                  ilut_tau=3e-3), False),
+    ("ilut-bicgstab-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, smoother=3), True),
     # GPU orthogonalisation variants of flexible GMRES, each against the oracle's CGS2:
     # two-pass Gram/Cholesky (R22) and the GPU's CGS2 (every case above without gmres_ortho
     # runs the GPU default, R23: the fp32-shadow first pass)
@@ -653,3 +690,40 @@ def test_step_graph_bit_identical(amg, envvars, kind, n, rk, kw):
     (xg, ig, rg, ng), (xe, ie, re_, ne) = runs
     assert ig == ie and rg == re_ and np.array_equal(xg, xe)
     assert ng >= 1 and ne >= 1  # graphed: the step graph; host-driven: the preconditioner graphs
+
+
+@pytest.mark.parametrize("kind,n,kw,h32,env", [
+    (gen.STOKES, 16, dict(precond=1, solver=2), True, {}),                      # split4 + B^T (TMA) + R fused
+    (gen.STOKES, 24, dict(precond=1, solver=2), True, dict(AMG_NO_TMA_SCHUR=1)),  # B^T on the lane kernels
+    (gen.STOKES, 24, dict(precond=1, solver=2), True, dict(AMG_SELLR_MIN_SLICES=1)),  # interleaved R copies
+    (gen.STOKES, 24, dict(precond=1, solver=2), True, dict(AMG_SELL_MIN_SLICES=1, AMG_SELLR=0)),  # sliced copies
+    (gen.STOKES, 10, dict(precond=1, solver=2, coarse_enough=40), False, {}),   # fp64: generic split, R fused
+    (gen.STOKES, 16, dict(precond=0, solver=1), True, {}),                      # monolithic 4x4: convert_M
+    (gen.POISSON3, 12, dict(precond=0, solver=0, coarse_enough=40), False, {}),  # monolithic 3x3 fp64
+    (gen.STOKES, 16, dict(precond=1, solver=3, schur_u_scalar=1, coarse_enough=300), True, {}),  # V2 (b = 1)
+], ids=["schur-f32", "schur-lane-BT", "schur-sellr", "schur-sell", "schur-f64", "mono-4x4", "mono-3x3-f64", "v2"])
+def test_fused_presmooth_bit_identical(amg, envvars, rng, kind, n, kw, h32, env):
+    # x = M f formed in the epilogue of the kernel producing f (split,
+    # B^T update, restriction, narrowing) -- the same preconditioner output and the same solve
+    # bit for bit as the separate K4a pass, with fewer kernels per application
+    envvars(**env)
+    ptr, col, val = gen.matrix(kind, n)
+    N = (len(ptr) - 1) * val.shape[-1]
+    r = torch.as_tensor(rng.standard_normal(N), device="cuda")
+    bvec = gen.rhs(gen.RHS_LID_NOISE if kind == gen.STOKES else gen.RHS_UNIFORM, n, val.shape[-1])
+    out = []
+    for fused in (1, 0):
+        A = amg.BSR.from_numpy(ptr, col, val)
+        dt = amg.F32 if h32 else amg.F64
+        S = amg.Solver(A, amg.default_params(hier_dtype=dt, vcycle_vec_dtype=dt, fused_presmooth=fused, **kw))
+        z = torch.zeros(N, dtype=torch.float64, device="cuda")
+        k0 = amg.kernel_launches()
+        S.apply_precond(r, z)
+        torch.cuda.synchronize()
+        k = amg.kernel_launches() - k0
+        x, rep = _solve(amg, S, bvec)
+        out.append((z.cpu().numpy(), k, x, rep.iters))
+    (z1, k1, x1, i1), (z0, k0_, x0, i0) = out
+    assert np.array_equal(z1, z0)
+    assert np.array_equal(x1, x0) and i1 == i0
+    assert k1 < k0_, (k1, k0_)
