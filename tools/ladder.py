@@ -34,6 +34,9 @@ EXTRA = {
     "V4-ilu0": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, smoother=amg.ILU0),
     "V4-plain-ilu0": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, coarsening=amg.PLAIN_AGG, smoother=amg.ILU0),
     "V4-shat-full": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, schur_shat=2),
+    # block ILUT(1e-2, 2) (R25): the paper's U-solver smoother; plain aggregation + ILUT = Listings V2-V4
+    "V4-ilut": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, smoother=amg.ILUT),
+    "V4-plain-ilut": dict(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, coarsening=amg.PLAIN_AGG, smoother=amg.ILUT),
 }
 SOLVERS = {"idrs5": amg.IDRS, "gmres30": amg.GMRES}
 
