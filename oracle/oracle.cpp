@@ -786,6 +786,26 @@ static void coarse_solve(const Coarse& C, const double* f, double* x, bool rf) {
   for (int32_t i = 0; i < N; ++i) x[i] = rf ? f32r(y[i]) : y[i];
 }
 
+// A with the blocks coupling different slabs removed (bd: slab bounds over block rows)
+static orc_mat slab_diagonal_blocks(const orc_mat& A, const vector<int32_t>& bd) {
+  vector<int32_t> part = part_of_rows(A.n, bd);
+  orc_mat F;
+  F.n = A.n;
+  F.m = A.m;
+  F.b = A.b;
+  F.ptr.assign(A.n + 1, 0);
+  const int bb = A.b * A.b;
+  for (int32_t i = 0; i < A.n; ++i) {
+    for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+      if (part[A.col[k]] == part[i]) {
+        F.col.push_back(A.col[k]);
+        F.val.insert(F.val.end(), A.blk(k), A.blk(k) + bb);
+      }
+    F.ptr[i + 1] = (int32_t)F.col.size();
+  }
+  return F;
+}
+
 // C7: repeat C2-C6 while n_l * b > coarse_enough and l < max_levels - 1;
 // stop if n_c == 0 or n_c >= n_l.  Coarsest: dense LU.
 static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
@@ -807,10 +827,14 @@ static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
       rc = smoothed_prolongator(A, adj, L.agg, L.nc, p.sa_omega, L.P);
     if (rc != ORC_OK) return rc;
     L.R = transpose(L.P);
-    if (p.smoother == ORC_ILU0)
-      rc = ilu0_factor(A, L.L, L.U, L.M);
-    else if (p.smoother == ORC_ILUT)
-      rc = ilut_factor(A, p.ilut_tau, p.ilut_p, L.L, L.U, L.M);
+    if (p.smoother == ORC_ILU0 || p.smoother == ORC_ILUT) {
+      // multi-rank (reading R26): each slab's factors are those of its diagonal block --
+      // the couplings between slabs are left out of the factorisation (block Jacobi across
+      // ranks, the usual parallel ILU); the level's residuals still use the whole A
+      const orc_mat Af = bd.size() > 2 ? slab_diagonal_blocks(A, bd) : orc_mat();
+      const orc_mat& F = bd.size() > 2 ? Af : A;
+      rc = p.smoother == ORC_ILU0 ? ilu0_factor(F, L.L, L.U, L.M) : ilut_factor(F, p.ilut_tau, p.ilut_p, L.L, L.U, L.M);
+    }
     else
       rc = smoother_blocks(A, p.smoother, p.jacobi_omega, L.M);
     if (rc != ORC_OK) return rc;

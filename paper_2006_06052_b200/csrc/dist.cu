@@ -414,6 +414,15 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       if (!rep) remap_shift(LL.R, bd[me], bd[me + 1] - bd[me]);
       LL.R.fast32 = GL.R.fast32;
       make_tma_plan(LL.R, s, &h->arena);
+      if (GL.Lf.ptr) {  // ILU(0) / ILUT: the slab's rows of the slab-local factors (R26)
+        for (auto [F, GF] : {std::pair<Mat*, const Mat*>{&LL.Lf, &GL.Lf}, {&LL.Uf, &GL.Uf}}) {
+          *F = slice_rows(h->arena, *GF, r0, r1, s);
+          if (!rep) remap_shift(*F, bd[me], bd[me + 1] - bd[me]);
+          F->fast32 = GF->fast32;
+          make_tma_plan(*F, s, &h->arena);
+        }
+        for (void*& w : LL.w) w = h->arena.alloc(std::max<int64_t>((r1 - r0) * LL.A.b, 1) * xs);
+      }
       const int bb = LL.A.b;
       const int64_t nl = LL.A.n;
       LL.M = h->arena.alloc(std::max<int64_t>(nl * bb * bb, 1) * dtype_size(h->vt));
@@ -535,7 +544,6 @@ int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_b
   if (rc != AMG_OK) return rc;
   if (A_local->n_block_cols != n_global_block_rows || row_begin < 0) return AMG_EDIM;
   if (p->precond == AMG_PC_SCHUR && p->schur_u_scalar) return AMG_EINVAL;  // single-device only (R18)
-  if (p->smoother == AMG_ILU0 || p->smoother == AMG_ILUT) return AMG_EINVAL;  // single-device only (R20)
   Handle* h = setup_dist_impl(A_local, row_begin, n_global_block_rows, c->c, p, (cudaStream_t)stream);
   *out = reinterpret_cast<amg_handle*>(h);
   return AMG_OK;

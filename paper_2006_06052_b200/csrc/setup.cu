@@ -1241,6 +1241,40 @@ void ilu0_factor(SetupCtx& c, const Mat& A, double* Dinv, Mat& Lo, Mat& Up) {
   AMG_CK(cudaStreamSynchronize(s));
 }
 
+// A without the blocks that couple different slabs (part: slab of every block row)
+__global__ void k_slab_count(int n, const int32_t* ptr, const int32_t* col, const int32_t* part, int32_t* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) c += part[col[k]] == part[i];
+  cnt[i] = c;
+}
+__global__ void k_slab_fill(int n, const int32_t* ptr, const int32_t* col, const double* val, const int32_t* part,
+                            int bb, const int32_t* optr, int32_t* ocol, double* oval) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o = optr[i];
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    if (part[col[k]] != part[i]) continue;
+    ocol[o] = col[k];
+    for (int e = 0; e < bb; ++e) oval[(int64_t)o * bb + e] = val[(int64_t)k * bb + e];
+    ++o;
+  }
+}
+Mat slab_diagonal_blocks(SetupCtx& c, const Mat& A, const int32_t* part) {
+  const int n = A.n;
+  int32_t* cnt = c.tmp.alloc_n<int32_t>(n + 1);
+  k_slab_count<<<grid_for(n, kT), kT, 0, c.s>>>(n, A.ptr, A.col, part, cnt);
+  AMG_CK_LAUNCH();
+  const int64_t nnz = scan(c, cnt, n);
+  Mat F = new_mat(c.tmp, n, A.m, A.b, nnz);
+  AMG_CK(cudaMemcpyAsync(F.ptr, cnt, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToDevice, c.s));
+  k_slab_fill<<<grid_for(n, kT), kT, 0, c.s>>>(n, A.ptr, A.col, (const double*)A.val, part, A.b * A.b, F.ptr, F.col,
+                                                (double*)F.val);
+  AMG_CK_LAUNCH();
+  return F;
+}
+
 // Block ILUT(tau, p) of A (fp64, reading R25): k_ilut_rows into per-row slabs, then
 // compacted into L_s / U_s.  D^-1 -> Dinv (n b^2).
 void ilut_factor(SetupCtx& c, const Mat& A, double tau, int pfill, double* Dinv, Mat& Lo, Mat& Up) {
@@ -1562,8 +1596,12 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     });
     check_err(c, "prolongator / smoother");
     Mat Lo, Up;
-    if (p.smoother == AMG_ILU0) ilu0_factor(c, A, M, Lo, Up);  // M <- D^-1
-    if (p.smoother == AMG_ILUT) ilut_factor(c, A, p.ilut_tau, p.ilut_p, M, Lo, Up);
+    if (p.smoother == AMG_ILU0 || p.smoother == AMG_ILUT) {  // M <- D^-1
+      // several slabs (reading R26): each slab's factors are those of its diagonal block
+      const Mat F = part ? slab_diagonal_blocks(c, A, part) : A;
+      if (p.smoother == AMG_ILU0) ilu0_factor(c, F, M, Lo, Up);
+      else ilut_factor(c, F, p.ilut_tau, p.ilut_p, M, Lo, Up);
+    }
     lvL.push_back(Lo);
     lvU.push_back(Up);
     Mat R = transpose(c, P);

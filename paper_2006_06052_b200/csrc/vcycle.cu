@@ -32,9 +32,11 @@ static void ilu_apply(Handle& h, Level& L, const void* g, const void* xb, void* 
   }
 }
 
-// x <- x + (LU)^-1 (f - A x)
+// x <- x + (LU)^-1 (f - A x)   (distributed: the residual with the level's halo; the
+// factors are slab-local, R26)
 static void ilu_step(Handle& h, Level& L, void* x, cudaStream_t s) {
-  launch_residual(L.A, L.f, x, L.r, h.xt, s);
+  halo_overlapped(h, L.halo, L.A, x, h.xt, L.A.b, s,
+                  [&](int r0, int r1) { launch_residual(L.A, L.f, x, L.r, h.xt, s, r0, r1); });
   ilu_apply(h, L, L.r, x, x, s);
 }
 

@@ -70,6 +70,11 @@ CASES = [
     ("amg-cg-f64", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=0, precond=0, hier_dtype=0, vcycle_vec_dtype=0,
                                                             coarse_enough=200)),
     ("schur-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1)),
+    # slab-local ILU factors (reading R26): ILU(0) and the paper's ILUT U-solver smoother
+    ("schur-ilu0-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1, smoother=2)),
+    ("schur-ilut-gmres", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=2, precond=1, smoother=3)),
+    ("amg-ilut-cg-f64", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=1, precond=0, smoother=3, hier_dtype=0,
+                                                                 vcycle_vec_dtype=0, coarse_enough=200)),
 ]
 
 
@@ -81,7 +86,8 @@ def test_dist_solve_parity(amg, P, name, kind, n, rk, kw):
     assert len(its) == 1, its  # identical control flow on every rank
     assert all(o[0].converged for o in out)
     assert relres <= 1e-8
-    ok = {"solver": "solver", "precond": "precond", "coarse_enough": "coarse_enough"}
+    ok = {"solver": "solver", "precond": "precond", "coarse_enough": "coarse_enough", "smoother": "smoother",
+          "ilut_tau": "ilut_tau", "ilut_p": "ilut_p", "ilu_sweeps": "ilu_sweeps"}
     op = oracle.default_params(nparts=P, hier_f32=int(kw.get("hier_dtype", 1) == 1),
                                vec_f32=int(kw.get("vcycle_vec_dtype", 1) == 1),
                                **{ok[k]: v for k, v in kw.items() if k in ok})

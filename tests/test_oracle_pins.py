@@ -766,6 +766,33 @@ def test_ilut_row_bounds(rng):
     assert nfill > 0  # the case exercises the fill limit
 
 
+@pytest.mark.parametrize("smoother", [oracle.ILU0, oracle.ILUT])
+def test_ilu_slab_local_factors(rng, smoother):
+    # reading R26: with nparts slabs the factors are those of the slabs' diagonal blocks --
+    # no block couples two slabs, and with tau = 0, p >= n (ILUT) they are the exact LU of
+    # the block-diagonal part (numpy); ILU(0) keeps (LU)_ij = a_ij on that part's pattern
+    n, b, P = 60, 2, 3
+    ptr, col, val = random_bsr(rng, n, b, density=0.12, dom=10, symmetric_pattern=True)
+    kw = dict(ilut_tau=0.0, ilut_p=n) if smoother == oracle.ILUT else {}
+    A, S = _solver(ptr, col, val, smoother=smoother, precond=oracle.PC_AMG, nparts=P, coarse_enough=10 * b,
+                   hier_f32=0, vec_f32=0, **kw)
+    assert S.levels >= 2
+    bd = [r * n // P for r in range(P + 1)]
+    part = np.repeat(np.arange(P), np.diff(bd))
+    L, U = _ilu_dense(S)
+    Ad = A.dense()
+    mask = np.kron(part[:, None] == part[None, :], np.ones((b, b), bool))
+    Abar = np.where(mask, Ad, 0.0)
+    assert not L[~mask].any() and not U[~mask].any()
+    LU = L @ U
+    if smoother == oracle.ILUT:
+        assert np.linalg.norm(LU - Abar) <= 1e-12 * np.linalg.norm(Abar)
+    else:
+        pat = (bsr_dense(ptr, col, np.ones_like(val)) != 0) & mask
+        assert np.abs(LU[pat] - Abar[pat]).max() <= 1e-12 * np.abs(Abar).max()
+        assert np.linalg.norm(LU - Abar) > 1e-6 * np.linalg.norm(Abar)  # a real incomplete factorisation
+
+
 def test_ilut_smoothed_solves_reach_dense_solution(rng):
     for kind, pc, solver in ((gen.STOKES, oracle.PC_SCHUR, oracle.GMRES), (gen.POISSON3, oracle.PC_AMG, oracle.IDRS)):
         ptr, col, val = gen.matrix(kind, 8)
@@ -1058,6 +1085,61 @@ def test_dense_solve_small(rng, solver, kind):
     xd = np.linalg.solve(A.dense(), b)
     assert r.converged and r.relres_true <= 1e-10
     assert np.linalg.norm(r.x - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
+def _dense_bsr(M):
+    n = M.shape[0]
+    ptr = np.arange(0, n * n + 1, n, dtype=np.int32)
+    col = np.tile(np.arange(n, dtype=np.int32), n)
+    return ptr, col, M.reshape(n * n, 1, 1).copy()
+
+
+@pytest.mark.parametrize("solver", ["cg", "bicgstab"])
+def test_krylov_iterates_match_scipy(rng, solver):
+    # unpreconditioned CG (SPD) and BiCGStab (nonsymmetric): the oracle's iterate after k
+    # steps equals scipy.sparse.linalg's textbook iterate after k steps (an independent
+    # implementation of Hestenes-Stiefel CG and van der Vorst's BiCGStab, shadow r^ = r_0)
+    import scipy.sparse.linalg as sla
+    n = 30
+    G = rng.standard_normal((n, n))
+    M = G @ G.T + n * np.eye(n) if solver == "cg" else G + 2.0 * np.sqrt(n) * np.eye(n)
+    b = rng.standard_normal(n)
+    ptr, col, val = _dense_bsr(M)
+    for k in range(1, 7):
+        A = oracle.Mat.from_arrays(ptr, col, val)
+        S = oracle.Solver(A, solver=oracle.CG if solver == "cg" else oracle.BICGSTAB, precond=oracle.PC_NONE,
+                          maxiter=k)
+        r = S.solve(b, rtol=1e-14)
+        assert r.iters == k
+        fn = sla.cg if solver == "cg" else sla.bicgstab
+        xs, _ = fn(M, b, x0=np.zeros(n), rtol=1e-300, atol=0.0, maxiter=k)
+        assert np.linalg.norm(r.x - xs) <= 1e-11 * np.linalg.norm(xs), (solver, k)
+
+
+def test_cg_terminates_in_distinct_eigenvalue_count():
+    # CG's minimal polynomial property: an SPD matrix with 3 distinct eigenvalues is solved in
+    # exactly 3 iterations (to rounding)
+    n = 24
+    Q, _ = np.linalg.qr(np.random.default_rng(5).standard_normal((n, n)))
+    M = Q @ np.diag(np.repeat([1.0, 4.0, 9.0], n // 3)) @ Q.T
+    ptr, col, val = _dense_bsr(M)
+    S = oracle.Solver(oracle.Mat.from_arrays(ptr, col, val), solver=oracle.CG, precond=oracle.PC_NONE)
+    r = S.solve(np.ones(n), rtol=1e-10)
+    assert r.converged and r.iters == 3
+
+
+def test_fp32_emulation_rounds_every_stored_vector(rng):
+    # C9 / R10: with vec_f32 the V-cycle's stored vectors are fp32, so the preconditioner
+    # output (widened exactly) is fp32-representable; with fp64 vectors it is not
+    ptr, col, val = gen.matrix(gen.STOKES, 6)
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    r = rng.standard_normal((len(ptr) - 1) * 4)
+    for pc in (oracle.PC_AMG, oracle.PC_SCHUR):
+        z32 = oracle.Solver(A, precond=pc, coarse_enough=64).precond(r)
+        assert np.array_equal(z32, z32.astype(np.float32).astype(np.float64))
+        z64 = oracle.Solver(A, precond=pc, coarse_enough=64, hier_f32=0, vec_f32=0).precond(r)
+        assert not np.array_equal(z64, z64.astype(np.float32).astype(np.float64))
+        assert 0 < np.linalg.norm(z32 - z64) <= 1e-4 * np.linalg.norm(z64)
 
 
 @pytest.mark.parametrize("ortho", [0, 1, 2])

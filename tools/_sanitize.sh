@@ -5,7 +5,7 @@ out=gpurun_out/r2/sanitizer.txt
 : > $out
 for tool in memcheck racecheck synccheck initcheck; do
   for c in cfg3 cfg4 cfg5 cg idrs dist2; do
-    timeout 900 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize.py $c \
+    timeout 600 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize.py $c \
       > gpurun_out/r2/san_${tool}_$c.log 2>&1
     rc=$?
     echo "$tool $c rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' gpurun_out/r2/san_${tool}_$c.log | tail -1)" >> $out

@@ -3,7 +3,7 @@
 Copies the repo (without .git) to a scratch directory, applies one source mutation
 to oracle/oracle.cpp, rebuilds the oracle there and runs the CPU pins
 (tests/test_oracle_pins.py).  A mutant is KILLED when at least one pin fails.
-Usage: python tools/oracle_mutants.py [name ...]
+Usage: python tools/oracle_mutants.py [name ...] | --all
 """
 from __future__ import annotations
 
@@ -32,6 +32,41 @@ MUTANTS = {
     "gram_f32_dots_off": ("p[i] = s.p.gmres_ortho == 2 ? dot_f32_basis(V[i], w) : dot(V[i], w);",
                           "p[i] = dot(V[i], w);"),
 }
+# a sweep over the other oracle functions (round 2): one plausible slip per function
+MUTANTS.update({
+    "spmv_beta_sign": ("if (beta != 0.0) v = v + beta * y[(int64_t)I * b + r];",
+                       "if (beta != 0.0) v = v - beta * y[(int64_t)I * b + r];"),
+    "spmv_block_transposed": ("acc[r] = acc[r] + a[r * b + c] * xj[c];\n    }\n    for (int r = 0; r < b; ++r) {\n      double v = alpha",
+                              "acc[r] = acc[r] + a[c * b + r] * xj[c];\n    }\n    for (int r = 0; r < b; ++r) {\n      double v = alpha"),
+    "residual_sign": ("double v = f[(int64_t)I * b + r] - acc[r];", "double v = f[(int64_t)I * b + r] + acc[r];"),
+    "strength_eps_unsquared": ("if (fro2(A.blk(k), b) > eps2 * dn[I] * dn[J]) {",
+                               "if (fro2(A.blk(k), b) > eps * dn[I] * dn[J]) {"),
+    "pass1_no_absorb": ("    for (int32_t J : adj[I]) agg[J] = id;\n", "    for (int32_t J : adj[I]) agg[J] = agg[J];\n"),
+    "spai0_theta_sqrt": ("theta = fro2(A.blk(kd), b) / den;", "theta = std::sqrt(fro2(A.blk(kd), b) / den);"),
+    "spgemm_sign": ("for (int e = 0; e < b * b; ++e) c[e] = c[e] + tmp[e];",
+                    "for (int e = 0; e < b * b; ++e) c[e] = c[e] - tmp[e];"),
+    "vcycle_no_post": ("for (int k = 0; k < s.p.npost; ++k) post_smooth(s, L, f.data(), x, rf);",
+                       "for (int k = 0; k < 0; ++k) post_smooth(s, L, f.data(), x, rf);"),
+    "coarse_no_pivot_div": ("    y[r] = y[r] / C.LU[(size_t)r * N + r];\n", "\n"),
+    "schur_eq10_sign": ("s.Shat_diag[i] = Cv[kd] - sum;", "s.Shat_diag[i] = Cv[kd] + sum;"),
+    "cg_alpha_inverted": ("double alpha = rho / pq;", "double alpha = pq / rho;"),
+    "bicgstab_beta": ("double beta = (rho / rho_old) * (alpha / omega);",
+                      "double beta = (rho / rho_old) * (omega / alpha);"),
+    "gmres_givens_sign": ("g[j + 1] = -sn[j] * g[j];", "g[j + 1] = sn[j] * g[j];"),
+    "idrs_kappa_inverted": ("if (rho < kappa) om = om * kappa / rho;", "if (rho < kappa) om = om * rho / kappa;"),
+    "ilu0_update_sign": ("for (int e = 0; e < bb; ++e) a[(size_t)jj * bb + e] = a[(size_t)jj * bb + e] - tmp[e];",
+                         "for (int e = 0; e < bb; ++e) a[(size_t)jj * bb + e] = a[(size_t)jj * bb + e] + tmp[e];"),
+    "ilut_tau_unscaled": ("const double tau_i = tau * std::sqrt(nrm2);", "const double tau_i = tau;"),
+    "ilut_drop_before_pivot": ("if (std::sqrt(fro2(tmp.data(), b)) < tau_i) {",
+                               "if (std::sqrt(fro2(it->second.data(), b)) < tau_i) {"),
+    "ilut_keep_smallest_fill": ("return x.first > y.first || (x.first == y.first && x.second < y.second);",
+                                "return x.first < y.first || (x.first == y.first && x.second < y.second);"),
+    "ilut_tie_higher_column": ("return x.first > y.first || (x.first == y.first && x.second < y.second);",
+                               "return x.first > y.first || (x.first == y.first && x.second > y.second);"),
+    "narrow_f32_off": ("static inline double f32r(double v) { return (double)(float)v; }",
+                       "static inline double f32r(double v) { return v; }"),
+})
+SWEEP = [k for k in MUTANTS if k not in ("no_reorth_safeguard", "gram_f32_dots_off")]
 DEFAULT = ["sa_sign", "no_lumping", "pass2_last"]
 # no_reorth_safeguard survives by design: without the guard a near-breakdown step ends the
 # cycle as a happy breakdown and the restart still converges (the guard saves iterations,
@@ -47,7 +82,9 @@ def run(name: str) -> bool:
                                                                  "__pycache__", "profiles"))
         src = os.path.join(dst, "oracle", "oracle.cpp")
         text = open(src).read()
-        assert text.count(old) == 1, f"mutation site for {name} not unique/found"
+        if text.count(old) != 1:
+            print(f"{name:12s} SITE NOT UNIQUE ({text.count(old)} matches)", flush=True)
+            return False
         open(src, "w").write(text.replace(old, new))
         subprocess.check_call([sys.executable, "-c", "import gen, oracle; gen.build(); oracle.build(True)"],
                               cwd=dst)
@@ -60,6 +97,6 @@ def run(name: str) -> bool:
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or DEFAULT
+    names = SWEEP if sys.argv[1:] == ["--all"] else (sys.argv[1:] or DEFAULT)
     ok = all([run(n) for n in names])
     sys.exit(0 if ok else 1)
