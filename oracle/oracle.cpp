@@ -808,10 +808,13 @@ static orc_mat slab_diagonal_blocks(const orc_mat& A, const vector<int32_t>& bd)
 
 // C7: repeat C2-C6 while n_l * b > coarse_enough and l < max_levels - 1;
 // stop if n_c == 0 or n_c >= n_l.  Coarsest: dense LU.
-static int build_hierarchy(orc_solver& s, const orc_mat& A0) {
+// unit: rows of A0 per partitioned row (the scalar U-solver of V2 has 3 scalar rows per cell
+// and its slabs follow the cells' slabs, R18 / C12)
+static int build_hierarchy(orc_solver& s, const orc_mat& A0, int unit = 1) {
   const orc_params& p = s.p;
   orc_mat A = A0;
-  vector<int32_t> bd = slab_bounds(A.n, p.nparts < 1 ? 1 : p.nparts);
+  vector<int32_t> bd = slab_bounds(A.n / unit, p.nparts < 1 ? 1 : p.nparts);
+  for (int32_t& v : bd) v *= unit;
   s.lv.clear();
   while ((int64_t)A.n * A.b > p.coarse_enough && (int32_t)s.lv.size() < p.max_levels - 1) {
     vector<vector<int32_t>> adj;
@@ -1300,7 +1303,7 @@ extern "C" int orc_setup(const orc_mat* A, const orc_params* p, orc_solver** out
     s->schur = true;
     rc = schur_setup(*s);
     if (rc == ORC_OK && p->schur_u_scalar) s->Au_s = scalar_expansion(s->Au);
-    if (rc == ORC_OK) rc = build_hierarchy(*s, p->schur_u_scalar ? s->Au_s : s->Au);
+    if (rc == ORC_OK) rc = build_hierarchy(*s, p->schur_u_scalar ? s->Au_s : s->Au, p->schur_u_scalar ? s->Au.b : 1);
   } else if (p->precond == ORC_PC_AMG) {
     rc = build_hierarchy(*s, s->A);
   }

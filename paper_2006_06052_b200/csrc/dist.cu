@@ -543,7 +543,6 @@ int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_b
   rc = check_params(p);
   if (rc != AMG_OK) return rc;
   if (A_local->n_block_cols != n_global_block_rows || row_begin < 0) return AMG_EDIM;
-  if (p->precond == AMG_PC_SCHUR && p->schur_u_scalar) return AMG_EINVAL;  // single-device only (R18)
   Handle* h = setup_dist_impl(A_local, row_begin, n_global_block_rows, c->c, p, (cudaStream_t)stream);
   *out = reinterpret_cast<amg_handle*>(h);
   return AMG_OK;

@@ -75,6 +75,10 @@ CASES = [
     ("schur-ilut-gmres", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=2, precond=1, smoother=3)),
     ("amg-ilut-cg-f64", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=1, precond=0, smoother=3, hier_dtype=0,
                                                                  vcycle_vec_dtype=0, coarse_enough=200)),
+    # the paper's V2: the U-solver hierarchy on the scalar expansion of A_u, slabs of 3 scalar rows per cell
+    ("schur-v2-scalar-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1, schur_u_scalar=1)),
+    ("schur-v2-scalar-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(solver=2, precond=1, schur_u_scalar=1,
+                                                                      hier_dtype=0, vcycle_vec_dtype=0)),
 ]
 
 
@@ -87,7 +91,7 @@ def test_dist_solve_parity(amg, P, name, kind, n, rk, kw):
     assert all(o[0].converged for o in out)
     assert relres <= 1e-8
     ok = {"solver": "solver", "precond": "precond", "coarse_enough": "coarse_enough", "smoother": "smoother",
-          "ilut_tau": "ilut_tau", "ilut_p": "ilut_p", "ilu_sweeps": "ilu_sweeps"}
+          "ilut_tau": "ilut_tau", "ilut_p": "ilut_p", "ilu_sweeps": "ilu_sweeps", "schur_u_scalar": "schur_u_scalar"}
     op = oracle.default_params(nparts=P, hier_f32=int(kw.get("hier_dtype", 1) == 1),
                                vec_f32=int(kw.get("vcycle_vec_dtype", 1) == 1),
                                **{ok[k]: v for k, v in kw.items() if k in ok})
