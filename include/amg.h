@@ -142,8 +142,8 @@ int amg_setup(const amg_bsr* A /* host struct, device arrays */, const amg_param
  * pmask (DEVICE, [n_block_rows * block_size] bytes, non-zero = pressure unknown) selects the
  * pressure unknowns among the scalar unknowns of A in any order; the split is taken on the
  * scalar expansion of A and the U-solver hierarchy is scalar (b = 1, as the paper's V2;
- * DESIGN.md reading R21).  p->precond must be AMG_PC_SCHUR, p->schur_shat 0 or 1; single
- * device (amg_setup_dist has no mask).  The mask may be freed after the call.  Errors as
+ * DESIGN.md reading R21).  p->precond must be AMG_PC_SCHUR, p->schur_shat 0 or 1 (several
+ * GPUs: amg_setup_dist_pmask).  The mask may be freed after the call.  Errors as
  * amg_setup; AMG_EINVAL also for an all-velocity or all-pressure mask. */
 int amg_setup_pmask(const amg_bsr* A, const uint8_t* pmask, const amg_params* p, void* stream,
                     struct amg_handle** out);
@@ -250,6 +250,15 @@ int amg_comm_init(const void* id128 /* host */, int32_t nranks, int32_t rank,
  * ids.  After this call amg_solve takes the LOCAL slices of b and x. */
 int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_block_rows,
                    struct amg_comm* c, const amg_params* p, void* stream, struct amg_handle** out);
+/* amg_setup_dist with a general scalar pressure mask (R21 on several ranks, R27):
+ * pmask_local (DEVICE, [A_local->n_block_rows * block_size] bytes, non-zero = pressure) marks
+ * this rank's scalar unknowns; each class is numbered globally in ascending scalar order, so a
+ * rank owns a contiguous range of velocity and of pressure unknowns, and the scalar U-solver
+ * hierarchy is slab-distributed by those ranges.  p->precond must be AMG_PC_SCHUR,
+ * p->schur_shat 0 or 1.  Collective; errors as amg_setup_dist. */
+int amg_setup_dist_pmask(const amg_bsr* A_local, const uint8_t* pmask_local, int64_t row_begin,
+                         int64_t n_global_block_rows, struct amg_comm* c, const amg_params* p, void* stream,
+                         struct amg_handle** out);
 void amg_comm_destroy(struct amg_comm* c);
 /* Thread-emulated communicator (testing the distributed path on ONE device): a group of
  * nranks host threads of this process, each with its own stream; exchanges are device
@@ -258,6 +267,28 @@ void amg_comm_destroy(struct amg_comm* c);
 int amg_local_group_create(int32_t nranks, void** group /* host out */);
 void amg_local_group_destroy(void* group);
 int amg_comm_init_local(void* group, int32_t rank, struct amg_comm** out);
+
+/* Host-staged communicator over a caller's transport (separate PROCESSES, e.g. a
+ * torch.distributed gloo group, on one device or several): every exchange is copied to host
+ * memory, handed to the callbacks below, and copied back; the stream is synchronised around
+ * each call, so no kernel ever waits on another process.  For testing the distributed data
+ * plane with real processes where NCCL cannot run (one GPU); the product path is NCCL.
+ * Every callback returns 0 on success; any other value fails the call with AMG_ENCCL.  All
+ * buffers are HOST memory owned by the library for the duration of the call. */
+typedef struct {
+  void* ctx;
+  /* in-place sum over ranks of n fp64 values */
+  int (*allreduce_sum)(void* ctx, double* vals, int32_t n);
+  /* all[r * n_each + i] = rank r's mine[i] */
+  int (*allgather_i64)(void* ctx, const int64_t* mine, int32_t n_each, int64_t* all);
+  /* grouped point-to-point: ns sends (peer, buffer, bytes) and nr receives, completed on return */
+  int (*exchange)(void* ctx, int32_t ns, const int32_t* send_peer, const void* const* send_buf,
+                  const int64_t* send_bytes, int32_t nr, const int32_t* recv_peer, void* const* recv_buf,
+                  const int64_t* recv_bytes);
+  int (*barrier)(void* ctx);
+} amg_host_comm_ops;
+int amg_comm_init_host(const amg_host_comm_ops* ops /* host, copied */, int32_t nranks, int32_t rank,
+                       struct amg_comm** out);
 
 #ifdef __cplusplus
 }

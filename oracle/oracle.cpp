@@ -810,11 +810,13 @@ static orc_mat slab_diagonal_blocks(const orc_mat& A, const vector<int32_t>& bd)
 // stop if n_c == 0 or n_c >= n_l.  Coarsest: dense LU.
 // unit: rows of A0 per partitioned row (the scalar U-solver of V2 has 3 scalar rows per cell
 // and its slabs follow the cells' slabs, R18 / C12)
-static int build_hierarchy(orc_solver& s, const orc_mat& A0, int unit = 1) {
+// bd0 (optional): explicit level-0 slab bounds (the pressure mask's velocity ranges, R27)
+static int build_hierarchy(orc_solver& s, const orc_mat& A0, int unit = 1, const vector<int32_t>* bd0 = nullptr) {
   const orc_params& p = s.p;
   orc_mat A = A0;
   vector<int32_t> bd = slab_bounds(A.n / unit, p.nparts < 1 ? 1 : p.nparts);
   for (int32_t& v : bd) v *= unit;
+  if (bd0) bd = *bd0;
   s.lv.clear();
   while ((int64_t)A.n * A.b > p.coarse_enough && (int32_t)s.lv.size() < p.max_levels - 1) {
     vector<vector<int32_t>> adj;
@@ -1326,7 +1328,15 @@ extern "C" int orc_setup_pmask(const orc_mat* A, const uint8_t* pmask, const orc
   s->masked = true;
   vector<uint8_t> pm(pmask, pmask + (size_t)A->n * A->b);
   int rc = schur_setup_pmask(*s, pm);
-  if (rc == ORC_OK) rc = build_hierarchy(*s, s->Au);
+  // P slabs of block rows (C12): the velocity unknowns of slab r, numbered in ascending scalar
+  // order, are the range [bu[r], bu[r+1]) -- the U-solver hierarchy's level-0 slabs (R27)
+  vector<int32_t> cb = slab_bounds(A->n, p->nparts < 1 ? 1 : p->nparts), bu(cb.size(), 0);
+  for (size_t r = 1; r < cb.size(); ++r) {
+    int32_t cnt = 0;
+    for (int64_t q = 0; q < (int64_t)cb[r] * A->b; ++q) cnt += pm[q] ? 0 : 1;
+    bu[r] = cnt;
+  }
+  if (rc == ORC_OK) rc = build_hierarchy(*s, s->Au, 1, &bu);
   if (rc != ORC_OK) {
     delete s;
     return rc;

@@ -68,7 +68,7 @@ EXPORTS = ["amg_params_default", "amg_status_string", "amg_setup", "amg_solve", 
            "amg_kernel_launches", "amg_profile_begin", "amg_profile_end", "amg_last_error",
            "bsr_plan_create", "bsr_plan_spmv", "bsr_plan_destroy", "amg_csr_to_bsr", "amg_memory_report",
            "amg_local_group_create", "amg_local_group_destroy", "amg_comm_init_local", "amg_setup_pmask",
-           "amg_solve_counters"]
+           "amg_solve_counters", "amg_setup_dist_pmask", "amg_comm_init_host"]
 
 _lib = None
 
@@ -104,6 +104,8 @@ def lib():
             "amg_comm_unique_id": (i32, [P]),
             "amg_comm_init": (i32, [P, i32, i32, P]),
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
+            "amg_setup_dist_pmask": (i32, [P, P, i64, i64, P, P, P, P]),
+            "amg_comm_init_host": (i32, [P, i32, i32, P]),
             "amg_comm_destroy": (None, [P]),
             "amg_kernel_launches": (i64, []),
             "amg_local_group_create": (i32, [i32, P]),
@@ -287,15 +289,20 @@ class Solver:
 
     def __init__(self, A: BSR, params: amg_params | None = None, stream=None, comm=None,
                  row_begin: int = 0, n_global: int | None = None, pmask=None, **kw):
-        """pmask: optional device uint8 tensor [n*b] (non-zero = pressure unknown) -> amg_setup_pmask."""
+        """pmask: optional device uint8 tensor [n*b] (non-zero = pressure unknown) -> amg_setup_pmask
+        (with comm: this rank's rows -> amg_setup_dist_pmask)."""
         self.params = params if params is not None else default_params(**kw)
         self.A = A
+        self.comm = comm  # the handle keeps the communicator's pointer: it must outlive the solver
         d = A.desc()
         h = ctypes.c_void_p()
         self.n_pressure = None
-        if pmask is not None:
-            if comm is not None:
-                raise ValueError("pmask: single device only")
+        if pmask is not None and comm is not None:  # this rank's rows of the mask (R27)
+            rc = lib().amg_setup_dist_pmask(ctypes.byref(d), ctypes.c_void_p(pmask.data_ptr()), row_begin,
+                                            A.m if n_global is None else n_global, comm.h, ctypes.byref(self.params),
+                                            _stream_ptr(stream), ctypes.byref(h))
+            self.n_pressure = int((pmask != 0).sum().item())
+        elif pmask is not None:
             rc = lib().amg_setup_pmask(ctypes.byref(d), ctypes.c_void_p(pmask.data_ptr()), ctypes.byref(self.params),
                                        _stream_ptr(stream), ctypes.byref(h))
             self.n_pressure = int((pmask != 0).sum().item())
@@ -453,9 +460,79 @@ class LocalGroup:
             self.h = None
 
 
+_AR = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32)
+_AG = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
+                       ctypes.POINTER(ctypes.c_int64))
+_EX = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                       ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
+                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64))
+_BA = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+
+
+class amg_host_comm_ops(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce_sum", _AR), ("allgather_i64", _AG), ("exchange", _EX),
+                ("barrier", _BA)]
+
+
+def _host_ops(pg=None):
+    """amg_host_comm_ops over a torch.distributed (CPU / gloo) process group: marshalling only
+    -- every buffer is a host array the library owns for the duration of the call."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def guard(fn):
+        def run(*a):
+            try:
+                fn(*a)
+                return 0
+            except Exception:  # reported as AMG_ENCCL by the library
+                return 1
+        return run
+
+    def allreduce(_, vals, n):
+        t = torch.from_numpy(np.ctypeslib.as_array(vals, (n,)))
+        dist.all_reduce(t, group=pg)
+
+    def allgather(_, mine, n_each, out):
+        world = dist.get_world_size(pg)
+        src = torch.from_numpy(np.ctypeslib.as_array(mine, (n_each,)).copy())
+        dst = torch.from_numpy(np.ctypeslib.as_array(out, (world * n_each,)))
+        dist.all_gather(list(dst.view(world, n_each).unbind(0)), src, group=pg)
+
+    def as_bytes(ptr, n):
+        return torch.from_numpy(np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), (max(n, 1),)))
+
+    def exchange(_, ns, sp, sb, sz, nr, rp, rb, rz):
+        reqs = [dist.isend(as_bytes(sb[i], sz[i])[:sz[i]], sp[i], group=pg) for i in range(ns) if sz[i]]
+        reqs += [dist.irecv(as_bytes(rb[i], rz[i])[:rz[i]], rp[i], group=pg) for i in range(nr) if rz[i]]
+        for r in reqs:
+            r.wait()
+
+    def barrier(_):
+        dist.barrier(group=pg)
+
+    cbs = (_AR(guard(allreduce)), _AG(guard(allgather)), _EX(guard(exchange)), _BA(guard(barrier)))
+    ops = amg_host_comm_ops(None, *cbs)
+    ops._keep = cbs  # the C function pointers live as long as these objects
+    return ops
+
+
 class Comm:
-    """NCCL communicator for amg_setup_dist (one process per GPU), or with
-    ``Comm.local(group, rank)`` the thread-emulated one."""
+    """NCCL communicator for amg_setup_dist (one process per GPU); ``Comm.local(group, rank)``
+    the thread-emulated one; ``Comm.host(pg)`` the host-staged one over a torch.distributed
+    (gloo) group -- separate processes, e.g. several on one GPU in the multi-process tests."""
+
+    @classmethod
+    def host(cls, pg=None):
+        import torch.distributed as dist
+        self = cls.__new__(cls)
+        self.ops = _host_ops(pg)  # the callbacks must outlive the communicator
+        h = ctypes.c_void_p()
+        _check(lib().amg_comm_init_host(ctypes.byref(self.ops), dist.get_world_size(pg), dist.get_rank(pg),
+                                        ctypes.byref(h)), "amg_comm_init_host")
+        self.h = h
+        return self
 
     @classmethod
     def local(cls, group: "LocalGroup", rank: int):

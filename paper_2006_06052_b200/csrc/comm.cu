@@ -3,6 +3,8 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "amg.h"
 #include "comm.h"
@@ -128,7 +130,69 @@ class LocalComm : public CommBase {
   void barrier() override { g->barrier(); }
 };
 
+class HostComm : public CommBase {
+ public:
+  HostOps ops;
+  struct Pending {
+    void* dbuf;
+    const void* sbuf;
+    size_t bytes;
+    int peer;
+  };
+  std::vector<Pending> sends, recvs;
+  HostComm(const HostOps& o, int n, int r) : ops(o) {
+    nranks = n;
+    rank = r;
+  }
+  static void ck(int rc, const char* what) {
+    if (rc != 0) fail(AMG_ENCCL, std::string("host communicator: ") + what + " callback failed");
+  }
+  void allreduce_sum(double* d, int n, cudaStream_t s) override {
+    if (nranks == 1 || n == 0) return;
+    std::vector<double> h(n);
+    AMG_CK(cudaMemcpyAsync(h.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    AMG_CK(cudaStreamSynchronize(s));
+    ck(ops.allreduce_sum(ops.ctx, h.data(), n), "allreduce_sum");
+    AMG_CK(cudaMemcpyAsync(d, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    AMG_CK(cudaStreamSynchronize(s));
+  }
+  void allgather_host(const int64_t* mine, int n_each, int64_t* all) override {
+    ck(ops.allgather_i64(ops.ctx, mine, n_each, all), "allgather_i64");
+  }
+  void group_begin() override {
+    sends.clear();
+    recvs.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t) override { sends.push_back({nullptr, buf, bytes, peer}); }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t) override { recvs.push_back({buf, nullptr, bytes, peer}); }
+  void group_end(cudaStream_t s) override {
+    AMG_CK(cudaStreamSynchronize(s));  // the send buffers are complete
+    std::vector<std::vector<char>> sh(sends.size()), rh(recvs.size());
+    std::vector<int32_t> sp, rp;
+    std::vector<const void*> sb;
+    std::vector<void*> rb;
+    std::vector<int64_t> sz, rz;
+    for (size_t i = 0; i < sends.size(); ++i) {
+      sh[i].resize(std::max<size_t>(sends[i].bytes, 1));
+      if (sends[i].bytes) AMG_CK(cudaMemcpy(sh[i].data(), sends[i].sbuf, sends[i].bytes, cudaMemcpyDeviceToHost));
+      sp.push_back(sends[i].peer), sb.push_back(sh[i].data()), sz.push_back((int64_t)sends[i].bytes);
+    }
+    for (size_t i = 0; i < recvs.size(); ++i) {
+      rh[i].resize(std::max<size_t>(recvs[i].bytes, 1));
+      rp.push_back(recvs[i].peer), rb.push_back(rh[i].data()), rz.push_back((int64_t)recvs[i].bytes);
+    }
+    ck(ops.exchange(ops.ctx, (int32_t)sp.size(), sp.data(), sb.data(), sz.data(), (int32_t)rp.size(), rp.data(),
+                    rb.data(), rz.data()),
+       "exchange");
+    for (size_t i = 0; i < recvs.size(); ++i)
+      if (recvs[i].bytes) AMG_CK(cudaMemcpyAsync(recvs[i].dbuf, rh[i].data(), recvs[i].bytes, cudaMemcpyHostToDevice, s));
+    AMG_CK(cudaStreamSynchronize(s));
+  }
+  void barrier() override { ck(ops.barrier(ops.ctx), "barrier"); }
+};
+
 CommBase* make_nccl_comm(const void* id128, int nranks, int rank) { return new NcclComm(id128, nranks, rank); }
+CommBase* make_host_comm(const HostOps& ops, int nranks, int rank) { return new HostComm(ops, nranks, rank); }
 CommBase* make_local_comm(LocalGroup* g, int rank) { return new LocalComm(g, rank); }
 
 }  // namespace amgb

@@ -1,7 +1,9 @@
 // comm.h -- communication layer of the row-slab distributed solve.
 //
-// Two implementations behind one interface:
+// Three implementations behind one interface:
 //  * NcclComm  -- one process per GPU, NCCL over NVLink/NVSwitch (the product path);
+//  * HostComm  -- separate processes over a caller's transport (callbacks on host copies:
+//    torch.distributed gloo in the multi-process tests);
 //  * LocalComm -- P ranks as P host threads of one process on one device, exchanging
 //    through device-to-device copies with host barriers.  It exists so that the
 //    distributed setup/solve can be tested on a single GPU: no kernel ever waits on
@@ -65,7 +67,17 @@ struct LocalGroup {
   }
 };
 
+struct HostOps {  // mirror of amg_host_comm_ops (amg.h)
+  void* ctx;
+  int (*allreduce_sum)(void*, double*, int32_t);
+  int (*allgather_i64)(void*, const int64_t*, int32_t, int64_t*);
+  int (*exchange)(void*, int32_t, const int32_t*, const void* const*, const int64_t*, int32_t, const int32_t*,
+                  void* const*, const int64_t*);
+  int (*barrier)(void*);
+};
+
 CommBase* make_nccl_comm(const void* id128, int nranks, int rank);
+CommBase* make_host_comm(const HostOps& ops, int nranks, int rank);
 CommBase* make_local_comm(LocalGroup* g, int rank);
 
 }  // namespace amgb

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cstdlib>
 #include <cstring>
 
@@ -190,11 +191,14 @@ void remap_shift(Mat& M, int64_t shift, int64_t width) {
   M.m = (int32_t)width;
 }
 
-// square distributed matrix: global columns -> [local | ghosts], ghost plan (both sides)
-void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bounds, Halo& H, cudaStream_t s) {
+// distributed matrix: global columns -> [local | ghosts], ghost plan (both sides).  The local
+// columns are [lo, lo + ncols) (ncols < 0: M.n, a square slab); bounds: the column owners.
+void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bounds, Halo& H, cudaStream_t s,
+                int64_t ncols = -1) {
   CommBase* comm = h.comm;
   const int P = comm->nranks, me = comm->rank;
-  const int64_t hi = lo + M.n;
+  const int32_t nl = (int32_t)(ncols < 0 ? M.n : ncols);
+  const int64_t hi = lo + nl;
   std::vector<int32_t> c(M.nnz);
   if (M.nnz) AMG_CK(cudaMemcpy(c.data(), M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
   std::vector<int32_t> ghosts;
@@ -204,11 +208,11 @@ void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bound
   ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
   for (auto& v : c) {
     if (v >= lo && v < hi) v = (int32_t)(v - lo);
-    else v = (int32_t)(M.n + (std::lower_bound(ghosts.begin(), ghosts.end(), v) - ghosts.begin()));
+    else v = (int32_t)(nl + (std::lower_bound(ghosts.begin(), ghosts.end(), v) - ghosts.begin()));
   }
   if (M.nnz) AMG_CK(cudaMemcpy(M.col, c.data(), sizeof(int32_t) * M.nnz, cudaMemcpyHostToDevice));
   H = Halo{};
-  H.nloc = M.n;
+  H.nloc = nl;
   H.nghost = (int)ghosts.size();
   {  // the longest run of rows without a ghost column (>= a quarter of the rows): overlap window
     std::vector<int32_t> hp((size_t)M.n + 1);
@@ -217,7 +221,7 @@ void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bound
     for (int32_t r = 0; r <= M.n; ++r) {
       bool ghost_row = r == M.n;
       if (r < M.n)
-        for (int32_t k = hp[r]; k < hp[r + 1] && !ghost_row; ++k) ghost_row = c[k] >= M.n;
+        for (int32_t k = hp[r]; k < hp[r + 1] && !ghost_row; ++k) ghost_row = c[k] >= nl;
       if (ghost_row) {
         if (r - run_lo > best_hi - best_lo) best_lo = run_lo, best_hi = r;
         run_lo = r + 1;
@@ -225,7 +229,7 @@ void build_halo(Handle& h, Mat& M, int64_t lo, const std::vector<int64_t>& bound
     }
     if ((int64_t)(best_hi - best_lo) * 4 >= M.n && H.nghost > 0) H.int_lo = best_lo, H.int_hi = best_hi;
   }
-  M.m = M.n + H.nghost;
+  M.m = nl + H.nghost;
   // how many ghosts I need from every rank; everybody learns the full P x P matrix
   std::vector<int64_t> need(P, 0), all((size_t)P * P);
   for (int32_t g : ghosts) {
@@ -284,7 +288,7 @@ void allgatherv_bytes(CommBase* comm, char* buf, const std::vector<int64_t>& off
 }
 
 Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, CommBase* comm, const amg_params* p,
-                        cudaStream_t s) {
+                        cudaStream_t s, const uint8_t* pmask = nullptr) {
   const int P = comm->nranks, me = comm->rank;
   const int b = A->block_size;
   // 1. slabs and the global matrix on every rank (fp64)
@@ -327,8 +331,17 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
   for (int r = 0; r < P; ++r) o[r] = nnz_off[r] * 8 * b * b, c[r] = (nnz_off[r + 1] - nnz_off[r]) * 8 * b * b;
   allgatherv_bytes(comm, (char*)G.val, o, c, s);
 
+  // the global pressure mask (R27): every rank's scalar rows, in rank order
+  uint8_t* gmask = nullptr;
+  if (pmask) {
+    gmask = tmp.alloc_n<uint8_t>(std::max<int64_t>(n_global * b, 1));
+    if (loc.n) AMG_CK(cudaMemcpyAsync(gmask + bounds[me] * b, pmask, (size_t)loc.n * b, cudaMemcpyDeviceToDevice, s));
+    for (int r = 0; r < P; ++r) o[r] = bounds[r] * b, c[r] = (bounds[r + 1] - bounds[r]) * b;
+    allgatherv_bytes(comm, (char*)gmask, o, c, s);
+  }
+
   // 2. the global hierarchy (identical on every rank), rank-local aggregation
-  Handle* Gh = build_handle(G, p, bounds, s, /*workspace=*/false);
+  Handle* Gh = build_handle(G, p, bounds, s, /*workspace=*/false, gmask);
   tmp.release();
   if (Gh->amg_active && Gh->lv.empty() && P > 1) {
     delete Gh;
@@ -358,7 +371,7 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
     make_tma_plan(h->A, s, &h->arena);
     h->alg_bytes_spmv = (double)h->A.nnz * (4.0 + 8.0 * b * b) + 4.0 * (h->A.n + 1) + 16.0 * h->A.n * b;
     const size_t xs = dtype_size(h->xt);
-    if (h->schur) {
+    if (h->schur && !Gh->masked) {
       const int64_t k0 = 0;
       (void)k0;
       int32_t pe[2];
@@ -378,6 +391,39 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       AMG_CK(cudaMemcpy(h->shat64, Gh->shat64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
       AMG_CK(cudaMemcpy(h->mS64, Gh->mS64 + bounds[me], 8 * h->n, cudaMemcpyDeviceToDevice));
       make_schur_views(h->A, h->nu, h->Bv, h->BTv, h->vt, h->Bm, h->BTm, s, &h->arena);
+    }
+    if (Gh->masked) {  // general pressure mask (R27): this rank's unknowns of each class
+      const auto &ub = Gh->ubounds, &pb = Gh->pbounds;
+      if ((int)ub.size() != P + 1 || (int)pb.size() != P + 1) fail(AMG_EINVAL, "amg_setup_dist_pmask: class ranges");
+      h->masked = true;
+      h->ubounds = ub;
+      h->pbounds = pb;
+      h->nu_s = (int32_t)(ub[me + 1] - ub[me]);
+      h->np_s = (int32_t)(pb[me + 1] - pb[me]);
+      // index maps: class position -> local scalar unknown
+      for (auto [dst, src, lo, cnt] : {std::tuple<int32_t**, const int32_t*, int64_t, int32_t>{&h->uidx, Gh->uidx, ub[me], h->nu_s},
+                                       {&h->pidx, Gh->pidx, pb[me], h->np_s}}) {
+        std::vector<int32_t> v(std::max(cnt, 1));
+        if (cnt) AMG_CK(cudaMemcpy(v.data(), src + lo, 4 * (size_t)cnt, cudaMemcpyDeviceToHost));
+        for (int32_t i = 0; i < cnt; ++i) v[i] -= (int32_t)(bounds[me] * b);
+        *dst = h->arena.alloc_n<int32_t>(std::max(cnt, 1));
+        AMG_CK(cudaMemcpy(*dst, v.data(), 4 * (size_t)std::max(cnt, 1), cudaMemcpyHostToDevice));
+      }
+      // scalar B (pressure rows x velocity columns) and B^T (velocity rows x pressure columns)
+      h->Bm = slice_rows(h->arena, Gh->Bm, pb[me], pb[me + 1], s);
+      build_halo(*h, h->Bm, ub[me], ub, h->haloBu, s, h->nu_s);
+      h->BTm = slice_rows(h->arena, Gh->BTm, ub[me], ub[me + 1], s);
+      build_halo(*h, h->BTm, pb[me], pb, h->haloBTp, s, h->np_s);
+      h->Bm.fast32 = h->BTm.fast32 = false;
+      make_tma_plan(h->Bm, s, &h->arena);
+      make_tma_plan(h->BTm, s, &h->arena);
+      const size_t vs = dtype_size(h->vt);
+      h->mS = h->arena.alloc(std::max(h->np_s, 1) * vs);
+      h->shat64 = h->arena.alloc_n<double>(std::max(h->np_s, 1));
+      h->mS64 = h->arena.alloc_n<double>(std::max(h->np_s, 1));
+      AMG_CK(cudaMemcpy(h->mS, (char*)Gh->mS + pb[me] * vs, h->np_s * vs, cudaMemcpyDeviceToDevice));
+      AMG_CK(cudaMemcpy(h->shat64, Gh->shat64 + pb[me], 8 * (size_t)h->np_s, cudaMemcpyDeviceToDevice));
+      AMG_CK(cudaMemcpy(h->mS64, Gh->mS64 + pb[me], 8 * (size_t)h->np_s, cudaMemcpyDeviceToDevice));
     }
     // hierarchy levels: levels 0 .. rep_from-1 as row slabs with halos; from rep_from on (the
     // first level with fewer than AMG_REPLICATE_ROWS block rows per rank, default 50,000;
@@ -431,7 +477,9 @@ Handle* setup_dist_impl(const amg_bsr* A, int64_t row_begin, int64_t n_global, C
       LL.agg = h->arena.alloc_n<int32_t>(std::max<int64_t>(nl, 1));
       AMG_CK(cudaMemcpy(LL.agg, GL.agg + r0, 4 * nl, cudaMemcpyDeviceToDevice));
       LL.nc = (int32_t)(c1 - c0);
-      const int64_t nx = (int64_t)(nl + LL.halo.nghost) * bb;
+      // level 0 of a masked Schur hierarchy also receives B's velocity ghosts (R27)
+      const int64_t ng = std::max<int64_t>(LL.halo.nghost, l == 0 && h->masked ? h->haloBu.nghost : 0);
+      const int64_t nx = (int64_t)(nl + ng) * bb;
       LL.f = h->arena.alloc(std::max<int64_t>(nl * bb, 1) * xs);
       LL.r = h->arena.alloc(std::max<int64_t>(nl * bb, 1) * xs);
       LL.x = h->arena.alloc(std::max<int64_t>(nx, 1) * xs);
@@ -528,10 +576,40 @@ int amg_comm_init_local(void* group, int32_t rank, struct amg_comm** out) {
   return AMG_OK;
 }
 
+int amg_comm_init_host(const amg_host_comm_ops* ops, int32_t nranks, int32_t rank, struct amg_comm** out) {
+  if (!ops || !out || nranks < 1 || rank < 0 || rank >= nranks || !ops->allreduce_sum || !ops->allgather_i64 ||
+      !ops->exchange || !ops->barrier)
+    return AMG_EINVAL;
+  static_assert(sizeof(HostOps) == sizeof(amg_host_comm_ops), "HostOps mirrors amg_host_comm_ops");
+  HostOps o;
+  std::memcpy(&o, ops, sizeof(o));
+  amg_comm* c = new amg_comm;
+  c->c = make_host_comm(o, nranks, rank);
+  *out = c;
+  return AMG_OK;
+}
+
 void amg_comm_destroy(struct amg_comm* c) {
   if (!c) return;
   delete c->c;
   delete c;
+}
+
+int amg_setup_dist_pmask(const amg_bsr* A_local, const uint8_t* pmask_local, int64_t row_begin,
+                         int64_t n_global_block_rows, struct amg_comm* c, const amg_params* p, void* stream,
+                         struct amg_handle** out) {
+  AMG_GUARD_BEGIN
+  if (!c || !c->c || !out || !pmask_local || !p) return AMG_EINVAL;
+  int rc = validate_bsr(A_local, false);
+  if (rc != AMG_OK) return rc;
+  rc = check_params(p);
+  if (rc != AMG_OK) return rc;
+  if (A_local->n_block_cols != n_global_block_rows || row_begin < 0) return AMG_EDIM;
+  if (p->precond != AMG_PC_SCHUR || p->schur_shat == 2) return AMG_EINVAL;
+  Handle* h = setup_dist_impl(A_local, row_begin, n_global_block_rows, c->c, p, (cudaStream_t)stream, pmask_local);
+  *out = reinterpret_cast<amg_handle*>(h);
+  return AMG_OK;
+  AMG_GUARD_END
 }
 
 int amg_setup_dist(const amg_bsr* A_local, int64_t row_begin, int64_t n_global_block_rows, struct amg_comm* c,

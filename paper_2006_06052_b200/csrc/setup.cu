@@ -1356,6 +1356,17 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
     AMG_CK_LAUNCH();
     const int64_t nu = scan(c, iu, (int)N), np = scan(c, ip, (int)N);
     if (nu == 0 || np == 0) fail(AMG_EINVAL, "pressure mask selects no velocity or no pressure unknown");
+    {  // each class's range per slab of block rows (several slabs: R27)
+      h.ubounds.assign(bounds0.size(), 0);
+      h.pbounds.assign(bounds0.size(), 0);
+      for (size_t r = 0; r < bounds0.size(); ++r) {
+        int32_t v[2];
+        AMG_CK(cudaMemcpy(&v[0], iu + bounds0[r] * b, 4, cudaMemcpyDeviceToHost));
+        AMG_CK(cudaMemcpy(&v[1], ip + bounds0[r] * b, 4, cudaMemcpyDeviceToHost));
+        h.ubounds[r] = v[0];
+        h.pbounds[r] = v[1];
+      }
+    }
     h.nu_s = (int32_t)nu;
     h.np_s = (int32_t)np;
     h.uidx = h.arena.alloc_n<int32_t>(nu);
@@ -1464,7 +1475,7 @@ void setup_build(Handle& h, const Mat& A64, const std::vector<int64_t>& bounds0,
   std::vector<int64_t> bounds = bounds0;
   if (h.schur && p.schur_u_scalar && !h.masked)
     for (int64_t& v : bounds) v *= h.nu;
-  if (h.masked) bounds = {0, (int64_t)h.nu_s};  // single device
+  if (h.masked) bounds = h.ubounds.size() > 2 ? h.ubounds : std::vector<int64_t>{0, (int64_t)h.nu_s};
   const int nparts = (int)bounds.size() - 1;
   h.lbounds.clear();
   h.lbounds.push_back(bounds);

@@ -73,7 +73,7 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     const size_t xs = dtype_size(h.xt);
     const int np = h.masked ? h.np_s : h.n;
     h.rp = h.arena.alloc(std::max(np, 1) * xs);
-    h.pp = h.arena.alloc(std::max(np + h.halo0.nghost, 1) * xs);
+    h.pp = h.arena.alloc(std::max(np + std::max(h.halo0.nghost, h.haloBTp.nghost), 1) * xs);
   }
   AMG_CK(cudaStreamCreateWithFlags(&h.work, cudaStreamNonBlocking));
   if (h.comm) {

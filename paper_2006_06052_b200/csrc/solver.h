@@ -75,6 +75,11 @@ struct Handle {
   bool masked = false;
   int32_t np_s = 0, nu_s = 0;
   int32_t *uidx = nullptr, *pidx = nullptr;
+  // distributed pressure mask (R27): the ranks' ranges of the velocity / pressure classes
+  // (global class numbering; ubounds = the U-solver hierarchy's level-0 slabs) and the ghost
+  // plans of the scalar B (velocity ghosts) and B^T (pressure ghosts)
+  std::vector<int64_t> ubounds, pbounds;
+  Halo haloBu, haloBTp;
   void *ru = nullptr, *rp = nullptr, *us = nullptr, *pp = nullptr, *ru2 = nullptr, *uu = nullptr;
   // AMG hierarchy (on A, or on A_u for Schur)
   int bh = 0;

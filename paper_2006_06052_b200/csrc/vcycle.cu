@@ -115,7 +115,9 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   if (h.masked) {  // general scalar pressure mask (R21): the same steps on the scalar split
     launch_mask_split(h.nu_s, h.np_s, h.uidx, h.pidx, r, scale, f0, h.rp, h.xt, s, scale_dev);
     void* us = vcycle_run(h, 0, s);
+    halo_exchange(h, h.haloBu, us, h.xt, 1, s);              // distributed (R27): B's velocity ghosts
     launch_schur_p(h.Bm, h.mS, h.rp, us, h.pp, h.xt, s);     // p = m_S o (r_p - B u*)
+    halo_exchange(h, h.haloBTp, h.pp, h.xt, 1, s);           // B^T's pressure ghosts
     launch_residual(h.BTm, f0, h.pp, f0, h.xt, s);           // r_u' = r_u - B^T p (in place)
     void* u = vcycle_run(h, 0, s);
     launch_mask_join(h.nu_s, h.np_s, h.uidx, h.pidx, u, h.pp, h.xt, z, zt, s);

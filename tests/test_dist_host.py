@@ -66,3 +66,54 @@ def test_gloo_world2():
     for r, p in enumerate(parts):
         lp = np.array(p[0])
         assert np.array_equal(lp + ptr[bd[r]], ptr[bd[r]:bd[r + 1] + 1])
+
+
+def _ops_worker(rank, world, port, q):
+    # the host-staged communicator's callbacks (amg_host_comm_ops over gloo) called the way
+    # the library calls them: host buffers behind raw pointers
+    import ctypes
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2006_06052_b200 import _host_ops
+        ops = _host_ops()
+        vals = (ctypes.c_double * 3)(1.0 + rank, 2.0, -rank)
+        assert ops.allreduce_sum(None, vals, 3) == 0
+        mine = (ctypes.c_int64 * 2)(10 * rank, 10 * rank + 1)
+        allv = (ctypes.c_int64 * (2 * world))()
+        assert ops.allgather_i64(None, mine, 2, allv) == 0
+        # ring exchange: send rank-stamped bytes to the next rank, receive from the previous
+        nxt, prv = (rank + 1) % world, (rank - 1) % world
+        sbuf = (ctypes.c_uint8 * 5)(*[rank * 10 + i for i in range(5)])
+        rbuf = (ctypes.c_uint8 * 5)()
+        sp, rp = (ctypes.c_int32 * 1)(nxt), (ctypes.c_int32 * 1)(prv)
+        sb = (ctypes.c_void_p * 1)(ctypes.addressof(sbuf))
+        rb = (ctypes.c_void_p * 1)(ctypes.addressof(rbuf))
+        sz = (ctypes.c_int64 * 1)(5)
+        assert ops.exchange(None, 1, sp, sb, sz, 1, rp, rb, sz) == 0
+        assert ops.barrier(None) == 0
+        q.put((rank, list(vals), list(allv), list(rbuf)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_comm_ops_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_ops_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, vals, allv, rbuf in res:
+        assert vals == [1.0 + 2.0 + 3.0, 6.0, -3.0]
+        assert allv == [0, 1, 10, 11, 20, 21]
+        prv = (rank - 1) % world
+        assert rbuf == [prv * 10 + i for i in range(5)]

@@ -206,3 +206,87 @@ def test_halo_overlap_interleaved_copy_is_exact(amg, envvars):
         runs.append((x, out[0][0].iters))
     assert runs[0][1] == runs[1][1]
     assert np.array_equal(runs[0][0], runs[1][0])
+
+
+def _dist_arrays(amg, P, ptr, col, val, bvec, mask, kw):
+    """P thread-emulated ranks on row slabs of the given global BSR arrays, with the rows'
+    slice of a scalar pressure mask (amg_setup_dist_pmask)."""
+    n, b = len(ptr) - 1, val.shape[-1]
+    group = amg.LocalGroup(P)
+    bounds = [r * n // P for r in range(P + 1)]
+    out, errs = [None] * P, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            r0, r1 = bounds[r], bounds[r + 1]
+            lp = (ptr[r0:r1 + 1] - ptr[r0]).astype(np.int32)
+            lc, lv = col[ptr[r0]:ptr[r1]], val[ptr[r0]:ptr[r1]]
+            A = amg.BSR.from_numpy(lp, lc, lv, n_block_cols=n)
+            pm = torch.as_tensor(mask[r0 * b:r1 * b].astype(np.uint8), device="cuda")
+            S = amg.Solver(A, amg.default_params(precond=1, **kw), stream=st, comm=amg.Comm.local(group, r),
+                           row_begin=r0, n_global=n, pmask=pm)
+            with torch.cuda.stream(st):
+                bl = torch.as_tensor(bvec[r0 * b:r1 * b], device="cuda")
+                x = torch.zeros_like(bl)
+            rep = S.solve(bl, x, 1e-8, stream=st)
+            st.synchronize()
+            out[r] = (rep, x.cpu().numpy(), [S.level_aggregates(l) for l in range(S.levels - 1)])
+        except Exception as e:  # surfaced below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+def _cellwise_scrambled_stokes(n, seed=7):
+    """4x4 Stokes blocks with the (u, v, w, p) order of every cell permuted at random: the
+    pressure sits at a different component in each cell (a general mask on a block matrix
+    whose slabs stay whole cells)."""
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    perm = np.array([np.random.default_rng(seed + i).permutation(4) for i in range(n ** 3)])
+    rows = np.repeat(np.arange(n ** 3), np.diff(ptr))
+    val2 = np.stack([val[k][np.ix_(perm[rows[k]], perm[col[k]])] for k in range(len(col))])
+    mask = (perm == 3).ravel()
+    return ptr, col, val2, mask
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("case", ["interleaved-f32-idrs", "cellwise-scrambled-f64-gmres"])
+def test_dist_pmask_parity(amg, P, case):
+    # reading R27: the general scalar pressure mask on P ranks -- each rank owns contiguous
+    # ranges of the velocity and of the pressure unknowns, the scalar U-solver hierarchy is
+    # slab-distributed by the velocity ranges; the oracle's P-slab pmask mode is the reference
+    if case.startswith("interleaved"):
+        n = 12
+        ptr, col, val = gen.matrix(gen.STOKES, n)
+        mask = np.arange(4 * n ** 3) % 4 == 3
+        kw = dict(solver=3)
+    else:
+        ptr, col, val, mask = _cellwise_scrambled_stokes(8)
+        kw = dict(solver=2, coarse_enough=100, hier_dtype=0, vcycle_vec_dtype=0)
+    N = len(mask)
+    bvec = np.random.default_rng(3).standard_normal(N)
+    out = _dist_arrays(amg, P, ptr, col, val, bvec, mask, kw)
+    its = {o[0].iters for o in out}
+    assert len(its) == 1, its
+    x = np.concatenate([o[1] for o in out])
+    A = oracle.Mat.from_arrays(ptr, col, val)
+    relres = np.linalg.norm(bvec - oracle.spmv(A, x)) / np.linalg.norm(bvec)
+    assert all(o[0].converged for o in out) and relres <= 1e-8
+    h32 = int(kw.get("hier_dtype", 1) == 1)
+    O = oracle.Solver(A, oracle.default_params(nparts=P, precond=oracle.PC_SCHUR, solver=kw["solver"], hier_f32=h32,
+                                               vec_f32=h32, coarse_enough=kw.get("coarse_enough", 3000)), pmask=mask)
+    ro = O.solve(bvec, rtol=1e-8)
+    assert abs(out[0][0].iters - ro.iters) <= 2, (out[0][0].iters, ro.iters)
+    assert out[0][0].levels == O.levels
+    for l in range(O.levels - 1):
+        oagg = O.level_agg(l)
+        agg = out[0][2][l] if (len(out[0][2][l]) == len(oagg) and P > 1) else np.concatenate([o[2][l] for o in out])
+        assert np.array_equal(agg, oagg), f"level {l}"

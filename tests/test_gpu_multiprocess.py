@@ -1,0 +1,39 @@
+"""The distributed path with real separate processes: P ranks launched by
+torch.distributed.run, each its own process and CUDA context on cuda:0, exchanging through
+the host-staged communicator over a gloo group (amg_comm_init_host).  NCCL itself cannot
+run two ranks on one GPU; the data plane here -- distributed setup (allgathers), halo
+exchanges, Krylov allreduces -- is the library's, only the transport differs.  Every rank
+must take the same iteration count, within +-2 of the oracle's P-slab mode, with the same
+slab-local aggregates and true relres <= 1e-8."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("case", ["schur-gmres", "amg-bicgstab", "schur-idrs-ilut"])
+def test_multiprocess_solve(P, case):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(P),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), case]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["P"] == P and len(set(d["iters"])) == 1 and all(d["converged"])
+    assert d["relres"] <= 1e-8
+    assert abs(d["iters"][0] - d["oracle_iters"]) <= 2, d
+    assert d["levels"] == d["oracle_levels"] and d["aggregates_equal"], d

@@ -21,8 +21,10 @@ cap() {  # name regex skip
 cap top 'k_bsr_sellr<\(int\)4.*double, float.*LEpiSpmv<double>' 0
 cap smooth 'k_bsr_sellr<\(int\)3, \(int\)3, \(int\)2, float, float, \(bool\)1, amgb::LEpiSmooth<float, float>>' 0
 cap resid 'k_bsr_sellr<\(int\)3, \(int\)3, \(int\)2, float, float, \(bool\)1, amgb::LEpiResidual<float>>' 0
-cap p0 'k_bsr_sellr<\(int\)3, \(int\)3, \(int\)2, float, float, \(bool\)1, amgb::LEpiSpmv<float>>' 1
-cap applym 'k_apply_M<\(int\)3, float, float>' 0
+cap p0 'k_bsr_sellr<\(int\)3, \(int\)3, \(int\)2, float, float, \(bool\)1, amgb::LEpiSpmvPre<float>>' 1
+cap r0m 'LEpiSpmvM' 0
+cap splitm 'k_split4_M' 0
+cap schurum 'EpiSchurUM' 0
 cap schurp 'LEpiSchurP' 0
 cap mdot32 'k_cgs_wide<\(int\)4, \(int\)0, float>' 2
 python tools/spmv_probe.py 4 1 0 5 > gpurun_out/${TAG}_spmv_plain.log 2>&1 || exit 1
