@@ -207,6 +207,21 @@ struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
   const V* mS;
   const X* rp;
   X* p;
+  // k_bsr_sellr: m_S and r_p of the row loaded ahead of its blocks (short rows, as K7)
+  static constexpr bool kPre = true;
+  struct PreT {
+    V m;
+    X r;
+  };
+  template <int BR>
+  __device__ __forceinline__ void pre(int row, PreT (&v)[BR]) const {
+    v[0].m = mS[row];
+    v[0].r = rp[row];
+  }
+  template <int BR>
+  __device__ __forceinline__ void row_pre(int row, const double (&yr)[BR], const PreT (&v)[BR]) const {
+    p[row] = to_out<X>((double)v[0].m * ((double)v[0].r - yr[0]));
+  }
   template <int BR>
   __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
     if (!L.valid) return;

@@ -325,8 +325,8 @@ void make_tma_plan(Mat& A, cudaStream_t s, Arena* arena, bool want_tma) {
     const bool square = A.br == 0 && A.bc == 0 && A.b >= 2 && A.b <= 4;
     // Schur B^T (nu x 1 blocks): interleaved copy 5.4 vs 5.15 TB/s (TMA rows); B (1 x nu) stays on
     // the lane kernel (5.1 vs 4.1 interleaved)
-    const bool rect = (A.br > 0 || A.bc > 0) && A.rows_per_block() > 1 && A.rows_per_block() <= 4 &&
-                      A.cols_per_block() <= 4;
+    const bool rect = (A.br > 0 || A.bc > 0) && (A.rows_per_block() > 1 || env_int("AMG_SCHUR_B_SELLR", 0)) &&
+                      A.rows_per_block() <= 4 && A.cols_per_block() <= 4;
     const int forced = env_set("AMG_LANE_VAR") ? env_int("AMG_LANE_VAR", 0) : -1;
     // interleaved row-per-lane copy (k_bsr_sellr): 0 never, 1 (default) square-block matrices with
     // 3..64 blocks per row on >= 64 slices per SM, 2 every square matrix with an arena.  Measured
@@ -921,6 +921,7 @@ void make_schur_views(const Mat& A, int nu, const void* Bv, const void* BTv, int
   // for the lane kernel)
   make_tma_plan(Bm, s, arena);
   make_tma_plan(BTm, s, arena, !env_int("AMG_NO_TMA_SCHUR", 0));
+  if (env_set("AMG_SCHUR_B_VAR")) Bm.lane_var = env_int("AMG_SCHUR_B_VAR", Bm.lane_var);  // A/B switch (tools)
 }
 
 void launch_schur_p(const Mat& Bm, const void* mS, const void* rp, const void* us, void* p, int xt, cudaStream_t s) {
