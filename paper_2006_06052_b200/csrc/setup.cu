@@ -576,9 +576,20 @@ __global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
     i = __shfl_sync(kFull, i, 0);
     if (i >= n) return;
     const int r0 = ptr[i], len0 = ptr[i + 1] - r0;
+    // a failed row (capacity, missing pivot, or another row's failure seen while waiting)
+    // records the error and is still marked done, empty: no warp ever waits forever
+    auto fail_row = [&](int code) {
+      if (lane == 0) {
+        if (code) set_err(err, code);
+        llen[i] = 0, ulen[i] = 0;
+      }
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) st_release(done + i, 1);
+    };
     if (len0 > kIlutCap) {
-      if (lane == 0) set_err(err, AMG_EINVAL);
-      return;  // the flag stays down: waiters on this row would hang -- setup fails anyway
+      fail_row(AMG_EINVAL);
+      continue;
     }
     for (int q = lane; q < len0; q += 32) {
       wc[q] = col[r0 + q];
@@ -595,6 +606,7 @@ __global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
     __syncwarp();
     int last = -1;
     bool overflow = false;
+    int bad = 0;  // this row's error code (AMG_E*, negative), or 1: another row failed
     for (;;) {
       // next k: the smallest live column in (last, i)
       const int len = *wlen;
@@ -607,7 +619,11 @@ __global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
       if (k == INT_MAX) break;
       const unsigned who = __ballot_sync(kFull, best == k);
       const int kq = __shfl_sync(kFull, bidx, __ffs(who) - 1);
-      while (ld_acquire(done + k) == 0) {
+      while (ld_acquire(done + k) == 0)
+        if (*(volatile int*)err) break;
+      if (__any_sync(kFull, *(volatile int*)err != 0)) {
+        bad = 1;
+        break;
       }
       // multiplier l = w_k D_k^-1 (lane e < BB: entry e, blk_mul's order)
       double le = 0.0;
@@ -661,10 +677,14 @@ __global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
           }
       }
       if (__any_sync(kFull, overflow)) {
-        if (lane == 0) set_err(err, AMG_EINVAL);
-        return;
+        bad = AMG_EINVAL;
+        break;
       }
       __syncwarp();
+    }
+    if (bad) {
+      fail_row(bad == 1 ? 0 : bad);
+      continue;
     }
     const int len = min(*wlen, kIlutCap);
     // pivot
@@ -673,8 +693,8 @@ __global__ void __launch_bounds__(32 * IlutShape<B>::W) k_ilut_rows(
       if (wc[q] == i) dq = q;
     const unsigned dm = __ballot_sync(kFull, dq >= 0);
     if (!dm) {
-      if (lane == 0) set_err(err, AMG_EZERODIAG);
-      return;
+      fail_row(AMG_EZERODIAG);
+      continue;
     }
     dq = __shfl_sync(kFull, dq, __ffs(dm) - 1);
     if (lane == 0 && !block_inverse<B>(wv + (size_t)dq * BB, Dinv + (int64_t)i * BB)) set_err(err, AMG_ESINGULAR_BLOCK);

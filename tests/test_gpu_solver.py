@@ -232,6 +232,27 @@ def test_ilut_random_matrices(amg, rng, tau, p):
             check_hierarchy(S, O, h32)
 
 
+def test_ilut_overflow_fails_cleanly(amg, rng):
+    # a row beyond the factorisation's working-row capacity (512 blocks) fails the setup with
+    # AMG_EINVAL -- and every row waiting on it is released (no hang)
+    n, b = 700, 1
+    rows = [np.arange(n)] + [np.array([0, i]) for i in range(1, n)]  # arrow matrix
+    ptr = np.zeros(n + 1, np.int32)
+    ptr[1:] = np.cumsum([len(r) for r in rows])
+    col = np.concatenate(rows).astype(np.int32)
+    val = rng.standard_normal((len(col), b, b)) * 0.1
+    for i in range(n):
+        val[ptr[i] + (0 if i == 0 else 1)] = 4.0
+    A = amg.BSR.from_numpy(ptr, col, val)
+    with pytest.raises(amg.AmgError) as e:
+        amg.Solver(A, amg.default_params(precond=0, solver=1, smoother=3, hier_dtype=0, vcycle_vec_dtype=0,
+                                         coarse_enough=10))
+    assert "ILUT" in str(e.value) or "-1" in str(e.value)
+    # the library is still usable afterwards
+    S = amg.Solver(A, amg.default_params(precond=0, solver=1, hier_dtype=0, vcycle_vec_dtype=0, coarse_enough=10))
+    assert S.levels >= 2
+
+
 def test_ilut_stencil_levels(amg):
     # every level of a 3x3 SA hierarchy (7-point stencil rows, then aggregated rows with 20-60
     # blocks and their fill) factorised on the GPU equals the oracle's factorisation
