@@ -888,15 +888,72 @@ __global__ void __launch_bounds__(256) k_dense_gemv(int N, const V* __restrict__
   if (lane == 0) x[warp] = to_out<X>(s);
 }
 
+// One CTA per row (rows of 1.5-3 K unknowns: cfg 1 / cfg 5): 16-byte loads of the row and of f
+// (rows 16-byte aligned: N * sizeof(V) % 16 == 0, else k_dense_gemv), fp64 partial sums
+// combined in a fixed order (warp butterflies, then the warps' sums in warp order).  The
+// warp-per-row kernel had ~10 warps per SM in flight and reached 1.5 TB/s.
+template <typename V, typename X>
+__global__ void __launch_bounds__(128) k_dense_gemv_cta(int N, const V* __restrict__ A, const X* __restrict__ f,
+                                                        X* __restrict__ x) {
+  constexpr int VW = 16 / sizeof(V);  // values per 16-byte load
+  const int row = blockIdx.x;
+  const V* a = A + (int64_t)row * N;
+  double s = 0.0;
+  const int nv = N / VW;
+  // 4 loads of the row in flight per thread (the loop is otherwise one dependent load deep)
+  constexpr int UN = 4;
+  int q = threadIdx.x;
+  for (; q + (UN - 1) * 128 < nv; q += UN * 128) {
+    V av[UN][VW];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      if constexpr (std::is_same_v<V, float>) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(a) + q + u * 128);
+        av[u][0] = t.x, av[u][1] = t.y, av[u][2] = t.z, av[u][3] = t.w;
+      } else {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(a) + q + u * 128);
+        av[u][0] = t.x, av[u][1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) s = fma((double)av[u][e], (double)__ldg(f + (q + u * 128) * VW + e), s);
+  }
+  for (; q < nv; q += 128) {
+    V av[VW];
+    if constexpr (std::is_same_v<V, float>) {
+      const float4 t = __ldcs(reinterpret_cast<const float4*>(a) + q);
+      av[0] = t.x, av[1] = t.y, av[2] = t.z, av[3] = t.w;
+    } else {
+      const double2 t = __ldcs(reinterpret_cast<const double2*>(a) + q);
+      av[0] = t.x, av[1] = t.y;
+    }
+#pragma unroll
+    for (int e = 0; e < VW; ++e) s = fma((double)av[e], (double)__ldg(f + q * VW + e), s);
+  }
+  for (int j = nv * VW + threadIdx.x; j < N; j += 128) s = fma((double)a[j], (double)__ldg(f + j), s);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  __shared__ double ws[4];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) x[row] = to_out<X>(((ws[0] + ws[1]) + ws[2]) + ws[3]);
+}
+
 void launch_dense_gemv(int32_t N, const void* Ainv, int vt, const void* f, void* x, int xt,
                        cudaStream_t s) {
   if (N == 0) return;
   ProfScope ps_(prof_name("coarse_gemv", 1, vt, xt), (double)N * N * dtype_size(vt) + 2.0 * N * dtype_size(xt), s);
+  const bool aligned = ((size_t)N * dtype_size(vt)) % 16 == 0 && ((uintptr_t)Ainv % 16) == 0;
   dispatch_t(vt, [&](auto v) {
     using V = decltype(v);
     dispatch_t(xt, [&](auto xx) {
       using X = decltype(xx);
-      k_dense_gemv<V, X><<<grid_for((int64_t)N * 32, 256), 256, 0, s>>>(N, (const V*)Ainv, (const X*)f, (X*)x);
+      if (aligned)
+        k_dense_gemv_cta<V, X><<<N, 128, 0, s>>>(N, (const V*)Ainv, (const X*)f, (X*)x);
+      else
+        k_dense_gemv<V, X><<<grid_for((int64_t)N * 32, 256), 256, 0, s>>>(N, (const V*)Ainv, (const X*)f, (X*)x);
     });
   });
   AMG_CK_LAUNCH();
