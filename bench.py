@@ -215,14 +215,16 @@ def config_dict(cfg, n, gpus):
             "l2": f"inputs larger than L2 (outer matrix {7 * n ** 3 * 132 / 1e9:.1f} GB fp64, 126 MB L2); no flush"}
 
 
-def spmv_cfg2(amg, torch, n=128, reps=30):
-    """cfg 2 SpMV microbench, 4x4 fp32 values x fp64 x (the metric's SpMV)."""
-    ptr, col, val = gen.matrix(gen.RAND27, n, 4)
-    x = gen.rhs(gen.X_UNIFORM, n, 4)
-    A = amg.BSR.from_numpy(ptr, col, val, dtype=torch.float32)
-    del val
-    xd = torch.as_tensor(x, device="cuda")
-    yd = torch.zeros_like(xd)
+def spmv_cfg2(amg, torch, n=128, reps=30, b=4, vdt="f32", xdt="f64", mats=None):
+    """cfg 2 SpMV microbench (default: 4x4 fp32 values x fp64 x, the metric's SpMV)."""
+    tdt = {"f32": torch.float32, "f64": torch.float64}
+    if mats is None:
+        mats = gen.matrix(gen.RAND27, n, b)
+    ptr, col, val = mats
+    x = gen.rhs(gen.X_UNIFORM, n, b)
+    A = amg.BSR.from_numpy(ptr, col, val, dtype=tdt[vdt])
+    xd = torch.as_tensor(x, device="cuda").to(tdt[xdt])
+    yd = torch.zeros(len(x), dtype=torch.float64 if xdt == "f64" else torch.float32, device="cuda")
     plan = amg.SpmvPlan(A)
     for _ in range(5):
         plan(xd, yd)
@@ -239,9 +241,10 @@ def spmv_cfg2(amg, torch, n=128, reps=30):
         per.append(a.elapsed_time(b) / reps)
     ms = statistics.median(per)
     Z, nr = len(col), n ** 3
-    byts = 4 * (nr + 1) + Z * (4 + 16 * 4) + nr * 4 * 8 * 2
-    return {"config": "cfg2 27-point 128^3, 4x4 fp32 values x fp64 x", "ms": ms, "GBs": byts / ms / 1e6,
-            "alg_bytes": byts}
+    sv, sx = (4 if vdt == "f32" else 8), (4 if xdt == "f32" else 8)
+    byts = 4 * (nr + 1) + Z * (4 + b * b * sv) + nr * b * sx * 2  # SURVEY.md §8(d) B_spmv
+    return {"config": f"cfg2 27-point {n}^3, {b}x{b} {'fp32' if vdt == 'f32' else 'fp64'} values x "
+                      f"{'fp32' if xdt == 'f32' else 'fp64'} x", "ms": ms, "GBs": byts / ms / 1e6, "alg_bytes": byts}
 
 
 def main():
@@ -418,6 +421,16 @@ def main():
         out["spmv"]["frac"] = out["spmv"]["GBs"] / peak
         out["spmv"]["frac_of_8000"] = out["spmv"]["GBs"] / 8000.0
         out["spmv"]["traffic"] = ncu_traffic("spmv_cfg2_b4_f32xf64")
+        # also b = 3 and the fp64 variants (and fp32 x fp32, the V-cycle's)
+        out["spmv_variants"] = []
+        for bb in (4, 3):
+            mats = gen.matrix(gen.RAND27, 128, bb)
+            for vd, xd_ in (("f64", "f64"), ("f32", "f64"), ("f32", "f32")):
+                r_ = spmv_cfg2(amg, torch, b=bb, vdt=vd, xdt=xd_, mats=mats)
+                r_["frac"] = r_["GBs"] / peak
+                out["spmv_variants"].append(r_)
+            del mats
+            torch.cuda.empty_cache()
     if not args.no_alt and world == 1 and args.cfg in (4, 5):
         # the paper's own outer solver (Table 1: IDR(5)) on the same workload, same PC/hierarchy
         # (a secondary line; the headline stays BASELINE's GMRES(30))
@@ -470,6 +483,11 @@ def main():
                 "workload": config_dict(oc, on, 1)["workload"], "value": t_, "unit": "s/solve", "iters": ro.iters,
                 "relres_true": ro.relres_true, "converged": ro.converged, "levels": ro.levels,
                 "solve_alg_GBs": ro.alg_bytes / t_ / 1e9, "solve_roofline_frac": ro.alg_bytes / t_ / 1e9 / peak}
+            og = oracle_full_size(oc)  # the oracle's measured run of this config (1 host thread)
+            if og:
+                out["other_configs"][f"cfg{oc}"]["oracle"] = {
+                    "solve_s": og["solve_s"], "setup_s": og["setup_s"], "iters": og["iters"], "threads": 1,
+                    "source": "tests/golden/oracle_full_size.json (tools/oracle_reference_runs.py, GPU box host)"}
             del So, bo, xo
             torch.cuda.empty_cache()
     if not args.no_cpu_baseline:

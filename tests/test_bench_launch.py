@@ -21,7 +21,11 @@ def _run(args, env=None):
 def test_gpus_2_relaunches_two_ranks():
     r = _run(["--gpus", "2", "--probe-launch"])
     assert r.returncode == 0, r.stderr[-2000:]
-    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    # the two ranks' lines may interleave on the shared stdout: decode every object in order
+    lines, dec, text, i = [], json.JSONDecoder(), r.stdout, 0
+    while (i := text.find("{", i)) >= 0:
+        obj, i = dec.raw_decode(text, i)
+        lines.append(obj)
     assert sorted(l["rank"] for l in lines) == [0, 1]
     assert all(l["world"] == 2 and l["sum"] == 2.0 for l in lines)
 
