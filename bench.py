@@ -232,13 +232,13 @@ def spmv_cfg2(amg, torch, n=128, reps=30, b=4, vdt="f32", xdt="f64", mats=None):
     # previous kernel), median over 5 groups
     per = []
     for _ in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         for _ in range(reps):
             plan(xd, yd)
-        b.record()
+        e1.record()
         torch.cuda.synchronize()
-        per.append(a.elapsed_time(b) / reps)
+        per.append(e0.elapsed_time(e1) / reps)
     ms = statistics.median(per)
     Z, nr = len(col), n ** 3
     sv, sx = (4 if vdt == "f32" else 8), (4 if xdt == "f32" else 8)
