@@ -254,7 +254,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=5, choices=[1, 3, 4, 5])
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--grid", "--n", dest="n", type=int, default=None)
     ap.add_argument("--cpu-n", type=int, default=96, help="grid of the cpu_baseline sample")
     ap.add_argument("--probe-launch", action="store_true",
                     help="launcher check: init the process group, print rank / world, exit")
@@ -262,6 +262,9 @@ def main():
     ap.add_argument("--no-spmv", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the IDR(5) secondary measurement")
     ap.add_argument("--no-other", action="store_true", help="skip the cfg 1/3/4 secondary measurements")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="host: TEST HARNESS ONLY -- ranks exchange through the host-staged communicator over "
+                         "gloo and may share one GPU (checks the N > 1 bench path; not a scaling measurement)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -271,7 +274,9 @@ def main():
             so.bind(("127.0.0.1", 0))
             port = so.getsockname()[1]
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+               # torch.distributed.run would read "--n" as an abbreviation of its own options
+               *["--grid" if a == "--n" else ("--grid=" + a[4:] if a.startswith("--n=") else a) for a in sys.argv[1:]]]
         sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -300,11 +305,17 @@ def main():
     import torch
     import paper_2006_06052_b200 as amg
 
+    host_comm = args.comm == "host"
+    if host_comm:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_comm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.n or gen.CONFIGS[args.cfg]["n"]
     nrows = n ** 3
     bd = amg.slab_bounds(nrows, world)
@@ -315,7 +326,7 @@ def main():
     A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=nrows)
     del val
     params = params_for(amg, args.cfg)
-    comm = amg.Comm(rank, world) if world > 1 else None
+    comm = (amg.Comm.host() if host_comm else amg.Comm(rank, world)) if world > 1 else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     S = amg.Solver(A, params, comm=comm, row_begin=r0, n_global=nrows)
@@ -348,11 +359,12 @@ def main():
     launches = (amg.kernel_launches() - l0)
     ms = e0.elapsed_time(e1) / args.steps
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if host_comm else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
     rep = reps[-1]
+    bsz = len(bvec) // (r1 - r0) if r1 > r0 else 4  # scalar unknowns per block row
 
     # end to end through the C ABI with HOST buffers (copies inside the timed region)
     bh = torch.as_tensor(bvec).pin_memory()
@@ -367,7 +379,7 @@ def main():
         te.append(time.perf_counter() - t0)
     e2e_s = statistics.median(te)
     if dist:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device="cpu" if host_comm else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
@@ -404,8 +416,9 @@ def main():
         "solve_roofline_frac": rep.alg_bytes / (ms * 1e-3) / 1e9 / peak,
         "solve_roofline_frac_of_8000": rep.alg_bytes / (ms * 1e-3) / 1e9 / 8000.0,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_s, "unit": "s/solve", "h2d_bytes_per_step": 2 * bh.numel() * 8,
-                "d2h_bytes_per_step": bh.numel() * 8},
+        # whole-job bytes: every rank copies its slab of b and x in and x out
+        "e2e": {"value": e2e_s, "unit": "s/solve", "h2d_bytes_per_step": 2 * nrows * bsz * 8,
+                "d2h_bytes_per_step": nrows * bsz * 8},
         "roofline": {"bound": "hbm", "kernel": top["kernel"], "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "frac_of_8000": achieved / 8000.0, "traffic": ncu_traffic(f"{top['kernel']}@cfg{args.cfg}") if n == 256 else None,
                      "traffic_source": "profiles/traffic.json (ncu --set full, one launch)", "peak_source": peak_src,
@@ -490,7 +503,9 @@ def main():
                     "source": "tests/golden/oracle_full_size.json (tools/oracle_reference_runs.py, GPU box host)"}
             del So, bo, xo
             torch.cuda.empty_cache()
-    if not args.no_cpu_baseline:
+    if host_comm:
+        out["comm"] = "host-staged over gloo (TEST HARNESS: ranks may share one GPU; not a scaling measurement)"
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
         # bounded live sample (~20 s of one host core): the oracle at cpu_n^3 of the same
         # generator, setup untimed, per-iteration time of 10 iterations, scaled by cells to n^3
         # and by the oracle's measured full-size iteration count

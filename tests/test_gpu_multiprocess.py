@@ -37,3 +37,21 @@ def test_multiprocess_solve(P, case):
     assert d["relres"] <= 1e-8
     assert abs(d["iters"][0] - d["oracle_iters"]) <= 2, d
     assert d["levels"] == d["oracle_levels"] and d["aggregates_equal"], d
+
+
+def test_bench_two_ranks_host_comm():
+    # bench.py's N > 1 path (self-launch under torch.distributed.run, slabs, barrier, max over
+    # ranks, rank-0 line, whole-job e2e bytes) with 2 processes on the one GPU through the
+    # host-staged communicator -- a check of the multi-rank bench code, not a scaling number
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--cfg", "4", "--n", "24", "--comm", "host"]
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 only
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["converged"] and d["relres_true"] <= 1e-8 and "host-staged" in d["comm"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 24 ** 3 * 8 and "cpu_baseline" not in d
