@@ -287,8 +287,13 @@ typedef struct {
                   const int64_t* recv_bytes);
   int (*barrier)(void* ctx);
 } amg_host_comm_ops;
+/* flags & 1: stream-ordered mode -- each exchange / reduction becomes device->pinned-host copies,
+ * a cudaLaunchHostFunc running the callback, and host->device copies, all on the caller's
+ * stream (no host synchronisation, so the solve's CUDA graphs capture them as they capture the
+ * NCCL calls); the callbacks then run on CUDA's host-function thread and must not call CUDA.
+ * Pinned staging: AMG_HOSTCOMM_POOL_MB (default 256) allocated here. */
 int amg_comm_init_host(const amg_host_comm_ops* ops /* host, copied */, int32_t nranks, int32_t rank,
-                       struct amg_comm** out);
+                       int32_t flags, struct amg_comm** out);
 
 #ifdef __cplusplus
 }

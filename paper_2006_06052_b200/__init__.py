@@ -105,7 +105,7 @@ def lib():
             "amg_comm_init": (i32, [P, i32, i32, P]),
             "amg_setup_dist": (i32, [P, i64, i64, P, P, P, P]),
             "amg_setup_dist_pmask": (i32, [P, P, i64, i64, P, P, P, P]),
-            "amg_comm_init_host": (i32, [P, i32, i32, P]),
+            "amg_comm_init_host": (i32, [P, i32, i32, i32, P]),
             "amg_comm_destroy": (None, [P]),
             "amg_kernel_launches": (i64, []),
             "amg_local_group_create": (i32, [i32, P]),
@@ -524,13 +524,14 @@ class Comm:
     (gloo) group -- separate processes, e.g. several on one GPU in the multi-process tests."""
 
     @classmethod
-    def host(cls, pg=None):
+    def host(cls, pg=None, ordered: bool = False):
+        """ordered: stream-ordered mode (copies + host functions on the stream, graph-capturable)."""
         import torch.distributed as dist
         self = cls.__new__(cls)
         self.ops = _host_ops(pg)  # the callbacks must outlive the communicator
         h = ctypes.c_void_p()
         _check(lib().amg_comm_init_host(ctypes.byref(self.ops), dist.get_world_size(pg), dist.get_rank(pg),
-                                        ctypes.byref(h)), "amg_comm_init_host")
+                                        1 if ordered else 0, ctypes.byref(h)), "amg_comm_init_host")
         self.h = h
         return self
 

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
 #include <algorithm>
 
 #include "amg.h"
@@ -133,6 +134,7 @@ class LocalComm : public CommBase {
 class HostComm : public CommBase {
  public:
   HostOps ops;
+  bool ordered;  // stream-ordered (capturable) mode: copies + cudaLaunchHostFunc, no host sync
   struct Pending {
     void* dbuf;
     const void* sbuf;
@@ -140,15 +142,76 @@ class HostComm : public CommBase {
     int peer;
   };
   std::vector<Pending> sends, recvs;
-  HostComm(const HostOps& o, int n, int r) : ops(o) {
+  // stream-ordered mode: one pinned staging call record per distinct exchange / reduction
+  // (keyed by its device buffers, sizes and peers), kept for the communicator's life so that
+  // a captured graph replays with the same host buffers
+  struct Call {
+    HostOps ops;
+    std::vector<int32_t> sp, rp;
+    std::vector<const void*> sb;
+    std::vector<void*> rb;
+    std::vector<int64_t> sz, rz;
+    double* red = nullptr;
+    int n = 0;
+    volatile int rc = 0;
+  };
+  std::map<std::vector<int64_t>, Call*> calls;
+  char* pool = nullptr;
+  size_t pool_size = 0, pool_used = 0;
+  HostComm(const HostOps& o, int n, int r, bool ord) : ops(o), ordered(ord) {
     nranks = n;
     rank = r;
+    if (ordered) {  // allocated up front: no allocation may happen inside a stream capture
+      pool_size = (size_t)env_int("AMG_HOSTCOMM_POOL_MB", 256) << 20;
+      AMG_CK(cudaMallocHost((void**)&pool, pool_size));
+    }
+  }
+  ~HostComm() override {
+    for (auto& kv : calls) delete kv.second;
+    if (pool) cudaFreeHost(pool);
   }
   static void ck(int rc, const char* what) {
     if (rc != 0) fail(AMG_ENCCL, std::string("host communicator: ") + what + " callback failed");
   }
+  void check_async() {
+    for (auto& kv : calls)
+      if (kv.second->rc) ck(kv.second->rc, "stream-ordered");
+  }
+  char* host_buf(size_t bytes) {
+    bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
+    if (pool_used + bytes > pool_size) fail(AMG_ENOMEM, "host communicator: staging pool exhausted (AMG_HOSTCOMM_POOL_MB)");
+    char* p = pool + pool_used;
+    pool_used += bytes;
+    return p;
+  }
+  static void CUDART_CB run_exchange(void* p) {
+    Call* c = static_cast<Call*>(p);
+    const int rc = c->ops.exchange(c->ops.ctx, (int32_t)c->sp.size(), c->sp.data(), c->sb.data(), c->sz.data(),
+                                   (int32_t)c->rp.size(), c->rp.data(), c->rb.data(), c->rz.data());
+    if (rc) c->rc = rc;
+  }
+  static void CUDART_CB run_allreduce(void* p) {
+    Call* c = static_cast<Call*>(p);
+    const int rc = c->ops.allreduce_sum(c->ops.ctx, c->red, c->n);
+    if (rc) c->rc = rc;
+  }
   void allreduce_sum(double* d, int n, cudaStream_t s) override {
     if (nranks == 1 || n == 0) return;
+    if (ordered) {
+      check_async();
+      std::vector<int64_t> key{1, (int64_t)(uintptr_t)d, n};
+      Call*& c = calls[key];
+      if (!c) {
+        c = new Call;
+        c->ops = ops;
+        c->n = n;
+        c->red = reinterpret_cast<double*>(host_buf(sizeof(double) * n));
+      }
+      AMG_CK(cudaMemcpyAsync(c->red, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      AMG_CK(cudaLaunchHostFunc(s, run_allreduce, c));
+      AMG_CK(cudaMemcpyAsync(d, c->red, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      return;
+    }
     std::vector<double> h(n);
     AMG_CK(cudaMemcpyAsync(h.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     AMG_CK(cudaStreamSynchronize(s));
@@ -166,6 +229,26 @@ class HostComm : public CommBase {
   void send(const void* buf, size_t bytes, int peer, cudaStream_t) override { sends.push_back({nullptr, buf, bytes, peer}); }
   void recv(void* buf, size_t bytes, int peer, cudaStream_t) override { recvs.push_back({buf, nullptr, bytes, peer}); }
   void group_end(cudaStream_t s) override {
+    if (ordered) {
+      check_async();
+      std::vector<int64_t> key{2};
+      for (auto& m : sends) key.insert(key.end(), {0, (int64_t)(uintptr_t)m.sbuf, (int64_t)m.bytes, m.peer});
+      for (auto& m : recvs) key.insert(key.end(), {1, (int64_t)(uintptr_t)m.dbuf, (int64_t)m.bytes, m.peer});
+      Call*& c = calls[key];
+      if (!c) {
+        c = new Call;
+        c->ops = ops;
+        for (auto& m : sends) c->sp.push_back(m.peer), c->sb.push_back(host_buf(m.bytes)), c->sz.push_back((int64_t)m.bytes);
+        for (auto& m : recvs) c->rp.push_back(m.peer), c->rb.push_back(host_buf(m.bytes)), c->rz.push_back((int64_t)m.bytes);
+      }
+      for (size_t i = 0; i < sends.size(); ++i)
+        if (sends[i].bytes)
+          AMG_CK(cudaMemcpyAsync(const_cast<void*>(c->sb[i]), sends[i].sbuf, sends[i].bytes, cudaMemcpyDeviceToHost, s));
+      AMG_CK(cudaLaunchHostFunc(s, run_exchange, c));
+      for (size_t i = 0; i < recvs.size(); ++i)
+        if (recvs[i].bytes) AMG_CK(cudaMemcpyAsync(recvs[i].dbuf, c->rb[i], recvs[i].bytes, cudaMemcpyHostToDevice, s));
+      return;
+    }
     AMG_CK(cudaStreamSynchronize(s));  // the send buffers are complete
     std::vector<std::vector<char>> sh(sends.size()), rh(recvs.size());
     std::vector<int32_t> sp, rp;
@@ -188,11 +271,17 @@ class HostComm : public CommBase {
       if (recvs[i].bytes) AMG_CK(cudaMemcpyAsync(recvs[i].dbuf, rh[i].data(), recvs[i].bytes, cudaMemcpyHostToDevice, s));
     AMG_CK(cudaStreamSynchronize(s));
   }
-  void barrier() override { ck(ops.barrier(ops.ctx), "barrier"); }
+  void barrier() override {
+    check_async();
+    ck(ops.barrier(ops.ctx), "barrier");
+  }
+  bool capturable() const override { return ordered; }
 };
 
 CommBase* make_nccl_comm(const void* id128, int nranks, int rank) { return new NcclComm(id128, nranks, rank); }
-CommBase* make_host_comm(const HostOps& ops, int nranks, int rank) { return new HostComm(ops, nranks, rank); }
+CommBase* make_host_comm(const HostOps& ops, int nranks, int rank, bool ordered) {
+  return new HostComm(ops, nranks, rank, ordered);
+}
 CommBase* make_local_comm(LocalGroup* g, int rank) { return new LocalComm(g, rank); }
 
 }  // namespace amgb

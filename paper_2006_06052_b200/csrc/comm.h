@@ -77,7 +77,7 @@ struct HostOps {  // mirror of amg_host_comm_ops (amg.h)
 };
 
 CommBase* make_nccl_comm(const void* id128, int nranks, int rank);
-CommBase* make_host_comm(const HostOps& ops, int nranks, int rank);
+CommBase* make_host_comm(const HostOps& ops, int nranks, int rank, bool ordered);
 CommBase* make_local_comm(LocalGroup* g, int rank);
 
 }  // namespace amgb

@@ -576,17 +576,21 @@ int amg_comm_init_local(void* group, int32_t rank, struct amg_comm** out) {
   return AMG_OK;
 }
 
-int amg_comm_init_host(const amg_host_comm_ops* ops, int32_t nranks, int32_t rank, struct amg_comm** out) {
+int amg_comm_init_host(const amg_host_comm_ops* ops, int32_t nranks, int32_t rank, int32_t flags,
+                       struct amg_comm** out) {
   if (!ops || !out || nranks < 1 || rank < 0 || rank >= nranks || !ops->allreduce_sum || !ops->allgather_i64 ||
       !ops->exchange || !ops->barrier)
     return AMG_EINVAL;
   static_assert(sizeof(HostOps) == sizeof(amg_host_comm_ops), "HostOps mirrors amg_host_comm_ops");
   HostOps o;
   std::memcpy(&o, ops, sizeof(o));
+  AMG_GUARD_BEGIN
+  CommBase* cb = make_host_comm(o, nranks, rank, (flags & 1) != 0);
   amg_comm* c = new amg_comm;
-  c->c = make_host_comm(o, nranks, rank);
+  c->c = cb;
   *out = c;
   return AMG_OK;
+  AMG_GUARD_END
 }
 
 void amg_comm_destroy(struct amg_comm* c) {

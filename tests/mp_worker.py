@@ -35,11 +35,16 @@ def main():
     lp, lc, lv = gen.matrix(kind, n, None, bd[rank], bd[rank + 1])
     b = lv.shape[-1]
     bvec = gen.rhs(rk, n, b)
-    S = amg.Solver(amg.BSR.from_numpy(lp, lc, lv, n_block_cols=N), amg.default_params(**kw), comm=amg.Comm.host(),
-                   row_begin=bd[rank], n_global=N)
+    ordered = os.environ.get("MP_ORDERED", "0") == "1"  # stream-ordered host comm: CUDA graphs capture it
+    S = amg.Solver(amg.BSR.from_numpy(lp, lc, lv, n_block_cols=N), amg.default_params(**kw),
+                   comm=amg.Comm.host(ordered=ordered), row_begin=bd[rank], n_global=N)
     bl = torch.as_tensor(bvec[bd[rank] * b:bd[rank + 1] * b], device="cuda")
     x = torch.zeros_like(bl)
     rep = S.solve(bl, x, 1e-8)
+    x2 = torch.zeros_like(bl)
+    rep2 = S.solve(bl, x2, 1e-8)  # a second solve replays the captured graphs (ordered mode)
+    same = bool(torch.equal(x, x2)) and rep2.iters == rep.iters
+    graphs = S.counters()["graphs"]
     parts = [None] * P
     dist.all_gather_object(parts, (rep.iters, rep.converged, x.cpu().numpy(),
                                    [S.level_aggregates(l).tolist() for l in range(S.levels - 1)]))
@@ -60,7 +65,7 @@ def main():
             aggs_ok &= bool(np.array_equal(agg, oagg))
         print(json.dumps({"case": case, "P": P, "iters": [p[0] for p in parts], "converged": [p[1] for p in parts],
                           "relres": relres, "oracle_iters": ro.iters, "levels": S.levels, "oracle_levels": O.levels,
-                          "aggregates_equal": aggs_ok}), flush=True)
+                          "aggregates_equal": aggs_ok, "graphs": graphs, "replay_identical": same}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -23,13 +23,17 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("ordered", [0, 1], ids=["sync", "graphs"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("case", ["schur-gmres", "amg-bicgstab", "schur-idrs-ilut"])
-def test_multiprocess_solve(P, case):
+def test_multiprocess_solve(P, case, ordered):
+    # ordered = 1: the stream-ordered host communicator -- the preconditioner and Krylov-step
+    # CUDA graphs capture every halo exchange and allreduce, as with NCCL
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(P),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), case]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, MP_ORDERED=str(ordered))
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
@@ -37,6 +41,8 @@ def test_multiprocess_solve(P, case):
     assert d["relres"] <= 1e-8
     assert abs(d["iters"][0] - d["oracle_iters"]) <= 2, d
     assert d["levels"] == d["oracle_levels"] and d["aggregates_equal"], d
+    assert d["replay_identical"], d
+    assert (d["graphs"] > 0) == bool(ordered), d  # graphs exist exactly when the transport is capturable
 
 
 def test_bench_two_ranks_host_comm():
