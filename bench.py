@@ -326,7 +326,7 @@ def main():
     A = amg.BSR.from_numpy(ptr, col, val, n_block_cols=nrows)
     del val
     params = params_for(amg, args.cfg)
-    comm = (amg.Comm.host() if host_comm else amg.Comm(rank, world)) if world > 1 else None
+    comm = (amg.Comm.host(ordered=True) if host_comm else amg.Comm(rank, world)) if world > 1 else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     S = amg.Solver(A, params, comm=comm, row_begin=r0, n_global=nrows)
