@@ -79,6 +79,9 @@ CASES = [
     ("schur-v2-scalar-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1, schur_u_scalar=1)),
     ("schur-v2-scalar-f64", gen.STOKES, 12, gen.RHS_FORCE_NOISE, dict(solver=2, precond=1, schur_u_scalar=1,
                                                                       hier_dtype=0, vcycle_vec_dtype=0)),
+    # SURVEY §8(f) #4 on several ranks: the explicit PETSc-style S_hat and plain aggregation
+    ("schur-shat-full-gmres", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(solver=2, precond=1, schur_shat=2)),
+    ("schur-plain-agg-idrs", gen.STOKES, 16, gen.RHS_LID_NOISE, dict(solver=3, precond=1, coarsening=1)),
 ]
 
 
@@ -91,7 +94,8 @@ def test_dist_solve_parity(amg, P, name, kind, n, rk, kw):
     assert all(o[0].converged for o in out)
     assert relres <= 1e-8
     ok = {"solver": "solver", "precond": "precond", "coarse_enough": "coarse_enough", "smoother": "smoother",
-          "ilut_tau": "ilut_tau", "ilut_p": "ilut_p", "ilu_sweeps": "ilu_sweeps", "schur_u_scalar": "schur_u_scalar"}
+          "ilut_tau": "ilut_tau", "ilut_p": "ilut_p", "ilu_sweeps": "ilu_sweeps", "schur_u_scalar": "schur_u_scalar",
+          "schur_shat": "schur_shat", "coarsening": "coarsening"}
     op = oracle.default_params(nparts=P, hier_f32=int(kw.get("hier_dtype", 1) == 1),
                                vec_f32=int(kw.get("vcycle_vec_dtype", 1) == 1),
                                **{ok[k]: v for k, v in kw.items() if k in ok})
