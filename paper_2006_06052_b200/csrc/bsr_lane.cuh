@@ -139,21 +139,11 @@ struct EpiPreT<E, true> {
   using type = typename E::PreT;
 };
 
-// L2 prefetch of an epilogue operand (k_bsr_warp: the row's output lanes request their
-// f / x / M entries at the start, so the epilogue after the row's reduction finds them in L2)
-__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-template <class E, class = void>
-struct EpiPf : std::false_type {};
-template <class E>
-struct EpiPf<E, std::void_t<decltype(&E::template pf<1>)>> : std::true_type {};
-
 template <typename X>
 struct LEpiResidual {  // r = f - A x
   static constexpr int kDots = 0;
   const X* f;
   X* res;
-  template <int BR>
-  __device__ __forceinline__ void pf(int64_t o) const { pf_l2(f + o); }
   template <int BR>
   __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
     if (!L.valid) return;
@@ -178,12 +168,6 @@ struct LEpiSmooth {  // xo = x + M (f - A g), M block-diagonal; g the gathered v
   const X* f;
   const X* x;
   X* xo;
-  template <int BR>
-  __device__ __forceinline__ void pf(int64_t o) const {
-    pf_l2(f + o);
-    pf_l2(M + o * BR);
-    if (x) pf_l2(x + o);
-  }
   template <int BR>
   __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
     const int64_t o = (int64_t)L.row * BR + L.r;
@@ -295,8 +279,6 @@ struct LEpiSpmvM {  // f = A g (K6 restriction: g = r of the finer level), x = M
   const V* M;
   X* f;
   X* x;
-  template <int BR>
-  __device__ __forceinline__ void pf(int64_t o) const { pf_l2(M + o * BR); }
   template <int BR>
   __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
     const int64_t o = (int64_t)L.row * BR + L.r;
@@ -548,9 +530,6 @@ __global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restri
   constexpr int BE = BR * BC;
   const int lane = threadIdx.x & 31;
   const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if constexpr (EpiPf<EPI>::value) {
-    if (lane < BR && row < n) epi.template pf<BR>((int64_t)row * BR + lane);
-  }
   int k0 = 0, k1 = 0;
   if (row < n) k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
   double acc[BR] = {};
