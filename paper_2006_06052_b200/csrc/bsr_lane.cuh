@@ -565,6 +565,67 @@ __global__ void __launch_bounds__(256) k_bsr_warp(int n, const int32_t* __restri
   epi(L);
 }
 
+// Long rows on few rows (restrictions R_l into the coarse levels: 150-240 blocks per row on
+// 22-45 K rows; coarse A_l of 54-68 blocks): G warps share one block row, warp p taking the
+// 32-block chunks p, p + G, p + 2G, ... of it, so a row is one or two load steps deep instead
+// of G times that; the G butterfly sums meet in shared memory and warp 0 of the row adds them
+// in part order (deterministic) and runs the epilogue.  256 threads = 8 / G rows per CTA.
+template <int BR, int BC, int U, int G, typename V, typename X, bool FAST, class EPI>
+__global__ void __launch_bounds__(256) k_bsr_warps(int n, const int32_t* __restrict__ ptr,
+                                                   const int32_t* __restrict__ col, const V* __restrict__ val,
+                                                   const X* __restrict__ x, EPI epi) {
+  static_assert(G == 2 || G == 4 || G == 8, "k_bsr_warps: G in {2, 4, 8}");
+  constexpr int BE = BR * BC;
+  __shared__ double part[8][BR];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, p = w % G;
+  const int row = blockIdx.x * (8 / G) + w / G;
+  int k0 = 0, k1 = 0;
+  if (row < n) k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  double acc[BR] = {};
+  for (int kb = k0 + 32 * p + lane; kb < k1; kb += 32 * G * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (kb + 32 * G * u < k1) ? __ldg(col + kb + 32 * G * u) : -1;
+    X xv[U][BC];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) ld_x<BC>(x + (int64_t)c[u] * BC, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c[u] < 0) continue;
+#pragma unroll
+      for (int i = 0; i < BR; ++i) {
+        V a[BC];
+        ld_row<BC, false>(val + (int64_t)(kb + 32 * G * u) * BE + i * BC, a);
+        acc[i] += item_dot<BC, V, X, FAST>(a, xv[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BR; ++i)
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < BR; ++i) part[w][i] = acc[i];
+  __syncthreads();
+  if (p != 0) return;
+#pragma unroll
+  for (int i = 0; i < BR; ++i) {
+    double t = part[w][i];
+#pragma unroll
+    for (int q = 1; q < G; ++q) t += part[w + q][i];
+    acc[i] = t;
+  }
+  LaneRow<BR> L;
+  L.row = row;
+  L.r = lane < BR ? lane : 0;
+  L.base = 0;
+  L.valid = lane < BR && row < n;
+  L.yr = pick<BR>(acc, L.r);
+  epi(L);
+}
+
 // ---------------------------------------------------------------- sliced BSR
 // Long rows: the library's solve copy also holds a SLICED layout of the same blocks
 // (SELL-C with C = 32/B consecutive block rows per slice, one warp per slice, padded to

@@ -113,6 +113,7 @@ struct Mat {
   int tma_tr = 0, tma_ntiles = 0, tma_ns = 0, tma_stage = 0, tma_col_off = 0, tma_val_off = 0, tma_grid = 0;
   int tma_wave = 1, tma_part_off = 0, tma_max_blk = 0, tma_smem = 0;
   int lane_var = kLaneRC2;  // bsr_lane.cuh variant (make_tma_plan)
+  int warp_g = 1;           // kLaneW: warps per block row (k_bsr_warps; set_lane_plan, by row length)
   // sliced copy of the blocks (kLaneSell; bsr_lane.cuh k_bsr_sell), owned by the builder's arena
   int32_t sell_ns = 0;
   int32_t* sell_ptr = nullptr;  // [sell_ns + 1] step offsets

@@ -100,8 +100,15 @@ void set_lane_plan(Mat& A, bool use_env) {
   // very long rows, or long rows on a matrix too small to fill the GPU with row-lane
   // warps (coarse levels): one warp per row
   const double lane_warps = (double)A.n / (32 / std::max(br, 1));
-  if (per_row > 64.0 || (per_row > 12.0 && lane_warps < (double)kSMs * 64)) var = kLaneW;
+  if (per_row > 64.0 || (per_row > 12.0 && lane_warps < (double)env_int("AMG_LANEW_WARPS", kSMs * 64))) var = kLaneW;
   A.lane_var = use_env ? env_int("AMG_LANE_VAR", var) : var;
+  // warp-per-row matrices with long rows: G warps per row (k_bsr_warps), by the row length
+  // (one or two 32-block chunks per warp)
+  // and only where the level has at most one wave of row warps (n <= kSMs * 64: cfg 3 levels
+  // 2-3, cfg 5 level 3; on 44 K-row levels the split loses, cfg 5 895 -> 914 ms)
+  const int g = A.n > (int64_t)kSMs * 64 ? 1 : per_row >= 160.0 ? 8 : (per_row >= 80.0 ? 4 : (per_row >= 40.0 ? 2 : 1));
+  A.warp_g = use_env && env_int("AMG_WARP_G", 0) > 0 ? env_int("AMG_WARP_G", 0) : g;
+  if (A.warp_g != 1 && A.warp_g != 2 && A.warp_g != 4 && A.warp_g != 8) fail(AMG_EINVAL, "AMG_WARP_G: 1, 2, 4 or 8");
   // a forced sliced / interleaved variant needs its copy (make_tma_plan builds it)
   if ((A.lane_var == kLaneSell && !A.sell_ptr) || (A.lane_var == kLaneSellR && !A.sell_vptr)) A.lane_var = var;
 }
@@ -488,6 +495,20 @@ static void launch_lane(const Mat& A, const X* x, EPI epi, cudaStream_t s, int r
   }
   if (!A.val && A.nnz > 0)
     fail(AMG_EINVAL, "BSR values released: this matrix runs on its interleaved / sliced copy only");
+  if (A.lane_var == kLaneW && A.warp_g > 1) {
+    auto go = [&](auto Gc) {
+      constexpr int G = decltype(Gc)::value;
+      const unsigned grid = (unsigned)(((int64_t)A.n + 8 / G - 1) / (8 / G));
+      if (can_fast && A.fast32)
+        k_bsr_warps<BR, BC, 2, G, V, X, can_fast, EPI><<<grid, 256, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+      else
+        k_bsr_warps<BR, BC, 2, G, V, X, false, EPI><<<grid, 256, 0, s>>>(A.n, A.ptr, A.col, (const V*)A.val, x, epi);
+    };
+    if (A.warp_g == 2) go(std::integral_constant<int, 2>{});
+    else if (A.warp_g == 4) go(std::integral_constant<int, 4>{});
+    else go(std::integral_constant<int, 8>{});
+    return;
+  }
   if (A.lane_var == kLaneW) {
     const unsigned grid = grid_for((int64_t)A.n * 32, kBlock);
     if (can_fast && A.fast32)
