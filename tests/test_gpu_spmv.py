@@ -225,6 +225,45 @@ def test_spmv_lane_variants(amg, rng, envvars, var, b):
         assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (var, b, vt, xt, yt)
 
 
+def _long_rows_bsr(rng, n, b):
+    """a few hundred rows of 0..300 blocks (the coarse restrictions' shape: R_l rows of
+    150-240 blocks on a few hundred coarse rows), empty rows included"""
+    ptr = np.zeros(n + 1, np.int32)
+    cols = []
+    for i in range(n):
+        L = 0 if i % 11 == 5 else int(rng.integers(1, 301))
+        c = np.sort(rng.choice(4 * n, size=L, replace=False)) if L else np.zeros(0, int)
+        cols.append(c)
+        ptr[i + 1] = ptr[i] + L
+    col = np.concatenate(cols).astype(np.int32)
+    return ptr, col, rng.standard_normal((len(col), b, b))
+
+
+@pytest.mark.parametrize("g", [1, 2, 4, 8])
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_spmv_warps_per_row(amg, rng, envvars, g, b):
+    # warp-per-row kernel with G warps per block row (k_bsr_warps): G partial sums per row
+    # meet in shared memory; a ragged last CTA (n not a multiple of 8 / G rows)
+    envvars(AMG_LANE_VAR=6, AMG_WARP_G=g)
+    n = 301
+    ptr, col, val = _long_rows_bsr(rng, n, b)
+    m = 4 * n
+    x = rng.uniform(-1, 1, m * b)
+    y0 = rng.standard_normal(n * b)
+    tdt = {amg.F32: torch.float32, amg.F64: torch.float64}
+    for vt, xt, yt in ((0, 0, 0), (1, 0, 0), (1, 1, 1)):
+        A = amg.BSR.from_numpy(ptr, col, val, dtype=tdt[vt], n_block_cols=m)
+        xd = torch.as_tensor(x).to("cuda", tdt[xt])
+        yd = torch.as_tensor(y0).to("cuda", tdt[yt])
+        amg.bsr_spmv(A, xd, yd, -0.5, 2.0)
+        y = yd.double().cpu().numpy()
+        vv = _r32(val) if vt == amg.F32 else val
+        xx = _r32(x) if xt == amg.F32 else x
+        yy = _r32(y0) if yt == amg.F32 else y0
+        ref = oracle.spmv(oracle.Mat.from_arrays(ptr, col, vv, n_cols=m), xx, -0.5, 2.0, yy)
+        assert _relerr(y, ref) <= (1e-12 if yt == amg.F64 else 2e-7), (g, b, vt, xt, yt)
+
+
 @pytest.mark.parametrize("b", [2, 3, 4])
 def test_spmv_sliced_copy(amg, rng, envvars, b):
     # force the sliced copy (k_bsr_sell) on a small ragged matrix: empty, short and long
