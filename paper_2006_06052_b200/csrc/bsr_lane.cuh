@@ -201,6 +201,64 @@ struct LEpiSmooth {  // xo = x + M (f - A g), M block-diagonal; g the gathered v
   }
 };
 
+// The last post-smoothing step of the Schur preconditioner's second U-solve with the join
+// (K9') in its epilogue: xo = x + M (f - A x) is stored straight into the output z as the
+// velocity slots of the interleaved (u, v, w, p) cells, with p[row] in slot 3 -- the values
+// LEpiSmooth + k_join4 would store (same expressions), without the u round trip
+template <typename V, typename X, typename Z>
+struct LEpiSmoothJoin {
+  static constexpr int kDots = 0;
+  const V* M;
+  const X* f;
+  const X* x;
+  const X* p;
+  Z* z;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    static_assert(BR == 3, "join: 3 velocity components + p");
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    const double res = L.valid ? (double)f[o] - L.yr : 0.0;
+    double rv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = __shfl_sync(kFull, res, L.base + c);
+    if (!L.valid) return;
+    double m[BR];
+    load_b<BR, false>(M + o * BR, m);
+    double t = m[0] * rv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], rv[c], t);
+    const X u = to_out<X>((double)x[o] + t);
+    z[(int64_t)L.row * 4 + L.r] = (Z)u;
+    if (L.r == 0) z[(int64_t)L.row * 4 + 3] = (Z)p[L.row];
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    static_assert(BR == 3, "join: 3 velocity components + p");
+    const int64_t o = (int64_t)row * BR;
+    double rv[BR], xv[BR], m[BR][BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = (double)f[o + c] - yr[c], xv[c] = (double)x[o + c];
+    const X pv = p[row];
+#pragma unroll
+    for (int i = 0; i < BR; ++i) load_b<BR, false>(M + (o + i) * BR, m[i]);
+    X u[BR];
+#pragma unroll
+    for (int i = 0; i < BR; ++i) {
+      double t = m[i][0] * rv[0];
+#pragma unroll
+      for (int c = 1; c < BR; ++c) t = fma(m[i][c], rv[c], t);
+      u[i] = to_out<X>(xv[i] + t);
+    }
+    if constexpr (std::is_same_v<Z, float>) {
+      reinterpret_cast<float4*>(z)[row] = make_float4((float)u[0], (float)u[1], (float)u[2], (float)pv);
+    } else {
+      double2* q = reinterpret_cast<double2*>(z + (int64_t)row * 4);
+      q[0] = make_double2((double)u[0], (double)u[1]);
+      q[1] = make_double2((double)u[2], (double)pv);
+    }
+  }
+};
+
 template <typename V, typename X>
 struct LEpiSchurP {  // p = m_S o (r_p - B u*)      (1 x nu blocks)
   static constexpr int kDots = 0;

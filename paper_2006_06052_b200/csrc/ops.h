@@ -88,6 +88,9 @@ void launch_mask_split(int32_t nu, int32_t np, const int32_t* uidx, const int32_
                        double scale, void* ru, void* rp, int xt, cudaStream_t s, const double* scale_dev = nullptr);
 void launch_mask_join(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const void* u, const void* p,
                       int xt, void* z, int zt, cudaStream_t s);
+bool smooth_join_ok(const Mat& A, int xt);
+void launch_smooth_join(const Mat& A, const void* M, const void* f, const void* x, const void* p, void* z, int zt,
+                        int xt, cudaStream_t s, int r0 = 0, int r1 = -1);
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt,
                  cudaStream_t s);
 // convert a whole vector between dtypes (narrowing RNE / exact widening); scale applied in fp64

@@ -159,7 +159,14 @@ void* level_f_slab(Handle& h, size_t l);
 // vcycle.cu
 // V-cycle from level `level` on that level's f buffer; returns the buffer holding x
 // pre_done: level `level`'s x = M f was already formed by the producer of f (fused K4a)
-void* vcycle_run(Handle& h, size_t level, cudaStream_t s, bool pre_done = false);
+// join target of the Schur apply's second U-solve (K9' fused into its last post-smoothing step)
+struct JoinOut {
+  const void* p;
+  void* z;
+  int zt;
+};
+// returns the level's x, or nullptr when `jo` was honoured (z written)
+void* vcycle_run(Handle& h, size_t level, cudaStream_t s, bool pre_done = false, const JoinOut* jo = nullptr);
 // can the producer of level l's f also form x = M f (fused K4a)?
 bool fuse_presmooth(const Handle& h, size_t level);
 void* level0_f(Handle& h);

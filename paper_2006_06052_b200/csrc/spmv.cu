@@ -702,6 +702,34 @@ void launch_smooth(const Mat& A, const void* M, const void* f, const void* x, vo
   launch_smooth_g("smooth", A, M, f, x, x, xo, xt, s, r0, r1);
 }
 
+// K5 + K9': the second U-solve's last post-smoothing step writes z = join(u, p) directly
+// (LEpiSmoothJoin; 3x3 fp32 velocity levels of the interleaved 4x4 Stokes layout)
+bool smooth_join_ok(const Mat& A, int xt) { return A.b == 3 && A.br == 0 && A.bc == 0 && A.tma_grid == 0 && xt == AMG_F32; }
+
+void launch_smooth_join(const Mat& A, const void* M, const void* f, const void* x, const void* p, void* z, int zt,
+                        int xt, cudaStream_t s, int r0, int r1) {
+  if (!smooth_join_ok(A, xt)) fail(AMG_EINVAL, "fused smooth + join: 3x3 fp32 velocity level only");
+  if (r1 < 0) r1 = A.n;
+  if (A.n == 0 || r1 <= r0) return;
+  const double frac = (double)(r1 - r0) / A.n;
+  // matrix, M, f and x read, x gathered (once: g == x), p read, z written
+  ProfScope ps_(prof_name("smooth_join", A.b, A.vt, zt),
+                frac * (mat_bytes(A) + (double)A.n * 9 * dtype_size(A.vt) + (double)A.n * 3 * 4 +
+                        (double)A.m * 3 * 4 + (double)A.n * 4 + (double)A.n * 4 * dtype_size(zt)),
+                s);
+  dispatch_t(A.vt, [&](auto v) {
+    using V = decltype(v);
+    dispatch_t(zt, [&](auto zz) {
+      using Z = decltype(zz);
+      launch_lane<3, 3, V, float>(
+          A, (const float*)x,
+          LEpiSmoothJoin<V, float, Z>{(const V*)M, (const float*)f, (const float*)x, (const float*)p, (Z*)z}, s, r0,
+          r1);
+    });
+  });
+  AMG_CK_LAUNCH();
+}
+
 void launch_ilu_usweep(const Mat& U, const void* Dinv, const void* y, const void* z, const void* xb, void* xo, int xt,
                        cudaStream_t s) {
   launch_smooth_g("ilu_u", U, Dinv, y, z, xb, xo, xt, s, 0, -1);

@@ -47,7 +47,7 @@ bool fuse_presmooth(const Handle& h, size_t l) {
   return h.p.fused_presmooth && l < h.lv.size() && !h.lv[l].Lf.ptr && !(h.comm && l >= h.rep_from);
 }
 
-void* vcycle_run(Handle& h, size_t l, cudaStream_t s, bool pre_done) {
+void* vcycle_run(Handle& h, size_t l, cudaStream_t s, bool pre_done, const JoinOut* jo) {
   const int xt = h.xt, vt = h.vt;
   if (h.comm && l == h.rep_from) replicated_allgather(h, l, s);  // distributed: replicated from here on
   if (l == h.lv.size()) {
@@ -82,11 +82,24 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s, bool pre_done) {
       ilu_step(h, L, x, s);
       continue;
     }
+    if (jo && k == h.p.npost - 1 && smooth_join_ok(L.A, xt)) {  // + K9' (the caller's join)
+      halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s, [&](int r0, int r1) {
+        launch_smooth_join(L.A, L.M, L.f, x, jo->p, jo->z, jo->zt, xt, s, r0, r1);
+      });
+      return nullptr;
+    }
     halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s,
                     [&](int r0, int r1) { launch_smooth(L.A, L.M, L.f, x, t, xt, s, r0, r1); });
     std::swap(x, t);
   }
   return x;
+}
+
+// is the Schur apply's join fused into the second U-solve's last post-smoothing step?
+static bool join_fused(const Handle& h) {
+  return h.schur && !h.masked && h.amg_active && !h.lv.empty() && h.b == 4 && h.pc == 3 && h.p.npost >= 1 &&
+         !h.lv[0].Lf.ptr && !(h.comm && h.rep_from == 0) && smooth_join_ok(h.lv[0].A, h.xt) &&
+         !env_int("AMG_NO_JOIN_FUSE", 0);
 }
 
 // z = M r.  Monolithic AMG: narrow r once (RNE), V-cycle, widen exactly (C9).
@@ -134,8 +147,9 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   // one of level 0's x / t buffers) is dead after K10, so x_0 may be overwritten here.
   const bool fu = fs && launch_schur_u_M(h.BTm, f0, h.pp, f0, M0, h.vt, x0, h.xt, s);
   if (!fu) launch_schur_u(h.BTm, f0, h.pp, f0, h.xt, s);
-  void* u = vcycle_run(h, 0, s, fu);                                                           // u = V(r_u')
-  launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                        // K9'
+  const JoinOut jo{h.pp, z, zt};
+  void* u = vcycle_run(h, 0, s, fu, join_fused(h) ? &jo : nullptr);                           // u = V(r_u')
+  if (u) launch_join(h.n, h.b, h.pc, u, h.pp, h.xt, z, zt, s);                                 // K9'
 }
 
 // The same application replayed from a CUDA graph: one graph per (r, z, zt, scale_dev)
@@ -237,6 +251,7 @@ double precond_bytes(const Handle& h) {
   t += nnz * (4.0 + 3.0 * sv) + 4.0 * (n + 1) + n * sv + n * 3 * sx + 2 * n * sx;  // K10
   t += nnz * (4.0 + 3.0 * sv) + 4.0 * (n + 1) + n * sx + 6.0 * n * sx;           // K11
   t += (double)N * sx + (double)N * 8.0;                        // join
+  if (join_fused(h)) t -= 6.0 * n * sx;                         // fused: no u write / u read
   return t;
 }
 

@@ -748,3 +748,38 @@ def test_fused_presmooth_bit_identical(amg, envvars, rng, kind, n, kw, h32, env)
     assert np.array_equal(z1, z0)
     assert np.array_equal(x1, x0) and i1 == i0
     assert k1 < k0_, (k1, k0_)
+
+
+@pytest.mark.parametrize("n,kw,env", [
+    (16, dict(precond=1, solver=2), {}),                                # GMRES: z stored fp32
+    (24, dict(precond=1, solver=2), dict(AMG_SELLR_MIN_SLICES=1)),      # level 0 on the interleaved copy
+    (24, dict(precond=1, solver=2), dict(AMG_SELLR=0)),                 # level 0 on the row lanes
+    (16, dict(precond=1, solver=1), {}),                                # BiCGStab: z fp64
+    (16, dict(precond=1, solver=2, npost=2), {}),                       # the last of two post-smoothing steps
+], ids=["gmres", "sellr", "lanes", "bicgstab", "npost2"])
+def test_fused_join_bit_identical(amg, envvars, rng, n, kw, env):
+    # the Schur preconditioner's join z = (u, p) written by the second
+    # U-solve's last post-smoothing step -- the same output and solve bit for bit as the
+    # separate K9' pass, one kernel fewer per application
+    envvars(**env)
+    ptr, col, val = gen.matrix(gen.STOKES, n)
+    N = (len(ptr) - 1) * 4
+    r = torch.as_tensor(rng.standard_normal(N), device="cuda")
+    bvec = gen.rhs(gen.RHS_LID_NOISE, n, 4)
+    out = []
+    for off in (0, 1):
+        envvars(AMG_NO_JOIN_FUSE=off)
+        A = amg.BSR.from_numpy(ptr, col, val)
+        S = amg.Solver(A, amg.default_params(hier_dtype=amg.F32, vcycle_vec_dtype=amg.F32, **kw))
+        z = torch.zeros(N, dtype=torch.float64, device="cuda")
+        k0 = amg.kernel_launches()
+        S.apply_precond(r, z)
+        torch.cuda.synchronize()
+        k = amg.kernel_launches() - k0
+        x, rep = _solve(amg, S, bvec)
+        out.append((z.cpu().numpy(), k, x, rep.iters, rep.alg_bytes))
+    (z1, k1, x1, i1, b1), (z0, k0_, x0, i0, b0) = out
+    assert np.array_equal(z1, z0)
+    assert np.array_equal(x1, x0) and i1 == i0
+    assert k1 == k0_ - 1, (k1, k0_)
+    assert b1 < b0
