@@ -101,9 +101,10 @@ typedef struct {
   double over_interp;        /* AMG_PLAIN_AGG: A_c = (1/over_interp) P^T A P, default 1.5
                                 (over-interpolation, reading R19); ignored for AMG_SA */
   int32_t ilu_sweeps;        /* AMG_ILU0 / AMG_ILUT: Jacobi sweeps per triangular solve, 1..16, default 2 */
-  int32_t gmres_ortho;       /* AMG_GMRES orthogonalisation: 2 (default) two-pass Gram/Cholesky with the
-                                first pass's dots on an fp32 shadow of the basis (R23; +31 fp32
-                                vectors of workspace); 1 two-pass Gram/Cholesky on the fp64 basis (R22);
+  int32_t gmres_ortho;       /* AMG_GMRES orthogonalisation: 3 (default) two-pass Gram/Cholesky with the
+                                first pass's dots on an fp16 shadow of the basis at unit-rms scale
+                                (R28; +31 fp16 vectors of workspace); 2 the same with an fp32
+                                shadow (R23; +31 fp32 vectors); 1 two-pass Gram/Cholesky on the fp64 basis (R22);
                                 0 CGS2 (three passes over the basis per step).  1 and 2 reorthogonalise a
                                 step whose new direction is still far from orthogonal (R22 safeguard) */
   int32_t fused_presmooth;   /* 1 (default): the pre-smoothing from zero x = M f (K4a) runs in the epilogue of

@@ -193,6 +193,15 @@ static double dot_f32_basis(const vector<double>& a, const vector<double>& b) {
   return s;
 }
 
+// gmres_ortho = 3 (reading R28): the unit basis vector a scaled to unit rms (x sqrt(N)), rounded
+// to IEEE binary16 (RNE, gradual underflow), scaled back
+static double dot_f16_basis(const vector<double>& a, const vector<double>& b) {
+  const double sq = std::sqrt((double)a.size());
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s = s + ((double)(_Float16)(a[i] * sq) / sq) * b[i];
+  return s;
+}
+
 // ---------------------------------------------------------------- block helpers
 // Frobenius norm squared, row-major order (C2 reading: Frobenius).
 static double fro2(const double* a, int b) {
@@ -1612,8 +1621,11 @@ static int solve_gmres(const orc_solver& s, const double* bp, double* xp, double
         // R(j+1, j+1) = sqrt(1 - |R(0:j, j+1)|^2); H(:, j) = h + ||w1|| R(:, j+1).
         const int k = j + 1;
         vector<double> p(k), hv(k), cv(k), qv(k), h2v(k);
-        // pass 1; gmres_ortho = 2 (reading R23): the dots read the basis rounded to fp32
-        for (int i = 0; i < k; ++i) p[i] = s.p.gmres_ortho == 2 ? dot_f32_basis(V[i], w) : dot(V[i], w);
+        // pass 1; gmres_ortho = 2 (reading R23): the dots read the basis rounded to fp32;
+        // 3 (R28): rounded to fp16 at unit-rms scale
+        for (int i = 0; i < k; ++i)
+          p[i] = s.p.gmres_ortho == 2 ? dot_f32_basis(V[i], w)
+                 : s.p.gmres_ortho == 3 ? dot_f16_basis(V[i], w) : dot(V[i], w);
         // project(pin): hout = R^-T pin, cv = R^-1 hout, w = w - t cv, qv = t^T w
         auto project = [&](const vector<double>& pin, vector<double>& hout) {
           for (int i = 0; i < k; ++i) {

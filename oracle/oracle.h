@@ -56,7 +56,8 @@ typedef struct {
   double over_interp;    /* plain aggregation: A_c = (1/over_interp) P^T A P (reading R19, 1.5) */
   int32_t ilu_sweeps;    /* ORC_ILU0 / ORC_ILUT: Jacobi sweeps per triangular solve (>= 1, default 2, R20) */
   int32_t gmres_ortho;   /* GMRES orthogonalisation: 0 CGS2 (default), 1 two-pass Gram/Cholesky
-                            (R22), 2 the same with the first pass's dots on the fp32-rounded basis (R23) */
+                            (R22), 2 the same with the first pass's dots on the fp32-rounded basis (R23),
+                            3 on the fp16-rounded basis at unit-rms scale (R28) */
   double ilut_tau;       /* ORC_ILUT drop tolerance relative to the row's 2-norm (1e-2) */
   int32_t ilut_p;        /* ORC_ILUT fill entries kept per row in each of L and U (2) */
 } orc_params;

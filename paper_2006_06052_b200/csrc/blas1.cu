@@ -6,6 +6,8 @@
 #include "comm.h"
 #include "prof.h"
 
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
@@ -79,44 +81,73 @@ __device__ __forceinline__ void reduce_finish(double (&acc)[K], int kout, double
 // (v_j = s_j V_j: the basis is stored unnormalised with device scales sc)
 // TV: element type of the basis as read (double; float for the fp32 shadow copy the GMRES
 // pass-1 multi-dot of reading R23 reads); wf (MODE 3, optional): fp32 copy of w_out
-template <int K, int MODE, typename TV = double>
+// the shadow copy of w_out written by MODE 3: fp32 as is (R23), or fp16 scaled by sig (R28:
+// sig = sqrt(N) / ||w||, the pre-update norm, so every entry of the shadow is <= sqrt(N) in
+// magnitude and its rms is ||w_out|| / ||w|| <= 1)
+template <typename WF>
+__device__ __forceinline__ WF to_shadow(double v, double sig) {
+  if constexpr (std::is_same_v<WF, __half>) return __double2half(v * sig);
+  else return (float)v;
+}
+
+template <int K, int MODE, typename TV = double, typename WF = float>
 __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double* __restrict__ sc,
                                              const double* __restrict__ coef, const double* w, double* w_out,
                                              double* partials, unsigned* ticket, double* out, int post,
-                                             double* inv, float* wf) {
+                                             double* inv, WF* wf) {
   constexpr int U = cgs_unroll<K>();
   __shared__ double c[K], sv[K];
+  __shared__ double sig;
   if (threadIdx.x < K) {
     sv[threadIdx.x] = sc ? sc[threadIdx.x] : 1.0;
     c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
   }
+  if (threadIdx.x == 0) sig = (MODE == 3 && std::is_same_v<WF, __half> && wf) ? coef[K] : 1.0;
   __syncthreads();
   constexpr int KA = (MODE == 2) ? 1 : (MODE == 3 ? K + 1 : K);
   double acc[KA];
 #pragma unroll
   for (int j = 0; j < KA; ++j) acc[j] = 0.0;
-  if constexpr (MODE == 0 && std::is_same_v<TV, float>) {
+  if constexpr (MODE == 0 && (std::is_same_v<TV, float> || std::is_same_v<TV, __half>)) {
     // fp32 shadow basis (reading R23): four consecutive elements per thread, one 16-byte load
-    // per vector (the scalar form kept one 4-byte load per vector in flight: 2-4 TB/s)
+    // per vector (the scalar form kept one 4-byte load per vector in flight: 2-4 TB/s); the
+    // fp16 shadow (R28): the same four elements in one 8-byte load
     const int64_t n4 = n / 4;
     for (int64_t i4 = (int64_t)blockIdx.x * kTM + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * kTM) {
-      float4 raw[K];
+      if constexpr (std::is_same_v<TV, float>) {
+        float4 raw[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j) raw[j] = __ldcs(reinterpret_cast<const float4*>(V.p[j]) + i4);
-      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
-      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+        for (int j = 0; j < K; ++j) raw[j] = __ldcs(reinterpret_cast<const float4*>(V.p[j]) + i4);
+        const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
+        const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        acc[j] = fma((double)raw[j].x, w0.x, acc[j]);
-        acc[j] = fma((double)raw[j].y, w0.y, acc[j]);
-        acc[j] = fma((double)raw[j].z, w1.x, acc[j]);
-        acc[j] = fma((double)raw[j].w, w1.y, acc[j]);
+        for (int j = 0; j < K; ++j) {
+          acc[j] = fma((double)raw[j].x, w0.x, acc[j]);
+          acc[j] = fma((double)raw[j].y, w0.y, acc[j]);
+          acc[j] = fma((double)raw[j].z, w1.x, acc[j]);
+          acc[j] = fma((double)raw[j].w, w1.y, acc[j]);
+        }
+      } else {  // fp16: widen each vector's four values as its load is consumed
+        uint2 hr[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) hr[j] = __ldcs(reinterpret_cast<const uint2*>(V.p[j]) + i4);
+        const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
+        const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].y));
+          acc[j] = fma((double)a.x, w0.x, acc[j]);
+          acc[j] = fma((double)a.y, w0.y, acc[j]);
+          acc[j] = fma((double)b.x, w1.x, acc[j]);
+          acc[j] = fma((double)b.y, w1.y, acc[j]);
+        }
       }
     }
     for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
       const double wi = w[i];
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc[j] = fma((double)reinterpret_cast<const TV*>(V.p[j])[i], wi, acc[j]);
+      for (int j = 0; j < K; ++j) acc[j] = fma((double)(float)reinterpret_cast<const TV*>(V.p[j])[i], wi, acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) acc[j] *= sv[j];
@@ -165,7 +196,7 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
 #pragma unroll
         for (int j = 0; j < K; ++j) v = fma(-c[j], vv[u][j], v);
         if (i < n) w_out[i] = v;
-        if (MODE == 3 && wf && i < n) wf[i] = (float)v;
+        if (MODE == 3 && wf && i < n) wf[i] = to_shadow<WF>(v, sig);
         if constexpr (MODE == 1 || MODE == 3) {
 #pragma unroll
           for (int j = 0; j < K; ++j) acc[j] = fma(sv[j] * vv[u][j], v, acc[j]);
@@ -217,20 +248,22 @@ __device__ __forceinline__ void finish_partials(int kout, double* partials, unsi
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-template <int NJ, int MODE, typename TV = double>
+template <int NJ, int MODE, typename TV = double, typename WF = float>
 __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V, const double* __restrict__ sc,
                                                      const double* __restrict__ coef, const double* w, double* w_out,
                                                      double* partials, unsigned* ticket, double* out, int post,
-                                                     double* inv, float* wf) {
+                                                     double* inv, WF* wf) {
   constexpr int T = kCW / 32;  // elements per lane per chunk
   __shared__ double c[32], sv[32];
   __shared__ double part[8][kCW + 1];
-  __shared__ double vs[kCW];
+  __shared__ __align__(16) double vs[kCW];
+  __shared__ double sig;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < k) {
     sv[threadIdx.x] = sc ? sc[threadIdx.x] : 1.0;
     c[threadIdx.x] = (MODE == 0) ? 0.0 : coef[threadIdx.x] * sv[threadIdx.x];
   }
+  if (threadIdx.x == 0) sig = (MODE == 3 && std::is_same_v<WF, __half> && wf) ? coef[k] : 1.0;
   __syncthreads();
   const TV* vp[NJ];
   bool own[NJ];
@@ -336,7 +369,7 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
 #pragma unroll
       for (int ww = 0; ww < 8; ++ww) v -= part[ww][threadIdx.x];
       if (it < n) w_out[it] = v;
-      if (MODE == 3 && wf && it < n) wf[it] = (float)v;
+      if (MODE == 3 && wf && it < n) wf[it] = to_shadow<WF>(v, sig);
       if constexpr (MODE == 2 || MODE == 3) nrm = fma(v, v, nrm);
       if constexpr (MODE != 2) {
         vs[threadIdx.x] = v;
@@ -387,6 +420,73 @@ __global__ void __launch_bounds__(kTW, 2) k_cgs_wide(int64_t n, int k, PtrList V
   }
 }
 
+// R28's pass-1 multi-dot for k > 12: out[j] = ms_j (h_j . w) over the fp16 shadows h_j, the
+// wide kernel's layout (warp w owns vectors w + 8q; lane owns elements i0 + 128 hh + 4 lane +
+// e of each 256-element chunk, one 8-byte load per vector and hh) at <= 64 registers so that
+// more blocks per SM keep the loads in flight (the shared template held 107 registers and ran
+// two blocks per SM: 3-4.5 TB/s; this one 5.2-6.3 at 8 blocks per SM)
+template <int NJ>
+__global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrList V, const double* __restrict__ ms,
+                                                        const double* w, double* partials, unsigned* ticket,
+                                                        double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const __half* vp[NJ];
+  bool own[NJ];
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) {
+    const int j = warp + 8 * q;
+    own[q] = j < k;
+    vp[q] = reinterpret_cast<const __half*>(own[q] ? V.p[j] : V.p[0]);
+  }
+  double acc[NJ];
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) acc[q] = 0.0;
+  for (int64_t i0 = (int64_t)blockIdx.x * kCW; i0 < n; i0 += (int64_t)gridDim.x * kCW) {
+    if (i0 + kCW <= n) {
+      uint2 hr[NJ][2];
+#pragma unroll
+      for (int q = 0; q < NJ; ++q)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) hr[q][hh] = __ldcs(reinterpret_cast<const uint2*>(vp[q] + i0 + 128 * hh + 4 * lane));
+      double2 wv[2][2];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) wv[hh][e] = __ldg(reinterpret_cast<const double2*>(w + i0 + 128 * hh + 4 * lane) + e);
+#pragma unroll
+      for (int q = 0; q < NJ; ++q)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hr[q][hh].x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hr[q][hh].y));
+          acc[q] = fma((double)a.x, wv[hh][0].x, acc[q]);
+          acc[q] = fma((double)a.y, wv[hh][0].y, acc[q]);
+          acc[q] = fma((double)b.x, wv[hh][1].x, acc[q]);
+          acc[q] = fma((double)b.y, wv[hh][1].y, acc[q]);
+        }
+    } else {
+      for (int hh = 0; hh < 2; ++hh)
+        for (int e = 0; e < 4; ++e) {
+          const int64_t i = i0 + 128 * hh + 4 * lane + e;
+          if (i < n) {
+            const double wi = w[i];
+#pragma unroll
+            for (int q = 0; q < NJ; ++q) acc[q] = fma((double)__half2float(vp[q][i]), wi, acc[q]);
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) {
+    double v = own[q] ? acc[q] : 0.0;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    const int j = warp + 8 * q;
+    if (lane == 0 && own[q]) partials[(int64_t)j * gridDim.x + blockIdx.x] = v * ms[j];
+  }
+  finish_partials(k, partials, ticket, out, 0, nullptr);
+}
+
 template <int K = 1, class F>
 void dispatch_k(int k, F&& f) {
   if (k == K) f(std::integral_constant<int, K>{});
@@ -394,35 +494,48 @@ void dispatch_k(int k, F&& f) {
   else fail(AMG_EINVAL, "multi-vector kernels take 1..32 vectors");
 }
 
-template <int MODE, typename TV = double>
+template <int MODE, typename TV = double, typename WF = float>
 void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const double* coef, const double* w,
                 double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s,
-                float* wf = nullptr) {
+                WF* wf = nullptr) {
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
-  const int wide_from = env_int("AMG_CGS_WIDE", 13);  // first k served by k_cgs_wide (tests force both)
+  // first k served by the wide kernels (tests force both); the fp16 multi-dot from k = 11 (the
+  // K-templated kernel ran k = 11 / 12 at 4.8 / 3.2 TB/s)
+  const int wide_from = env_int("AMG_CGS_WIDE", (MODE == 0 && std::is_same_v<TV, __half>) ? 11 : 13);
   if (k >= wide_from) {
     const int64_t work = (n + kCW - 1) / kCW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * kSMs, (int64_t)kMaxPartials, work}));
     auto go = [&](auto kern) {
       kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
     };
-    if (k <= 16) go(k_cgs_wide<2, MODE, TV>);
-    else if (k <= 24) go(k_cgs_wide<3, MODE, TV>);
-    else go(k_cgs_wide<4, MODE, TV>);
+    if constexpr (MODE == 0 && std::is_same_v<TV, __half>) {  // R28: the fp16 multi-dot
+      const int g16 = (int)std::max<int64_t>(
+          1, std::min<int64_t>({(int64_t)env_int("AMG_F16_BLOCKS", 8) * kSMs, (int64_t)kMaxPartials, work}));
+      auto go16 = [&](auto kern) { kern<<<g16, kTW, 0, s>>>(n, k, V, sc, w, partials, ticket, out); };
+      if (k <= 16) go16(k_mdot16_wide<2>);
+      else if (k <= 24) go16(k_mdot16_wide<3>);
+      else go16(k_mdot16_wide<4>);
+      AMG_CK_LAUNCH();
+      return;
+    } else {
+      if (k <= 16) go(k_cgs_wide<2, MODE, TV, WF>);
+      else if (k <= 24) go(k_cgs_wide<3, MODE, TV, WF>);
+      else go(k_cgs_wide<4, MODE, TV, WF>);
+    }
     AMG_CK_LAUNCH();
     return;
   }
   dispatch_k(k, [&](auto Kc) {
     constexpr int K = decltype(Kc)::value;
     constexpr int U = cgs_unroll<K>();
-    static int occ = 0;  // per (K, MODE, TV) instantiation
+    static int occ = 0;  // per (K, MODE, TV, WF) instantiation
     if (occ == 0) {
-      AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, MODE, TV>, kTM, 0));
+      AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, MODE, TV, WF>, kTM, 0));
       occ = std::max(occ, 1);
     }
     const int64_t work = (n + (int64_t)kTM * U - 1) / ((int64_t)kTM * U);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)occ * kSMs, (int64_t)kMaxPartials, work}));
-    k_cgs<K, MODE, TV><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
+    k_cgs<K, MODE, TV, WF><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
   });
   AMG_CK_LAUNCH();
 }
@@ -576,15 +689,46 @@ void launch_mdot_scaled_f32(int64_t n, int k, const PtrList& Vf, const double* s
   finalize_global(comm, out, k, false, s);
 }
 
+void launch_mdot_scaled_f16(int64_t n, int k, const PtrList& Vh, const double* ms, const double* w, double* partials,
+                            double* out, cudaStream_t s, CommBase* comm) {
+  ProfScope ps_(prof_name("mdot", k, AMG_F16, -1), 2.0 * n * k + 8.0 * n, s);
+  launch_cgs<0, __half>(n, k, Vh, ms, nullptr, w, nullptr, partials, out, 0, nullptr, s);
+  finalize_global(comm, out, k, false, s);
+}
+
+// dst = fp16(src * sig), sig the power of two at or below mul * *s_dev (the fp16 shadow of V_0 at
+// about unit rms: mul = sqrt(N), s_dev = 1 / ||V_0||); *m_out = *s_dev / sig
+__global__ void k_to_half_scaled(int64_t n, const double* __restrict__ src, const double* __restrict__ s_dev,
+                                 double mul, __half* __restrict__ dst, double* m_out) {
+  int e = 0;
+  frexp(mul * *s_dev, &e);
+  const double sig = ldexp(1.0, e - 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = *s_dev / sig;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT)
+    dst[i] = __double2half(src[i] * sig);
+}
+
+void launch_to_half_scaled(int64_t n, const double* src, const double* s_dev, double mul, void* dst, double* m_out,
+                           cudaStream_t s) {
+  ProfScope ps_(prof_name("convert", 1, AMG_F16, AMG_F64), 10.0 * n, s);
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, (int64_t)kSMs * 16));
+  k_to_half_scaled<<<g, kT, 0, s>>>(n, src, s_dev, mul, (__half*)dst, m_out);
+  AMG_CK_LAUNCH();
+}
+
 __global__ void k_set_inv1(double* dst, const double* src) { *dst = 1.0 / *src; }
 
 void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
                                 const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
-                                CommBase* comm, float* wf_out) {
+                                CommBase* comm, void* wf_out, int wf_type) {
   if (k + 1 > 32) fail(AMG_EINVAL, "update + dots + norm: at most 31 vectors");
   {
-    ProfScope ps_(prof_name("cgs_update_dots_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2) + (wf_out ? 4.0 * n : 0.0), s);
-    launch_cgs<3>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s, wf_out);
+    const double ws = wf_out ? (wf_type == AMG_F16 ? 2.0 : 4.0) : 0.0;
+    ProfScope ps_(prof_name("cgs_update_dots_nrm", k, AMG_F64, -1), 8.0 * n * (k + 2) + ws * n, s);
+    if (wf_out && wf_type == AMG_F16)
+      launch_cgs<3, double, __half>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s, (__half*)wf_out);
+    else
+      launch_cgs<3>(n, k, V, sc, coef, w, w_out, partials, out, 0, nullptr, s, (float*)wf_out);
   }
   finalize_global(comm, out, k + 1, false, s);
 }

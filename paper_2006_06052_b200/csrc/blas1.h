@@ -39,7 +39,14 @@ void launch_mdot_scaled_f32(int64_t n, int k, const PtrList& Vf, const double* s
 // (optional): an fp32 copy of w_out written in the same pass (the shadow basis of R23)
 void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double* sc, const double* coef,
                                 const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
-                                CommBase* comm = nullptr, float* wf_out = nullptr);
+                                CommBase* comm = nullptr, void* wf_out = nullptr, int wf_type = AMG_F32);
+// reading R28: the pass-1 multi-dot on an fp16 shadow (Vh.p[j] are __half*) stored at scale
+// sig_j; ms[j] = s_j / sig_j (device)
+void launch_mdot_scaled_f16(int64_t n, int k, const PtrList& Vh, const double* ms, const double* w, double* partials,
+                            double* out, cudaStream_t s, CommBase* comm = nullptr);
+// dst (__half) = fp16(src * sig), sig = the power of two at or below mul * *s_dev; *m_out = *s_dev / sig
+void launch_to_half_scaled(int64_t n, const double* src, const double* s_dev, double mul, void* dst, double* m_out,
+                           cudaStream_t s);
 // w -= sum_j coef[j] V_j  (coef: device)
 void launch_maxpy(int64_t n, int k, const PtrList& V, const double* coef, double* w, cudaStream_t s);
 // x += sum_j y[j] Z_j  (Z of dtype zt, y: device)

@@ -89,7 +89,7 @@ int amg_params_default(amg_params* p) {
   p->schur_shat = 1;
   p->over_interp = 1.5;
   p->ilu_sweeps = 2;
-  p->gmres_ortho = 2;
+  p->gmres_ortho = 3;  // R28: fp16 shadow for the pass-1 dots
   p->fused_presmooth = 1;
   p->ilut_p = 2;
   p->ilut_tau = 1e-2;

@@ -35,7 +35,9 @@ struct Error {
 
 #define AMG_CK_LAUNCH() AMG_CK(cudaGetLastError())
 
-inline size_t dtype_size(int dt) { return dt == AMG_F32 ? 4 : 8; }
+// internal element type (not a public amg_dtype): the GMRES pass-1 fp16 shadow basis (R28)
+constexpr int AMG_F16 = 2;
+inline size_t dtype_size(int dt) { return dt == AMG_F32 ? 4 : (dt == AMG_F16 ? 2 : 8); }
 
 // Lab / test switches (AMG_*): read from the environment whenever a plan is made or an
 // apply starts, never cached, so a test can A/B a kernel variant within one process.  None

@@ -529,9 +529,20 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   const int64_t N = c.N;
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hh(m + 1);
   const bool gram = h.p.gmres_ortho >= 1;
-  const bool shadow = h.p.gmres_ortho == 2;  // reading R23: pass-1 dots on the fp32 shadow basis
-  auto shadow0 = [&]() {  // the fp32 shadow of V_0 (the other shadows come out of the update pass)
+  const bool shadow = h.p.gmres_ortho >= 2;  // reading R23 / R28: pass-1 dots on an fp32 / fp16 shadow basis
+  const bool half = h.p.gmres_ortho == 3;
+  // R28: shadow j holds fp16(V_j sig_j), sig_j the power of two at or below sqrt(N) / ||w|| (w: the
+  // pre-update vector the update pass turned into V_j; V_0: sig_0 = sqrt(N) s_0); the pass-1 dots
+  // scale by m_j = s_j / sig_j
+  double* msc = h.dscal + 192;
+  const double sqN = std::sqrt((double)std::max<int64_t>(N, 1));
+  auto shadow0 = [&]() {  // the shadow of V_0 (the other shadows come out of the update pass)
     if (!shadow) return;
+    if (half) {
+      launch_to_half_scaled(N, h.V[0], h.dscal + 128, sqN, h.Vs[0], msc, c.s);  // s_0 = 1 / ||V_0||; m_0
+      c.bytes += 10.0 * N;
+      return;
+    }
     launch_convert(N, h.V[0], AMG_F64, h.Vs[0], AMG_F32, 1.0, c.s);
     c.bytes += 12.0 * N;
   };
@@ -563,7 +574,18 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     for (; j < m && !stop; ++j) {
       c.pc(h.V[j], h.Z[j], h.zt, sc + j);  // z_j = M(v_j), v_j = s_j V_j (s_j on the device)
       double* w = h.V[j + 1];
-      c.spmv(h.Z[j], h.zt, w);
+      if (half) {  // R28: ||w||^2 (the shadow scale of V_{j+1}) with the SpMV, into dscal[250]
+        if (h.comm || !launch_spmv_dot(h.A, h.Z[j], h.zt, w, nullptr, nullptr, 1, h.partials, h.dscal + 250, c.s,
+                                       h.comm)) {
+          c.spmv(h.Z[j], h.zt, w);
+          launch_dot(N, w, AMG_F64, w, AMG_F64, h.partials, h.dscal + 250, false, c.s, h.comm);
+          c.bytes += 8.0 * N;
+        } else {
+          c.bytes += h.alg_bytes_spmv + N * ((double)dtype_size(h.zt) - 8.0);
+        }
+      } else {
+        c.spmv(h.Z[j], h.zt, w);
+      }
       PtrList Vl{};
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
       double hn = 0.0;
@@ -583,16 +605,31 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
         // t_{j+1} = w1 / ||w1||; R's new column from G's (R^-T q / ||w1||);
         // H(:, j) = h + ||w1|| R(:, j+1).
         const int k = j + 1;
+        double sig = 1.0;  // R28: the fp16 shadow scale of V_{j+1}
         if (shadow) {
           PtrList Vf{};
           for (int i = 0; i < k; ++i) Vf.p[i] = reinterpret_cast<const double*>(h.Vs[i]);
-          launch_mdot_scaled_f32(N, k, Vf, sc, w, h.partials, h.dscal, c.s, h.comm);
-          c.bytes += 4.0 * N * k + 8.0 * N;
+          if (half) {
+            launch_mdot_scaled_f16(N, k, Vf, msc, w, h.partials, h.dscal, c.s, h.comm);
+            c.bytes += 2.0 * N * k + 8.0 * N;
+            AMG_CK(cudaMemcpyAsync(h.hscal + 250, h.dscal + 250, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+          } else {
+            launch_mdot_scaled_f32(N, k, Vf, sc, w, h.partials, h.dscal, c.s, h.comm);
+            c.bytes += 4.0 * N * k + 8.0 * N;
+          }
         } else {
           launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
           c.bytes += 8.0 * N * (k + 1.0);
         }
         c.read(k);
+        if (half && h.hscal[250] > 0.0 && finite(h.hscal[250])) {
+          // a power of two at or below sqrt(N) / ||w||: the scaling is exact, and ||w||'s last
+          // bits (its summation order differs between the fused single-device SpMV + dot and the
+          // distributed SpMV then dot) do not reach the shadow
+          int e = 0;
+          std::frexp(sqN / std::sqrt(h.hscal[250]), &e);
+          sig = std::ldexp(1.0, e - 1);
+        }
         // h = R^-T p (forward substitution), c' = R^-1 h (back substitution); the update pass
         // w -= t c' returns q = t^T w and ||w||^2.  hacc accumulates Q^T w over the passes.
         auto project = [&](const double* pin, double* hout) {
@@ -607,10 +644,11 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
             cv[i] = t / R[(size_t)i * (m + 1) + i];
           }
           for (int i = 0; i < k; ++i) h.hscal[96 + i] = cv[i];
-          AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+          h.hscal[96 + k] = sig;  // R28: the fp16 shadow's scale (coef[k] of the update kernel)
+          AMG_CK(cudaMemcpyAsync(h.dscal + 96, h.hscal + 96, sizeof(double) * (k + 1), cudaMemcpyHostToDevice, c.s));
           launch_cgs_update_dots_nrm(N, k, Vl, sc, h.dscal + 96, w, w, h.partials, h.dscal + 32, c.s, h.comm,
-                                     shadow ? h.Vs[j + 1] : nullptr);
-          c.bytes += 8.0 * N * (k + 2.0) + (shadow ? 4.0 * N : 0.0);  // k basis vectors and w read, w written
+                                     shadow ? h.Vs[j + 1] : nullptr, half ? AMG_F16 : AMG_F32);
+          c.bytes += 8.0 * N * (k + 2.0) + (shadow ? (half ? 2.0 : 4.0) * N : 0.0);  // k vectors and w read, w written
           c.read(32 + k + 1);
         };
         std::vector<double> pin(h.hscal, h.hscal + k), h2(k);
@@ -647,6 +685,10 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
         }
         h.hscal[100 + m] = 1.0 / std::sqrt(std::max(h.hscal[32 + k], 0.0));  // s_{j+1}: t_{j+1} = s w1
         AMG_CK(cudaMemcpyAsync(sc + j + 1, h.hscal + 100 + m, sizeof(double), cudaMemcpyHostToDevice, c.s));
+        if (half) {  // m_{j+1} = s_{j+1} / sig_{j+1}
+          h.hscal[223] = h.hscal[100 + m] / sig;
+          AMG_CK(cudaMemcpyAsync(msc + j + 1, h.hscal + 223, sizeof(double), cudaMemcpyHostToDevice, c.s));
+        }
         for (int i = 0; i < k; ++i) hh[i] = hv[i];
       }
       s_host = 1.0 / hn;

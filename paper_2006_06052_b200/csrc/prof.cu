@@ -35,7 +35,8 @@ cudaEvent_t prof_event() {
 const char* prof_name(const char* base, int b, int vt, int xt) {
   static std::map<std::string, std::string>* names = new std::map<std::string, std::string>();
   char buf[128];
-  snprintf(buf, sizeof(buf), "%s_b%d_%s%s", base, b, vt == AMG_F32 ? "f32" : "f64", xt < 0 ? "" : (xt == AMG_F32 ? "xf32" : "xf64"));
+  snprintf(buf, sizeof(buf), "%s_b%d_%s%s", base, b, vt == AMG_F32 ? "f32" : (vt == 2 /* AMG_F16, common.cuh */ ? "f16" : "f64"),
+           xt < 0 ? "" : (xt == AMG_F32 ? "xf32" : "xf64"));
   auto it = names->find(buf);
   if (it == names->end()) it = names->emplace(buf, buf).first;
   return it->second.c_str();

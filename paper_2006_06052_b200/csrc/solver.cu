@@ -55,6 +55,8 @@ void alloc_workspace(Handle& h, cudaStream_t s) {
     for (int i = 0; i < m; ++i) h.Z.push_back(h.arena.alloc(std::max<int64_t>(Nx, 1) * dtype_size(h.zt)));
     if (h.p.gmres_ortho == 2)
       for (int i = 0; i <= m; ++i) h.Vs.push_back(h.arena.alloc_n<float>(std::max<int64_t>(N, 1)));
+    if (h.p.gmres_ortho == 3)  // fp16: 2 bytes per element, 16-byte aligned rows for the vector loads
+      for (int i = 0; i <= m; ++i) h.Vs.push_back(h.arena.alloc(((size_t)std::max<int64_t>(N, 1) * 2 + 15) & ~size_t(15)));
   }
   if (h.p.solver == AMG_IDRS) {
     // IDR(s): shadow space P (N), G (N), U (with ghost space: U_k feeds the SpMV)
@@ -110,7 +112,7 @@ int check_params(const amg_params* p) {
   if ((p->smoother == AMG_ILU0 || p->smoother == AMG_ILUT) && (p->ilu_sweeps < 1 || p->ilu_sweeps > 16))
     return AMG_EINVAL;
   if (p->smoother == AMG_ILUT && (p->ilut_p < 0 || !(p->ilut_tau >= 0.0))) return AMG_EINVAL;
-  if (p->gmres_ortho < 0 || p->gmres_ortho > 2) return AMG_EINVAL;
+  if (p->gmres_ortho < 0 || p->gmres_ortho > 3) return AMG_EINVAL;
   if (p->fused_presmooth < 0 || p->fused_presmooth > 1) return AMG_EINVAL;
   if ((p->hier_dtype != AMG_F32 && p->hier_dtype != AMG_F64) ||
       (p->vcycle_vec_dtype != AMG_F32 && p->vcycle_vec_dtype != AMG_F64))
@@ -430,7 +432,7 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   else if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
   v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
   const int64_t N = (int64_t)h->n * h->b;
-  v[6] = 4LL * N * (int64_t)h->Vs.size() + 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
+  v[6] = (h->p.gmres_ortho == 3 ? 2LL : 4LL) * N * (int64_t)h->Vs.size() + 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +
                     (int64_t)h->Ui.size()) +
          (int64_t)h->Z.size() * N * dtype_size(h->zt);
   v[7] = h->arena.bytes();

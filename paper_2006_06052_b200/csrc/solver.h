@@ -91,7 +91,7 @@ struct Handle {
   std::vector<double*> vec;
   // GMRES basis (fp64) and preconditioned basis Z (fp32 when the PC output is fp32-exact)
   std::vector<double*> V;
-  std::vector<float*> Vs;          // gmres_ortho = 2: fp32 shadow of V for the pass-1 dots (R23)
+  std::vector<void*> Vs;           // gmres_ortho = 2 / 3: fp32 / fp16 shadow of V for the pass-1 dots (R23 / R28)
   std::vector<void*> Z;
   int zt = AMG_F64;
   // IDR(s) (AMG_IDRS): shadow space, G = A U, U (search directions); shadow seed base

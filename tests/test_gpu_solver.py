@@ -328,8 +328,8 @@ SOLVE_CASES = [
                                                                   ilut_tau=3e-3), False),
     ("ilut-bicgstab-cfg3-16", gen.STOKES, 16, gen.RHS_LID, dict(precond=0, solver=1, smoother=3), True),
     # GPU orthogonalisation variants of flexible GMRES, each against the oracle's CGS2:
-    # two-pass Gram/Cholesky (R22) and the GPU's CGS2 (every case above without gmres_ortho
-    # runs the GPU default, R23: the fp32-shadow first pass)
+    # two-pass Gram/Cholesky (R22), its fp32-shadow first pass (R23) and the GPU's CGS2 (every
+    # case above without gmres_ortho runs the GPU default, R28: the fp16-shadow first pass)
     ("gram-gmres-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
     ("gram-gmres-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_ortho=1), True),
     ("gram-gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10, gmres_ortho=1),
@@ -339,6 +339,11 @@ SOLVE_CASES = [
     ("cgs2-gmres-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_ortho=0), True),
     ("cgs2-gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10, gmres_ortho=0),
      False),
+    ("f32-gmres-cfg4-16", gen.STOKES, 16, gen.RHS_FORCE_NOISE, dict(precond=1, solver=2, gmres_ortho=2), True),
+    ("f32-gmres-cfg5-24", gen.STOKES, 24, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_ortho=2), True),
+    ("f32-gmres-m10-f64", gen.STOKES, 12, gen.RHS_LID_NOISE, dict(precond=1, solver=2, gmres_m=10, gmres_ortho=2),
+     False),
+    ("f32-gmres-poisson", gen.POISSON3, 16, gen.RHS_UNIFORM, dict(precond=0, solver=2, gmres_ortho=2), False),
 ]
 
 
@@ -428,7 +433,7 @@ def test_error_codes(amg):
         amg.Solver(amg.BSR.from_numpy(ptr, col, v), coarse_enough=30)
     assert e.value.status == amg.ESINGULAR_BLOCK
     # bad params
-    for bad in (dict(gmres_m=40), dict(coarsening=2), dict(schur_shat=3), dict(over_interp=0.0), dict(gmres_ortho=3)):
+    for bad in (dict(gmres_m=40), dict(coarsening=2), dict(schur_shat=3), dict(over_interp=0.0), dict(gmres_ortho=4)):
         with pytest.raises(amg.AmgError) as e:
             amg.Solver(amg.BSR.from_numpy(ptr, col, val), **bad)
         assert e.value.status == amg.EINVAL, bad
@@ -451,11 +456,11 @@ def test_fp32_vs_fp64_iteration_parity(amg):
     assert abs(its[0] - its[1]) <= 1
 
 
-@pytest.mark.parametrize("ortho", [1, 2])
+@pytest.mark.parametrize("ortho", [1, 2, 3])
 @pytest.mark.parametrize("wide", [1, 99])
 def test_gram_gmres_kernel_paths(amg, envvars, wide, ortho):
-    # the update + dots + norm pass (and, ortho = 2, the fp32-shadow multi-dot) on the wide
-    # (wide=1) and K-templated (wide=99) kernels
+    # the update + dots + norm pass (and, ortho = 2 / 3, the fp32 / fp16-shadow multi-dot) on
+    # the wide (wide=1) and K-templated (wide=99) kernels
     envvars(AMG_CGS_WIDE=wide)
     n = 16
     ptr, col, val = gen.matrix(gen.STOKES, n)
@@ -640,7 +645,7 @@ def test_gram_gmres_reorthogonalisation_safeguard(amg, envvars, eigs, force):
     ptr, col, val = _block_diag_matrix(np.array(eigs), 2000, 3, rng)
     bvec = rng.standard_normal(6000)
     res = {}
-    for ortho in (0, 1, 2):
+    for ortho in (0, 1, 2, 3):
         A = amg.BSR.from_numpy(ptr, col, val)
         S = amg.Solver(A, amg.default_params(solver=amg.GMRES, precond=amg.PC_NONE, gmres_ortho=ortho,
                                              maxiter=1000))
@@ -648,7 +653,7 @@ def test_gram_gmres_reorthogonalisation_safeguard(amg, envvars, eigs, force):
         true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
         res[ortho] = (rep, true, S.counters()["reorth_passes"])
     r0, t0, _ = res[0]
-    for o in (1, 2):
+    for o in (1, 2, 3):
         r1, t1, reorth = res[o]
         assert r0.converged and r1.converged and t0 <= 1e-8 and t1 <= 1e-8, (o, t0, t1)
         assert abs(r0.iters - r1.iters) <= 2, (o, r0.iters, r1.iters)

@@ -1142,7 +1142,7 @@ def test_fp32_emulation_rounds_every_stored_vector(rng):
         assert 0 < np.linalg.norm(z32 - z64) <= 1e-4 * np.linalg.norm(z64)
 
 
-@pytest.mark.parametrize("ortho", [0, 1, 2])
+@pytest.mark.parametrize("ortho", [0, 1, 2, 3])
 def test_gmres_finite_termination(rng, ortho):
     n = 20
     ptr, col, val = random_bsr(rng, n, 1, density=1.0, dom=10)
@@ -1164,24 +1164,29 @@ def test_gmres_two_pass_orthogonalisation_is_arnoldi(rng):
     ptr, col, val = random_bsr(rng, n, 1, density=0.2, dom=3)
     A = oracle.Mat.from_arrays(ptr, col, val)
     b = rng.standard_normal(n)
-    # (R23, gmres_ortho = 2: the first pass's dots on the fp32-rounded basis -- only the
-    # projection coefficients change, the Arnoldi relation and R stay exact, so the minimal
-    # residuals agree step by step as well)
+    # (R23, gmres_ortho = 2: the first pass's dots on the fp32-rounded basis; R28, 3: on the
+    # fp16-rounded basis -- only the projection coefficients change, the Arnoldi relation and
+    # R stay exact, so the minimal residuals agree step by step as well)
     hs = []
-    for ortho in (0, 1, 2):
+    for ortho in (0, 1, 2, 3):
         S = oracle.Solver(A, solver=oracle.GMRES, gmres_m=40, precond=oracle.PC_NONE, gmres_ortho=ortho)
         hs.append(np.array(S.solve(b, rtol=1e-10, history=True).history))
-    for o in (1, 2):
+    for o in (1, 2, 3):
         k = min(len(hs[0]), len(hs[o]))
         assert abs(len(hs[0]) - len(hs[o])) <= 1
-        assert np.allclose(hs[0][:k], hs[o][:k], rtol=1e-6, atol=1e-14)
+        if o < 3:
+            assert np.allclose(hs[0][:k], hs[o][:k], rtol=1e-6, atol=1e-14)
+        else:  # fp16 coefficients: the same history to 1e-6 down to 1e-8, within 1e-4 below it
+            hi = hs[0][:k] > 1e-8
+            assert np.allclose(hs[0][:k][hi], hs[o][:k][hi], rtol=1e-6, atol=0)
+            assert np.allclose(hs[0][:k], hs[o][:k], rtol=1e-4, atol=1e-14)
     for kind, pc in ((gen.STOKES, oracle.PC_SCHUR), (gen.POISSON3, oracle.PC_AMG)):
         ptr, col, val = gen.matrix(kind, 8)
         A = oracle.Mat.from_arrays(ptr, col, val)
         b = rng.standard_normal((len(ptr) - 1) * val.shape[-1])
         rs = [oracle.Solver(A, solver=oracle.GMRES, precond=pc, gmres_ortho=o, coarse_enough=60).solve(b, rtol=1e-10)
-              for o in (0, 1, 2)]
-        for o in (1, 2):
+              for o in (0, 1, 2, 3)]
+        for o in (1, 2, 3):
             assert rs[0].iters == rs[o].iters and rs[0].converged and rs[o].converged
             assert np.linalg.norm(rs[0].x - rs[o].x) <= 1e-8 * np.linalg.norm(rs[0].x)
 
