@@ -104,50 +104,67 @@ __global__ void __launch_bounds__(kTM) k_cgs(int64_t n, PtrList V, const double*
   }
   if (threadIdx.x == 0) sig = (MODE == 3 && std::is_same_v<WF, __half> && wf) ? coef[K] : 1.0;
   __syncthreads();
-  constexpr int KA = (MODE == 2) ? 1 : (MODE == 3 ? K + 1 : K);
+  constexpr bool H16 = MODE == 0 && std::is_same_v<TV, __half>;  // R28's multi-dot: + w . w in acc[K]
+  constexpr int KA = (MODE == 2) ? 1 : ((MODE == 3 || H16) ? K + 1 : K);
   double acc[KA];
 #pragma unroll
   for (int j = 0; j < KA; ++j) acc[j] = 0.0;
-  if constexpr (MODE == 0 && (std::is_same_v<TV, float> || std::is_same_v<TV, __half>)) {
-    // fp32 shadow basis (reading R23): four consecutive elements per thread, one 16-byte load
-    // per vector (the scalar form kept one 4-byte load per vector in flight: 2-4 TB/s); the
-    // fp16 shadow (R28): the same four elements in one 8-byte load
+  if constexpr (H16) {
+    // fp16 shadow basis (reading R28): four consecutive elements per thread, one 8-byte load per
+    // vector, each vector's values widened as its load is consumed; w . w on the side
     const int64_t n4 = n / 4;
     for (int64_t i4 = (int64_t)blockIdx.x * kTM + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * kTM) {
-      if constexpr (std::is_same_v<TV, float>) {
-        float4 raw[K];
+      uint2 hr[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) raw[j] = __ldcs(reinterpret_cast<const float4*>(V.p[j]) + i4);
-        const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
-        const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+      for (int j = 0; j < K; ++j) hr[j] = __ldcs(reinterpret_cast<const uint2*>(V.p[j]) + i4);
+      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
+      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          acc[j] = fma((double)raw[j].x, w0.x, acc[j]);
-          acc[j] = fma((double)raw[j].y, w0.y, acc[j]);
-          acc[j] = fma((double)raw[j].z, w1.x, acc[j]);
-          acc[j] = fma((double)raw[j].w, w1.y, acc[j]);
-        }
-      } else {  // fp16: widen each vector's four values as its load is consumed
-        uint2 hr[K];
+      for (int j = 0; j < K; ++j) {
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].y));
+        acc[j] = fma((double)a.x, w0.x, acc[j]);
+        acc[j] = fma((double)a.y, w0.y, acc[j]);
+        acc[j] = fma((double)b.x, w1.x, acc[j]);
+        acc[j] = fma((double)b.y, w1.y, acc[j]);
+      }
+      acc[K] = fma(w0.x, w0.x, acc[K]);
+      acc[K] = fma(w0.y, w0.y, acc[K]);
+      acc[K] = fma(w1.x, w1.x, acc[K]);
+      acc[K] = fma(w1.y, w1.y, acc[K]);
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
+      const double wi = w[i];
 #pragma unroll
-        for (int j = 0; j < K; ++j) hr[j] = __ldcs(reinterpret_cast<const uint2*>(V.p[j]) + i4);
-        const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
-        const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+      for (int j = 0; j < K; ++j) acc[j] = fma((double)__half2float(reinterpret_cast<const __half*>(V.p[j])[i]), wi, acc[j]);
+      acc[K] = fma(wi, wi, acc[K]);
+    }
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].x));
-          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hr[j].y));
-          acc[j] = fma((double)a.x, w0.x, acc[j]);
-          acc[j] = fma((double)a.y, w0.y, acc[j]);
-          acc[j] = fma((double)b.x, w1.x, acc[j]);
-          acc[j] = fma((double)b.y, w1.y, acc[j]);
-        }
+    for (int j = 0; j < K; ++j) acc[j] *= sv[j];
+    reduce_finish<KA>(acc, KA, partials, ticket, out, post, inv);
+    return;
+  } else if constexpr (MODE == 0 && std::is_same_v<TV, float>) {
+    // fp32 shadow basis (reading R23): four consecutive elements per thread, one 16-byte load
+    // per vector (the scalar form kept one 4-byte load per vector in flight: 2-4 TB/s)
+    const int64_t n4 = n / 4;
+    for (int64_t i4 = (int64_t)blockIdx.x * kTM + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * kTM) {
+      float4 raw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) raw[j] = __ldcs(reinterpret_cast<const float4*>(V.p[j]) + i4);
+      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4);
+      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(w) + 2 * i4 + 1);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        acc[j] = fma((double)raw[j].x, w0.x, acc[j]);
+        acc[j] = fma((double)raw[j].y, w0.y, acc[j]);
+        acc[j] = fma((double)raw[j].z, w1.x, acc[j]);
+        acc[j] = fma((double)raw[j].w, w1.y, acc[j]);
       }
     }
     for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kTM + threadIdx.x; i < n; i += (int64_t)gridDim.x * kTM) {
       const double wi = w[i];
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc[j] = fma((double)(float)reinterpret_cast<const TV*>(V.p[j])[i], wi, acc[j]);
+      for (int j = 0; j < K; ++j) acc[j] = fma((double)reinterpret_cast<const TV*>(V.p[j])[i], wi, acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) acc[j] *= sv[j];
@@ -441,6 +458,7 @@ __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrLis
   double acc[NJ];
 #pragma unroll
   for (int q = 0; q < NJ; ++q) acc[q] = 0.0;
+  double ww = 0.0;  // w . w (warp 0, whose lanes cover the whole chunk): the next shadow's scale
   for (int64_t i0 = (int64_t)blockIdx.x * kCW; i0 < n; i0 += (int64_t)gridDim.x * kCW) {
     if (i0 + kCW <= n) {
       uint2 hr[NJ][2];
@@ -464,6 +482,14 @@ __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrLis
           acc[q] = fma((double)b.x, wv[hh][1].x, acc[q]);
           acc[q] = fma((double)b.y, wv[hh][1].y, acc[q]);
         }
+      if (warp == 0)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          ww = fma(wv[hh][0].x, wv[hh][0].x, ww);
+          ww = fma(wv[hh][0].y, wv[hh][0].y, ww);
+          ww = fma(wv[hh][1].x, wv[hh][1].x, ww);
+          ww = fma(wv[hh][1].y, wv[hh][1].y, ww);
+        }
     } else {
       for (int hh = 0; hh < 2; ++hh)
         for (int e = 0; e < 4; ++e) {
@@ -472,6 +498,7 @@ __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrLis
             const double wi = w[i];
 #pragma unroll
             for (int q = 0; q < NJ; ++q) acc[q] = fma((double)__half2float(vp[q][i]), wi, acc[q]);
+            if (warp == 0) ww = fma(wi, wi, ww);
           }
         }
     }
@@ -484,7 +511,19 @@ __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrLis
     const int j = warp + 8 * q;
     if (lane == 0 && own[q]) partials[(int64_t)j * gridDim.x + blockIdx.x] = v * ms[j];
   }
-  finish_partials(k, partials, ticket, out, 0, nullptr);
+  if (warp == 0) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) ww += __shfl_xor_sync(kFull, ww, off);
+    if (lane == 0) partials[(int64_t)k * gridDim.x + blockIdx.x] = ww;
+  }
+  finish_partials(k + 1, partials, ticket, out, 0, nullptr);  // out[k] = w . w
+}
+
+template <int KMAX, int K = 1, class F>
+void dispatch_k_upto(int k, F&& f) {
+  if (k == K) f(std::integral_constant<int, K>{});
+  else if constexpr (K < KMAX) dispatch_k_upto<KMAX, K + 1>(k, f);
+  else fail(AMG_EINVAL, "multi-vector kernel: too many vectors for this variant");
 }
 
 template <int K = 1, class F>
@@ -499,29 +538,43 @@ void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const doub
                 double* w_out, double* partials, double* out, int post, double* inv, cudaStream_t s,
                 WF* wf = nullptr) {
   unsigned* ticket = reinterpret_cast<unsigned*>(partials + (size_t)kMaxPartials * 32);
-  // first k served by the wide kernels (tests force both); the fp16 multi-dot from k = 11 (the
-  // K-templated kernel ran k = 11 / 12 at 4.8 / 3.2 TB/s)
-  const int wide_from = env_int("AMG_CGS_WIDE", (MODE == 0 && std::is_same_v<TV, __half>) ? 11 : 13);
+  if constexpr (MODE == 0 && std::is_same_v<TV, __half>) {  // R28: the fp16 multi-dot (+ w . w)
+    if (k < std::min(env_int("AMG_F16_WIDE", 11), 13)) {  // K-templated (k = 11 / 12 there: 4.8 / 3.2 TB/s)
+      dispatch_k_upto<12>(k, [&](auto Kc) {
+        constexpr int K = decltype(Kc)::value;
+        static int occ = 0;
+        if (occ == 0) {
+          AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cgs<K, 0, __half, float>, kTM, 0));
+          occ = std::max(occ, 1);
+        }
+        const int64_t work = (n + (int64_t)kTM * 4 - 1) / ((int64_t)kTM * 4);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)occ * kSMs, (int64_t)kMaxPartials, work}));
+        k_cgs<K, 0, __half, float><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv,
+                                                      (float*)nullptr);
+      });
+      AMG_CK_LAUNCH();
+      return;
+    }
+    const int64_t work = (n + kCW - 1) / kCW;
+    const int g16 = (int)std::max<int64_t>(
+        1, std::min<int64_t>({(int64_t)env_int("AMG_F16_BLOCKS", 8) * kSMs, (int64_t)kMaxPartials, work}));
+    auto go16 = [&](auto kern) { kern<<<g16, kTW, 0, s>>>(n, k, V, sc, w, partials, ticket, out); };
+    if (k <= 16) go16(k_mdot16_wide<2>);
+    else if (k <= 24) go16(k_mdot16_wide<3>);
+    else go16(k_mdot16_wide<4>);
+    AMG_CK_LAUNCH();
+    return;
+  } else {
+  const int wide_from = env_int("AMG_CGS_WIDE", 13);  // first k served by k_cgs_wide (tests force both)
   if (k >= wide_from) {
     const int64_t work = (n + kCW - 1) / kCW;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * kSMs, (int64_t)kMaxPartials, work}));
     auto go = [&](auto kern) {
       kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
     };
-    if constexpr (MODE == 0 && std::is_same_v<TV, __half>) {  // R28: the fp16 multi-dot
-      const int g16 = (int)std::max<int64_t>(
-          1, std::min<int64_t>({(int64_t)env_int("AMG_F16_BLOCKS", 8) * kSMs, (int64_t)kMaxPartials, work}));
-      auto go16 = [&](auto kern) { kern<<<g16, kTW, 0, s>>>(n, k, V, sc, w, partials, ticket, out); };
-      if (k <= 16) go16(k_mdot16_wide<2>);
-      else if (k <= 24) go16(k_mdot16_wide<3>);
-      else go16(k_mdot16_wide<4>);
-      AMG_CK_LAUNCH();
-      return;
-    } else {
-      if (k <= 16) go(k_cgs_wide<2, MODE, TV, WF>);
-      else if (k <= 24) go(k_cgs_wide<3, MODE, TV, WF>);
-      else go(k_cgs_wide<4, MODE, TV, WF>);
-    }
+    if (k <= 16) go(k_cgs_wide<2, MODE, TV, WF>);
+    else if (k <= 24) go(k_cgs_wide<3, MODE, TV, WF>);
+    else go(k_cgs_wide<4, MODE, TV, WF>);
     AMG_CK_LAUNCH();
     return;
   }
@@ -538,6 +591,7 @@ void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const doub
     k_cgs<K, MODE, TV, WF><<<g, kTM, 0, s>>>(n, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
   });
   AMG_CK_LAUNCH();
+  }
 }
 
 // out[j] = sum of the nblk partials of reduction j, in a fixed order
@@ -691,9 +745,10 @@ void launch_mdot_scaled_f32(int64_t n, int k, const PtrList& Vf, const double* s
 
 void launch_mdot_scaled_f16(int64_t n, int k, const PtrList& Vh, const double* ms, const double* w, double* partials,
                             double* out, cudaStream_t s, CommBase* comm) {
+  if (k + 1 > 32) fail(AMG_EINVAL, "fp16 multi-dot: at most 31 vectors");
   ProfScope ps_(prof_name("mdot", k, AMG_F16, -1), 2.0 * n * k + 8.0 * n, s);
   launch_cgs<0, __half>(n, k, Vh, ms, nullptr, w, nullptr, partials, out, 0, nullptr, s);
-  finalize_global(comm, out, k, false, s);
+  finalize_global(comm, out, k + 1, false, s);
 }
 
 // dst = fp16(src * sig), sig the power of two at or below mul * *s_dev (the fp16 shadow of V_0 at

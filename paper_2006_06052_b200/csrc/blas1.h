@@ -41,7 +41,7 @@ void launch_cgs_update_dots_nrm(int64_t n, int k, const PtrList& V, const double
                                 const double* w, double* w_out, double* partials, double* out, cudaStream_t s,
                                 CommBase* comm = nullptr, void* wf_out = nullptr, int wf_type = AMG_F32);
 // reading R28: the pass-1 multi-dot on an fp16 shadow (Vh.p[j] are __half*) stored at scale
-// sig_j; ms[j] = s_j / sig_j (device)
+// sig_j; ms[j] = s_j / sig_j (device); out[k] = w . w (k + 1 outputs)
 void launch_mdot_scaled_f16(int64_t n, int k, const PtrList& Vh, const double* ms, const double* w, double* partials,
                             double* out, cudaStream_t s, CommBase* comm = nullptr);
 // dst (__half) = fp16(src * sig), sig = the power of two at or below mul * *s_dev; *m_out = *s_dev / sig

@@ -532,8 +532,8 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
   const bool shadow = h.p.gmres_ortho >= 2;  // reading R23 / R28: pass-1 dots on an fp32 / fp16 shadow basis
   const bool half = h.p.gmres_ortho == 3;
   // R28: shadow j holds fp16(V_j sig_j), sig_j the power of two at or below sqrt(N) / ||w|| (w: the
-  // pre-update vector the update pass turned into V_j; V_0: sig_0 = sqrt(N) s_0); the pass-1 dots
-  // scale by m_j = s_j / sig_j
+  // pre-update vector the update pass turned into V_j, ||w||^2 from the pass-1 multi-dot; V_0:
+  // sig_0 from sqrt(N) s_0); the pass-1 dots scale by m_j = s_j / sig_j
   double* msc = h.dscal + 192;
   const double sqN = std::sqrt((double)std::max<int64_t>(N, 1));
   auto shadow0 = [&]() {  // the shadow of V_0 (the other shadows come out of the update pass)
@@ -574,18 +574,7 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
     for (; j < m && !stop; ++j) {
       c.pc(h.V[j], h.Z[j], h.zt, sc + j);  // z_j = M(v_j), v_j = s_j V_j (s_j on the device)
       double* w = h.V[j + 1];
-      if (half) {  // R28: ||w||^2 (the shadow scale of V_{j+1}) with the SpMV, into dscal[250]
-        if (h.comm || !launch_spmv_dot(h.A, h.Z[j], h.zt, w, nullptr, nullptr, 1, h.partials, h.dscal + 250, c.s,
-                                       h.comm)) {
-          c.spmv(h.Z[j], h.zt, w);
-          launch_dot(N, w, AMG_F64, w, AMG_F64, h.partials, h.dscal + 250, false, c.s, h.comm);
-          c.bytes += 8.0 * N;
-        } else {
-          c.bytes += h.alg_bytes_spmv + N * ((double)dtype_size(h.zt) - 8.0);
-        }
-      } else {
-        c.spmv(h.Z[j], h.zt, w);
-      }
+      c.spmv(h.Z[j], h.zt, w);
       PtrList Vl{};
       for (int i = 0; i <= j; ++i) Vl.p[i] = h.V[i];
       double hn = 0.0;
@@ -609,10 +598,9 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
         if (shadow) {
           PtrList Vf{};
           for (int i = 0; i < k; ++i) Vf.p[i] = reinterpret_cast<const double*>(h.Vs[i]);
-          if (half) {
+          if (half) {  // + dscal[k] = ||w||^2 (the shadow scale of V_{j+1})
             launch_mdot_scaled_f16(N, k, Vf, msc, w, h.partials, h.dscal, c.s, h.comm);
             c.bytes += 2.0 * N * k + 8.0 * N;
-            AMG_CK(cudaMemcpyAsync(h.hscal + 250, h.dscal + 250, sizeof(double), cudaMemcpyDeviceToHost, c.s));
           } else {
             launch_mdot_scaled_f32(N, k, Vf, sc, w, h.partials, h.dscal, c.s, h.comm);
             c.bytes += 4.0 * N * k + 8.0 * N;
@@ -621,13 +609,14 @@ int solve_gmres(Ctx& c, const double* b, double* x, double rtol, double nb, amg_
           launch_mdot_scaled(N, k, Vl, sc, w, h.partials, h.dscal, c.s, h.comm);
           c.bytes += 8.0 * N * (k + 1.0);
         }
-        c.read(k);
-        if (half && h.hscal[250] > 0.0 && finite(h.hscal[250])) {
+        c.read(half ? k + 1 : k);
+        const double wnorm2 = half ? h.hscal[k] : 0.0;
+        if (half && wnorm2 > 0.0 && finite(wnorm2)) {
           // a power of two at or below sqrt(N) / ||w||: the scaling is exact, and ||w||'s last
           // bits (its summation order differs between the fused single-device SpMV + dot and the
           // distributed SpMV then dot) do not reach the shadow
           int e = 0;
-          std::frexp(sqN / std::sqrt(h.hscal[250]), &e);
+          std::frexp(sqN / std::sqrt(wnorm2), &e);
           sig = std::ldexp(1.0, e - 1);
         }
         // h = R^-T p (forward substitution), c' = R^-1 h (back substitution); the update pass

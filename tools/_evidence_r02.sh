@@ -26,7 +26,9 @@ cap r0m 'LEpiSpmvM' 0
 cap splitm 'k_split4_M' 0
 cap schurum 'EpiSchurUM' 0
 cap schurp 'LEpiSchurP' 0
-cap mdot32 'k_cgs_wide<\(int\)4, \(int\)0, float>' 2
+cap mdot16 'k_mdot16_wide<\(int\)4>' 2
+cap update 'k_cgs_wide<\(int\)4, \(int\)3, double, __half>' 2
+cap smoothjoin 'LEpiSmoothJoin' 0
 python tools/spmv_probe.py 4 1 0 5 > gpurun_out/${TAG}_spmv_plain.log 2>&1 || exit 1
 rm -f /tmp/spmv.ncu-rep
 ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_bsr_sellr" -s 2 -c 1 \

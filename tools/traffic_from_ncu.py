@@ -20,6 +20,9 @@ KEYS = {
     "split_M_b4_f64xf32@cfg5": ("splitm", "K9 split + the level-0 pre-smoothing (fused K4a)"),
     "schur_u_M_b3_f32xf32@cfg5": ("schurum", "K11 B^T update + the level-0 pre-smoothing (fused K4a)"),
     "schur_p_b3_f32xf32@cfg5": ("schurp", "K10 Schur B product"),
+    "smooth_join_b3_f32xf32@cfg5": ("smoothjoin", "level-0 last post-smoothing + join z = (u, p) (fused K9')"),
+    "mdot_b25_f16@cfg5": ("mdot16", "GMRES pass-1 multi-dot on the fp16 shadow (R28), k >= 25"),
+    "cgs_update_dots_nrm_b25_f64@cfg5": ("update", "GMRES pass-2 update + dots + norm, k >= 25"),
     "spmv_cfg2_b4_f32xf64": ("spmv", "cfg-2 4x4 fp32 x fp64 SpMV, one launch"),
 }
 
