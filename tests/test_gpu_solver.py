@@ -788,3 +788,26 @@ def test_fused_join_bit_identical(amg, envvars, rng, n, kw, env):
     assert np.array_equal(x1, x0) and i1 == i0
     assert k1 == k0_ - 1, (k1, k0_)
     assert b1 < b0
+
+
+def test_f16_shadow_wide_dynamic_range(amg):
+    # reading R28: the fp16 shadow is scaled to about unit rms by a power of two, so basis
+    # vectors whose entries span 12 orders of magnitude neither overflow nor lose the dots that
+    # matter (the smallest entries underflow): a right-hand side scaled by 10^[-6, 6] block by
+    # block, no preconditioner; the fp16-shadow GMRES converges like the GPU's CGS2 and the
+    # fp32-shadow form
+    rng = np.random.default_rng(28)
+    ptr, col, val = _block_diag_matrix(np.logspace(0, 1.5, 50), 3000, 3, rng)
+    sc = 10.0 ** rng.uniform(-6, 6, 3000)
+    bvec = rng.standard_normal(9000) * np.repeat(sc, 3)
+    res = {}
+    for ortho in (0, 2, 3):
+        S = amg.Solver(amg.BSR.from_numpy(ptr, col, val), amg.default_params(
+            solver=amg.GMRES, precond=amg.PC_NONE, gmres_ortho=ortho, maxiter=2000))
+        x, rep = _solve(amg, S, bvec)
+        assert np.all(np.isfinite(x))
+        true = np.linalg.norm(bvec - oracle.spmv(oracle.Mat.from_arrays(ptr, col, val), x)) / np.linalg.norm(bvec)
+        res[ortho] = (rep.converged, rep.iters, true)
+    for o in (0, 2, 3):
+        assert res[o][0] and res[o][2] <= 1e-8, (o, res[o])
+    assert abs(res[3][1] - res[0][1]) <= 2 and abs(res[2][1] - res[0][1]) <= 2, res
