@@ -201,6 +201,50 @@ struct LEpiSmooth {  // xo = x + M (f - A g), M block-diagonal; g the gathered v
   }
 };
 
+// The monolithic preconditioner's last post-smoothing step with the widening of its output
+// (C9: the fp32 V-cycle result widened exactly into the outer fp64 z) in its epilogue:
+// x + M (f - A x) rounded to X as LEpiSmooth stores it, then stored widened into z -- the
+// values LEpiSmooth + k_convert would store, without the x round trip
+template <typename V, typename X, typename Z>
+struct LEpiSmoothWiden {
+  static constexpr int kDots = 0;
+  const V* M;
+  const X* f;
+  const X* x;
+  Z* z;
+  template <int BR>
+  __device__ __forceinline__ void operator()(const LaneRow<BR>& L) const {
+    const int64_t o = (int64_t)L.row * BR + L.r;
+    const double res = L.valid ? (double)f[o] - L.yr : 0.0;
+    double rv[BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = __shfl_sync(kFull, res, L.base + c);
+    if (!L.valid) return;
+    double m[BR];
+    load_b<BR, false>(M + o * BR, m);
+    double t = m[0] * rv[0];
+#pragma unroll
+    for (int c = 1; c < BR; ++c) t = fma(m[c], rv[c], t);
+    z[o] = (Z)to_out<X>((double)x[o] + t);
+  }
+  template <int BR>
+  __device__ __forceinline__ void row(int row, const double (&yr)[BR]) const {
+    const int64_t o = (int64_t)row * BR;
+    double rv[BR], xv[BR], m[BR][BR];
+#pragma unroll
+    for (int c = 0; c < BR; ++c) rv[c] = (double)f[o + c] - yr[c], xv[c] = (double)x[o + c];
+#pragma unroll
+    for (int i = 0; i < BR; ++i) load_b<BR, false>(M + (o + i) * BR, m[i]);
+#pragma unroll
+    for (int i = 0; i < BR; ++i) {
+      double t = m[i][0] * rv[0];
+#pragma unroll
+      for (int c = 1; c < BR; ++c) t = fma(m[i][c], rv[c], t);
+      z[o + i] = (Z)to_out<X>(xv[i] + t);
+    }
+  }
+};
+
 // The last post-smoothing step of the Schur preconditioner's second U-solve with the join
 // (K9') in its epilogue: xo = x + M (f - A x) is stored straight into the output z as the
 // velocity slots of the interleaved (u, v, w, p) cells, with p[row] in slot 3 -- the values

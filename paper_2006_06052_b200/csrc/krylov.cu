@@ -407,14 +407,15 @@ int solve_bicgstab_graphed(Ctx& c, const double* b, double* x, double rtol, doub
   cudaGraphExec_t G = nullptr;
   for (const auto& e : h.step_graphs)
     if (e.first == x) G = e.second;
-  const double step_bytes = 2.0 * h.alg_bytes_precond + 2.0 * (h.alg_bytes_spmv) + 136.0 * N;  // p 32N, rh.v 8N, s 24N, s.t 8N, x + r 64N
+  // p 32N, rh.v 8N, s 24N, s.t 8N, x + r 64N (p fused into the apply's narrowing: its re-read goes)
+  const double step_bytes = 2.0 * h.alg_bytes_precond + 2.0 * (h.alg_bytes_spmv) + 136.0 * N - (bicg_p_fused(h) ? 8.0 * N : 0.0);
   if (!G) {
     const int64_t l0 = t_launches;
     cudaGraph_t graph = nullptr;
     AMG_CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
     try {
-      launch_bicg_p(N, r, v, p, sc, c.s);                                    // p
-      precond_apply(h, p, ph, AMG_F64, c.s);                                 // ph = M p
+      const BicgPre pre{r, v, p, sc};
+      precond_apply(h, p, ph, AMG_F64, c.s, 1.0, nullptr, &pre);             // p; ph = M p
       if (h.comm || !launch_spmv_dot(h.A, ph, AMG_F64, v, rh, nullptr, 1, h.partials, sc + kBicgRv, c.s, h.comm)) {
         halo_overlapped(h, h.halo0, h.A, ph, AMG_F64, h.b, c.s,
                         [&](int r0, int r1) { launch_spmv(h.A, 1.0, ph, AMG_F64, 0.0, v, AMG_F64, c.s, r0, r1); });

@@ -62,6 +62,9 @@ bool launch_schur_u_M(const Mat& BTm, const void* ru, const void* p, void* ru2, 
 bool launch_split_M(int32_t n, int b, int pc, const double* r, double scale, void* ru, void* rp, int xt, const void* M,
                     int mvt, void* xu, cudaStream_t s, const double* scale_dev = nullptr);
 // narrow + K4a  f = narrow(scale r) (n block rows of b), x = M f
+// k_bicg_p fused with launch_convert_M (scale 1): p = r + beta (p - omega v), f = narrow(p), x = M f
+bool launch_bicg_p_convert_M(int32_t n, int b, const double* r, const double* v, double* p, const double* sc, void* f,
+                             int xt, const void* M, int mvt, void* x, cudaStream_t s);
 bool launch_convert_M(int32_t n, int b, const double* r, double scale, void* f, int xt, const void* M, int mvt, void* x,
                       cudaStream_t s, const double* scale_dev = nullptr);
 // K8  x = Ainv f (dense N x N, values vt, vectors xt)
@@ -89,6 +92,10 @@ void launch_mask_split(int32_t nu, int32_t np, const int32_t* uidx, const int32_
 void launch_mask_join(int32_t nu, int32_t np, const int32_t* uidx, const int32_t* pidx, const void* u, const void* p,
                       int xt, void* z, int zt, cudaStream_t s);
 bool smooth_join_ok(const Mat& A, int xt);
+// K5 + the monolithic apply's widening: the last post-smoothing step writes z (dtype zt)
+bool smooth_widen_ok(const Mat& A, int xt, int zt);
+void launch_smooth_widen(const Mat& A, const void* M, const void* f, const void* x, void* z, int zt, int xt,
+                         cudaStream_t s, int r0 = 0, int r1 = -1);
 void launch_smooth_join(const Mat& A, const void* M, const void* f, const void* x, const void* p, void* z, int zt,
                         int xt, cudaStream_t s, int r0 = 0, int r1 = -1);
 void launch_join(int32_t n, int b, int pc, const void* u, const void* p, int xt, void* z, int zt,

@@ -171,8 +171,17 @@ void* vcycle_run(Handle& h, size_t level, cudaStream_t s, bool pre_done = false,
 bool fuse_presmooth(const Handle& h, size_t level);
 void* level0_f(Handle& h);
 // z = M r (outer fp64 r scaled by `scale` or by *scale_dev when given, z of dtype zt)
+// pre (BiCGStab's step graph): form the input r = pre->p = pre->r + beta (pre->p - omega pre->v)
+// first (k_bicg_p), fused into the monolithic apply's narrowing where bicg_p_fused(h)
+struct BicgPre {
+  const double* r;
+  const double* v;
+  double* p;
+  const double* sc;
+};
 void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale = 1.0,
-                   const double* scale_dev = nullptr);
+                   const double* scale_dev = nullptr, const BicgPre* pre = nullptr);
+bool bicg_p_fused(const Handle& h);
 // the same, replayed from a per-(r, z, zt, scale_dev) CUDA graph (s must not be the legacy stream)
 void precond_apply_graphed(Handle& h, const double* r, void* z, int zt, cudaStream_t s, const double* scale_dev);
 double precond_bytes(const Handle& h);

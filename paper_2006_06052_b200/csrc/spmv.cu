@@ -730,6 +730,40 @@ void launch_smooth_join(const Mat& A, const void* M, const void* f, const void* 
   AMG_CK_LAUNCH();
 }
 
+// K5 + the monolithic apply's output conversion (LEpiSmoothWiden): 3x3 / 4x4 levels on the
+// lane kernels; fp32 vectors widened into fp64 z, or z of the vectors' own dtype (the plain
+// smoother writing z)
+bool smooth_widen_ok(const Mat& A, int xt, int zt) {
+  return A.br == 0 && A.bc == 0 && A.tma_grid == 0 && (A.b == 3 || A.b == 4) &&
+         (xt == zt || (xt == AMG_F32 && zt == AMG_F64));
+}
+
+void launch_smooth_widen(const Mat& A, const void* M, const void* f, const void* x, void* z, int zt, int xt,
+                         cudaStream_t s, int r0, int r1) {
+  if (!smooth_widen_ok(A, xt, zt)) fail(AMG_EINVAL, "fused smooth + widen: 3x3 / 4x4 lane-kernel level only");
+  if (xt == zt) return launch_smooth_g("smooth", A, M, f, x, x, z, xt, s, r0, r1);
+  if (r1 < 0) r1 = A.n;
+  if (A.n == 0 || r1 <= r0) return;
+  const double frac = (double)(r1 - r0) / A.n;
+  // matrix, M, f and x read, x gathered (once), z written (fp64)
+  ProfScope ps_(prof_name("smooth_widen", A.b, A.vt, zt),
+                frac * (mat_bytes(A) + (double)A.n * A.b * A.b * dtype_size(A.vt) + 2.0 * A.n * A.b * 4 +
+                        (double)A.m * A.b * 4 + (double)A.n * A.b * 8),
+                s);
+  dispatch_t(A.vt, [&](auto v) {
+    using V = decltype(v);
+    auto go = [&](auto Bc) {
+      constexpr int B = decltype(Bc)::value;
+      launch_lane<B, B, V, float>(
+          A, (const float*)x, LEpiSmoothWiden<V, float, double>{(const V*)M, (const float*)f, (const float*)x, (double*)z},
+          s, r0, r1);
+    };
+    if (A.b == 3) go(std::integral_constant<int, 3>{});
+    else go(std::integral_constant<int, 4>{});
+  });
+  AMG_CK_LAUNCH();
+}
+
 void launch_ilu_usweep(const Mat& U, const void* Dinv, const void* y, const void* z, const void* xb, void* xo, int xt,
                        cudaStream_t s) {
   launch_smooth_g("ilu_u", U, Dinv, y, z, xb, xo, xt, s, 0, -1);
@@ -915,6 +949,59 @@ bool launch_convert_M(int32_t n, int b, const double* r, double scale, void* f, 
       dispatch_t(xt, [&](auto xx) {
         using X = decltype(xx);
         k_convert_M<B, V, X><<<grid_for(n, 256), 256, 0, s>>>(n, r, scale, scale_dev, (X*)f, (const V*)M, (X*)x);
+      });
+    });
+  });
+  AMG_CK_LAUNCH();
+  return true;
+}
+
+// BiCGStab's direction update p = r + beta (p - omega v) (k_bicg_p's expressions, device
+// scalars) with the monolithic apply's narrowing + K4a of p in the same pass: p written, f =
+// narrow(p), x = M f -- the values k_bicg_p + k_convert_M (scale 1) store, without p's re-read
+template <int B, typename V, typename X>
+__global__ void __launch_bounds__(256) k_bicg_p_convert_M(int n, const double* __restrict__ r,
+                                                          const double* __restrict__ v, double* __restrict__ p,
+                                                          const double* __restrict__ sc, X* __restrict__ f,
+                                                          const V* __restrict__ M, X* __restrict__ x) {
+  const bool first = sc[kBicgFirst] != 0.0;
+  const double beta = (sc[kBicgRho] / sc[kBicgRhoOld]) * (sc[kBicgAlpha] / sc[kBicgOmega]);
+  const double b2 = -beta * sc[kBicgOmega];
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int64_t o = row * B;
+  double fv[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) {
+    const double pv = first ? r[o + c] : fma(1.0, r[o + c], fma(b2, v[o + c], beta * p[o + c]));
+    p[o + c] = pv;
+    const X t = to_out<X>(pv * 1.0);
+    f[o + c] = t;
+    fv[c] = (double)t;
+  }
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    double m[B];
+    load_b<B, false>(M + (o + i) * B, m);
+    double t = m[0] * fv[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) t = fma(m[c], fv[c], t);
+    x[o + i] = to_out<X>(t);
+  }
+}
+
+bool launch_bicg_p_convert_M(int32_t n, int b, const double* r, const double* v, double* p, const double* sc, void* f,
+                             int xt, const void* M, int mvt, void* x, cudaStream_t s) {
+  if (n == 0) return true;
+  ProfScope ps_(prof_name("bicg_p_convert_M", b, AMG_F64, xt),
+                (double)n * b * (32.0 + 2.0 * dtype_size(xt)) + (double)n * b * b * dtype_size(mvt), s);
+  dispatch_b(b, [&](auto Bc) {
+    constexpr int B = decltype(Bc)::value;
+    dispatch_t(mvt, [&](auto vv) {
+      using V = decltype(vv);
+      dispatch_t(xt, [&](auto xx) {
+        using X = decltype(xx);
+        k_bicg_p_convert_M<B, V, X><<<grid_for(n, 256), 256, 0, s>>>(n, r, v, p, sc, (X*)f, (const V*)M, (X*)x);
       });
     });
   });

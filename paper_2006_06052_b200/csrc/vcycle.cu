@@ -82,9 +82,10 @@ void* vcycle_run(Handle& h, size_t l, cudaStream_t s, bool pre_done, const JoinO
       ilu_step(h, L, x, s);
       continue;
     }
-    if (jo && k == h.p.npost - 1 && smooth_join_ok(L.A, xt)) {  // + K9' (the caller's join)
+    if (jo && k == h.p.npost - 1 && (jo->p ? smooth_join_ok(L.A, xt) : smooth_widen_ok(L.A, xt, jo->zt))) {
       halo_overlapped(h, L.halo, L.A, x, xt, L.A.b, s, [&](int r0, int r1) {
-        launch_smooth_join(L.A, L.M, L.f, x, jo->p, jo->z, jo->zt, xt, s, r0, r1);
+        if (jo->p) launch_smooth_join(L.A, L.M, L.f, x, jo->p, jo->z, jo->zt, xt, s, r0, r1);  // + K9' (the join)
+        else launch_smooth_widen(L.A, L.M, L.f, x, jo->z, jo->zt, xt, s, r0, r1);  // + the output conversion
       });
       return nullptr;
     }
@@ -102,12 +103,27 @@ static bool join_fused(const Handle& h) {
          !env_int("AMG_NO_JOIN_FUSE", 0);
 }
 
+// is the monolithic apply's output conversion fused into level 0's last post-smoothing step?
+static bool widen_fused(const Handle& h, int zt) {
+  return !h.schur && h.amg_active && !h.lv.empty() && h.p.npost >= 1 && !h.lv[0].Lf.ptr &&
+         !(h.comm && h.rep_from == 0) && (int64_t)h.lv[0].A.n * h.lv[0].A.b == (int64_t)h.n * h.b &&
+         smooth_widen_ok(h.lv[0].A, h.xt, zt) && !env_int("AMG_NO_WIDEN_FUSE", 0);
+}
+
 // z = M r.  Monolithic AMG: narrow r once (RNE), V-cycle, widen exactly (C9).
 // Schur (C10): split + narrow; u* = V(r_u); p = m_S o (r_p - B u*); r_u' = r_u - B^T p;
 // u = V(r_u'); z = join(u, p).
+bool bicg_p_fused(const Handle& h) {
+  return !h.schur && h.amg_active && fuse_presmooth(h, 0) && h.lv[0].A.b == h.b && !env_int("AMG_NO_BICGP_FUSE", 0);
+}
+
 void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, double scale,
-                   const double* scale_dev) {
+                   const double* scale_dev, const BicgPre* pre) {
   const int64_t N = (int64_t)h.n * h.b;
+  if (pre && !bicg_p_fused(h)) {  // the direction update on its own (k_bicg_p), then the apply
+    launch_bicg_p(N, pre->r, pre->v, pre->p, pre->sc, s);
+    pre = nullptr;
+  }
   if (!h.amg_active) {
     launch_convert(N, r, AMG_F64, z, zt, scale, s, scale_dev);
     return;
@@ -119,10 +135,13 @@ void precond_apply(Handle& h, const double* r, void* z, int zt, cudaStream_t s, 
   void* x0 = f0M ? h.lv[0].x : nullptr;
   const void* M0 = f0M ? h.lv[0].M : nullptr;
   if (!h.schur) {
-    const bool fused = f0M && launch_convert_M(h.n, h.b, r, scale, f0, h.xt, M0, h.vt, x0, s, scale_dev);
+    const bool fused =
+        f0M && (pre ? launch_bicg_p_convert_M(h.n, h.b, pre->r, pre->v, pre->p, pre->sc, f0, h.xt, M0, h.vt, x0, s)
+                    : launch_convert_M(h.n, h.b, r, scale, f0, h.xt, M0, h.vt, x0, s, scale_dev));
     if (!fused) launch_convert(N, r, AMG_F64, f0, h.xt, scale, s, scale_dev);
-    void* x = vcycle_run(h, 0, s, fused);
-    launch_convert(N, x, h.xt, z, zt, 1.0, s);
+    const JoinOut jw{nullptr, z, zt};  // p == nullptr: widen into z
+    void* x = vcycle_run(h, 0, s, fused, widen_fused(h, zt) ? &jw : nullptr);
+    if (x) launch_convert(N, x, h.xt, z, zt, 1.0, s);
     return;
   }
   if (h.masked) {  // general scalar pressure mask (R21): the same steps on the scalar split
@@ -237,7 +256,8 @@ double precond_bytes(const Handle& h) {
   const int64_t N = (int64_t)h.n * h.b;
   const double sx = (double)dtype_size(h.xt), sv = (double)dtype_size(h.vt);
   if (!h.amg_active) return (double)N * 16.0;
-  if (!h.schur) return vcycle_bytes(h) + (double)N * (8.0 + sx) * 2.0;
+  if (!h.schur)  // convert in, convert out (fused into K5: its x' write and the re-read go)
+    return vcycle_bytes(h) + (double)N * (8.0 + sx) * 2.0 - (widen_fused(h, h.p.solver == AMG_GMRES ? h.zt : AMG_F64) ? 2.0 * N * sx : 0.0);
   if (h.masked) {
     const double nu = h.nu_s, np = h.np_s;
     double t = 2.0 * vcycle_bytes(h) + (double)N * (12.0 + sx) + (double)N * (4.0 + sx + 8.0);  // split, join

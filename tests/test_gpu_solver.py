@@ -790,6 +790,69 @@ def test_fused_join_bit_identical(amg, envvars, rng, n, kw, env):
     assert b1 < b0
 
 
+@pytest.mark.parametrize("kind,n,rhs,kw,env", [
+    (gen.STOKES, 16, gen.RHS_LID, dict(solver=1, hier_dtype=1, vcycle_vec_dtype=1), {}),      # cfg 3 shape: 4x4 fp32 -> fp64 z
+    (gen.STOKES, 24, gen.RHS_LID, dict(solver=1, hier_dtype=1, vcycle_vec_dtype=1),
+     dict(AMG_SELLR_MIN_SLICES=1)),                                                           # level 0 on the interleaved copy
+    (gen.STOKES, 24, gen.RHS_LID, dict(solver=1, hier_dtype=1, vcycle_vec_dtype=1), dict(AMG_SELLR=0)),  # row lanes
+    (gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=0), {}),                                  # cfg 1: 3x3 fp64, z of the same dtype
+    (gen.POISSON3, 16, gen.RHS_UNIFORM, dict(solver=0, hier_dtype=1, vcycle_vec_dtype=1), {}),  # 3x3 fp32 -> fp64
+    (gen.STOKES, 16, gen.RHS_LID, dict(solver=2, hier_dtype=1, vcycle_vec_dtype=1), {}),      # GMRES: z fp32 (same dtype)
+    (gen.STOKES, 16, gen.RHS_LID, dict(solver=1, hier_dtype=1, vcycle_vec_dtype=1, npost=2), {}),  # last of two steps
+], ids=["cfg3", "sellr", "lanes", "cfg1-f64", "b3-f32", "gmres-f32z", "npost2"])
+def test_fused_widen_bit_identical(amg, envvars, rng, kind, n, rhs, kw, env):
+    # the monolithic preconditioner's output conversion (the fp32
+    # V-cycle result widened into the outer z, C9) written by level 0's last post-smoothing
+    # step -- the same output and solve bit for bit as the separate conversion pass, one kernel
+    # fewer per application
+    envvars(**env)
+    ptr, col, val = gen.matrix(kind, n)
+    b = gen.block_size(kind)
+    N = (len(ptr) - 1) * b
+    r = torch.as_tensor(rng.standard_normal(N), device="cuda")
+    bvec = gen.rhs(rhs, n, b)
+    out = []
+    for off in (0, 1):
+        envvars(AMG_NO_WIDEN_FUSE=off)
+        A = amg.BSR.from_numpy(ptr, col, val)
+        S = amg.Solver(A, amg.default_params(precond=amg.PC_AMG, **kw))
+        z = torch.zeros(N, dtype=torch.float64, device="cuda")
+        k0 = amg.kernel_launches()
+        S.apply_precond(r, z)
+        torch.cuda.synchronize()
+        k = amg.kernel_launches() - k0
+        x, rep = _solve(amg, S, bvec)
+        out.append((z.cpu().numpy(), k, x, rep.iters, rep.alg_bytes))
+    (z1, k1, x1, i1, b1), (z0, k0_, x0, i0, b0) = out
+    assert np.array_equal(z1, z0)
+    assert np.array_equal(x1, x0) and i1 == i0
+    assert k1 == k0_ - 1, (k1, k0_)
+    assert b1 < b0
+
+
+@pytest.mark.parametrize("kind,n,rhs,kw", [
+    (gen.STOKES, 16, gen.RHS_LID, dict(hier_dtype=1, vcycle_vec_dtype=1)),   # cfg 3 shape: 4x4 fp32
+    (gen.STOKES, 24, gen.RHS_LID, dict(hier_dtype=1, vcycle_vec_dtype=1)),
+    (gen.POISSON3, 16, gen.RHS_UNIFORM, dict()),                             # 3x3 fp64
+], ids=["stokes16", "stokes24", "poisson-f64"])
+def test_fused_bicg_p_bit_identical(amg, envvars, kind, n, rhs, kw):
+    # BiCGStab's direction update p = r + beta (p - omega v) formed
+    # in the monolithic apply's narrowing pass -- the same iterates bit for bit as the separate
+    # k_bicg_p, fewer bytes and kernels per step
+    ptr, col, val = gen.matrix(kind, n)
+    bvec = gen.rhs(rhs, n, gen.block_size(kind))
+    out = []
+    for off in (0, 1):
+        envvars(AMG_NO_BICGP_FUSE=off)
+        S = amg.Solver(amg.BSR.from_numpy(ptr, col, val), amg.default_params(precond=amg.PC_AMG, solver=1, **kw))
+        k0 = amg.kernel_launches()
+        x, rep = _solve(amg, S, bvec)
+        out.append((x, rep.iters, rep.alg_bytes, amg.kernel_launches() - k0))
+    (x1, i1, b1, k1), (x0, i0, b0, k0_) = out
+    assert np.array_equal(x1, x0) and i1 == i0
+    assert b1 < b0 and k1 < k0_, (b1, b0, k1, k0_)
+
+
 def test_f16_shadow_wide_dynamic_range(amg):
     # reading R28: the fp16 shadow is scaled to about unit rms by a power of two, so basis
     # vectors whose entries span 12 orders of magnitude neither overflow nor lose the dots that
