@@ -18,6 +18,10 @@ bool has_solve_copy(const Mat& A);
 void release_bsr_values(Mat& A, Arena& arena, cudaStream_t s);
 // A's BSR values (A.vt, nnz * br * bc) re-materialised from its solve copy into out (device)
 void values_from_copy(const Mat& A, void* out, cudaStream_t s);
+// the BSR column indices of a matrix whose values are already released go too (its copy carries
+// them in its own layout); cols_from_copy re-materialises them (export), given A.ptr
+void release_bsr_cols(Mat& A, Arena& arena, cudaStream_t s);
+void cols_from_copy(const Mat& A, int32_t* out, cudaStream_t s);
 
 // S1: scalar CSR -> BSR (convert.cu); returns nnzb, fills bptr/bcol/bval when bptr != nullptr
 int64_t csr_to_bsr(int32_t n, int32_t m, int32_t b, int64_t nnz, const int32_t* ptr, const int32_t* col,

@@ -172,6 +172,17 @@ Handle* build_handle(const Mat& src, const amg_params* p, const std::vector<int6
         release_bsr_values(L.A, h->arena, s);
         release_bsr_values(L.P, h->arena, s);
         release_bsr_values(L.R, h->arena, s);
+        // and their column indices (the copies carry them; the export re-materialises them
+        // from the copy and the kept row pointers): 1.3 GB at cfg 5
+        release_bsr_cols(L.A, h->arena, s);
+        release_bsr_cols(L.P, h->arena, s);
+        release_bsr_cols(L.R, h->arena, s);
+      }
+      // B^T's values behind its interleaved copy (1.4 GB at cfg 5; the outer pattern stays:
+      // B runs on the lane kernel over it)
+      if (h->schur && !h->masked) {
+        release_bsr_values(h->BTm, h->arena, s);
+        if (!h->BTm.val) h->BTv = nullptr;
       }
     }
     h->alg_bytes_precond = precond_bytes(*h);
@@ -345,7 +356,14 @@ int amg_level_export(struct amg_handle* hh, int32_t level, int32_t which, int32_
                           : (which == 0 ? LL.A : which == 1 ? LL.P : which == 2 ? LL.R : which == 4 ? LL.Lf : LL.Uf);
   AMG_CK(cudaDeviceSynchronize());
   AMG_CK(cudaMemcpy(ptr, M.ptr, sizeof(int32_t) * (M.n + 1), cudaMemcpyDeviceToHost));
-  if (M.nnz > 0) AMG_CK(cudaMemcpy(col, M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
+  if (M.nnz > 0 && M.col) AMG_CK(cudaMemcpy(col, M.col, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
+  if (M.nnz > 0 && !M.col) {  // released column indices: re-materialised from the solve copy
+    int32_t* tc = nullptr;
+    AMG_CK(cudaMalloc(&tc, sizeof(int32_t) * M.nnz));
+    cols_from_copy(M, tc, nullptr);
+    AMG_CK(cudaMemcpy(col, tc, sizeof(int32_t) * M.nnz, cudaMemcpyDeviceToHost));
+    cudaFree(tc);
+  }
   const int64_t cnt = M.nnz * M.b * M.b;
   double* tmp = nullptr;
   void* src = M.val;
@@ -406,7 +424,7 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
   auto mat = [&](const Mat& M) -> int64_t {
     if (!M.ptr) return 0;
     return 4LL * (M.n + 1) +
-           M.nnz * (4LL + (M.val ? (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt) : 0LL));
+           M.nnz * ((M.col ? 4LL : 0LL) + (M.val ? (int64_t)M.rows_per_block() * M.cols_per_block() * dtype_size(M.vt) : 0LL));
   };
   auto sell = [&](const Mat& M) -> int64_t {
     if ((M.lane_var != kLaneSell && M.lane_var != kLaneSellR) || !M.sell_ptr) return 0;
@@ -429,7 +447,9 @@ int amg_memory_report(struct amg_handle* hh, int64_t* out, int32_t n) {
     v[3] += (int64_t)L.A.n * L.A.b * L.A.b * dtype_size(h->vt);
   }
   if (h->schur && h->masked) v[4] = mat(h->Bm) + mat(h->BTm) + (int64_t)h->np_s * dtype_size(h->vt);
-  else if (h->schur) v[4] = 2LL * h->A.nnz * h->nu * dtype_size(h->vt) + (int64_t)h->n * dtype_size(h->vt);
+  else if (h->schur)  // B / B^T values on the outer pattern (B^T's released behind its copy), m_S, copies
+    v[4] = ((h->Bv ? 1LL : 0LL) + (h->BTv ? 1LL : 0LL)) * h->A.nnz * h->nu * dtype_size(h->vt) +
+           (int64_t)h->n * dtype_size(h->vt) + sell(h->Bm) + sell(h->BTm);
   v[5] = (int64_t)h->coarse.N * h->coarse.N * dtype_size(h->vt);
   const int64_t N = (int64_t)h->n * h->b;
   v[6] = (h->p.gmres_ortho == 3 ? 2LL : 4LL) * N * (int64_t)h->Vs.size() + 8LL * N * ((int64_t)h->vec.size() + 2 /* host staging */ + (int64_t)h->V.size() + (int64_t)h->Pi.size() + (int64_t)h->Gi.size() +

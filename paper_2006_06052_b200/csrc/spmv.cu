@@ -1360,6 +1360,38 @@ void release_bsr_values(Mat& A, Arena& arena, cudaStream_t s) {
   A.val = nullptr;
 }
 
+// inverse of the column part of k_sell_fill / k_sellr_fill (C = 32 for the interleaved copy):
+// slot (s, g) holds row s * C + g, or perm[slot] (sorted windows); its j-th step's column is
+// the row's j-th BSR column
+__global__ void k_sell_unfill_col(int n, int C, int ns, const int32_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ sptr, const int32_t* __restrict__ perm,
+                                  const int32_t* __restrict__ scol, int32_t* __restrict__ col) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * C) return;
+  const int s = (int)(t / C), g = (int)(t % C);
+  int64_t row = (int64_t)s * C + g;
+  if (perm) row = perm[t] >= 0 ? perm[t] : n;
+  if (row >= n) return;
+  const int k0 = ptr[row], len = ptr[row + 1] - k0;
+  for (int j = 0; j < len; ++j) col[k0 + j] = scol[((int64_t)sptr[s] + j) * C + g];
+}
+
+void release_bsr_cols(Mat& A, Arena& arena, cudaStream_t s) {
+  if (!A.col || A.val || A.nnz == 0 || !has_solve_copy(A) || A.tma_grid > 0) return;
+  AMG_CK(cudaStreamSynchronize(s));
+  arena.release_one(A.col);
+  A.col = nullptr;
+}
+
+void cols_from_copy(const Mat& A, int32_t* out, cudaStream_t s) {
+  if (A.nnz == 0) return;
+  if (!has_solve_copy(A)) fail(AMG_EINVAL, "cols_from_copy: no solve copy");
+  const int C = A.lane_var == kLaneSellR ? 32 : 32 / A.b;
+  k_sell_unfill_col<<<grid_for((int64_t)A.sell_ns * C, 256), 256, 0, s>>>(A.n, C, A.sell_ns, A.ptr, A.sell_ptr,
+                                                                         A.sell_perm, A.sell_col, out);
+  AMG_CK_LAUNCH();
+}
+
 void values_from_copy(const Mat& A, void* out, cudaStream_t s) {
   if (A.nnz == 0) return;
   if (!has_solve_copy(A)) fail(AMG_EINVAL, "values_from_copy: no solve copy");
