@@ -664,8 +664,10 @@ def test_gram_gmres_reorthogonalisation_safeguard(amg, envvars, eigs, force):
     assert abs(O.solve(bvec, rtol=1e-8).iters - r1.iters) <= 2
 
 
-@pytest.mark.parametrize("copy", ["sellr", "sell"])
-def test_released_values_rematerialised_from_copies(amg, envvars, copy):
+@pytest.mark.parametrize("copy,kw", [("sellr", dict(precond=1, solver=2)), ("sell", dict(precond=1, solver=2)),
+                                     ("sellr", dict(precond=0, solver=1)), ("sell", dict(precond=0, solver=1))],
+                         ids=["sellr-schur", "sell-schur", "sellr-monolithic", "sell-monolithic"])
+def test_released_values_rematerialised_from_copies(amg, envvars, copy, kw):
     # a single-device handle frees the BSR values of every matrix whose
     # interleaved / sliced copy carries its products; the export re-materialises them from the
     # copy (bit-exact with the oracle), and the solve is unchanged
@@ -680,8 +682,8 @@ def test_released_values_rematerialised_from_copies(amg, envvars, copy):
     for keep in (0, 1):
         if keep:
             envvars(AMG_KEEP_VALUES=1)
-        A, S, O = make_pair(amg, ptr, col, val, hier32=True, precond=1, solver=2)
-        check_hierarchy(S, O, True)
+        A, S, O = make_pair(amg, ptr, col, val, hier32=True, **kw)
+        check_hierarchy(S, O, True)  # values and column indices re-materialised from the copies
         x, rep = _solve(amg, S, bvec)
         res.append((S.memory_report(), x, rep.iters))
     (m0, x0, i0), (m1, x1, i1) = res
