@@ -175,8 +175,16 @@ def run_reference(args, rank: int):
         return
     n_full = args.n or gen.CONFIGS[args.cfg]["n"]
     full = oracle_full_size(args.cfg) if n_full == gen.CONFIGS[args.cfg]["n"] else None
+    # wall-clock bound: at most REF_BUDGET_S (default 540 s) of oracle iterations, estimated from
+    # the measured full-size run; the line reports the iterations actually executed
+    warm, steps, capped = args.warmup, args.steps, False
+    if full and full.get("solve_s") and full.get("iters"):
+        cap = max(2, int(float(os.environ.get("REF_BUDGET_S", "540")) / (full["solve_s"] / full["iters"])))
+        if warm + steps > cap:
+            warm = min(warm, max(1, cap // 5))
+            steps, capped = cap - warm, True
     t0 = time.perf_counter()
-    r = oracle_iterations(args.cfg, n_full, args.warmup, args.steps)
+    r = oracle_iterations(args.cfg, n_full, warm, steps)
     wall = time.perf_counter() - t0
     its = full["iters"] if full else None
     if its is None:  # no full-size run on record (a non-default --n): run the whole solve once
@@ -196,7 +204,7 @@ def run_reference(args, rank: int):
         "data": "synthetic", "config": config_dict(args.cfg, n_full, args.gpus),
         "cpu_baseline": {"value": v, "unit": "s/solve", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "s/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": wall,
+        "wall_s": wall, "capped_to_wall_budget": capped,
     }
     print(json.dumps(line), flush=True)
 
