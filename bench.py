@@ -517,7 +517,11 @@ def main():
         # bounded live sample (~20 s of one host core): the oracle at cpu_n^3 of the same
         # generator, setup untimed, per-iteration time of 10 iterations, scaled by cells to n^3
         # and by the oracle's measured full-size iteration count
-        c = oracle_iterations(args.cfg, args.cpu_n, 2, 8)
+        # GMRES(30): an iteration's CGS2 cost grows with its index in the cycle, so time
+        # iterations 12..19 (mean index 15.5; the 64-iteration solve's mean is 14.7), not the
+        # cheap first ones (round 2, run r02f: iterations 2-4 take 17.6 s at 256^3, 6-25 20.8 s)
+        skip = 11 if CFG_SOLVER[args.cfg][1] == "gmres" else 2
+        c = oracle_iterations(args.cfg, args.cpu_n, skip, 8)
         full = oracle_full_size(args.cfg) if n == gen.CONFIGS[args.cfg]["n"] else None
         its = full["iters"] if full else rep.iters
         scale = (n / args.cpu_n) ** 3
@@ -526,8 +530,8 @@ def main():
         out["cpu_baseline"] = {
             "value": v, "unit": "s/solve", "cores": 1, "kind": "oracle",
             "sample": f"oracle (1 thread of {ncpu}: {model}) on the cfg-{args.cfg} generator at {args.cpu_n}^3: "
-                      f"setup {c['setup_s']:.1f} s untimed, {c['iters_timed']} Krylov iterations at "
-                      f"{c['per_iter_s']:.3f} s each, scaled x{scale:.1f} cells to {n}^3 and x{its} iterations "
+                      f"setup {c['setup_s']:.1f} s untimed, {c['iters_timed']} Krylov iterations (after "
+                      f"{c['iters_skipped']} untimed ones) at {c['per_iter_s']:.3f} s each, scaled x{scale:.1f} cells to {n}^3 and x{its} iterations "
                       f"({'the oracle' + chr(39) + 's full-size count' if full else 'the GPU count'})",
             "full_size_measured": ({"solve_s": full["solve_s"], "setup_s": full["setup_s"], "iters": full["iters"],
                                     "source": "tests/golden/oracle_full_size.json (tools/oracle_reference_runs.py, "
