@@ -266,7 +266,7 @@ __device__ __forceinline__ void finish_partials(int kout, double* partials, unsi
 }
 
 template <int NJ, int MODE, typename TV = double, typename WF = float>
-__global__ void __launch_bounds__(kTW, (NJ == 2 ? 3 : 2)) k_cgs_wide(int64_t n, int k, PtrList V, const double* __restrict__ sc,
+__global__ void __launch_bounds__(kTW, (NJ <= 3 ? 3 : 2)) k_cgs_wide(int64_t n, int k, PtrList V, const double* __restrict__ sc,
                                                      const double* __restrict__ coef, const double* w, double* w_out,
                                                      double* partials, unsigned* ticket, double* out, int post,
                                                      double* inv, WF* wf) {
@@ -568,9 +568,12 @@ void launch_cgs(int64_t n, int k, const PtrList& V, const double* sc, const doub
   const int wide_from = env_int("AMG_CGS_WIDE", 13);  // first k served by k_cgs_wide (tests force both)
   if (k >= wide_from) {
     const int64_t work = (n + kCW - 1) / kCW;
-    // two vectors per warp (k <= 16) fit three blocks per SM: the third hides the idle slots
-    // of the warps that own one vector only (AMG_CGS_BPS2 = 2: the two-block grid, A/B)
-    const int bps = k <= 16 ? std::min(std::max(env_int("AMG_CGS_BPS2", 3), 1), 3) : 2;
+    // two or three vectors per warp (k <= 24) fit three blocks per SM at 80 registers: the
+    // third hides the idle slots of the warps that own one vector fewer (AMG_CGS_BPS2 /
+    // AMG_CGS_BPS3 = 2: the two-block grid, A/B).  Four vectors per warp spill 160 bytes at 80
+    // registers and run at 4.2-4.6 TB/s against 6.2-6.5 with two blocks of 126 registers.
+    const int bps = k <= 16 ? std::min(std::max(env_int("AMG_CGS_BPS2", 3), 1), 3)
+                    : k <= 24 ? std::min(std::max(env_int("AMG_CGS_BPS3", 3), 1), 3) : 2;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)bps * kSMs, (int64_t)kMaxPartials, work}));
     auto go = [&](auto kern) {
       kern<<<g, kTW, 0, s>>>(n, k, V, sc, coef, w, w_out, partials, ticket, out, post, inv, wf);
