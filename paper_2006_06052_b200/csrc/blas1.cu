@@ -465,7 +465,8 @@ __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrLis
 #pragma unroll
       for (int q = 0; q < NJ; ++q)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) hr[q][hh] = __ldcs(reinterpret_cast<const uint2*>(vp[q] + i0 + 128 * hh + 4 * lane));
+        for (int hh = 0; hh < 2; ++hh)  // a warp without a q-th vector (k < 8 (q + 1)) loads nothing for it
+          hr[q][hh] = own[q] ? __ldcs(reinterpret_cast<const uint2*>(vp[q] + i0 + 128 * hh + 4 * lane)) : make_uint2(0u, 0u);
       double2 wv[2][2];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh)
