@@ -441,7 +441,10 @@ __global__ void __launch_bounds__(kTW, (NJ <= 3 ? 3 : 2)) k_cgs_wide(int64_t n, 
 // wide kernel's layout (warp w owns vectors w + 8q; lane owns elements i0 + 128 hh + 4 lane +
 // e of each 256-element chunk, one 8-byte load per vector and hh) at <= 64 registers so that
 // more blocks per SM keep the loads in flight (the shared template held 107 registers and ran
-// two blocks per SM: 3-4.5 TB/s; this one 5.2-6.3 at 8 blocks per SM)
+// two blocks per SM: 3-4.5 TB/s; this one 5.2-6.3 at 8 blocks per SM).  Measured and dropped
+// (run r02m): 40 / 48 registers for NJ = 2 / 3 (6 / 5 resident blocks) -- 0.87 -> 1.30 ms at
+// k = 13, 1.11 -> 1.22 at k = 17; the time per launch is flat inside an NJ group, with or
+// without the loads of the slots a warp does not own (run r02l).
 template <int NJ>
 __global__ void __launch_bounds__(kTW, 4) k_mdot16_wide(int64_t n, int k, PtrList V, const double* __restrict__ ms,
                                                         const double* w, double* partials, unsigned* ticket,
